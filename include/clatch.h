@@ -1,0 +1,162 @@
+/* clatch.h — C ABI of the B200-native CLATCH hot paths (sm_100a).
+ *
+ * Drop-in boundary for the two data-parallel paths of the reference
+ * ("latchkit", arXiv 1609.03986): LATCH descriptor extraction and brute-force
+ * Hamming top-2 matching. Plain C: pointers, sizes, int status codes — no C++
+ * types, no torch types, no exceptions. The reference's C++ functions
+ * (namespace latch) and Python bindings call these through the shims shown in
+ * INTEGRATION.md; paths below are relative to /root/reference/proj.
+ *
+ * Division of labour:
+ *   host shim   margin filter, glibc cos/sin (bit parity needs the host libm),
+ *               ratio / max-distance / cross-check filter pass, error re-raise
+ *   this ABI    everything per-sample and per-pair: window resampling, triplet
+ *               SSD compares, bit packing, XOR+popcount, top-2 selection
+ *
+ * There is NO CPU fallback: every compute entry point fails with
+ * CLATCH_ERR_NO_DEVICE / CLATCH_ERR_CUDA when the GPU path cannot run.
+ *
+ * Threading: a clatch_ctx owns one CUDA device, one stream and its scratch
+ * buffers; calls on one ctx must be serialised by the caller, distinct ctxs are
+ * independent (one process or thread per GPU).
+ */
+#ifndef CLATCH_H
+#define CLATCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CLATCH_API __attribute__((visibility("default")))
+#else
+#define CLATCH_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct clatch_ctx clatch_ctx;
+
+/* Status codes. Codes >= 100 are 100 + latch::ErrorCode (include/latch/errors.hpp:10-40)
+ * so a shim can re-raise latch::Error(static_cast<ErrorCode>(rc - 100), clatch_last_error()). */
+enum {
+    CLATCH_OK = 0,
+    CLATCH_ERR_INVALID = 1,      /* null pointer, bad size, bad pitch ... */
+    CLATCH_ERR_CUDA = 2,         /* a CUDA runtime call failed; see clatch_last_error() */
+    CLATCH_ERR_NO_DEVICE = 3,    /* no CUDA device / not an sm_100 part */
+    CLATCH_ERR_NONFINITE = 5,    /* non-finite keypoint coordinate or angle reached the device path
+                                    (the reference would std::terminate in a worker thread,
+                                    src/parallel.hpp:33-35 + src/image.cpp:110-112) */
+    CLATCH_ERR_TOO_CLOSE_TO_BORDER = 107, /* ErrorCode::TooCloseToBorder  (src/descriptor.cpp:30-33) */
+    CLATCH_ERR_BAD_HEADER = 108,          /* ErrorCode::BadHeader         (src/pattern.cpp:73-82) */
+    CLATCH_ERR_BAD_TRIPLET_COUNT = 109,   /* ErrorCode::BadTripletCount */
+    CLATCH_ERR_COORD_RANGE = 110,         /* ErrorCode::CoordinateOutOfRange (src/pattern.cpp:54-61) */
+    CLATCH_ERR_DEGENERATE = 111,          /* ErrorCode::DegenerateTriplet (src/pattern.cpp:62-65) */
+    CLATCH_ERR_LENGTH_MISMATCH = 119,     /* ErrorCode::LengthMismatch    (src/match.cpp:15-18) */
+    CLATCH_ERR_EMPTY_GALLERY = 120        /* ErrorCode::EmptyGallery      (src/match.cpp:34,55) */
+};
+
+/* Message for the last failing call on this thread (never NULL). */
+CLATCH_API const char* clatch_last_error(void);
+
+/* ---- context ---------------------------------------------------------------- */
+
+/* Binds a context to CUDA device `device` (one per GPU; replaces the reference's
+ * std::thread fan-out, src/parallel.hpp:17-38). No pattern is installed yet: call
+ * clatch_set_pattern before extracting. */
+CLATCH_API int clatch_ctx_create(int device, clatch_ctx** out);
+CLATCH_API void clatch_ctx_destroy(clatch_ctx* ctx);
+
+/* Device facts for reporting: SM count, SM clock (kHz), name (<= 255 chars). */
+CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_khz, char* name, size_t cap);
+
+/* Block until everything queued on the context's own stream has finished. */
+CLATCH_API int clatch_synchronize(clatch_ctx* ctx);
+
+/* ---- pattern (replaces TripletPattern / WeightMask, include/latch/pattern.hpp:19-52) ----
+ * triplets: T rows {ax, ay, bx, by, cx, cy}, top-left patch corners in window
+ * coordinates; mask: K*K row-major non-negative finite weights, or NULL for all
+ * ones. Validation mirrors parse_pattern (src/pattern.cpp:54-66,78-82,118-131):
+ * T > 0 and T % 8 == 0, 1 <= K <= 64, coords in [0, 64-K], companions distinct,
+ * weights finite, >= 0 and not all zero. T=512, K=8 with the 7x7-emulating 0/1
+ * mask selects the specialised kernel; anything else runs the generic kernel. */
+CLATCH_API int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, const double* mask);
+
+/* Bytes per descriptor (T/8) of the installed pattern, 0 if none. */
+CLATCH_API int clatch_descriptor_bytes(clatch_ctx* ctx);
+
+/* ---- host-side keypoint preparation (no GPU work) ----------------------------
+ * Replaces the serial margin pre-pass of describe_all (src/descriptor.cpp:94-97,
+ * keypoint_in_margin :23-27) and hoists the per-keypoint trig of extract_window
+ * (:35-36) onto the host's glibc so results stay bit-identical to the reference.
+ * kps: n rows of `cols` (2..4) doubles {x, y[, theta[, score]]}; missing theta = 0
+ * (bindings/module.cpp:49-62). Writes, for the m keypoints inside the 46 px
+ * margin of a width x height image, in input order: xycs[4*j] = {x, y, cos(theta),
+ * sin(theta)} and kept[j] = input index. `workers` <= 0 uses all cores. Fails with
+ * CLATCH_ERR_NONFINITE if a kept keypoint has a non-finite theta. */
+CLATCH_API int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, int height,
+                             int workers, double* xycs, int64_t* kept, size_t* m);
+
+/* ---- extraction (replaces describe / describe_all, src/descriptor.cpp:79-105; the
+ * arithmetic of extract_window :29-49, sample_bilinear src/image.cpp:109-126 and
+ * triplet_bit src/descriptor.cpp:51-77 runs on the device, fp64, unfused) --------
+ * Host-buffer forms copy in, run, copy out and return when `out` is ready.
+ * img: row-major, `pitch` in ELEMENTS between rows (>= width). xycs: M rows from
+ * clatch_prepare_keypoints (all inside the margin — not re-checked on device).
+ * out: M * T/8 bytes, bit t of a descriptor at byte t>>3, bit t&7 (LSB first). */
+CLATCH_API int clatch_extract_u8(clatch_ctx* ctx, const uint8_t* img, int width, int height, size_t pitch,
+                      const double* xycs, size_t M, uint8_t* out);
+CLATCH_API int clatch_extract_f64(clatch_ctx* ctx, const double* img, int width, int height, size_t pitch,
+                       const double* xycs, size_t M, uint8_t* out);
+
+/* Device-resident forms: all pointers are device memory on the context's device,
+ * work is queued on `stream` (a cudaStream_t; NULL = the legacy default stream)
+ * and NOT synchronised. */
+CLATCH_API int clatch_extract_u8_dev(clatch_ctx* ctx, const uint8_t* d_img, int width, int height,
+                          size_t pitch, const double* d_xycs, size_t M, uint8_t* d_out,
+                          void* stream);
+CLATCH_API int clatch_extract_f64_dev(clatch_ctx* ctx, const double* d_img, int width, int height,
+                           size_t pitch, const double* d_xycs, size_t M, uint8_t* d_out,
+                           void* stream);
+
+/* ---- matching (replaces knn2 / the two parallel_for passes of match_brute_force,
+ * src/match.cpp:33-67; hamming :14-31 is the per-pair arithmetic) -----------------
+ * For every query q: best_idx = lowest train index at the minimum Hamming
+ * distance, best_dist = that distance, second_dist = the runner-up distance (may
+ * equal best_dist; 8*bytes+1 when N == 1). Any of the three outputs may be NULL.
+ * N == 0 fails with CLATCH_ERR_EMPTY_GALLERY (checked before Q == 0, as the
+ * reference does); Q == 0 succeeds and writes nothing. `bytes` is the descriptor
+ * length (any > 0; 64 takes the tiled kernel). */
+CLATCH_API int clatch_match_top2(clatch_ctx* ctx, const uint8_t* queries, size_t Q, const uint8_t* train,
+                      size_t N, int bytes, int32_t* best_idx, int32_t* best_dist,
+                      int32_t* second_dist);
+CLATCH_API int clatch_match_top2_dev(clatch_ctx* ctx, const uint8_t* d_queries, size_t Q,
+                          const uint8_t* d_train, size_t N, int bytes, int32_t* d_best_idx,
+                          int32_t* d_best_dist, int32_t* d_second_dist, void* stream);
+
+/* Filter pass of match_brute_force (src/match.cpp:69-79), host side, over forward
+ * top-2 triples: ratio (accept iff best < ratio * second, evaluated in double),
+ * max_distance (accept iff best <= max), cross-check (accept iff
+ * reverse_best[best_idx] == q; pass NULL to skip). out: up to Q rows {probe,
+ * gallery, distance, second_distance} in ascending probe order; *count rows. */
+CLATCH_API int clatch_filter_matches(const int32_t* best_idx, const int32_t* best_dist,
+                          const int32_t* second_dist, size_t Q, int has_ratio, double ratio,
+                          int has_max, int max_distance, const int32_t* reverse_best,
+                          int32_t* out, size_t* count);
+
+/* Whole match_brute_force (src/match.cpp:52-81) on host buffers: forward top-2 on
+ * the device, reverse pass on the device when cross_check, filter pass on the host. */
+CLATCH_API int clatch_match_brute_force(clatch_ctx* ctx, const uint8_t* probes, size_t Q,
+                             const uint8_t* gallery, size_t N, int bytes, int has_ratio,
+                             double ratio, int cross_check, int has_max, int max_distance,
+                             int32_t* out, size_t* count);
+
+/* Kernel launches issued through this context since creation (bench.py's
+ * gpu_launches claim is read from here, not estimated). */
+CLATCH_API uint64_t clatch_launch_count(clatch_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CLATCH_H */

@@ -282,6 +282,7 @@ class Ref:
         L.ref_bench_describe.argtypes = [C.c_void_p, C.c_size_t, C.c_int]
         L.ref_bench_describe.restype = C.c_size_t
         L.ref_bench_set_gallery.argtypes = [C.c_void_p, _u8p, C.c_size_t, C.c_int]
+        L.ref_bench_gallery_from_probes.argtypes = [C.c_void_p]
         L.ref_bench_set_probes.argtypes = [C.c_void_p, _u8p, C.c_size_t, C.c_int]
         L.ref_bench_match.argtypes = [C.c_void_p, C.c_size_t, C.c_int, _u64p]
         L.ref_bench_match.restype = C.c_size_t

@@ -380,6 +380,11 @@ void ref_bench_set_gallery(void* state, const std::uint8_t* gallery, std::size_t
     static_cast<RefBenchState*>(state)->gallery = make_descriptors(gallery, n, bytes);
 }
 
+void ref_bench_gallery_from_probes(void* state) {
+    auto* s = static_cast<RefBenchState*>(state);
+    s->gallery = s->probes;
+}
+
 void ref_bench_set_probes(void* state, const std::uint8_t* probes, std::size_t n, int bytes) {
     static_cast<RefBenchState*>(state)->probes = make_descriptors(probes, n, bytes);
 }

@@ -1,0 +1,450 @@
+// C ABI of the CLATCH hot paths (include/clatch.h): context, pattern install,
+// host-side keypoint preparation, host-buffer wrappers and the match filter pass.
+// Reference citations are relative to /root/reference/proj.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <thread>
+
+#include "clatch_internal.cuh"
+
+namespace clatch {
+
+namespace {
+thread_local std::string g_error = "";
+}
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+    set_error(std::string("CUDA error '") + cudaGetErrorString(e) + "' in " + what);
+    return e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? CLATCH_ERR_NO_DEVICE
+                                                                       : CLATCH_ERR_CUDA;
+}
+
+int DeviceBuffer::reserve(size_t bytes) {
+    if (bytes <= cap) return CLATCH_OK;
+    if (ptr) CLATCH_CUDA(cudaFree(ptr));
+    ptr = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+    CLATCH_CUDA(cudaMalloc(&ptr, want));
+    cap = want;
+    return CLATCH_OK;
+}
+
+void DeviceBuffer::release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+}
+
+namespace {
+
+int invalid(const std::string& msg) {
+    set_error(msg);
+    return CLATCH_ERR_INVALID;
+}
+
+int resolve_workers(int workers) {   // src/parallel.hpp:9-13
+    if (workers > 0) return workers;
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw > 0 ? static_cast<int>(hw) : 1;
+}
+
+// WeightMask::seven_by_seven (src/pattern.cpp:28-35): ones on the top-left 7x7, zero last row/col.
+bool is_seven_by_seven(const std::vector<double>& w, int K) {
+    if (K != 8) return false;
+    for (int r = 0; r < 8; ++r)
+        for (int c = 0; c < 8; ++c)
+            if (w[r * 8 + c] != ((r < 7 && c < 7) ? 1.0 : 0.0)) return false;
+    return true;
+}
+
+} // namespace
+
+} // namespace clatch
+
+using namespace clatch;
+
+extern "C" {
+
+const char* clatch_last_error(void) { return g_error.c_str(); }
+
+int clatch_ctx_create(int device, clatch_ctx** out) {
+    if (!out) return invalid("clatch_ctx_create: out is null");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        set_error(std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                  "); the CLATCH paths have no CPU fallback");
+        return CLATCH_ERR_NO_DEVICE;
+    }
+    if (device < 0 || device >= count) return invalid("clatch_ctx_create: device index out of range");
+    CLATCH_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CLATCH_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        set_error(std::string("device '") + prop.name + "' is sm_" + std::to_string(prop.major) +
+                  std::to_string(prop.minor) + "; this library is built for sm_100a only");
+        return CLATCH_ERR_NO_DEVICE;
+    }
+    auto* ctx = new clatch_ctx;
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device);
+    ctx->sm_clock_khz = khz;
+    std::snprintf(ctx->name, sizeof(ctx->name), "%s", prop.name);
+    cudaError_t se = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (se != cudaSuccess) {
+        delete ctx;
+        return cuda_fail(se, "cudaStreamCreateWithFlags");
+    }
+    *out = ctx;
+    return CLATCH_OK;
+}
+
+void clatch_ctx_destroy(clatch_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+    }
+    for (DeviceBuffer* b : {&ctx->img, &ctx->kps, &ctx->desc, &ctx->q, &ctx->t, &ctx->res,
+                            &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->pattern.slots,
+                            &ctx->pattern.triplets})
+        b->release();
+    delete ctx;
+}
+
+int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_khz, char* name, size_t cap) {
+    if (!ctx) return invalid("clatch_device_info: ctx is null");
+    if (sm_count) *sm_count = ctx->sm_count;
+    if (sm_clock_khz) *sm_clock_khz = ctx->sm_clock_khz;
+    if (name && cap) {
+        std::strncpy(name, ctx->name, cap - 1);
+        name[cap - 1] = 0;
+    }
+    return CLATCH_OK;
+}
+
+int clatch_synchronize(clatch_ctx* ctx) {
+    if (!ctx) return invalid("clatch_synchronize: ctx is null");
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    CLATCH_CUDA(cudaStreamSynchronize(ctx->stream));
+    return CLATCH_OK;
+}
+
+uint64_t clatch_launch_count(clatch_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int clatch_descriptor_bytes(clatch_ctx* ctx) { return ctx ? ctx->pattern.T / 8 : 0; }
+
+int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, const double* mask) {
+    if (!ctx || !triplets) return invalid("clatch_set_pattern: null argument");
+    // Same acceptance rules as parse_pattern (src/pattern.cpp:78-82, 54-66, 118-131).
+    if (T <= 0 || T % 8 != 0) {
+        set_error("BadHeader: T must be a positive multiple of 8, got " + std::to_string(T));
+        return CLATCH_ERR_BAD_HEADER;
+    }
+    if (T > 32768) return invalid("clatch_set_pattern: T > 32768 is not supported");
+    if (K < 1 || K > kWindow) {
+        set_error("BadHeader: K out of range: " + std::to_string(K));
+        return CLATCH_ERR_BAD_HEADER;
+    }
+    const int max_coord = kWindow - K;
+    for (int t = 0; t < T; ++t) {
+        const int16_t* v = triplets + 6 * t;
+        for (int i = 0; i < 6; ++i)
+            if (v[i] < 0 || v[i] > max_coord) {
+                set_error("CoordinateOutOfRange: coordinate " + std::to_string(v[i]) +
+                          " outside [0, " + std::to_string(max_coord) + "]");
+                return CLATCH_ERR_COORD_RANGE;
+            }
+        if (v[2] == v[4] && v[3] == v[5]) {
+            set_error("DegenerateTriplet: companion patches coincide at (" + std::to_string(v[2]) +
+                      ", " + std::to_string(v[3]) + ")");
+            return CLATCH_ERR_DEGENERATE;
+        }
+    }
+    std::vector<double> w(static_cast<size_t>(K) * K, 1.0);
+    if (mask) {
+        bool any = false;
+        for (size_t i = 0; i < w.size(); ++i) {
+            if (!std::isfinite(mask[i]) || mask[i] < 0.0) {
+                set_error("BadHeader: bad weight in row " + std::to_string(i / K));
+                return CLATCH_ERR_BAD_HEADER;
+            }
+            w[i] = mask[i];
+            any = any || mask[i] > 0.0;
+        }
+        if (!any) {
+            set_error("BadHeader: weight mask is all zeros");
+            return CLATCH_ERR_BAD_HEADER;
+        }
+    }
+
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    Pattern& pat = ctx->pattern;
+    pat.T = T;
+    pat.K = K;
+    pat.weights = w;
+    pat.fast = (T == kFastT) && is_seven_by_seven(w, K);
+    if (int rc = pat.triplets.reserve(sizeof(int16_t) * 6 * T)) return rc;
+    CLATCH_CUDA(cudaMemcpy(pat.triplets.ptr, triplets, sizeof(int16_t) * 6 * T, cudaMemcpyHostToDevice));
+    if (int rc = upload_weights(w.data(), K * K)) return rc;
+    if (pat.fast) {
+        std::vector<ushort4> slots(T);
+        for (int t = 0; t < T; ++t) {
+            const int16_t* v = triplets + 6 * t;
+            slots[t].x = static_cast<unsigned short>(v[1] * kWinStride + v[0]);
+            slots[t].y = static_cast<unsigned short>(v[3] * kWinStride + v[2]);
+            slots[t].z = static_cast<unsigned short>(v[5] * kWinStride + v[4]);
+            slots[t].w = static_cast<unsigned short>(t);
+        }
+        if (int rc = pat.slots.reserve(sizeof(ushort4) * T)) return rc;
+        CLATCH_CUDA(cudaMemcpy(pat.slots.ptr, slots.data(), sizeof(ushort4) * T, cudaMemcpyHostToDevice));
+    }
+    return CLATCH_OK;
+}
+
+int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, int height,
+                             int workers, double* xycs, int64_t* kept, size_t* m) {
+    if (!m) return invalid("clatch_prepare_keypoints: m is null");
+    *m = 0;
+    if (cols < 2 || cols > 4) return invalid("keypoints must be (N, 2..4): x, y[, theta[, score]]");
+    if (n == 0) return CLATCH_OK;
+    if (!kps || !xycs || !kept) return invalid("clatch_prepare_keypoints: null buffer");
+    // keypoint_in_margin, src/descriptor.cpp:23-27 (NaN fails every comparison).
+    const double xmax = static_cast<double>(width - 1), ymax = static_cast<double>(height - 1);
+    size_t count = 0;
+    for (size_t i = 0; i < n; ++i) {
+        const double x = kps[i * cols], y = kps[i * cols + 1];
+        if (x - kMargin >= 0.0 && y - kMargin >= 0.0 && x + kMargin <= xmax && y + kMargin <= ymax)
+            kept[count++] = static_cast<int64_t>(i);
+    }
+    *m = count;
+    if (count == 0) return CLATCH_OK;
+    // cos/sin of extract_window (src/descriptor.cpp:35-36) through the host libm.
+    int nthreads = std::min<size_t>(resolve_workers(workers), (count + 4095) / 4096);
+    nthreads = std::max(nthreads, 1);
+    std::vector<int> bad(nthreads, 0);
+    auto work = [&](int w) {
+        const size_t chunk = (count + nthreads - 1) / nthreads;
+        const size_t begin = w * chunk, end = std::min(count, begin + chunk);
+        for (size_t j = begin; j < end; ++j) {
+            const double* k = kps + static_cast<size_t>(kept[j]) * cols;
+            const double theta = cols > 2 ? k[2] : 0.0;
+            const double c = std::cos(theta), s = std::sin(theta);
+            if (!std::isfinite(c) || !std::isfinite(s)) bad[w] = 1;
+            xycs[4 * j + 0] = k[0];
+            xycs[4 * j + 1] = k[1];
+            xycs[4 * j + 2] = c;
+            xycs[4 * j + 3] = s;
+        }
+    };
+    if (nthreads == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (int w = 0; w < nthreads; ++w) pool.emplace_back(work, w);
+        for (std::thread& t : pool) t.join();
+    }
+    for (int b : bad)
+        if (b) {
+            set_error("a keypoint inside the margin has a non-finite orientation");
+            return CLATCH_ERR_NONFINITE;
+        }
+    return CLATCH_OK;
+}
+
+// ---- extraction ---------------------------------------------------------------
+
+static int check_extract(clatch_ctx* ctx, const void* img, int width, int height, size_t pitch,
+                         const void* xycs, size_t M, const void* out) {
+    if (!ctx) return invalid("extract: ctx is null");
+    if (ctx->pattern.T == 0) return invalid("extract: no pattern installed (clatch_set_pattern)");
+    if (!img || width <= 0 || height <= 0 || pitch < static_cast<size_t>(width))
+        return invalid("extract: bad image (null, empty or pitch < width)");
+    if (M > 0 && (!xycs || !out)) return invalid("extract: null keypoint/output buffer");
+    return CLATCH_OK;
+}
+
+int clatch_extract_u8_dev(clatch_ctx* ctx, const uint8_t* d_img, int width, int height,
+                          size_t pitch, const double* d_xycs, size_t M, uint8_t* d_out,
+                          void* stream) {
+    if (int rc = check_extract(ctx, d_img, width, height, pitch, d_xycs, M, d_out)) return rc;
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    return launch_extract_u8(ctx, d_img, width, height, pitch, d_xycs, M, d_out,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int clatch_extract_f64_dev(clatch_ctx* ctx, const double* d_img, int width, int height,
+                           size_t pitch, const double* d_xycs, size_t M, uint8_t* d_out,
+                           void* stream) {
+    if (int rc = check_extract(ctx, d_img, width, height, pitch, d_xycs, M, d_out)) return rc;
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    return launch_extract_f64(ctx, d_img, width, height, pitch, d_xycs, M, d_out,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int clatch_extract_u8(clatch_ctx* ctx, const uint8_t* img, int width, int height, size_t pitch,
+                      const double* xycs, size_t M, uint8_t* out) {
+    if (int rc = check_extract(ctx, img, width, height, pitch, xycs, M, out)) return rc;
+    if (M == 0) return CLATCH_OK;
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    const size_t dpitch = (static_cast<size_t>(width) + 15) / 16 * 16;   // 16-byte rows for vector staging
+    const size_t bytes = static_cast<size_t>(ctx->pattern.T) / 8;
+    if (int rc = ctx->img.reserve(dpitch * height)) return rc;
+    if (int rc = ctx->kps.reserve(sizeof(double) * 4 * M)) return rc;
+    if (int rc = ctx->desc.reserve(bytes * M)) return rc;
+    cudaStream_t st = ctx->stream;
+    CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, dpitch, img, pitch, width, height,
+                                  cudaMemcpyHostToDevice, st));
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->kps.ptr, xycs, sizeof(double) * 4 * M, cudaMemcpyHostToDevice, st));
+    if (int rc = launch_extract_u8(ctx, ctx->img.as<uint8_t>(), width, height, dpitch,
+                                   ctx->kps.as<double>(), M, ctx->desc.as<uint8_t>(), st))
+        return rc;
+    CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * M, cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    return CLATCH_OK;
+}
+
+int clatch_extract_f64(clatch_ctx* ctx, const double* img, int width, int height, size_t pitch,
+                       const double* xycs, size_t M, uint8_t* out) {
+    if (int rc = check_extract(ctx, img, width, height, pitch, xycs, M, out)) return rc;
+    if (M == 0) return CLATCH_OK;
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    const size_t bytes = static_cast<size_t>(ctx->pattern.T) / 8;
+    if (int rc = ctx->img.reserve(sizeof(double) * width * height)) return rc;
+    if (int rc = ctx->kps.reserve(sizeof(double) * 4 * M)) return rc;
+    if (int rc = ctx->desc.reserve(bytes * M)) return rc;
+    cudaStream_t st = ctx->stream;
+    CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, sizeof(double) * width, img, sizeof(double) * pitch,
+                                  sizeof(double) * width, height, cudaMemcpyHostToDevice, st));
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->kps.ptr, xycs, sizeof(double) * 4 * M, cudaMemcpyHostToDevice, st));
+    if (int rc = launch_extract_f64(ctx, ctx->img.as<double>(), width, height, width,
+                                    ctx->kps.as<double>(), M, ctx->desc.as<uint8_t>(), st))
+        return rc;
+    CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * M, cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    return CLATCH_OK;
+}
+
+// ---- matching -----------------------------------------------------------------
+
+static int check_match(clatch_ctx* ctx, const void* q, size_t Q, const void* t, size_t N, int bytes) {
+    if (!ctx) return invalid("match: ctx is null");
+    if (bytes <= 0) return invalid("match: descriptor length must be positive");
+    if (N == 0) {   // before the empty-probes early-out, src/match.cpp:55-56
+        set_error("EmptyGallery: matching needs a nonempty gallery");
+        return CLATCH_ERR_EMPTY_GALLERY;
+    }
+    if (N > 0x7fffffffull) return invalid("match: more than 2^31-1 train descriptors");
+    if (!t || (Q > 0 && !q)) return invalid("match: null descriptor buffer");
+    return CLATCH_OK;
+}
+
+int clatch_match_top2_dev(clatch_ctx* ctx, const uint8_t* d_queries, size_t Q,
+                          const uint8_t* d_train, size_t N, int bytes, int32_t* d_best_idx,
+                          int32_t* d_best_dist, int32_t* d_second_dist, void* stream) {
+    if (int rc = check_match(ctx, d_queries, Q, d_train, N, bytes)) return rc;
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    return launch_match_top2(ctx, d_queries, Q, d_train, N, bytes, d_best_idx, d_best_dist,
+                             d_second_dist, static_cast<cudaStream_t>(stream));
+}
+
+int clatch_match_top2(clatch_ctx* ctx, const uint8_t* queries, size_t Q, const uint8_t* train,
+                      size_t N, int bytes, int32_t* best_idx, int32_t* best_dist,
+                      int32_t* second_dist) {
+    if (int rc = check_match(ctx, queries, Q, train, N, bytes)) return rc;
+    if (Q == 0) return CLATCH_OK;
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = ctx->q.reserve(Q * bytes)) return rc;
+    if (int rc = ctx->res.reserve(sizeof(int32_t) * 3 * Q)) return rc;
+    cudaStream_t st = ctx->stream;
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->q.ptr, queries, Q * bytes, cudaMemcpyHostToDevice, st));
+    const uint8_t* d_train = ctx->q.as<uint8_t>();
+    if (train != queries || N != Q) {   // self-match uploads the set once
+        if (int rc = ctx->t.reserve(N * bytes)) return rc;
+        CLATCH_CUDA(cudaMemcpyAsync(ctx->t.ptr, train, N * bytes, cudaMemcpyHostToDevice, st));
+        d_train = ctx->t.as<uint8_t>();
+    }
+    int32_t* r = ctx->res.as<int32_t>();
+    if (int rc = launch_match_top2(ctx, ctx->q.as<uint8_t>(), Q, d_train, N, bytes, r, r + Q, r + 2 * Q, st))
+        return rc;
+    if (best_idx) CLATCH_CUDA(cudaMemcpyAsync(best_idx, r, sizeof(int32_t) * Q, cudaMemcpyDeviceToHost, st));
+    if (best_dist) CLATCH_CUDA(cudaMemcpyAsync(best_dist, r + Q, sizeof(int32_t) * Q, cudaMemcpyDeviceToHost, st));
+    if (second_dist)
+        CLATCH_CUDA(cudaMemcpyAsync(second_dist, r + 2 * Q, sizeof(int32_t) * Q, cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    return CLATCH_OK;
+}
+
+int clatch_filter_matches(const int32_t* best_idx, const int32_t* best_dist,
+                          const int32_t* second_dist, size_t Q, int has_ratio, double ratio,
+                          int has_max, int max_distance, const int32_t* reverse_best,
+                          int32_t* out, size_t* count) {
+    if (!count) return invalid("clatch_filter_matches: count is null");
+    *count = 0;
+    if (Q == 0) return CLATCH_OK;
+    if (!best_idx || !best_dist || !second_dist || !out)
+        return invalid("clatch_filter_matches: null buffer");
+    size_t m = 0;
+    for (size_t p = 0; p < Q; ++p) {   // src/match.cpp:69-79, same order of tests
+        const int best = best_dist[p], second = second_dist[p], idx = best_idx[p];
+        if (has_ratio && !(best < ratio * second)) continue;   // int -> double, as in the reference
+        if (has_max && best > max_distance) continue;
+        if (reverse_best && reverse_best[idx] != static_cast<int32_t>(p)) continue;
+        out[4 * m + 0] = static_cast<int32_t>(p);
+        out[4 * m + 1] = idx;
+        out[4 * m + 2] = best;
+        out[4 * m + 3] = second;
+        ++m;
+    }
+    *count = m;
+    return CLATCH_OK;
+}
+
+int clatch_match_brute_force(clatch_ctx* ctx, const uint8_t* probes, size_t Q,
+                             const uint8_t* gallery, size_t N, int bytes, int has_ratio,
+                             double ratio, int cross_check, int has_max, int max_distance,
+                             int32_t* out, size_t* count) {
+    if (!count) return invalid("clatch_match_brute_force: count is null");
+    *count = 0;
+    if (int rc = check_match(ctx, probes, Q, gallery, N, bytes)) return rc;
+    if (Q == 0) return CLATCH_OK;   // src/match.cpp:56
+    if (!out) return invalid("clatch_match_brute_force: out is null");
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    // Both sets go up once; forward and (optionally) reverse passes reuse them on the device.
+    if (int rc = ctx->q.reserve(Q * bytes)) return rc;
+    if (int rc = ctx->res.reserve(sizeof(int32_t) * (3 * Q + N))) return rc;
+    cudaStream_t st = ctx->stream;
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->q.ptr, probes, Q * bytes, cudaMemcpyHostToDevice, st));
+    const uint8_t* d_gallery = ctx->q.as<uint8_t>();
+    if (gallery != probes || N != Q) {   // self-match uploads the set once
+        if (int rc = ctx->t.reserve(N * bytes)) return rc;
+        CLATCH_CUDA(cudaMemcpyAsync(ctx->t.ptr, gallery, N * bytes, cudaMemcpyHostToDevice, st));
+        d_gallery = ctx->t.as<uint8_t>();
+    }
+    int32_t* r = ctx->res.as<int32_t>();
+    if (int rc = launch_match_top2(ctx, ctx->q.as<uint8_t>(), Q, d_gallery, N, bytes, r, r + Q, r + 2 * Q, st))
+        return rc;
+    std::vector<int32_t> host(3 * Q + (cross_check ? N : 0));
+    if (cross_check) {   // reverse_best[g] = knn2(gallery[g], probes).best_index, src/match.cpp:62-67
+        if (int rc = launch_match_top2(ctx, d_gallery, N, ctx->q.as<uint8_t>(), Q, bytes, r + 3 * Q, nullptr,
+                                       nullptr, st))
+            return rc;
+    }
+    CLATCH_CUDA(cudaMemcpyAsync(host.data(), r, sizeof(int32_t) * host.size(), cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    return clatch_filter_matches(host.data(), host.data() + Q, host.data() + 2 * Q, Q, has_ratio, ratio,
+                                 has_max, max_distance, cross_check ? host.data() + 3 * Q : nullptr, out,
+                                 count);
+}
+
+} // extern "C"

@@ -1,0 +1,338 @@
+// LATCH descriptor extraction for sm_100a — bit-exact restatement of the reference's
+// fp64 arithmetic (paths relative to /root/reference/proj):
+//   extract_window    src/descriptor.cpp:29-49    oriented 64x64 bilinear resample
+//   sample_bilinear   src/image.cpp:109-126       top/bottom/blend, each op rounded
+//   triplet_bit       src/descriptor.cpp:51-77    two sequential weighted SSD chains, strict >
+//   describe          src/descriptor.cpp:79-88    LSB-first bit packing
+//
+// Numerical contract: every multiply/add is an individually rounded
+// fp64 operation (__dmul_rn/__dadd_rn/__dsub_rn never contract into FMA), the
+// accumulation order inside one SSD chain is the reference's row-major order, and
+// cos/sin arrive from the host's libm. No tree reductions anywhere.
+//
+// Kernel shape: persistent CTAs (a multiple of the SM count), one keypoint per CTA
+// iteration. Per keypoint: (1) stage the <=92x92 u8 footprint into shared memory with
+// 16-byte loads, (2) 256 threads resample the 4096 window samples into a padded fp64
+// window in shared memory, (3) each thread owns whole triplets (both SSD chains) and
+// reads the window with immediate-offset 64-bit shared loads, (4) predicate bits are
+// packed with __ballot_sync and stored as 32-bit words.
+
+#include <cstdio>
+
+#include "clatch_internal.cuh"
+
+namespace clatch {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// Mask weights for the generic kernel: read with a warp-uniform index, so the
+// constant cache broadcasts them.
+__constant__ double c_weights[kMaxConstWeights];
+
+struct ExtractParams {
+    const void* img;
+    int width, height;
+    size_t pitch;              // elements
+    const double* xycs;        // M x {x, y, cos, sin}
+    unsigned long long M;
+    uint8_t* out;              // M x T/8
+    const ushort4* slots;      // fast kernel: T x {a, b, c, bit}
+    const short* triplets;     // generic kernel: T x 6
+    int T, K;
+    const int* flags;          // optional device flags (f64 promotion), may be null
+    int run_if_flag;           // run only when flags[0] == run_if_flag (if flags != null)
+};
+
+__device__ __forceinline__ double u8_to_f64(unsigned v) { return static_cast<double>(v); }
+
+// One bilinear sample with the reference's exact operation order (src/image.cpp:121-125).
+__device__ __forceinline__ double blend(double fx, double fy, double p00, double p10, double p01,
+                                        double p11) {
+    const double gx = __dsub_rn(1.0, fx);
+    const double gy = __dsub_rn(1.0, fy);
+    const double top = __dadd_rn(__dmul_rn(gx, p00), __dmul_rn(fx, p10));
+    const double bottom = __dadd_rn(__dmul_rn(gx, p01), __dmul_rn(fx, p11));
+    return __dadd_rn(__dmul_rn(gy, top), __dmul_rn(fy, bottom));
+}
+
+// Stage rows [ty0, ty0+92) x 16-byte-aligned columns [ax0, ax0+112) of a u8 image.
+__device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const uint8_t* img, size_t pitch,
+                                              int height, int ax0, int ty0, bool aligned) {
+    if (aligned) {
+        constexpr int kChunks = kTileW / 16;
+        for (int i = threadIdx.x; i < kTileH * kChunks; i += kThreads) {
+            const int r = i / kChunks, c = i - r * kChunks;
+            const int gx = ax0 + 16 * c;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (static_cast<size_t>(gx) < pitch && ty0 + r < height)
+                v = __ldg(reinterpret_cast<const uint4*>(img + static_cast<size_t>(ty0 + r) * pitch + gx));
+            *reinterpret_cast<uint4*>(tile + r * kTileW + 16 * c) = v;
+        }
+    } else {
+        for (int i = threadIdx.x; i < kTileH * kTileW; i += kThreads) {
+            const int r = i / kTileW, c = i - r * kTileW;
+            const int gx = ax0 + c;
+            uint8_t v = 0;
+            if (static_cast<size_t>(gx) < pitch && ty0 + r < height)
+                v = __ldg(img + static_cast<size_t>(ty0 + r) * pitch + gx);
+            tile[i] = v;
+        }
+    }
+}
+
+// Phase A: resample the oriented window (src/descriptor.cpp:35-47). Thread -> column
+// u = tid & 63, rows v = (tid >> 6) + 4k; sx = (x + c*du) - s*dv, sy = (y + s*du) + c*dv.
+template <bool kU8>
+__device__ __forceinline__ void build_window(double* win, const uint8_t* tile, int ax0, int ty0,
+                                             const double* img64, size_t pitch, double x, double y,
+                                             double c, double s) {
+    const int u = threadIdx.x & 63;
+    const double du = static_cast<double>(u) - 31.5;
+    const double xa = __dadd_rn(x, __dmul_rn(c, du));
+    const double ya = __dadd_rn(y, __dmul_rn(s, du));
+#pragma unroll 4
+    for (int v = threadIdx.x >> 6; v < kWindow; v += kThreads / 64) {
+        const double dv = static_cast<double>(v) - 31.5;
+        const double sx = __dsub_rn(xa, __dmul_rn(s, dv));
+        const double sy = __dadd_rn(ya, __dmul_rn(c, dv));
+        const int x0 = __double2int_rd(sx);   // inside the margin: 1 <= x0 <= width-3, no clamps fire
+        const int y0 = __double2int_rd(sy);
+        const double fx = __dsub_rn(sx, static_cast<double>(x0));
+        const double fy = __dsub_rn(sy, static_cast<double>(y0));
+        double p00, p10, p01, p11;
+        if (kU8) {
+            const uint8_t* p = tile + (y0 - ty0) * kTileW + (x0 - ax0);
+            p00 = u8_to_f64(p[0]);
+            p10 = u8_to_f64(p[1]);
+            p01 = u8_to_f64(p[kTileW]);
+            p11 = u8_to_f64(p[kTileW + 1]);
+        } else {
+            const double* p = img64 + static_cast<size_t>(y0) * pitch + x0;
+            p00 = __ldg(p);
+            p10 = __ldg(p + 1);
+            p01 = __ldg(p + pitch);
+            p11 = __ldg(p + pitch + 1);
+        }
+        win[v * kWinStride + u] = blend(fx, fy, p00, p10, p01, p11);
+    }
+}
+
+// Phase B (specialised): one triplet = two independent 49-term chains over the
+// 7x7 live pixels of the 8x8 patch, row-major (src/descriptor.cpp:61-75 with the
+// zero-weight terms skipped — exact because w*e*e is +0.0 there and d + 0.0 == d).
+__device__ __forceinline__ bool triplet_bit_7x7(const double* win, int oa, int ob, int oc) {
+    const double* pa = win + oa;
+    const double* pb = win + ob;
+    const double* pc = win + oc;
+    double d1 = 0.0, d2 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+#pragma unroll
+        for (int c = 0; c < 7; ++c) {
+            const int o = r * kWinStride + c;
+            const double a = pa[o];
+            const double e1 = __dsub_rn(a, pb[o]);
+            const double e2 = __dsub_rn(a, pc[o]);
+            d1 = __dadd_rn(d1, __dmul_rn(e1, e1));
+            d2 = __dadd_rn(d2, __dmul_rn(e2, e2));
+        }
+    }
+    return d1 > d2;
+}
+
+template <bool kU8>
+__global__ void __launch_bounds__(kThreads, 4) extract_fast_kernel(ExtractParams p) {
+    if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
+
+    __shared__ __align__(16) double s_win[kWindow * kWinStride];
+    __shared__ __align__(16) uint8_t s_tile[kU8 ? kTileH * kTileW : 16];
+    __shared__ uint8_t s_bits[kFastT];
+
+    const int tid = threadIdx.x;
+    // Slots tid and tid + 256 stay in registers for the whole persistent loop.
+    const ushort4 slot0 = __ldg(p.slots + tid);
+    const ushort4 slot1 = __ldg(p.slots + tid + kThreads);
+    const bool aligned = kU8 && (reinterpret_cast<uintptr_t>(p.img) % 16 == 0) && (p.pitch % 16 == 0);
+
+    for (unsigned long long kp = blockIdx.x; kp < p.M; kp += gridDim.x) {
+        const double x = __ldg(p.xycs + 4 * kp + 0);
+        const double y = __ldg(p.xycs + 4 * kp + 1);
+        const double c = __ldg(p.xycs + 4 * kp + 2);
+        const double s = __ldg(p.xycs + 4 * kp + 3);
+        int ax0 = 0, ty0 = 0;
+        if (kU8) {
+            // Footprint: columns floor(x)-45 .. floor(x)+46, same for rows (|offset| <= 44.55 px).
+            const int tx0 = __double2int_rd(x) - 45;
+            ty0 = __double2int_rd(y) - 45;
+            ax0 = aligned ? (tx0 & ~15) : tx0;
+            stage_tile_u8(s_tile, static_cast<const uint8_t*>(p.img), p.pitch, p.height, ax0, ty0,
+                          aligned);
+        }
+        __syncthreads();   // tile ready; previous keypoint's window/bit readers are done
+        build_window<kU8>(s_win, s_tile, ax0, ty0, static_cast<const double*>(p.img), p.pitch, x, y,
+                          c, s);
+        __syncthreads();
+        s_bits[slot0.w] = triplet_bit_7x7(s_win, slot0.x, slot0.y, slot0.z);
+        s_bits[slot1.w] = triplet_bit_7x7(s_win, slot1.x, slot1.y, slot1.z);
+        __syncthreads();
+        // Bit t -> byte t>>3, bit t&7 == bit t of the little-endian 32-bit word t>>5.
+        const unsigned w0 = __ballot_sync(0xffffffffu, s_bits[tid] != 0);
+        const unsigned w1 = __ballot_sync(0xffffffffu, s_bits[tid + kThreads] != 0);
+        if ((tid & 31) == 0) {
+            unsigned* out32 = reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8));
+            out32[tid >> 5] = w0;
+            out32[(tid >> 5) + kThreads / 32] = w1;
+        }
+    }
+}
+
+// Generic pattern: any T (multiple of 8), 1 <= K <= 64, arbitrary non-negative weights.
+// d += (w*e)*e exactly as the reference writes it (src/descriptor.cpp:70-71).
+template <bool kU8>
+__global__ void __launch_bounds__(kThreads, 2) extract_generic_kernel(ExtractParams p) {
+    if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
+
+    __shared__ __align__(16) double s_win[kWindow * kWinStride];
+    __shared__ __align__(16) uint8_t s_tile[kU8 ? kTileH * kTileW : 16];
+    extern __shared__ uint8_t s_dynbits[];   // T bytes
+
+    const int tid = threadIdx.x;
+    const int K = p.K, T = p.T;
+    const bool aligned = kU8 && (reinterpret_cast<uintptr_t>(p.img) % 16 == 0) && (p.pitch % 16 == 0);
+
+    for (unsigned long long kp = blockIdx.x; kp < p.M; kp += gridDim.x) {
+        const double x = __ldg(p.xycs + 4 * kp + 0);
+        const double y = __ldg(p.xycs + 4 * kp + 1);
+        const double c = __ldg(p.xycs + 4 * kp + 2);
+        const double s = __ldg(p.xycs + 4 * kp + 3);
+        int ax0 = 0, ty0 = 0;
+        if (kU8) {
+            const int tx0 = __double2int_rd(x) - 45;
+            ty0 = __double2int_rd(y) - 45;
+            ax0 = aligned ? (tx0 & ~15) : tx0;
+            stage_tile_u8(s_tile, static_cast<const uint8_t*>(p.img), p.pitch, p.height, ax0, ty0,
+                          aligned);
+        }
+        __syncthreads();
+        build_window<kU8>(s_win, s_tile, ax0, ty0, static_cast<const double*>(p.img), p.pitch, x, y,
+                          c, s);
+        __syncthreads();
+        for (int t = tid; t < T; t += kThreads) {
+            const short* tr = p.triplets + 6 * t;
+            const double* pa = s_win + tr[1] * kWinStride + tr[0];
+            const double* pb = s_win + tr[3] * kWinStride + tr[2];
+            const double* pc = s_win + tr[5] * kWinStride + tr[4];
+            double d1 = 0.0, d2 = 0.0;
+            for (int r = 0; r < K; ++r) {
+                for (int col = 0; col < K; ++col) {
+                    const double w = c_weights[r * K + col];
+                    const double a = pa[col];
+                    const double e1 = __dsub_rn(a, pb[col]);
+                    const double e2 = __dsub_rn(a, pc[col]);
+                    d1 = __dadd_rn(d1, __dmul_rn(__dmul_rn(w, e1), e1));
+                    d2 = __dadd_rn(d2, __dmul_rn(__dmul_rn(w, e2), e2));
+                }
+                pa += kWinStride;
+                pb += kWinStride;
+                pc += kWinStride;
+            }
+            s_dynbits[t] = d1 > d2;
+        }
+        __syncthreads();
+        for (int b = tid; b < T / 8; b += kThreads) {
+            unsigned byte = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) byte |= (s_dynbits[8 * b + i] ? 1u : 0u) << i;
+            p.out[kp * (T / 8) + b] = static_cast<uint8_t>(byte);
+        }
+    }
+}
+
+// f64 -> u8 promotion: flags[0] = 1 if some pixel is not an integer in [0, 255]
+// (or not finite), else stays 0; dst receives the (lossless when flags[0]==0) u8 copy.
+__global__ void classify_convert_kernel(const double* src, size_t src_pitch, uint8_t* dst,
+                                        size_t dst_pitch, int width, int height, int* flags) {
+    const size_t n = static_cast<size_t>(width) * height;
+    bool bad = false;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int yy = static_cast<int>(i / width), xx = static_cast<int>(i - static_cast<size_t>(yy) * width);
+        const double v = src[static_cast<size_t>(yy) * src_pitch + xx];
+        const bool ok = (v >= 0.0) && (v <= 255.0) && (v == floor(v));   // NaN/inf fail
+        bad |= !ok;
+        dst[static_cast<size_t>(yy) * dst_pitch + xx] = ok ? static_cast<uint8_t>(v) : 0;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1);
+}
+
+int grid_for(const clatch_ctx* ctx, size_t M, int ctas_per_sm) {
+    const size_t cap = static_cast<size_t>(ctx->sm_count) * ctas_per_sm;
+    return static_cast<int>(M < cap ? M : cap);
+}
+
+template <bool kU8>
+int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, size_t pitch,
+                   const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream,
+                   const int* flags, int run_if_flag) {
+    const Pattern& pat = ctx->pattern;
+    ExtractParams p{};
+    p.img = d_img;
+    p.width = width;
+    p.height = height;
+    p.pitch = pitch;
+    p.xycs = d_xycs;
+    p.M = M;
+    p.out = d_out;
+    p.slots = pat.slots.as<ushort4>();
+    p.triplets = pat.triplets.as<short>();
+    p.T = pat.T;
+    p.K = pat.K;
+    p.flags = flags;
+    p.run_if_flag = run_if_flag;
+    if (pat.fast) {
+        extract_fast_kernel<kU8><<<grid_for(ctx, M, 4), kThreads, 0, stream>>>(p);
+    } else {
+        extract_generic_kernel<kU8><<<grid_for(ctx, M, 2), kThreads, pat.T, stream>>>(p);
+    }
+    ++ctx->launches;
+    CLATCH_CUDA(cudaGetLastError());
+    return CLATCH_OK;
+}
+
+} // namespace
+
+int upload_weights(const double* w, int count) {
+    CLATCH_CUDA(cudaMemcpyToSymbol(c_weights, w, sizeof(double) * count));
+    return CLATCH_OK;
+}
+
+int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,
+                      const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream) {
+    if (M == 0) return CLATCH_OK;
+    return launch_extract<true>(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, nullptr, 0);
+}
+
+int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
+                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream) {
+    if (M == 0) return CLATCH_OK;
+    // Promote to u8 on the device when every pixel is an integer in [0,255] (true for
+    // every PGM-sourced image, src/image.cpp:75-76); both kernels are queued and the
+    // flag picks one on the device, so no host round trip is needed.
+    const size_t u8_pitch = (static_cast<size_t>(width) + 15) / 16 * 16;
+    if (int rc = ctx->img_u8.reserve(u8_pitch * height)) return rc;
+    if (int rc = ctx->flags.reserve(sizeof(int))) return rc;
+    int* flags = ctx->flags.as<int>();
+    CLATCH_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), stream));
+    classify_convert_kernel<<<ctx->sm_count * 8, 256, 0, stream>>>(
+        d_img, pitch, ctx->img_u8.as<uint8_t>(), u8_pitch, width, height, flags);
+    ++ctx->launches;
+    CLATCH_CUDA(cudaGetLastError());
+    if (int rc = launch_extract<true>(ctx, ctx->img_u8.ptr, width, height, u8_pitch, d_xycs, M, d_out,
+                                      stream, flags, 0))
+        return rc;
+    return launch_extract<false>(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, flags, 1);
+}
+
+} // namespace clatch

@@ -1,0 +1,81 @@
+// Internal declarations shared by the C-ABI translation units. Not installed.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "clatch.h"
+
+namespace clatch {
+
+constexpr int kWindow = 64;        // oriented window side (proj/include/latch/pattern.hpp:12)
+constexpr int kMargin = 46;        // proj/include/latch/descriptor.hpp:17
+constexpr int kWinStride = 65;     // padded row stride of the fp64 window in shared memory
+constexpr int kTileW = 112;        // staged u8 footprint: 92 px + 16-byte alignment slack
+constexpr int kTileH = 92;         // rows floor(y)-45 .. floor(y)+46
+constexpr int kFastT = 512;        // specialised kernel: T = 512, K = 8, 7x7-of-8x8 mask
+constexpr int kMaxConstWeights = 64 * 64;
+
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define CLATCH_CUDA(expr)                                            \
+    do {                                                             \
+        cudaError_t _e = (expr);                                     \
+        if (_e != cudaSuccess) return ::clatch::cuda_fail(_e, #expr); \
+    } while (0)
+
+// Grow-only device scratch buffer.
+struct DeviceBuffer {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    int reserve(size_t bytes);
+    void release();
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct Pattern {
+    int T = 0;
+    int K = 0;
+    bool fast = false;             // T=512, K=8, 7x7-of-8x8 binary mask
+    // Slot tables (device): slot j of the specialised kernel computes bit `bit[j]`
+    // from window offsets (row*kWinStride+col) a/b/c; packed as ushort4 {a, b, c, bit}.
+    DeviceBuffer slots;            // T * ushort4
+    DeviceBuffer triplets;         // generic kernel: T * 6 int16
+    std::vector<double> weights;   // K*K
+};
+
+} // namespace clatch
+
+struct clatch_ctx {
+    int device = 0;
+    int sm_count = 0;
+    int sm_clock_khz = 0;
+    char name[256] = {0};
+    cudaStream_t stream = nullptr;
+    clatch::Pattern pattern;
+    uint64_t launches = 0;
+    // scratch for the host-buffer entry points
+    clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8;
+};
+
+namespace clatch {
+
+// extraction (clatch_extract.cu)
+int upload_weights(const double* w, int count);
+int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,
+                      const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
+int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
+                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
+
+// matching (clatch_match.cu)
+int launch_match_top2(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
+                      int bytes, int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second,
+                      cudaStream_t stream);
+
+} // namespace clatch

@@ -1,0 +1,257 @@
+// Brute-force Hamming top-2 matching for sm_100a — exact restatement of the
+// reference (paths relative to /root/reference/proj):
+//   hamming   src/match.cpp:14-31   XOR + popcount over the descriptor bytes
+//   knn2      src/match.cpp:33-50   best / runner-up, strict '<' => lowest index wins ties,
+//                                   sentinel 8*bytes+1
+// Pure integer work, so any evaluation order is exact as long as ties resolve
+// toward the lowest train index.
+//
+// Tiled kernel (64-byte descriptors): one query per thread held in 16 registers;
+// the train set streams through a double-buffered shared-memory tile filled by the
+// TMA bulk-copy engine (cp.async.bulk + mbarrier); every thread reads the same train
+// descriptor with four broadcast 128-bit shared loads and runs XOR + __popc. The
+// train set is split across blockIdx.y so small query sets still fill 148 SMs; a
+// second tiny kernel merges the per-split partial top-2 (splits are ascending index
+// ranges, so "earlier split wins ties" keeps the lowest index).
+
+#include <algorithm>
+
+#include "clatch_internal.cuh"
+
+namespace clatch {
+
+namespace {
+
+constexpr int kMatchThreads = 128;   // queries per CTA
+constexpr int kTileDesc = 128;       // train descriptors per shared-memory tile (8 KiB)
+constexpr int kDescBytes = 64;
+constexpr int kDescWords = 16;
+
+struct Partial {                     // per (split, query)
+    int best_idx;
+    int best_dist;
+    int second_dist;
+    int pad;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_LOOP:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra WAIT_DONE;\n"
+        "bra WAIT_LOOP;\n"
+        "WAIT_DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk copy global -> shared through the TMA engine (SASS: UBLKCP).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ int hamming16(const unsigned (&q)[kDescWords], const uint4* t) {
+    int d = 0;
+#pragma unroll
+    for (int i = 0; i < kDescWords / 4; ++i) {
+        const uint4 v = t[i];   // same address in every lane: one broadcast wavefront
+        d += __popc(q[4 * i + 0] ^ v.x) + __popc(q[4 * i + 1] ^ v.y) + __popc(q[4 * i + 2] ^ v.z) +
+             __popc(q[4 * i + 3] ^ v.w);
+    }
+    return d;
+}
+
+// grid = (ceil(Q/128), splits). Split s scans train rows [s*per_split, min(N, (s+1)*per_split)).
+__global__ void __launch_bounds__(kMatchThreads) match64_kernel(const uint8_t* __restrict__ queries,
+                                                                unsigned long long Q,
+                                                                const uint8_t* __restrict__ train,
+                                                                unsigned long long N,
+                                                                unsigned long long per_split,
+                                                                Partial* __restrict__ partial) {
+    __shared__ __align__(128) uint4 s_tile[2][kTileDesc * kDescBytes / 16];
+    __shared__ __align__(8) uint64_t s_bar[2];
+
+    const int tid = threadIdx.x;
+    const unsigned long long qi = static_cast<unsigned long long>(blockIdx.x) * kMatchThreads + tid;
+    const unsigned long long n_begin = static_cast<unsigned long long>(blockIdx.y) * per_split;
+    const unsigned long long n_end = min(N, n_begin + per_split);
+    const int tiles = static_cast<int>((n_end - n_begin + kTileDesc - 1) / kTileDesc);
+
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](int tile) {   // thread 0 only
+        const unsigned long long first = n_begin + static_cast<unsigned long long>(tile) * kTileDesc;
+        const unsigned count = static_cast<unsigned>(min(static_cast<unsigned long long>(kTileDesc), n_end - first));
+        const unsigned bytes = count * kDescBytes;
+        uint64_t* bar = &s_bar[tile & 1];
+        mbar_expect_tx(bar, bytes);
+        bulk_load(s_tile[tile & 1], train + first * kDescBytes, bytes, bar);
+    };
+    if (tid == 0 && tiles > 0) issue(0);
+
+    unsigned q[kDescWords];
+    {
+        const unsigned long long src = qi < Q ? qi : Q - 1;   // tail threads shadow the last query
+        const uint4* qp = reinterpret_cast<const uint4*>(queries + src * kDescBytes);
+#pragma unroll
+        for (int i = 0; i < kDescWords / 4; ++i) {
+            const uint4 v = __ldg(qp + i);
+            q[4 * i + 0] = v.x;
+            q[4 * i + 1] = v.y;
+            q[4 * i + 2] = v.z;
+            q[4 * i + 3] = v.w;
+        }
+    }
+
+    const int sentinel = 8 * kDescBytes + 1;
+    int best = sentinel, second = sentinel, best_idx = -1;
+
+    for (int tile = 0; tile < tiles; ++tile) {
+        if (tid == 0 && tile + 1 < tiles) issue(tile + 1);   // buffer (tile+1)&1 was released by the
+                                                             // __syncthreads closing iteration tile-1
+        mbar_wait(&s_bar[tile & 1], (tile >> 1) & 1);
+        const unsigned long long first = n_begin + static_cast<unsigned long long>(tile) * kTileDesc;
+        const int count = static_cast<int>(min(static_cast<unsigned long long>(kTileDesc), n_end - first));
+        const uint4* t = s_tile[tile & 1];
+#pragma unroll 4
+        for (int j = 0; j < count; ++j) {
+            const int d = hamming16(q, t + j * (kDescBytes / 16));
+            // knn2 update, src/match.cpp:41-47
+            if (d < best) {
+                second = best;
+                best = d;
+                best_idx = static_cast<int>(first - n_begin) + j;
+            } else if (d < second) {
+                second = d;
+            }
+        }
+        __syncthreads();   // everyone is done with this buffer before it is refilled
+    }
+
+    if (qi < Q) {
+        Partial r;
+        r.best_idx = best_idx < 0 ? -1 : static_cast<int>(n_begin) + best_idx;
+        r.best_dist = best;
+        r.second_dist = second;
+        r.pad = 0;
+        partial[static_cast<unsigned long long>(blockIdx.y) * Q + qi] = r;
+    }
+}
+
+// Merge per-split partials in ascending split order (== ascending index ranges).
+__global__ void merge_partials_kernel(const Partial* __restrict__ partial, unsigned long long Q,
+                                      int splits, int sentinel, int32_t* __restrict__ best_idx,
+                                      int32_t* __restrict__ best_dist, int32_t* __restrict__ second_dist) {
+    const unsigned long long qi = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (qi >= Q) return;
+    int best = sentinel, second = sentinel, idx = -1;
+    for (int s = 0; s < splits; ++s) {
+        const Partial r = partial[static_cast<unsigned long long>(s) * Q + qi];
+        if (r.best_dist < best) {          // strictly better: earlier splits keep ties
+            second = min(best, r.second_dist);
+            best = r.best_dist;
+            idx = r.best_idx;
+        } else {
+            second = min(second, r.best_dist);
+        }
+    }
+    if (best_idx) best_idx[qi] = idx;
+    if (best_dist) best_dist[qi] = best;
+    if (second_dist) second_dist[qi] = second;
+}
+
+// Any descriptor length (byte tail included, src/match.cpp:28-29): one query per
+// thread, operands straight from global memory through L1. Correctness path for
+// non-64-byte descriptors, not a tuned one.
+__global__ void match_generic_kernel(const uint8_t* __restrict__ queries, unsigned long long Q,
+                                     const uint8_t* __restrict__ train, unsigned long long N, int bytes,
+                                     int32_t* __restrict__ best_idx, int32_t* __restrict__ best_dist,
+                                     int32_t* __restrict__ second_dist) {
+    const unsigned long long qi = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (qi >= Q) return;
+    const uint8_t* q = queries + qi * bytes;
+    const int sentinel = 8 * bytes + 1;
+    int best = sentinel, second = sentinel, idx = -1;
+    for (unsigned long long g = 0; g < N; ++g) {
+        const uint8_t* t = train + g * bytes;
+        int d = 0;
+        for (int i = 0; i < bytes; ++i) d += __popc(static_cast<unsigned>(q[i] ^ __ldg(t + i)));
+        if (d < best) {
+            second = best;
+            best = d;
+            idx = static_cast<int>(g);
+        } else if (d < second) {
+            second = d;
+        }
+    }
+    if (best_idx) best_idx[qi] = idx;
+    if (best_dist) best_dist[qi] = best;
+    if (second_dist) second_dist[qi] = second;
+}
+
+} // namespace
+
+int launch_match_top2(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
+                      int bytes, int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second,
+                      cudaStream_t stream) {
+    if (Q == 0) return CLATCH_OK;
+    const bool tiled = bytes == kDescBytes && reinterpret_cast<uintptr_t>(d_q) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(d_t) % 16 == 0;
+    if (!tiled) {
+        const unsigned blocks = static_cast<unsigned>((Q + 127) / 128);
+        match_generic_kernel<<<blocks, 128, 0, stream>>>(d_q, Q, d_t, N, bytes, d_best_idx, d_best_dist,
+                                                         d_second);
+        ++ctx->launches;
+        CLATCH_CUDA(cudaGetLastError());
+        return CLATCH_OK;
+    }
+    const size_t qblocks = (Q + kMatchThreads - 1) / kMatchThreads;
+    // Enough CTAs for ~8 resident per SM, but never a split shorter than two tiles.
+    const size_t want = static_cast<size_t>(ctx->sm_count) * 8;
+    size_t splits = std::max<size_t>(1, (want + qblocks - 1) / qblocks);
+    const size_t max_splits = std::max<size_t>(1, N / (2 * kTileDesc));
+    splits = std::min(splits, std::min<size_t>(max_splits, 65535));
+    size_t per_split = (N + splits - 1) / splits;
+    per_split = (per_split + kTileDesc - 1) / kTileDesc * kTileDesc;
+    splits = (N + per_split - 1) / per_split;
+
+    if (int rc = ctx->partial.reserve(sizeof(Partial) * splits * Q)) return rc;
+    Partial* partial = ctx->partial.as<Partial>();
+    dim3 grid(static_cast<unsigned>(qblocks), static_cast<unsigned>(splits));
+    match64_kernel<<<grid, kMatchThreads, 0, stream>>>(d_q, Q, d_t, N, per_split, partial);
+    ++ctx->launches;
+    CLATCH_CUDA(cudaGetLastError());
+    merge_partials_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(
+        partial, Q, static_cast<int>(splits), 8 * bytes + 1, d_best_idx, d_best_dist, d_second);
+    ++ctx->launches;
+    CLATCH_CUDA(cudaGetLastError());
+    return CLATCH_OK;
+}
+
+} // namespace clatch

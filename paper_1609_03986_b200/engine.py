@@ -1,0 +1,204 @@
+"""One CLATCH context per GPU: the Python face of include/clatch.h.
+
+`Engine` owns a clatch_ctx (device, stream, scratch) and exposes both forms of the
+ABI: host-buffer calls on numpy arrays (what the reference-facing API uses) and
+device-resident calls on torch CUDA tensors (torch is only the allocator / stream
+provider here — the kernels are libclatch.so's own).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import _lib
+from ._lib import f64p, i16p, i32p, i64p, u8p
+from .pattern import TripletPattern, default_pattern
+
+
+def _ptr(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+class Engine:
+    def __init__(self, device: int | None = None):
+        self.lib = _lib.load()
+        if device is None:
+            device = int(os.environ.get("CLATCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+        handle = C.c_void_p()
+        _lib.check(self.lib.clatch_ctx_create(int(device), C.byref(handle)))
+        self.ctx = handle
+        self.device = int(device)
+        self._pattern_key = None
+        self._pattern = None
+        self._lock = threading.Lock()
+        sm, khz = C.c_int(), C.c_int()
+        name = C.create_string_buffer(256)
+        _lib.check(self.lib.clatch_device_info(self.ctx, C.byref(sm), C.byref(khz), name, 256))
+        self.sm_count, self.sm_clock_khz, self.name = sm.value, khz.value, name.value.decode()
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.clatch_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- pattern ---------------------------------------------------------
+    def set_pattern(self, pattern: TripletPattern | None = None) -> TripletPattern:
+        pattern = pattern or default_pattern()
+        key = pattern.key()
+        if key != self._pattern_key:
+            trip = np.ascontiguousarray(pattern.triplets, np.int16)
+            w = np.ascontiguousarray(pattern.weights, np.float64)
+            _lib.check(self.lib.clatch_set_pattern(self.ctx, _ptr(trip, i16p), pattern.bit_count,
+                                                   pattern.patch_size, _ptr(w, f64p)))
+            self._pattern_key, self._pattern = key, pattern
+        return pattern
+
+    @property
+    def descriptor_bytes(self) -> int:
+        return int(self.lib.clatch_descriptor_bytes(self.ctx))
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.clatch_launch_count(self.ctx))
+
+    def synchronize(self):
+        _lib.check(self.lib.clatch_synchronize(self.ctx))
+
+    # ---- host-side preparation ----------------------------------------------
+    def prepare_keypoints(self, keypoints: np.ndarray, width: int, height: int, workers: int = 0):
+        """-> (xycs float64 (M,4) = x, y, cos, sin; kept int64 (M,) input indices)."""
+        kps = np.ascontiguousarray(keypoints, np.float64)
+        n, cols = kps.shape
+        xycs = np.empty((n, 4), np.float64)
+        kept = np.empty(n, np.int64)
+        m = C.c_size_t()
+        _lib.check(self.lib.clatch_prepare_keypoints(_ptr(kps, f64p), n, cols, width, height, workers,
+                                                     _ptr(xycs, f64p), _ptr(kept, i64p), C.byref(m)))
+        return xycs[:m.value], kept[:m.value]
+
+    # ---- extraction, host buffers --------------------------------------------
+    def extract(self, image: np.ndarray, xycs: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """image: 2-D uint8 or float64 (rows may be strided); xycs from prepare_keypoints."""
+        nbytes = self.descriptor_bytes
+        m = len(xycs)
+        if out is None:
+            out = np.empty((m, nbytes), np.uint8)
+        h, w = image.shape
+        if image.strides[1] != image.itemsize or image.strides[0] % image.itemsize:
+            image = np.ascontiguousarray(image)
+        pitch = image.strides[0] // image.itemsize
+        xycs = np.ascontiguousarray(xycs, np.float64)
+        with self._lock:
+            if image.dtype == np.uint8:
+                rc = self.lib.clatch_extract_u8(self.ctx, _ptr(image, u8p), w, h, pitch,
+                                                _ptr(xycs, f64p), m, _ptr(out, u8p))
+            elif image.dtype == np.float64:
+                rc = self.lib.clatch_extract_f64(self.ctx, _ptr(image, f64p), w, h, pitch,
+                                                 _ptr(xycs, f64p), m, _ptr(out, u8p))
+            else:
+                raise TypeError("image dtype must be uint8 or float64")
+        _lib.check(rc)
+        return out
+
+    # ---- extraction, device tensors --------------------------------------------
+    def extract_device(self, image, xycs, out=None, stream=None):
+        """image: torch CUDA tensor (H, W) uint8 or float64, unit inner stride; xycs: CUDA
+        float64 (M, 4). Queues on `stream` (default: torch's current stream); no sync."""
+        import torch
+        assert image.is_cuda and xycs.is_cuda and image.dim() == 2 and image.stride(1) == 1
+        m = xycs.shape[0]
+        if out is None:
+            out = torch.empty((m, self.descriptor_bytes), dtype=torch.uint8, device=image.device)
+        st = (stream or torch.cuda.current_stream(image.device)).cuda_stream
+        h, w = image.shape
+        fn = {torch.uint8: self.lib.clatch_extract_u8_dev,
+              torch.float64: self.lib.clatch_extract_f64_dev}[image.dtype]
+        _lib.check(fn(self.ctx, image.data_ptr(), w, h, image.stride(0), xycs.data_ptr(), m,
+                      out.data_ptr(), st))
+        return out
+
+    # ---- matching, host buffers ------------------------------------------------
+    def match_top2(self, queries: np.ndarray, train: np.ndarray):
+        """-> (best_idx, best_dist, second_dist) int32 (Q,) each."""
+        q = np.ascontiguousarray(queries, np.uint8)
+        t = q if train is queries else np.ascontiguousarray(train, np.uint8)
+        nq, nt = len(q), len(t)
+        nbytes = q.shape[1] if q.ndim == 2 else t.shape[1]
+        res = np.empty((3, nq), np.int32)
+        with self._lock:
+            rc = self.lib.clatch_match_top2(self.ctx, _ptr(q, u8p), nq, _ptr(t, u8p), nt, nbytes,
+                                            _ptr(res[0], i32p), _ptr(res[1], i32p), _ptr(res[2], i32p))
+        _lib.check(rc)
+        return res[0], res[1], res[2]
+
+    def match_brute_force(self, probes: np.ndarray, gallery: np.ndarray, ratio=None,
+                          cross_check=False, max_distance=None) -> np.ndarray:
+        """-> int32 (M, 4) rows [probe, gallery, distance, second_distance]."""
+        p = np.ascontiguousarray(probes, np.uint8)
+        g = np.ascontiguousarray(gallery, np.uint8)
+        nq, nt = len(p), len(g)
+        out = np.empty((max(nq, 1), 4), np.int32)
+        count = C.c_size_t()
+        with self._lock:
+            rc = self.lib.clatch_match_brute_force(
+                self.ctx, _ptr(p, u8p), nq, _ptr(g, u8p), nt, p.shape[1],
+                int(ratio is not None), float(ratio) if ratio is not None else 0.0, int(cross_check),
+                int(max_distance is not None), int(max_distance) if max_distance is not None else 0,
+                _ptr(out, i32p), C.byref(count))
+        _lib.check(rc)
+        return out[:count.value].copy()
+
+    def filter_matches(self, best_idx, best_dist, second_dist, ratio=None, max_distance=None,
+                       reverse_best=None) -> np.ndarray:
+        bi = np.ascontiguousarray(best_idx, np.int32)
+        bd = np.ascontiguousarray(best_dist, np.int32)
+        sd = np.ascontiguousarray(second_dist, np.int32)
+        rb = None if reverse_best is None else np.ascontiguousarray(reverse_best, np.int32)
+        nq = len(bi)
+        out = np.empty((max(nq, 1), 4), np.int32)
+        count = C.c_size_t()
+        _lib.check(self.lib.clatch_filter_matches(
+            _ptr(bi, i32p), _ptr(bd, i32p), _ptr(sd, i32p), nq, int(ratio is not None),
+            float(ratio) if ratio is not None else 0.0, int(max_distance is not None),
+            int(max_distance) if max_distance is not None else 0,
+            None if rb is None else _ptr(rb, i32p), _ptr(out, i32p), C.byref(count)))
+        return out[:count.value].copy()
+
+    # ---- matching, device tensors ------------------------------------------------
+    def match_top2_device(self, queries, train, out=None, stream=None):
+        """queries (Q, B), train (N, B): contiguous CUDA uint8 tensors. Returns an int32 CUDA
+        tensor (3, Q): rows best_idx, best_dist, second_dist. Queued, not synchronised."""
+        import torch
+        assert queries.is_cuda and train.is_cuda and queries.is_contiguous() and train.is_contiguous()
+        nq, nbytes = queries.shape
+        if out is None:
+            out = torch.empty((3, nq), dtype=torch.int32, device=queries.device)
+        st = (stream or torch.cuda.current_stream(queries.device)).cuda_stream
+        _lib.check(self.lib.clatch_match_top2_dev(
+            self.ctx, queries.data_ptr(), nq, train.data_ptr(), train.shape[0], nbytes,
+            out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(), st))
+        return out
+
+
+_engines: dict[int, Engine] = {}
+_engines_lock = threading.Lock()
+
+
+def get_engine(device: int | None = None) -> Engine:
+    """Process-wide engine for `device` (default CLATCH_DEVICE / LOCAL_RANK / 0)."""
+    if device is None:
+        device = int(os.environ.get("CLATCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    with _engines_lock:
+        eng = _engines.get(device)
+        if eng is None:
+            eng = _engines[device] = Engine(device)
+        return eng

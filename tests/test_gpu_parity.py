@@ -1,0 +1,366 @@
+"""Parity tests proper: the CUDA path, called through the C ABI (ctypes -> libclatch.so),
+against the reference's golden fixtures, the committed reference vectors and the CPU
+oracle on the same seeded inputs. Bit-exact everywhere (bytes, indices, distances).
+
+Test names follow the reference's own suites (proj/tests/test_descriptor.cpp,
+test_match.cpp, acceptance.cpp, python/test_smoke.py).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN, parse_ltch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lk():
+    import paper_1609_03986_b200 as pkg
+    pkg.get_engine()          # fails loudly here if libclatch.so or the GPU is missing
+    return pkg
+
+
+# ---------------------------------------------------------------- extraction ----
+
+def test_golden_bits(lk, golden_image_u8):
+    # acceptance.cpp:96-118
+    want = (GOLDEN / "golden_bits.bin").read_bytes()
+    for img in (golden_image_u8, golden_image_u8.astype(np.float64)):
+        kept, desc = lk.describe(img, np.array([[128.0, 128.0, 0.3, 0.0]]))
+        assert desc.shape == (1, 64) and desc.dtype == np.uint8
+        assert desc[0].tobytes() == want
+
+
+def test_golden_descriptor_file(lk, golden_image_u8):
+    # acceptance.cpp:120-130
+    kps = np.load(GOLDEN / "golden_keypoints_f64.npy")
+    fkps, fdesc = parse_ltch((GOLDEN / "golden_descriptors.bin").read_bytes())
+    for img in (golden_image_u8, golden_image_u8.astype(np.float64)):
+        kept, desc = lk.describe(img, kps)
+        assert np.array_equal(desc, fdesc)
+        assert np.array_equal(kept.astype(np.float32), fkps)
+
+
+@pytest.mark.parametrize("tag,maker,args", [("struct", "structured_image", (83, 160, 160)),
+                                            ("noise", "random_image", (1609, 200, 150))])
+def test_reference_vectors(lk, port, vectors, tag, maker, args):
+    img = getattr(port, maker)(*args)
+    kps = vectors[f"desc_{tag}_kps"]
+    for im in (img, img.astype(np.uint8)):
+        kept, desc = lk.describe(im, kps)
+        assert np.array_equal(kept, kps[vectors[f"desc_{tag}_kept"]])   # order kept, violators dropped
+        assert np.array_equal(desc, vectors[f"desc_{tag}_out"])
+
+
+@pytest.mark.parametrize("name", ["t8k8", "t64k5w", "t16k12z", "t24k1"])
+def test_custom_patterns(lk, port, vectors, name):
+    # generic kernel: python/test_smoke.py:105-123 describes with a T=8 pattern
+    img = port.structured_image(97, 140, 140)
+    text = (GOLDEN / f"pattern_{name}.latchpat").read_text()
+    for im in (img, img.astype(np.uint8)):
+        kept, desc = lk.describe(im, vectors["pat_kps"], pattern=text)
+        assert desc.shape == vectors[f"pat_{name}_out"].shape
+        assert np.array_equal(desc, vectors[f"pat_{name}_out"])
+    # and back to the built-in pattern on the same context
+    kept, desc = lk.describe(img, vectors["pat_kps"][:4])
+    assert np.array_equal(desc, port.describe_all(img, vectors["pat_kps"][:4])[1])
+
+
+def test_default_pattern_text_matches_builtin(lk, port):
+    # python/test_smoke.py:96-103
+    text = lk.default_pattern()
+    assert text.startswith("LATCHPAT v1 T=512 K=8\n")
+    img = port.structured_image(5, 150, 150)
+    kps = port.random_keypoints(6, 150, 150, 40)
+    _, implicit = lk.describe(img, kps)
+    _, explicit = lk.describe(img, kps, pattern=text)
+    assert np.array_equal(implicit, explicit)
+
+
+def test_describe_all_drops_margin_violators(lk, port):
+    # test_descriptor.cpp:178-201
+    img = port.structured_image(101, 140, 140)
+    kps = np.array([[50.0, 50.0, 0.5, 9.0], [10.0, 70.0, 0.0, 8.0], [70.0, 50.0, -0.5, 7.0],
+                    [70.0, 139.0, 0.0, 6.0], [93.0, 93.0, 2.0, 5.0]])
+    kept, desc = lk.describe(img, kps, workers=1)
+    assert len(kept) == 3
+    assert np.array_equal(kept, kps[[0, 2, 4]])            # theta and score pass through
+    for k, d in zip(kept, desc):
+        assert np.array_equal(d, port.describe(img, k))
+    for workers in (2, 8):
+        assert np.array_equal(lk.describe(img, kps, workers=workers)[1], desc)
+    # bare (x, y) rows get theta = 0 (python/test_smoke.py:49-52)
+    upright, d0 = lk.describe(img, kps[:, :2])
+    assert upright.shape == (3, 4) and np.all(upright[:, 2:] == 0.0)
+    assert np.array_equal(d0[0], port.describe(img, [50.0, 50.0, 0.0, 0.0]))
+    # nothing inside the margin
+    kept, desc = lk.describe(img, np.array([[1.0, 1.0, 0.0, 0.0]]))
+    assert kept.shape == (0, 4) and desc.shape == (0, 64)
+    kept, desc = lk.describe(img, np.zeros((0, 4)))
+    assert kept.shape == (0, 4) and desc.shape == (0, 64)
+
+
+def test_margin_edges_and_special_angles(lk, port):
+    # test_descriptor.cpp:57-87: half-integer centre, half turn, exact 46 px margin
+    img = port.random_image(67, 128, 128)
+    kps = np.array([[63.5, 63.5, 0.0, 0.0], [63.5, 63.5, np.pi, 0.0], [46.0, 46.0, 1.0, 0.0],
+                    [81.0, 81.0, -2.0, 0.0], [46.0, 81.0, np.pi / 2, 0.0],
+                    [45.999, 46.0, 0.0, 0.0], [46.0, 81.001, 0.0, 0.0], [np.nan, 60.0, 0.0, 0.0]])
+    kept, desc = lk.describe(img, kps)
+    want_kept, want = port.describe_all(img, kps)
+    assert list(want_kept) == [0, 1, 2, 3, 4]
+    assert np.array_equal(kept, kps[want_kept]) and np.array_equal(desc, want)
+
+
+def test_brightness_invariance(lk, port):
+    # test_descriptor.cpp:145-161, acceptance.cpp:260-280 (exact)
+    img = port.structured_image(89, 128, 128)
+    kps = port.random_keypoints(90, 128, 128, 30)
+    _, base = lk.describe(img, kps)
+    for shift in (30.0, -50.0, 1.0):
+        _, d = lk.describe(img + shift, kps)
+        assert np.array_equal(d, base)
+
+
+def test_non_integer_image_uses_f64_sampling(lk, port):
+    # eval.cpp:76-84 produces non-integer images (warp + noise): no u8 promotion possible
+    rng = np.random.default_rng(0)
+    img = rng.random((150, 170)) * 255.0
+    kps = port.random_keypoints(78, 170, 150, 120)
+    kept, desc = lk.describe(img, kps)
+    assert np.array_equal(desc, port.describe_all(img, kps)[1])
+    # one fractional pixel far from every window must still disable promotion safely
+    img2 = port.structured_image(3, 170, 150)
+    img2[0, 0] = 0.5
+    assert np.array_equal(lk.describe(img2, kps)[1], port.describe_all(img2, kps)[1])
+    # float32 input is force-cast like the reference does
+    img3 = port.random_image(4, 170, 150).astype(np.float32)
+    assert np.array_equal(lk.describe(img3, kps)[1], port.describe_all(img3.astype(np.float64), kps)[1])
+
+
+def test_strided_and_odd_width_images(lk, port):
+    # pitch not a multiple of 16 and non-contiguous rows exercise the staging paths
+    full = port.random_image_u8(12, 333, 201)
+    kps = port.random_keypoints(13, 301, 190, 80)
+    view = full[5:195, 16:317]                 # 190 x 301 window into a wider buffer
+    want = port.describe_all(np.ascontiguousarray(view).astype(np.float64), kps)[1]
+    assert np.array_equal(lk.describe(view, kps)[1], want)
+    assert np.array_equal(lk.describe(np.ascontiguousarray(view), kps)[1], want)
+    assert np.array_equal(lk.describe(view.astype(np.float64), kps)[1], want)
+
+
+@pytest.mark.parametrize("w,h,n,img_seed,kp_seed", [(640, 480, 2000, 1609, 1610),     # BASELINE cfg1
+                                                    (1920, 1080, 10000, 3986, 3987)])  # BASELINE cfg2
+def test_baseline_configs_extract_and_match(lk, port, w, h, n, img_seed, kp_seed):
+    img_u8 = port.random_image_u8(img_seed, w, h)
+    kps = port.random_keypoints(kp_seed, w, h, n)
+    kps[::97, 1] = 20.0                        # ~1 % margin violators
+    kept, desc = lk.describe(img_u8, kps)
+    want_kept, want = port.describe_all(img_u8.astype(np.float64), kps)
+    assert np.array_equal(kept, kps[want_kept])
+    assert np.array_equal(desc, want)
+    # top-2 self-match with planted duplicates (ties -> lowest index)
+    gallery = desc.copy()
+    gallery[len(gallery) // 2] = gallery[11]
+    gallery[-1] = gallery[12]
+    eng = lk.get_engine()
+    bi, bd, sd = eng.match_top2(desc, gallery)
+    # oracle on a sample of rows at cfg2 size, all rows at cfg1 size
+    rows = np.arange(len(desc)) if n <= 2000 else np.unique(
+        np.r_[0:64, 11, 12, len(desc) // 2, len(desc) - 1, np.random.default_rng(1).integers(0, len(desc), 400)])
+    want3 = port.knn2_all(desc[rows], gallery)
+    assert np.array_equal(np.stack([bi, bd, sd], 1)[rows], want3)
+    assert bi[11] == 11 and bd[11] == 0 and sd[11] == 0        # duplicate is the runner-up
+    assert bi[len(gallery) // 2] == 11                         # lowest index wins the tie
+
+
+def test_structured_large_image(lk, port):
+    # flat regions make d1 ~ d2 ~ rounding noise: the hardest case for bit parity
+    img = port.structured_image(2024, 800, 600)
+    kps = port.random_keypoints(2025, 800, 600, 1500)
+    assert np.array_equal(lk.describe(img, kps)[1], port.describe_all(img, kps)[1])
+
+
+def test_extract_device_api(lk, port):
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    eng.set_pattern(None)
+    img = port.random_image_u8(7, 640, 480)
+    kps = port.random_keypoints(8, 640, 480, 500)
+    xycs, kept = eng.prepare_keypoints(kps, 640, 480)
+    want = port.describe_all(img.astype(np.float64), kps)[1]
+    d_xycs = torch.from_numpy(xycs).cuda()
+    for host_img in (img, img.astype(np.float64)):
+        out = eng.extract_device(torch.from_numpy(host_img).cuda(), d_xycs)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), want)
+    # side stream
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        out = eng.extract_device(torch.from_numpy(img).cuda(), d_xycs)
+    st.synchronize()
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+# ------------------------------------------------------------------ matching ----
+
+def _ones(k, nbytes=64):
+    bits = np.zeros(nbytes * 8, np.uint8)
+    bits[:k] = 1
+    return np.packbits(bits, bitorder="little")
+
+
+def test_hamming_counts_differing_bits(lk, port):
+    # test_match.cpp:41-66
+    assert lk.hamming(np.array([0x00], np.uint8), np.array([0x00], np.uint8)) == 0
+    assert lk.hamming(np.array([0xff], np.uint8), np.array([0x00], np.uint8)) == 8
+    assert lk.hamming(np.array([0xaa], np.uint8), np.array([0x55], np.uint8)) == 8
+    assert lk.hamming(np.array([0x0f, 0xf0], np.uint8), np.array([0x00, 0xf0], np.uint8)) == 4
+    assert lk.hamming(_ones(512), _ones(0)) == 512
+    assert lk.hamming(_ones(200), _ones(137)) == 63
+    with pytest.raises(RuntimeError):
+        lk.hamming(np.zeros(1, np.uint8), np.zeros(2, np.uint8))
+    d = port.random_descriptors(109, 40, 64)
+    for a, b in zip(d[::2], d[1::2]):
+        assert lk.hamming(a, b) == port.hamming(a, b) == lk.hamming(b, a)
+        assert lk.hamming(a, a) == 0
+    t = port.random_descriptors(113, 20, 13)       # byte tail
+    for a, b in zip(t[::2], t[1::2]):
+        assert lk.hamming(a, b) == int(np.unpackbits(a ^ b).sum())
+
+
+def test_knn2_ties_and_sentinel(lk):
+    # test_match.cpp:68-81
+    eng = lk.get_engine()
+    gallery = np.stack([_ones(10), _ones(3), _ones(7), _ones(3)])
+    bi, bd, sd = eng.match_top2(_ones(0)[None], gallery)
+    assert (bi[0], bd[0], sd[0]) == (1, 3, 3)
+    bi, bd, sd = eng.match_top2(_ones(0)[None], _ones(9)[None])
+    assert (bi[0], bd[0], sd[0]) == (0, 9, 513)
+
+
+def test_filters_known_answers(lk):
+    # test_match.cpp:105-158
+    p0 = _ones(0)[None]
+    assert len(lk.match(p0, np.stack([_ones(4), _ones(4)]), ratio=1.0)) == 0      # strict <
+    spread = np.stack([_ones(4), _ones(9)])
+    kept = lk.match(p0, spread, ratio=0.5)
+    assert kept.tolist() == [[0, 0, 4, 9]]
+    assert len(lk.match(p0, spread, ratio=0.4)) == 0
+    assert len(lk.match(p0, _ones(400)[None], ratio=0.8)) == 1                    # sentinel 513
+    assert len(lk.match(p0, _ones(7)[None], max_distance=7)) == 1                 # inclusive
+    assert len(lk.match(p0, _ones(7)[None], max_distance=6)) == 0
+    probes = np.stack([_ones(1), _ones(2)])
+    gallery = np.stack([_ones(0), _ones(30)])
+    got = lk.match(probes, gallery, cross_check=True)
+    assert got.tolist() == [[0, 0, 1, 30]]
+    assert len(lk.match(probes, gallery)) == 2
+
+
+@pytest.mark.parametrize("seed,q,n,ratio,maxd", [(131, 60, 45, 0.9, 250), (515, 500, 500, 0.8, 240)])
+def test_matcher_every_filter_combination(lk, port, vectors, seed, q, n, ratio, maxd):
+    # test_match.cpp:160-188 and acceptance.cpp:164-216
+    d = port.random_descriptors(seed, q + n, 64)
+    probes, gallery = d[:q].copy(), d[q:].copy()
+    if seed == 131:
+        gallery[10] = gallery[3]; gallery[44] = gallery[7]; probes[5] = gallery[3]
+    else:
+        gallery[7] = gallery[3]; gallery[450] = gallery[11]; probes[5] = gallery[3]; probes[301] = probes[5]
+    bi, bd, sd = lk.get_engine().match_top2(probes, gallery)
+    assert np.array_equal(np.stack([bi, bd, sd], 1), vectors[f"m{seed}_knn2"])
+    for combo in range(8):
+        kw = dict(ratio=ratio if combo & 1 else None, cross_check=bool(combo & 2),
+                  max_distance=maxd if combo & 4 else None)
+        want = vectors[f"m{seed}_combo{combo}"]
+        for workers in (1, 2, 8):
+            got = lk.match(probes, gallery, workers=workers, **kw)
+            assert got.dtype == np.int32 and np.array_equal(got, want)
+        assert np.all(np.diff(got[:, 0]) > 0)
+
+
+def test_tail_length_descriptors(lk, port, vectors):
+    d = port.random_descriptors(113, 53, 13)
+    probes, gallery = d[:20].copy(), d[20:].copy()
+    bi, bd, sd = lk.get_engine().match_top2(probes, gallery)
+    assert np.array_equal(np.stack([bi, bd, sd], 1), vectors["m113_knn2"])
+    for nbytes in (1, 8, 32, 100):
+        dd = port.random_descriptors(nbytes, 70, nbytes)
+        assert np.array_equal(lk.match(dd[:30], dd[30:], ratio=0.95),
+                              port.match(dd[:30], dd[30:], ratio=0.95))
+
+
+def test_match_edge_cases(lk):
+    # test_match.cpp:190-192, python/test_smoke.py:126-136
+    with pytest.raises(RuntimeError):
+        lk.match(np.zeros((2, 64), np.uint8), np.zeros((0, 64), np.uint8))
+    with pytest.raises(RuntimeError):
+        lk.match(np.zeros((0, 64), np.uint8), np.zeros((0, 64), np.uint8))   # gallery checked first
+    empty = lk.match(np.zeros((0, 64), np.uint8), np.zeros((3, 64), np.uint8))
+    assert empty.shape == (0, 4) and empty.dtype == np.int32
+    with pytest.raises(ValueError):
+        lk.match(np.zeros(64, np.uint8), np.zeros((3, 64), np.uint8))
+    with pytest.raises(RuntimeError):
+        lk.match(np.zeros((2, 64), np.uint8), np.zeros((3, 32), np.uint8))
+
+
+@pytest.mark.parametrize("q,n", [(1, 1), (1, 127), (3, 128), (130, 129), (257, 1000), (5, 40000),
+                                 (1000, 1), (4096, 4097)])
+def test_ragged_shapes_against_oracle(lk, port, q, n):
+    # tile tails, split tails, more CTAs than work, a single train row
+    d = port.random_descriptors(1000 + q + n, q + n, 64)
+    probes, gallery = d[:q].copy(), d[q:].copy()
+    if n > 3:
+        gallery[n - 1] = gallery[0]            # tie between the first and the last split
+        probes[0] = gallery[0]
+    bi, bd, sd = lk.get_engine().match_top2(probes, gallery)
+    assert np.array_equal(np.stack([bi, bd, sd], 1), port.knn2_all(probes, gallery))
+
+
+def test_self_match_properties_large(lk, port):
+    # size-independent properties at 100k x 100k (1e10 compares; no CPU oracle at this size)
+    n = 100_000
+    d = port.random_descriptors(41, n, 64)
+    d[70_000] = d[123]                          # planted duplicate pair
+    d[99_999] = d[0]
+    bi, bd, sd = lk.get_engine().match_top2(d, d)
+    assert np.all(bd == 0)                      # every row finds itself (or an identical row)
+    assert np.all(bi <= np.arange(n))           # ... at the lowest such index
+    assert bi[70_000] == 123 and sd[70_000] == 0 and sd[123] == 0
+    assert bi[99_999] == 0 and sd[0] == 0
+    mask = np.ones(n, bool); mask[[0, 123, 70_000, 99_999]] = False
+    assert np.all(bi[mask] == np.arange(n)[mask])
+    assert np.all((sd[mask] > 150) & (sd[mask] < 256))   # Binomial(512, 1/2) minimum over 1e5 draws
+    rows = np.random.default_rng(3).integers(0, n, 48)
+    assert np.array_equal(np.stack([bi, bd, sd], 1)[rows], port.knn2_all(d[rows], d))
+
+
+def test_match_device_api(lk, port):
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    d = port.random_descriptors(9, 3000, 64)
+    probes, gallery = d[:1000].copy(), d[1000:].copy()
+    out = eng.match_top2_device(torch.from_numpy(probes).cuda(), torch.from_numpy(gallery).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().T, port.knn2_all(probes, gallery))
+
+
+def test_python_smoke_shapes(lk, golden_image_u8):
+    # python/test_smoke.py:30-53 without detect(): the golden keypoints stand in
+    golden = golden_image_u8.astype(np.float64)
+    keypoints = np.load(GOLDEN / "golden_keypoints_f64.npy")
+    kept, desc = lk.describe(golden, keypoints)
+    assert desc.dtype == np.uint8 and desc.shape == (len(kept), lk.descriptor_bytes)
+    assert 0 < len(kept) <= len(keypoints)
+    matches = lk.match(desc, desc)
+    assert matches.shape == (len(desc), 4)
+    assert np.array_equal(matches[:, 0], np.arange(len(desc)))
+    assert np.all(matches[:, 2] == 0)
+    assert np.array_equal(desc[matches[:, 1]], desc[matches[:, 0]])
+    assert np.array_equal(lk.match(desc, desc, workers=2), matches)
+    a, b = desc[0], desc[1]
+    assert lk.hamming(a, b) == int(np.unpackbits(a ^ b).sum())
+    with pytest.raises(RuntimeError):
+        lk.describe(np.zeros((128, 128)), np.array([[64.0, 64.0]]), pattern="not a pattern")
+    with pytest.raises(ValueError):
+        lk.describe(np.zeros(16), np.array([[64.0, 64.0]]))

@@ -1,0 +1,164 @@
+"""CPU-only checks of the host side: the C-ABI library loads and exports every symbol
+include/clatch.h declares, the host-only entry points (keypoint preparation, match
+filter pass) agree with the oracle, the pattern reader mirrors the reference's, and
+the product refuses to run without a GPU instead of falling back to anything."""
+import ctypes as C
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN, ROOT
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1609_03986_b200 import _lib
+    return _lib.load()
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_1609_03986_b200 import _lib
+    header = (ROOT / "include" / "clatch.h").read_text()
+    declared = set(re.findall(r"CLATCH_API[^;(]*?\b(clatch_\w+)\s*\(", header))
+    assert len(declared) >= 17
+    assert declared == set(_lib.EXPORTS)
+    for name in declared:
+        assert getattr(lib, name) is not None
+
+
+def test_header_compiles_as_plain_c(tmp_path):
+    import subprocess
+    src = tmp_path / "t.c"
+    src.write_text('#include "clatch.h"\nint main(void){return CLATCH_OK;}\n')
+    subprocess.run(["/usr/bin/gcc", "-std=c99", "-pedantic", "-Werror", "-I", str(ROOT / "include"),
+                    "-c", str(src), "-o", str(tmp_path / "t.o")], check=True)
+
+
+def test_prepare_keypoints_matches_oracle_margin_and_libm(lib, port):
+    from paper_1609_03986_b200.engine import Engine
+    prep = Engine.prepare_keypoints.__get__(type("E", (), {"lib": lib})())
+    w, h = 300, 200
+    kps = port.random_keypoints(5, w, h, 20000)
+    kps[::7, 0] -= 60.0
+    kps[::11, 1] += 120.0
+    kps[3] = [46.0, 46.0, 0.1, 0]
+    kps[4] = [w - 47.0, h - 47.0, 0.2, 0]
+    kps[5] = [w - 46.999, 60.0, 0.3, 0]
+    kps[6] = [np.nan, 60.0, 0.3, 0]
+    for workers in (1, 3, 0):
+        xycs, kept = prep(kps, w, h, workers)
+        want = np.array([i for i in range(len(kps)) if port.in_margin(w, h, kps[i, 0], kps[i, 1])])
+        assert np.array_equal(kept, want)
+        assert np.array_equal(xycs[:, :2], kps[kept, :2])
+        # same libm as the oracle: math.cos/sin are glibc's
+        import math
+        assert np.array_equal(xycs[:, 2], [math.cos(t) for t in kps[kept, 2]])
+        assert np.array_equal(xycs[:, 3], [math.sin(t) for t in kps[kept, 2]])
+    xy_only, kept2 = prep(kps[:, :2].copy(), w, h, 1)
+    assert np.array_equal(kept2, kept) and np.all(xy_only[:, 2] == 1.0) and np.all(xy_only[:, 3] == 0.0)
+    bad = kps[:10].copy()
+    bad[3, 2] = np.inf
+    with pytest.raises(RuntimeError):
+        prep(bad, w, h, 1)
+
+
+def test_filter_pass_matches_oracle(lib, port):
+    from paper_1609_03986_b200.engine import Engine
+    filt = Engine.filter_matches.__get__(type("E", (), {"lib": lib})())
+    d = port.random_descriptors(77, 700, 64)
+    probes, gallery = d[:300].copy(), d[300:].copy()
+    gallery[9] = gallery[2]
+    probes[4] = gallery[2]
+    fwd = port.knn2_all(probes, gallery)
+    rev = port.knn2_all(gallery, probes)[:, 0]
+    for combo in range(8):
+        kw = dict(ratio=0.85 if combo & 1 else None, max_distance=235 if combo & 4 else None)
+        got = filt(fwd[:, 0], fwd[:, 1], fwd[:, 2], reverse_best=rev if combo & 2 else None, **kw)
+        want = port.match(probes, gallery, cross_check=bool(combo & 2), **kw)
+        assert np.array_equal(got, want)
+
+
+def test_pattern_reader(ref=None):
+    from paper_1609_03986_b200 import LatchError
+    from paper_1609_03986_b200.pattern import default_pattern, format_pattern, parse_pattern
+    pat = default_pattern()
+    assert (pat.bit_count, pat.patch_size) == (512, 8) and pat.triplets.shape == (512, 6)
+    w = pat.weights.reshape(8, 8)
+    assert np.all(w[:7, :7] == 1.0) and np.all(w[7] == 0.0) and np.all(w[:, 7] == 0.0)
+    assert format_pattern(pat) == (ROOT / "paper_1609_03986_b200/data/default_pattern.latchpat").read_text()
+    for name in ("t8k8", "t64k5w", "t16k12z", "t24k1"):
+        text = (GOLDEN / f"pattern_{name}.latchpat").read_text()
+        p = parse_pattern(text)
+        T, K, trip, weights = oracle.parse_pattern_text(text)
+        assert (p.bit_count, p.patch_size) == (T, K)
+        assert np.array_equal(p.triplets, trip) and np.array_equal(p.weights, weights)
+        assert parse_pattern(format_pattern(p)).key() == p.key()
+    # error categories of src/pattern.cpp:68-131
+    for text, code in [("", "BadHeader"), ("not a pattern", "BadHeader"),
+                       ("LATCHPAT v1 T=12 K=8\n", "BadHeader"), ("LATCHPAT v1 T=8 K=0\n", "BadHeader"),
+                       ("LATCHPAT v1 T=8 K=8\n1 2 3 4 5 6\n", "BadTripletCount"),
+                       ("LATCHPAT v1 T=8 K=8\n" + "1 2 3 4 5 60\n" * 8, "CoordinateOutOfRange"),
+                       ("LATCHPAT v1 T=8 K=8\n" + "1 2 3 4 3 4\n" * 8, "DegenerateTriplet"),
+                       ("LATCHPAT v1 T=8 K=2\n" + "1 2 3 4 5 6\n" * 8 + "WEIGHTS\n0 0\n0 0\n", "BadHeader"),
+                       ("LATCHPAT v1 T=8 K=2\n" + "1 2 3 4 5 6\n" * 8 + "WEIGHTS\n1 -1\n0 0\n", "BadHeader"),
+                       ("LATCHPAT v1 T=8 K=8\n" + "1 2 3 4 5 6\n" * 9, "BadTripletCount")]:
+        with pytest.raises(LatchError) as e:
+            parse_pattern(text)
+        assert e.value.code == code, text
+
+
+def test_pattern_reader_agrees_with_reference(ref):
+    from paper_1609_03986_b200.pattern import parse_pattern
+    for name in ("t8k8", "t64k5w", "t16k12z", "t24k1"):
+        text = (GOLDEN / f"pattern_{name}.latchpat").read_text()
+        p = parse_pattern(text)
+        T, K, trip, weights = ref.parse_pattern(text)
+        assert (p.bit_count, p.patch_size) == (T, K)
+        assert np.array_equal(p.triplets, trip) and np.array_equal(p.weights, weights)
+    for bad in ("", "nope", "LATCHPAT v1 T=8 K=8\n1 2 3 4 5 6\n",
+                "LATCHPAT v1 T=8 K=8\n" + "1 2 3 4 3 4\n" * 8):
+        with pytest.raises(RuntimeError):
+            ref.parse_pattern(bad)
+        with pytest.raises(RuntimeError):
+            parse_pattern(bad)
+
+
+def test_argument_errors_need_no_device():
+    import paper_1609_03986_b200 as lk
+    with pytest.raises(ValueError):
+        lk.describe(np.zeros(16), np.zeros((1, 2)))
+    with pytest.raises(ValueError):
+        lk.describe(np.zeros((100, 100)), np.zeros((1, 5)))
+    with pytest.raises(RuntimeError):
+        lk.describe(np.zeros((128, 128)), np.array([[64.0, 64.0]]), pattern="not a pattern")
+    with pytest.raises(RuntimeError):
+        lk.match(np.zeros((2, 64), np.uint8), np.zeros((0, 64), np.uint8))
+    assert lk.match(np.zeros((0, 64), np.uint8), np.zeros((3, 64), np.uint8)).shape == (0, 4)
+    with pytest.raises(RuntimeError):
+        lk.hamming(np.zeros(64, np.uint8), np.zeros(32, np.uint8))
+    assert (lk.descriptor_bits, lk.descriptor_bytes, lk.window_margin, lk.orientation_radius) == (512, 64, 46, 15)
+
+
+def test_no_gpu_means_loud_failure_not_fallback():
+    """On a box without CUDA the product must raise, never compute on the CPU."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_1609_03986_b200 as lk
+    from paper_1609_03986_b200 import ClatchDeviceError
+    with pytest.raises(ClatchDeviceError):
+        lk.describe(np.zeros((128, 128)), np.array([[64.0, 64.0]]))
+    with pytest.raises(ClatchDeviceError):
+        lk.match(np.zeros((2, 64), np.uint8), np.zeros((2, 64), np.uint8))
+    with pytest.raises(ClatchDeviceError):
+        lk.hamming(np.zeros(64, np.uint8), np.zeros(64, np.uint8))
+
+
+def test_product_never_imports_the_oracle():
+    pkg = ROOT / "paper_1609_03986_b200"
+    for path in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
+        text = path.read_text()
+        assert "import oracle" not in text and "from oracle" not in text, path
+        assert "latch_oracle" not in text and "liblatch_ref" not in text, path

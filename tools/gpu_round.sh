@@ -1,0 +1,28 @@
+#!/usr/bin/env bash
+# One GPU-box visit: smoke, GPU parity tests, pipe-rate microbench, bench (both arms),
+# ncu launch list and one full capture per hot kernel. Everything lands in gpurun_out/.
+# Usage (from the build container): gpurun --timeout 2400 -- 'bash tools/gpu_round.sh [tag]'
+set -u
+TAG="${1:-r1}"
+OUT=gpurun_out/$TAG
+mkdir -p "$OUT"
+nvidia-smi > "$OUT/nvidia-smi.txt" 2>&1
+nproc > "$OUT/nproc.txt"
+echo "== smoke"; timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?" | tee -a "$OUT/smoke.log"
+echo "== pytest -m gpu"; timeout 1500 python -m pytest tests -m gpu -x -q > "$OUT/pytest_gpu.log" 2>&1; echo "pytest rc=$?" | tee -a "$OUT/pytest_gpu.log"
+tail -5 "$OUT/pytest_gpu.log"
+echo "== pipe peaks"; timeout 120 ./tools/pipe_peaks > "$OUT/pipe_peaks.json" 2> "$OUT/pipe_peaks.err"; cat "$OUT/pipe_peaks.json"
+echo "== bench ours"; timeout 900 python bench.py --steps 20 --warmup 5 > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?"; cat "$OUT/bench.json"; tail -3 "$OUT/bench.err"
+echo "== bench reference"; timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"; cat "$OUT/bench_reference.json"
+if [ "${SKIP_NCU:-0}" != "1" ]; then
+echo "== ncu launch list"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$OUT/launches.csv" \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$OUT/ncu_launches.log" 2>&1
+echo "== ncu full: extraction"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:extract_ -s 3 -c 1 -f -o "$OUT/prof_extract" \
+    python bench.py --steps 2 --warmup 3 --phase extract --no-cpu-baseline > "$OUT/ncu_extract.log" 2>&1
+echo "== ncu full: matching"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:match64 -s 3 -c 1 -f -o "$OUT/prof_match" \
+    python bench.py --steps 2 --warmup 3 --phase match --no-cpu-baseline > "$OUT/ncu_match.log" 2>&1
+fi
+ls -la "$OUT"
