@@ -172,7 +172,7 @@ def test_baseline_configs_extract_and_match(lk, port, w, h, n, img_seed, kp_seed
     want3 = port.knn2_all(desc[rows], gallery)
     assert np.array_equal(np.stack([bi, bd, sd], 1)[rows], want3)
     assert bi[11] == 11 and bd[11] == 0 and sd[11] == 0        # duplicate is the runner-up
-    assert bi[len(gallery) // 2] == 11                         # lowest index wins the tie
+    assert bi[12] == 12 and sd[12] == 0                        # lowest index wins the tie
 
 
 def test_structured_large_image(lk, port):
