@@ -110,6 +110,17 @@ CLATCH_API int clatch_extract_u8(clatch_ctx* ctx, const uint8_t* img, int width,
 CLATCH_API int clatch_extract_f64(clatch_ctx* ctx, const double* img, int width, int height, size_t pitch,
                        const double* xycs, size_t M, uint8_t* out);
 
+/* describe_all in one call (src/descriptor.cpp:90-105): margin filter + host trig +
+ * upload + extraction + download. The image upload is queued first so the DMA overlaps
+ * the host-side trig pass. kps: n rows of `cols` (2..4) doubles; kept: room for n input
+ * indices; out: room for n descriptors; *m receives the number kept (input order). */
+CLATCH_API int clatch_describe_all_u8(clatch_ctx* ctx, const uint8_t* img, int width, int height, size_t pitch,
+                           const double* kps, size_t n, int cols, int workers, int64_t* kept,
+                           uint8_t* out, size_t* m);
+CLATCH_API int clatch_describe_all_f64(clatch_ctx* ctx, const double* img, int width, int height, size_t pitch,
+                            const double* kps, size_t n, int cols, int workers, int64_t* kept,
+                            uint8_t* out, size_t* m);
+
 /* Device-resident forms: all pointers are device memory on the context's device,
  * work is queued on `stream` (a cudaStream_t; NULL = the legacy default stream)
  * and NOT synchronised. */

@@ -82,9 +82,7 @@ def describe(image, keypoints, pattern=None, workers=0):
     kps = _keypoint_array(keypoints)
     eng = get_engine()
     eng.set_pattern(pat)
-    h, w = img.shape
-    xycs, kept = eng.prepare_keypoints(kps, w, h, workers)
-    desc = eng.extract(img, xycs)
+    kept, desc = eng.describe_all(img, kps, workers)
     full = np.zeros((len(kept), 4), np.float64)
     full[:, :kps.shape[1]] = kps[kept]
     return full, desc

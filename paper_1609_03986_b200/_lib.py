@@ -60,6 +60,10 @@ _SIGNATURES = {
                                     u8p]),
     "clatch_extract_f64": (C.c_int, [C.c_void_p, f64p, C.c_int, C.c_int, C.c_size_t, f64p, C.c_size_t,
                                      u8p]),
+    "clatch_describe_all_u8": (C.c_int, [C.c_void_p, u8p, C.c_int, C.c_int, C.c_size_t, f64p, C.c_size_t,
+                                         C.c_int, C.c_int, i64p, u8p, szp]),
+    "clatch_describe_all_f64": (C.c_int, [C.c_void_p, f64p, C.c_int, C.c_int, C.c_size_t, f64p, C.c_size_t,
+                                          C.c_int, C.c_int, i64p, u8p, szp]),
     "clatch_extract_u8_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_size_t,
                                         C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
     "clatch_extract_f64_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_size_t,

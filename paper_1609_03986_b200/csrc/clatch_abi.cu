@@ -5,10 +5,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
 #include "clatch_internal.cuh"
+#include "slot_assign.hpp"
 
 namespace clatch {
 
@@ -104,6 +106,7 @@ int clatch_ctx_create(int device, clatch_ctx** out) {
         delete ctx;
         return cuda_fail(se, "cudaStreamCreateWithFlags");
     }
+    if (const char* v = std::getenv("CLATCH_MATCH_VARIANT")) ctx->match_variant = std::atoi(v);
     *out = ctx;
     return CLATCH_OK;
 }
@@ -198,16 +201,13 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
     CLATCH_CUDA(cudaMemcpy(pat.triplets.ptr, triplets, sizeof(int16_t) * 6 * T, cudaMemcpyHostToDevice));
     if (int rc = upload_weights(w.data(), K * K)) return rc;
     if (pat.fast) {
-        std::vector<ushort4> slots(T);
-        for (int t = 0; t < T; ++t) {
-            const int16_t* v = triplets + 6 * t;
-            slots[t].x = static_cast<unsigned short>(v[1] * kWinStride + v[0]);
-            slots[t].y = static_cast<unsigned short>(v[3] * kWinStride + v[2]);
-            slots[t].z = static_cast<unsigned short>(v[5] * kWinStride + v[4]);
-            slots[t].w = static_cast<unsigned short>(t);
-        }
-        if (int rc = pat.slots.reserve(sizeof(ushort4) * T)) return rc;
-        CLATCH_CUDA(cudaMemcpy(pat.slots.ptr, slots.data(), sizeof(ushort4) * T, cudaMemcpyHostToDevice));
+        // Lane placement that keeps the 64-bit window loads (nearly) bank-conflict free.
+        const SlotPlan plan = plan_slots(triplets, T, kWinStride, 1000000);
+        pat.slot_degree = plan.avg_degree;
+        pat.slot_degree_identity = plan.avg_degree_identity;
+        static_assert(sizeof(SlotEntry) == sizeof(ushort4), "slot layout");
+        if (int rc = pat.slots.reserve(sizeof(SlotEntry) * T)) return rc;
+        CLATCH_CUDA(cudaMemcpy(pat.slots.ptr, plan.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
     }
     return CLATCH_OK;
 }
@@ -333,6 +333,71 @@ int clatch_extract_f64(clatch_ctx* ctx, const double* img, int width, int height
     CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * M, cudaMemcpyDeviceToHost, st));
     CLATCH_CUDA(cudaStreamSynchronize(st));
     return CLATCH_OK;
+}
+
+} // extern "C"
+
+template <typename Pixel>
+static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int height, size_t pitch,
+                             const double* kps, size_t n, int cols, int workers, int64_t* kept,
+                             uint8_t* out, size_t* m) {
+    if (!m) return invalid("describe_all: m is null");
+    *m = 0;
+    if (int rc = check_extract(ctx, img, width, height, pitch, kps, 0, out)) return rc;
+    if (cols < 2 || cols > 4) return invalid("keypoints must be (N, 2..4): x, y[, theta[, score]]");
+    if (n == 0) return CLATCH_OK;
+    if (!kps || !kept || !out) return invalid("describe_all: null keypoint/output buffer");
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    constexpr bool kU8 = sizeof(Pixel) == 1;
+    const size_t dpitch = kU8 ? (static_cast<size_t>(width) + 15) / 16 * 16 : static_cast<size_t>(width);
+    const size_t bytes = static_cast<size_t>(ctx->pattern.T) / 8;
+    if (int rc = ctx->img.reserve(sizeof(Pixel) * dpitch * height)) return rc;
+    if (int rc = ctx->kps.reserve(sizeof(double) * 4 * n)) return rc;
+    if (int rc = ctx->desc.reserve(bytes * n)) return rc;
+    cudaStream_t st = ctx->stream;
+    // 1. image DMA first ...
+    CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, sizeof(Pixel) * dpitch, img, sizeof(Pixel) * pitch,
+                                  sizeof(Pixel) * width, height, cudaMemcpyHostToDevice, st));
+    // 2. ... while the host filters by margin and evaluates cos/sin with its own libm
+    ctx->host_xycs.resize(4 * n);
+    size_t count = 0;
+    if (int rc = clatch_prepare_keypoints(kps, n, cols, width, height, workers, ctx->host_xycs.data(), kept,
+                                          &count)) {
+        cudaStreamSynchronize(st);
+        return rc;
+    }
+    *m = count;
+    if (count == 0) {
+        CLATCH_CUDA(cudaStreamSynchronize(st));
+        return CLATCH_OK;
+    }
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->kps.ptr, ctx->host_xycs.data(), sizeof(double) * 4 * count,
+                                cudaMemcpyHostToDevice, st));
+    int rc;
+    if (kU8)
+        rc = launch_extract_u8(ctx, ctx->img.as<uint8_t>(), width, height, dpitch, ctx->kps.as<double>(), count,
+                               ctx->desc.as<uint8_t>(), st);
+    else
+        rc = launch_extract_f64(ctx, ctx->img.as<double>(), width, height, dpitch, ctx->kps.as<double>(), count,
+                                ctx->desc.as<uint8_t>(), st);
+    if (rc) return rc;
+    CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    return CLATCH_OK;
+}
+
+extern "C" {
+
+int clatch_describe_all_u8(clatch_ctx* ctx, const uint8_t* img, int width, int height, size_t pitch,
+                           const double* kps, size_t n, int cols, int workers, int64_t* kept,
+                           uint8_t* out, size_t* m) {
+    return describe_all_impl<uint8_t>(ctx, img, width, height, pitch, kps, n, cols, workers, kept, out, m);
+}
+
+int clatch_describe_all_f64(clatch_ctx* ctx, const double* img, int width, int height, size_t pitch,
+                            const double* kps, size_t n, int cols, int workers, int64_t* kept,
+                            uint8_t* out, size_t* m) {
+    return describe_all_impl<double>(ctx, img, width, height, pitch, kps, n, cols, workers, kept, out, m);
 }
 
 // ---- matching -----------------------------------------------------------------

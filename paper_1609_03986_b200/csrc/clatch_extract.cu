@@ -45,7 +45,27 @@ struct ExtractParams {
     int run_if_flag;           // run only when flags[0] == run_if_flag (if flags != null)
 };
 
-__device__ __forceinline__ double u8_to_f64(unsigned v) { return static_cast<double>(v); }
+// Exact u8 -> f64 without the 16-lane/clk conversion pipe (I2F.F64 runs at 16/clk/SM on
+// B200, profiles/r1a_pipe_peaks.json): splice the byte into the mantissa of 2^52 and
+// subtract 2^52 — one DADD on the 64-lane fp64 pipe, result exactly v.
+__device__ __forceinline__ double u8_to_f64(unsigned v) {
+    return __dsub_rn(__hiloint2double(0x43300000, static_cast<int>(v)), 4503599627370496.0);
+}
+
+// floor() of a double in (0, 2^31) as both int and double, again without F2I/I2F:
+// t = s + (2^52 + 2^51) rounds s to the nearest integer into the low mantissa bits;
+// step down by one when that rounded up. Both results are exact, so fx = s - floor(s)
+// is bit-identical to the reference's `x - x0` (src/image.cpp:113,121).
+__device__ __forceinline__ void floor_exact(double s, int& i, double& f) {
+    const double kMagic = 6755399441055744.0;
+    const double t = __dadd_rn(s, kMagic);
+    i = __double2loint(t);
+    f = __dsub_rn(t, kMagic);
+    if (f > s) {
+        i -= 1;
+        f = __dsub_rn(f, 1.0);
+    }
+}
 
 // One bilinear sample with the reference's exact operation order (src/image.cpp:121-125).
 __device__ __forceinline__ double blend(double fx, double fy, double p00, double p10, double p01,
@@ -97,10 +117,12 @@ __device__ __forceinline__ void build_window(double* win, const uint8_t* tile, i
         const double dv = static_cast<double>(v) - 31.5;
         const double sx = __dsub_rn(xa, __dmul_rn(s, dv));
         const double sy = __dadd_rn(ya, __dmul_rn(c, dv));
-        const int x0 = __double2int_rd(sx);   // inside the margin: 1 <= x0 <= width-3, no clamps fire
-        const int y0 = __double2int_rd(sy);
-        const double fx = __dsub_rn(sx, static_cast<double>(x0));
-        const double fy = __dsub_rn(sy, static_cast<double>(y0));
+        int x0, y0;                           // inside the margin: 1 <= x0 <= width-3, no clamps fire
+        double x0f, y0f;
+        floor_exact(sx, x0, x0f);
+        floor_exact(sy, y0, y0f);
+        const double fx = __dsub_rn(sx, x0f);
+        const double fy = __dsub_rn(sy, y0f);
         double p00, p10, p01, p11;
         if (kU8) {
             const uint8_t* p = tile + (y0 - ty0) * kTileW + (x0 - ax0);
@@ -122,7 +144,9 @@ __device__ __forceinline__ void build_window(double* win, const uint8_t* tile, i
 // Phase B (specialised): one triplet = two independent 49-term chains over the
 // 7x7 live pixels of the 8x8 patch, row-major (src/descriptor.cpp:61-75 with the
 // zero-weight terms skipped — exact because w*e*e is +0.0 there and d + 0.0 == d).
-__device__ __forceinline__ bool triplet_bit_7x7(const double* win, int oa, int ob, int oc) {
+// `ob`/`oc` are the companions in LOAD order; the slot planner (slot_assign.hpp) may have
+// swapped them to dodge a bank conflict, in which case the caller tests d2 > d1.
+__device__ __forceinline__ bool triplet_bit_7x7(const double* win, int oa, int ob, int oc, bool swapped) {
     const double* pa = win + oa;
     const double* pb = win + ob;
     const double* pc = win + oc;
@@ -139,7 +163,7 @@ __device__ __forceinline__ bool triplet_bit_7x7(const double* win, int oa, int o
             d2 = __dadd_rn(d2, __dmul_rn(e2, e2));
         }
     }
-    return d1 > d2;
+    return swapped ? d2 > d1 : d1 > d2;
 }
 
 template <bool kU8>
@@ -174,8 +198,8 @@ __global__ void __launch_bounds__(kThreads, 4) extract_fast_kernel(ExtractParams
         build_window<kU8>(s_win, s_tile, ax0, ty0, static_cast<const double*>(p.img), p.pitch, x, y,
                           c, s);
         __syncthreads();
-        s_bits[slot0.w] = triplet_bit_7x7(s_win, slot0.x, slot0.y, slot0.z);
-        s_bits[slot1.w] = triplet_bit_7x7(s_win, slot1.x, slot1.y, slot1.z);
+        s_bits[slot0.w & 0x7fff] = triplet_bit_7x7(s_win, slot0.x, slot0.y, slot0.z, slot0.w >> 15);
+        s_bits[slot1.w & 0x7fff] = triplet_bit_7x7(s_win, slot1.x, slot1.y, slot1.z, slot1.w >> 15);
         __syncthreads();
         // Bit t -> byte t>>3, bit t&7 == bit t of the little-endian 32-bit word t>>5.
         const unsigned w0 = __ballot_sync(0xffffffffu, s_bits[tid] != 0);

@@ -48,6 +48,8 @@ struct Pattern {
     DeviceBuffer slots;            // T * ushort4
     DeviceBuffer triplets;         // generic kernel: T * 6 int16
     std::vector<double> weights;   // K*K
+    double slot_degree = 0.0;           // planned / table-order shared-load conflict degree
+    double slot_degree_identity = 0.0;
 };
 
 } // namespace clatch
@@ -60,8 +62,10 @@ struct clatch_ctx {
     cudaStream_t stream = nullptr;
     clatch::Pattern pattern;
     uint64_t launches = 0;
+    int match_variant = 1;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC (CLATCH_MATCH_VARIANT)
     // scratch for the host-buffer entry points
     clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8;
+    std::vector<double> host_xycs;   // describe_all staging
 };
 
 namespace clatch {

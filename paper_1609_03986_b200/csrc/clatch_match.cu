@@ -9,8 +9,13 @@
 // Tiled kernel (64-byte descriptors): one query per thread held in 16 registers;
 // the train set streams through a double-buffered shared-memory tile filled by the
 // TMA bulk-copy engine (cp.async.bulk + mbarrier); every thread reads the same train
-// descriptor with four broadcast 128-bit shared loads and runs XOR + __popc. The
-// train set is split across blockIdx.y so small query sets still fill 148 SMs; a
+// descriptor with four broadcast 128-bit shared loads. POPC issues on the 16-lane/clk XU
+// pipe, which the plain XOR+__popc form saturates (profiles/r1a_match_ncu.json: XU 93.7 %
+// active, ALU 38 %), so the 16 XOR words are first compressed with carry-save adders
+// (two LOP3 each, on the 64-lane ALU pipe) into words of weight 1, 2 (and 4) and only
+// those are popcounted: 9 (or 7) POPC per 512-bit compare instead of 16. Top-2 selection
+// runs on packed keys (distance << 21 | local index): min/max only, lowest index wins
+// ties by construction. The train set is split across blockIdx.y so small query sets still fill 148 SMs; a
 // second tiny kernel merges the per-split partial top-2 (splits are ascending index
 // ranges, so "earlier split wins ties" keeps the lowest index).
 
@@ -71,18 +76,58 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
         : "memory");
 }
 
-__device__ __forceinline__ int hamming16(const unsigned (&q)[kDescWords], const uint4* t) {
-    int d = 0;
+// Carry-save adder: three words of weight w -> one of weight w (sum) + one of weight 2w (carry).
+__device__ __forceinline__ void csa(unsigned& sum, unsigned& carry, unsigned a, unsigned b, unsigned c) {
+    sum = a ^ b ^ c;                        // LOP3 0x96
+    carry = (a & b) | (a & c) | (b & c);    // LOP3 0xE8
+}
+
+// Hamming distance of two 512-bit descriptors. kVariant 0: 16 POPC. 1: 7 CSA + 9 POPC.
+// 2: 9 CSA + 7 POPC. All exact (integer identities).
+template <int kVariant>
+__device__ __forceinline__ unsigned hamming16(const unsigned (&q)[kDescWords], const uint4* t) {
+    unsigned x[kDescWords];
 #pragma unroll
     for (int i = 0; i < kDescWords / 4; ++i) {
         const uint4 v = t[i];   // same address in every lane: one broadcast wavefront
-        d += __popc(q[4 * i + 0] ^ v.x) + __popc(q[4 * i + 1] ^ v.y) + __popc(q[4 * i + 2] ^ v.z) +
-             __popc(q[4 * i + 3] ^ v.w);
+        x[4 * i + 0] = q[4 * i + 0] ^ v.x;
+        x[4 * i + 1] = q[4 * i + 1] ^ v.y;
+        x[4 * i + 2] = q[4 * i + 2] ^ v.z;
+        x[4 * i + 3] = q[4 * i + 3] ^ v.w;
     }
-    return d;
+    if (kVariant == 0) {
+        unsigned d = 0;
+#pragma unroll
+        for (int i = 0; i < kDescWords; ++i) d += __popc(x[i]);
+        return d;
+    }
+    unsigned o[7], w2[9];
+    csa(o[0], w2[0], x[0], x[1], x[2]);
+    csa(o[1], w2[1], x[3], x[4], x[5]);
+    csa(o[2], w2[2], x[6], x[7], x[8]);
+    csa(o[3], w2[3], x[9], x[10], x[11]);
+    csa(o[4], w2[4], x[12], x[13], x[14]);
+    csa(o[5], w2[5], o[0], o[1], o[2]);
+    csa(o[6], w2[6], o[3], o[4], x[15]);
+    const unsigned ones = __popc(o[5]) + __popc(o[6]);
+    if (kVariant == 1) {
+        const unsigned twos = __popc(w2[0]) + __popc(w2[1]) + __popc(w2[2]) + __popc(w2[3]) +
+                              __popc(w2[4]) + __popc(w2[5]) + __popc(w2[6]);
+        return ones + 2 * twos;
+    }
+    unsigned w4[2];
+    csa(w2[7], w4[0], w2[0], w2[1], w2[2]);
+    csa(w2[8], w4[1], w2[3], w2[4], w2[5]);
+    const unsigned twos = __popc(w2[6]) + __popc(w2[7]) + __popc(w2[8]);
+    const unsigned fours = __popc(w4[0]) + __popc(w4[1]);
+    return ones + 2 * twos + 4 * fours;
 }
 
+constexpr int kKeyShift = 21;                       // local train index bits inside a packed key
+constexpr unsigned kKeyIndexMask = (1u << kKeyShift) - 1;
+
 // grid = (ceil(Q/128), splits). Split s scans train rows [s*per_split, min(N, (s+1)*per_split)).
+template <int kVariant>
 __global__ void __launch_bounds__(kMatchThreads) match64_kernel(const uint8_t* __restrict__ queries,
                                                                 unsigned long long Q,
                                                                 const uint8_t* __restrict__ train,
@@ -129,36 +174,35 @@ __global__ void __launch_bounds__(kMatchThreads) match64_kernel(const uint8_t* _
         }
     }
 
-    const int sentinel = 8 * kDescBytes + 1;
-    int best = sentinel, second = sentinel, best_idx = -1;
+    // Packed keys: (distance << 21) | index inside this split. Scanning with min/max keeps
+    // the two smallest keys; equal distances order by index, so the lowest index wins
+    // (knn2's strict '<', src/match.cpp:41-47) and the runner-up may tie the best.
+    const unsigned sentinel_key = (static_cast<unsigned>(8 * kDescBytes + 1) << kKeyShift) | kKeyIndexMask;
+    unsigned best_key = sentinel_key, second_key = sentinel_key;
 
     for (int tile = 0; tile < tiles; ++tile) {
         if (tid == 0 && tile + 1 < tiles) issue(tile + 1);   // buffer (tile+1)&1 was released by the
                                                              // __syncthreads closing iteration tile-1
         mbar_wait(&s_bar[tile & 1], (tile >> 1) & 1);
-        const unsigned long long first = n_begin + static_cast<unsigned long long>(tile) * kTileDesc;
-        const int count = static_cast<int>(min(static_cast<unsigned long long>(kTileDesc), n_end - first));
+        const int count = static_cast<int>(
+            min(static_cast<unsigned long long>(kTileDesc), n_end - n_begin - static_cast<unsigned long long>(tile) * kTileDesc));
         const uint4* t = s_tile[tile & 1];
+        const unsigned base = static_cast<unsigned>(tile) * kTileDesc;
 #pragma unroll 4
         for (int j = 0; j < count; ++j) {
-            const int d = hamming16(q, t + j * (kDescBytes / 16));
-            // knn2 update, src/match.cpp:41-47
-            if (d < best) {
-                second = best;
-                best = d;
-                best_idx = static_cast<int>(first - n_begin) + j;
-            } else if (d < second) {
-                second = d;
-            }
+            const unsigned d = hamming16<kVariant>(q, t + j * (kDescBytes / 16));
+            const unsigned key = (d << kKeyShift) + (base + j);
+            second_key = min(second_key, max(best_key, key));
+            best_key = min(best_key, key);
         }
         __syncthreads();   // everyone is done with this buffer before it is refilled
     }
 
     if (qi < Q) {
         Partial r;
-        r.best_idx = best_idx < 0 ? -1 : static_cast<int>(n_begin) + best_idx;
-        r.best_dist = best;
-        r.second_dist = second;
+        r.best_idx = best_key == sentinel_key ? -1 : static_cast<int>(n_begin + (best_key & kKeyIndexMask));
+        r.best_dist = static_cast<int>(best_key >> kKeyShift);
+        r.second_dist = static_cast<int>(second_key >> kKeyShift);
         r.pad = 0;
         partial[static_cast<unsigned long long>(blockIdx.y) * Q + qi] = r;
     }
@@ -237,6 +281,7 @@ int launch_match_top2(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8
     size_t splits = std::max<size_t>(1, (want + qblocks - 1) / qblocks);
     const size_t max_splits = std::max<size_t>(1, N / (2 * kTileDesc));
     splits = std::min(splits, std::min<size_t>(max_splits, 65535));
+    splits = std::max(splits, (N + kKeyIndexMask - 1) / kKeyIndexMask);   // local index must fit the key
     size_t per_split = (N + splits - 1) / splits;
     per_split = (per_split + kTileDesc - 1) / kTileDesc * kTileDesc;
     splits = (N + per_split - 1) / per_split;
@@ -244,7 +289,11 @@ int launch_match_top2(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8
     if (int rc = ctx->partial.reserve(sizeof(Partial) * splits * Q)) return rc;
     Partial* partial = ctx->partial.as<Partial>();
     dim3 grid(static_cast<unsigned>(qblocks), static_cast<unsigned>(splits));
-    match64_kernel<<<grid, kMatchThreads, 0, stream>>>(d_q, Q, d_t, N, per_split, partial);
+    switch (ctx->match_variant) {
+        case 0: match64_kernel<0><<<grid, kMatchThreads, 0, stream>>>(d_q, Q, d_t, N, per_split, partial); break;
+        case 2: match64_kernel<2><<<grid, kMatchThreads, 0, stream>>>(d_q, Q, d_t, N, per_split, partial); break;
+        default: match64_kernel<1><<<grid, kMatchThreads, 0, stream>>>(d_q, Q, d_t, N, per_split, partial); break;
+    }
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
     merge_partials_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(

@@ -1,0 +1,154 @@
+// Bank-conflict-aware placement of triplets onto lanes for the specialised
+// extraction kernel (host side, runs once per clatch_set_pattern).
+//
+// In the SSD phase lane j of a warp reads window[(y_j + r) * stride + x_j + c] for its
+// own triplet's anchor / companion patches with 64-bit shared loads. Such a load is
+// served per half-warp (16 lanes x 8 B = 128 B) and is conflict-free iff the 16 lanes
+// hit 16 distinct 8-byte bank pairs, i.e. distinct (y_j * stride + x_j) mod 16 — the
+// same for every (r, c) step because all lanes advance by the same offset. Measured on
+// B200 (profiles/r1a_pipe_peaks.json): 126.8 B/clk/SM when distinct, 42 B/clk/SM for
+// random slots. With the triplets in table order the average degree is 3.1
+// (profiles/r1a_extract_ncu.json: 65 % of shared wavefronts are conflict replays).
+//
+// Freedom used here: (1) which triplet sits in which (half-warp, lane) slot — the bit
+// index travels with the slot; (2) swapping the two companions of a triplet (the kernel
+// then tests d2 > d1 instead of d1 > d2, i.e. the same predicate). A deterministic
+// simulated annealing minimises sum over (half-warp, load) of the worst bank-pair
+// multiplicity, with the number of colliding lanes as a tie-breaking gradient.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+namespace clatch {
+
+struct SlotEntry {
+    uint16_t a, b, c;   // window offsets (y * stride + x) of the loads issued 1st, 2nd, 3rd
+    uint16_t bit;       // descriptor bit index; bit 15 set => companions swapped
+};
+
+struct SlotPlan {
+    std::vector<SlotEntry> slots;   // T entries, slot = thread-visible position
+    double avg_degree = 0.0;        // mean worst multiplicity over (half-warp, load)
+    double avg_degree_identity = 0.0;
+};
+
+namespace detail {
+
+struct GroupHist {
+    uint8_t h[3][16];
+};
+
+inline int hist_cost(const uint8_t* h) {
+    int mx = 0, excess = 0;
+    for (int r = 0; r < 16; ++r) {
+        mx = std::max<int>(mx, h[r]);
+        excess += h[r] > 1 ? h[r] - 1 : 0;
+    }
+    return 16 * mx + excess;
+}
+
+inline int hist_degree(const uint8_t* h) {
+    int mx = 0;
+    for (int r = 0; r < 16; ++r) mx = std::max<int>(mx, h[r]);
+    return mx;
+}
+
+} // namespace detail
+
+// triplets: T x {ax, ay, bx, by, cx, cy}. T must be a multiple of 16.
+inline SlotPlan plan_slots(const int16_t* triplets, int T, int stride, int iterations = 400000) {
+    using namespace detail;
+    const int G = T / 16;
+    std::vector<uint16_t> off(3 * T);
+    for (int t = 0; t < T; ++t)
+        for (int k = 0; k < 3; ++k)
+            off[3 * t + k] = static_cast<uint16_t>(triplets[6 * t + 2 * k + 1] * stride + triplets[6 * t + 2 * k]);
+
+    std::vector<int> order(T);            // order[slot] = triplet
+    std::vector<uint8_t> flip(T, 0);      // per triplet
+    for (int t = 0; t < T; ++t) order[t] = t;
+    auto res = [&](int t, int k) {        // residue of load k of triplet t under its flip
+        const int kk = (k == 0 || !flip[t]) ? k : 3 - k;
+        return off[3 * t + kk] & 15;
+    };
+    std::vector<GroupHist> hist(G);
+    auto rebuild = [&](int g) {
+        GroupHist gh{};
+        for (int l = 0; l < 16; ++l)
+            for (int k = 0; k < 3; ++k) ++gh.h[k][res(order[16 * g + l], k)];
+        hist[g] = gh;
+    };
+    auto gcost = [&](int g) { return hist_cost(hist[g].h[0]) + hist_cost(hist[g].h[1]) + hist_cost(hist[g].h[2]); };
+    auto degree = [&]() {
+        double s = 0;
+        for (int g = 0; g < G; ++g)
+            for (int k = 0; k < 3; ++k) s += hist_degree(hist[g].h[k]);
+        return s / (3.0 * G);
+    };
+    for (int g = 0; g < G; ++g) rebuild(g);
+    SlotPlan plan;
+    plan.avg_degree_identity = degree();
+
+    uint64_t rng = 0x9E3779B97F4A7C15ull;   // fixed seed: the plan is a pure function of the pattern
+    auto next = [&]() {
+        rng ^= rng << 13;
+        rng ^= rng >> 7;
+        rng ^= rng << 17;
+        return rng;
+    };
+    std::vector<int> cost(G);
+    for (int g = 0; g < G; ++g) cost[g] = gcost(g);
+    const double t0 = 6.0;
+    for (int it = 0; it < iterations && G > 1; ++it) {
+        const double temp = t0 * (1.0 - static_cast<double>(it) / iterations) + 0.05;
+        const uint64_t r = next();
+        const auto accept = [&](int delta) {
+            if (delta <= 0) return true;
+            const double u = static_cast<double>((next() >> 11) & 0xFFFFF) / 1048576.0;
+            return u < std::exp(-delta / temp);
+        };
+        if ((r & 7) == 0) {                       // flip the companions of one triplet
+            const int p = static_cast<int>((r >> 8) % T), g = p / 16, t = order[p];
+            const GroupHist saved = hist[g];
+            for (int k = 1; k < 3; ++k) --hist[g].h[k][res(t, k)];
+            flip[t] ^= 1;
+            for (int k = 1; k < 3; ++k) ++hist[g].h[k][res(t, k)];
+            const int nc = gcost(g);
+            if (accept(nc - cost[g])) cost[g] = nc;
+            else { flip[t] ^= 1; hist[g] = saved; }
+            continue;
+        }
+        const int p = static_cast<int>((r >> 8) % T), q = static_cast<int>((r >> 32) % T);
+        const int g1 = p / 16, g2 = q / 16;
+        if (g1 == g2) continue;
+        const GroupHist s1 = hist[g1], s2 = hist[g2];
+        const int tp = order[p], tq = order[q];
+        for (int k = 0; k < 3; ++k) {
+            --hist[g1].h[k][res(tp, k)]; ++hist[g1].h[k][res(tq, k)];
+            --hist[g2].h[k][res(tq, k)]; ++hist[g2].h[k][res(tp, k)];
+        }
+        const int n1 = gcost(g1), n2 = gcost(g2);
+        if (accept(n1 + n2 - cost[g1] - cost[g2])) {
+            order[p] = tq; order[q] = tp; cost[g1] = n1; cost[g2] = n2;
+        } else {
+            hist[g1] = s1; hist[g2] = s2;
+        }
+    }
+    plan.avg_degree = degree();
+    plan.slots.resize(T);
+    for (int s = 0; s < T; ++s) {
+        const int t = order[s];
+        SlotEntry e;
+        e.a = off[3 * t + 0];
+        e.b = off[3 * t + (flip[t] ? 2 : 1)];
+        e.c = off[3 * t + (flip[t] ? 1 : 2)];
+        e.bit = static_cast<uint16_t>(t | (flip[t] ? 0x8000 : 0));
+        plan.slots[s] = e;
+    }
+    return plan;
+}
+
+} // namespace clatch

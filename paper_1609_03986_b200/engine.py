@@ -109,6 +109,31 @@ class Engine:
         _lib.check(rc)
         return out
 
+    def describe_all(self, image: np.ndarray, keypoints: np.ndarray, workers: int = 0):
+        """describe_all in one ABI call: -> (kept int64 (M,), descriptors uint8 (M, T/8))."""
+        h, w = image.shape
+        if image.strides[1] != image.itemsize or image.strides[0] % image.itemsize:
+            image = np.ascontiguousarray(image)
+        pitch = image.strides[0] // image.itemsize
+        kps = np.ascontiguousarray(keypoints, np.float64)
+        n, cols = kps.shape
+        kept = np.empty(n, np.int64)
+        out = np.empty((n, self.descriptor_bytes), np.uint8)
+        m = C.c_size_t()
+        with self._lock:
+            if image.dtype == np.uint8:
+                rc = self.lib.clatch_describe_all_u8(self.ctx, _ptr(image, u8p), w, h, pitch, _ptr(kps, f64p),
+                                                     n, cols, workers, _ptr(kept, i64p), _ptr(out, u8p),
+                                                     C.byref(m))
+            elif image.dtype == np.float64:
+                rc = self.lib.clatch_describe_all_f64(self.ctx, _ptr(image, f64p), w, h, pitch,
+                                                      _ptr(kps, f64p), n, cols, workers, _ptr(kept, i64p),
+                                                      _ptr(out, u8p), C.byref(m))
+            else:
+                raise TypeError("image dtype must be uint8 or float64")
+        _lib.check(rc)
+        return kept[:m.value], out[:m.value]
+
     # ---- extraction, device tensors --------------------------------------------
     def extract_device(self, image, xycs, out=None, stream=None):
         """image: torch CUDA tensor (H, W) uint8 or float64, unit inner stride; xycs: CUDA

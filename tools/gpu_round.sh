@@ -13,6 +13,13 @@ echo "== pytest -m gpu"; timeout 1500 python -m pytest tests -m gpu -x -q > "$OU
 tail -5 "$OUT/pytest_gpu.log"
 echo "== pipe peaks"; timeout 120 ./tools/pipe_peaks > "$OUT/pipe_peaks.json" 2> "$OUT/pipe_peaks.err"; cat "$OUT/pipe_peaks.json"
 echo "== bench ours"; timeout 900 python bench.py --steps 20 --warmup 5 > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?"; cat "$OUT/bench.json"; tail -3 "$OUT/bench.err"
+if [ "${VARIANTS:-0}" = "1" ]; then
+for v in 0 1 2; do
+  echo "== matcher variant $v"
+  CLATCH_MATCH_VARIANT=$v timeout 300 python bench.py --steps 20 --warmup 5 --phase match --no-cpu-baseline > "$OUT/bench_match_v$v.json" 2>> "$OUT/bench.err"
+  python -c "import json;d=json.load(open('$OUT/bench_match_v$v.json'));print('variant $v compares/s', d['compares_per_s'], 'ms', d['kernels']['match64_kernel']['ms'])"
+done
+fi
 echo "== bench reference"; timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"; cat "$OUT/bench_reference.json"
 if [ "${SKIP_NCU:-0}" != "1" ]; then
 echo "== ncu launch list"
