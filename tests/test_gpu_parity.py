@@ -254,7 +254,7 @@ def test_filters_known_answers(lk):
     probes = np.stack([_ones(1), _ones(2)])
     gallery = np.stack([_ones(0), _ones(30)])
     got = lk.match(probes, gallery, cross_check=True)
-    assert got.tolist() == [[0, 0, 1, 30]]
+    assert got.tolist() == [[0, 0, 1, 29]]
     assert len(lk.match(probes, gallery)) == 2
 
 
