@@ -1,0 +1,364 @@
+// latch_b200.hpp — C++ host face of the B200 CLATCH paths (header-only, over clatch.h).
+//
+// Mirrors the slice of the reference's C++ API that sits on the two hot paths, with the
+// same names, argument meaning and error behaviour, so host code written against
+// "latchkit" keeps compiling when it includes this header instead of
+// latch/descriptor.hpp + latch/match.hpp (paths relative to /root/reference/proj):
+//
+//   describe_all / describe / keypoint_in_margin   include/latch/descriptor.hpp:48-67
+//   match_brute_force / knn2 / hamming             include/latch/match.hpp:13-45
+//   Image, Keypoint, Descriptor, TripletPattern,
+//   WeightMask, Triplet, MatchOptions, MatchPair   image.hpp:12-29, detect.hpp:11-16,
+//                                                  descriptor.hpp:31-42, pattern.hpp:19-52
+//   Error / ErrorCode                              errors.hpp:10-56
+//   parse_pattern / default_pattern                pattern.hpp:100-108
+//
+// Everything per-sample / per-pair runs on the GPU through the C ABI; this header only
+// converts containers, keeps the reference's early-outs and re-raises status codes as
+// latch::Error. There is no CPU arithmetic path here: without a B200 every compute call
+// throws. In a real integration the reference keeps its own type definitions and only the
+// bodies of the functions below move (INTEGRATION.md shows the patch).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <optional>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "clatch.h"
+
+namespace latch {
+
+// ---- errors (errors.hpp:10-56) ----------------------------------------------------
+enum class ErrorCode {
+    NotPGM, UnsupportedDepth, Truncated, Malformed, OutOfBounds, BadScale,
+    ImageTooSmall, TooCloseToBorder,
+    BadHeader, BadTripletCount, CoordinateOutOfRange, DegenerateTriplet, MissingInfo,
+    GridSizeMismatch, LabelParse, NoPositives, NoNegatives, EmptyPairs, InsufficientCandidates,
+    LengthMismatch, EmptyGallery,
+    NoKeypoints,
+    DeviceUnavailable   // extension: the GPU path could not run (no CPU fallback exists)
+};
+
+inline const char* error_code_name(ErrorCode code) {
+    static const char* const names[] = {
+        "NotPGM", "UnsupportedDepth", "Truncated", "Malformed", "OutOfBounds", "BadScale",
+        "ImageTooSmall", "TooCloseToBorder", "BadHeader", "BadTripletCount", "CoordinateOutOfRange",
+        "DegenerateTriplet", "MissingInfo", "GridSizeMismatch", "LabelParse", "NoPositives",
+        "NoNegatives", "EmptyPairs", "InsufficientCandidates", "LengthMismatch", "EmptyGallery",
+        "NoKeypoints", "DeviceUnavailable"};
+    return names[static_cast<int>(code)];
+}
+
+class Error : public std::runtime_error {
+public:
+    Error(ErrorCode code, const std::string& message)
+        : std::runtime_error(prefixed(code, message)), code_(code) {}
+    ErrorCode code() const noexcept { return code_; }
+
+private:
+    static std::string prefixed(ErrorCode code, const std::string& m) {
+        const std::string name = error_code_name(code);
+        return m.compare(0, name.size(), name) == 0 ? m : name + ": " + m;
+    }
+    ErrorCode code_;
+};
+
+[[noreturn]] inline void raise(ErrorCode code, const std::string& message) { throw Error(code, message); }
+
+// ---- data types ---------------------------------------------------------------------
+inline constexpr int kWindowSize = 64;
+inline constexpr int kDefaultPatchSize = 8;
+inline constexpr int kDefaultBitCount = 512;
+inline constexpr int kWindowMargin = 46;
+
+struct Image {   // image.hpp:12-29: row-major doubles, pixel centres at integers
+    int width = 0, height = 0;
+    std::vector<double> data;
+    Image() = default;
+    Image(int w, int h) : width(w), height(h), data(static_cast<std::size_t>(w) * h, 0.0) {}
+    Image(int w, int h, std::vector<double> v) : width(w), height(h), data(std::move(v)) {}
+    double at(int x, int y) const { return data[static_cast<std::size_t>(y) * width + x]; }
+    double& at(int x, int y) { return data[static_cast<std::size_t>(y) * width + x]; }
+};
+
+struct Keypoint { double x = 0, y = 0, theta = 0, score = 0; };   // detect.hpp:11-16
+
+struct Descriptor {   // descriptor.hpp:31-42: bit t in byte t/8, position t%8
+    std::vector<std::uint8_t> bytes;
+    bool bit(std::size_t t) const { return (bytes[t >> 3] >> (t & 7)) & 1u; }
+    void set_bit(std::size_t t, bool v) {
+        const auto b = static_cast<std::uint8_t>(1u << (t & 7));
+        if (v) bytes[t >> 3] |= b; else bytes[t >> 3] &= static_cast<std::uint8_t>(~b);
+    }
+    std::size_t bit_count() const { return bytes.size() * 8; }
+    bool operator==(const Descriptor& o) const { return bytes == o.bytes; }
+};
+
+struct Triplet { int ax = 0, ay = 0, bx = 0, by = 0, cx = 0, cy = 0; };   // pattern.hpp:19-25
+
+struct WeightMask {   // pattern.hpp:30-42
+    int size = kDefaultPatchSize;
+    std::vector<double> weights;
+    static WeightMask ones(int size = kDefaultPatchSize) {
+        WeightMask m; m.size = size; m.weights.assign(static_cast<std::size_t>(size) * size, 1.0); return m;
+    }
+    static WeightMask seven_by_seven() {
+        WeightMask m = ones(kDefaultPatchSize);
+        for (int i = 0; i < 8; ++i) m.weights[7 * 8 + i] = m.weights[i * 8 + 7] = 0.0;
+        return m;
+    }
+};
+
+struct TripletPattern {   // pattern.hpp:46-52
+    int bit_count = kDefaultBitCount;
+    int patch_size = kDefaultPatchSize;
+    std::vector<Triplet> triplets;
+    WeightMask mask;
+};
+
+struct MatchPair { int probe_index = 0, gallery_index = 0, distance = 0, second_distance = 0; };
+
+struct MatchOptions {   // match.hpp:20-25
+    std::optional<double> ratio;
+    bool cross_check = false;
+    std::optional<int> max_distance;
+    int workers = 0;   // accepted for source compatibility; the GPU grid replaces the thread fan-out
+};
+
+struct Knn2Result { int best_index = -1, best_distance = 0, second_distance = 0; };
+
+// ---- the shared GPU context -----------------------------------------------------------
+namespace b200 {
+
+[[noreturn]] inline void rethrow(int rc) {
+    const std::string msg = clatch_last_error();
+    if (rc >= 100 && rc <= 121) throw Error(static_cast<ErrorCode>(rc - 100), msg);
+    if (rc == CLATCH_ERR_NONFINITE) throw Error(ErrorCode::OutOfBounds, msg);
+    if (rc == CLATCH_ERR_INVALID) throw std::invalid_argument(msg);
+    throw Error(ErrorCode::DeviceUnavailable, msg);
+}
+
+inline void check(int rc) { if (rc != CLATCH_OK) rethrow(rc); }
+
+struct Context {
+    clatch_ctx* ctx = nullptr;
+    std::mutex mutex;                 // one ctx: calls are serialised (clatch.h threading note)
+    const void* pattern_tag = nullptr;
+    std::vector<std::int16_t> pattern_coords;
+    std::vector<double> pattern_weights;
+    int pattern_t = 0, pattern_k = 0;
+    ~Context() { if (ctx) clatch_ctx_destroy(ctx); }
+};
+
+inline Context& context() {
+    static Context c;
+    if (!c.ctx) {
+        const char* dev = std::getenv("CLATCH_DEVICE");
+        check(clatch_ctx_create(dev ? std::atoi(dev) : 0, &c.ctx));
+    }
+    return c;
+}
+
+// Installs `pattern` unless the very same table is already on the device.
+inline void use_pattern(Context& c, const TripletPattern& pattern) {
+    std::vector<std::int16_t> coords;
+    coords.reserve(pattern.triplets.size() * 6);
+    for (const Triplet& t : pattern.triplets)
+        for (int v : {t.ax, t.ay, t.bx, t.by, t.cx, t.cy}) coords.push_back(static_cast<std::int16_t>(v));
+    if (c.pattern_t == pattern.bit_count && c.pattern_k == pattern.patch_size && c.pattern_coords == coords &&
+        c.pattern_weights == pattern.mask.weights)
+        return;
+    if (static_cast<int>(pattern.triplets.size()) != pattern.bit_count ||
+        static_cast<int>(pattern.mask.weights.size()) != pattern.patch_size * pattern.patch_size)
+        raise(ErrorCode::BadTripletCount, "pattern tables do not match T / K");
+    check(clatch_set_pattern(c.ctx, coords.data(), pattern.bit_count, pattern.patch_size,
+                             pattern.mask.weights.data()));
+    c.pattern_t = pattern.bit_count;
+    c.pattern_k = pattern.patch_size;
+    c.pattern_coords = std::move(coords);
+    c.pattern_weights = pattern.mask.weights;
+}
+
+inline std::vector<std::uint8_t> flatten(const std::vector<Descriptor>& set, std::size_t bytes) {
+    std::vector<std::uint8_t> flat(set.size() * bytes);
+    for (std::size_t i = 0; i < set.size(); ++i) {
+        if (set[i].bytes.size() != bytes)   // hamming's check, src/match.cpp:15-18
+            raise(ErrorCode::LengthMismatch, "descriptor lengths differ: " + std::to_string(bytes) + " vs " +
+                                                 std::to_string(set[i].bytes.size()));
+        std::memcpy(flat.data() + i * bytes, set[i].bytes.data(), bytes);
+    }
+    return flat;
+}
+
+} // namespace b200
+
+// ---- pattern text (pattern.hpp:100-108; src/pattern.cpp:68-131) ---------------------------
+inline TripletPattern parse_pattern(const std::string& text) {
+    std::istringstream in(text);
+    std::string line;
+    if (!std::getline(in, line)) raise(ErrorCode::BadHeader, "empty pattern file");
+    int T = 0, K = 0;
+    if (std::sscanf(line.c_str(), "LATCHPAT v1 T=%d K=%d", &T, &K) != 2)
+        raise(ErrorCode::BadHeader, "bad header line '" + line + "'");
+    if (T <= 0 || T % 8 != 0) raise(ErrorCode::BadHeader, "T must be a positive multiple of 8, got " + std::to_string(T));
+    if (K < 1 || K > kWindowSize) raise(ErrorCode::BadHeader, "K out of range: " + std::to_string(K));
+    TripletPattern p;
+    p.bit_count = T;
+    p.patch_size = K;
+    bool weights = false;
+    while (std::getline(in, line)) {
+        if (line.empty()) continue;
+        if (line == "WEIGHTS") { weights = true; break; }
+        if (static_cast<int>(p.triplets.size()) == T)
+            raise(ErrorCode::BadTripletCount, "more than T=" + std::to_string(T) + " triplet lines");
+        Triplet t;
+        if (std::sscanf(line.c_str(), "%d %d %d %d %d %d", &t.ax, &t.ay, &t.bx, &t.by, &t.cx, &t.cy) != 6)
+            raise(ErrorCode::BadTripletCount, "bad triplet line '" + line + "'");
+        for (int c : {t.ax, t.ay, t.bx, t.by, t.cx, t.cy})
+            if (c < 0 || c > kWindowSize - K)
+                raise(ErrorCode::CoordinateOutOfRange, "coordinate " + std::to_string(c) + " outside [0, " +
+                                                           std::to_string(kWindowSize - K) + "]");
+        if (t.bx == t.cx && t.by == t.cy)
+            raise(ErrorCode::DegenerateTriplet, "companion patches coincide at (" + std::to_string(t.bx) + ", " +
+                                                    std::to_string(t.by) + ")");
+        p.triplets.push_back(t);
+    }
+    if (static_cast<int>(p.triplets.size()) != T)
+        raise(ErrorCode::BadTripletCount, "expected " + std::to_string(T) + " triplets, got " +
+                                              std::to_string(p.triplets.size()));
+    if (!weights) { p.mask = WeightMask::ones(K); return p; }
+    p.mask.size = K;
+    bool any = false;
+    for (int row = 0; row < K; ++row) {
+        if (!std::getline(in, line)) raise(ErrorCode::BadHeader, "truncated WEIGHTS section");
+        std::istringstream ls(line);
+        for (int col = 0; col < K; ++col) {
+            double w;
+            if (!(ls >> w) || !std::isfinite(w) || w < 0.0)
+                raise(ErrorCode::BadHeader, "bad weight in row " + std::to_string(row));
+            p.mask.weights.push_back(w);
+            any = any || w > 0.0;
+        }
+    }
+    if (!any) raise(ErrorCode::BadHeader, "weight mask is all zeros");
+    return p;
+}
+
+inline TripletPattern load_pattern_file(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) raise(ErrorCode::BadHeader, "cannot open pattern file '" + path + "'");
+    std::ostringstream buf;
+    buf << f.rdbuf();
+    return parse_pattern(buf.str());
+}
+
+/// The shipped 512-triplet table (pattern_default.cpp:527-539), read once from the LATCHPAT
+/// file named by CLATCH_DEFAULT_PATTERN (default: paper_1609_03986_b200/data/default_pattern.latchpat
+/// relative to the working directory). A reference build keeps its compiled-in table instead.
+inline const TripletPattern& default_pattern() {
+    static const TripletPattern p = [] {
+        const char* env = std::getenv("CLATCH_DEFAULT_PATTERN");
+        return load_pattern_file(env ? env : "paper_1609_03986_b200/data/default_pattern.latchpat");
+    }();
+    return p;
+}
+
+// ---- extraction (descriptor.hpp:48-67) ------------------------------------------------------
+inline bool keypoint_in_margin(const Image& image, const Keypoint& k) {   // src/descriptor.cpp:23-27
+    return k.x - kWindowMargin >= 0.0 && k.y - kWindowMargin >= 0.0 && k.x + kWindowMargin <= image.width - 1 &&
+           k.y + kWindowMargin <= image.height - 1;
+}
+
+/// Batch extraction: margin violators are silently dropped, the rest keep their input
+/// order; output is identical for any `workers` (it only sizes the host-side trig pass).
+inline std::vector<std::pair<Keypoint, Descriptor>> describe_all(const Image& image,
+                                                                 const std::vector<Keypoint>& keypoints,
+                                                                 const TripletPattern& pattern, int workers = 0) {
+    static_assert(sizeof(Keypoint) == 4 * sizeof(double), "Keypoint must be 4 packed doubles");
+    b200::Context& c = b200::context();
+    std::lock_guard<std::mutex> lock(c.mutex);
+    b200::use_pattern(c, pattern);
+    const std::size_t n = keypoints.size(), bytes = static_cast<std::size_t>(pattern.bit_count) / 8;
+    std::vector<std::int64_t> kept(n);
+    std::vector<std::uint8_t> flat(n * bytes);
+    std::size_t m = 0;
+    b200::check(clatch_describe_all_f64(c.ctx, image.data.data(), image.width, image.height,
+                                        static_cast<std::size_t>(image.width),
+                                        reinterpret_cast<const double*>(keypoints.data()), n, 4, workers,
+                                        kept.data(), flat.data(), &m));
+    std::vector<std::pair<Keypoint, Descriptor>> out(m);
+    for (std::size_t j = 0; j < m; ++j) {
+        out[j].first = keypoints[static_cast<std::size_t>(kept[j])];
+        out[j].second.bytes.assign(flat.begin() + static_cast<std::ptrdiff_t>(j * bytes),
+                                   flat.begin() + static_cast<std::ptrdiff_t>((j + 1) * bytes));
+    }
+    return out;
+}
+
+/// Full descriptor for one keypoint. Throws TooCloseToBorder outside the margin.
+inline Descriptor describe(const Image& image, const Keypoint& keypoint, const TripletPattern& pattern) {
+    if (!keypoint_in_margin(image, keypoint))   // src/descriptor.cpp:30-33
+        raise(ErrorCode::TooCloseToBorder, "keypoint (" + std::to_string(keypoint.x) + ", " +
+                                               std::to_string(keypoint.y) + ") violates the " +
+                                               std::to_string(kWindowMargin) + "-pixel margin");
+    return describe_all(image, {keypoint}, pattern, 1).at(0).second;
+}
+
+// ---- matching (match.hpp:27-45) ---------------------------------------------------------------
+/// Best and second-best gallery distances for one probe; ties go to the smallest index.
+inline Knn2Result knn2(const Descriptor& probe, const std::vector<Descriptor>& gallery) {
+    if (gallery.empty()) raise(ErrorCode::EmptyGallery, "knn2 needs a nonempty gallery");
+    const std::size_t bytes = probe.bytes.size();
+    const std::vector<std::uint8_t> g = b200::flatten(gallery, bytes);
+    b200::Context& c = b200::context();
+    std::lock_guard<std::mutex> lock(c.mutex);
+    std::int32_t r[3];
+    b200::check(clatch_match_top2(c.ctx, probe.bytes.data(), 1, g.data(), gallery.size(), static_cast<int>(bytes),
+                                  &r[0], &r[1], &r[2]));
+    return {r[0], r[1], r[2]};
+}
+
+/// Number of differing bits. Lengths must match (LengthMismatch otherwise).
+inline int hamming(const Descriptor& a, const Descriptor& b) {
+    if (a.bytes.size() != b.bytes.size())
+        raise(ErrorCode::LengthMismatch, "descriptor lengths differ: " + std::to_string(a.bytes.size()) + " vs " +
+                                             std::to_string(b.bytes.size()));
+    if (a.bytes.empty()) return 0;
+    return knn2(a, {b}).best_distance;
+}
+
+/// Brute-force matcher with optional ratio, cross-check and distance-cutoff filters.
+/// Output sorted by probe index.
+inline std::vector<MatchPair> match_brute_force(const std::vector<Descriptor>& probes,
+                                                const std::vector<Descriptor>& gallery,
+                                                const MatchOptions& options = {}) {
+    if (gallery.empty()) raise(ErrorCode::EmptyGallery, "matching needs a nonempty gallery");   // src/match.cpp:55
+    if (probes.empty()) return {};                                                              // :56
+    const std::size_t bytes = probes[0].bytes.size();
+    const std::vector<std::uint8_t> p = b200::flatten(probes, bytes), g = b200::flatten(gallery, bytes);
+    std::vector<std::int32_t> rows(probes.size() * 4);
+    std::size_t count = 0;
+    b200::Context& c = b200::context();
+    std::lock_guard<std::mutex> lock(c.mutex);
+    b200::check(clatch_match_brute_force(c.ctx, p.data(), probes.size(), g.data(), gallery.size(),
+                                         static_cast<int>(bytes), options.ratio.has_value(),
+                                         options.ratio.value_or(0.0), options.cross_check,
+                                         options.max_distance.has_value(), options.max_distance.value_or(0),
+                                         rows.data(), &count));
+    std::vector<MatchPair> out(count);
+    for (std::size_t i = 0; i < count; ++i)
+        out[i] = {rows[4 * i], rows[4 * i + 1], rows[4 * i + 2], rows[4 * i + 3]};
+    return out;
+}
+
+} // namespace latch
