@@ -227,6 +227,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     eng = lk.get_engine(local)
     eng.set_pattern(None)
+    if args.match_variant is not None:
+        eng.set_option("match_variant", args.match_variant)
 
     w, h, n, _, _ = WORKLOADS[args.workload]
     img, kps = synth_inputs(args.workload, rank)
@@ -408,6 +410,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--phase", choices=["both", "extract", "match"], default="both")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--match-variant", type=int, default=None, help="override the matcher kernel variant (0..3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -71,6 +71,11 @@ CLATCH_API void clatch_ctx_destroy(clatch_ctx* ctx);
 /* Device facts for reporting: SM count, SM clock (kHz), name (<= 255 chars). */
 CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_khz, char* name, size_t cap);
 
+/* Tuning knobs (never change results). key "match_variant": 0 = XOR + 16 POPC, 1 = carry-save
+ * compression + 9 POPC (default), 2 = 9 CSA + 7 POPC, 3 = tcgen05 int8 GEMM on the tensor cores.
+ * Unknown keys fail with CLATCH_ERR_INVALID. */
+CLATCH_API int clatch_set_option(clatch_ctx* ctx, const char* key, int value);
+
 /* Block until everything queued on the context's own stream has finished. */
 CLATCH_API int clatch_synchronize(clatch_ctx* ctx);
 
@@ -162,6 +167,13 @@ CLATCH_API int clatch_match_brute_force(clatch_ctx* ctx, const uint8_t* probes, 
                              const uint8_t* gallery, size_t N, int bytes, int has_ratio,
                              double ratio, int cross_check, int has_max, int max_distance,
                              int32_t* out, size_t* count);
+
+/* Diagnostic for the tensor-core matcher: runs it on host buffers and also returns the raw
+ * int32 accumulators of the first 128-query x 256-train tile (row-major 128 x 256; entry
+ * (i, j) must equal 512 - 2 * hamming(query i, train j) for i < Q, j < N). */
+CLATCH_API int clatch_debug_tc_tile(clatch_ctx* ctx, const uint8_t* queries, size_t Q, const uint8_t* train,
+                         size_t N, int32_t* tile_out, int32_t* best_idx, int32_t* best_dist,
+                         int32_t* second_dist);
 
 /* Kernel launches issued through this context since creation (bench.py's
  * gpu_launches claim is read from here, not estimated). */

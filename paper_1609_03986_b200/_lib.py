@@ -52,6 +52,7 @@ _SIGNATURES = {
     "clatch_device_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p,
                                      C.c_size_t]),
     "clatch_synchronize": (C.c_int, [C.c_void_p]),
+    "clatch_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
     "clatch_set_pattern": (C.c_int, [C.c_void_p, i16p, C.c_int, C.c_int, f64p]),
     "clatch_descriptor_bytes": (C.c_int, [C.c_void_p]),
     "clatch_prepare_keypoints": (C.c_int, [f64p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, f64p,
@@ -76,6 +77,7 @@ _SIGNATURES = {
                                         C.c_int, i32p, i32p, szp]),
     "clatch_match_brute_force": (C.c_int, [C.c_void_p, u8p, C.c_size_t, u8p, C.c_size_t, C.c_int,
                                            C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, i32p, szp]),
+    "clatch_debug_tc_tile": (C.c_int, [C.c_void_p, u8p, C.c_size_t, u8p, C.c_size_t, i32p, i32p, i32p, i32p]),
     "clatch_launch_count": (C.c_uint64, [C.c_void_p]),
 }
 

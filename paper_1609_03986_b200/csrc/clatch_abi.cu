@@ -119,7 +119,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
         cudaStreamDestroy(ctx->stream);
     }
     for (DeviceBuffer* b : {&ctx->img, &ctx->kps, &ctx->desc, &ctx->q, &ctx->t, &ctx->res,
-                            &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->pattern.slots,
+                            &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->pattern.slots,
                             &ctx->pattern.triplets})
         b->release();
     delete ctx;
@@ -134,6 +134,16 @@ int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_khz, char* 
         name[cap - 1] = 0;
     }
     return CLATCH_OK;
+}
+
+int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
+    if (!ctx || !key) return invalid("clatch_set_option: null argument");
+    if (std::strcmp(key, "match_variant") == 0) {
+        if (value < 0 || value > 3) return invalid("match_variant must be 0..3");
+        ctx->match_variant = value;
+        return CLATCH_OK;
+    }
+    return invalid(std::string("clatch_set_option: unknown key '") + key + "'");
 }
 
 int clatch_synchronize(clatch_ctx* ctx) {
@@ -442,6 +452,31 @@ int clatch_match_top2(clatch_ctx* ctx, const uint8_t* queries, size_t Q, const u
     int32_t* r = ctx->res.as<int32_t>();
     if (int rc = launch_match_top2(ctx, ctx->q.as<uint8_t>(), Q, d_train, N, bytes, r, r + Q, r + 2 * Q, st))
         return rc;
+    if (best_idx) CLATCH_CUDA(cudaMemcpyAsync(best_idx, r, sizeof(int32_t) * Q, cudaMemcpyDeviceToHost, st));
+    if (best_dist) CLATCH_CUDA(cudaMemcpyAsync(best_dist, r + Q, sizeof(int32_t) * Q, cudaMemcpyDeviceToHost, st));
+    if (second_dist)
+        CLATCH_CUDA(cudaMemcpyAsync(second_dist, r + 2 * Q, sizeof(int32_t) * Q, cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    return CLATCH_OK;
+}
+
+int clatch_debug_tc_tile(clatch_ctx* ctx, const uint8_t* queries, size_t Q, const uint8_t* train, size_t N,
+                         int32_t* tile_out, int32_t* best_idx, int32_t* best_dist, int32_t* second_dist) {
+    if (int rc = check_match(ctx, queries, Q, train, N, 64)) return rc;
+    if (Q == 0 || !tile_out) return invalid("clatch_debug_tc_tile: empty query set or null output");
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = ctx->q.reserve(Q * 64)) return rc;
+    if (int rc = ctx->t.reserve(N * 64)) return rc;
+    if (int rc = ctx->res.reserve(sizeof(int32_t) * (3 * Q + 128 * 256))) return rc;
+    cudaStream_t st = ctx->stream;
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->q.ptr, queries, Q * 64, cudaMemcpyHostToDevice, st));
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->t.ptr, train, N * 64, cudaMemcpyHostToDevice, st));
+    int32_t* r = ctx->res.as<int32_t>();
+    CLATCH_CUDA(cudaMemsetAsync(r + 3 * Q, 0, sizeof(int32_t) * 128 * 256, st));
+    if (int rc = launch_match_top2_tc(ctx, ctx->q.as<uint8_t>(), Q, ctx->t.as<uint8_t>(), N, r, r + Q, r + 2 * Q, st,
+                                      r + 3 * Q))
+        return rc;
+    CLATCH_CUDA(cudaMemcpyAsync(tile_out, r + 3 * Q, sizeof(int32_t) * 128 * 256, cudaMemcpyDeviceToHost, st));
     if (best_idx) CLATCH_CUDA(cudaMemcpyAsync(best_idx, r, sizeof(int32_t) * Q, cudaMemcpyDeviceToHost, st));
     if (best_dist) CLATCH_CUDA(cudaMemcpyAsync(best_dist, r + Q, sizeof(int32_t) * Q, cudaMemcpyDeviceToHost, st));
     if (second_dist)

@@ -62,9 +62,9 @@ struct clatch_ctx {
     cudaStream_t stream = nullptr;
     clatch::Pattern pattern;
     uint64_t launches = 0;
-    int match_variant = 1;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC (CLATCH_MATCH_VARIANT)
+    int match_variant = 1;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
     // scratch for the host-buffer entry points
-    clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8;
+    clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t;
     std::vector<double> host_xycs;   // describe_all staging
 };
 
@@ -77,7 +77,18 @@ int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int heig
 int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
                        const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
 
-// matching (clatch_match.cu)
+// matching (clatch_match.cu, clatch_match_tc.cu)
+struct Partial {   // per (train split, query) partial top-2
+    int best_idx;
+    int best_dist;
+    int second_dist;
+    int pad;
+};
+void launch_merge_partials(const Partial* partial, unsigned long long Q, int splits, int sentinel,
+                           int32_t* best_idx, int32_t* best_dist, int32_t* second_dist, cudaStream_t stream);
+int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
+                         int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
+                         int32_t* d_dump = nullptr);
 int launch_match_top2(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
                       int bytes, int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second,
                       cudaStream_t stream);

@@ -32,13 +32,6 @@ constexpr int kTileDesc = 128;       // train descriptors per shared-memory tile
 constexpr int kDescBytes = 64;
 constexpr int kDescWords = 16;
 
-struct Partial {                     // per (split, query)
-    int best_idx;
-    int best_dist;
-    int second_dist;
-    int pad;
-};
-
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -261,6 +254,12 @@ __global__ void match_generic_kernel(const uint8_t* __restrict__ queries, unsign
 
 } // namespace
 
+void launch_merge_partials(const Partial* partial, unsigned long long Q, int splits, int sentinel,
+                           int32_t* best_idx, int32_t* best_dist, int32_t* second_dist, cudaStream_t stream) {
+    merge_partials_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(partial, Q, splits, sentinel,
+                                                                                      best_idx, best_dist, second_dist);
+}
+
 int launch_match_top2(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
                       int bytes, int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second,
                       cudaStream_t stream) {
@@ -275,6 +274,8 @@ int launch_match_top2(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8
         CLATCH_CUDA(cudaGetLastError());
         return CLATCH_OK;
     }
+    if (ctx->match_variant == 3)
+        return launch_match_top2_tc(ctx, d_q, Q, d_t, N, d_best_idx, d_best_dist, d_second, stream);
     const size_t qblocks = (Q + kMatchThreads - 1) / kMatchThreads;
     // Enough CTAs for ~8 resident per SM, but never a split shorter than two tiles.
     const size_t want = static_cast<size_t>(ctx->sm_count) * 8;

@@ -70,6 +70,10 @@ class Engine:
     def launch_count(self) -> int:
         return int(self.lib.clatch_launch_count(self.ctx))
 
+    def set_option(self, key: str, value: int):
+        """Tuning knobs that never change results, e.g. set_option("match_variant", 3)."""
+        _lib.check(self.lib.clatch_set_option(self.ctx, key.encode(), int(value)))
+
     def synchronize(self):
         _lib.check(self.lib.clatch_synchronize(self.ctx))
 

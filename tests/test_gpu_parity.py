@@ -364,3 +364,34 @@ def test_python_smoke_shapes(lk, golden_image_u8):
         lk.describe(np.zeros((128, 128)), np.array([[64.0, 64.0]]), pattern="not a pattern")
     with pytest.raises(ValueError):
         lk.describe(np.zeros(16), np.array([[64.0, 64.0]]))
+
+
+# ------------------------------------------------- matcher kernel variants ----
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_every_matcher_variant_is_exact(lk, port, variant):
+    """All four 64-byte matcher kernels (plain popc, two carry-save forms, tcgen05 int8 GEMM)
+    must give the reference's knn2 triples bit for bit, including ties, tails and a lone row."""
+    eng = lk.get_engine()
+    eng.set_option("match_variant", variant)
+    try:
+        for q, n in [(1, 1), (5, 255), (129, 256), (130, 257), (300, 1000), (1000, 5000), (77, 40000)]:
+            d = port.random_descriptors(7000 + q + n, q + n, 64)
+            probes, gallery = d[:q].copy(), d[q:].copy()
+            if n > 3:
+                gallery[n - 1] = gallery[0]
+                gallery[n // 2] = gallery[1]
+                probes[0] = gallery[0]
+                probes[q - 1] = gallery[1]
+            bi, bd, sd = eng.match_top2(probes, gallery)
+            assert np.array_equal(np.stack([bi, bd, sd], 1), port.knn2_all(probes, gallery)), (variant, q, n)
+        # extremes of the distance range: all-zero vs all-one rows, and exact duplicates
+        probes = np.zeros((3, 64), np.uint8)
+        probes[1] = 0xFF
+        probes[2, :32] = 0xFF
+        gallery = np.stack([np.full(64, 0xFF, np.uint8), np.zeros(64, np.uint8), np.zeros(64, np.uint8)])
+        bi, bd, sd = eng.match_top2(probes, gallery)
+        assert np.array_equal(np.stack([bi, bd, sd], 1), port.knn2_all(probes, gallery))
+        assert (bi[0], bd[0], sd[0]) == (1, 0, 0) and (bi[1], bd[1], sd[1]) == (0, 0, 512)
+    finally:
+        eng.set_option("match_variant", 1)
