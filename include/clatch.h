@@ -72,7 +72,7 @@ CLATCH_API void clatch_ctx_destroy(clatch_ctx* ctx);
 CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_khz, char* name, size_t cap);
 
 /* Tuning knobs (never change results). key "match_variant": 0 = XOR + 16 POPC, 1 = carry-save
- * compression + 9 POPC (default), 2 = 9 CSA + 7 POPC, 3 = tcgen05 int8 GEMM on the tensor cores.
+ * compression + 9 POPC, 2 = 9 CSA + 7 POPC, 3 = tcgen05 int8 GEMM on the tensor cores (default).
  * Unknown keys fail with CLATCH_ERR_INVALID. */
 CLATCH_API int clatch_set_option(clatch_ctx* ctx, const char* key, int value);
 

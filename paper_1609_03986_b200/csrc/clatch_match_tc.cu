@@ -289,7 +289,7 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp, const uint8_t* __restrict__ b
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
         }
-        // merge the two column halves of each row (half 0 holds the lower indices -> wins ties)
+        // merge the two column halves of each row
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpilogueWarps));   // all MMAs done => A region is free
         const int row = quarter * 32 + lane;
         if (half == 1) {
@@ -300,7 +300,8 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp, const uint8_t* __restrict__ b
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpilogueWarps));
         if (half == 0) {
             const int ob = merge_buf[row * 4 + 0], os = merge_buf[row * 4 + 1], oi = merge_buf[row * 4 + 2];
-            if (ob > best) {
+            // the halves interleave in index order across tiles, so ties compare indices
+            if (ob > best || (ob == best && oi >= 0 && oi < best_idx)) {
                 second = max(best, os);
                 best = ob;
                 best_idx = oi;

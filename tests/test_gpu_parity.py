@@ -394,4 +394,4 @@ def test_every_matcher_variant_is_exact(lk, port, variant):
         assert np.array_equal(np.stack([bi, bd, sd], 1), port.knn2_all(probes, gallery))
         assert (bi[0], bd[0], sd[0]) == (1, 0, 0) and (bi[1], bd[1], sd[1]) == (0, 0, 512)
     finally:
-        eng.set_option("match_variant", 1)
+        eng.set_option("match_variant", 3)

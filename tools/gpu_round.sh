@@ -14,9 +14,9 @@ tail -5 "$OUT/pytest_gpu.log"
 echo "== pipe peaks"; timeout 120 ./tools/pipe_peaks > "$OUT/pipe_peaks.json" 2> "$OUT/pipe_peaks.err"; cat "$OUT/pipe_peaks.json"
 echo "== bench ours"; timeout 900 python bench.py --steps 20 --warmup 5 > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?"; cat "$OUT/bench.json"; tail -3 "$OUT/bench.err"
 if [ "${VARIANTS:-0}" = "1" ]; then
-for v in 0 1 2; do
+for v in 0 1 2 3; do
   echo "== matcher variant $v"
-  CLATCH_MATCH_VARIANT=$v timeout 300 python bench.py --steps 20 --warmup 5 --phase match --no-cpu-baseline > "$OUT/bench_match_v$v.json" 2>> "$OUT/bench.err"
+  timeout 300 python bench.py --steps 20 --warmup 5 --phase match --no-cpu-baseline --match-variant $v > "$OUT/bench_match_v$v.json" 2>> "$OUT/bench.err"
   python -c "import json;d=json.load(open('$OUT/bench_match_v$v.json'));print('variant $v compares/s', d['compares_per_s'], 'ms', d['kernels']['match64_kernel']['ms'])"
 done
 fi
@@ -28,6 +28,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 echo "== ncu full: extraction"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:extract_ -s 3 -c 1 -f -o "$OUT/prof_extract" \
     python bench.py --steps 2 --warmup 3 --phase extract --no-cpu-baseline > "$OUT/ncu_extract.log" 2>&1
+echo "== ncu full: tensor-core matching"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_tc -s 3 -c 1 -f -o "$OUT/prof_match_tc" \
+    python bench.py --steps 2 --warmup 3 --phase match --no-cpu-baseline --match-variant 3 > "$OUT/ncu_match_tc.log" 2>&1
 echo "== ncu full: matching"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:match64 -s 3 -c 1 -f -o "$OUT/prof_match" \
     python bench.py --steps 2 --warmup 3 --phase match --no-cpu-baseline > "$OUT/ncu_match.log" 2>&1
