@@ -229,6 +229,8 @@ def run_ours(args):
     eng.set_pattern(None)
     if args.match_variant is not None:
         eng.set_option("match_variant", args.match_variant)
+    if args.extract_variant is not None:
+        eng.set_option("extract_variant", args.extract_variant)
 
     w, h, n, _, _ = WORKLOADS[args.workload]
     img, kps = synth_inputs(args.workload, rank)
@@ -411,6 +413,7 @@ def main():
     ap.add_argument("--phase", choices=["both", "extract", "match"], default="both")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--match-variant", type=int, default=None, help="override the matcher kernel variant (0..3)")
+    ap.add_argument("--extract-variant", type=int, default=None, help="override the extraction kernel variant (0..1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

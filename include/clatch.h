@@ -73,7 +73,8 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
 
 /* Tuning knobs (never change results). key "match_variant": 0 = XOR + 16 POPC, 1 = carry-save
  * compression + 9 POPC, 2 = 9 CSA + 7 POPC, 3 = tcgen05 int8 GEMM on the tensor cores (default).
- * Unknown keys fail with CLATCH_ERR_INVALID. */
+ * key "extract_variant": 0 = one window per CTA, 1 = four windows per CTA with conflict-free
+ * shared loads (default). Unknown keys fail with CLATCH_ERR_INVALID. */
 CLATCH_API int clatch_set_option(clatch_ctx* ctx, const char* key, int value);
 
 /* Block until everything queued on the context's own stream has finished. */

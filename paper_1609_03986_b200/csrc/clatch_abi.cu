@@ -119,7 +119,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
         cudaStreamDestroy(ctx->stream);
     }
     for (DeviceBuffer* b : {&ctx->img, &ctx->kps, &ctx->desc, &ctx->q, &ctx->t, &ctx->res,
-                            &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->pattern.slots,
+                            &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->pattern.slots, &ctx->pattern.slots_quad,
                             &ctx->pattern.triplets})
         b->release();
     delete ctx;
@@ -141,6 +141,11 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
     if (std::strcmp(key, "match_variant") == 0) {
         if (value < 0 || value > 3) return invalid("match_variant must be 0..3");
         ctx->match_variant = value;
+        return CLATCH_OK;
+    }
+    if (std::strcmp(key, "extract_variant") == 0) {
+        if (value < 0 || value > 1) return invalid("extract_variant must be 0 or 1");
+        ctx->extract_variant = value;
         return CLATCH_OK;
     }
     return invalid(std::string("clatch_set_option: unknown key '") + key + "'");
@@ -218,6 +223,10 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
         static_assert(sizeof(SlotEntry) == sizeof(ushort4), "slot layout");
         if (int rc = pat.slots.reserve(sizeof(SlotEntry) * T)) return rc;
         CLATCH_CUDA(cudaMemcpy(pat.slots.ptr, plan.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
+        const SlotPlan quad = plan_slots_quad(triplets, T, kWinStride, 300000);
+        pat.slot_degree_quad = quad.avg_degree;
+        if (int rc = pat.slots_quad.reserve(sizeof(SlotEntry) * T)) return rc;
+        CLATCH_CUDA(cudaMemcpy(pat.slots_quad.ptr, quad.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
     }
     return CLATCH_OK;
 }

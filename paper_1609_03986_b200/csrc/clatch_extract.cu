@@ -17,6 +17,7 @@
 // reads the window with immediate-offset 64-bit shared loads, (4) predicate bits are
 // packed with __ballot_sync and stored as 32-bit words.
 
+#include <algorithm>
 #include <cstdio>
 
 #include "clatch_internal.cuh"
@@ -78,11 +79,12 @@ __device__ __forceinline__ double blend(double fx, double fy, double p00, double
 }
 
 // Stage rows [ty0, ty0+92) x 16-byte-aligned columns [ax0, ax0+112) of a u8 image.
+template <int kGroup = kThreads>
 __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const uint8_t* img, size_t pitch,
-                                              int height, int ax0, int ty0, bool aligned) {
+                                              int height, int ax0, int ty0, bool aligned, int tid = threadIdx.x) {
     if (aligned) {
         constexpr int kChunks = kTileW / 16;
-        for (int i = threadIdx.x; i < kTileH * kChunks; i += kThreads) {
+        for (int i = tid; i < kTileH * kChunks; i += kGroup) {
             const int r = i / kChunks, c = i - r * kChunks;
             const int gx = ax0 + 16 * c;
             uint4 v = make_uint4(0, 0, 0, 0);
@@ -91,7 +93,7 @@ __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const uint8_t* img,
             *reinterpret_cast<uint4*>(tile + r * kTileW + 16 * c) = v;
         }
     } else {
-        for (int i = threadIdx.x; i < kTileH * kTileW; i += kThreads) {
+        for (int i = tid; i < kTileH * kTileW; i += kGroup) {
             const int r = i / kTileW, c = i - r * kTileW;
             const int gx = ax0 + c;
             uint8_t v = 0;
@@ -107,13 +109,13 @@ __device__ __forceinline__ void stage_tile_u8(uint8_t* tile, const uint8_t* img,
 template <bool kU8>
 __device__ __forceinline__ void build_window(double* win, const uint8_t* tile, int ax0, int ty0,
                                              const double* img64, size_t pitch, double x, double y,
-                                             double c, double s) {
-    const int u = threadIdx.x & 63;
+                                             double c, double s, int tid = threadIdx.x) {
+    const int u = tid & 63;
     const double du = static_cast<double>(u) - 31.5;
     const double xa = __dadd_rn(x, __dmul_rn(c, du));
     const double ya = __dadd_rn(y, __dmul_rn(s, du));
 #pragma unroll 4
-    for (int v = threadIdx.x >> 6; v < kWindow; v += kThreads / 64) {
+    for (int v = tid >> 6; v < kWindow; v += kThreads / 64) {
         const double dv = static_cast<double>(v) - 31.5;
         const double sx = __dsub_rn(xa, __dmul_rn(s, dv));
         const double sy = __dadd_rn(ya, __dmul_rn(c, dv));
@@ -208,6 +210,76 @@ __global__ void __launch_bounds__(kThreads, 4) extract_fast_kernel(ExtractParams
             unsigned* out32 = reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8));
             out32[tid >> 5] = w0;
             out32[(tid >> 5) + kThreads / 32] = w1;
+        }
+    }
+}
+
+
+// ---- quad kernel: four keypoints per CTA iteration, conflict-free SSD loads ----------------
+// Same arithmetic as extract_fast_kernel; what changes is who sits next to whom. The CTA
+// (1024 threads, one per SM) keeps four windows in shared memory, window w displaced by
+// 4*w bank pairs (kQuadWinPitch % 16 == 4). In the SSD phase each half-warp holds 4 triplets x
+// 4 keypoints (lane = 4*i + w): the four lanes of a triplet land on residues r, r+4, r+8,
+// r+12, so the half-warp is conflict-free whenever its 4 triplets differ mod 4 in each load —
+// which plan_slots_quad arranges for all but ~7 % of the (half-warp, load) pairs.
+constexpr int kQuad = 4;
+constexpr int kQuadThreads = kQuad * kThreads;                       // 1024
+constexpr int kQuadWinPitch = 4164;                                  // doubles; 4164 % 16 == 4
+constexpr int kQuadSmemBytes = kQuad * kQuadWinPitch * 8 + kQuad * kTileH * kTileW + kQuad * kFastT;
+
+template <bool kU8>
+__global__ void __launch_bounds__(kQuadThreads, 1) extract_quad_kernel(ExtractParams p) {
+    if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
+
+    extern __shared__ __align__(16) uint8_t s_quad[];
+    double* const s_win = reinterpret_cast<double*>(s_quad);
+    uint8_t* const s_tile = s_quad + kQuad * kQuadWinPitch * 8;
+    uint8_t* const s_bits = s_tile + kQuad * kTileH * kTileW;
+
+    const int tid = threadIdx.x;
+    // phases 1-2: thread group `grp` (256 threads) builds window `grp`
+    const int grp = tid >> 8, gt = tid & (kThreads - 1);
+    // phase 3: half-warp hw holds triplet slots 4*hw .. 4*hw+3 (and +256) for keypoints 0..3
+    const int hw = tid >> 4, j = tid & 15, kb = j & 3, ti = j >> 2;
+    const ushort4 slot0 = __ldg(p.slots + 4 * hw + ti);
+    const ushort4 slot1 = __ldg(p.slots + 4 * hw + ti + kFastT / 2);
+    const double* const my_win = s_win + kb * kQuadWinPitch;
+    uint8_t* const my_bits = s_bits + kb * kFastT;
+    const bool aligned = kU8 && (reinterpret_cast<uintptr_t>(p.img) % 16 == 0) && (p.pitch % 16 == 0);
+    const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
+
+    for (unsigned long long quad = blockIdx.x; quad < quads; quad += gridDim.x) {
+        const unsigned long long kp = quad * kQuad + grp;
+        const bool valid = kp < p.M;
+        double x = 0, y = 0, c = 0, s = 0;
+        int ax0 = 0, ty0 = 0;
+        if (valid) {
+            x = __ldg(p.xycs + 4 * kp + 0);
+            y = __ldg(p.xycs + 4 * kp + 1);
+            c = __ldg(p.xycs + 4 * kp + 2);
+            s = __ldg(p.xycs + 4 * kp + 3);
+            if (kU8) {
+                const int tx0 = __double2int_rd(x) - 45;
+                ty0 = __double2int_rd(y) - 45;
+                ax0 = aligned ? (tx0 & ~15) : tx0;
+                stage_tile_u8<kThreads>(s_tile + grp * kTileH * kTileW, static_cast<const uint8_t*>(p.img), p.pitch,
+                                        p.height, ax0, ty0, aligned, gt);
+            }
+        }
+        __syncthreads();   // tiles ready; the previous quad's window / bit readers are done
+        if (valid)
+            build_window<kU8>(s_win + grp * kQuadWinPitch, s_tile + grp * kTileH * kTileW, ax0, ty0,
+                              static_cast<const double*>(p.img), p.pitch, x, y, c, s, gt);
+        __syncthreads();
+        my_bits[slot0.w & 0x7fff] = triplet_bit_7x7(my_win, slot0.x, slot0.y, slot0.z, slot0.w >> 15);
+        my_bits[slot1.w & 0x7fff] = triplet_bit_7x7(my_win, slot1.x, slot1.y, slot1.z, slot1.w >> 15);
+        __syncthreads();
+        const unsigned w0 = __ballot_sync(0xffffffffu, s_bits[grp * kFastT + gt] != 0);
+        const unsigned w1 = __ballot_sync(0xffffffffu, s_bits[grp * kFastT + gt + kThreads] != 0);
+        if ((tid & 31) == 0 && valid) {
+            unsigned* out32 = reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8));
+            out32[gt >> 5] = w0;
+            out32[(gt >> 5) + kThreads / 32] = w1;
         }
     }
 }
@@ -315,7 +387,20 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     p.K = pat.K;
     p.flags = flags;
     p.run_if_flag = run_if_flag;
-    if (pat.fast) {
+    if (pat.fast && ctx->extract_variant == 1) {
+        static bool configured = false;
+        if (!configured) {
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_quad_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kQuadSmemBytes));
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_quad_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kQuadSmemBytes));
+            configured = true;
+        }
+        p.slots = pat.slots_quad.as<ushort4>();
+        const size_t quads = (M + kQuad - 1) / kQuad;
+        const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
+        extract_quad_kernel<kU8><<<grid, kQuadThreads, kQuadSmemBytes, stream>>>(p);
+    } else if (pat.fast) {
         extract_fast_kernel<kU8><<<grid_for(ctx, M, 4), kThreads, 0, stream>>>(p);
     } else {
         extract_generic_kernel<kU8><<<grid_for(ctx, M, 2), kThreads, pat.T, stream>>>(p);

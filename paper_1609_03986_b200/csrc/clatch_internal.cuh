@@ -45,11 +45,13 @@ struct Pattern {
     bool fast = false;             // T=512, K=8, 7x7-of-8x8 binary mask
     // Slot tables (device): slot j of the specialised kernel computes bit `bit[j]`
     // from window offsets (row*kWinStride+col) a/b/c; packed as ushort4 {a, b, c, bit}.
-    DeviceBuffer slots;            // T * ushort4
+    DeviceBuffer slots;            // T * ushort4 (single-window kernel: half-warps of 16 triplets)
+    DeviceBuffer slots_quad;       // T * ushort4 (quad kernel: half-warps of 4 triplets x 4 keypoints)
     DeviceBuffer triplets;         // generic kernel: T * 6 int16
     std::vector<double> weights;   // K*K
     double slot_degree = 0.0;           // planned / table-order shared-load conflict degree
     double slot_degree_identity = 0.0;
+    double slot_degree_quad = 0.0;
 };
 
 } // namespace clatch
@@ -62,6 +64,7 @@ struct clatch_ctx {
     cudaStream_t stream = nullptr;
     clatch::Pattern pattern;
     uint64_t launches = 0;
+    int extract_variant = 1;       // 0: one window per CTA (4 CTAs/SM), 1: quad kernel (4 windows per CTA)
     int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
     // scratch for the host-buffer entry points
     clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t;

@@ -151,4 +151,98 @@ inline SlotPlan plan_slots(const int16_t* triplets, int T, int stride, int itera
     return plan;
 }
 
+// ---- "quad" placement -------------------------------------------------------------------
+// The quad kernel keeps FOUR keypoints' windows in shared memory, window w displaced by
+// 4*w bank pairs, and fills each half-warp with 4 triplets x 4 keypoints (lane = 4*i + w).
+// The four lanes of one triplet then sit on residues x, x+4, x+8, x+12, so a half-warp is
+// conflict-free as soon as its 4 triplets have distinct residues MOD 4 in each of the three
+// loads — a far weaker condition than 16 distinct residues mod 16, and one that almost every
+// group can meet (only the mod-4 histogram imbalance of the table remains).
+inline SlotPlan plan_slots_quad(const int16_t* triplets, int T, int stride, int iterations = 300000) {
+    const int G = T / 4;
+    std::vector<uint16_t> off(3 * T);
+    for (int t = 0; t < T; ++t)
+        for (int k = 0; k < 3; ++k)
+            off[3 * t + k] = static_cast<uint16_t>(triplets[6 * t + 2 * k + 1] * stride + triplets[6 * t + 2 * k]);
+    std::vector<int> order(T);
+    std::vector<uint8_t> flip(T, 0);
+    for (int t = 0; t < T; ++t) order[t] = t;
+    auto res = [&](int t, int k) {
+        const int kk = (k == 0 || !flip[t]) ? k : 3 - k;
+        return off[3 * t + kk] & 3;
+    };
+    // cost of a group: per load, 16 * (worst multiplicity) + colliding lanes
+    auto gcost = [&](int g, int* degree_sum) {
+        int cost = 0;
+        for (int k = 0; k < 3; ++k) {
+            int h[4] = {0, 0, 0, 0};
+            for (int l = 0; l < 4; ++l) ++h[res(order[4 * g + l], k)];
+            int mx = 0, excess = 0;
+            for (int r = 0; r < 4; ++r) {
+                mx = std::max(mx, h[r]);
+                excess += h[r] > 1 ? h[r] - 1 : 0;
+            }
+            cost += 16 * mx + excess;
+            if (degree_sum) *degree_sum += mx;
+        }
+        return cost;
+    };
+    auto degree = [&]() {
+        int sum = 0;
+        for (int g = 0; g < G; ++g) gcost(g, &sum);
+        return sum / (3.0 * G);
+    };
+    SlotPlan plan;
+    plan.avg_degree_identity = degree();
+    uint64_t rng = 0x9E3779B97F4A7C15ull;
+    auto next = [&]() {
+        rng ^= rng << 13;
+        rng ^= rng >> 7;
+        rng ^= rng << 17;
+        return rng;
+    };
+    std::vector<int> cost(G);
+    for (int g = 0; g < G; ++g) cost[g] = gcost(g, nullptr);
+    for (int it = 0; it < iterations && G > 1; ++it) {
+        const double temp = 4.0 * (1.0 - static_cast<double>(it) / iterations) + 0.05;
+        const uint64_t r = next();
+        const auto accept = [&](int delta) {
+            if (delta <= 0) return true;
+            const double u = static_cast<double>((next() >> 11) & 0xFFFFF) / 1048576.0;
+            return u < std::exp(-delta / temp);
+        };
+        if ((r & 7) == 0) {
+            const int p = static_cast<int>((r >> 8) % T), g = p / 4, t = order[p];
+            flip[t] ^= 1;
+            const int nc = gcost(g, nullptr);
+            if (accept(nc - cost[g])) cost[g] = nc;
+            else flip[t] ^= 1;
+            continue;
+        }
+        const int p = static_cast<int>((r >> 8) % T), q = static_cast<int>((r >> 32) % T);
+        const int g1 = p / 4, g2 = q / 4;
+        if (g1 == g2) continue;
+        std::swap(order[p], order[q]);
+        const int n1 = gcost(g1, nullptr), n2 = gcost(g2, nullptr);
+        if (accept(n1 + n2 - cost[g1] - cost[g2])) {
+            cost[g1] = n1;
+            cost[g2] = n2;
+        } else {
+            std::swap(order[p], order[q]);
+        }
+    }
+    plan.avg_degree = degree();
+    plan.slots.resize(T);
+    for (int s = 0; s < T; ++s) {
+        const int t = order[s];
+        SlotEntry e;
+        e.a = off[3 * t + 0];
+        e.b = off[3 * t + (flip[t] ? 2 : 1)];
+        e.c = off[3 * t + (flip[t] ? 1 : 2)];
+        e.bit = static_cast<uint16_t>(t | (flip[t] ? 0x8000 : 0));
+        plan.slots[s] = e;
+    }
+    return plan;
+}
+
 } // namespace clatch

@@ -395,3 +395,23 @@ def test_every_matcher_variant_is_exact(lk, port, variant):
         assert (bi[0], bd[0], sd[0]) == (1, 0, 0) and (bi[1], bd[1], sd[1]) == (0, 0, 512)
     finally:
         eng.set_option("match_variant", 3)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_every_extraction_variant_is_exact(lk, port, variant):
+    """Both specialised extraction kernels (one window per CTA / four windows per CTA) must be
+    bit-identical to the oracle, including keypoint counts that do not fill a quad."""
+    eng = lk.get_engine()
+    eng.set_option("extract_variant", variant)
+    try:
+        img = port.structured_image(2030 + variant, 400, 300)
+        for n in (1, 2, 3, 5, 127, 1001):
+            kps = port.random_keypoints(2040 + n, 400, 300, n)
+            want = port.describe_all(img, kps)[1]
+            assert np.array_equal(lk.describe(img.astype(np.uint8), kps)[1], want), (variant, n, "u8")
+            assert np.array_equal(lk.describe(img, kps)[1], want), (variant, n, "f64")
+        fimg = np.random.default_rng(variant).random((300, 400)) * 255.0
+        kps = port.random_keypoints(2050, 400, 300, 203)
+        assert np.array_equal(lk.describe(fimg, kps)[1], port.describe_all(fimg, kps)[1])
+    finally:
+        eng.set_option("extract_variant", 1)

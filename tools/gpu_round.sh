@@ -14,6 +14,11 @@ tail -5 "$OUT/pytest_gpu.log"
 echo "== pipe peaks"; timeout 120 ./tools/pipe_peaks > "$OUT/pipe_peaks.json" 2> "$OUT/pipe_peaks.err"; cat "$OUT/pipe_peaks.json"
 echo "== bench ours"; timeout 900 python bench.py --steps 20 --warmup 5 > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?"; cat "$OUT/bench.json"; tail -3 "$OUT/bench.err"
 if [ "${VARIANTS:-0}" = "1" ]; then
+for v in 0 1; do
+  echo "== extraction variant $v"
+  timeout 300 python bench.py --steps 20 --warmup 5 --phase extract --no-cpu-baseline --extract-variant $v > "$OUT/bench_extract_v$v.json" 2>> "$OUT/bench.err"
+  python -c "import json;d=json.load(open('$OUT/bench_extract_v$v.json'));print('extract variant $v desc/s', d['descriptors_per_s'])"
+done
 for v in 0 1 2 3; do
   echo "== matcher variant $v"
   timeout 300 python bench.py --steps 20 --warmup 5 --phase match --no-cpu-baseline --match-variant $v > "$OUT/bench_match_v$v.json" 2>> "$OUT/bench.err"
