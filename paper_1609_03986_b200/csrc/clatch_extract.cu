@@ -54,18 +54,15 @@ __device__ __forceinline__ double u8_to_f64(unsigned v) {
 }
 
 // floor() of a double in (0, 2^31) as both int and double, again without F2I/I2F:
-// t = s + (2^52 + 2^51) rounds s to the nearest integer into the low mantissa bits;
-// step down by one when that rounded up. Both results are exact, so fx = s - floor(s)
-// is bit-identical to the reference's `x - x0` (src/image.cpp:113,121).
+// adding 2^52 + 2^51 with round-toward-minus-infinity leaves magic + floor(s) exactly (the
+// ulp is 1 at that magnitude), the integer sits in the low mantissa word, and subtracting
+// the magic is exact. So fx = s - floor(s) is bit-identical to the reference's `x - x0`
+// (src/image.cpp:113,121) at two DADDs instead of two 16-lane/clk conversions.
 __device__ __forceinline__ void floor_exact(double s, int& i, double& f) {
     const double kMagic = 6755399441055744.0;
-    const double t = __dadd_rn(s, kMagic);
+    const double t = __dadd_rd(s, kMagic);
     i = __double2loint(t);
     f = __dsub_rn(t, kMagic);
-    if (f > s) {
-        i -= 1;
-        f = __dsub_rn(f, 1.0);
-    }
 }
 
 // One bilinear sample with the reference's exact operation order (src/image.cpp:121-125).
@@ -120,6 +117,44 @@ __device__ __forceinline__ void build_window(double* win, const uint8_t* tile, i
         const double sx = __dsub_rn(xa, __dmul_rn(s, dv));
         const double sy = __dadd_rn(ya, __dmul_rn(c, dv));
         int x0, y0;                           // inside the margin: 1 <= x0 <= width-3, no clamps fire
+        double x0f, y0f;
+        floor_exact(sx, x0, x0f);
+        floor_exact(sy, y0, y0f);
+        const double fx = __dsub_rn(sx, x0f);
+        const double fy = __dsub_rn(sy, y0f);
+        double p00, p10, p01, p11;
+        if (kU8) {
+            const uint8_t* p = tile + (y0 - ty0) * kTileW + (x0 - ax0);
+            p00 = u8_to_f64(p[0]);
+            p10 = u8_to_f64(p[1]);
+            p01 = u8_to_f64(p[kTileW]);
+            p11 = u8_to_f64(p[kTileW + 1]);
+        } else {
+            const double* p = img64 + static_cast<size_t>(y0) * pitch + x0;
+            p00 = __ldg(p);
+            p10 = __ldg(p + 1);
+            p01 = __ldg(p + pitch);
+            p11 = __ldg(p + pitch + 1);
+        }
+        win[v * kWinStride + u] = blend(fx, fy, p00, p10, p01, p11);
+    }
+}
+
+// Same resampling with the per-row products s*dv and c*dv read from a 2 x 64 shared table
+// (filled once per keypoint; all lanes of a warp share v, so the reads broadcast).
+template <bool kU8>
+__device__ __forceinline__ void build_window_tab(double* win, const uint8_t* tile, int ax0, int ty0,
+                                                 const double* img64, size_t pitch, double x, double y,
+                                                 double c, double s, const double* tab, int tid) {
+    const int u = tid & 63;
+    const double du = static_cast<double>(u) - 31.5;
+    const double xa = __dadd_rn(x, __dmul_rn(c, du));
+    const double ya = __dadd_rn(y, __dmul_rn(s, du));
+#pragma unroll 4
+    for (int v = tid >> 6; v < kWindow; v += kThreads / 64) {
+        const double sx = __dsub_rn(xa, tab[v]);
+        const double sy = __dadd_rn(ya, tab[kWindow + v]);
+        int x0, y0;
         double x0f, y0f;
         floor_exact(sx, x0, x0f);
         floor_exact(sy, y0, y0f);
@@ -225,7 +260,35 @@ __global__ void __launch_bounds__(kThreads, 4) extract_fast_kernel(ExtractParams
 constexpr int kQuad = 4;
 constexpr int kQuadThreads = kQuad * kThreads;                       // 1024
 constexpr int kQuadWinPitch = 4164;                                  // doubles; 4164 % 16 == 4
-constexpr int kQuadSmemBytes = kQuad * kQuadWinPitch * 8 + kQuad * kTileH * kTileW + kQuad * kFastT;
+constexpr int kQuadTileBytes = kTileH * kTileW;                      // 10304
+constexpr int kQuadSmemBytes = kQuad * kQuadWinPitch * 8             // windows
+                               + 2 * kQuad * kQuadTileBytes          // double-buffered u8 tiles
+                               + kQuad * kFastT                      // predicate bytes
+                               + kQuad * 2 * kWindow * 8;            // s*dv, c*dv tables
+
+// Footprint origin of keypoint (x, y): rows floor(y)-45.., 16-byte aligned columns.
+__device__ __forceinline__ void tile_origin(double x, double y, bool aligned, int& ax0, int& ty0) {
+    int xi, yi;
+    double unused;
+    floor_exact(x, xi, unused);
+    floor_exact(y, yi, unused);
+    ty0 = yi - 45;
+    ax0 = aligned ? ((xi - 45) & ~15) : (xi - 45);
+}
+
+// Asynchronous (LDGSTS) staging of one keypoint's tile by a 256-thread group.
+__device__ __forceinline__ void stage_tile_async(uint8_t* tile, const uint8_t* img, size_t pitch, int height,
+                                                 int ax0, int ty0, int gt) {
+    constexpr int kChunks = kTileW / 16;
+    for (int i = gt; i < kTileH * kChunks; i += kThreads) {
+        const int r = i / kChunks, c = i - r * kChunks;
+        const int gx = ax0 + 16 * c;
+        const bool in = static_cast<size_t>(gx) < pitch && ty0 + r < height;
+        const uint8_t* src = in ? img + static_cast<size_t>(ty0 + r) * pitch + gx : img;
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(tile + r * kTileW + 16 * c));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0) : "memory");
+    }
+}
 
 template <bool kU8>
 __global__ void __launch_bounds__(kQuadThreads, 1) extract_quad_kernel(ExtractParams p) {
@@ -234,43 +297,72 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_quad_kernel(ExtractPa
     extern __shared__ __align__(16) uint8_t s_quad[];
     double* const s_win = reinterpret_cast<double*>(s_quad);
     uint8_t* const s_tile = s_quad + kQuad * kQuadWinPitch * 8;
-    uint8_t* const s_bits = s_tile + kQuad * kTileH * kTileW;
+    uint8_t* const s_bits = s_tile + 2 * kQuad * kQuadTileBytes;
+    double* const s_tab = reinterpret_cast<double*>(s_bits + kQuad * kFastT);
 
     const int tid = threadIdx.x;
-    // phases 1-2: thread group `grp` (256 threads) builds window `grp`
+    // staging / resampling: thread group `grp` (256 threads) owns keypoint `grp` of the quad
     const int grp = tid >> 8, gt = tid & (kThreads - 1);
-    // phase 3: half-warp hw holds triplet slots 4*hw .. 4*hw+3 (and +256) for keypoints 0..3
+    // SSD: half-warp hw holds triplet slots 4*hw .. 4*hw+3 (and +256) for keypoints 0..3
     const int hw = tid >> 4, j = tid & 15, kb = j & 3, ti = j >> 2;
     const ushort4 slot0 = __ldg(p.slots + 4 * hw + ti);
     const ushort4 slot1 = __ldg(p.slots + 4 * hw + ti + kFastT / 2);
     const double* const my_win = s_win + kb * kQuadWinPitch;
     uint8_t* const my_bits = s_bits + kb * kFastT;
+    double* const my_tab = s_tab + grp * 2 * kWindow;
+    const uint8_t* const img8 = static_cast<const uint8_t*>(p.img);
     const bool aligned = kU8 && (reinterpret_cast<uintptr_t>(p.img) % 16 == 0) && (p.pitch % 16 == 0);
     const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
 
-    for (unsigned long long quad = blockIdx.x; quad < quads; quad += gridDim.x) {
+    // Prefetch the first quad's tiles; later quads are prefetched under the SSD phase.
+    if (kU8 && aligned) {
+        const unsigned long long kp = static_cast<unsigned long long>(blockIdx.x) * kQuad + grp;
+        if (blockIdx.x < quads && kp < p.M) {
+            int ax0, ty0;
+            tile_origin(__ldg(p.xycs + 4 * kp), __ldg(p.xycs + 4 * kp + 1), true, ax0, ty0);
+            stage_tile_async(s_tile + grp * kQuadTileBytes, img8, p.pitch, p.height, ax0, ty0, gt);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+
+    int buf = 0;
+    for (unsigned long long quad = blockIdx.x; quad < quads; quad += gridDim.x, buf ^= 1) {
         const unsigned long long kp = quad * kQuad + grp;
         const bool valid = kp < p.M;
         double x = 0, y = 0, c = 0, s = 0;
         int ax0 = 0, ty0 = 0;
+        uint8_t* const tile = s_tile + (buf * kQuad + grp) * kQuadTileBytes;
         if (valid) {
             x = __ldg(p.xycs + 4 * kp + 0);
             y = __ldg(p.xycs + 4 * kp + 1);
             c = __ldg(p.xycs + 4 * kp + 2);
             s = __ldg(p.xycs + 4 * kp + 3);
             if (kU8) {
-                const int tx0 = __double2int_rd(x) - 45;
-                ty0 = __double2int_rd(y) - 45;
-                ax0 = aligned ? (tx0 & ~15) : tx0;
-                stage_tile_u8<kThreads>(s_tile + grp * kTileH * kTileW, static_cast<const uint8_t*>(p.img), p.pitch,
-                                        p.height, ax0, ty0, aligned, gt);
+                tile_origin(x, y, aligned, ax0, ty0);
+                if (!aligned) stage_tile_u8<kThreads>(tile, img8, p.pitch, p.height, ax0, ty0, false, gt);
+            }
+            if (gt < kWindow) {   // per-row products of extract_window (src/descriptor.cpp:44-45)
+                const double dv = static_cast<double>(gt) - 31.5;
+                my_tab[gt] = __dmul_rn(s, dv);
+                my_tab[kWindow + gt] = __dmul_rn(c, dv);
             }
         }
-        __syncthreads();   // tiles ready; the previous quad's window / bit readers are done
+        if (kU8 && aligned) asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();   // tiles + tables ready; the previous quad's window / bit readers are done
         if (valid)
-            build_window<kU8>(s_win + grp * kQuadWinPitch, s_tile + grp * kTileH * kTileW, ax0, ty0,
-                              static_cast<const double*>(p.img), p.pitch, x, y, c, s, gt);
+            build_window_tab<kU8>(s_win + grp * kQuadWinPitch, tile, ax0, ty0, static_cast<const double*>(p.img),
+                                  p.pitch, x, y, c, s, my_tab, gt);
         __syncthreads();
+        if (kU8 && aligned) {   // next quad's tiles stream in while the SSD phase runs
+            const unsigned long long nq = quad + gridDim.x, nkp = nq * kQuad + grp;
+            if (nq < quads && nkp < p.M) {
+                int nax0, nty0;
+                tile_origin(__ldg(p.xycs + 4 * nkp), __ldg(p.xycs + 4 * nkp + 1), true, nax0, nty0);
+                stage_tile_async(s_tile + ((buf ^ 1) * kQuad + grp) * kQuadTileBytes, img8, p.pitch, p.height, nax0,
+                                 nty0, gt);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
         my_bits[slot0.w & 0x7fff] = triplet_bit_7x7(my_win, slot0.x, slot0.y, slot0.z, slot0.w >> 15);
         my_bits[slot1.w & 0x7fff] = triplet_bit_7x7(my_win, slot1.x, slot1.y, slot1.z, slot1.w >> 15);
         __syncthreads();
