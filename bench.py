@@ -42,6 +42,10 @@ UNIT = "keypoints/s (1 keypoint = 1 descriptor extracted + M Hamming compares)"
 FP64_OPS_PER_DESC = 4096 * 15 + 512 * 49 * 2 * 3          # non-fused fp64 ops
 SMEM_BYTES_PER_DESC = 512 * 49 * 3 * 8                     # 8-byte window reads in the SSD phase
 POPC_PER_COMPARE = 16
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
+# captures of the same command (profiles/*_ncu.json); cold-cache replay, so an upper bound.
+TRAFFIC_NCU = {"extract_quad_kernel<u8>": 2.42e6,                 # profiles/r1f_extract_quad_ncu.json
+               "match_tc_kernel (tcgen05 kind::i8)": 10.45e6}     # profiles/r1e_match_tc_ncu.json
 
 
 def synth_inputs(workload: str, rank: int = 0):
@@ -327,51 +331,71 @@ def run_ours(args):
     peaks = load_peaks()
     per_step = t_dev / args.steps
     ext_s, mat_s = t_ext / args.steps, t_mat / args.steps
-    kernels = {}
+    sm_mhz = clocks.summary()["sm_mhz"] or 1965.0
+    sms = eng.sm_count
+    pipes = peaks.get("pipes", {})
+    mv = args.match_variant if args.match_variant is not None else 3
+    ev = args.extract_variant if args.extract_variant is not None else 1
+    ext_name = "extract_quad_kernel<u8>" if ev == 1 else "extract_fast_kernel<u8>"
+    mat_name = "match_tc_kernel (tcgen05 kind::i8)" if mv == 3 else f"match64_kernel<{mv}>"
+    kernels, pipe_roofline = {}, {}
     if ext_s > 0:
         alg_bytes = img.nbytes + m * 32 + m * 64            # image once + keypoint records + descriptors out
-        kernels["extract_fast_kernel<u8>"] = {
+        smem_gbs = m * SMEM_BYTES_PER_DESC / ext_s / 1e9
+        fp64_gops = m * FP64_OPS_PER_DESC / ext_s / 1e9
+        kernels[ext_name] = {
             "ms": ext_s * 1e3, "descriptors_per_s": m / ext_s,
             "hbm": {"achieved": alg_bytes / ext_s / 1e9, "algorithmic_bytes_per_launch": alg_bytes},
-            "fp64_gops": m * FP64_OPS_PER_DESC / ext_s / 1e9,
-            "smem_gbs": m * SMEM_BYTES_PER_DESC / ext_s / 1e9,
+            "fp64_gops": fp64_gops, "smem_gbs": smem_gbs,
+        }
+        smem_peak = pipes.get("lds64_gbs", sms * 128 * sm_mhz * 1e6 / 1e9)
+        fp64_peak = pipes.get("fp64_nonfused_gops", sms * 64 * sm_mhz * 1e6 / 1e9)
+        pipe_roofline["extract"] = {
+            "bound": "shared-memory wavefronts (602 KB of 8-byte window reads per descriptor)",
+            "smem": {"achieved_gbs": smem_gbs, "peak_gbs": smem_peak, "frac": smem_gbs / smem_peak},
+            "fp64": {"achieved_gops": fp64_gops, "peak_gops": fp64_peak, "frac": fp64_gops / fp64_peak},
+            "peak_source": "measured microbench (profiles/pipe_peaks.json)" if pipes else
+                           f"theoretical: {sms} SMs x 128 B/clk and x 64 lanes/clk at the sampled {sm_mhz:.0f} MHz",
         }
     if mat_s > 0:
         alg_bytes = 2 * m * 64 + 3 * 4 * m                  # both sets once + top-2 triples out
-        kernels["match64_kernel"] = {
-            "ms": mat_s * 1e3, "compares_per_s": m * m / mat_s,
+        cps = m * m / mat_s
+        kernels[mat_name] = {
+            "ms": mat_s * 1e3, "compares_per_s": cps,
             "hbm": {"achieved": alg_bytes / mat_s / 1e9, "algorithmic_bytes_per_launch": alg_bytes},
-            "popc_gops": m * m * POPC_PER_COMPARE / mat_s / 1e9,
         }
+        if mv == 3:
+            # one compare = 512 int8 MACs = 1024 ops; int8 dense peak = 2 x the bf16 peak
+            tops = cps * 1024 / 1e12
+            bf16 = None
+            try:
+                bf16 = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])
+            except Exception:
+                pass
+            peak = 2 * bf16 if bf16 else 2 * 1590.0
+            pipe_roofline["match"] = {
+                "bound": "tensor", "achieved": tops, "peak": peak, "unit": "TOP/s (int8)", "frac": tops / peak,
+                "peak_source": ("2 x measured bf16 burst GEMM peak (MEASURED_PEAKS.json); nominal int8 dense 4500"
+                                if bf16 else "2 x fallback bf16 peak"),
+                "includes": "bit->int8 expansion of both sets, the GEMM + top-2 epilogue, and the split merge",
+            }
+        else:
+            popc = {0: 16, 1: 9, 2: 7}[mv]
+            popc_peak = pipes.get("popc_gops", sms * 16 * sm_mhz * 1e6 / 1e9)
+            pipe_roofline["match"] = {
+                "bound": "popc (XU pipe)", "achieved_gops": cps * popc / 1e9, "peak_gops": popc_peak,
+                "frac": cps * popc / 1e9 / popc_peak, "popc_per_compare": popc,
+                "peak_source": "measured microbench (profiles/pipe_peaks.json)" if pipes else
+                               f"theoretical: {sms} SMs x 16 POPC/clk at the sampled {sm_mhz:.0f} MHz",
+            }
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     roofline = {
         "kernel": dom, "bound": "hbm", "achieved": kernels[dom]["hbm"]["achieved"], "peak": peaks["hbm_gbs"],
         "unit": "GB/s", "frac": kernels[dom]["hbm"]["achieved"] / peaks["hbm_gbs"], "peak_source": peaks["source"],
-        "traffic": None,
-        "note": "neither kernel is HBM-bound (SURVEY.md §8d): see 'pipe_roofline' for the binding pipes",
+        "traffic": TRAFFIC_NCU.get(dom),
+        "note": "contract form (algorithmic HBM bytes / kernel time). Neither kernel is HBM-bound "
+                "(SURVEY.md 8d): the binding resources and their fractions are in 'pipe_roofline'",
     }
-    sm_mhz = clocks.summary()["sm_mhz"] or 1965.0
-    sms = eng.sm_count
-    pipes = peaks.get("pipes", {})
-    pipe_roofline = {}
-    if "extract_fast_kernel<u8>" in kernels:
-        k = kernels["extract_fast_kernel<u8>"]
-        smem_peak = pipes.get("lds64_gbs", sms * 128 * sm_mhz * 1e6 / 1e9)
-        fp64_peak = pipes.get("fp64_nonfused_gops", sms * 64 * sm_mhz * 1e6 / 1e9)
-        pipe_roofline["extract"] = {
-            "smem": {"achieved_gbs": k["smem_gbs"], "peak_gbs": smem_peak, "frac": k["smem_gbs"] / smem_peak},
-            "fp64": {"achieved_gops": k["fp64_gops"], "peak_gops": fp64_peak, "frac": k["fp64_gops"] / fp64_peak},
-            "peak_source": "measured microbench (profiles/pipe_peaks.json)" if pipes else
-                           f"theoretical: {sms} SMs x 128 B/clk and x 64 lanes/clk at the sampled {sm_mhz:.0f} MHz",
-        }
-    if "match64_kernel" in kernels:
-        k = kernels["match64_kernel"]
-        popc_peak = pipes.get("popc_gops", sms * 16 * sm_mhz * 1e6 / 1e9)
-        pipe_roofline["match"] = {
-            "popc": {"achieved_gops": k["popc_gops"], "peak_gops": popc_peak, "frac": k["popc_gops"] / popc_peak},
-            "peak_source": "measured microbench (profiles/pipe_peaks.json)" if pipes else
-                           f"theoretical: {sms} SMs x 16 POPC/clk at the sampled {sm_mhz:.0f} MHz",
-        }
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

@@ -83,8 +83,10 @@ def describe(image, keypoints, pattern=None, workers=0):
     eng = get_engine()
     eng.set_pattern(pat)
     kept, desc = eng.describe_all(img, kps, workers)
+    if kps.shape[1] == 4:
+        return kps.take(kept, axis=0), desc
     full = np.zeros((len(kept), 4), np.float64)
-    full[:, :kps.shape[1]] = kps[kept]
+    full[:, :kps.shape[1]] = kps.take(kept, axis=0)
     return full, desc
 
 

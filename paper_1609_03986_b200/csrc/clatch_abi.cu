@@ -7,6 +7,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 
 #include "clatch_internal.cuh"
@@ -44,6 +47,76 @@ void DeviceBuffer::release() {
 }
 
 namespace {
+
+// Persistent host workers for the trig pass: spawning std::threads per call (what the
+// reference's parallel_for does, src/parallel.hpp:26-37) costs more than the work itself at
+// 10 k keypoints.
+class WorkerPool {
+public:
+    static WorkerPool& instance() {
+        static WorkerPool pool;
+        return pool;
+    }
+    // Runs fn(i) for i in [0, parts) on up to `parts` threads (the caller takes part 0).
+    void run(int parts, const std::function<void(int)>& fn) {
+        if (parts <= 1) {
+            fn(0);
+            return;
+        }
+        std::unique_lock<std::mutex> call_lock(call_mutex_);   // one parallel region at a time
+        ensure(parts - 1);
+        {
+            std::lock_guard<std::mutex> lock(mutex_);
+            fn_ = &fn;
+            next_ = 1;
+            parts_ = parts;
+            pending_ = parts - 1;
+        }
+        wake_.notify_all();
+        fn(0);
+        std::unique_lock<std::mutex> lock(mutex_);
+        done_.wait(lock, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+private:
+    WorkerPool() = default;
+    ~WorkerPool() {
+        {
+            std::lock_guard<std::mutex> lock(mutex_);
+            stop_ = true;
+        }
+        wake_.notify_all();
+        for (std::thread& t : threads_) t.join();
+    }
+    void ensure(int n) {
+        while (static_cast<int>(threads_.size()) < n) threads_.emplace_back([this] { loop(); });
+    }
+    void loop() {
+        for (;;) {
+            int part = -1;
+            const std::function<void(int)>* fn = nullptr;
+            {
+                std::unique_lock<std::mutex> lock(mutex_);
+                wake_.wait(lock, [&] { return stop_ || next_ < parts_; });
+                if (stop_) return;
+                part = next_++;
+                fn = fn_;
+            }
+            (*fn)(part);
+            {
+                std::lock_guard<std::mutex> lock(mutex_);
+                if (--pending_ == 0) done_.notify_all();
+            }
+        }
+    }
+    std::mutex call_mutex_, mutex_;
+    std::condition_variable wake_, done_;
+    std::vector<std::thread> threads_;
+    const std::function<void(int)>* fn_ = nullptr;
+    int next_ = 0, parts_ = 0, pending_ = 0;
+    bool stop_ = false;
+};
 
 int invalid(const std::string& msg) {
     set_error(msg);
@@ -249,7 +322,7 @@ int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, i
     *m = count;
     if (count == 0) return CLATCH_OK;
     // cos/sin of extract_window (src/descriptor.cpp:35-36) through the host libm.
-    int nthreads = std::min<size_t>(resolve_workers(workers), (count + 4095) / 4096);
+    int nthreads = std::min<size_t>(resolve_workers(workers), (count + 1023) / 1024);
     nthreads = std::max(nthreads, 1);
     std::vector<int> bad(nthreads, 0);
     auto work = [&](int w) {
@@ -266,13 +339,7 @@ int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, i
             xycs[4 * j + 3] = s;
         }
     };
-    if (nthreads == 1) {
-        work(0);
-    } else {
-        std::vector<std::thread> pool;
-        for (int w = 0; w < nthreads; ++w) pool.emplace_back(work, w);
-        for (std::thread& t : pool) t.join();
-    }
+    WorkerPool::instance().run(nthreads, work);
     for (int b : bad)
         if (b) {
             set_error("a keypoint inside the margin has a non-finite orientation");

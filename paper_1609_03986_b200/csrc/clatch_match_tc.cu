@@ -354,13 +354,25 @@ int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
         ++ctx->launches;
     }
     CLATCH_CUDA(cudaGetLastError());
-    // Splits: aim for a whole number of waves of one CTA per SM; never more splits than tiles.
-    size_t splits = 1;
-    if (qtiles < static_cast<size_t>(ctx->sm_count)) splits = std::max<size_t>(1, ctx->sm_count / qtiles);
-    splits = std::min(splits, ttiles);
-    splits = std::min<size_t>(splits, 65535);
-    const size_t per_split = (ttiles + splits - 1) / splits;
-    splits = (ttiles + per_split - 1) / per_split;
+    // Split the train range over blockIdx.y when there are too few query tiles to fill the
+    // SMs. Model: CTAs run in waves of one per SM; a CTA costs (tiles + kOverhead) tile-times
+    // (barrier init, TMEM allocation, 64 KiB A load, pipeline fill, merge). Pick the split count with the smallest makespan.
+    size_t best_splits = 1, best_per = ttiles;
+    {
+        const size_t sms = static_cast<size_t>(ctx->sm_count), kOverhead = 8;   // measured: ~8 us of fixed cost per CTA vs ~1 us per tile
+        size_t best_cost = ~static_cast<size_t>(0);
+        for (size_t s = 1; s <= std::min<size_t>(ttiles, 64); ++s) {
+            const size_t per = (ttiles + s - 1) / s, actual = (ttiles + per - 1) / per;
+            const size_t waves = (qtiles * actual + sms - 1) / sms;
+            const size_t cost = waves * (per + kOverhead);
+            if (cost < best_cost) {
+                best_cost = cost;
+                best_splits = actual;
+                best_per = per;
+            }
+        }
+    }
+    const size_t splits = best_splits, per_split = best_per;
     if (int rc = ctx->partial.reserve(sizeof(Partial) * splits * Q)) return rc;
     dim3 grid(static_cast<unsigned>(qtiles), static_cast<unsigned>(splits));
     match_tc_kernel<<<grid, kTcThreads, kTcSmemBytes, stream>>>(ctx->exp_q.as<uint8_t>(), ctx->exp_t.as<uint8_t>(), Q,

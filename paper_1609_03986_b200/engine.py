@@ -53,13 +53,16 @@ class Engine:
     # ---- pattern ---------------------------------------------------------
     def set_pattern(self, pattern: TripletPattern | None = None) -> TripletPattern:
         pattern = pattern or default_pattern()
+        if pattern is self._pattern:
+            return pattern
         key = pattern.key()
         if key != self._pattern_key:
             trip = np.ascontiguousarray(pattern.triplets, np.int16)
             w = np.ascontiguousarray(pattern.weights, np.float64)
             _lib.check(self.lib.clatch_set_pattern(self.ctx, _ptr(trip, i16p), pattern.bit_count,
                                                    pattern.patch_size, _ptr(w, f64p)))
-            self._pattern_key, self._pattern = key, pattern
+            self._pattern_key = key
+        self._pattern = pattern
         return pattern
 
     @property

@@ -37,7 +37,11 @@ class TripletPattern:
         return self.bit_count // 8
 
     def key(self):
-        return (self.bit_count, self.patch_size, self.triplets.tobytes(), self.weights.tobytes())
+        k = self.__dict__.get("_key")
+        if k is None:
+            k = (self.bit_count, self.patch_size, self.triplets.tobytes(), self.weights.tobytes())
+            object.__setattr__(self, "_key", k)
+        return k
 
 
 def _scan_ints(line: str, want: int):

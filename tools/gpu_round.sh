@@ -22,7 +22,7 @@ done
 for v in 0 1 2 3; do
   echo "== matcher variant $v"
   timeout 300 python bench.py --steps 20 --warmup 5 --phase match --no-cpu-baseline --match-variant $v > "$OUT/bench_match_v$v.json" 2>> "$OUT/bench.err"
-  python -c "import json;d=json.load(open('$OUT/bench_match_v$v.json'));print('variant $v compares/s', d['compares_per_s'], 'ms', d['kernels']['match64_kernel']['ms'])"
+  python -c "import json;d=json.load(open('$OUT/bench_match_v$v.json'));print('variant $v compares/s', d['compares_per_s'], 'ms', list(d['kernels'].values())[0]['ms'])"
 done
 fi
 echo "== bench reference"; timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"; cat "$OUT/bench_reference.json"
@@ -31,7 +31,7 @@ echo "== ncu launch list"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$OUT/ncu_launches.log" 2>&1
 echo "== ncu full: extraction"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:extract_ -s 3 -c 1 -f -o "$OUT/prof_extract" \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:extract_quad -s 3 -c 1 -f -o "$OUT/prof_extract" \
     python bench.py --steps 2 --warmup 3 --phase extract --no-cpu-baseline > "$OUT/ncu_extract.log" 2>&1
 echo "== ncu full: tensor-core matching"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_tc -s 3 -c 1 -f -o "$OUT/prof_match_tc" \
