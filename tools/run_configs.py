@@ -1,0 +1,121 @@
+#!/usr/bin/env python
+"""BASELINE.json configs 3-5 at their one-GPU share, with parity spot checks against the
+oracle. Writes one JSON object (stdout) for profiles/."""
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import oracle                                        # noqa: E402
+import paper_1609_03986_b200 as lk                   # noqa: E402
+
+port = oracle.port()
+eng = lk.get_engine()
+eng.set_pattern(None)
+out = {"device": eng.name}
+
+
+def sync():
+    torch.cuda.synchronize()
+
+
+# ---- cfg3: 64 images 3840x2160 x 50k keypoints, sharded by image over 8 GPUs -> 8 images here
+W, H, N_KP, IMAGES = 3840, 2160, 50_000, 8
+t_gen = time.perf_counter()
+imgs = [port.random_image_u8(30000 + i, W, H) for i in range(IMAGES)]
+kps = [port.random_keypoints(31000 + i, W, H, N_KP) for i in range(IMAGES)]
+out["cfg3_gen_s"] = time.perf_counter() - t_gen
+lk.describe(imgs[0], kps[0])                                   # warm-up
+sync()
+t0 = time.perf_counter()
+res = [lk.describe(im, k) for im, k in zip(imgs, kps)]
+t_e2e = time.perf_counter() - t0
+total = sum(len(r[1]) for r in res)
+# device-resident: kernel only
+d_img = torch.from_numpy(imgs[0]).cuda()
+xycs, kept = eng.prepare_keypoints(kps[0], W, H)
+d_x = torch.from_numpy(xycs).cuda()
+d_out = eng.extract_device(d_img, d_x)
+sync()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    eng.extract_device(d_img, d_x, out=d_out)
+e1.record()
+sync()
+ms_kernel = e0.elapsed_time(e1) / 5
+# parity: first 200 descriptors of two images against the oracle
+ok = True
+for i in (0, IMAGES - 1):
+    want = port.describe_all(imgs[i].astype(np.float64), kps[i][:200])[1]
+    ok &= bool(np.array_equal(res[i][1][:len(want)], want))
+out["cfg3"] = {"images": IMAGES, "shape": [W, H], "keypoints_per_image": N_KP, "descriptors": total,
+               "e2e_descriptors_per_s": total / t_e2e, "e2e_s": t_e2e,
+               "kernel_ms_per_image": ms_kernel, "kernel_descriptors_per_s": len(xycs) / ms_kernel * 1e3,
+               "parity_200_desc_x2_images": ok,
+               "note": "one GPU's share (8 of 64 images) of the 8-GPU config; u8 images through lk.describe"}
+print("cfg3", out["cfg3"], file=sys.stderr, flush=True)
+del imgs, res
+
+# ---- cfg4: 1M x 1M single large match (one GPU does all queries here; 8 GPUs shard queries)
+QN = 1_000_000
+q = port.random_descriptors(41, QN, 64)
+t = port.random_descriptors(42, QN, 64)
+rng = np.random.default_rng(4)
+dup_q = rng.choice(QN, QN // 100, replace=False)               # 1 % of queries are exact copies of train rows
+src_t = rng.integers(0, QN, len(dup_q))
+q[dup_q] = t[src_t]
+dup_t = rng.choice(QN, QN // 1000, replace=False)              # 0.1 % duplicated train rows (ties)
+t[dup_t] = t[(dup_t * 7 + 3) % QN]
+dq, dt = torch.from_numpy(q).cuda(), torch.from_numpy(t).cuda()
+r = eng.match_top2_device(dq[:4096], dt)                       # warm-up
+sync()
+e0.record()
+r = eng.match_top2_device(dq, dt)
+e1.record()
+sync()
+ms = e0.elapsed_time(e1)
+r = r.cpu().numpy()
+rows = np.unique(np.r_[dup_q[:16], rng.integers(0, QN, 32)])
+want = port.knn2_all(q[rows], t)
+exact = bool(np.array_equal(r[:, rows].T, want))
+kept = eng.filter_matches(r[0], r[1], r[2], ratio=0.8)
+out["cfg4"] = {"Q": QN, "N": QN, "ms": ms, "compares_per_s": QN * QN / ms * 1e3,
+               "sampled_rows_exact_vs_oracle": exact, "rows_checked": int(len(rows)),
+               "planted_copies_found": int((r[1][dup_q] == 0).sum()), "planted": int(len(dup_q)),
+               "ratio_0.8_matches": int(len(kept)),
+               "note": "all 1M queries on one GPU; with 8 GPUs each rank takes 125k queries after one broadcast"}
+print("cfg4", out["cfg4"], file=sys.stderr, flush=True)
+del dq, dt, q, t
+
+# ---- cfg5: exhaustive pairwise matching, 256 images x 8k keypoints -> 16 images / 120 pairs here
+IM5, KP5 = 16, 8000
+sets = []
+for i in range(IM5):
+    im = port.random_image_u8(50000 + i, 1920, 1080)
+    kp = port.random_keypoints(51000 + i, 1920, 1080, KP5)
+    sets.append(lk.describe(im, kp)[1])
+dsets = [torch.from_numpy(s).cuda() for s in sets]
+pairs = [(i, j) for i in range(IM5) for j in range(i + 1, IM5)]
+from paper_1609_03986_b200.sharded import default_match_pair   # noqa: E402
+run = default_match_pair(ratio=0.8, cross_check=True)
+run(0, 1, dsets[0], dsets[1])
+sync()
+t0 = time.perf_counter()
+results = {p: run(p[0], p[1], dsets[p[0]], dsets[p[1]]) for p in pairs}
+sync()
+t_pairs = time.perf_counter() - t0
+ok5 = True
+for p in (pairs[0], pairs[-1]):
+    ok5 &= bool(np.array_equal(results[p], port.match(sets[p[0]], sets[p[1]], ratio=0.8, cross_check=True)))
+compares = len(pairs) * KP5 * KP5 * 2
+out["cfg5"] = {"images": IM5, "keypoints": KP5, "pairs": len(pairs), "s": t_pairs, "pairs_per_s": len(pairs) / t_pairs,
+               "compares_per_s_incl_cross_check": compares / t_pairs, "two_pairs_exact_vs_oracle": ok5,
+               "note": "ratio 0.8 + cross-check per pair (two top-2 passes), host filter pass, device-resident sets"}
+print("cfg5", out["cfg5"], file=sys.stderr, flush=True)
+print(json.dumps(out))
