@@ -169,6 +169,36 @@ CLATCH_API int clatch_match_brute_force(clatch_ctx* ctx, const uint8_t* probes, 
                              double ratio, int cross_check, int has_max, int max_distance,
                              int32_t* out, size_t* count);
 
+/* ---- device-resident descriptor sets (64-byte descriptors) -----------------------------
+ * A set owns a device copy of n descriptors plus the int8 operand forms the tensor-core
+ * matcher consumes, so that extraction output can feed any number of matches without
+ * going back to the host and without being re-expanded (the SfM-style "every image against
+ * every other image" workload; the reference has no counterpart — it re-reads
+ * std::vector<Descriptor> per call, src/match.cpp:52-67).
+ * `descriptors` is host memory (on_device = 0) or device memory on the context's device
+ * (on_device = 1); it is copied, the caller keeps ownership. */
+typedef struct clatch_set clatch_set;
+CLATCH_API int clatch_set_create(clatch_ctx* ctx, const uint8_t* descriptors, size_t n, int on_device, clatch_set** out);
+CLATCH_API void clatch_set_destroy(clatch_set* set);
+CLATCH_API size_t clatch_set_count(const clatch_set* set);
+
+/* match_brute_force (src/match.cpp:52-81) between two resident sets; same outputs as
+ * clatch_match_brute_force. */
+CLATCH_API int clatch_match_sets(clatch_ctx* ctx, const clatch_set* probes, const clatch_set* gallery, int has_ratio,
+                      double ratio, int cross_check, int has_max, int max_distance, int32_t* out,
+                      size_t* count);
+
+/* Batched form: pairs[2*p], pairs[2*p+1] index `sets`; pair p matches sets[pairs[2p]] (probes)
+ * against sets[pairs[2p+1]] (gallery) with the given filters. All pairs (and, with
+ * cross_check, their reverse passes) run in as few kernel launches as memory allows. The
+ * accepted rows {probe, gallery, distance, second_distance} of all pairs are concatenated in
+ * `out` (room for cap_rows rows); pair p owns rows [offsets[p], offsets[p+1]). Fails with
+ * CLATCH_ERR_INVALID if cap_rows is too small, CLATCH_ERR_EMPTY_GALLERY on an empty gallery. */
+CLATCH_API int clatch_match_set_pairs(clatch_ctx* ctx, const clatch_set* const* sets, size_t num_sets,
+                           const int32_t* pairs, size_t num_pairs, int has_ratio, double ratio,
+                           int cross_check, int has_max, int max_distance, int32_t* out, size_t cap_rows,
+                           size_t* offsets);
+
 /* Diagnostic for the tensor-core matcher: runs it on host buffers and also returns the raw
  * int32 accumulators of the first 128-query x 256-train tile (row-major 128 x 256; entry
  * (i, j) must equal 512 - 2 * hamming(query i, train j) for i < Q, j < N). */

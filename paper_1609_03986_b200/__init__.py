@@ -14,7 +14,7 @@ from __future__ import annotations
 import numpy as np
 
 from ._lib import ClatchDeviceError, LatchError
-from .engine import Engine, get_engine
+from .engine import DescriptorSet, Engine, get_engine
 from .pattern import (TripletPattern, default_pattern as _default_pattern, default_pattern_text,
                       format_pattern, parse_pattern, pattern_from_text)
 
@@ -26,7 +26,7 @@ orientation_radius = 15
 
 __all__ = [
     "default_pattern", "describe", "descriptor_bits", "descriptor_bytes", "hamming", "match",
-    "orientation_radius", "window_margin", "Engine", "get_engine", "LatchError",
+    "orientation_radius", "window_margin", "Engine", "DescriptorSet", "get_engine", "LatchError",
     "ClatchDeviceError", "TripletPattern", "parse_pattern", "format_pattern",
 ]
 

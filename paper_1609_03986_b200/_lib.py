@@ -77,6 +77,13 @@ _SIGNATURES = {
                                         C.c_int, i32p, i32p, szp]),
     "clatch_match_brute_force": (C.c_int, [C.c_void_p, u8p, C.c_size_t, u8p, C.c_size_t, C.c_int,
                                            C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, i32p, szp]),
+    "clatch_set_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.POINTER(C.c_void_p)]),
+    "clatch_set_destroy": (None, [C.c_void_p]),
+    "clatch_set_count": (C.c_size_t, [C.c_void_p]),
+    "clatch_match_sets": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int,
+                                    C.c_int, i32p, szp]),
+    "clatch_match_set_pairs": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_size_t, i32p, C.c_size_t, C.c_int,
+                                         C.c_double, C.c_int, C.c_int, C.c_int, i32p, C.c_size_t, szp]),
     "clatch_debug_tc_tile": (C.c_int, [C.c_void_p, u8p, C.c_size_t, u8p, C.c_size_t, i32p, i32p, i32p, i32p]),
     "clatch_launch_count": (C.c_uint64, [C.c_void_p]),
 }

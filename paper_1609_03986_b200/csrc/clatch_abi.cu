@@ -192,7 +192,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
         cudaStreamDestroy(ctx->stream);
     }
     for (DeviceBuffer* b : {&ctx->img, &ctx->kps, &ctx->desc, &ctx->q, &ctx->t, &ctx->res,
-                            &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->pattern.slots, &ctx->pattern.slots_quad,
+                            &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->items, &ctx->pattern.slots, &ctx->pattern.slots_quad,
                             &ctx->pattern.triplets})
         b->release();
     delete ctx;
@@ -533,6 +533,181 @@ int clatch_match_top2(clatch_ctx* ctx, const uint8_t* queries, size_t Q, const u
     if (second_dist)
         CLATCH_CUDA(cudaMemcpyAsync(second_dist, r + 2 * Q, sizeof(int32_t) * Q, cudaMemcpyDeviceToHost, st));
     CLATCH_CUDA(cudaStreamSynchronize(st));
+    return CLATCH_OK;
+}
+
+} // extern "C"
+
+struct clatch_set {
+    clatch_ctx* ctx = nullptr;
+    size_t n = 0;
+    DeviceBuffer packed, exp_a, exp_b;
+};
+
+namespace {
+
+// Forward (+ reverse) top-2 of a batch of set pairs in one launch, results to `host`:
+// per pair [best_idx n_i][best_dist n_i][second n_i][reverse_best n_j if cross_check].
+int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t* pairs, size_t first, size_t count,
+                   bool cross_check, std::vector<int32_t>& host, std::vector<size_t>& pair_offset) {
+    pair_offset.assign(count + 1, 0);
+    size_t items = 0;
+    for (size_t p = 0; p < count; ++p) {
+        const clatch_set* a = sets[pairs[2 * (first + p)]];
+        const clatch_set* b = sets[pairs[2 * (first + p) + 1]];
+        pair_offset[p + 1] = pair_offset[p] + 3 * a->n + (cross_check ? b->n : 0);
+        items += tc_query_tiles(a->n) + (cross_check ? tc_query_tiles(b->n) : 0);
+    }
+    const size_t total = pair_offset[count];
+    if (int rc = ctx->res.reserve(sizeof(int32_t) * std::max<size_t>(total, 1))) return rc;
+    if (int rc = ctx->items.reserve(sizeof(TcItem) * std::max<size_t>(items, 1))) return rc;
+    int32_t* r = ctx->res.as<int32_t>();
+    std::vector<TcItem> table;
+    table.reserve(items);
+    for (size_t p = 0; p < count; ++p) {
+        const clatch_set* a = sets[pairs[2 * (first + p)]];
+        const clatch_set* b = sets[pairs[2 * (first + p) + 1]];
+        int32_t* base = r + pair_offset[p];
+        for (int q = 0; q < tc_query_tiles(a->n); ++q)
+            table.push_back({a->exp_a.as<uint8_t>(), b->exp_b.as<uint8_t>(), static_cast<unsigned>(a->n),
+                             static_cast<unsigned>(b->n), static_cast<unsigned>(q), 0, base, base + a->n,
+                             base + 2 * a->n});
+        if (cross_check)   // reverse_best[g] = knn2(gallery[g], probes).best_index, src/match.cpp:62-67
+            for (int q = 0; q < tc_query_tiles(b->n); ++q)
+                table.push_back({b->exp_a.as<uint8_t>(), a->exp_b.as<uint8_t>(), static_cast<unsigned>(b->n),
+                                 static_cast<unsigned>(a->n), static_cast<unsigned>(q), 0, base + 3 * a->n, nullptr,
+                                 nullptr});
+    }
+    cudaStream_t st = ctx->stream;
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->items.ptr, table.data(), sizeof(TcItem) * table.size(), cudaMemcpyHostToDevice, st));
+    if (int rc = launch_match_tc_items(ctx, ctx->items.as<TcItem>(), table.size(), st)) return rc;
+    host.resize(total);
+    CLATCH_CUDA(cudaMemcpyAsync(host.data(), r, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));   // also keeps `table` alive until the H2D copy is done
+    return CLATCH_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int clatch_set_create(clatch_ctx* ctx, const uint8_t* descriptors, size_t n, int on_device, clatch_set** out) {
+    if (!ctx || !out) return invalid("clatch_set_create: null argument");
+    *out = nullptr;
+    if (n > 0 && !descriptors) return invalid("clatch_set_create: null descriptors");
+    if (n > 0x7fffffffull) return invalid("clatch_set_create: too many descriptors");
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    auto* set = new clatch_set;
+    set->ctx = ctx;
+    set->n = n;
+    int rc = CLATCH_OK;
+    if (n > 0) {
+        cudaStream_t st = ctx->stream;
+        if (!rc) rc = set->packed.reserve(n * 64);
+        if (!rc) rc = set->exp_a.reserve(tc_expanded_bytes(n, true));
+        if (!rc) rc = set->exp_b.reserve(tc_expanded_bytes(n, false));
+        if (!rc) {
+            cudaError_t e = cudaMemcpyAsync(set->packed.ptr, descriptors, n * 64,
+                                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(set)");
+        }
+        if (!rc) rc = launch_tc_expand(ctx, set->packed.as<uint8_t>(), n, true, set->exp_a.as<uint8_t>(), st);
+        if (!rc) rc = launch_tc_expand(ctx, set->packed.as<uint8_t>(), n, false, set->exp_b.as<uint8_t>(), st);
+        if (!rc) {
+            cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) rc = cuda_fail(e, "cudaStreamSynchronize(set)");
+        }
+    }
+    if (rc) {
+        clatch_set_destroy(set);
+        return rc;
+    }
+    *out = set;
+    return CLATCH_OK;
+}
+
+void clatch_set_destroy(clatch_set* set) {
+    if (!set) return;
+    cudaSetDevice(set->ctx->device);
+    set->packed.release();
+    set->exp_a.release();
+    set->exp_b.release();
+    delete set;
+}
+
+size_t clatch_set_count(const clatch_set* set) { return set ? set->n : 0; }
+
+int clatch_match_set_pairs(clatch_ctx* ctx, const clatch_set* const* sets, size_t num_sets, const int32_t* pairs,
+                           size_t num_pairs, int has_ratio, double ratio, int cross_check, int has_max,
+                           int max_distance, int32_t* out, size_t cap_rows, size_t* offsets) {
+    if (!ctx || !offsets) return invalid("clatch_match_set_pairs: null argument");
+    offsets[0] = 0;
+    if (num_pairs == 0) return CLATCH_OK;
+    if (!sets || !pairs || !out) return invalid("clatch_match_set_pairs: null buffer");
+    for (size_t p = 0; p < num_pairs; ++p) {
+        const int32_t i = pairs[2 * p], j = pairs[2 * p + 1];
+        if (i < 0 || j < 0 || static_cast<size_t>(i) >= num_sets || static_cast<size_t>(j) >= num_sets || !sets[i] ||
+            !sets[j])
+            return invalid("clatch_match_set_pairs: pair index out of range");
+        if (sets[i]->ctx != ctx || sets[j]->ctx != ctx) return invalid("clatch_match_set_pairs: set from another context");
+        if (sets[j]->n == 0) {   // src/match.cpp:55
+            set_error("EmptyGallery: matching needs a nonempty gallery");
+            return CLATCH_ERR_EMPTY_GALLERY;
+        }
+    }
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    // Chunks bounded by result bytes (<= 256 MiB of top-2 triples per launch).
+    const size_t kChunkInts = (256u << 20) / sizeof(int32_t);
+    std::vector<int32_t> host;
+    std::vector<size_t> pair_offset;
+    size_t rows_out = 0;
+    for (size_t first = 0; first < num_pairs;) {
+        size_t count = 0, ints = 0;
+        while (first + count < num_pairs) {
+            const size_t need = 3 * sets[pairs[2 * (first + count)]]->n +
+                                (cross_check ? sets[pairs[2 * (first + count) + 1]]->n : 0);
+            if (count > 0 && ints + need > kChunkInts) break;
+            ints += need;
+            ++count;
+        }
+        if (int rc = run_pair_batch(ctx, sets, pairs, first, count, cross_check != 0, host, pair_offset)) return rc;
+        // filter pass per pair (src/match.cpp:69-79): parallel into per-pair scratch, then compact in order
+        std::vector<size_t> scratch_off(count + 1, 0), kept(count, 0);
+        for (size_t p = 0; p < count; ++p) scratch_off[p + 1] = scratch_off[p] + 4 * sets[pairs[2 * (first + p)]]->n;
+        std::vector<int32_t> scratch(std::max<size_t>(scratch_off[count], 1));
+        const int parts = static_cast<int>(std::min<size_t>(count, resolve_workers(0)));
+        WorkerPool::instance().run(parts, [&](int part) {
+            for (size_t p = part; p < count; p += parts) {
+                const size_t n = sets[pairs[2 * (first + p)]]->n;
+                const int32_t* base = host.data() + pair_offset[p];
+                clatch_filter_matches(base, base + n, base + 2 * n, n, has_ratio, ratio, has_max, max_distance,
+                                      cross_check ? base + 3 * n : nullptr, scratch.data() + scratch_off[p], &kept[p]);
+            }
+        });
+        for (size_t p = 0; p < count; ++p) {
+            if (rows_out + kept[p] > cap_rows) return invalid("clatch_match_set_pairs: cap_rows too small");
+            std::memcpy(out + 4 * rows_out, scratch.data() + scratch_off[p], sizeof(int32_t) * 4 * kept[p]);
+            rows_out += kept[p];
+            offsets[first + p + 1] = rows_out;
+        }
+        first += count;
+    }
+    return CLATCH_OK;
+}
+
+int clatch_match_sets(clatch_ctx* ctx, const clatch_set* probes, const clatch_set* gallery, int has_ratio,
+                      double ratio, int cross_check, int has_max, int max_distance, int32_t* out,
+                      size_t* count) {
+    if (!count) return invalid("clatch_match_sets: count is null");
+    *count = 0;
+    if (!ctx || !probes || !gallery) return invalid("clatch_match_sets: null argument");
+    const clatch_set* sets[2] = {probes, gallery};
+    const int32_t pair[2] = {0, 1};
+    size_t offsets[2] = {0, 0};
+    if (int rc = clatch_match_set_pairs(ctx, sets, 2, pair, 1, has_ratio, ratio, cross_check, has_max, max_distance,
+                                        out, probes->n, offsets))
+        return rc;
+    *count = offsets[1];
     return CLATCH_OK;
 }
 

@@ -150,9 +150,32 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
 // ---------------------------------------------------------------- the kernel ----
 // grid = (query tiles, splits). Split s owns train tiles [s*tiles_per_split, ...).
 __global__ void __launch_bounds__(kTcThreads, 1)
-match_tc_kernel(const uint8_t* __restrict__ a_exp, const uint8_t* __restrict__ b_exp, unsigned long long Q,
-                unsigned long long N, int total_tiles, int tiles_per_split, Partial* __restrict__ partial,
-                int* __restrict__ dump /* optional: raw accumulators of this CTA's first tile, 128 x 256 */) {
+match_tc_kernel(const uint8_t* __restrict__ a_exp_arg, const uint8_t* __restrict__ b_exp_arg, unsigned long long Q_arg,
+                unsigned long long N_arg, int total_tiles, int tiles_per_split, Partial* __restrict__ partial,
+                int* __restrict__ dump /* optional: raw accumulators of this CTA's first tile, 128 x 256 */,
+                const TcItem* __restrict__ items /* optional: one work item per CTA (batched set pairs) */) {
+    // Work of this CTA: either derived from (blockIdx.x = query tile, blockIdx.y = train split) or
+    // read from the item table (batched matching of many set pairs in one launch).
+    const uint8_t* a_exp = a_exp_arg;
+    const uint8_t* b_exp = b_exp_arg;
+    unsigned long long Q = Q_arg, N = N_arg;
+    unsigned qtile = blockIdx.x;
+    int tile_begin = blockIdx.y * tiles_per_split;
+    int tile_end = min(total_tiles, tile_begin + tiles_per_split);
+    int32_t *o_idx = nullptr, *o_best = nullptr, *o_second = nullptr;
+    if (items != nullptr) {
+        const TcItem it = items[blockIdx.x];
+        a_exp = it.a_exp;
+        b_exp = it.b_exp;
+        Q = it.Q;
+        N = it.N;
+        qtile = it.qtile;
+        tile_begin = 0;
+        tile_end = static_cast<int>((it.N + kTcN - 1) / kTcN);
+        o_idx = it.best_idx;
+        o_best = it.best_dist;
+        o_second = it.second_dist;
+    }
     extern __shared__ uint8_t smem_raw[];
     const unsigned raw = smem_u32(smem_raw);
     const unsigned base = (raw + 1023u) & ~1023u;              // SWIZZLE_128B atoms need 1024-B alignment
@@ -169,8 +192,6 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp, const uint8_t* __restrict__ b
     int* merge_buf = reinterpret_cast<int*>(gen_base);         // reused after the main loop (A region)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile_begin = blockIdx.y * tiles_per_split;
-    const int tile_end = min(total_tiles, tile_begin + tiles_per_split);
     const int ntiles = tile_end - tile_begin;
 
     if (threadIdx.x == 0) {
@@ -199,7 +220,7 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp, const uint8_t* __restrict__ b
         // ===== producer =====
         if (lane == 0) {
             mbar_expect_tx(bar_a, kTcABytes);
-            bulk_load(smem_a, a_exp + static_cast<unsigned long long>(blockIdx.x) * kTcABytes, kTcABytes, bar_a);
+            bulk_load(smem_a, a_exp + static_cast<unsigned long long>(qtile) * kTcABytes, kTcABytes, bar_a);
             int stage = 0;
             unsigned phase = 0;
             for (int t = 0; t < ntiles; ++t) {
@@ -256,7 +277,7 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp, const uint8_t* __restrict__ b
             for (int chunk = 0; chunk < 4; ++chunk) {
                 int v[32];
                 tmem_ld32(tmem_base + lane_addr + buf * kTcN + half * 128 + chunk * 32, v);
-                if (dump != nullptr && t == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+                if (dump != nullptr && t == 0 && qtile == 0 && blockIdx.y == 0) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
                         dump[(quarter * 32 + lane) * kTcN + half * 128 + chunk * 32 + i] = v[i];
@@ -308,14 +329,23 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp, const uint8_t* __restrict__ b
             } else {
                 second = max(second, ob);
             }
-            const unsigned long long qi = static_cast<unsigned long long>(blockIdx.x) * kTcM + row;
+            const unsigned long long qi = static_cast<unsigned long long>(qtile) * kTcM + row;
             if (qi < Q) {
-                Partial r;
-                r.best_idx = best_idx < 0 ? -1 : tile_begin * kTcN + best_idx;
-                r.best_dist = best == INT_MIN ? 513 : (512 - best) >> 1;
-                r.second_dist = second == INT_MIN ? 513 : (512 - second) >> 1;
-                r.pad = 0;
-                partial[static_cast<unsigned long long>(blockIdx.y) * Q + qi] = r;
+                const int idx = best_idx < 0 ? -1 : tile_begin * kTcN + best_idx;
+                const int bd = best == INT_MIN ? 513 : (512 - best) >> 1;
+                const int sd = second == INT_MIN ? 513 : (512 - second) >> 1;
+                if (items != nullptr) {          // whole train range seen: these are final
+                    if (o_idx) o_idx[qi] = idx;
+                    if (o_best) o_best[qi] = bd;
+                    if (o_second) o_second[qi] = sd;
+                } else {
+                    Partial r;
+                    r.best_idx = idx;
+                    r.best_dist = bd;
+                    r.second_dist = sd;
+                    r.pad = 0;
+                    partial[static_cast<unsigned long long>(blockIdx.y) * Q + qi] = r;
+                }
             }
         }
     }
@@ -330,14 +360,48 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp, const uint8_t* __restrict__ b
 
 } // namespace
 
-int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
-                         int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
-                         int32_t* d_dump) {
+static int configure_tc() {
     static bool configured = false;
     if (!configured) {
         CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemBytes));
         configured = true;
     }
+    return CLATCH_OK;
+}
+
+size_t tc_expanded_bytes(size_t rows, bool as_queries) {
+    return as_queries ? (rows + kTcM - 1) / kTcM * kTcABytes
+                      : (rows + kTcN - 1) / kTcN * (kTcKBlocks * kTcStageBytes);
+}
+
+int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, bool as_queries, uint8_t* d_out,
+                     cudaStream_t stream) {
+    const int rows_per_tile = as_queries ? kTcM : kTcN;
+    const unsigned long long rows = (n + rows_per_tile - 1) / rows_per_tile * rows_per_tile, threads = rows * 32;
+    if (rows == 0) return CLATCH_OK;
+    expand_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(d_packed, n, rows, rows_per_tile,
+                                                                                    d_out);
+    ++ctx->launches;
+    CLATCH_CUDA(cudaGetLastError());
+    return CLATCH_OK;
+}
+
+int tc_query_tiles(size_t rows) { return static_cast<int>((rows + kTcM - 1) / kTcM); }
+
+int launch_match_tc_items(clatch_ctx* ctx, const TcItem* d_items, size_t count, cudaStream_t stream) {
+    if (count == 0) return CLATCH_OK;
+    if (int rc = configure_tc()) return rc;
+    match_tc_kernel<<<static_cast<unsigned>(count), kTcThreads, kTcSmemBytes, stream>>>(nullptr, nullptr, 0, 0, 0, 0,
+                                                                                      nullptr, nullptr, d_items);
+    ++ctx->launches;
+    CLATCH_CUDA(cudaGetLastError());
+    return CLATCH_OK;
+}
+
+int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
+                         int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
+                         int32_t* d_dump) {
+    if (int rc = configure_tc()) return rc;
     const size_t qtiles = (Q + kTcM - 1) / kTcM, ttiles = (N + kTcN - 1) / kTcN;
     if (int rc = ctx->exp_q.reserve(qtiles * kTcABytes)) return rc;
     if (int rc = ctx->exp_t.reserve(ttiles * kTcKBlocks * kTcStageBytes)) return rc;
@@ -378,7 +442,7 @@ int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
     match_tc_kernel<<<grid, kTcThreads, kTcSmemBytes, stream>>>(ctx->exp_q.as<uint8_t>(), ctx->exp_t.as<uint8_t>(), Q,
                                                                 N, static_cast<int>(ttiles),
                                                                 static_cast<int>(per_split),
-                                                                ctx->partial.as<Partial>(), d_dump);
+                                                                ctx->partial.as<Partial>(), d_dump, nullptr);
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
     launch_merge_partials(ctx->partial.as<Partial>(), Q, static_cast<int>(splits), 513, d_best_idx, d_best_dist, d_second, stream);

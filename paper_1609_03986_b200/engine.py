@@ -22,6 +22,28 @@ def _ptr(a: np.ndarray, t):
     return a.ctypes.data_as(t)
 
 
+class DescriptorSet:
+    """Device-resident set of 64-byte descriptors (clatch_set): uploaded / copied once, kept with
+    its tensor-core operand forms, reusable across any number of matches."""
+
+    def __init__(self, engine: "Engine", handle, count: int):
+        self.engine, self.handle, self.count = engine, handle, count
+
+    def __len__(self):
+        return self.count
+
+    def close(self):
+        if self.handle:
+            self.engine.lib.clatch_set_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Engine:
     def __init__(self, device: int | None = None):
         self.lib = _lib.load()
@@ -204,6 +226,58 @@ class Engine:
             int(max_distance) if max_distance is not None else 0,
             None if rb is None else _ptr(rb, i32p), _ptr(out, i32p), C.byref(count)))
         return out[:count.value].copy()
+
+    # ---- resident descriptor sets ----------------------------------------------------
+    def create_set(self, descriptors) -> DescriptorSet:
+        """descriptors: (N, 64) uint8 numpy array (uploaded) or torch CUDA tensor (copied on device)."""
+        handle = C.c_void_p()
+        if isinstance(descriptors, np.ndarray):
+            d = np.ascontiguousarray(descriptors, np.uint8)
+            if d.ndim != 2 or d.shape[1] != 64:
+                raise ValueError("descriptor sets hold (N, 64) uint8 rows")
+            with self._lock:
+                rc = self.lib.clatch_set_create(self.ctx, d.ctypes.data, len(d), 0, C.byref(handle))
+            n = len(d)
+        else:
+            import torch
+            d = descriptors.contiguous()
+            if d.dim() != 2 or d.shape[1] != 64 or d.dtype != torch.uint8 or not d.is_cuda:
+                raise ValueError("descriptor sets hold (N, 64) uint8 rows")
+            torch.cuda.current_stream(d.device).synchronize()   # the copy runs on the context's stream
+            with self._lock:
+                rc = self.lib.clatch_set_create(self.ctx, d.data_ptr(), d.shape[0], 1, C.byref(handle))
+            n = d.shape[0]
+        _lib.check(rc)
+        return DescriptorSet(self, handle, n)
+
+    def match_sets(self, probes: DescriptorSet, gallery: DescriptorSet, ratio=None, cross_check=False,
+                   max_distance=None) -> np.ndarray:
+        out = np.empty((max(len(probes), 1), 4), np.int32)
+        count = C.c_size_t()
+        with self._lock:
+            rc = self.lib.clatch_match_sets(
+                self.ctx, probes.handle, gallery.handle, int(ratio is not None),
+                float(ratio) if ratio is not None else 0.0, int(cross_check), int(max_distance is not None),
+                int(max_distance) if max_distance is not None else 0, _ptr(out, i32p), C.byref(count))
+        _lib.check(rc)
+        return out[:count.value].copy()
+
+    def match_set_pairs(self, sets, pairs, ratio=None, cross_check=False, max_distance=None):
+        """All (probe set, gallery set) index pairs in as few launches as memory allows.
+        -> list of (M_p, 4) int32 arrays, one per pair, in the order given."""
+        pairs = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+        handles = (C.c_void_p * len(sets))(*[s.handle for s in sets])
+        cap = int(sum(len(sets[i]) for i in pairs[:, 0])) if len(pairs) else 0
+        out = np.empty((max(cap, 1), 4), np.int32)
+        offsets = np.zeros(len(pairs) + 1, np.uintp)
+        with self._lock:
+            rc = self.lib.clatch_match_set_pairs(
+                self.ctx, handles, len(sets), _ptr(pairs, i32p), len(pairs), int(ratio is not None),
+                float(ratio) if ratio is not None else 0.0, int(cross_check), int(max_distance is not None),
+                int(max_distance) if max_distance is not None else 0, _ptr(out, i32p), cap,
+                offsets.ctypes.data_as(_lib.szp))
+        _lib.check(rc)
+        return [out[int(offsets[p]):int(offsets[p + 1])] for p in range(len(pairs))]
 
     # ---- matching, device tensors ------------------------------------------------
     def match_top2_device(self, queries, train, out=None, stream=None):

@@ -138,6 +138,28 @@ def match_all_pairs_sharded(desc_sets: Sequence, match_pair: Callable, num_image
     return {(i, j): match_pair(i, j, desc_sets[i], desc_sets[j]) for i, j in pairs_for_rank(n, rank, world)}
 
 
+def match_all_pairs_resident(desc_sets: Sequence, ratio=None, cross_check=False, max_distance=None,
+                             num_images: int | None = None):
+    """cfg5 on the CUDA path: this rank's share of the (i < j) pairs, batched through resident
+    descriptor sets (each image is uploaded and expanded once, all pairs run in a few launches).
+    `desc_sets[i]` is a (M_i, 64) uint8 numpy array or CUDA tensor. Returns {(i, j): (M,4) int32}."""
+    from .engine import get_engine
+    rank, world = _world()
+    n = num_images if num_images is not None else len(desc_sets)
+    mine = pairs_for_rank(n, rank, world)
+    eng = get_engine()
+    needed = sorted({i for p in mine for i in p})
+    sets = {i: eng.create_set(desc_sets[i]) for i in needed}
+    order = {i: k for k, i in enumerate(needed)}
+    try:
+        res = eng.match_set_pairs([sets[i] for i in needed], [(order[i], order[j]) for i, j in mine],
+                                  ratio=ratio, cross_check=cross_check, max_distance=max_distance)
+    finally:
+        for s in sets.values():
+            s.close()
+    return {p: r.copy() for p, r in zip(mine, res)}
+
+
 def default_match_pair(ratio=None, cross_check=False, max_distance=None):
     """match_pair callable for match_all_pairs_sharded running the CUDA matcher on device
     tensors and the reference's filter pass on the host (src/match.cpp:69-79)."""

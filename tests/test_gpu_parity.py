@@ -415,3 +415,40 @@ def test_every_extraction_variant_is_exact(lk, port, variant):
         assert np.array_equal(lk.describe(fimg, kps)[1], port.describe_all(fimg, kps)[1])
     finally:
         eng.set_option("extract_variant", 1)
+
+
+# ------------------------------------------------------ resident sets, batched pairs ----
+
+def test_resident_sets_and_batched_pairs(lk, port):
+    """cfg5 shape: every image against every other image through resident descriptor sets.
+    Each pair must equal the reference's match_brute_force with the same filters."""
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    sizes = [300, 1, 257, 128, 1000]
+    raw = [port.random_descriptors(900 + i, n, 64) for i, n in enumerate(sizes)]
+    raw[2][5] = raw[0][7]                 # cross-image duplicates -> zero distances and ties
+    raw[4][11] = raw[0][7]
+    raw[4][12] = raw[4][11]
+    sets = [eng.create_set(raw[0]), eng.create_set(torch.from_numpy(raw[1]).cuda()), eng.create_set(raw[2]),
+            eng.create_set(torch.from_numpy(raw[3]).cuda()), eng.create_set(raw[4])]
+    assert [len(s) for s in sets] == sizes
+    pairs = [(i, j) for i in range(5) for j in range(5) if i != j]
+    for kw in ({}, {"ratio": 0.9}, {"cross_check": True}, {"ratio": 0.85, "cross_check": True, "max_distance": 240}):
+        got = eng.match_set_pairs(sets, pairs, **kw)
+        for (i, j), g in zip(pairs, got):
+            assert np.array_equal(g, port.match(raw[i], raw[j], **kw)), (i, j, kw)
+    one = eng.match_sets(sets[0], sets[4], ratio=0.9, cross_check=True)
+    assert np.array_equal(one, port.match(raw[0], raw[4], ratio=0.9, cross_check=True))
+    assert eng.match_set_pairs(sets, []) == []
+    empty = eng.create_set(np.zeros((0, 64), np.uint8))
+    assert len(eng.match_sets(empty, sets[0])) == 0            # empty probes -> no rows
+    with pytest.raises(RuntimeError):
+        eng.match_sets(sets[0], empty)                          # empty gallery -> EmptyGallery
+    for s in sets:
+        s.close()
+    # the sharded driver's single-process form
+    from paper_1609_03986_b200 import sharded
+    res = sharded.match_all_pairs_resident(raw, ratio=0.9, cross_check=True)
+    assert sorted(res) == sharded.pairs_for_rank(5, 0, 1)
+    for (i, j), m in res.items():
+        assert np.array_equal(m, port.match(raw[i], raw[j], ratio=0.9, cross_check=True))
