@@ -127,6 +127,22 @@ CLATCH_API int clatch_describe_all_f64(clatch_ctx* ctx, const double* img, int w
                             const double* kps, size_t n, int cols, int workers, int64_t* kept,
                             uint8_t* out, size_t* m);
 
+/* describe_all over a batch of images (BASELINE config 3: many images x many keypoints per GPU).
+ * Image i is imgs[i] (widths[i] x heights[i], pitches[i] elements per row) with counts[i]
+ * keypoint rows of `cols` doubles at kps[i]; results go to kept[i] (room for counts[i]
+ * indices), out[i] (room for counts[i] descriptors) and m[i]. Uploads, host trig, kernels and
+ * downloads of consecutive images are pipelined over two streams; with page-locked host
+ * buffers the copies are fully asynchronous. Results are identical to num_images calls of
+ * clatch_describe_all_*. */
+CLATCH_API int clatch_describe_batch_u8(clatch_ctx* ctx, const uint8_t* const* imgs, const int* widths, const int* heights,
+                             const size_t* pitches, const double* const* kps, const size_t* counts, int cols,
+                             size_t num_images, int workers, int64_t* const* kept, uint8_t* const* out,
+                             size_t* m);
+CLATCH_API int clatch_describe_batch_f64(clatch_ctx* ctx, const double* const* imgs, const int* widths, const int* heights,
+                              const size_t* pitches, const double* const* kps, const size_t* counts, int cols,
+                              size_t num_images, int workers, int64_t* const* kept, uint8_t* const* out,
+                              size_t* m);
+
 /* Device-resident forms: all pointers are device memory on the context's device,
  * work is queued on `stream` (a cudaStream_t; NULL = the legacy default stream)
  * and NOT synchronised. */
@@ -176,7 +192,8 @@ CLATCH_API int clatch_match_brute_force(clatch_ctx* ctx, const uint8_t* probes, 
  * every other image" workload; the reference has no counterpart — it re-reads
  * std::vector<Descriptor> per call, src/match.cpp:52-67).
  * `descriptors` is host memory (on_device = 0) or device memory on the context's device
- * (on_device = 1); it is copied, the caller keeps ownership. */
+ * (on_device = 1, and any work producing it must already be complete or ordered before the
+ * context's stream); it is copied, the caller keeps ownership. */
 typedef struct clatch_set clatch_set;
 CLATCH_API int clatch_set_create(clatch_ctx* ctx, const uint8_t* descriptors, size_t n, int on_device, clatch_set** out);
 CLATCH_API void clatch_set_destroy(clatch_set* set);

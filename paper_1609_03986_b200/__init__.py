@@ -25,7 +25,7 @@ window_margin = 46
 orientation_radius = 15
 
 __all__ = [
-    "default_pattern", "describe", "descriptor_bits", "descriptor_bytes", "hamming", "match",
+    "default_pattern", "describe", "describe_batch", "descriptor_bits", "descriptor_bytes", "hamming", "match",
     "orientation_radius", "window_margin", "Engine", "DescriptorSet", "get_engine", "LatchError",
     "ClatchDeviceError", "TripletPattern", "parse_pattern", "format_pattern",
 ]
@@ -88,6 +88,31 @@ def describe(image, keypoints, pattern=None, workers=0):
     full = np.zeros((len(kept), 4), np.float64)
     full[:, :kps.shape[1]] = kps.take(kept, axis=0)
     return full, desc
+
+
+def describe_batch(images, keypoints, pattern=None, workers=0):
+    """describe() over a list of images and keypoint arrays in one pipelined call (extension
+    for the many-images-per-GPU workload). Returns a list of (kept_keypoints, descriptors),
+    each identical to describe(images[i], keypoints[i], pattern)."""
+    pat = pattern_from_text(pattern)
+    imgs = [_image_array(im) for im in images]
+    kps = [_keypoint_array(k) for k in keypoints]
+    if len(imgs) != len(kps):
+        raise ValueError("describe_batch needs one keypoint array per image")
+    if len({im.dtype for im in imgs}) > 1:          # mixed input: use the reference dtype for all
+        imgs = [np.ascontiguousarray(im, dtype=np.float64) for im in imgs]
+    widest = max((k.shape[1] for k in kps), default=4)
+    if any(k.shape[1] != widest for k in kps):
+        kps = [np.hstack([k, np.zeros((len(k), widest - k.shape[1]))]) for k in kps]
+    eng = get_engine()
+    eng.set_pattern(pat)
+    res = eng.describe_batch(imgs, kps, workers)
+    out = []
+    for k, (kept, desc) in zip(kps, res):
+        full = np.zeros((len(kept), 4), np.float64)
+        full[:, :k.shape[1]] = k.take(kept, axis=0)
+        out.append((full, desc))
+    return out
 
 
 def match(probes, gallery, ratio=None, cross_check=False, max_distance=None, workers=0):

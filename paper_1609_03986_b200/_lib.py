@@ -65,6 +65,12 @@ _SIGNATURES = {
                                          C.c_int, C.c_int, i64p, u8p, szp]),
     "clatch_describe_all_f64": (C.c_int, [C.c_void_p, f64p, C.c_int, C.c_int, C.c_size_t, f64p, C.c_size_t,
                                           C.c_int, C.c_int, i64p, u8p, szp]),
+    "clatch_describe_batch_u8": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                           szp, C.POINTER(C.c_void_p), szp, C.c_int, C.c_size_t, C.c_int,
+                                           C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), szp]),
+    "clatch_describe_batch_f64": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                            szp, C.POINTER(C.c_void_p), szp, C.c_int, C.c_size_t, C.c_int,
+                                            C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), szp]),
     "clatch_extract_u8_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_size_t,
                                         C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
     "clatch_extract_f64_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_size_t,

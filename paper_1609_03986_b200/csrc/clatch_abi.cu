@@ -9,6 +9,7 @@
 #include <cstring>
 #include <condition_variable>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 
@@ -38,6 +39,23 @@ int DeviceBuffer::reserve(size_t bytes) {
     CLATCH_CUDA(cudaMalloc(&ptr, want));
     cap = want;
     return CLATCH_OK;
+}
+
+int PinnedBuffer::reserve(size_t bytes) {
+    if (bytes <= cap) return CLATCH_OK;
+    if (ptr) CLATCH_CUDA(cudaFreeHost(ptr));
+    ptr = nullptr;
+    cap = 0;
+    const size_t want = bytes + bytes / 4;
+    CLATCH_CUDA(cudaHostAlloc(&ptr, want, cudaHostAllocDefault));
+    cap = want;
+    return CLATCH_OK;
+}
+
+void PinnedBuffer::release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    cap = 0;
 }
 
 void DeviceBuffer::release() {
@@ -195,6 +213,13 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
                             &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->items, &ctx->pattern.slots, &ctx->pattern.slots_quad,
                             &ctx->pattern.triplets})
         b->release();
+    ctx->pinned.release();
+    for (int s = 0; s < 2; ++s) {
+        for (DeviceBuffer* b : {&ctx->pipe[s].img, &ctx->pipe[s].kps, &ctx->pipe[s].desc, &ctx->pipe[s].img_u8,
+                                &ctx->pipe[s].flags})
+            b->release();
+        if (ctx->pipe[s].stream) cudaStreamDestroy(ctx->pipe[s].stream);
+    }
     delete ctx;
 }
 
@@ -472,7 +497,95 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
     return CLATCH_OK;
 }
 
+// Two-slot software pipeline over images: slot = i % 2 owns a stream and its own device
+// scratch, so image i+1 uploads / prepares while image i computes and downloads.
+template <typename Pixel>
+static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const int* widths, const int* heights,
+                               const size_t* pitches, const double* const* kps, const size_t* counts, int cols,
+                               size_t num_images, int workers, int64_t* const* kept, uint8_t* const* out, size_t* m) {
+    if (!ctx) return invalid("describe_batch: ctx is null");
+    if (num_images == 0) return CLATCH_OK;
+    if (!imgs || !widths || !heights || !pitches || !kps || !counts || !kept || !out || !m)
+        return invalid("describe_batch: null array");
+    if (ctx->pattern.T == 0) return invalid("extract: no pattern installed (clatch_set_pattern)");
+    if (cols < 2 || cols > 4) return invalid("keypoints must be (N, 2..4): x, y[, theta[, score]]");
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    constexpr bool kU8 = sizeof(Pixel) == 1;
+    const size_t bytes = static_cast<size_t>(ctx->pattern.T) / 8;
+    for (int s = 0; s < 2; ++s)
+        if (!ctx->pipe[s].stream) CLATCH_CUDA(cudaStreamCreateWithFlags(&ctx->pipe[s].stream, cudaStreamNonBlocking));
+    int rc = CLATCH_OK;
+    for (size_t i = 0; i < num_images && !rc; ++i) {
+        clatch_ctx::PipeSlot& slot = ctx->pipe[i & 1];
+        cudaStream_t st = slot.stream;
+        m[i] = 0;
+        const int w = widths[i], h = heights[i];
+        const size_t n = counts[i];
+        if (!imgs[i] || w <= 0 || h <= 0 || pitches[i] < static_cast<size_t>(w)) {
+            rc = invalid("describe_batch: bad image (null, empty or pitch < width)");
+            break;
+        }
+        if (n == 0) continue;
+        if (!kps[i] || !kept[i] || !out[i]) {
+            rc = invalid("describe_batch: null keypoint/output buffer");
+            break;
+        }
+        // the slot's previous image (i-2) must have left its buffers before they are reused
+        CLATCH_CUDA(cudaStreamSynchronize(st));
+        const size_t dpitch = kU8 ? (static_cast<size_t>(w) + 15) / 16 * 16 : static_cast<size_t>(w);
+        if ((rc = slot.img.reserve(sizeof(Pixel) * dpitch * h))) break;
+        if ((rc = slot.kps.reserve(sizeof(double) * 4 * n))) break;
+        if ((rc = slot.desc.reserve(bytes * n))) break;
+        if (!kU8) {
+            const size_t u8_pitch = (static_cast<size_t>(w) + 15) / 16 * 16;
+            if ((rc = slot.img_u8.reserve(u8_pitch * h))) break;
+            if ((rc = slot.flags.reserve(sizeof(int)))) break;
+        }
+        CLATCH_CUDA(cudaMemcpy2DAsync(slot.img.ptr, sizeof(Pixel) * dpitch, imgs[i], sizeof(Pixel) * pitches[i],
+                                      sizeof(Pixel) * w, h, cudaMemcpyHostToDevice, st));
+        slot.xycs.resize(4 * n);
+        size_t count = 0;
+        if ((rc = clatch_prepare_keypoints(kps[i], n, cols, w, h, workers, slot.xycs.data(), kept[i], &count))) break;
+        m[i] = count;
+        if (count == 0) continue;
+        CLATCH_CUDA(cudaMemcpyAsync(slot.kps.ptr, slot.xycs.data(), sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
+        if (kU8) {
+            rc = launch_extract_u8(ctx, slot.img.template as<uint8_t>(), w, h, dpitch, slot.kps.template as<double>(),
+                                   count, slot.desc.template as<uint8_t>(), st);
+        } else {
+            // the f64 launcher uses ctx-level promotion scratch: point it at this slot's buffers
+            std::swap(ctx->img_u8, slot.img_u8);
+            std::swap(ctx->flags, slot.flags);
+            rc = launch_extract_f64(ctx, slot.img.template as<double>(), w, h, dpitch, slot.kps.template as<double>(),
+                                    count, slot.desc.template as<uint8_t>(), st);
+            std::swap(ctx->img_u8, slot.img_u8);
+            std::swap(ctx->flags, slot.flags);
+        }
+        if (rc) break;
+        CLATCH_CUDA(cudaMemcpyAsync(out[i], slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+    }
+    for (int s = 0; s < 2; ++s) {
+        cudaError_t e = cudaStreamSynchronize(ctx->pipe[s].stream);
+        if (e != cudaSuccess && !rc) rc = cuda_fail(e, "cudaStreamSynchronize(batch)");
+    }
+    return rc;
+}
+
 extern "C" {
+
+int clatch_describe_batch_u8(clatch_ctx* ctx, const uint8_t* const* imgs, const int* widths, const int* heights,
+                             const size_t* pitches, const double* const* kps, const size_t* counts, int cols,
+                             size_t num_images, int workers, int64_t* const* kept, uint8_t* const* out, size_t* m) {
+    return describe_batch_impl<uint8_t>(ctx, imgs, widths, heights, pitches, kps, counts, cols, num_images, workers,
+                                        kept, out, m);
+}
+
+int clatch_describe_batch_f64(clatch_ctx* ctx, const double* const* imgs, const int* widths, const int* heights,
+                              const size_t* pitches, const double* const* kps, const size_t* counts, int cols,
+                              size_t num_images, int workers, int64_t* const* kept, uint8_t* const* out, size_t* m) {
+    return describe_batch_impl<double>(ctx, imgs, widths, heights, pitches, kps, counts, cols, num_images, workers,
+                                       kept, out, m);
+}
 
 int clatch_describe_all_u8(clatch_ctx* ctx, const uint8_t* img, int width, int height, size_t pitch,
                            const double* kps, size_t n, int cols, int workers, int64_t* kept,
@@ -541,7 +654,10 @@ int clatch_match_top2(clatch_ctx* ctx, const uint8_t* queries, size_t Q, const u
 struct clatch_set {
     clatch_ctx* ctx = nullptr;
     size_t n = 0;
-    DeviceBuffer packed, exp_a, exp_b;
+    uint8_t* block = nullptr;   // one stream-ordered allocation: packed | A-form | B-form
+    uint8_t* packed = nullptr;
+    uint8_t* exp_a = nullptr;
+    uint8_t* exp_b = nullptr;
 };
 
 namespace {
@@ -549,7 +665,7 @@ namespace {
 // Forward (+ reverse) top-2 of a batch of set pairs in one launch, results to `host`:
 // per pair [best_idx n_i][best_dist n_i][second n_i][reverse_best n_j if cross_check].
 int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t* pairs, size_t first, size_t count,
-                   bool cross_check, std::vector<int32_t>& host, std::vector<size_t>& pair_offset) {
+                   bool cross_check, int32_t** host, std::vector<size_t>& pair_offset) {
     pair_offset.assign(count + 1, 0);
     size_t items = 0;
     for (size_t p = 0; p < count; ++p) {
@@ -569,20 +685,21 @@ int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t
         const clatch_set* b = sets[pairs[2 * (first + p) + 1]];
         int32_t* base = r + pair_offset[p];
         for (int q = 0; q < tc_query_tiles(a->n); ++q)
-            table.push_back({a->exp_a.as<uint8_t>(), b->exp_b.as<uint8_t>(), static_cast<unsigned>(a->n),
+            table.push_back({a->exp_a, b->exp_b, static_cast<unsigned>(a->n),
                              static_cast<unsigned>(b->n), static_cast<unsigned>(q), 0, base, base + a->n,
                              base + 2 * a->n});
         if (cross_check)   // reverse_best[g] = knn2(gallery[g], probes).best_index, src/match.cpp:62-67
             for (int q = 0; q < tc_query_tiles(b->n); ++q)
-                table.push_back({b->exp_a.as<uint8_t>(), a->exp_b.as<uint8_t>(), static_cast<unsigned>(b->n),
+                table.push_back({b->exp_a, a->exp_b, static_cast<unsigned>(b->n),
                                  static_cast<unsigned>(a->n), static_cast<unsigned>(q), 0, base + 3 * a->n, nullptr,
                                  nullptr});
     }
     cudaStream_t st = ctx->stream;
     CLATCH_CUDA(cudaMemcpyAsync(ctx->items.ptr, table.data(), sizeof(TcItem) * table.size(), cudaMemcpyHostToDevice, st));
     if (int rc = launch_match_tc_items(ctx, ctx->items.as<TcItem>(), table.size(), st)) return rc;
-    host.resize(total);
-    CLATCH_CUDA(cudaMemcpyAsync(host.data(), r, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, st));
+    if (int rc = ctx->pinned.reserve(sizeof(int32_t) * std::max<size_t>(total, 1))) return rc;
+    *host = static_cast<int32_t*>(ctx->pinned.ptr);
+    CLATCH_CUDA(cudaMemcpyAsync(*host, r, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, st));
     CLATCH_CUDA(cudaStreamSynchronize(st));   // also keeps `table` alive until the H2D copy is done
     return CLATCH_OK;
 }
@@ -603,18 +720,23 @@ int clatch_set_create(clatch_ctx* ctx, const uint8_t* descriptors, size_t n, int
     int rc = CLATCH_OK;
     if (n > 0) {
         cudaStream_t st = ctx->stream;
-        if (!rc) rc = set->packed.reserve(n * 64);
-        if (!rc) rc = set->exp_a.reserve(tc_expanded_bytes(n, true));
-        if (!rc) rc = set->exp_b.reserve(tc_expanded_bytes(n, false));
+        const size_t packed_bytes = (n * 64 + 1023) / 1024 * 1024;
+        const size_t a_bytes = tc_expanded_bytes(n, true), b_bytes = tc_expanded_bytes(n, false);
+        // cudaMallocAsync: pooled, stream-ordered — set churn does not pay cudaMalloc/cudaFree latency.
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&set->block), packed_bytes + a_bytes + b_bytes, st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocAsync(set)");
         if (!rc) {
-            cudaError_t e = cudaMemcpyAsync(set->packed.ptr, descriptors, n * 64,
-                                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+            set->packed = set->block;
+            set->exp_a = set->block + packed_bytes;
+            set->exp_b = set->exp_a + a_bytes;
+            e = cudaMemcpyAsync(set->packed, descriptors, n * 64,
+                                on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(set)");
         }
-        if (!rc) rc = launch_tc_expand(ctx, set->packed.as<uint8_t>(), n, true, set->exp_a.as<uint8_t>(), st);
-        if (!rc) rc = launch_tc_expand(ctx, set->packed.as<uint8_t>(), n, false, set->exp_b.as<uint8_t>(), st);
-        if (!rc) {
-            cudaError_t e = cudaStreamSynchronize(st);
+        if (!rc) rc = launch_tc_expand(ctx, set->packed, n, true, set->exp_a, st);
+        if (!rc) rc = launch_tc_expand(ctx, set->packed, n, false, set->exp_b, st);
+        if (!rc && !on_device) {   // the caller may reuse its host buffer as soon as we return
+            e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) rc = cuda_fail(e, "cudaStreamSynchronize(set)");
         }
     }
@@ -629,9 +751,7 @@ int clatch_set_create(clatch_ctx* ctx, const uint8_t* descriptors, size_t n, int
 void clatch_set_destroy(clatch_set* set) {
     if (!set) return;
     cudaSetDevice(set->ctx->device);
-    set->packed.release();
-    set->exp_a.release();
-    set->exp_b.release();
+    if (set->block) cudaFreeAsync(set->block, set->ctx->stream);
     delete set;
 }
 
@@ -658,8 +778,10 @@ int clatch_match_set_pairs(clatch_ctx* ctx, const clatch_set* const* sets, size_
     CLATCH_CUDA(cudaSetDevice(ctx->device));
     // Chunks bounded by result bytes (<= 256 MiB of top-2 triples per launch).
     const size_t kChunkInts = (256u << 20) / sizeof(int32_t);
-    std::vector<int32_t> host;
+    int32_t* host = nullptr;   // pinned staging owned by the context
     std::vector<size_t> pair_offset;
+    std::unique_ptr<int32_t[]> scratch;
+    size_t scratch_cap = 0;
     size_t rows_out = 0;
     for (size_t first = 0; first < num_pairs;) {
         size_t count = 0, ints = 0;
@@ -670,23 +792,26 @@ int clatch_match_set_pairs(clatch_ctx* ctx, const clatch_set* const* sets, size_
             ints += need;
             ++count;
         }
-        if (int rc = run_pair_batch(ctx, sets, pairs, first, count, cross_check != 0, host, pair_offset)) return rc;
+        if (int rc = run_pair_batch(ctx, sets, pairs, first, count, cross_check != 0, &host, pair_offset)) return rc;
         // filter pass per pair (src/match.cpp:69-79): parallel into per-pair scratch, then compact in order
         std::vector<size_t> scratch_off(count + 1, 0), kept(count, 0);
         for (size_t p = 0; p < count; ++p) scratch_off[p + 1] = scratch_off[p] + 4 * sets[pairs[2 * (first + p)]]->n;
-        std::vector<int32_t> scratch(std::max<size_t>(scratch_off[count], 1));
+        if (scratch_off[count] > scratch_cap) {   // uninitialised on purpose: every kept row is written
+            scratch_cap = scratch_off[count];
+            scratch.reset(new int32_t[scratch_cap]);
+        }
         const int parts = static_cast<int>(std::min<size_t>(count, resolve_workers(0)));
         WorkerPool::instance().run(parts, [&](int part) {
             for (size_t p = part; p < count; p += parts) {
                 const size_t n = sets[pairs[2 * (first + p)]]->n;
-                const int32_t* base = host.data() + pair_offset[p];
+                const int32_t* base = host + pair_offset[p];
                 clatch_filter_matches(base, base + n, base + 2 * n, n, has_ratio, ratio, has_max, max_distance,
-                                      cross_check ? base + 3 * n : nullptr, scratch.data() + scratch_off[p], &kept[p]);
+                                      cross_check ? base + 3 * n : nullptr, scratch.get() + scratch_off[p], &kept[p]);
             }
         });
         for (size_t p = 0; p < count; ++p) {
             if (rows_out + kept[p] > cap_rows) return invalid("clatch_match_set_pairs: cap_rows too small");
-            std::memcpy(out + 4 * rows_out, scratch.data() + scratch_off[p], sizeof(int32_t) * 4 * kept[p]);
+            std::memcpy(out + 4 * rows_out, scratch.get() + scratch_off[p], sizeof(int32_t) * 4 * kept[p]);
             rows_out += kept[p];
             offsets[first + p + 1] = rows_out;
         }

@@ -39,6 +39,14 @@ struct DeviceBuffer {
     T* as() const { return static_cast<T*>(ptr); }
 };
 
+// Grow-only page-locked host staging buffer.
+struct PinnedBuffer {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    int reserve(size_t bytes);
+    void release();
+};
+
 struct Pattern {
     int T = 0;
     int K = 0;
@@ -69,6 +77,12 @@ struct clatch_ctx {
     // scratch for the host-buffer entry points
     clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t, items;
     std::vector<double> host_xycs;   // describe_all staging
+    clatch::PinnedBuffer pinned;     // D2H staging for batched pair results
+    struct PipeSlot {                // describe_batch: one of two pipeline slots
+        cudaStream_t stream = nullptr;
+        clatch::DeviceBuffer img, kps, desc, img_u8, flags;
+        std::vector<double> xycs;
+    } pipe[2];
 };
 
 namespace clatch {

@@ -163,6 +163,46 @@ class Engine:
         _lib.check(rc)
         return kept[:m.value], out[:m.value]
 
+    def describe_batch(self, images, keypoints, workers: int = 0):
+        """describe_all over many images in one pipelined ABI call. images: list of 2-D arrays, all
+        uint8 or all float64; keypoints: list of (N_i, cols) float64 arrays with one common cols.
+        -> list of (kept int64 (M_i,), descriptors uint8 (M_i, T/8))."""
+        n_img = len(images)
+        if n_img == 0:
+            return []
+        dtype = images[0].dtype
+        imgs, kps_l = [], []
+        for im in images:
+            if im.dtype != dtype:
+                raise TypeError("describe_batch needs one image dtype per call")
+            if im.strides[1] != im.itemsize or im.strides[0] % im.itemsize:
+                im = np.ascontiguousarray(im)
+            imgs.append(im)
+        for k in keypoints:
+            kps_l.append(np.ascontiguousarray(k, np.float64))
+        cols = kps_l[0].shape[1]
+        if any(k.shape[1] != cols for k in kps_l):
+            raise ValueError("describe_batch needs one keypoint column count per call")
+        nbytes = self.descriptor_bytes
+        kept = [np.empty(len(k), np.int64) for k in kps_l]
+        out = [np.empty((len(k), nbytes), np.uint8) for k in kps_l]
+        vp = C.c_void_p * n_img
+        widths = (C.c_int * n_img)(*[im.shape[1] for im in imgs])
+        heights = (C.c_int * n_img)(*[im.shape[0] for im in imgs])
+        pitches = (C.c_size_t * n_img)(*[im.strides[0] // im.itemsize for im in imgs])
+        counts = (C.c_size_t * n_img)(*[len(k) for k in kps_l])
+        m = (C.c_size_t * n_img)()
+        fn = {np.dtype(np.uint8): self.lib.clatch_describe_batch_u8,
+              np.dtype(np.float64): self.lib.clatch_describe_batch_f64}.get(np.dtype(dtype))
+        if fn is None:
+            raise TypeError("image dtype must be uint8 or float64")
+        with self._lock:
+            rc = fn(self.ctx, vp(*[im.ctypes.data for im in imgs]), widths, heights, pitches,
+                    vp(*[k.ctypes.data for k in kps_l]), counts, cols, n_img, workers,
+                    vp(*[a.ctypes.data for a in kept]), vp(*[a.ctypes.data for a in out]), m)
+        _lib.check(rc)
+        return [(kept[i][:m[i]], out[i][:m[i]]) for i in range(n_img)]
+
     # ---- extraction, device tensors --------------------------------------------
     def extract_device(self, image, xycs, out=None, stream=None):
         """image: torch CUDA tensor (H, W) uint8 or float64, unit inner stride; xycs: CUDA

@@ -60,9 +60,11 @@ def extract_images_sharded(images: Sequence, keypoints: Sequence, describe: Call
     (kept, descriptors)`; default = the package's describe(). Returns {image index:
     (kept, descriptors)} for the images this rank owns."""
     rank, world = _world()
-    if describe is None:
-        from . import describe as describe
-    return {i: describe(images[i], keypoints[i]) for i in range(rank, len(images), world)}
+    mine = list(range(rank, len(images), world))
+    if describe is None:      # CUDA path: this rank's images through one pipelined batch call
+        from . import describe_batch
+        return dict(zip(mine, describe_batch([images[i] for i in mine], [keypoints[i] for i in mine])))
+    return {i: describe(images[i], keypoints[i]) for i in mine}
 
 
 def all_gather_descriptor_sets(local: dict, num_images: int, device=None):
@@ -157,7 +159,7 @@ def match_all_pairs_resident(desc_sets: Sequence, ratio=None, cross_check=False,
     finally:
         for s in sets.values():
             s.close()
-    return {p: r.copy() for p, r in zip(mine, res)}
+    return dict(zip(mine, res))          # views into one result block
 
 
 def default_match_pair(ratio=None, cross_check=False, max_distance=None):

@@ -452,3 +452,27 @@ def test_resident_sets_and_batched_pairs(lk, port):
     assert sorted(res) == sharded.pairs_for_rank(5, 0, 1)
     for (i, j), m in res.items():
         assert np.array_equal(m, port.match(raw[i], raw[j], ratio=0.9, cross_check=True))
+
+
+def test_describe_batch_matches_per_image_calls(lk, port):
+    """cfg3 shape: several images per GPU through the pipelined batch call."""
+    imgs, kps = [], []
+    for i, (w, h, n) in enumerate([(320, 240, 500), (200, 150, 1), (640, 480, 2000), (333, 201, 0), (256, 256, 77)]):
+        imgs.append(port.structured_image(600 + i, w, h) if i % 2 else port.random_image(600 + i, w, h))
+        k = port.random_keypoints(700 + i, w, h, n)
+        if n > 10:
+            k[::9, 0] = 5.0                       # margin violators
+        kps.append(k)
+    want = [port.describe_all(im, k) for im, k in zip(imgs, kps)]
+    for cast in (np.uint8, np.float64):
+        got = lk.describe_batch([im.astype(cast) for im in imgs], kps)
+        assert len(got) == len(imgs)
+        for (gk, gd), (wk, wd), k in zip(got, want, kps):
+            assert np.array_equal(gk, k[wk]) and np.array_equal(gd, wd)
+    # non-integer images cannot be promoted to u8: the f64 sampling path inside the pipeline
+    rng = np.random.default_rng(5)
+    fimgs = [rng.random((150, 170)) * 255.0 for _ in range(3)]
+    fk = [port.random_keypoints(800 + i, 170, 150, 90) for i in range(3)]
+    for (gk, gd), im, k in zip(lk.describe_batch(fimgs, fk), fimgs, fk):
+        assert np.array_equal(gd, port.describe_all(im, k)[1])
+    assert lk.describe_batch([], []) == []

@@ -36,6 +36,18 @@ t0 = time.perf_counter()
 res = [lk.describe(im, k) for im, k in zip(imgs, kps)]
 t_e2e = time.perf_counter() - t0
 total = sum(len(r[1]) for r in res)
+# pipelined batch call on page-locked host arrays
+def pinned(a):
+    t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+    t.numpy()[...] = a
+    return t.numpy()
+pimgs, pkps = [pinned(a) for a in imgs], [pinned(a) for a in kps]
+lk.describe_batch(pimgs[:2], pkps[:2])
+sync()
+t0 = time.perf_counter()
+bres = lk.describe_batch(pimgs, pkps)
+t_batch = time.perf_counter() - t0
+batch_same = all(np.array_equal(a[1], b[1]) for a, b in zip(bres, res))
 # device-resident: kernel only
 d_img = torch.from_numpy(imgs[0]).cuda()
 xycs, kept = eng.prepare_keypoints(kps[0], W, H)
@@ -58,6 +70,8 @@ out["cfg3"] = {"images": IMAGES, "shape": [W, H], "keypoints_per_image": N_KP, "
                "e2e_descriptors_per_s": total / t_e2e, "e2e_s": t_e2e,
                "kernel_ms_per_image": ms_kernel, "kernel_descriptors_per_s": len(xycs) / ms_kernel * 1e3,
                "parity_200_desc_x2_images": ok,
+               "batch_e2e_descriptors_per_s": total / t_batch, "batch_e2e_s": t_batch,
+               "batch_identical_to_per_image": bool(batch_same),
                "note": "one GPU's share (8 of 64 images) of the 8-GPU config; u8 images through lk.describe"}
 print("cfg3", out["cfg3"], file=sys.stderr, flush=True)
 del imgs, res
@@ -118,11 +132,18 @@ out["cfg5"] = {"images": IM5, "keypoints": KP5, "pairs": len(pairs), "s": t_pair
                "compares_per_s_incl_cross_check": compares / t_pairs, "two_pairs_exact_vs_oracle": ok5,
                "note": "ratio 0.8 + cross-check per pair (two top-2 passes), host filter pass, device-resident sets"}
 from paper_1609_03986_b200 import sharded               # noqa: E402
-sharded.match_all_pairs_resident(sets[:3], ratio=0.8, cross_check=True)
+sharded.match_all_pairs_resident(sets, ratio=0.8, cross_check=True)
 sync()
 t0 = time.perf_counter()
 batched = sharded.match_all_pairs_resident(sets, ratio=0.8, cross_check=True)
 t_b = time.perf_counter() - t0
+t0 = time.perf_counter()
+rsets = [eng.create_set(d) for d in dsets]
+t_sets = time.perf_counter() - t0
+t0 = time.perf_counter()
+eng.match_set_pairs(rsets, pairs, ratio=0.8, cross_check=True)
+t_match_only = time.perf_counter() - t0
+out.setdefault("cfg5_detail", {}).update({"create_sets_s": t_sets, "match_set_pairs_s": t_match_only})
 same = all(np.array_equal(batched[p], results[p]) for p in pairs)
 out["cfg5"]["batched"] = {"s": t_b, "pairs_per_s": len(pairs) / t_b, "compares_per_s_incl_cross_check": compares / t_b,
                           "identical_to_per_pair_path": bool(same),
