@@ -109,6 +109,9 @@ def describe_batch(images, keypoints, pattern=None, workers=0):
     res = eng.describe_batch(imgs, kps, workers)
     out = []
     for k, (kept, desc) in zip(kps, res):
+        if k.shape[1] == 4:
+            out.append((k.take(kept, axis=0), desc))
+            continue
         full = np.zeros((len(kept), 4), np.float64)
         full[:, :k.shape[1]] = k.take(kept, axis=0)
         out.append((full, desc))

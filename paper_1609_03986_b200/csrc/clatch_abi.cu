@@ -218,6 +218,8 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
         for (DeviceBuffer* b : {&ctx->pipe[s].img, &ctx->pipe[s].kps, &ctx->pipe[s].desc, &ctx->pipe[s].img_u8,
                                 &ctx->pipe[s].flags})
             b->release();
+        ctx->pipe[s].h_xycs.release();
+        ctx->pipe[s].h_desc.release();
         if (ctx->pipe[s].stream) cudaStreamDestroy(ctx->pipe[s].stream);
     }
     delete ctx;
@@ -530,8 +532,13 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
             rc = invalid("describe_batch: null keypoint/output buffer");
             break;
         }
-        // the slot's previous image (i-2) must have left its buffers before they are reused
+        // the slot's previous image (i-2) must have left its buffers before they are reused;
+        // its descriptors wait in page-locked staging and move to the caller's array now
         CLATCH_CUDA(cudaStreamSynchronize(st));
+        if (slot.pending_out) {
+            std::memcpy(slot.pending_out, slot.h_desc.ptr, slot.pending_bytes);
+            slot.pending_out = nullptr;
+        }
         const size_t dpitch = kU8 ? (static_cast<size_t>(w) + 15) / 16 * 16 : static_cast<size_t>(w);
         if ((rc = slot.img.reserve(sizeof(Pixel) * dpitch * h))) break;
         if ((rc = slot.kps.reserve(sizeof(double) * 4 * n))) break;
@@ -543,12 +550,14 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         }
         CLATCH_CUDA(cudaMemcpy2DAsync(slot.img.ptr, sizeof(Pixel) * dpitch, imgs[i], sizeof(Pixel) * pitches[i],
                                       sizeof(Pixel) * w, h, cudaMemcpyHostToDevice, st));
-        slot.xycs.resize(4 * n);
+        if ((rc = slot.h_xycs.reserve(sizeof(double) * 4 * n))) break;
+        if ((rc = slot.h_desc.reserve(bytes * n))) break;
+        double* const xycs = static_cast<double*>(slot.h_xycs.ptr);
         size_t count = 0;
-        if ((rc = clatch_prepare_keypoints(kps[i], n, cols, w, h, workers, slot.xycs.data(), kept[i], &count))) break;
+        if ((rc = clatch_prepare_keypoints(kps[i], n, cols, w, h, workers, xycs, kept[i], &count))) break;
         m[i] = count;
         if (count == 0) continue;
-        CLATCH_CUDA(cudaMemcpyAsync(slot.kps.ptr, slot.xycs.data(), sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
+        CLATCH_CUDA(cudaMemcpyAsync(slot.kps.ptr, xycs, sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
         if (kU8) {
             rc = launch_extract_u8(ctx, slot.img.template as<uint8_t>(), w, h, dpitch, slot.kps.template as<double>(),
                                    count, slot.desc.template as<uint8_t>(), st);
@@ -562,11 +571,17 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
             std::swap(ctx->flags, slot.flags);
         }
         if (rc) break;
-        CLATCH_CUDA(cudaMemcpyAsync(out[i], slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+        // page-locked staging keeps the download asynchronous even when out[i] is pageable
+        CLATCH_CUDA(cudaMemcpyAsync(slot.h_desc.ptr, slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+        slot.pending_out = out[i];
+        slot.pending_bytes = bytes * count;
     }
     for (int s = 0; s < 2; ++s) {
-        cudaError_t e = cudaStreamSynchronize(ctx->pipe[s].stream);
+        clatch_ctx::PipeSlot& slot = ctx->pipe[s];
+        cudaError_t e = cudaStreamSynchronize(slot.stream);
         if (e != cudaSuccess && !rc) rc = cuda_fail(e, "cudaStreamSynchronize(batch)");
+        if (slot.pending_out && !rc) std::memcpy(slot.pending_out, slot.h_desc.ptr, slot.pending_bytes);
+        slot.pending_out = nullptr;
     }
     return rc;
 }

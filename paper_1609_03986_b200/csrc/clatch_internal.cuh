@@ -81,7 +81,9 @@ struct clatch_ctx {
     struct PipeSlot {                // describe_batch: one of two pipeline slots
         cudaStream_t stream = nullptr;
         clatch::DeviceBuffer img, kps, desc, img_u8, flags;
-        std::vector<double> xycs;
+        clatch::PinnedBuffer h_xycs, h_desc;   // page-locked staging
+        uint8_t* pending_out = nullptr;         // caller array awaiting h_desc
+        size_t pending_bytes = 0;
     } pipe[2];
 };
 
