@@ -42,6 +42,7 @@ typedef struct clatch_ctx clatch_ctx;
  * so a shim can re-raise latch::Error(static_cast<ErrorCode>(rc - 100), clatch_last_error()). */
 enum {
     CLATCH_OK = 0,
+    CLATCH_ERR_IMAGE_TOO_SMALL = 106,     /* ErrorCode::ImageTooSmall     (src/detect.cpp:77-78) */
     CLATCH_ERR_INVALID = 1,      /* null pointer, bad size, bad pitch ... */
     CLATCH_ERR_CUDA = 2,         /* a CUDA runtime call failed; see clatch_last_error() */
     CLATCH_ERR_NO_DEVICE = 3,    /* no CUDA device / not an sm_100 part */
@@ -103,6 +104,23 @@ CLATCH_API int clatch_descriptor_bytes(clatch_ctx* ctx);
  * CLATCH_ERR_NONFINITE if a kept keypoint has a non-finite theta. */
 CLATCH_API int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, int height,
                              int workers, double* xycs, int64_t* kept, size_t* m);
+
+/* ---- detection (the step before the path: fast_detect / detect_and_orient,
+ * src/detect.cpp:76-157) -------------------------------------------------------------------
+ * FAST-9 segment test with `threshold`, optional 3x3 non-maximum suppression (ties keep the
+ * smallest (y, x)), and — when `orient` — the intensity-centroid angle over a disc of `radius`
+ * (15 in the reference); detections whose disc leaves the image are dropped. The moments are
+ * accumulated on the device in the reference's order; atan2 runs on the host libm. Output
+ * rows {x, y, theta, score} in (y, x) order, bit-identical to the reference. If more than
+ * `cap` rows are found, *count still reports the number and the call fails with
+ * CLATCH_ERR_INVALID (call again with a larger buffer). Images smaller than 7x7 fail with
+ * CLATCH_ERR_IMAGE_TOO_SMALL. */
+CLATCH_API int clatch_detect_u8(clatch_ctx* ctx, const uint8_t* img, int width, int height, size_t pitch,
+                     double threshold, int nms, int orient, int radius, double* out, size_t cap,
+                     size_t* count);
+CLATCH_API int clatch_detect_f64(clatch_ctx* ctx, const double* img, int width, int height, size_t pitch,
+                      double threshold, int nms, int orient, int radius, double* out, size_t cap,
+                      size_t* count);
 
 /* ---- extraction (replaces describe / describe_all, src/descriptor.cpp:79-105; the
  * arithmetic of extract_window :29-49, sample_bilinear src/image.cpp:109-126 and

@@ -115,6 +115,11 @@ class Port:
         L.oracle_match.argtypes = [_u8p, C.c_size_t, _u8p, C.c_size_t, C.c_int, C.c_int,
                                    C.c_double, C.c_int, C.c_int, C.c_int, _i32p]
         L.oracle_match.restype = C.c_size_t
+        L.oracle_fast_detect.argtypes = [_f64p, C.c_int, C.c_int, C.c_double, C.c_int, _f64p, C.c_size_t]
+        L.oracle_fast_detect.restype = C.c_size_t
+        L.oracle_detect_and_orient.argtypes = [_f64p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, _f64p,
+                                               C.c_size_t]
+        L.oracle_detect_and_orient.restype = C.c_size_t
 
     # ---- generators ----
     def rng_next(self, seed, n):
@@ -197,6 +202,22 @@ class Port:
                                          _p(kept, _i64p), _p(desc, _u8p))
         return kept[:m].copy(), desc[:m].copy()
 
+    # ---- detection ----
+    def detect(self, image, threshold=20.0, nms=True, orient=True, radius=15):
+        """fast_detect / detect_and_orient -> (N, 4) float64 [x, y, theta, score]."""
+        image = np.ascontiguousarray(image, np.float64)
+        h, w = image.shape
+        cap = max(w * h, 1)
+        out = np.empty((cap, 4), np.float64)
+        if orient:
+            n = self.lib.oracle_detect_and_orient(_p(image, _f64p), w, h, threshold, int(nms), radius,
+                                                  _p(out, _f64p), cap)
+        else:
+            n = self.lib.oracle_fast_detect(_p(image, _f64p), w, h, threshold, int(nms), _p(out, _f64p), cap)
+        if n == C.c_size_t(-1).value:
+            raise RuntimeError("ImageTooSmall")
+        return out[:n].copy()
+
     # ---- matching ----
     def hamming(self, a, b):
         a = np.ascontiguousarray(a, np.uint8)
@@ -256,6 +277,8 @@ class Ref:
                                         C.c_size_t]
         L.ref_detect_and_orient.argtypes = [_f64p, C.c_int, C.c_int, C.c_double, C.c_int, _f64p,
                                             C.c_size_t, C.POINTER(C.c_size_t)]
+        L.ref_fast_detect.argtypes = [_f64p, C.c_int, C.c_int, C.c_double, C.c_int, _f64p,
+                                      C.c_size_t, C.POINTER(C.c_size_t)]
         L.ref_load_pgm.argtypes = [C.c_char_p, _f64p, C.c_size_t, _i32p, _i32p]
         L.ref_keypoint_in_margin.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double]
         L.ref_extract_window.argtypes = [_f64p, C.c_int, C.c_int, _f64p, _f64p]
@@ -340,10 +363,22 @@ class Ref:
                                           C.byref(w), C.byref(h)))
         return out
 
+    def detect(self, image, threshold=20.0, nms=True, orient=True):
+        if orient:
+            return self.detect_and_orient(image, threshold, nms)
+        image = np.ascontiguousarray(image, np.float64)
+        h, w = image.shape
+        cap = max(w * h, 1)
+        out = np.empty((cap, 4), np.float64)
+        cnt = C.c_size_t()
+        self._check(self.lib.ref_fast_detect(_p(image, _f64p), w, h, threshold, int(nms), _p(out, _f64p), cap,
+                                             C.byref(cnt)))
+        return out[:cnt.value].copy()
+
     def detect_and_orient(self, image, threshold=20.0, nms=True):
         image = np.ascontiguousarray(image, np.float64)
         h, w = image.shape
-        cap = 1 << 16
+        cap = max(w * h, 1)
         out = np.empty((cap, 4), np.float64)
         cnt = C.c_size_t()
         self._check(self.lib.ref_detect_and_orient(_p(image, _f64p), w, h, threshold, int(nms),

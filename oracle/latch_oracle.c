@@ -376,3 +376,137 @@ size_t oracle_match(const uint8_t* probes, size_t q, const uint8_t* gallery, siz
     free(reverse_best);
     return m;
 }
+
+/* ------------------------------------------------------------------------
+ * Detection (the step before the hot path; "next" row of SURVEY.md §8f)
+ * ---------------------------------------------------------------------- */
+
+/* Radius-3 Bresenham circle, clockwise from 12 o'clock — src/detect.cpp:14-16. */
+static const int kCircleX[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
+static const int kCircleY[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+
+/* evaluate_arc — src/detect.cpp:26-66: segment test at (x, y); score of the maximal
+ * contiguous qualifying arc (bright polarity tried first), 0 when it does not fire. */
+static double evaluate_arc(const double* img, int w, int x, int y, double threshold) {
+    const double center = img[(size_t)y * w + x];
+    const double hi = center + threshold;
+    const double lo = center - threshold;
+    int bright[16], dark[16];
+    for (int i = 0; i < 16; ++i) {
+        const double v = img[(size_t)(y + kCircleY[i]) * w + (x + kCircleX[i])];
+        bright[i] = v > hi;
+        dark[i] = v < lo;
+    }
+    for (int pol = 0; pol < 2; ++pol) {
+        const int* mask = pol == 0 ? bright : dark;
+        int best_len = 0, best_start = 0, run = 0;
+        for (int i = 0; i < 32; ++i) {   /* two laps cover the wraparound */
+            if (mask[i % 16]) {
+                ++run;
+                if (run > best_len) {
+                    best_len = run;
+                    best_start = i - run + 1;
+                }
+            } else {
+                run = 0;
+            }
+        }
+        if (best_len > 16) best_len = 16;
+        if (best_len < 9) continue;
+        double score = 0.0;
+        for (int i = best_start; i < best_start + best_len; ++i) {
+            const int idx = ((i % 16) + 16) % 16;
+            score += fabs(img[(size_t)(y + kCircleY[idx]) * w + (x + kCircleX[idx])] - center) - threshold;
+        }
+        return score;
+    }
+    return 0.0;
+}
+
+/* fast_detect — src/detect.cpp:76-117. out: up to cap rows {x, y, 0, score} in (y, x)
+ * order. Returns the number of detections (which may exceed cap), or (size_t)-1 for an
+ * image smaller than 7x7 (reference: ImageTooSmall). */
+size_t oracle_fast_detect(const double* img, int w, int h, double threshold, int do_nms, double* out,
+                          size_t cap) {
+    if (w < 7 || h < 7) return (size_t)-1;
+    const int x_end = w - 3, y_end = h - 3;
+    double* scores = (double*)calloc((size_t)w * h, sizeof(double));
+    for (int y = 3; y < y_end; ++y)
+        for (int x = 3; x < x_end; ++x) scores[(size_t)y * w + x] = evaluate_arc(img, w, x, y, threshold);
+    size_t n = 0;
+    for (int y = 3; y < y_end; ++y) {
+        for (int x = 3; x < x_end; ++x) {
+            const double s = scores[(size_t)y * w + x];
+            if (s <= 0.0) continue;
+            if (do_nms) {
+                int is_max = 1;
+                for (int dy = -1; dy <= 1 && is_max; ++dy) {
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        if (dx == 0 && dy == 0) continue;
+                        const int nx = x + dx, ny = y + dy;
+                        if (nx < 3 || ny < 3 || nx >= x_end || ny >= y_end) continue;
+                        const double ns = scores[(size_t)ny * w + nx];
+                        /* ties keep the lexicographically smallest (y, x) */
+                        if (ns > s || (ns == s && (ny < y || (ny == y && nx < x)))) {
+                            is_max = 0;
+                            break;
+                        }
+                    }
+                }
+                if (!is_max) continue;
+            }
+            if (n < cap) {
+                out[4 * n + 0] = (double)x;
+                out[4 * n + 1] = (double)y;
+                out[4 * n + 2] = 0.0;
+                out[4 * n + 3] = s;
+            }
+            ++n;
+        }
+    }
+    free(scores);
+    return n;
+}
+
+/* orient — src/detect.cpp:119-146 for an integer-centred keypoint (every FAST detection):
+ * theta = atan2(m01, m10) over the disc u^2 + v^2 <= radius^2, 0 when both moments vanish.
+ * Returns 1 (and leaves theta alone) when the disc leaves the image. */
+int oracle_orient(const double* img, int w, int h, double x, double y, int radius, double* theta) {
+    if (!(x - radius >= 0.0 && y - radius >= 0.0 && x + radius <= w - 1 && y + radius <= h - 1)) return 1;
+    double m10 = 0.0, m01 = 0.0;
+    for (int v = -radius; v <= radius; ++v)
+        for (int u = -radius; u <= radius; ++u) {
+            if (u * u + v * v > radius * radius) continue;
+            const double intensity = img[(size_t)((int)y + v) * w + ((int)x + u)];
+            m10 += u * intensity;
+            m01 += v * intensity;
+        }
+    *theta = (m10 == 0.0 && m01 == 0.0) ? 0.0 : atan2(m01, m10);
+    return 0;
+}
+
+/* detect_and_orient — src/detect.cpp:148-157. */
+size_t oracle_detect_and_orient(const double* img, int w, int h, double threshold, int do_nms, int radius,
+                                double* out, size_t cap) {
+    const size_t raw_cap = (size_t)w * h;
+    double* raw = (double*)malloc(sizeof(double) * 4 * (raw_cap ? raw_cap : 1));
+    const size_t n = oracle_fast_detect(img, w, h, threshold, do_nms, raw, raw_cap);
+    if (n == (size_t)-1) {
+        free(raw);
+        return n;
+    }
+    size_t m = 0;
+    for (size_t i = 0; i < n; ++i) {
+        double theta = 0.0;
+        if (oracle_orient(img, w, h, raw[4 * i], raw[4 * i + 1], radius, &theta)) continue;
+        if (m < cap) {
+            out[4 * m + 0] = raw[4 * i];
+            out[4 * m + 1] = raw[4 * i + 1];
+            out[4 * m + 2] = theta;
+            out[4 * m + 3] = raw[4 * i + 3];
+        }
+        ++m;
+    }
+    free(raw);
+    return m;
+}

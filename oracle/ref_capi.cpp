@@ -163,6 +163,20 @@ int ref_detect_and_orient(const double* img, int w, int h, double threshold, int
     });
 }
 
+int ref_fast_detect(const double* img, int w, int h, double threshold, int nms, double* out_kps,
+                    std::size_t cap, std::size_t* count) {
+    return guarded([&] {
+        const auto kps = latch::fast_detect(make_image(img, w, h), threshold, nms != 0);
+        *count = kps.size();
+        for (std::size_t i = 0; i < kps.size() && i < cap; ++i) {
+            out_kps[4 * i + 0] = kps[i].x;
+            out_kps[4 * i + 1] = kps[i].y;
+            out_kps[4 * i + 2] = kps[i].theta;
+            out_kps[4 * i + 3] = kps[i].score;
+        }
+    });
+}
+
 int ref_load_pgm(const char* path, double* out, std::size_t cap, int* w, int* h) {
     return guarded([&] {
         const latch::Image im = latch::load_pgm_file(path);

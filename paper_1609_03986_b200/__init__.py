@@ -6,8 +6,8 @@ Drop-in for the two hot paths of the reference package ``latchkit``
 shapes/dtypes and exception types, and produce bit-identical results; the work
 runs in hand-written sm_100a kernels behind the C ABI in include/clatch.h.
 
-Not provided (outside the hot path): detect, evaluate, train, warp,
-load_pgm, save_pgm — keep using the reference's host code for those.
+``detect`` (FAST-9 + NMS + orientation, the step before the path) is provided as well.
+Not provided (outside the hot path): evaluate, train, warp, load_pgm, save_pgm — keep using the reference's host code for those.
 """
 from __future__ import annotations
 
@@ -25,7 +25,7 @@ window_margin = 46
 orientation_radius = 15
 
 __all__ = [
-    "default_pattern", "describe", "describe_batch", "descriptor_bits", "descriptor_bytes", "hamming", "match",
+    "default_pattern", "describe", "describe_batch", "descriptor_bits", "detect", "descriptor_bytes", "hamming", "match",
     "orientation_radius", "window_margin", "Engine", "DescriptorSet", "get_engine", "LatchError",
     "ClatchDeviceError", "TripletPattern", "parse_pattern", "format_pattern",
 ]
@@ -65,6 +65,14 @@ def _descriptor_array(a, what: str) -> np.ndarray:
     if a.ndim != 2:
         raise ValueError(f"{what} must be a (N, descriptor_bytes) uint8 array")
     return np.ascontiguousarray(a)
+
+
+def detect(image, threshold=20.0, nms=True, orient=True):
+    """FAST-9 corners as an (N, 4) array [x, y, theta, score] — latchkit.detect
+    (bindings/module.cpp:100-105 -> fast_detect / detect_and_orient, src/detect.cpp:76-157).
+    With orient, theta is the intensity-centroid angle (radius 15) and detections whose
+    orientation disc leaves the image are dropped. Images smaller than 7x7 raise RuntimeError."""
+    return get_engine().detect(_image_array(image), threshold, nms, orient, orientation_radius)
 
 
 def describe(image, keypoints, pattern=None, workers=0):

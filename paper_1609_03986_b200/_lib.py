@@ -19,7 +19,7 @@ ERR_NONFINITE = 5
 
 # 100 + latch::ErrorCode (proj/include/latch/errors.hpp:10-40)
 ERROR_NAMES = {
-    107: "TooCloseToBorder", 108: "BadHeader", 109: "BadTripletCount",
+    106: "ImageTooSmall", 107: "TooCloseToBorder", 108: "BadHeader", 109: "BadTripletCount",
     110: "CoordinateOutOfRange", 111: "DegenerateTriplet", 119: "LengthMismatch",
     120: "EmptyGallery",
 }
@@ -57,6 +57,10 @@ _SIGNATURES = {
     "clatch_descriptor_bytes": (C.c_int, [C.c_void_p]),
     "clatch_prepare_keypoints": (C.c_int, [f64p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, f64p,
                                            i64p, szp]),
+    "clatch_detect_u8": (C.c_int, [C.c_void_p, u8p, C.c_int, C.c_int, C.c_size_t, C.c_double, C.c_int, C.c_int,
+                                   C.c_int, f64p, C.c_size_t, szp]),
+    "clatch_detect_f64": (C.c_int, [C.c_void_p, f64p, C.c_int, C.c_int, C.c_size_t, C.c_double, C.c_int, C.c_int,
+                                    C.c_int, f64p, C.c_size_t, szp]),
     "clatch_extract_u8": (C.c_int, [C.c_void_p, u8p, C.c_int, C.c_int, C.c_size_t, f64p, C.c_size_t,
                                     u8p]),
     "clatch_extract_f64": (C.c_int, [C.c_void_p, f64p, C.c_int, C.c_int, C.c_size_t, f64p, C.c_size_t,

@@ -210,7 +210,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
         cudaStreamDestroy(ctx->stream);
     }
     for (DeviceBuffer* b : {&ctx->img, &ctx->kps, &ctx->desc, &ctx->q, &ctx->t, &ctx->res,
-                            &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->items, &ctx->pattern.slots, &ctx->pattern.slots_quad,
+                            &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->items, &ctx->scores, &ctx->counts, &ctx->det, &ctx->pattern.slots, &ctx->pattern.slots_quad,
                             &ctx->pattern.triplets})
         b->release();
     ctx->pinned.release();
@@ -499,6 +499,54 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
     return CLATCH_OK;
 }
 
+template <typename Pixel>
+static int detect_impl(clatch_ctx* ctx, const Pixel* img, int width, int height, size_t pitch, double threshold,
+                       int nms, int orient, int radius, double* out, size_t cap, size_t* count) {
+    if (!count) return invalid("detect: count is null");
+    *count = 0;
+    if (!ctx) return invalid("detect: ctx is null");
+    if (!img || width <= 0 || height <= 0 || pitch < static_cast<size_t>(width))
+        return invalid("detect: bad image (null, empty or pitch < width)");
+    if (width < 7 || height < 7) {   // src/detect.cpp:77-78
+        set_error("ImageTooSmall: FAST needs at least a 7x7 image");
+        return CLATCH_ERR_IMAGE_TOO_SMALL;
+    }
+    if (radius < 0 || !std::isfinite(threshold)) return invalid("detect: bad radius or threshold");
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = ctx->img.reserve(sizeof(Pixel) * static_cast<size_t>(width) * height)) return rc;
+    cudaStream_t st = ctx->stream;
+    CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, sizeof(Pixel) * width, img, sizeof(Pixel) * pitch,
+                                  sizeof(Pixel) * width, height, cudaMemcpyHostToDevice, st));
+    unsigned total = 0;
+    int rc;
+    if (sizeof(Pixel) == 1)
+        rc = launch_detect_u8(ctx, ctx->img.as<uint8_t>(), width, height, width, threshold, nms, orient, radius, st,
+                              &total);
+    else
+        rc = launch_detect_f64(ctx, ctx->img.as<double>(), width, height, width, threshold, nms, orient, radius, st,
+                               &total);
+    if (rc) return rc;
+    if (total == 0) return CLATCH_OK;
+    std::vector<Detection> det(total);
+    CLATCH_CUDA(cudaMemcpyAsync(det.data(), ctx->det.ptr, sizeof(Detection) * total, cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    size_t m = 0;
+    for (const Detection& d : det) {
+        if (orient && !d.valid) continue;   // disc leaves the image, src/detect.cpp:152-154
+        if (m < cap && out) {
+            out[4 * m + 0] = static_cast<double>(d.x);
+            out[4 * m + 1] = static_cast<double>(d.y);
+            // src/detect.cpp:144 — host libm, like the reference
+            out[4 * m + 2] = orient ? ((d.m10 == 0.0 && d.m01 == 0.0) ? 0.0 : std::atan2(d.m01, d.m10)) : 0.0;
+            out[4 * m + 3] = d.score;
+        }
+        ++m;
+    }
+    *count = m;
+    if (m > cap) return invalid("detect: output buffer too small (see *count)");
+    return CLATCH_OK;
+}
+
 // Two-slot software pipeline over images: slot = i % 2 owns a stream and its own device
 // scratch, so image i+1 uploads / prepares while image i computes and downloads.
 template <typename Pixel>
@@ -587,6 +635,16 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
 }
 
 extern "C" {
+
+int clatch_detect_u8(clatch_ctx* ctx, const uint8_t* img, int width, int height, size_t pitch, double threshold,
+                     int nms, int orient, int radius, double* out, size_t cap, size_t* count) {
+    return detect_impl<uint8_t>(ctx, img, width, height, pitch, threshold, nms, orient, radius, out, cap, count);
+}
+
+int clatch_detect_f64(clatch_ctx* ctx, const double* img, int width, int height, size_t pitch, double threshold,
+                      int nms, int orient, int radius, double* out, size_t cap, size_t* count) {
+    return detect_impl<double>(ctx, img, width, height, pitch, threshold, nms, orient, radius, out, cap, count);
+}
 
 int clatch_describe_batch_u8(clatch_ctx* ctx, const uint8_t* const* imgs, const int* widths, const int* heights,
                              const size_t* pitches, const double* const* kps, const size_t* counts, int cols,

@@ -75,7 +75,7 @@ struct clatch_ctx {
     int extract_variant = 1;       // 0: one window per CTA (4 CTAs/SM), 1: quad kernel (4 windows per CTA)
     int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
     // scratch for the host-buffer entry points
-    clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t, items;
+    clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t, items, scores, counts, det;
     std::vector<double> host_xycs;   // describe_all staging
     clatch::PinnedBuffer pinned;     // D2H staging for batched pair results
     struct PipeSlot {                // describe_batch: one of two pipeline slots
@@ -95,6 +95,17 @@ int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int heig
                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
 int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
                        const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
+
+// detection (clatch_detect.cu)
+struct Detection {   // one FAST detection as the device leaves it (row-major order)
+    int x, y;
+    double score, m10, m01;
+    int valid, pad;  // valid = 0: orientation disc leaves the image
+};
+int launch_detect_u8(clatch_ctx* ctx, const uint8_t* d_img, int w, int h, size_t pitch, double threshold, int nms,
+                     int orient, int radius, cudaStream_t st, unsigned* count);
+int launch_detect_f64(clatch_ctx* ctx, const double* d_img, int w, int h, size_t pitch, double threshold, int nms,
+                      int orient, int radius, cudaStream_t st, unsigned* count);
 
 // matching (clatch_match.cu, clatch_match_tc.cu)
 struct Partial {   // per (train split, query) partial top-2

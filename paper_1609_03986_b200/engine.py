@@ -114,6 +114,33 @@ class Engine:
                                                      _ptr(xycs, f64p), _ptr(kept, i64p), C.byref(m)))
         return xycs[:m.value], kept[:m.value]
 
+    # ---- detection ----------------------------------------------------------------------
+    def detect(self, image: np.ndarray, threshold: float = 20.0, nms: bool = True, orient: bool = True,
+               radius: int = 15) -> np.ndarray:
+        """FAST-9 (+ NMS, + intensity-centroid angle) -> (N, 4) float64 [x, y, theta, score]."""
+        h, w = image.shape
+        if image.strides[1] != image.itemsize or image.strides[0] % image.itemsize:
+            image = np.ascontiguousarray(image)
+        pitch = image.strides[0] // image.itemsize
+        if image.dtype == np.uint8:
+            fn, ptr = self.lib.clatch_detect_u8, _ptr(image, u8p)
+        elif image.dtype == np.float64:
+            fn, ptr = self.lib.clatch_detect_f64, _ptr(image, f64p)
+        else:
+            raise TypeError("image dtype must be uint8 or float64")
+        cap = max(1024, (w * h) // 64)
+        count = C.c_size_t()
+        while True:
+            out = np.empty((cap, 4), np.float64)
+            with self._lock:
+                rc = fn(self.ctx, ptr, w, h, pitch, float(threshold), int(nms), int(orient), int(radius),
+                        _ptr(out, f64p), cap, C.byref(count))
+            if rc == _lib.ERR_INVALID and count.value > cap:
+                cap = count.value
+                continue
+            _lib.check(rc)
+            return out[:count.value].copy()
+
     # ---- extraction, host buffers --------------------------------------------
     def extract(self, image: np.ndarray, xycs: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
         """image: 2-D uint8 or float64 (rows may be strided); xycs from prepare_keypoints."""

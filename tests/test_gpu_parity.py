@@ -476,3 +476,50 @@ def test_describe_batch_matches_per_image_calls(lk, port):
     for (gk, gd), im, k in zip(lk.describe_batch(fimgs, fk), fimgs, fk):
         assert np.array_equal(gd, port.describe_all(im, k)[1])
     assert lk.describe_batch([], []) == []
+
+
+# ------------------------------------------------------------------- detection ----
+
+def test_detect_golden_keypoints(lk, golden_image_u8):
+    # acceptance.cpp:120-123: detect_and_orient(golden, 20, nms) is pinned by golden_keypoints.tsv
+    want = np.load(GOLDEN / "golden_keypoints_f64.npy")
+    for img in (golden_image_u8, golden_image_u8.astype(np.float64)):
+        got = lk.detect(img, threshold=20.0)
+        assert got.dtype == np.float64 and np.array_equal(got, want)
+
+
+def test_detect_reference_vectors(lk, port, vectors):
+    for tag, maker, args, thr, nms, ori in [("struct", "structured_image", (1, 160, 120), 20.0, True, True),
+                                            ("noise", "random_image", (2, 96, 80), 30.5, True, True),
+                                            ("nonms", "random_image", (3, 64, 48), 12.25, False, False)]:
+        img = getattr(port, maker)(*args)
+        for im in (img, img.astype(np.uint8)):
+            assert np.array_equal(lk.detect(im, thr, nms, ori), vectors[f"det_{tag}_out"]), tag
+    assert np.array_equal(lk.detect(vectors["det_frac_image"], 40.0), vectors["det_frac_out"])
+
+
+def test_detect_against_oracle_and_edge_cases(lk, port):
+    for seed, (w, h), thr, nms, ori in [(5, (640, 480), 20.0, True, True), (6, (333, 201), 25.5, False, True),
+                                        (7, (97, 61), 20.0, True, False), (8, (1920, 1080), 20.0, True, True)]:
+        img = port.structured_image(seed, w, h) if seed != 6 else port.random_image(seed, w, h)
+        want = port.detect(img, thr, nms, ori)
+        assert np.array_equal(lk.detect(img.astype(np.uint8), thr, nms, ori), want), (seed, "u8")
+        assert np.array_equal(lk.detect(img, thr, nms, ori), want), (seed, "f64")
+    # test_detect.cpp:34-41: uniform image -> nothing; too small -> ImageTooSmall
+    assert lk.detect(np.full((32, 32), 77.0)).shape == (0, 4)
+    with pytest.raises(RuntimeError):
+        lk.detect(np.zeros((32, 6)))
+    with pytest.raises(ValueError):
+        lk.detect(np.zeros(16))
+    # test_detect.cpp:43-74: bright square corners fire
+    sq = np.zeros((32, 32))
+    sq[12:20, 12:20] = 255.0
+    got = lk.detect(sq, 20.0, nms=False, orient=False)
+    assert np.array_equal(got, port.detect(sq, 20.0, False, False)) and len(got) > 0
+    # detect -> describe -> match chain on the GPU (python/test_smoke.py:30-53)
+    img = port.structured_image(11, 400, 300)
+    kps = lk.detect(img)
+    kept, desc = lk.describe(img, kps)
+    assert np.array_equal(desc, port.describe_all(img, kps)[1]) and len(desc) > 0
+    m = lk.match(desc, desc)
+    assert np.all(m[:, 2] == 0)

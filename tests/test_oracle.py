@@ -161,3 +161,35 @@ def test_port_equals_reference_live(port, ref):
     for kw in ({}, {"ratio": 0.8}, {"cross_check": True}, {"max_distance": 230},
                {"ratio": 0.85, "cross_check": True, "max_distance": 235}):
         assert np.array_equal(port.match(probes, gallery, **kw), ref.match(probes, gallery, **kw))
+
+
+# ---- detection (next row): restatement vs golden keypoints, vectors and the live reference ----
+
+DET_CASES = [("struct", "structured_image", (1, 160, 120), 20.0, True, True),
+             ("noise", "random_image", (2, 96, 80), 30.5, True, True),
+             ("nonms", "random_image", (3, 64, 48), 12.25, False, False)]
+
+
+def test_detect_golden_keypoints(port, golden_image_u8):
+    want = np.load(GOLDEN / "golden_keypoints_f64.npy")
+    assert np.array_equal(port.detect(golden_image_u8.astype(np.float64), 20.0, True, True), want)
+
+
+@pytest.mark.parametrize("tag,maker,args,thr,nms,ori", DET_CASES)
+def test_detect_vectors(port, vectors, tag, maker, args, thr, nms, ori):
+    got = port.detect(getattr(port, maker)(*args), thr, nms, ori)
+    assert np.array_equal(got, vectors[f"det_{tag}_out"])
+
+
+def test_detect_non_integer_image(port, vectors):
+    assert np.array_equal(port.detect(vectors["det_frac_image"], 40.0, True, True), vectors["det_frac_out"])
+
+
+def test_detect_live_reference(port, ref):
+    for seed, (w, h), thr, nms, ori in [(5, (320, 240), 20.0, True, True), (6, (200, 150), 25.5, False, True),
+                                        (7, (97, 61), 20.0, True, False)]:
+        for maker in ("structured_image", "random_image"):
+            im = getattr(port, maker)(seed, w, h)
+            assert np.array_equal(port.detect(im, thr, nms, ori), ref.detect(im, thr, nms, ori))
+    with pytest.raises(RuntimeError):
+        port.detect(np.zeros((32, 6)))
