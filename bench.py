@@ -225,7 +225,8 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    use_dist = "RANK" in os.environ          # under torchrun (any world size) exercise the NCCL path
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -264,7 +265,7 @@ def run_ours(args):
         flush.zero_()
     events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     launches0 = eng.launch_count
     with ClockSampler(local) as clocks:
@@ -273,14 +274,14 @@ def run_ours(args):
             step(events[i])
             flush.zero_()                     # L2 flush between steps, outside the event pairs
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dist:
             dist.barrier()
         t_wall = time.perf_counter() - t_wall0
     launches = eng.launch_count - launches0
     t_ext = sum(e[0].elapsed_time(e[1]) for e in events) / 1e3
     t_mat = sum(e[1].elapsed_time(e[2]) for e in events) / 1e3
     t_dev = t_ext + t_mat
-    if world > 1:
+    if use_dist:
         t = torch.tensor([t_dev, t_ext, t_mat], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_dev, t_ext, t_mat = t.tolist()
@@ -302,14 +303,14 @@ def run_ours(args):
         for _ in range(max(3, args.warmup)):
             api_step()
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             out = api_step()
         torch.cuda.synchronize()
         t_api = time.perf_counter() - t0
-        if world > 1:
+        if use_dist:
             dist.barrier()
             tt = torch.tensor([t_api], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -323,7 +324,7 @@ def run_ours(args):
         assert len(out) == m
 
     if rank != 0:
-        if world > 1:
+        if use_dist:
             dist.destroy_process_group()
         return
 
@@ -423,7 +424,7 @@ def run_ours(args):
         "device": eng.name, "sm_count": sms,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

@@ -1,0 +1,35 @@
+#!/usr/bin/env python
+"""Small end-to-end pass over every kernel for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import oracle                                  # noqa: E402
+import paper_1609_03986_b200 as lk             # noqa: E402
+
+port = oracle.port()
+eng = lk.get_engine()
+img = port.structured_image(3, 320, 240)
+kps = lk.detect(img)
+kps = np.vstack([kps, port.random_keypoints(4, 320, 240, 37)])
+for variant in (0, 1):
+    eng.set_option("extract_variant", variant)
+    for im in (img.astype(np.uint8), img, img + 0.25):
+        kept, desc = lk.describe(im, kps)
+        assert np.array_equal(desc, port.describe_all(im.astype(np.float64), kps)[1])
+text = (ROOT / "tests/golden/pattern_t64k5w.latchpat").read_text()
+lk.describe(img, kps[:50], pattern=text)
+kept, desc = lk.describe(img.astype(np.uint8), kps)
+for variant in (0, 1, 2, 3):
+    eng.set_option("match_variant", variant)
+    got = lk.match(desc, desc[::2], ratio=0.9, cross_check=True)
+    assert np.array_equal(got, port.match(desc, desc[::2], ratio=0.9, cross_check=True))
+d13 = port.random_descriptors(1, 90, 13)
+lk.match(d13[:40], d13[40:])
+sets = [eng.create_set(desc[:300]), eng.create_set(desc[300:]), eng.create_set(desc[::3])]
+eng.match_set_pairs(sets, [(0, 1), (1, 2), (2, 0)], ratio=0.8, cross_check=True)
+lk.describe_batch([img.astype(np.uint8)] * 3, [kps, kps[:10], kps[:200]])
+print("sanitize pass done:", len(desc), "descriptors")
