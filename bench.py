@@ -227,6 +227,9 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     use_dist = "RANK" in os.environ          # under torchrun (any world size) exercise the NCCL path
     if use_dist:
+        # NCCL_DEBUG=VERSION/INFO writes to stdout; keep stdout to the one JSON line
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", "INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

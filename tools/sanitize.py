@@ -29,7 +29,8 @@ for variant in (0, 1, 2, 3):
     assert np.array_equal(got, port.match(desc, desc[::2], ratio=0.9, cross_check=True))
 d13 = port.random_descriptors(1, 90, 13)
 lk.match(d13[:40], d13[40:])
-sets = [eng.create_set(desc[:300]), eng.create_set(desc[300:]), eng.create_set(desc[::3])]
+third = max(1, len(desc) // 3)
+sets = [eng.create_set(desc[:third]), eng.create_set(desc[third:]), eng.create_set(desc[::3])]
 eng.match_set_pairs(sets, [(0, 1), (1, 2), (2, 0)], ratio=0.8, cross_check=True)
 lk.describe_batch([img.astype(np.uint8)] * 3, [kps, kps[:10], kps[:200]])
 print("sanitize pass done:", len(desc), "descriptors")
