@@ -727,10 +727,9 @@ int clatch_match_top2(clatch_ctx* ctx, const uint8_t* queries, size_t Q, const u
 struct clatch_set {
     clatch_ctx* ctx = nullptr;
     size_t n = 0;
-    uint8_t* block = nullptr;   // one stream-ordered allocation: packed | A-form | B-form
+    uint8_t* block = nullptr;   // one stream-ordered allocation: packed | int8 operand form
     uint8_t* packed = nullptr;
-    uint8_t* exp_a = nullptr;
-    uint8_t* exp_b = nullptr;
+    uint8_t* exp = nullptr;
 };
 
 namespace {
@@ -758,12 +757,12 @@ int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t
         const clatch_set* b = sets[pairs[2 * (first + p) + 1]];
         int32_t* base = r + pair_offset[p];
         for (int q = 0; q < tc_query_tiles(a->n); ++q)
-            table.push_back({a->exp_a, b->exp_b, static_cast<unsigned>(a->n),
+            table.push_back({a->exp, b->exp, static_cast<unsigned>(a->n),
                              static_cast<unsigned>(b->n), static_cast<unsigned>(q), 0, base, base + a->n,
                              base + 2 * a->n});
         if (cross_check)   // reverse_best[g] = knn2(gallery[g], probes).best_index, src/match.cpp:62-67
             for (int q = 0; q < tc_query_tiles(b->n); ++q)
-                table.push_back({b->exp_a, a->exp_b, static_cast<unsigned>(b->n),
+                table.push_back({b->exp, a->exp, static_cast<unsigned>(b->n),
                                  static_cast<unsigned>(a->n), static_cast<unsigned>(q), 0, base + 3 * a->n, nullptr,
                                  nullptr});
     }
@@ -794,20 +793,18 @@ int clatch_set_create(clatch_ctx* ctx, const uint8_t* descriptors, size_t n, int
     if (n > 0) {
         cudaStream_t st = ctx->stream;
         const size_t packed_bytes = (n * 64 + 1023) / 1024 * 1024;
-        const size_t a_bytes = tc_expanded_bytes(n, true), b_bytes = tc_expanded_bytes(n, false);
+        const size_t exp_bytes = tc_expanded_bytes(n);
         // cudaMallocAsync: pooled, stream-ordered — set churn does not pay cudaMalloc/cudaFree latency.
-        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&set->block), packed_bytes + a_bytes + b_bytes, st);
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&set->block), packed_bytes + exp_bytes, st);
         if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocAsync(set)");
         if (!rc) {
             set->packed = set->block;
-            set->exp_a = set->block + packed_bytes;
-            set->exp_b = set->exp_a + a_bytes;
+            set->exp = set->block + packed_bytes;
             e = cudaMemcpyAsync(set->packed, descriptors, n * 64,
                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(set)");
         }
-        if (!rc) rc = launch_tc_expand(ctx, set->packed, n, true, set->exp_a, st);
-        if (!rc) rc = launch_tc_expand(ctx, set->packed, n, false, set->exp_b, st);
+        if (!rc) rc = launch_tc_expand(ctx, set->packed, n, set->exp, st);
         if (!rc && !on_device) {   // the caller may reuse its host buffer as soon as we return
             e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) rc = cuda_fail(e, "cudaStreamSynchronize(set)");

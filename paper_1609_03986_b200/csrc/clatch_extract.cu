@@ -480,13 +480,12 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     p.flags = flags;
     p.run_if_flag = run_if_flag;
     if (pat.fast && ctx->extract_variant == 1) {
-        static bool configured = false;
-        if (!configured) {
+        if (!ctx->quad_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_quad_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kQuadSmemBytes));
             CLATCH_CUDA(cudaFuncSetAttribute(extract_quad_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kQuadSmemBytes));
-            configured = true;
+            ctx->quad_configured = true;
         }
         p.slots = pat.slots_quad.as<ushort4>();
         const size_t quads = (M + kQuad - 1) / kQuad;

@@ -72,6 +72,7 @@ struct clatch_ctx {
     cudaStream_t stream = nullptr;
     clatch::Pattern pattern;
     uint64_t launches = 0;
+    bool tc_configured = false, quad_configured = false;   // opt-in smem sizes set on this device
     int extract_variant = 1;       // 0: one window per CTA (4 CTAs/SM), 1: quad kernel (4 windows per CTA)
     int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
     // scratch for the host-buffer entry points
@@ -115,8 +116,8 @@ struct Partial {   // per (train split, query) partial top-2
     int pad;
 };
 struct TcItem {    // one CTA of the tensor-core matcher in batched mode: 128 queries x a whole train set
-    const uint8_t* a_exp;    // query set, expanded (A layout)
-    const uint8_t* b_exp;    // train set, expanded (B layout)
+    const uint8_t* a_exp;    // query set, expanded
+    const uint8_t* b_exp;    // train set, expanded (same layout)
     unsigned Q, N;           // real row counts
     unsigned qtile;          // which 128-row query tile
     unsigned pad;
@@ -124,10 +125,9 @@ struct TcItem {    // one CTA of the tensor-core matcher in batched mode: 128 qu
     int32_t* best_dist;
     int32_t* second_dist;
 };
-size_t tc_expanded_bytes(size_t rows, bool as_queries);
+size_t tc_expanded_bytes(size_t rows);
 int tc_query_tiles(size_t rows);
-int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, bool as_queries, uint8_t* d_out,
-                     cudaStream_t stream);
+int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t* d_out, cudaStream_t stream);
 int launch_match_tc_items(clatch_ctx* ctx, const TcItem* d_items, size_t count, cudaStream_t stream);
 void launch_merge_partials(const Partial* partial, unsigned long long Q, int splits, int sentinel,
                            int32_t* best_idx, int32_t* best_dist, int32_t* second_dist, cudaStream_t stream);

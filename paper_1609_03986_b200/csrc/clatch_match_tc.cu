@@ -10,12 +10,14 @@
 // compares/s even with carry-save compression; tcgen05.mma kind::i8 does
 // 8192 MAC/clk/SM = 16 compares/clk/SM.
 //
-// Structure (one CTA = 128 queries x a contiguous range of 256-row train tiles):
+// Structure (persistent CTAs, one per SM; a work item = 128 queries x a contiguous range of
+// 256-row train tiles):
 //   expand_kernel        bits -> int8, written to HBM directly in the UMMA canonical K-major
 //                        SWIZZLE_128B layout (8 rows x 128 B atoms, 16-byte chunk index XOR row),
-//                        so every operand tile is one contiguous block in global memory
-//   warp 0 (1 thread)    TMA bulk copies (cp.async.bulk + mbarrier expect-tx): A once (64 KiB),
-//                        B in 4-stage ring of [256 rows x 128 B of K] = 32 KiB stages
+//                        128-row tiles, so every operand block is contiguous in global memory and
+//                        one expansion of a set serves it as queries and as train rows
+//   warp 0 (1 thread)    TMA bulk copies (cp.async.bulk + mbarrier expect-tx): A once per work item
+//                        (64 KiB), B in a 4-stage ring of [256 rows x 128 B of K] = 32 KiB stages
 //   warp 1 (1 thread)    tcgen05.mma.cta_group::1.kind::i8, M=128, N=256, K=32 x 16 per tile,
 //                        accumulators double-buffered in TMEM (2 x 256 columns);
 //                        tcgen05.commit releases smem stages and publishes finished tiles
@@ -43,13 +45,18 @@ constexpr int kTcABytes = kTcM * 512;             // 65536
 constexpr int kTcStageBytes = kTcN * kTcKBlock;   // 32768
 constexpr int kTcEpilogueWarps = 8;
 constexpr int kTcThreads = 32 * (2 + kTcEpilogueWarps);   // 320
-constexpr int kTcSmemBytes = kTcABytes + kTcStages * kTcStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kTcSmemBytes = kTcABytes + kTcStages * kTcStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
+                             2048 /*half-merge buffer*/;
 
 // ---------------------------------------------------------------- expansion ----
-// rows_per_tile = 128 (queries, A operand) or 256 (train, B operand). One thread writes one
-// 16-byte chunk (16 K-elements) of one row. Rows >= n are zero (masked in the epilogue).
+// One layout serves both operands: 128-row tiles, each [4 K-blocks][16 atoms][1024 B]. A query
+// tile (A operand, M = 128) is one 64 KiB block; a train tile (B operand, N = 256) takes, per
+// K-block, the 16 KiB of two consecutive 128-row tiles. One thread writes one 16-byte chunk
+// (16 K-elements) of one row. Rows >= n (padding up to a multiple of 256) are zero and are
+// masked in the epilogue.
 __global__ void expand_kernel(const uint8_t* __restrict__ packed, unsigned long long n,
-                              unsigned long long padded_rows, int rows_per_tile, uint8_t* __restrict__ out) {
+                              unsigned long long padded_rows, uint8_t* __restrict__ out) {
+    constexpr int rows_per_tile = kTcM;
     const unsigned long long idx = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     const unsigned long long row = idx >> 5;          // 32 chunks per row
     if (row >= padded_rows) return;
@@ -148,54 +155,85 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
 }
 
 // ---------------------------------------------------------------- the kernel ----
-// grid = (query tiles, splits). Split s owns train tiles [s*tiles_per_split, ...).
-__global__ void __launch_bounds__(kTcThreads, 1)
-match_tc_kernel(const uint8_t* __restrict__ a_exp_arg, const uint8_t* __restrict__ b_exp_arg, unsigned long long Q_arg,
-                unsigned long long N_arg, int total_tiles, int tiles_per_split, Partial* __restrict__ partial,
-                int* __restrict__ dump /* optional: raw accumulators of this CTA's first tile, 128 x 256 */,
-                const TcItem* __restrict__ items /* optional: one work item per CTA (batched set pairs) */) {
-    // Work of this CTA: either derived from (blockIdx.x = query tile, blockIdx.y = train split) or
-    // read from the item table (batched matching of many set pairs in one launch).
-    const uint8_t* a_exp = a_exp_arg;
-    const uint8_t* b_exp = b_exp_arg;
-    unsigned long long Q = Q_arg, N = N_arg;
-    unsigned qtile = blockIdx.x;
-    int tile_begin = blockIdx.y * tiles_per_split;
-    int tile_end = min(total_tiles, tile_begin + tiles_per_split);
-    int32_t *o_idx = nullptr, *o_best = nullptr, *o_second = nullptr;
-    if (items != nullptr) {
-        const TcItem it = items[blockIdx.x];
-        a_exp = it.a_exp;
-        b_exp = it.b_exp;
-        Q = it.Q;
-        N = it.N;
-        qtile = it.qtile;
-        tile_begin = 0;
-        tile_end = static_cast<int>((it.N + kTcN - 1) / kTcN);
-        o_idx = it.best_idx;
-        o_best = it.best_dist;
-        o_second = it.second_dist;
+// Persistent: gridDim.x CTAs (one per SM) each walk work items blockIdx.x, +gridDim.x, ...
+// A work item = one 128-query tile against a contiguous range of 256-row train tiles. Items
+// come either from (query tile, train split) arithmetic (single match; partial results go to
+// `partial` and are merged afterwards) or from an item table (batched set pairs; each item
+// covers a whole train set and writes final results). Barriers, TMEM and the smem ring are
+// set up once per CTA; only the 64 KiB A operand is reloaded per item.
+struct TcWork {
+    const uint8_t* a;     // expanded query tile (64 KiB)
+    const uint8_t* b;     // expanded train set (B form), tile 0
+    unsigned long long Q, N;
+    unsigned qtile;
+    int tile_begin, ntiles, split;
+    int32_t *o_idx, *o_best, *o_second;   // final outputs (item-table mode) or null
+};
+
+struct TcArgs {
+    const uint8_t* a_exp;
+    const uint8_t* b_exp;
+    unsigned long long Q, N;
+    int qtiles, total_tiles, tiles_per_split, num_items;
+    Partial* partial;
+    int* dump;               // optional: raw accumulators of item 0's first tile, 128 x 256
+    const TcItem* items;     // optional item table
+};
+
+__device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item) {
+    TcWork w;
+    if (g.items != nullptr) {
+        const TcItem it = g.items[item];
+        w.a = it.a_exp + static_cast<unsigned long long>(it.qtile) * kTcABytes;
+        w.b = it.b_exp;
+        w.Q = it.Q;
+        w.N = it.N;
+        w.qtile = it.qtile;
+        w.tile_begin = 0;
+        w.ntiles = static_cast<int>((it.N + kTcN - 1) / kTcN);
+        w.split = 0;
+        w.o_idx = it.best_idx;
+        w.o_best = it.best_dist;
+        w.o_second = it.second_dist;
+    } else {
+        // consecutive CTAs take different query tiles of the SAME split: they stream the same
+        // train tiles at the same time, so HBM sees them once and L2 serves the rest
+        w.split = item / g.qtiles;
+        w.qtile = static_cast<unsigned>(item - w.split * g.qtiles);
+        w.a = g.a_exp + static_cast<unsigned long long>(w.qtile) * kTcABytes;
+        w.b = g.b_exp;
+        w.Q = g.Q;
+        w.N = g.N;
+        w.tile_begin = w.split * g.tiles_per_split;
+        w.ntiles = min(g.total_tiles, w.tile_begin + g.tiles_per_split) - w.tile_begin;
+        w.o_idx = w.o_best = w.o_second = nullptr;
     }
+    return w;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g) {
     extern __shared__ uint8_t smem_raw[];
     const unsigned raw = smem_u32(smem_raw);
     const unsigned base = (raw + 1023u) & ~1023u;              // SWIZZLE_128B atoms need 1024-B alignment
     const unsigned smem_a = base;
     const unsigned smem_b = base + kTcABytes;
     const unsigned bars = smem_b + kTcStages * kTcStageBytes;  // 8-byte mbarriers
-    const unsigned bar_a = bars;
-    const unsigned bar_full = bars + 8;                        // [kTcStages]
+    const unsigned bar_a_full = bars;
+    const unsigned bar_a_empty = bars + 8;
+    const unsigned bar_full = bars + 16;                       // [kTcStages]
     const unsigned bar_empty = bar_full + 8 * kTcStages;       // [kTcStages]
     const unsigned bar_tfull = bar_empty + 8 * kTcStages;      // [2]
     const unsigned bar_tempty = bar_tfull + 16;                // [2]
     uint8_t* const gen_base = smem_raw + (base - raw);
-    volatile unsigned* tmem_slot = reinterpret_cast<volatile unsigned*>(gen_base + kTcABytes + kTcStages * kTcStageBytes + 128);
-    int* merge_buf = reinterpret_cast<int*>(gen_base);         // reused after the main loop (A region)
+    uint8_t* const tail = gen_base + kTcABytes + kTcStages * kTcStageBytes;
+    volatile unsigned* tmem_slot = reinterpret_cast<volatile unsigned*>(tail + 128);
+    int* merge_buf = reinterpret_cast<int*>(tail + 256);       // 128 rows x 4 ints
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntiles = tile_end - tile_begin;
 
     if (threadIdx.x == 0) {
-        mbar_init(bar_a, 1);
+        mbar_init(bar_a_full, 1);
+        mbar_init(bar_a_empty, 1);
         for (int s = 0; s < kTcStages; ++s) {
             mbar_init(bar_full + 8 * s, 1);
             mbar_init(bar_empty + 8 * s, 1);
@@ -219,45 +257,58 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp_arg, const uint8_t* __restrict
     if (warp == 0) {
         // ===== producer =====
         if (lane == 0) {
-            mbar_expect_tx(bar_a, kTcABytes);
-            bulk_load(smem_a, a_exp + static_cast<unsigned long long>(qtile) * kTcABytes, kTcABytes, bar_a);
             int stage = 0;
-            unsigned phase = 0;
-            for (int t = 0; t < ntiles; ++t) {
-                const uint8_t* src = b_exp + static_cast<unsigned long long>(tile_begin + t) * (kTcKBlocks * kTcStageBytes);
-                for (int kb = 0; kb < kTcKBlocks; ++kb) {
-                    mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-                    mbar_expect_tx(bar_full + 8 * stage, kTcStageBytes);
-                    bulk_load(smem_b + stage * kTcStageBytes, src + kb * kTcStageBytes, kTcStageBytes,
-                              bar_full + 8 * stage);
-                    if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+            unsigned phase = 0, a_phase = 0;
+            for (int item = blockIdx.x; item < g.num_items; item += gridDim.x) {
+                const TcWork w = tc_decode(g, item);
+                mbar_wait(bar_a_empty, a_phase ^ 1);           // previous item's MMAs are done with A
+                mbar_expect_tx(bar_a_full, kTcABytes);
+                bulk_load(smem_a, w.a, kTcABytes, bar_a_full);
+                a_phase ^= 1;
+                for (int t = 0; t < w.ntiles; ++t) {
+                    // train tile = two consecutive 128-row tiles of the expanded set
+                    const uint8_t* src = w.b + static_cast<unsigned long long>(w.tile_begin + t) * (2 * kTcABytes);
+                    for (int kb = 0; kb < kTcKBlocks; ++kb) {
+                        mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                        mbar_expect_tx(bar_full + 8 * stage, kTcStageBytes);
+                        const unsigned dst = smem_b + stage * kTcStageBytes;
+                        bulk_load(dst, src + kb * (kTcStageBytes / 2), kTcStageBytes / 2, bar_full + 8 * stage);
+                        bulk_load(dst + kTcStageBytes / 2, src + kTcABytes + kb * (kTcStageBytes / 2), kTcStageBytes / 2,
+                                  bar_full + 8 * stage);
+                        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
-            mbar_wait(bar_a, 0);
-            int stage = 0;
-            unsigned phase = 0;
-            for (int t = 0; t < ntiles; ++t) {
-                const int buf = t & 1;
-                mbar_wait(bar_tempty + 8 * buf, ((t >> 1) & 1) ^ 1);   // epilogue drained this accumulator
-                tc_fence_after();
-                const unsigned tmem_d = tmem_base + buf * kTcN;
-                for (int kb = 0; kb < kTcKBlocks; ++kb) {
-                    mbar_wait(bar_full + 8 * stage, phase);
+            int stage = 0, tcount = 0;
+            unsigned phase = 0, a_phase = 0;
+            for (int item = blockIdx.x; item < g.num_items; item += gridDim.x) {
+                const TcWork w = tc_decode(g, item);
+                mbar_wait(bar_a_full, a_phase);
+                a_phase ^= 1;
+                for (int t = 0; t < w.ntiles; ++t, ++tcount) {
+                    const int buf = tcount & 1;
+                    mbar_wait(bar_tempty + 8 * buf, ((tcount >> 1) & 1) ^ 1);   // epilogue drained this accumulator
                     tc_fence_after();
-                    const unsigned a_addr = smem_a + kb * (kTcM * kTcKBlock);
-                    const unsigned b_addr = smem_b + stage * kTcStageBytes;
+                    const unsigned tmem_d = tmem_base + buf * kTcN;
+                    for (int kb = 0; kb < kTcKBlocks; ++kb) {
+                        mbar_wait(bar_full + 8 * stage, phase);
+                        tc_fence_after();
+                        const unsigned a_addr = smem_a + kb * (kTcM * kTcKBlock);
+                        const unsigned b_addr = smem_b + stage * kTcStageBytes;
 #pragma unroll
-                    for (int k = 0; k < kTcKBlock / 32; ++k)
-                        tc_mma_i8(tmem_d, umma_desc(a_addr + 32 * k), umma_desc(b_addr + 32 * k), kIdesc,
-                                  (kb | k) != 0);
-                    tc_commit(bar_empty + 8 * stage);      // stage reusable once these MMAs have read it
-                    if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+                        for (int k = 0; k < kTcKBlock / 32; ++k)
+                            tc_mma_i8(tmem_d, umma_desc(a_addr + 32 * k), umma_desc(b_addr + 32 * k), kIdesc,
+                                      (kb | k) != 0);
+                        tc_commit(bar_empty + 8 * stage);      // stage reusable once these MMAs have read it
+                        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+                    }
+                    tc_commit(bar_tfull + 8 * buf);            // accumulator complete
                 }
-                tc_commit(bar_tfull + 8 * buf);            // accumulator complete
+                tc_commit(bar_a_empty);                        // every MMA of this item has read A
             }
         }
     } else {
@@ -266,87 +317,90 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp_arg, const uint8_t* __restrict
         const int quarter = warp & 3;                       // TMEM lane quarter this warp may touch
         const int half = ew >> 2;                           // which 128 of the 256 columns
         const unsigned lane_addr = static_cast<unsigned>(quarter * 32) << 16;
-        int best = INT_MIN, second = INT_MIN, best_idx = -1;
-        for (int t = 0; t < ntiles; ++t) {
-            const int buf = t & 1;
-            mbar_wait(bar_tfull + 8 * buf, (t >> 1) & 1);
-            tc_fence_after();
-            const long long col0 = static_cast<long long>(tile_begin + t) * kTcN + half * 128;
-            const long long valid = static_cast<long long>(N) - col0;   // columns < valid are real rows
+        const int row = quarter * 32 + lane;
+        int tcount = 0;
+        for (int item = blockIdx.x; item < g.num_items; item += gridDim.x) {
+            const TcWork w = tc_decode(g, item);
+            int best = INT_MIN, second = INT_MIN, best_idx = -1;
+            for (int t = 0; t < w.ntiles; ++t, ++tcount) {
+                const int buf = tcount & 1;
+                mbar_wait(bar_tfull + 8 * buf, (tcount >> 1) & 1);
+                tc_fence_after();
+                const long long col0 = static_cast<long long>(w.tile_begin + t) * kTcN + half * 128;
+                const long long valid = static_cast<long long>(w.N) - col0;   // columns < valid are real rows
 #pragma unroll 1
-            for (int chunk = 0; chunk < 4; ++chunk) {
-                int v[32];
-                tmem_ld32(tmem_base + lane_addr + buf * kTcN + half * 128 + chunk * 32, v);
-                if (dump != nullptr && t == 0 && qtile == 0 && blockIdx.y == 0) {
+                for (int chunk = 0; chunk < 4; ++chunk) {
+                    int v[32];
+                    tmem_ld32(tmem_base + lane_addr + buf * kTcN + half * 128 + chunk * 32, v);
+                    if (g.dump != nullptr && item == 0 && t == 0) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        dump[(quarter * 32 + lane) * kTcN + half * 128 + chunk * 32 + i] = v[i];
-                }
-                const long long cvalid = valid - chunk * 32;
-                if (cvalid < 32) {                          // last tile only: mask the zero padding rows
+                        for (int i = 0; i < 32; ++i) g.dump[row * kTcN + half * 128 + chunk * 32 + i] = v[i];
+                    }
+                    const long long cvalid = valid - chunk * 32;
+                    if (cvalid < 32) {                          // last tile only: mask the zero padding rows
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (i >= cvalid) v[i] = INT_MIN;
-                }
-                int m = v[0];
+                        for (int i = 0; i < 32; ++i)
+                            if (i >= cvalid) v[i] = INT_MIN;
+                    }
+                    int m = v[0];
 #pragma unroll
-                for (int i = 1; i < 32; i += 2) m = max(m, max(v[i], i + 1 < 32 ? v[i + 1] : INT_MIN));
-                if (m > second) {                           // something in this chunk enters the top-2
-                    const int cbase = static_cast<int>(col0 - static_cast<long long>(tile_begin) * kTcN) + chunk * 32;
+                    for (int i = 1; i < 32; i += 2) m = max(m, max(v[i], i + 1 < 32 ? v[i + 1] : INT_MIN));
+                    if (m > second) {                           // something in this chunk enters the top-2
+                        const int cbase = t * kTcN + half * 128 + chunk * 32;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const int d = v[i];
-                        if (d > best) {                     // strict: earlier (lower) index keeps ties
-                            second = best;
-                            best = d;
-                            best_idx = cbase + i;
-                        } else if (d > second) {
-                            second = d;
+                        for (int i = 0; i < 32; ++i) {
+                            const int d = v[i];
+                            if (d > best) {                     // strict: earlier (lower) index keeps ties
+                                second = best;
+                                best = d;
+                                best_idx = cbase + i;
+                            } else if (d > second) {
+                                second = d;
+                            }
                         }
                     }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
-        }
-        // merge the two column halves of each row
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpilogueWarps));   // all MMAs done => A region is free
-        const int row = quarter * 32 + lane;
-        if (half == 1) {
-            merge_buf[row * 4 + 0] = best;
-            merge_buf[row * 4 + 1] = second;
-            merge_buf[row * 4 + 2] = best_idx;
-        }
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpilogueWarps));
-        if (half == 0) {
-            const int ob = merge_buf[row * 4 + 0], os = merge_buf[row * 4 + 1], oi = merge_buf[row * 4 + 2];
-            // the halves interleave in index order across tiles, so ties compare indices
-            if (ob > best || (ob == best && oi >= 0 && oi < best_idx)) {
-                second = max(best, os);
-                best = ob;
-                best_idx = oi;
-            } else {
-                second = max(second, ob);
+            // merge the two column halves of each row
+            if (half == 1) {
+                merge_buf[row * 4 + 0] = best;
+                merge_buf[row * 4 + 1] = second;
+                merge_buf[row * 4 + 2] = best_idx;
             }
-            const unsigned long long qi = static_cast<unsigned long long>(qtile) * kTcM + row;
-            if (qi < Q) {
-                const int idx = best_idx < 0 ? -1 : tile_begin * kTcN + best_idx;
-                const int bd = best == INT_MIN ? 513 : (512 - best) >> 1;
-                const int sd = second == INT_MIN ? 513 : (512 - second) >> 1;
-                if (items != nullptr) {          // whole train range seen: these are final
-                    if (o_idx) o_idx[qi] = idx;
-                    if (o_best) o_best[qi] = bd;
-                    if (o_second) o_second[qi] = sd;
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpilogueWarps) : "memory");
+            if (half == 0) {
+                const int ob = merge_buf[row * 4 + 0], os = merge_buf[row * 4 + 1], oi = merge_buf[row * 4 + 2];
+                // the halves interleave in index order across tiles, so ties compare indices
+                if (ob > best || (ob == best && oi >= 0 && oi < best_idx)) {
+                    second = max(best, os);
+                    best = ob;
+                    best_idx = oi;
                 } else {
-                    Partial r;
-                    r.best_idx = idx;
-                    r.best_dist = bd;
-                    r.second_dist = sd;
-                    r.pad = 0;
-                    partial[static_cast<unsigned long long>(blockIdx.y) * Q + qi] = r;
+                    second = max(second, ob);
+                }
+                const unsigned long long qi = static_cast<unsigned long long>(w.qtile) * kTcM + row;
+                if (qi < w.Q) {
+                    const int idx = best_idx < 0 ? -1 : w.tile_begin * kTcN + best_idx;
+                    const int bd = best == INT_MIN ? 513 : (512 - best) >> 1;
+                    const int sd = second == INT_MIN ? 513 : (512 - second) >> 1;
+                    if (g.items != nullptr) {          // whole train range seen: these are final
+                        if (w.o_idx) w.o_idx[qi] = idx;
+                        if (w.o_best) w.o_best[qi] = bd;
+                        if (w.o_second) w.o_second[qi] = sd;
+                    } else {
+                        Partial r;
+                        r.best_idx = idx;
+                        r.best_dist = bd;
+                        r.second_dist = sd;
+                        r.pad = 0;
+                        g.partial[static_cast<unsigned long long>(w.split) * w.Q + qi] = r;
+                    }
                 }
             }
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpilogueWarps) : "memory");   // merge_buf free again
         }
     }
 
@@ -360,27 +414,21 @@ match_tc_kernel(const uint8_t* __restrict__ a_exp_arg, const uint8_t* __restrict
 
 } // namespace
 
-static int configure_tc() {
-    static bool configured = false;
-    if (!configured) {
+// The opt-in shared-memory size is a per-device function attribute: remember it per context.
+static int configure_tc(clatch_ctx* ctx) {
+    if (!ctx->tc_configured) {
         CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemBytes));
-        configured = true;
+        ctx->tc_configured = true;
     }
     return CLATCH_OK;
 }
 
-size_t tc_expanded_bytes(size_t rows, bool as_queries) {
-    return as_queries ? (rows + kTcM - 1) / kTcM * kTcABytes
-                      : (rows + kTcN - 1) / kTcN * (kTcKBlocks * kTcStageBytes);
-}
+size_t tc_expanded_bytes(size_t rows) { return (rows + kTcN - 1) / kTcN * (2 * static_cast<size_t>(kTcABytes)); }
 
-int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, bool as_queries, uint8_t* d_out,
-                     cudaStream_t stream) {
-    const int rows_per_tile = as_queries ? kTcM : kTcN;
-    const unsigned long long rows = (n + rows_per_tile - 1) / rows_per_tile * rows_per_tile, threads = rows * 32;
+int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t* d_out, cudaStream_t stream) {
+    const unsigned long long rows = (n + kTcN - 1) / kTcN * kTcN, threads = rows * 32;
     if (rows == 0) return CLATCH_OK;
-    expand_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(d_packed, n, rows, rows_per_tile,
-                                                                                    d_out);
+    expand_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(d_packed, n, rows, d_out);
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
     return CLATCH_OK;
@@ -390,9 +438,12 @@ int tc_query_tiles(size_t rows) { return static_cast<int>((rows + kTcM - 1) / kT
 
 int launch_match_tc_items(clatch_ctx* ctx, const TcItem* d_items, size_t count, cudaStream_t stream) {
     if (count == 0) return CLATCH_OK;
-    if (int rc = configure_tc()) return rc;
-    match_tc_kernel<<<static_cast<unsigned>(count), kTcThreads, kTcSmemBytes, stream>>>(nullptr, nullptr, 0, 0, 0, 0,
-                                                                                      nullptr, nullptr, d_items);
+    if (int rc = configure_tc(ctx)) return rc;
+    TcArgs g{};
+    g.num_items = static_cast<int>(count);
+    g.items = d_items;
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>(count, ctx->sm_count));
+    match_tc_kernel<<<grid, kTcThreads, kTcSmemBytes, stream>>>(g);
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
     return CLATCH_OK;
@@ -401,48 +452,51 @@ int launch_match_tc_items(clatch_ctx* ctx, const TcItem* d_items, size_t count, 
 int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
                          int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
                          int32_t* d_dump) {
-    if (int rc = configure_tc()) return rc;
+    if (int rc = configure_tc(ctx)) return rc;
     const size_t qtiles = (Q + kTcM - 1) / kTcM, ttiles = (N + kTcN - 1) / kTcN;
-    if (int rc = ctx->exp_q.reserve(qtiles * kTcABytes)) return rc;
-    if (int rc = ctx->exp_t.reserve(ttiles * kTcKBlocks * kTcStageBytes)) return rc;
-    {
-        const unsigned long long rows = qtiles * kTcM, threads = rows * 32;
-        expand_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(d_q, Q, rows, kTcM,
-                                                                                        ctx->exp_q.as<uint8_t>());
-        ++ctx->launches;
+    // Both sets go to the tensor cores as int8; a self-match expands its one set once.
+    const bool self = d_q == d_t && Q == N;
+    if (int rc = ctx->exp_t.reserve(tc_expanded_bytes(N))) return rc;
+    if (int rc = launch_tc_expand(ctx, d_t, N, ctx->exp_t.as<uint8_t>(), stream)) return rc;
+    const uint8_t* a_exp = ctx->exp_t.as<uint8_t>();
+    if (!self) {
+        if (int rc = ctx->exp_q.reserve(tc_expanded_bytes(Q))) return rc;
+        if (int rc = launch_tc_expand(ctx, d_q, Q, ctx->exp_q.as<uint8_t>(), stream)) return rc;
+        a_exp = ctx->exp_q.as<uint8_t>();
     }
+    // Split the train range when there are too few query tiles to keep every SM busy. Model: the
+    // persistent CTAs run ceil(items / SMs) rounds; an item costs (tiles + kOverhead) tile-times
+    // (A reload + pipeline refill). Pick the split count with the smallest makespan.
+    size_t splits = 1, per_split = ttiles;
     {
-        const unsigned long long rows = ttiles * kTcN, threads = rows * 32;
-        expand_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(d_t, N, rows, kTcN,
-                                                                                        ctx->exp_t.as<uint8_t>());
-        ++ctx->launches;
-    }
-    CLATCH_CUDA(cudaGetLastError());
-    // Split the train range over blockIdx.y when there are too few query tiles to fill the
-    // SMs. Model: CTAs run in waves of one per SM; a CTA costs (tiles + kOverhead) tile-times
-    // (barrier init, TMEM allocation, 64 KiB A load, pipeline fill, merge). Pick the split count with the smallest makespan.
-    size_t best_splits = 1, best_per = ttiles;
-    {
-        const size_t sms = static_cast<size_t>(ctx->sm_count), kOverhead = 8;   // measured: ~8 us of fixed cost per CTA vs ~1 us per tile
-        size_t best_cost = ~static_cast<size_t>(0);
+        const size_t sms = static_cast<size_t>(ctx->sm_count);
+        const double kOverhead = 1.5;
+        double best_cost = 1e300;
         for (size_t s = 1; s <= std::min<size_t>(ttiles, 64); ++s) {
             const size_t per = (ttiles + s - 1) / s, actual = (ttiles + per - 1) / per;
-            const size_t waves = (qtiles * actual + sms - 1) / sms;
-            const size_t cost = waves * (per + kOverhead);
-            if (cost < best_cost) {
+            const size_t rounds = (qtiles * actual + sms - 1) / sms;
+            const double cost = rounds * (per + kOverhead);
+            if (cost < best_cost - 1e-9) {
                 best_cost = cost;
-                best_splits = actual;
-                best_per = per;
+                splits = actual;
+                per_split = per;
             }
         }
     }
-    const size_t splits = best_splits, per_split = best_per;
     if (int rc = ctx->partial.reserve(sizeof(Partial) * splits * Q)) return rc;
-    dim3 grid(static_cast<unsigned>(qtiles), static_cast<unsigned>(splits));
-    match_tc_kernel<<<grid, kTcThreads, kTcSmemBytes, stream>>>(ctx->exp_q.as<uint8_t>(), ctx->exp_t.as<uint8_t>(), Q,
-                                                                N, static_cast<int>(ttiles),
-                                                                static_cast<int>(per_split),
-                                                                ctx->partial.as<Partial>(), d_dump, nullptr);
+    TcArgs g{};
+    g.a_exp = a_exp;
+    g.b_exp = ctx->exp_t.as<uint8_t>();
+    g.Q = Q;
+    g.N = N;
+    g.qtiles = static_cast<int>(qtiles);
+    g.total_tiles = static_cast<int>(ttiles);
+    g.tiles_per_split = static_cast<int>(per_split);
+    g.num_items = static_cast<int>(qtiles * splits);
+    g.partial = ctx->partial.as<Partial>();
+    g.dump = d_dump;
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>(qtiles * splits, ctx->sm_count));
+    match_tc_kernel<<<grid, kTcThreads, kTcSmemBytes, stream>>>(g);
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
     launch_merge_partials(ctx->partial.as<Partial>(), Q, static_cast<int>(splits), 513, d_best_idx, d_best_dist, d_second, stream);
