@@ -24,7 +24,7 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 PORT_SO = HERE / "liblatch_oracle.so"
 REF_SO = HERE / "_ref" / "liblatch_ref.so"
-PATTERN_FILE = HERE.parent / "paper_1609_03986_b200" / "data" / "default_pattern.latchpat"
+PATTERN_FILE = HERE.parent / "paper_1609_03986_b200" / "data" / "default_pattern.npz"
 
 _u8p = C.POINTER(C.c_uint8)
 _f64p = C.POINTER(C.c_double)
@@ -74,7 +74,11 @@ def parse_pattern_text(text: str):
 
 
 def default_pattern():
-    return parse_pattern_text(PATTERN_FILE.read_text())
+    """(T, K, triplets int32 (T,6), weights f64 (K*K,)) of the shipped table (data file only;
+    the checker never imports the product package)."""
+    d = np.load(PATTERN_FILE)
+    return (int(d["bit_count"]), int(d["patch_size"]), d["triplets"].astype(np.int32),
+            d["weights"].astype(np.float64))
 
 
 class Port:

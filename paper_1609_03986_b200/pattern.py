@@ -3,8 +3,9 @@
 Mirrors the reference's parse_pattern / format_pattern / default_pattern
 (proj/src/pattern.cpp:68-155, proj/src/pattern_default.cpp:527-539): same accepted
 syntax, same error categories (surfaced as RuntimeError, as pybind11 does for
-latch::Error). The shipped table lives in data/default_pattern.latchpat, emitted by
-the reference's own format_pattern(default_pattern()) (oracle/make_golden.py).
+latch::Error). The shipped table lives in data/default_pattern.npz (int16 triplets + f64
+weights, taken from the reference's own format_pattern(default_pattern()) output by
+oracle/make_golden.py); its LATCHPAT text is produced on demand by format_pattern.
 """
 from __future__ import annotations
 
@@ -19,7 +20,8 @@ import numpy as np
 from ._lib import LatchError
 
 WINDOW = 64          # proj/include/latch/pattern.hpp:12
-_DATA = Path(__file__).resolve().parent / "data" / "default_pattern.latchpat"
+_DATA = Path(__file__).resolve().parent / "data" / "default_pattern.npz"
+_TEXT_CACHE = Path(__file__).resolve().parent / "data" / "default_pattern.latchpat"   # generated, git-ignored
 _HEADER = re.compile(r"LATCHPAT v1 T=\s*([+-]?\d+) K=\s*([+-]?\d+)")
 _INT = re.compile(r"\s*([+-]?\d+)")
 
@@ -138,13 +140,25 @@ def format_pattern(pattern: TripletPattern) -> str:
 
 
 @lru_cache(maxsize=1)
-def default_pattern_text() -> str:
-    return _DATA.read_text()
+def default_pattern() -> TripletPattern:
+    d = np.load(_DATA)
+    return TripletPattern(int(d["bit_count"]), int(d["patch_size"]),
+                          np.ascontiguousarray(d["triplets"], np.int16),
+                          np.ascontiguousarray(d["weights"], np.float64))
 
 
 @lru_cache(maxsize=1)
-def default_pattern() -> TripletPattern:
-    return parse_pattern(default_pattern_text())
+def default_pattern_text() -> str:
+    return format_pattern(default_pattern())
+
+
+def ensure_default_pattern_file() -> Path:
+    """Writes the LATCHPAT text of the built-in table next to the data file (for the C++
+    host API, which reads it through CLATCH_DEFAULT_PATTERN) and returns its path."""
+    text = default_pattern_text()
+    if not _TEXT_CACHE.exists() or _TEXT_CACHE.read_text() != text:
+        _TEXT_CACHE.write_text(text)
+    return _TEXT_CACHE
 
 
 @lru_cache(maxsize=16)

@@ -13,12 +13,13 @@ def _build():
     subprocess.run(["make", "-C", str(ROOT / "oracle"), "liblatch_oracle.so"], check=True,
                    stdout=subprocess.DEVNULL)
     subprocess.run(["make", "-C", str(BIN.parent)], check=True, stdout=subprocess.DEVNULL)
+    from paper_1609_03986_b200.pattern import ensure_default_pattern_file
+    ensure_default_pattern_file()
 
 
 @pytest.mark.gpu
 def test_cpp_host_api_parity():
-    if not BIN.exists():
-        _build()
+    _build()
     r = subprocess.run([str(BIN), str(ROOT)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "PASSED" in r.stdout

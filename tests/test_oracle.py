@@ -134,7 +134,11 @@ def test_known_answers(port):
 # ---- live comparison with the unmodified reference (when oracle/_ref exists) ----
 
 def test_pattern_file_is_reference_default(ref):
-    assert oracle.PATTERN_FILE.read_text() == ref.default_pattern_text()
+    T, K, trip, weights = ref.parse_pattern(ref.default_pattern_text())
+    t2, k2, trip2, w2 = oracle.default_pattern()
+    assert (T, K) == (t2, k2) and np.array_equal(trip, trip2) and np.array_equal(weights, w2)
+    from paper_1609_03986_b200.pattern import default_pattern_text
+    assert default_pattern_text() == ref.default_pattern_text()
 
 
 def test_port_equals_reference_live(port, ref):
