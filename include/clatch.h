@@ -203,6 +203,16 @@ CLATCH_API int clatch_match_brute_force(clatch_ctx* ctx, const uint8_t* probes, 
                              double ratio, int cross_check, int has_max, int max_distance,
                              int32_t* out, size_t* count);
 
+/* ---- trainer scoring (the parallel body of select_triplets, src/pattern.cpp:340-346,397-400) ---
+ * bit (c, i) = triplet_bit(window i, candidate c, mask) for n upright 64x64 training patches
+ * (`windows`: n x 4096 doubles, row-major, as Window64::from_image lays them out) and C candidate
+ * triplets (`candidates`: C rows {ax, ay, bx, by, cx, cy}, coordinates in [0, 64-K]). `mask` is
+ * K*K weights or NULL for all ones. out: C rows of row_bytes >= ceil(n/8) bytes in BitVector
+ * order (bit i of row c at byte i>>3, bit i&7; include/latch/pattern.hpp:70-90). Greedy
+ * selection (src/pattern.cpp:431-450) stays on the host. */
+CLATCH_API int clatch_triplet_bits(clatch_ctx* ctx, const double* windows, size_t n, const int16_t* candidates,
+                        size_t C, int K, const double* mask, uint8_t* out, size_t row_bytes);
+
 /* ---- device-resident descriptor sets (64-byte descriptors) -----------------------------
  * A set owns a device copy of n descriptors plus the int8 operand forms the tensor-core
  * matcher consumes, so that extraction output can feed any number of matches without

@@ -119,6 +119,7 @@ class Port:
         L.oracle_match.argtypes = [_u8p, C.c_size_t, _u8p, C.c_size_t, C.c_int, C.c_int,
                                    C.c_double, C.c_int, C.c_int, C.c_int, _i32p]
         L.oracle_match.restype = C.c_size_t
+        L.oracle_triplet_bits.argtypes = [_f64p, C.c_size_t, _i32p, C.c_size_t, C.c_int, _f64p, _u8p, C.c_size_t]
         L.oracle_fast_detect.argtypes = [_f64p, C.c_int, C.c_int, C.c_double, C.c_int, _f64p, C.c_size_t]
         L.oracle_fast_detect.restype = C.c_size_t
         L.oracle_detect_and_orient.argtypes = [_f64p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, _f64p,
@@ -206,6 +207,19 @@ class Port:
                                          _p(kept, _i64p), _p(desc, _u8p))
         return kept[:m].copy(), desc[:m].copy()
 
+    # ---- trainer scoring ----
+    def triplet_bits(self, windows, candidates, K, weights):
+        """-> uint8 (C, ceil(n/8)): bit i of row c = triplet_bit(window i, candidate c)."""
+        windows = np.ascontiguousarray(windows, np.float64).reshape(-1, 4096)
+        cand = np.ascontiguousarray(candidates, np.int32).reshape(-1, 6)
+        weights = np.ascontiguousarray(weights, np.float64)
+        n, c = len(windows), len(cand)
+        row = (n + 7) // 8
+        out = np.zeros((c, row), np.uint8)
+        self.lib.oracle_triplet_bits(_p(windows, _f64p), n, _p(cand, _i32p), c, K, _p(weights, _f64p),
+                                     _p(out, _u8p), row)
+        return out
+
     # ---- detection ----
     def detect(self, image, threshold=20.0, nms=True, orient=True, radius=15):
         """fast_detect / detect_and_orient -> (N, 4) float64 [x, y, theta, score]."""
@@ -281,6 +295,8 @@ class Ref:
                                         C.c_size_t]
         L.ref_detect_and_orient.argtypes = [_f64p, C.c_int, C.c_int, C.c_double, C.c_int, _f64p,
                                             C.c_size_t, C.POINTER(C.c_size_t)]
+        L.ref_triplet_bits.argtypes = [_f64p, C.c_size_t, _i32p, C.c_size_t, C.c_int, _f64p, _u8p, C.c_size_t]
+        L.ref_sample_candidates.argtypes = [C.c_size_t, C.c_int, C.c_uint64, _i32p]
         L.ref_fast_detect.argtypes = [_f64p, C.c_int, C.c_int, C.c_double, C.c_int, _f64p,
                                       C.c_size_t, C.POINTER(C.c_size_t)]
         L.ref_load_pgm.argtypes = [C.c_char_p, _f64p, C.c_size_t, _i32p, _i32p]
@@ -365,6 +381,22 @@ class Ref:
         out = np.empty((h.value, w.value), np.float64)
         self._check(self.lib.ref_load_pgm(str(path).encode(), _p(out, _f64p), out.size,
                                           C.byref(w), C.byref(h)))
+        return out
+
+    def sample_candidates(self, count, K, seed):
+        out = np.zeros((count, 6), np.int32)
+        self._check(self.lib.ref_sample_candidates(count, K, seed, _p(out, _i32p)))
+        return out
+
+    def triplet_bits(self, windows, candidates, K, weights):
+        windows = np.ascontiguousarray(windows, np.float64).reshape(-1, 4096)
+        cand = np.ascontiguousarray(candidates, np.int32).reshape(-1, 6)
+        weights = np.ascontiguousarray(weights, np.float64)
+        n, c = len(windows), len(cand)
+        row = (n + 7) // 8
+        out = np.zeros((c, row), np.uint8)
+        self._check(self.lib.ref_triplet_bits(_p(windows, _f64p), n, _p(cand, _i32p), c, K, _p(weights, _f64p),
+                                              _p(out, _u8p), row))
         return out
 
     def detect(self, image, threshold=20.0, nms=True, orient=True):

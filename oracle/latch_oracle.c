@@ -510,3 +510,19 @@ size_t oracle_detect_and_orient(const double* img, int w, int h, double threshol
     free(raw);
     return m;
 }
+
+/* ------------------------------------------------------------------------
+ * Trainer scoring (next row): triplet_bits_over — src/pattern.cpp:340-346, the body of
+ * select_triplets' parallel_for (:397-400). windows: n upright 64x64 patches
+ * (Window64::from_image, src/descriptor.cpp:13-21); candidates: C x 6 ints. out: C rows of
+ * `row_bytes` bytes, bit i of row c = triplet_bit(window i, candidate c) stored LSB-first
+ * (BitVector, include/latch/pattern.hpp:70-90).
+ * ---------------------------------------------------------------------- */
+void oracle_triplet_bits(const double* windows, size_t n, const int* candidates, size_t C, int K,
+                         const double* weights, uint8_t* out, size_t row_bytes) {
+    memset(out, 0, C * row_bytes);
+    for (size_t c = 0; c < C; ++c)
+        for (size_t i = 0; i < n; ++i)
+            if (oracle_triplet_bit(windows + i * 4096, candidates + 6 * c, K, weights))
+                out[c * row_bytes + (i >> 3)] |= (uint8_t)(1u << (i & 7));
+}

@@ -163,6 +163,40 @@ int ref_detect_and_orient(const double* img, int w, int h, double threshold, int
     });
 }
 
+// triplet_bits (src/pattern.cpp:352-360) for C candidates over n 64x64 patches -> C rows of
+// row_bytes bytes, BitVector layout (bit i of row c, LSB first).
+int ref_triplet_bits(const double* windows, std::size_t n, const int* candidates, std::size_t C, int K,
+                     const double* weights, std::uint8_t* out, std::size_t row_bytes) {
+    return guarded([&] {
+        latch::PatchDataset dataset;
+        for (std::size_t i = 0; i < n; ++i) {
+            dataset.patches.push_back(make_image(windows + i * 4096, 64, 64));
+            dataset.labels.push_back(static_cast<long>(i));
+        }
+        latch::WeightMask mask;
+        mask.size = K;
+        mask.weights.assign(weights, weights + static_cast<std::size_t>(K) * K);
+        std::memset(out, 0, C * row_bytes);
+        for (std::size_t c = 0; c < C; ++c) {
+            const int* t = candidates + 6 * c;
+            const latch::BitVector bits = latch::triplet_bits({t[0], t[1], t[2], t[3], t[4], t[5]}, mask, dataset);
+            for (std::size_t i = 0; i < n; ++i)
+                if (bits.get(i)) out[c * row_bytes + (i >> 3)] |= static_cast<std::uint8_t>(1u << (i & 7));
+        }
+    });
+}
+
+// sample_candidates (src/pattern.cpp) -> count x 6 ints.
+int ref_sample_candidates(std::size_t count, int K, std::uint64_t seed, int* out) {
+    return guarded([&] {
+        const auto cand = latch::sample_candidates(count, K, seed);
+        for (std::size_t i = 0; i < cand.size(); ++i) {
+            const int v[6] = {cand[i].ax, cand[i].ay, cand[i].bx, cand[i].by, cand[i].cx, cand[i].cy};
+            std::memcpy(out + 6 * i, v, sizeof(v));
+        }
+    });
+}
+
 int ref_fast_detect(const double* img, int w, int h, double threshold, int nms, double* out_kps,
                     std::size_t cap, std::size_t* count) {
     return guarded([&] {

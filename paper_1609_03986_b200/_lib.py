@@ -87,6 +87,8 @@ _SIGNATURES = {
                                         C.c_int, i32p, i32p, szp]),
     "clatch_match_brute_force": (C.c_int, [C.c_void_p, u8p, C.c_size_t, u8p, C.c_size_t, C.c_int,
                                            C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, i32p, szp]),
+    "clatch_triplet_bits": (C.c_int, [C.c_void_p, f64p, C.c_size_t, i16p, C.c_size_t, C.c_int, f64p, u8p,
+                                      C.c_size_t]),
     "clatch_set_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.POINTER(C.c_void_p)]),
     "clatch_set_destroy": (None, [C.c_void_p]),
     "clatch_set_count": (C.c_size_t, [C.c_void_p]),

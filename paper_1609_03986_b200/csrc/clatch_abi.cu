@@ -780,6 +780,45 @@ int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t
 
 extern "C" {
 
+int clatch_triplet_bits(clatch_ctx* ctx, const double* windows, size_t n, const int16_t* candidates, size_t C, int K,
+                        const double* mask, uint8_t* out, size_t row_bytes) {
+    if (!ctx) return invalid("clatch_triplet_bits: ctx is null");
+    if (K < 1 || K > kWindow) return invalid("clatch_triplet_bits: K out of range");
+    if (n == 0 || C == 0) return CLATCH_OK;
+    if (!windows || !candidates || !out) return invalid("clatch_triplet_bits: null buffer");
+    if (row_bytes < (n + 7) / 8) return invalid("clatch_triplet_bits: row_bytes < ceil(n / 8)");
+    if (n > 0x7fffffffu || C > 0x7fffffffu) return invalid("clatch_triplet_bits: too many patches or candidates");
+    for (size_t c = 0; c < C; ++c)
+        for (int i = 0; i < 6; ++i)
+            if (candidates[6 * c + i] < 0 || candidates[6 * c + i] > kWindow - K) {
+                set_error("CoordinateOutOfRange: candidate coordinate outside [0, " + std::to_string(kWindow - K) + "]");
+                return CLATCH_ERR_COORD_RANGE;
+            }
+    std::vector<double> w(static_cast<size_t>(K) * K, 1.0);
+    if (mask) w.assign(mask, mask + w.size());
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    const size_t words_per_patch = (C + 31) / 32, out_words = (n + 31) / 32;
+    if (int rc = ctx->img.reserve(sizeof(double) * 4096 * n)) return rc;
+    if (int rc = ctx->kps.reserve(sizeof(int16_t) * 6 * C)) return rc;
+    if (int rc = ctx->partial.reserve(sizeof(unsigned) * words_per_patch * n)) return rc;
+    if (int rc = ctx->res.reserve(sizeof(unsigned) * out_words * C)) return rc;
+    cudaStream_t st = ctx->stream;
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->img.ptr, windows, sizeof(double) * 4096 * n, cudaMemcpyHostToDevice, st));
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->kps.ptr, candidates, sizeof(int16_t) * 6 * C, cudaMemcpyHostToDevice, st));
+    if (int rc = launch_triplet_bits(ctx, ctx->img.as<double>(), n, ctx->kps.as<short>(), C, K, w.data(),
+                                     ctx->partial.as<unsigned>(), ctx->res.as<unsigned>(), st))
+        return rc;
+    std::vector<unsigned> host(out_words * C);
+    CLATCH_CUDA(cudaMemcpyAsync(host.data(), ctx->res.ptr, sizeof(unsigned) * host.size(), cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));   // also covers the constant-memory upload of `w`
+    const size_t live = (n + 7) / 8;
+    for (size_t c = 0; c < C; ++c) {
+        std::memcpy(out + c * row_bytes, host.data() + c * out_words, live);   // little-endian words == byte order
+        if (row_bytes > live) std::memset(out + c * row_bytes + live, 0, row_bytes - live);
+    }
+    return CLATCH_OK;
+}
+
 int clatch_set_create(clatch_ctx* ctx, const uint8_t* descriptors, size_t n, int on_device, clatch_set** out) {
     if (!ctx || !out) return invalid("clatch_set_create: null argument");
     *out = nullptr;

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
 #include <string>
@@ -107,6 +108,10 @@ int launch_detect_u8(clatch_ctx* ctx, const uint8_t* d_img, int w, int h, size_t
                      int orient, int radius, cudaStream_t st, unsigned* count);
 int launch_detect_f64(clatch_ctx* ctx, const double* d_img, int w, int h, size_t pitch, double threshold, int nms,
                       int orient, int radius, cudaStream_t st, unsigned* count);
+
+// trainer scoring (clatch_score.cu)
+int launch_triplet_bits(clatch_ctx* ctx, const double* d_windows, size_t n, const short* d_candidates, size_t C, int K,
+                        const double* weights, unsigned* d_by_patch, unsigned* d_out, cudaStream_t st);
 
 // matching (clatch_match.cu, clatch_match_tc.cu)
 struct Partial {   // per (train split, query) partial top-2

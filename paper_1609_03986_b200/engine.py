@@ -294,6 +294,24 @@ class Engine:
             None if rb is None else _ptr(rb, i32p), _ptr(out, i32p), C.byref(count)))
         return out[:count.value].copy()
 
+    # ---- trainer scoring ----------------------------------------------------------------
+    def triplet_bits(self, windows: np.ndarray, candidates: np.ndarray, patch_size: int = 8, mask=None):
+        """bit (c, i) = triplet_bit(window i, candidate c, mask): windows (n, 64, 64) float64 upright
+        patches, candidates (C, 6) ints -> uint8 (C, ceil(n/8)), LSB-first (BitVector order)."""
+        w = np.ascontiguousarray(windows, np.float64).reshape(-1, 4096)
+        cand = np.ascontiguousarray(candidates, np.int16).reshape(-1, 6)
+        m = None if mask is None else np.ascontiguousarray(mask, np.float64).reshape(-1)
+        if m is not None and m.size != patch_size * patch_size:
+            raise ValueError("mask must hold patch_size * patch_size weights")
+        n, c = len(w), len(cand)
+        row = (n + 7) // 8
+        out = np.zeros((c, row), np.uint8)
+        with self._lock:
+            rc = self.lib.clatch_triplet_bits(self.ctx, _ptr(w, f64p), n, _ptr(cand, i16p), c, int(patch_size),
+                                              None if m is None else _ptr(m, f64p), _ptr(out, u8p), row)
+        _lib.check(rc)
+        return out
+
     # ---- resident descriptor sets ----------------------------------------------------
     def create_set(self, descriptors) -> DescriptorSet:
         """descriptors: (N, 64) uint8 numpy array (uploaded) or torch CUDA tensor (copied on device)."""

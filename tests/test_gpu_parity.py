@@ -523,3 +523,31 @@ def test_detect_against_oracle_and_edge_cases(lk, port):
     assert np.array_equal(desc, port.describe_all(img, kps)[1]) and len(desc) > 0
     m = lk.match(desc, desc)
     assert np.all(m[:, 2] == 0)
+
+
+# ------------------------------------------------------------ trainer scoring ----
+
+def test_triplet_bits_scoring(lk, port, vectors):
+    """select_triplets' parallel body (src/pattern.cpp:340-346,397-400) on the GPU."""
+    eng = lk.get_engine()
+    wins = np.stack([port.random_image(300 + i, 64, 64) for i in range(45)])
+    wins[40:] = np.stack([port.structured_image(400 + i, 64, 64) for i in range(5)])
+    _, _, _, seven = oracle.default_pattern()
+    assert np.array_equal(eng.triplet_bits(wins, vectors["score_candidates_k8"], 8, seven), vectors["score_bits_seven"])
+    assert np.array_equal(eng.triplet_bits(wins, vectors["score_candidates_k8"], 8), vectors["score_bits_ones"])
+    assert np.array_equal(eng.triplet_bits(wins, vectors["score_candidates_k5"], 5, vectors["score_weights_k5"]),
+                          vectors["score_bits_k5"])
+    # larger, ragged sizes against the oracle (n and C not multiples of 32)
+    rng = np.random.default_rng(3)
+    big = np.stack([port.random_image(900 + i, 64, 64) for i in range(77)])
+    cand = rng.integers(0, 57, size=(1001, 6)).astype(np.int16)
+    assert np.array_equal(eng.triplet_bits(big, cand, 8, seven), port.triplet_bits(big, cand, 8, seven))
+    with pytest.raises(RuntimeError):
+        eng.triplet_bits(big, np.full((1, 6), 60, np.int16), 8)      # coordinate outside [0, 64-K]
+    assert eng.triplet_bits(big[:0], cand, 8).shape == (1001, 0)
+    # the extraction pattern is untouched by scoring (separate constant bank)
+    img = port.structured_image(5, 200, 150)
+    kps = port.random_keypoints(6, 200, 150, 20)
+    assert np.array_equal(lk.describe(img, kps, pattern=(GOLDEN / "pattern_t64k5w.latchpat").read_text())[1],
+                          port.describe_all(img, kps, pattern=oracle.parse_pattern_text(
+                              (GOLDEN / "pattern_t64k5w.latchpat").read_text()))[1])

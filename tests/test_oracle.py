@@ -197,3 +197,21 @@ def test_detect_live_reference(port, ref):
             assert np.array_equal(port.detect(im, thr, nms, ori), ref.detect(im, thr, nms, ori))
     with pytest.raises(RuntimeError):
         port.detect(np.zeros((32, 6)))
+
+
+# ---- trainer scoring (next row): candidate bits over upright patches ----
+
+def _score_windows(port):
+    wins = np.stack([port.random_image(300 + i, 64, 64) for i in range(45)])
+    wins[40:] = np.stack([port.structured_image(400 + i, 64, 64) for i in range(5)])
+    return wins
+
+
+def test_triplet_bits_vectors(port, vectors):
+    wins = _score_windows(port)
+    _, _, _, seven = oracle.default_pattern()
+    assert np.array_equal(port.triplet_bits(wins, vectors["score_candidates_k8"], 8, seven), vectors["score_bits_seven"])
+    assert np.array_equal(port.triplet_bits(wins, vectors["score_candidates_k8"], 8, np.ones(64)),
+                          vectors["score_bits_ones"])
+    assert np.array_equal(port.triplet_bits(wins, vectors["score_candidates_k5"], 5, vectors["score_weights_k5"]),
+                          vectors["score_bits_k5"])
