@@ -44,8 +44,8 @@ SMEM_BYTES_PER_DESC = 512 * 49 * 3 * 8                     # 8-byte window reads
 POPC_PER_COMPARE = 16
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
 # captures of the same command (profiles/*_ncu.json); cold-cache replay, so an upper bound.
-TRAFFIC_NCU = {"extract_quad_kernel<u8>": 2.42e6,                 # profiles/r1f_extract_quad_ncu.json
-               "match_tc_kernel (tcgen05 kind::i8)": 10.45e6}     # profiles/r1e_match_tc_ncu.json
+TRAFFIC_NCU = {"extract_quad_kernel<u8>": 2.419e+06,                 # profiles/r1t_extract_ncu.json
+               "match_tc_kernel (tcgen05 kind::i8)": 5.273e+06}     # profiles/r1t_match_tc_ncu.json
 
 
 def synth_inputs(workload: str, rank: int = 0):
