@@ -12,6 +12,7 @@
 //                                                  descriptor.hpp:31-42, pattern.hpp:19-52
 //   Error / ErrorCode                              errors.hpp:10-56
 //   parse_pattern / default_pattern                pattern.hpp:100-108
+//   fast_detect / detect_and_orient                detect.hpp:18-40 (the step before the path)
 //
 // Everything per-sample / per-pair runs on the GPU through the C ABI; this header only
 // converts containers, keeps the reference's early-outs and re-raises status codes as
@@ -20,6 +21,7 @@
 // bodies of the functions below move (INTEGRATION.md shows the patch).
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -142,7 +144,7 @@ namespace b200 {
 
 [[noreturn]] inline void rethrow(int rc) {
     const std::string msg = clatch_last_error();
-    if (rc >= 100 && rc <= 121) throw Error(static_cast<ErrorCode>(rc - 100), msg);
+    if (rc >= 100 && rc <= 121) throw Error(static_cast<ErrorCode>(rc - 100), msg);   // 100 + ErrorCode
     if (rc == CLATCH_ERR_NONFINITE) throw Error(ErrorCode::OutOfBounds, msg);
     if (rc == CLATCH_ERR_INVALID) throw std::invalid_argument(msg);
     throw Error(ErrorCode::DeviceUnavailable, msg);
@@ -271,6 +273,47 @@ inline const TripletPattern& default_pattern() {
         return load_pattern_file(env ? env : "paper_1609_03986_b200/data/default_pattern.latchpat");
     }();
     return p;
+}
+
+// ---- detection (detect.hpp:18-40; the step before the path) ----------------------------------
+inline constexpr int kFastBorder = 3;
+inline constexpr int kDefaultFastThreshold = 20;
+inline constexpr int kOrientationRadius = 15;
+
+namespace b200 {
+inline std::vector<Keypoint> run_detect(const Image& image, double threshold, bool do_nms, bool orient, int radius) {
+    Context& c = context();
+    std::lock_guard<std::mutex> lock(c.mutex);
+    std::size_t cap = std::max<std::size_t>(1024, static_cast<std::size_t>(image.width) * image.height / 64), count = 0;
+    std::vector<double> rows;
+    for (;;) {
+        rows.resize(cap * 4);
+        const int rc = clatch_detect_f64(c.ctx, image.data.data(), image.width, image.height,
+                                         static_cast<std::size_t>(image.width), threshold, do_nms, orient, radius,
+                                         rows.data(), cap, &count);
+        if (rc == CLATCH_ERR_INVALID && count > cap) {   // buffer too small: *count holds the need
+            cap = count;
+            continue;
+        }
+        check(rc);
+        break;
+    }
+    std::vector<Keypoint> out(count);
+    for (std::size_t i = 0; i < count; ++i) out[i] = {rows[4 * i], rows[4 * i + 1], rows[4 * i + 2], rows[4 * i + 3]};
+    return out;
+}
+} // namespace b200
+
+/// FAST-9 segment test (+ 3x3 NMS, ties keep the smallest (y, x)); output sorted by (y, x), theta 0.
+inline std::vector<Keypoint> fast_detect(const Image& image, double threshold, bool do_nms) {
+    return b200::run_detect(image, threshold, do_nms, false, kOrientationRadius);
+}
+
+/// fast_detect followed by the intensity-centroid orientation; detections whose disc does not
+/// fit in the image are dropped.
+inline std::vector<Keypoint> detect_and_orient(const Image& image, double threshold, bool do_nms,
+                                               int radius = kOrientationRadius) {
+    return b200::run_detect(image, threshold, do_nms, true, radius);
 }
 
 // ---- extraction (descriptor.hpp:48-67) ------------------------------------------------------

@@ -214,6 +214,13 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
                             &ctx->pattern.triplets})
         b->release();
     ctx->pinned.release();
+    ctx->pin_xycs.release();
+    ctx->pin_desc.release();
+    if (ctx->copy_stream) {
+        cudaStreamDestroy(ctx->copy_stream);
+        for (cudaEvent_t e : ctx->band_events)
+            if (e) cudaEventDestroy(e);
+    }
     for (int s = 0; s < 2; ++s) {
         for (DeviceBuffer* b : {&ctx->pipe[s].img, &ctx->pipe[s].kps, &ctx->pipe[s].desc, &ctx->pipe[s].img_u8,
                                 &ctx->pipe[s].flags})
@@ -450,6 +457,11 @@ int clatch_extract_f64(clatch_ctx* ctx, const double* img, int width, int height
 
 } // extern "C"
 
+// describe_all with a banded upload: the image goes up in row bands on a copy stream while
+// the host filters keypoints and evaluates cos/sin; keypoints are bucketed by the band in
+// which their 92-row footprint ends, and each bucket's extraction is queued on the compute
+// stream behind that band's arrival event. Extraction of band b overlaps the DMA of bands
+// b+1.. (a 16.6 MB float64 frame costs more to upload than to describe).
 template <typename Pixel>
 static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int height, size_t pitch,
                              const double* kps, size_t n, int cols, int workers, int64_t* kept,
@@ -467,35 +479,106 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
     if (int rc = ctx->img.reserve(sizeof(Pixel) * dpitch * height)) return rc;
     if (int rc = ctx->kps.reserve(sizeof(double) * 4 * n)) return rc;
     if (int rc = ctx->desc.reserve(bytes * n)) return rc;
+    if (int rc = ctx->pin_xycs.reserve(sizeof(double) * 4 * n)) return rc;
+    if (int rc = ctx->pin_desc.reserve(bytes * n)) return rc;
     cudaStream_t st = ctx->stream;
+
+    // Bands of >= 2 MiB, at most 8; small images go up in one piece.
+    const size_t image_bytes = sizeof(Pixel) * static_cast<size_t>(width) * height;
+    int bands = static_cast<int>(std::min<size_t>(8, image_bytes / (2u << 20)));
+    if (bands < 2 || n < 512) bands = 1;
+    const int band_rows = (height + bands - 1) / bands;
+    if (bands > 1 && !ctx->copy_stream) {
+        CLATCH_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : ctx->band_events) CLATCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     // 1. image DMA first ...
-    CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, sizeof(Pixel) * dpitch, img, sizeof(Pixel) * pitch,
-                                  sizeof(Pixel) * width, height, cudaMemcpyHostToDevice, st));
+    if (bands == 1) {
+        CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, sizeof(Pixel) * dpitch, img, sizeof(Pixel) * pitch,
+                                      sizeof(Pixel) * width, height, cudaMemcpyHostToDevice, st));
+    } else {
+        // the copy stream must not overwrite the image while earlier work on `st` still reads it
+        CLATCH_CUDA(cudaEventRecord(ctx->band_events[0], st));
+        CLATCH_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_events[0], 0));
+        for (int b = 0; b < bands; ++b) {
+            const int r0 = b * band_rows, r1 = std::min(height, r0 + band_rows);
+            CLATCH_CUDA(cudaMemcpy2DAsync(static_cast<Pixel*>(ctx->img.ptr) + static_cast<size_t>(r0) * dpitch,
+                                          sizeof(Pixel) * dpitch, img + static_cast<size_t>(r0) * pitch,
+                                          sizeof(Pixel) * pitch, sizeof(Pixel) * width, r1 - r0,
+                                          cudaMemcpyHostToDevice, ctx->copy_stream));
+            CLATCH_CUDA(cudaEventRecord(ctx->band_events[b], ctx->copy_stream));
+        }
+    }
     // 2. ... while the host filters by margin and evaluates cos/sin with its own libm
-    ctx->host_xycs.resize(4 * n);
+    double* const xycs = static_cast<double*>(ctx->pin_xycs.ptr);
     size_t count = 0;
-    if (int rc = clatch_prepare_keypoints(kps, n, cols, width, height, workers, ctx->host_xycs.data(), kept,
-                                          &count)) {
+    auto drain = [&] {
         cudaStreamSynchronize(st);
+        if (bands > 1) cudaStreamSynchronize(ctx->copy_stream);
+    };
+    if (int rc = clatch_prepare_keypoints(kps, n, cols, width, height, workers, xycs, kept, &count)) {
+        drain();
         return rc;
     }
     *m = count;
     if (count == 0) {
-        CLATCH_CUDA(cudaStreamSynchronize(st));
+        drain();
         return CLATCH_OK;
     }
-    CLATCH_CUDA(cudaMemcpyAsync(ctx->kps.ptr, ctx->host_xycs.data(), sizeof(double) * 4 * count,
-                                cudaMemcpyHostToDevice, st));
-    int rc;
-    if (kU8)
-        rc = launch_extract_u8(ctx, ctx->img.as<uint8_t>(), width, height, dpitch, ctx->kps.as<double>(), count,
-                               ctx->desc.as<uint8_t>(), st);
-    else
-        rc = launch_extract_f64(ctx, ctx->img.as<double>(), width, height, dpitch, ctx->kps.as<double>(), count,
-                                ctx->desc.as<uint8_t>(), st);
-    if (rc) return rc;
-    CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
-    CLATCH_CUDA(cudaStreamSynchronize(st));
+    // 3. bucket the kept keypoints by the band in which their footprint (rows floor(y)-45 ..
+    //    floor(y)+46) ends; a stable counting sort keeps input order inside a bucket
+    std::vector<uint32_t> order;          // order[slot] = kept-index computed in that slot
+    size_t bucket_begin[9] = {0};
+    if (bands > 1) {
+        std::vector<uint8_t> band_of(count);
+        size_t hist[9] = {0};
+        for (size_t j = 0; j < count; ++j) {
+            const int bottom = static_cast<int>(std::floor(xycs[4 * j + 1])) + 46;
+            const int b = std::min(bands - 1, bottom / band_rows);
+            band_of[j] = static_cast<uint8_t>(b);
+            ++hist[b + 1];
+        }
+        for (int b = 0; b < bands; ++b) bucket_begin[b + 1] = bucket_begin[b] + hist[b + 1];
+        order.resize(count);
+        size_t cursor[8];
+        for (int b = 0; b < bands; ++b) cursor[b] = bucket_begin[b];
+        for (size_t j = 0; j < count; ++j) order[cursor[band_of[j]]++] = static_cast<uint32_t>(j);
+        ctx->host_xycs.resize(4 * count);   // permuted copy goes to the pinned buffer in place
+        std::memcpy(ctx->host_xycs.data(), xycs, sizeof(double) * 4 * count);
+        for (size_t s = 0; s < count; ++s) std::memcpy(xycs + 4 * s, ctx->host_xycs.data() + 4 * order[s], 32);
+    } else {
+        bucket_begin[1] = count;
+    }
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->kps.ptr, xycs, sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
+    // 4. per band: wait for its rows, (f64) classify them, extract the bucket
+    int rc = CLATCH_OK;
+    for (int b = 0; b < bands && !rc; ++b) {
+        const int r0 = b * band_rows, r1 = bands == 1 ? height : std::min(height, r0 + band_rows);
+        if (bands > 1) CLATCH_CUDA(cudaStreamWaitEvent(st, ctx->band_events[b], 0));
+        const size_t begin = bucket_begin[b], cnt = bucket_begin[b + 1] - begin;
+        const double* d_x = ctx->kps.as<double>() + 4 * begin;
+        uint8_t* d_o = ctx->desc.as<uint8_t>() + bytes * begin;
+        if (kU8) {
+            rc = launch_extract_u8(ctx, ctx->img.as<uint8_t>(), width, height, dpitch, d_x, cnt, d_o, st);
+        } else {
+            rc = launch_classify_rows(ctx, ctx->img.as<double>(), width, height, dpitch, r0, r1, b == 0, st);
+            if (!rc) rc = launch_extract_f64_classified(ctx, ctx->img.as<double>(), width, height, dpitch, d_x, cnt, d_o, st);
+        }
+    }
+    if (rc) {
+        drain();
+        return rc;
+    }
+    // 5. descriptors come back through page-locked staging; undo the bucket order on the way out
+    if (bands == 1) {
+        CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+        CLATCH_CUDA(cudaStreamSynchronize(st));
+    } else {
+        CLATCH_CUDA(cudaMemcpyAsync(ctx->pin_desc.ptr, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+        CLATCH_CUDA(cudaStreamSynchronize(st));
+        const uint8_t* src = static_cast<const uint8_t*>(ctx->pin_desc.ptr);
+        for (size_t s = 0; s < count; ++s) std::memcpy(out + bytes * order[s], src + bytes * s, bytes);
+    }
     return CLATCH_OK;
 }
 

@@ -440,13 +440,15 @@ __global__ void __launch_bounds__(kThreads, 2) extract_generic_kernel(ExtractPar
 
 // f64 -> u8 promotion: flags[0] = 1 if some pixel is not an integer in [0, 255]
 // (or not finite), else stays 0; dst receives the (lossless when flags[0]==0) u8 copy.
+// Rows [row0, row1) only, so an image that arrives in row bands can be classified band by band;
+// the flag accumulates ("some pixel seen so far is not a u8 value").
 __global__ void classify_convert_kernel(const double* src, size_t src_pitch, uint8_t* dst,
-                                        size_t dst_pitch, int width, int height, int* flags) {
-    const size_t n = static_cast<size_t>(width) * height;
+                                        size_t dst_pitch, int width, int row0, int row1, int* flags) {
+    const size_t n = static_cast<size_t>(width) * (row1 - row0);
     bool bad = false;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int yy = static_cast<int>(i / width), xx = static_cast<int>(i - static_cast<size_t>(yy) * width);
+        const int yy = row0 + static_cast<int>(i / width), xx = static_cast<int>(i % width);
         const double v = src[static_cast<size_t>(yy) * src_pitch + xx];
         const bool ok = (v >= 0.0) && (v <= 255.0) && (v == floor(v));   // NaN/inf fail
         bad |= !ok;
@@ -514,25 +516,42 @@ int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int heig
     return launch_extract<true>(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, nullptr, 0);
 }
 
-int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
-                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream) {
-    if (M == 0) return CLATCH_OK;
-    // Promote to u8 on the device when every pixel is an integer in [0,255] (true for
-    // every PGM-sourced image, src/image.cpp:75-76); both kernels are queued and the
-    // flag picks one on the device, so no host round trip is needed.
+// f64 images are promoted to u8 on the device when every pixel is an integer in [0,255] (true
+// for every PGM-sourced image, src/image.cpp:75-76). Classification and extraction are
+// separate steps so that a banded upload can interleave them: classify the rows that have
+// arrived, then extract the keypoints whose footprints lie inside them. Both extraction
+// kernels are queued and the device flag picks one — no host round trip.
+int launch_classify_rows(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch, int row0,
+                         int row1, bool reset, cudaStream_t stream) {
     const size_t u8_pitch = (static_cast<size_t>(width) + 15) / 16 * 16;
     if (int rc = ctx->img_u8.reserve(u8_pitch * height)) return rc;
     if (int rc = ctx->flags.reserve(sizeof(int))) return rc;
     int* flags = ctx->flags.as<int>();
-    CLATCH_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), stream));
-    classify_convert_kernel<<<ctx->sm_count * 8, 256, 0, stream>>>(
-        d_img, pitch, ctx->img_u8.as<uint8_t>(), u8_pitch, width, height, flags);
+    if (reset) CLATCH_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), stream));
+    if (row1 <= row0) return CLATCH_OK;
+    classify_convert_kernel<<<ctx->sm_count * 8, 256, 0, stream>>>(d_img, pitch, ctx->img_u8.as<uint8_t>(), u8_pitch,
+                                                                   width, row0, row1, flags);
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
+    return CLATCH_OK;
+}
+
+int launch_extract_f64_classified(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
+                                  const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream) {
+    if (M == 0) return CLATCH_OK;
+    const size_t u8_pitch = (static_cast<size_t>(width) + 15) / 16 * 16;
+    int* flags = ctx->flags.as<int>();
     if (int rc = launch_extract<true>(ctx, ctx->img_u8.ptr, width, height, u8_pitch, d_xycs, M, d_out,
                                       stream, flags, 0))
         return rc;
     return launch_extract<false>(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, flags, 1);
+}
+
+int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
+                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream) {
+    if (M == 0) return CLATCH_OK;
+    if (int rc = launch_classify_rows(ctx, d_img, width, height, pitch, 0, height, true, stream)) return rc;
+    return launch_extract_f64_classified(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream);
 }
 
 } // namespace clatch

@@ -80,6 +80,9 @@ struct clatch_ctx {
     clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t, items, scores, counts, det;
     std::vector<double> host_xycs;   // describe_all staging
     clatch::PinnedBuffer pinned;     // D2H staging for batched pair results
+    clatch::PinnedBuffer pin_xycs, pin_desc;   // describe_all staging (banded upload path)
+    cudaStream_t copy_stream = nullptr;        // image bands stream in here while kernels run on `stream`
+    cudaEvent_t band_events[8] = {};
     struct PipeSlot {                // describe_batch: one of two pipeline slots
         cudaStream_t stream = nullptr;
         clatch::DeviceBuffer img, kps, desc, img_u8, flags;
@@ -97,6 +100,10 @@ int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int heig
                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
 int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
                        const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
+int launch_classify_rows(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch, int row0,
+                         int row1, bool reset, cudaStream_t stream);
+int launch_extract_f64_classified(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
+                                  const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
 
 // detection (clatch_detect.cu)
 struct Detection {   // one FAST detection as the device leaves it (row-major order)

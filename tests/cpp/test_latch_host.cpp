@@ -13,6 +13,9 @@
 #include "latch_b200.hpp"
 
 extern "C" {   // oracle/latch_oracle.c — test infrastructure
+size_t oracle_detect_and_orient(const double* img, int w, int h, double threshold, int do_nms, int radius,
+                                double* out, size_t cap);
+size_t oracle_fast_detect(const double* img, int w, int h, double threshold, int do_nms, double* out, size_t cap);
 void oracle_structured_image(uint64_t seed, int w, int h, double* out);
 void oracle_random_image(uint64_t seed, int w, int h, double* out);
 void oracle_random_descriptors(uint64_t seed, size_t n, int bytes, uint8_t* out);
@@ -272,6 +275,33 @@ int main(int argc, char** argv) {
         for (size_t i = 0; i < 65536; ++i) golden.data[i] = static_cast<unsigned char>(pgm[header + i]);
         const Descriptor d = latch::describe(golden, {128.0, 128.0, 0.3, 0.0}, pattern);
         CHECK(std::string(d.bytes.begin(), d.bytes.end()) == bits);
+    }
+
+    // ---- detection (test_detect.cpp:34-41, 128-151; acceptance.cpp:120-123) ----
+    {
+        Image flat(32, 32);
+        for (double& v : flat.data) v = 77.0;
+        CHECK(latch::fast_detect(flat, 20.0, true).empty());
+        CHECK_THROWS_CODE(latch::fast_detect(Image(6, 32), 20.0, true), ErrorCode::ImageTooSmall);
+        for (int structured = 0; structured < 2; ++structured) {
+            const Image img = make_image(structured != 0, 21 + structured, 320, 240);
+            std::vector<double> want(4 * img.data.size());
+            const size_t n = oracle_detect_and_orient(img.data.data(), img.width, img.height, 20.0, 1, 15, want.data(),
+                                                      img.data.size());
+            const auto got = latch::detect_and_orient(img, 20.0, true);
+            CHECK(got.size() == n);
+            bool same = got.size() == n;
+            for (size_t i = 0; same && i < n; ++i)
+                same = got[i].x == want[4 * i] && got[i].y == want[4 * i + 1] && got[i].theta == want[4 * i + 2] &&
+                       got[i].score == want[4 * i + 3];
+            CHECK(same);
+            const size_t m = oracle_fast_detect(img.data.data(), img.width, img.height, 25.5, 0, want.data(),
+                                                img.data.size());
+            const auto raw = latch::fast_detect(img, 25.5, false);
+            CHECK(raw.size() == m);
+            for (size_t i = 1; i < raw.size(); ++i)   // sorted by (y, x)
+                CHECK((raw[i - 1].y < raw[i].y || (raw[i - 1].y == raw[i].y && raw[i - 1].x < raw[i].x)));
+        }
     }
 
     std::printf("%s: %d checks, %d failures\n", g_failures ? "FAILED" : "PASSED", g_checks, g_failures);

@@ -551,3 +551,25 @@ def test_triplet_bits_scoring(lk, port, vectors):
     assert np.array_equal(lk.describe(img, kps, pattern=(GOLDEN / "pattern_t64k5w.latchpat").read_text())[1],
                           port.describe_all(img, kps, pattern=oracle.parse_pattern_text(
                               (GOLDEN / "pattern_t64k5w.latchpat").read_text()))[1])
+
+
+def test_banded_upload_large_images(lk, port):
+    """Images above a few MB go up in row bands with extraction overlapping the DMA; keypoints
+    are bucketed by band and un-permuted on the way out. Results and order must not change."""
+    w, h = 1920, 1080
+    img = port.structured_image(77, w, h)                     # float64: 16.6 MB -> 7 bands
+    kps = port.random_keypoints(78, w, h, 1500)
+    kps[::50, 1] = 30.0                                       # margin violators stay dropped, order kept
+    kps[5] = [100.0, 46.0, 0.3, 1.0]                          # footprint ends in the first band
+    kps[6] = [100.0, h - 47.0, -0.3, 2.0]                     # ... and in the last one
+    want_kept, want = port.describe_all(img, kps)
+    kept, desc = lk.describe(img, kps)
+    assert np.array_equal(kept, kps[want_kept]) and np.array_equal(desc, want)
+    frac = img + 0.25                                         # non-integer: f64 sampling kernel per band
+    assert np.array_equal(lk.describe(frac, kps)[1], port.describe_all(frac, kps)[1])
+    frac2 = img.copy()
+    frac2[h - 3, w - 3] = 0.5                                 # only the LAST band is non-integer
+    assert np.array_equal(lk.describe(frac2, kps)[1], port.describe_all(frac2, kps)[1])
+    big = port.random_image_u8(79, 3840, 2160)                # uint8: 8.3 MB -> 4 bands
+    k2 = port.random_keypoints(80, 3840, 2160, 700)
+    assert np.array_equal(lk.describe(big, k2)[1], port.describe_all(big.astype(np.float64), k2)[1])
