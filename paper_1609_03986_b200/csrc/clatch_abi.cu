@@ -457,11 +457,10 @@ int clatch_extract_f64(clatch_ctx* ctx, const double* img, int width, int height
 
 } // extern "C"
 
-// describe_all with a banded upload: the image goes up in row bands on a copy stream while
-// the host filters keypoints and evaluates cos/sin; keypoints are bucketed by the band in
-// which their 92-row footprint ends, and each bucket's extraction is queued on the compute
-// stream behind that band's arrival event. Extraction of band b overlaps the DMA of bands
-// b+1.. (a 16.6 MB float64 frame costs more to upload than to describe).
+// describe_all. The image DMA is queued first so that it overlaps the host-side margin filter
+// and trig pass. Optionally (see `bands` below) the image goes up in row bands on a copy stream,
+// keypoints are bucketed by the band in which their 92-row footprint ends, and each bucket's
+// extraction is queued behind that band's arrival event.
 template <typename Pixel>
 static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int height, size_t pitch,
                              const double* kps, size_t n, int cols, int workers, int64_t* kept,
@@ -483,10 +482,13 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
     if (int rc = ctx->pin_desc.reserve(bytes * n)) return rc;
     cudaStream_t st = ctx->stream;
 
-    // Bands of >= 2 MiB, at most 8; small images go up in one piece.
-    const size_t image_bytes = sizeof(Pixel) * static_cast<size_t>(width) * height;
-    int bands = static_cast<int>(std::min<size_t>(8, image_bytes / (2u << 20)));
-    if (bands < 2 || n < 512) bands = 1;
+    // Opt-in (CLATCH_UPLOAD_BANDS=2..8): measured on B200 with a 16.6 MB float64 frame and 10 k
+    // keypoints, 1/2/3/4 bands take 0.73/0.76/0.80/0.85 ms — each band costs three launches, an
+    // event wait and a partial last wave of the persistent kernel, more than the overlap returns —
+    // so one piece is the default.
+    int bands = 1;
+    if (const char* env = std::getenv("CLATCH_UPLOAD_BANDS")) bands = std::max(1, std::min(8, std::atoi(env)));
+    if (n < 2048) bands = 1;
     const int band_rows = (height + bands - 1) / bands;
     if (bands > 1 && !ctx->copy_stream) {
         CLATCH_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));

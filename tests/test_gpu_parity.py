@@ -553,12 +553,15 @@ def test_triplet_bits_scoring(lk, port, vectors):
                               (GOLDEN / "pattern_t64k5w.latchpat").read_text()))[1])
 
 
-def test_banded_upload_large_images(lk, port):
-    """Images above a few MB go up in row bands with extraction overlapping the DMA; keypoints
-    are bucketed by band and un-permuted on the way out. Results and order must not change."""
+@pytest.mark.parametrize("bands", ["1", "3"])
+def test_banded_upload_large_images(lk, port, bands, monkeypatch):
+    """CLATCH_UPLOAD_BANDS: the image can go up in row bands with extraction queued per band;
+    keypoints are bucketed by band and un-permuted on the way out. Results and order must not
+    change."""
+    monkeypatch.setenv("CLATCH_UPLOAD_BANDS", bands)
     w, h = 1920, 1080
-    img = port.structured_image(77, w, h)                     # float64: 16.6 MB -> 7 bands
-    kps = port.random_keypoints(78, w, h, 1500)
+    img = port.structured_image(77, w, h)                     # float64, 16.6 MB
+    kps = port.random_keypoints(78, w, h, 2500)
     kps[::50, 1] = 30.0                                       # margin violators stay dropped, order kept
     kps[5] = [100.0, 46.0, 0.3, 1.0]                          # footprint ends in the first band
     kps[6] = [100.0, h - 47.0, -0.3, 2.0]                     # ... and in the last one
@@ -570,6 +573,6 @@ def test_banded_upload_large_images(lk, port):
     frac2 = img.copy()
     frac2[h - 3, w - 3] = 0.5                                 # only the LAST band is non-integer
     assert np.array_equal(lk.describe(frac2, kps)[1], port.describe_all(frac2, kps)[1])
-    big = port.random_image_u8(79, 3840, 2160)                # uint8: 8.3 MB -> 4 bands
-    k2 = port.random_keypoints(80, 3840, 2160, 700)
+    big = port.random_image_u8(79, 3840, 2160)                # uint8, 8.3 MB
+    k2 = port.random_keypoints(80, 3840, 2160, 2100)
     assert np.array_equal(lk.describe(big, k2)[1], port.describe_all(big.astype(np.float64), k2)[1])
