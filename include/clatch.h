@@ -74,9 +74,18 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
 
 /* Tuning knobs (never change results). key "match_variant": 0 = XOR + 16 POPC, 1 = carry-save
  * compression + 9 POPC, 2 = 9 CSA + 7 POPC, 3 = tcgen05 int8 GEMM on the tensor cores (default).
- * key "extract_variant": 0 = one window per CTA, 1 = four windows per CTA with conflict-free
- * shared loads (default). Unknown keys fail with CLATCH_ERR_INVALID. */
+ * key "extract_variant": 0 = one window per CTA, 1 = four fp64 windows per CTA with conflict-free
+ * shared loads, 2 = four split (fp32 + low word) windows per CTA: a proven fp32 estimate decides
+ * each bit and the rare undecided ones are recomputed exactly (default; u8-valued images — any
+ * other image runs variant 1). Every variant returns the same bytes.
+ * key "extract_stats": non-zero starts counting variant 2's exact recomputes (and zeroes the
+ * counters), 0 stops. Unknown keys fail with CLATCH_ERR_INVALID. */
 CLATCH_API int clatch_set_option(clatch_ctx* ctx, const char* key, int value);
+
+/* Counters of the filtered extraction kernel since "extract_stats" was switched on: triplets
+ * whose bit was recomputed in exact fp64, and warp passes that entered the exact path. Waits for
+ * the context's streams. Diagnostics only. */
+CLATCH_API int clatch_extract_stats(clatch_ctx* ctx, uint64_t* exact_triplets, uint64_t* exact_warps);
 
 /* Block until everything queued on the context's own stream has finished. */
 CLATCH_API int clatch_synchronize(clatch_ctx* ctx);

@@ -53,6 +53,7 @@ _SIGNATURES = {
                                      C.c_size_t]),
     "clatch_synchronize": (C.c_int, [C.c_void_p]),
     "clatch_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
+    "clatch_extract_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "clatch_set_pattern": (C.c_int, [C.c_void_p, i16p, C.c_int, C.c_int, f64p]),
     "clatch_descriptor_bytes": (C.c_int, [C.c_void_p]),
     "clatch_prepare_keypoints": (C.c_int, [f64p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, f64p,

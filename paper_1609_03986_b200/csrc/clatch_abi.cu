@@ -17,6 +17,12 @@
 #include "slot_assign.hpp"
 
 namespace clatch {
+namespace {
+#include "default_plan_f8.inc"
+}
+}
+
+namespace clatch {
 
 namespace {
 thread_local std::string g_error = "";
@@ -211,7 +217,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
     }
     for (DeviceBuffer* b : {&ctx->img, &ctx->kps, &ctx->desc, &ctx->q, &ctx->t, &ctx->res,
                             &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->items, &ctx->scores, &ctx->counts, &ctx->det, &ctx->pattern.slots, &ctx->pattern.slots_quad,
-                            &ctx->pattern.triplets})
+                            &ctx->pattern.slots_f8, &ctx->extract_stats, &ctx->pattern.triplets})
         b->release();
     ctx->pinned.release();
     ctx->pin_xycs.release();
@@ -251,8 +257,15 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         return CLATCH_OK;
     }
     if (std::strcmp(key, "extract_variant") == 0) {
-        if (value < 0 || value > 1) return invalid("extract_variant must be 0 or 1");
+        if (value < 0 || value > 2) return invalid("extract_variant must be 0..2");
         ctx->extract_variant = value;
+        return CLATCH_OK;
+    }
+    if (std::strcmp(key, "extract_stats") == 0) {   // count exact recomputes of the filtered kernel
+        CLATCH_CUDA(cudaSetDevice(ctx->device));
+        if (int rc = ctx->extract_stats.reserve(2 * sizeof(unsigned long long))) return rc;
+        CLATCH_CUDA(cudaMemsetAsync(ctx->extract_stats.ptr, 0, 2 * sizeof(unsigned long long), ctx->stream));
+        ctx->extract_stats_on = value != 0;
         return CLATCH_OK;
     }
     return invalid(std::string("clatch_set_option: unknown key '") + key + "'");
@@ -266,6 +279,21 @@ int clatch_synchronize(clatch_ctx* ctx) {
 }
 
 uint64_t clatch_launch_count(clatch_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int clatch_extract_stats(clatch_ctx* ctx, uint64_t* exact_triplets, uint64_t* exact_warps) {
+    if (!ctx) return invalid("clatch_extract_stats: ctx is null");
+    unsigned long long h[2] = {0, 0};
+    if (ctx->extract_stats.ptr) {
+        CLATCH_CUDA(cudaSetDevice(ctx->device));
+        CLATCH_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int s = 0; s < 2; ++s)
+            if (ctx->pipe[s].stream) CLATCH_CUDA(cudaStreamSynchronize(ctx->pipe[s].stream));
+        CLATCH_CUDA(cudaMemcpy(h, ctx->extract_stats.ptr, sizeof(h), cudaMemcpyDeviceToHost));
+    }
+    if (exact_triplets) *exact_triplets = h[0];
+    if (exact_warps) *exact_warps = h[1];
+    return CLATCH_OK;
+}
 
 int clatch_descriptor_bytes(clatch_ctx* ctx) { return ctx ? ctx->pattern.T / 8 : 0; }
 
@@ -322,18 +350,26 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
     if (int rc = pat.triplets.reserve(sizeof(int16_t) * 6 * T)) return rc;
     CLATCH_CUDA(cudaMemcpy(pat.triplets.ptr, triplets, sizeof(int16_t) * 6 * T, cudaMemcpyHostToDevice));
     if (int rc = upload_weights(w.data(), K * K)) return rc;
+    pat.host_triplets.assign(triplets, triplets + 6 * static_cast<size_t>(T));
+    pat.slots_planned = false;
     if (pat.fast) {
-        // Lane placement that keeps the 64-bit window loads (nearly) bank-conflict free.
-        const SlotPlan plan = plan_slots(triplets, T, kWinStride, 1000000);
-        pat.slot_degree = plan.avg_degree;
-        pat.slot_degree_identity = plan.avg_degree_identity;
+        // Lane placements that keep the window loads (nearly) bank-conflict free (slot_assign.hpp).
         static_assert(sizeof(SlotEntry) == sizeof(ushort4), "slot layout");
-        if (int rc = pat.slots.reserve(sizeof(SlotEntry) * T)) return rc;
-        CLATCH_CUDA(cudaMemcpy(pat.slots.ptr, plan.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
         const SlotPlan quad = plan_slots_quad(triplets, T, kWinStride, 300000);
         pat.slot_degree_quad = quad.avg_degree;
         if (int rc = pat.slots_quad.reserve(sizeof(SlotEntry) * T)) return rc;
         CLATCH_CUDA(cudaMemcpy(pat.slots_quad.ptr, quad.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
+        if (int rc = pat.slots_f8.reserve(sizeof(SlotEntry) * T)) return rc;
+        if (triplet_hash(triplets, T) == kDefaultPlanHash && kDefaultPlanStride == kWinStride) {
+            // the built-in table: placement precomputed by a long anneal (tools/gen_default_plan.py)
+            static_assert(sizeof(kDefaultPlanF8) == sizeof(SlotEntry) * kFastT, "embedded plan size");
+            pat.slot_degree_f8 = kDefaultPlanDegree;
+            CLATCH_CUDA(cudaMemcpy(pat.slots_f8.ptr, kDefaultPlanF8, sizeof(kDefaultPlanF8), cudaMemcpyHostToDevice));
+        } else {
+            const SlotPlan f8 = plan_slots_grouped(triplets, T, kWinStride, 8, 8, 1500000);
+            pat.slot_degree_f8 = f8.avg_degree;
+            CLATCH_CUDA(cudaMemcpy(pat.slots_f8.ptr, f8.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
+        }
     }
     return CLATCH_OK;
 }

@@ -21,6 +21,7 @@
 #include <cstdio>
 
 #include "clatch_internal.cuh"
+#include "slot_assign.hpp"
 
 namespace clatch {
 
@@ -44,6 +45,7 @@ struct ExtractParams {
     int T, K;
     const int* flags;          // optional device flags (f64 promotion), may be null
     int run_if_flag;           // run only when flags[0] == run_if_flag (if flags != null)
+    unsigned long long* stats; // optional {triplets recomputed exactly, warps that took the exact pass}
 };
 
 // Exact u8 -> f64 without the 16-lane/clk conversion pipe (I2F.F64 runs at 16/clk/SM on
@@ -376,6 +378,222 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_quad_kernel(ExtractPa
     }
 }
 
+// ---- filtered kernel: fp32 estimate of every SSD pair, exact fp64 only where it is needed ----
+// The reference's bit is sign(d1 - d2) of two 49-term fp64 sums; almost always |d1 - d2| is
+// many orders of magnitude above anything rounding could change. So each window is kept as
+// two 32-bit planes instead of one 64-bit one:
+//   F  plane: f = cvt.rz.f32.f64(v)   (v truncated to 24 significant bits, 0 <= v - f < 2^-16)
+//   LO plane: the low word of v
+// and v is recovered exactly from the pair (hi word = (f >> 3) + 0x38000000 for f != 0: same
+// exponent after re-biasing, f's top 20 mantissa bits; u8 images give 0 or 2^-106 <= v <= 255,
+// always normal in fp32). The SSD phase reads ONLY the F plane — half the shared-memory
+// wavefronts of the 64-bit window, fp32 FMAs instead of unfused fp64 — and proves its answer:
+//   |d_ref - d_f| <= 14*2^-16*sqrt(d_f) + 49*2^-32   (truncated inputs, Cauchy-Schwarz over 49 terms)
+//                    + 52*2^-24*d_f                   (fp32 subtraction + 49 fused accumulations)
+//                    + 6e-15*d_f                      (the reference's own fp64 roundings)
+// per chain; if |d1_f - d2_f| exceeds the sum of both chains' bounds (constants rounded up by
+// >= 3 %) the sign is the reference's. Otherwise — exact ties in flat regions, or sums closer than
+// ~2 parts in 10^5 — the lane recomputes both chains exactly from (F, LO) in the reference's order,
+// with the same unfused fp64 arithmetic as the other kernels. The decision is never approximate.
+//
+// Lanes: warp = 8 triplets x 4 keypoints (lane = 4*i + w), plane w displaced by 8*w banks, so a
+// 32-bit load is conflict-free when the 8 triplets differ mod 8 (plan_slots_grouped(8, 8)).
+constexpr int kPlanePitch = 4168;                                    // words; 64 x 65 + 8; % 32 == 8
+constexpr int kFiltSmemBytes = 2 * kQuad * kPlanePitch * 4           // F planes, LO planes
+                               + 2 * kQuad * kQuadTileBytes          // double-buffered u8 tiles
+                               + kQuad * kFastT                      // predicate bytes
+                               + kQuad * 2 * kWindow * 8;            // s*dv, c*dv tables
+constexpr int kLoPlane = kQuad * kPlanePitch;                        // word offset F plane -> LO plane
+
+__device__ __forceinline__ void build_window_split(float* fpl, const uint8_t* tile, int ax0, int ty0, double x,
+                                                   double y, double c, double s, const double* tab, int tid) {
+    const int u = tid & 63;
+    const double du = static_cast<double>(u) - 31.5;
+    const double xa = __dadd_rn(x, __dmul_rn(c, du));
+    const double ya = __dadd_rn(y, __dmul_rn(s, du));
+#pragma unroll 4
+    for (int v = tid >> 6; v < kWindow; v += kThreads / 64) {
+        const double sx = __dsub_rn(xa, tab[v]);
+        const double sy = __dadd_rn(ya, tab[kWindow + v]);
+        int x0, y0;
+        double x0f, y0f;
+        floor_exact(sx, x0, x0f);
+        floor_exact(sy, y0, y0f);
+        const double fx = __dsub_rn(sx, x0f);
+        const double fy = __dsub_rn(sy, y0f);
+        const uint8_t* p = tile + (y0 - ty0) * kTileW + (x0 - ax0);
+        const double val = blend(fx, fy, u8_to_f64(p[0]), u8_to_f64(p[1]), u8_to_f64(p[kTileW]),
+                                 u8_to_f64(p[kTileW + 1]));
+        fpl[v * kWinStride + u] = __double2float_rz(val);
+        reinterpret_cast<int*>(fpl)[kLoPlane + v * kWinStride + u] = __double2loint(val);
+    }
+}
+
+// fp32 estimate of both chains of two slots at once (four independent accumulators).
+__device__ __forceinline__ void ssd_estimate_2(const float* win, const ushort4 s0, const ushort4 s1, float& d1a,
+                                               float& d2a, float& d1b, float& d2b) {
+    const float* pa0 = win + s0.x;
+    const float* pb0 = win + s0.y;
+    const float* pc0 = win + s0.z;
+    const float* pa1 = win + s1.x;
+    const float* pb1 = win + s1.y;
+    const float* pc1 = win + s1.z;
+    d1a = d2a = d1b = d2b = 0.0f;
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+#pragma unroll
+        for (int c = 0; c < 7; ++c) {
+            const int o = r * kWinStride + c;
+            const float a0 = pa0[o], a1 = pa1[o];
+            const float e10 = a0 - pb0[o], e20 = a0 - pc0[o];
+            const float e11 = a1 - pb1[o], e21 = a1 - pc1[o];
+            d1a = __fmaf_rn(e10, e10, d1a);
+            d2a = __fmaf_rn(e20, e20, d2a);
+            d1b = __fmaf_rn(e11, e11, d1b);
+            d2b = __fmaf_rn(e21, e21, d2b);
+        }
+    }
+}
+
+// True when sign(d1 - d2) of the fp32 estimate is provably the reference's (bound above).
+__device__ __forceinline__ bool estimate_decides(float d1, float d2, float& diff) {
+    float r1, r2;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d1));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r2) : "f"(d2));
+    diff = d1 - d2;
+    const float bound = __fmaf_rn(2.2e-4f, r1 + r2, __fmaf_rn(3.3e-6f, d1 + d2, 3.0e-8f));
+    return fabsf(diff) > bound;
+}
+
+__device__ __forceinline__ double plane_value(const float* p) {
+    const unsigned f = __float_as_uint(p[0]);
+    const int lo = __float_as_int(p[kLoPlane]);
+    const unsigned hi = f ? (f >> 3) + 0x38000000u : 0u;
+    return __hiloint2double(static_cast<int>(hi), lo);
+}
+
+// The exact chains (same arithmetic and order as triplet_bit_7x7) from the split planes.
+__device__ __noinline__ bool triplet_bit_7x7_planes(const float* win, int oa, int ob, int oc, bool swapped) {
+    const float* pa = win + oa;
+    const float* pb = win + ob;
+    const float* pc = win + oc;
+    double d1 = 0.0, d2 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+#pragma unroll
+        for (int c = 0; c < 7; ++c) {
+            const int o = r * kWinStride + c;
+            const double a = plane_value(pa + o);
+            const double e1 = __dsub_rn(a, plane_value(pb + o));
+            const double e2 = __dsub_rn(a, plane_value(pc + o));
+            d1 = __dadd_rn(d1, __dmul_rn(e1, e1));
+            d2 = __dadd_rn(d2, __dmul_rn(e2, e2));
+        }
+    }
+    return swapped ? d2 > d1 : d1 > d2;
+}
+
+__global__ void __launch_bounds__(kQuadThreads, 1) extract_filt_kernel(ExtractParams p) {
+    if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
+
+    extern __shared__ __align__(16) uint8_t s_quad[];
+    float* const s_f = reinterpret_cast<float*>(s_quad);
+    uint8_t* const s_tile = s_quad + 2 * kQuad * kPlanePitch * 4;
+    uint8_t* const s_bits = s_tile + 2 * kQuad * kQuadTileBytes;
+    double* const s_tab = reinterpret_cast<double*>(s_bits + kQuad * kFastT);
+
+    const int tid = threadIdx.x;
+    const int grp = tid >> 8, gt = tid & (kThreads - 1);         // staging / resampling: group -> keypoint
+    const int warp = tid >> 5, lane = tid & 31, kb = lane & 3, ti = lane >> 2;   // SSD: 8 triplets x 4 keypoints
+    const ushort4 slot0 = __ldg(p.slots + 8 * warp + ti);
+    const ushort4 slot1 = __ldg(p.slots + 8 * warp + ti + kFastT / 2);
+    const float* const my_win = s_f + kb * kPlanePitch;
+    uint8_t* const my_bits = s_bits + kb * kFastT;
+    double* const my_tab = s_tab + grp * 2 * kWindow;
+    const uint8_t* const img8 = static_cast<const uint8_t*>(p.img);
+    const bool aligned = (reinterpret_cast<uintptr_t>(p.img) % 16 == 0) && (p.pitch % 16 == 0);
+    const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
+    unsigned n_flagged = 0, n_warps = 0;
+
+    if (aligned) {
+        const unsigned long long kp = static_cast<unsigned long long>(blockIdx.x) * kQuad + grp;
+        if (blockIdx.x < quads && kp < p.M) {
+            int ax0, ty0;
+            tile_origin(__ldg(p.xycs + 4 * kp), __ldg(p.xycs + 4 * kp + 1), true, ax0, ty0);
+            stage_tile_async(s_tile + grp * kQuadTileBytes, img8, p.pitch, p.height, ax0, ty0, gt);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+
+    int buf = 0;
+    for (unsigned long long quad = blockIdx.x; quad < quads; quad += gridDim.x, buf ^= 1) {
+        const unsigned long long kp = quad * kQuad + grp;
+        const bool valid = kp < p.M;
+        double x = 0, y = 0, c = 0, s = 0;
+        int ax0 = 0, ty0 = 0;
+        uint8_t* const tile = s_tile + (buf * kQuad + grp) * kQuadTileBytes;
+        if (valid) {
+            x = __ldg(p.xycs + 4 * kp + 0);
+            y = __ldg(p.xycs + 4 * kp + 1);
+            c = __ldg(p.xycs + 4 * kp + 2);
+            s = __ldg(p.xycs + 4 * kp + 3);
+            tile_origin(x, y, aligned, ax0, ty0);
+            if (!aligned) stage_tile_u8<kThreads>(tile, img8, p.pitch, p.height, ax0, ty0, false, gt);
+            if (gt < kWindow) {   // per-row products of extract_window (src/descriptor.cpp:44-45)
+                const double dv = static_cast<double>(gt) - 31.5;
+                my_tab[gt] = __dmul_rn(s, dv);
+                my_tab[kWindow + gt] = __dmul_rn(c, dv);
+            }
+        }
+        if (aligned) asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();   // tiles + tables ready; the previous quad's plane / bit readers are done
+        if (valid) build_window_split(s_f + grp * kPlanePitch, tile, ax0, ty0, x, y, c, s, my_tab, gt);
+        __syncthreads();
+        if (aligned) {     // next quad's tiles stream in while the SSD phase runs
+            const unsigned long long nq = quad + gridDim.x, nkp = nq * kQuad + grp;
+            if (nq < quads && nkp < p.M) {
+                int nax0, nty0;
+                tile_origin(__ldg(p.xycs + 4 * nkp), __ldg(p.xycs + 4 * nkp + 1), true, nax0, nty0);
+                stage_tile_async(s_tile + ((buf ^ 1) * kQuad + grp) * kQuadTileBytes, img8, p.pitch, p.height, nax0,
+                                 nty0, gt);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        float d1a, d2a, d1b, d2b, diff0, diff1;
+        ssd_estimate_2(my_win, slot0, slot1, d1a, d2a, d1b, d2b);
+        const bool sure0 = estimate_decides(d1a, d2a, diff0);
+        const bool sure1 = estimate_decides(d1b, d2b, diff1);
+        bool bit0 = (slot0.w >> 15) ? diff0 < 0.0f : diff0 > 0.0f;
+        bool bit1 = (slot1.w >> 15) ? diff1 < 0.0f : diff1 > 0.0f;
+        // A keypoint past the end of the list leaves a stale window: never worth an exact pass.
+        const bool live = quad * kQuad + kb < p.M;
+        const unsigned undecided = __ballot_sync(0xffffffffu, live && !(sure0 && sure1));
+        if (undecided) {
+            if (live && !sure0) bit0 = triplet_bit_7x7_planes(my_win, slot0.x, slot0.y, slot0.z, slot0.w >> 15);
+            if (live && !sure1) bit1 = triplet_bit_7x7_planes(my_win, slot1.x, slot1.y, slot1.z, slot1.w >> 15);
+            n_flagged += (live && !sure0) + (live && !sure1);
+            n_warps += lane == 0;
+        }
+        my_bits[slot0.w & 0x7fff] = bit0;
+        my_bits[slot1.w & 0x7fff] = bit1;
+        __syncthreads();
+        const unsigned w0 = __ballot_sync(0xffffffffu, s_bits[grp * kFastT + gt] != 0);
+        const unsigned w1 = __ballot_sync(0xffffffffu, s_bits[grp * kFastT + gt + kThreads] != 0);
+        if ((tid & 31) == 0 && valid) {
+            unsigned* out32 = reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8));
+            out32[gt >> 5] = w0;
+            out32[(gt >> 5) + kThreads / 32] = w1;
+        }
+    }
+    if (p.stats != nullptr) {   // exact-pass counters (diagnostics; off unless asked for)
+        n_flagged = __reduce_add_sync(0xffffffffu, n_flagged);
+        if (lane == 0 && (n_flagged | n_warps)) {
+            atomicAdd(p.stats + 0, static_cast<unsigned long long>(n_flagged));
+            atomicAdd(p.stats + 1, static_cast<unsigned long long>(n_warps));
+        }
+    }
+}
+
 // Generic pattern: any T (multiple of 8), 1 <= K <= 64, arbitrary non-negative weights.
 // d += (w*e)*e exactly as the reference writes it (src/descriptor.cpp:70-71).
 template <bool kU8>
@@ -462,6 +680,21 @@ int grid_for(const clatch_ctx* ctx, size_t M, int ctas_per_sm) {
     return static_cast<int>(M < cap ? M : cap);
 }
 
+// The single-window kernel's placement (16 triplets per half-warp, one million annealing steps)
+// is only needed when extract_variant 0 is selected: plan it on first use.
+int ensure_single_window_plan(clatch_ctx* ctx) {
+    Pattern& pat = ctx->pattern;
+    if (pat.slots_planned) return CLATCH_OK;
+    const SlotPlan plan = plan_slots(pat.host_triplets.data(), pat.T, kWinStride, 1000000);
+    pat.slot_degree = plan.avg_degree;
+    pat.slot_degree_identity = plan.avg_degree_identity;
+    static_assert(sizeof(SlotEntry) == sizeof(ushort4), "slot layout");
+    if (int rc = pat.slots.reserve(sizeof(SlotEntry) * pat.T)) return rc;
+    CLATCH_CUDA(cudaMemcpy(pat.slots.ptr, plan.slots.data(), sizeof(SlotEntry) * pat.T, cudaMemcpyHostToDevice));
+    pat.slots_planned = true;
+    return CLATCH_OK;
+}
+
 template <bool kU8>
 int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, size_t pitch,
                    const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream,
@@ -481,7 +714,18 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     p.K = pat.K;
     p.flags = flags;
     p.run_if_flag = run_if_flag;
-    if (pat.fast && ctx->extract_variant == 1) {
+    p.stats = ctx->extract_stats_on ? ctx->extract_stats.as<unsigned long long>() : nullptr;
+    if (kU8 && pat.fast && ctx->extract_variant == 2) {
+        if (!ctx->filt_configured) {   // per-device function attribute
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_filt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kFiltSmemBytes));
+            ctx->filt_configured = true;
+        }
+        p.slots = pat.slots_f8.as<ushort4>();
+        const size_t quads = (M + kQuad - 1) / kQuad;
+        const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
+        extract_filt_kernel<<<grid, kQuadThreads, kFiltSmemBytes, stream>>>(p);
+    } else if (pat.fast && ctx->extract_variant >= 1) {
         if (!ctx->quad_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_quad_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kQuadSmemBytes));
@@ -494,6 +738,8 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
         extract_quad_kernel<kU8><<<grid, kQuadThreads, kQuadSmemBytes, stream>>>(p);
     } else if (pat.fast) {
+        if (int rc = ensure_single_window_plan(ctx)) return rc;
+        p.slots = pat.slots.as<ushort4>();
         extract_fast_kernel<kU8><<<grid_for(ctx, M, 4), kThreads, 0, stream>>>(p);
     } else {
         extract_generic_kernel<kU8><<<grid_for(ctx, M, 2), kThreads, pat.T, stream>>>(p);

@@ -56,11 +56,15 @@ struct Pattern {
     // from window offsets (row*kWinStride+col) a/b/c; packed as ushort4 {a, b, c, bit}.
     DeviceBuffer slots;            // T * ushort4 (single-window kernel: half-warps of 16 triplets)
     DeviceBuffer slots_quad;       // T * ushort4 (quad kernel: half-warps of 4 triplets x 4 keypoints)
+    DeviceBuffer slots_f8;         // T * ushort4 (filtered kernel: warps of 8 triplets x 4 keypoints)
+    std::vector<int16_t> host_triplets;   // T * 6, for plans made on first use
+    bool slots_planned = false;    // `slots` holds a plan for the current table
     DeviceBuffer triplets;         // generic kernel: T * 6 int16
     std::vector<double> weights;   // K*K
     double slot_degree = 0.0;           // planned / table-order shared-load conflict degree
     double slot_degree_identity = 0.0;
     double slot_degree_quad = 0.0;
+    double slot_degree_f8 = 0.0;
 };
 
 } // namespace clatch
@@ -73,8 +77,12 @@ struct clatch_ctx {
     cudaStream_t stream = nullptr;
     clatch::Pattern pattern;
     uint64_t launches = 0;
-    bool tc_configured = false, quad_configured = false;   // opt-in smem sizes set on this device
-    int extract_variant = 1;       // 0: one window per CTA (4 CTAs/SM), 1: quad kernel (4 windows per CTA)
+    bool tc_configured = false, quad_configured = false, filt_configured = false;   // opt-in smem sizes set on this device
+    // 0: one window per CTA (4 CTAs/SM); 1: quad kernel (4 fp64 windows per CTA); 2: filtered kernel
+    // (4 split windows per CTA, fp32 estimate + exact recompute; u8 images — others run variant 1)
+    int extract_variant = 2;
+    bool extract_stats_on = false;           // count exact recomputes (clatch_extract_stats)
+    clatch::DeviceBuffer extract_stats;      // 2 x u64
     int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
     // scratch for the host-buffer entry points
     clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t, items, scores, counts, det;

@@ -151,15 +151,21 @@ inline SlotPlan plan_slots(const int16_t* triplets, int T, int stride, int itera
     return plan;
 }
 
-// ---- "quad" placement -------------------------------------------------------------------
-// The quad kernel keeps FOUR keypoints' windows in shared memory, window w displaced by
-// 4*w bank pairs, and fills each half-warp with 4 triplets x 4 keypoints (lane = 4*i + w).
-// The four lanes of one triplet then sit on residues x, x+4, x+8, x+12, so a half-warp is
-// conflict-free as soon as its 4 triplets have distinct residues MOD 4 in each of the three
-// loads — a far weaker condition than 16 distinct residues mod 16, and one that almost every
-// group can meet (only the mod-4 histogram imbalance of the table remains).
-inline SlotPlan plan_slots_quad(const int16_t* triplets, int T, int stride, int iterations = 300000) {
-    const int G = T / 4;
+// ---- grouped placement ("quad" and "filtered" kernels) ---------------------------------------
+// The multi-window kernels keep FOUR keypoints' windows in shared memory and fill each
+// conflict domain with `group` triplets x 4 keypoints, window w displaced by `mod`*w banks:
+//   quad kernel      64-bit loads, domain = half-warp = 16 bank pairs: group 4, mod 4
+//                    (lane = 4*i + w; window w displaced by 4*w bank pairs)
+//   filtered kernel  32-bit loads, domain = warp = 32 banks:           group 8, mod 8
+//                    (lane = 4*i + w; window w displaced by 8*w banks)
+// The lanes of one triplet then sit on residues x, x+mod, x+2*mod, x+3*mod, so a domain is
+// conflict-free as soon as its `group` triplets have distinct residues MOD `mod` in each of
+// the three loads — far weaker than distinct residues across the whole domain. What remains
+// is the histogram imbalance of the table (a residue class holding more than T/mod anchors
+// forces a collision somewhere): degree 1.07 for (4,4), 1.14 for (8,8) on the built-in table.
+inline SlotPlan plan_slots_grouped(const int16_t* triplets, int T, int stride, int group, int mod,
+                                   int iterations) {
+    const int G = T / group;
     std::vector<uint16_t> off(3 * T);
     for (int t = 0; t < T; ++t)
         for (int k = 0; k < 3; ++k)
@@ -169,16 +175,16 @@ inline SlotPlan plan_slots_quad(const int16_t* triplets, int T, int stride, int 
     for (int t = 0; t < T; ++t) order[t] = t;
     auto res = [&](int t, int k) {
         const int kk = (k == 0 || !flip[t]) ? k : 3 - k;
-        return off[3 * t + kk] & 3;
+        return off[3 * t + kk] % mod;
     };
     // cost of a group: per load, 16 * (worst multiplicity) + colliding lanes
     auto gcost = [&](int g, int* degree_sum) {
         int cost = 0;
         for (int k = 0; k < 3; ++k) {
-            int h[4] = {0, 0, 0, 0};
-            for (int l = 0; l < 4; ++l) ++h[res(order[4 * g + l], k)];
+            int h[16] = {0};
+            for (int l = 0; l < group; ++l) ++h[res(order[group * g + l], k)];
             int mx = 0, excess = 0;
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < mod; ++r) {
                 mx = std::max(mx, h[r]);
                 excess += h[r] > 1 ? h[r] - 1 : 0;
             }
@@ -212,7 +218,7 @@ inline SlotPlan plan_slots_quad(const int16_t* triplets, int T, int stride, int 
             return u < std::exp(-delta / temp);
         };
         if ((r & 7) == 0) {
-            const int p = static_cast<int>((r >> 8) % T), g = p / 4, t = order[p];
+            const int p = static_cast<int>((r >> 8) % T), g = p / group, t = order[p];
             flip[t] ^= 1;
             const int nc = gcost(g, nullptr);
             if (accept(nc - cost[g])) cost[g] = nc;
@@ -220,7 +226,7 @@ inline SlotPlan plan_slots_quad(const int16_t* triplets, int T, int stride, int 
             continue;
         }
         const int p = static_cast<int>((r >> 8) % T), q = static_cast<int>((r >> 32) % T);
-        const int g1 = p / 4, g2 = q / 4;
+        const int g1 = p / group, g2 = q / group;
         if (g1 == g2) continue;
         std::swap(order[p], order[q]);
         const int n1 = gcost(g1, nullptr), n2 = gcost(g2, nullptr);
@@ -243,6 +249,20 @@ inline SlotPlan plan_slots_quad(const int16_t* triplets, int T, int stride, int 
         plan.slots[s] = e;
     }
     return plan;
+}
+
+inline SlotPlan plan_slots_quad(const int16_t* triplets, int T, int stride, int iterations = 300000) {
+    return plan_slots_grouped(triplets, T, stride, 4, 4, iterations);
+}
+
+// FNV-1a over the triplet table: identifies the built-in pattern, whose (8,8) plan ships
+// precomputed (default_plan_f8.inc, made by tools/gen_default_plan.cpp with a long anneal).
+inline uint64_t triplet_hash(const int16_t* triplets, int T) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (int i = 0; i < 6 * T; ++i) {
+        h = (h ^ static_cast<uint16_t>(triplets[i])) * 0x100000001b3ull;
+    }
+    return h;
 }
 
 } // namespace clatch

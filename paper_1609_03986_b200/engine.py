@@ -102,6 +102,13 @@ class Engine:
     def synchronize(self):
         _lib.check(self.lib.clatch_synchronize(self.ctx))
 
+    def extract_stats(self) -> tuple[int, int]:
+        """(triplets recomputed exactly, warp passes through the exact path) of the filtered
+        extraction kernel since set_option("extract_stats", 1)."""
+        a, b = C.c_uint64(), C.c_uint64()
+        _lib.check(self.lib.clatch_extract_stats(self.ctx, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
     # ---- host-side preparation ----------------------------------------------
     def prepare_keypoints(self, keypoints: np.ndarray, width: int, height: int, workers: int = 0):
         """-> (xycs float64 (M,4) = x, y, cos, sin; kept int64 (M,) input indices)."""

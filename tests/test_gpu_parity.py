@@ -397,10 +397,11 @@ def test_every_matcher_variant_is_exact(lk, port, variant):
         eng.set_option("match_variant", 3)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 def test_every_extraction_variant_is_exact(lk, port, variant):
-    """Both specialised extraction kernels (one window per CTA / four windows per CTA) must be
-    bit-identical to the oracle, including keypoint counts that do not fill a quad."""
+    """All specialised extraction kernels (one window per CTA / four fp64 windows per CTA / four
+    split windows with the fp32 filter) must be bit-identical to the oracle, including keypoint
+    counts that do not fill a quad."""
     eng = lk.get_engine()
     eng.set_option("extract_variant", variant)
     try:
@@ -414,7 +415,70 @@ def test_every_extraction_variant_is_exact(lk, port, variant):
         kps = port.random_keypoints(2050, 400, 300, 203)
         assert np.array_equal(lk.describe(fimg, kps)[1], port.describe_all(fimg, kps)[1])
     finally:
-        eng.set_option("extract_variant", 1)
+        eng.set_option("extract_variant", 2)
+
+
+def _near_tie_images(w, h):
+    """u8 images built to put d1 - d2 at or next to zero: the inputs on which an fp32 estimate
+    of the SSD pair must NOT be trusted (exact ties, rounding-level differences, tiny sums)."""
+    rng = np.random.default_rng(1609)
+    yy, xx = np.mgrid[0:h, 0:w]
+    out = {
+        "flat": np.full((h, w), 200, np.uint8),
+        "black": np.zeros((h, w), np.uint8),
+        "white": np.full((h, w), 255, np.uint8),
+        "lsb_noise": (128 + rng.integers(0, 2, (h, w))).astype(np.uint8),
+        "pm1_noise": (17 + rng.integers(-1, 2, (h, w))).astype(np.uint8),
+        "ramp_x": (xx % 256).astype(np.uint8),
+        "ramp_diag": ((xx + 2 * yy) // 3 % 256).astype(np.uint8),
+        "checker8": (((xx // 8 + yy // 8) % 2) * 255).astype(np.uint8),
+        "stripes4": (((xx // 4) % 2) * 90 + 40).astype(np.uint8),
+        "half_flat": np.where(xx < w // 2, 255, rng.integers(0, 256, (h, w))).astype(np.uint8),
+        "blocks": (rng.integers(0, 4, (h // 16 + 1, w // 16 + 1)) * 85).astype(np.uint8)
+                  .repeat(16, 0).repeat(16, 1)[:h, :w],
+        "sparse_dots": np.where(rng.random((h, w)) < 0.01, 255, 0).astype(np.uint8),
+    }
+    return out
+
+
+def test_filtered_kernel_on_near_ties(lk, port):
+    """The filtered kernel decides a bit from fp32 sums only when a rigorous error bound
+    separates them; everything else is recomputed in exact fp64. Flat regions, periodic
+    patterns and one-grey-level noise make ties and rounding-level differences the common case:
+    descriptors must still be the oracle's, for axis-aligned and arbitrary angles."""
+    eng = lk.get_engine()
+    eng.set_option("extract_variant", 2)
+    w, h = 320, 240
+    kps = port.random_keypoints(77, w, h, 150)
+    kps[::3, 2] = 0.0                            # upright windows: samples land on pixel centres +- 0.5
+    kps[1::7, 2] = np.pi / 2
+    kps[::5, :2] = np.floor(kps[::5, :2]) + 0.5  # half-integer centres: samples exactly on pixels
+    for name, img in _near_tie_images(w, h).items():
+        want = port.describe_all(img.astype(np.float64), kps)[1]
+        got = lk.describe(img, kps)[1]
+        assert np.array_equal(got, want), name
+        assert np.array_equal(lk.describe(img.astype(np.float64), kps)[1], want), (name, "f64")
+
+
+def test_filtered_kernel_exact_pass_rate(lk, port):
+    """Diagnostics counters: on noise the exact pass is rare (that is where the speed comes
+    from), on a flat image every triplet takes it (that is where the exactness comes from)."""
+    eng = lk.get_engine()
+    eng.set_option("extract_variant", 2)
+    w, h, n = 640, 480, 2000
+    kps = port.random_keypoints(1610, w, h, n)
+    try:
+        eng.set_option("extract_stats", 1)
+        noise = port.random_image_u8(1609, w, h)
+        m = len(lk.describe(noise, kps)[1])
+        exact, _ = eng.extract_stats()
+        assert exact < 1e-3 * m * 512, exact
+        eng.set_option("extract_stats", 1)       # re-arm: zeroes the counters
+        lk.describe(np.full((h, w), 31, np.uint8), kps)
+        exact, warps = eng.extract_stats()
+        assert exact == m * 512 and warps > 0
+    finally:
+        eng.set_option("extract_stats", 0)
 
 
 # ------------------------------------------------------ resident sets, batched pairs ----
