@@ -438,21 +438,26 @@ __device__ __forceinline__ void ssd_estimate_2(const float* win, const ushort4 s
     const float* pa1 = win + s1.x;
     const float* pb1 = win + s1.y;
     const float* pc1 = win + s1.z;
-    d1a = d2a = d1b = d2b = 0.0f;
+    // Packed fp32x2 arithmetic (sm_100 FFMA2): component 0 = slot 0, component 1 = slot 1.
+    // a - b is fma(b, -1, a): one rounding, the same value as a subtraction.
+    const float2 neg1 = make_float2(-1.0f, -1.0f);
+    float2 d1 = make_float2(0.0f, 0.0f), d2 = d1;
 #pragma unroll
     for (int r = 0; r < 7; ++r) {
 #pragma unroll
         for (int c = 0; c < 7; ++c) {
             const int o = r * kWinStride + c;
-            const float a0 = pa0[o], a1 = pa1[o];
-            const float e10 = a0 - pb0[o], e20 = a0 - pc0[o];
-            const float e11 = a1 - pb1[o], e21 = a1 - pc1[o];
-            d1a = __fmaf_rn(e10, e10, d1a);
-            d2a = __fmaf_rn(e20, e20, d2a);
-            d1b = __fmaf_rn(e11, e11, d1b);
-            d2b = __fmaf_rn(e21, e21, d2b);
+            const float2 a = make_float2(pa0[o], pa1[o]);
+            const float2 e1 = __ffma2_rn(make_float2(pb0[o], pb1[o]), neg1, a);
+            const float2 e2 = __ffma2_rn(make_float2(pc0[o], pc1[o]), neg1, a);
+            d1 = __ffma2_rn(e1, e1, d1);
+            d2 = __ffma2_rn(e2, e2, d2);
         }
     }
+    d1a = d1.x;
+    d1b = d1.y;
+    d2a = d2.x;
+    d2b = d2.y;
 }
 
 // True when sign(d1 - d2) of the fp32 estimate is provably the reference's (bound above).
