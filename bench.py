@@ -339,8 +339,9 @@ def run_ours(args):
     sms = eng.sm_count
     pipes = peaks.get("pipes", {})
     mv = args.match_variant if args.match_variant is not None else 3
-    ev = args.extract_variant if args.extract_variant is not None else 2
-    ext_name = {0: "extract_fast_kernel<u8>", 1: "extract_quad_kernel<u8>", 2: "extract_filt_kernel"}[ev]
+    ev = args.extract_variant if args.extract_variant is not None else 3
+    ext_name = {0: "extract_fast_kernel<u8>", 1: "extract_quad_kernel<u8>", 2: "extract_filt_kernel",
+                3: "extract_pipe_kernel"}[ev]
     mat_name = "match_tc_kernel (tcgen05 kind::i8)" if mv == 3 else f"match64_kernel<{mv}>"
     kernels, pipe_roofline = {}, {}
     if ext_s > 0:
@@ -441,7 +442,7 @@ def main():
     ap.add_argument("--phase", choices=["both", "extract", "match"], default="both")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--match-variant", type=int, default=None, help="override the matcher kernel variant (0..3)")
-    ap.add_argument("--extract-variant", type=int, default=None, help="override the extraction kernel variant (0..2)")
+    ap.add_argument("--extract-variant", type=int, default=None, help="override the extraction kernel variant (0..3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

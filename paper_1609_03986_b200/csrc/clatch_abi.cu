@@ -219,6 +219,10 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
                             &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->items, &ctx->scores, &ctx->counts, &ctx->det, &ctx->pattern.slots, &ctx->pattern.slots_quad,
                             &ctx->pattern.slots_f8, &ctx->extract_stats, &ctx->pattern.triplets})
         b->release();
+    for (auto& t : ctx->tex_images) {
+        if (t.tex) cudaDestroyTextureObject(t.tex);
+        if (t.array) cudaFreeArray(t.array);
+    }
     ctx->pinned.release();
     ctx->pin_xycs.release();
     ctx->pin_desc.release();
@@ -257,7 +261,7 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         return CLATCH_OK;
     }
     if (std::strcmp(key, "extract_variant") == 0) {
-        if (value < 0 || value > 2) return invalid("extract_variant must be 0..2");
+        if (value < 0 || value > 3) return invalid("extract_variant must be 0..3");
         ctx->extract_variant = value;
         return CLATCH_OK;
     }

@@ -46,6 +46,7 @@ struct ExtractParams {
     const int* flags;          // optional device flags (f64 promotion), may be null
     int run_if_flag;           // run only when flags[0] == run_if_flag (if flags != null)
     unsigned long long* stats; // optional {triplets recomputed exactly, warps that took the exact pass}
+    cudaTextureObject_t tex;   // pipelined kernel: the u8 image as a gather-enabled CUDA array
 };
 
 // Exact u8 -> f64 without the 16-lane/clk conversion pipe (I2F.F64 runs at 16/clk/SM on
@@ -470,12 +471,14 @@ __device__ __forceinline__ bool estimate_decides(float d1, float d2, float& diff
     return fabsf(diff) > bound;
 }
 
-__device__ __forceinline__ double plane_value(const float* p) {
+__device__ __forceinline__ double plane_value_at(const float* p, int lo_off) {
     const unsigned f = __float_as_uint(p[0]);
-    const int lo = __float_as_int(p[kLoPlane]);
+    const int lo = __float_as_int(p[lo_off]);
     const unsigned hi = f ? (f >> 3) + 0x38000000u : 0u;
     return __hiloint2double(static_cast<int>(hi), lo);
 }
+
+__device__ __forceinline__ double plane_value(const float* p) { return plane_value_at(p, kLoPlane); }
 
 // The exact chains (same arithmetic and order as triplet_bit_7x7) from the split planes.
 __device__ __noinline__ bool triplet_bit_7x7_planes(const float* win, int oa, int ob, int oc, bool swapped) {
@@ -599,6 +602,217 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_filt_kernel(ExtractPa
     }
 }
 
+// ---- pipelined kernel: resampling and SSD run side by side ----------------------------------
+// The filtered kernel alternates two phases that starve each other's pipes: resampling is
+// fp64-bound (LSU half idle), the SSD estimate is LSU-bound (fp64 idle). Here the CTA is split
+// into 16 producer warps and 16 consumer warps (four of each per SM sub-partition):
+//   producers  resample quad q+1 into F planes [next] — footprints come from the texture unit
+//              (tex2Dgather on a u8 CUDA array: the four texels of the bilinear footprint in
+//              one instruction, no tile staging, no LSU traffic), then pack quad q-1's bits;
+//   consumers  run the fp32 estimate of quad q on F planes [cur].
+// One __syncthreads per quad flips the buffers. Eight F planes and four LO planes fit in shared
+// memory (200 KB) because LO planes are no longer written up front: when some lane cannot
+// decide a bit, the consumers re-resample just that window's LO plane (same exact arithmetic,
+// same texels), meet on a consumer-only barrier, and the undecided lanes run the exact chains
+// as in the filtered kernel. On textured images that happens for ~1 % of the windows.
+constexpr int kPipeRole = 512;                                       // threads per role
+constexpr int kPipePlanes = 12;                                      // F[2][4] + LO[4]
+constexpr int kPipeSmemBytes = kPipePlanes * kPlanePitch * 4 + 2 * kQuad * kFastT + kQuad * 2 * kWindow * 8 + 64 + 128;
+
+__device__ __forceinline__ void role_barrier(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kPipeRole) : "memory");
+}
+
+// The 2x2 footprint whose top-left texel is (x0, y0): gather at the footprint's centre, half a
+// texel away from every selection boundary (tools/tex_probe.cu checks the component order).
+__device__ __forceinline__ uchar4 footprint(cudaTextureObject_t tex, int x0, int y0) {
+    // (2^23 + x0) - (2^23 - 1) = x0 + 1 exactly, without an integer->float conversion
+    const float fx = __uint_as_float(0x4B000000u | static_cast<unsigned>(x0)) - 8388607.0f;
+    const float fy = __uint_as_float(0x4B000000u | static_cast<unsigned>(y0)) - 8388607.0f;
+    return tex2Dgather<uchar4>(tex, fx, fy, 0);
+}
+
+// One window sample, exactly as extract_window / sample_bilinear compute it.
+__device__ __forceinline__ double sample_exact(cudaTextureObject_t tex, double xa, double ya, double sdv,
+                                               double cdv) {
+    const double sx = __dsub_rn(xa, sdv);
+    const double sy = __dadd_rn(ya, cdv);
+    int x0, y0;
+    double x0f, y0f;
+    floor_exact(sx, x0, x0f);
+    floor_exact(sy, y0, y0f);
+    const double fx = __dsub_rn(sx, x0f);
+    const double fy = __dsub_rn(sy, y0f);
+    const uchar4 g = footprint(tex, x0, y0);   // w = (x0,y0), z = (x0+1,y0), x = (x0,y0+1), y = (x0+1,y0+1)
+    return blend(fx, fy, u8_to_f64(g.w), u8_to_f64(g.z), u8_to_f64(g.x), u8_to_f64(g.y));
+}
+
+__device__ __noinline__ bool triplet_bit_7x7_planes_at(const float* win, int lo_off, int oa, int ob, int oc,
+                                                       bool swapped) {
+    const float* pa = win + oa;
+    const float* pb = win + ob;
+    const float* pc = win + oc;
+    double d1 = 0.0, d2 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+#pragma unroll
+        for (int c = 0; c < 7; ++c) {
+            const int o = r * kWinStride + c;
+            const double a = plane_value_at(pa + o, lo_off);
+            const double e1 = __dsub_rn(a, plane_value_at(pb + o, lo_off));
+            const double e2 = __dsub_rn(a, plane_value_at(pc + o, lo_off));
+            d1 = __dadd_rn(d1, __dmul_rn(e1, e1));
+            d2 = __dadd_rn(d2, __dmul_rn(e2, e2));
+        }
+    }
+    return swapped ? d2 > d1 : d1 > d2;
+}
+
+__global__ void __launch_bounds__(kQuadThreads, 1) extract_pipe_kernel(ExtractParams p) {
+    if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
+
+    extern __shared__ __align__(16) uint8_t s_quad[];
+    float* const s_f = reinterpret_cast<float*>(s_quad);                       // F[2][4], then LO[4]
+    uint8_t* const s_bits = s_quad + kPipePlanes * kPlanePitch * 4;            // [2][4][512]
+    double* const s_tab = reinterpret_cast<double*>(s_bits + 2 * kQuad * kFastT);   // [4][2][64]
+    int* const s_mask = reinterpret_cast<int*>(s_tab + kQuad * 2 * kWindow);   // [2] windows needing LO
+    double* const s_kp = reinterpret_cast<double*>(s_mask + 16);               // [4][x, y, cos, sin] of the next quad
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool producer = (warp >> 2) & 1;                   // 4 producer + 4 consumer warps per sub-partition
+    const int rw = ((warp >> 3) << 2) | (warp & 3);          // role-local warp 0..15
+    const int rt = rw * 32 + lane;                           // role-local thread 0..511
+    const int u = rt & 63, v0 = rt >> 6;                     // resampling: column u, rows v0 + 8k
+    const double du = static_cast<double>(u) - 31.5;
+    const int kb = lane & 3, ti = lane >> 2;                 // SSD: 8 triplets x 4 keypoints per warp
+    const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
+    const long long nq = blockIdx.x < quads ? static_cast<long long>((quads - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+    ushort4 slot[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) slot[j] = __ldg(p.slots + 8 * (rw + 16 * j) + ti);
+    unsigned n_flagged = 0, n_windows = 0;
+    if (tid == 0) s_mask[0] = s_mask[1] = 0;
+
+    for (long long it = -1; it <= nq; ++it) {
+        const int cur = static_cast<int>(it & 1), nxt = cur ^ 1;
+        if (producer) {
+            if (it >= 1) {   // pack the bits of the quad consumed in the previous iteration
+                const unsigned long long kp = (blockIdx.x + (it - 1) * gridDim.x) * kQuad + (rt >> 7);
+                const uint8_t* bits = s_bits + (nxt * kQuad + (rt >> 7)) * kFastT;
+                const int j = rt & 127;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const unsigned w32 = __ballot_sync(0xffffffffu, bits[128 * k + j] != 0);
+                    if (lane == 0 && kp < p.M)
+                        reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8))[4 * k + (j >> 5)] = w32;
+                }
+            }
+            if (it + 1 < nq) {   // resample the next quad into F[nxt]
+                const unsigned long long kp0 = (blockIdx.x + (it + 1) * gridDim.x) * kQuad;
+                {   // keypoint records and the per-row products of extract_window (src/descriptor.cpp:44-45)
+                    // for all four windows; a keypoint past the end repeats the last one (result unused)
+                    const int w = rt >> 7, e = rt & 127;
+                    const unsigned long long kp = min(kp0 + w, p.M - 1);
+                    const double dv = static_cast<double>(e & 63) - 31.5;
+                    s_tab[w * 2 * kWindow + e] = __dmul_rn(__ldg(p.xycs + 4 * kp + ((e >> 6) ? 2 : 3)), dv);
+                    if (e < 4) s_kp[4 * w + e] = __ldg(p.xycs + 4 * kp + e);
+                }
+                role_barrier(1);
+                // Software pipeline over this thread's 32 samples (4 windows x 8 rows): the gather of
+                // sample i + kDepth is in flight while sample i is blended, so the texture latency
+                // hides behind this warp's own fp64 work instead of stalling it.
+                constexpr int kDepth = 4, kPer = kWindow / (kPipeRole / 64), kTotal = kQuad * kPer;
+                double pfx[kDepth], pfy[kDepth], xa = 0.0, ya = 0.0;
+                uchar4 pg[kDepth];
+                float* const fbase = s_f + nxt * kQuad * kPlanePitch + v0 * kWinStride + u;
+#pragma unroll
+                for (int i = 0; i < kTotal + kDepth; ++i) {
+                    if (i >= kDepth) {
+                        const int j = i - kDepth, sl = j % kDepth;
+                        const uchar4 g = pg[sl];   // w = (x0,y0), z = (x0+1,y0), x = (x0,y0+1), y = (x0+1,y0+1)
+                        const double val = blend(pfx[sl], pfy[sl], u8_to_f64(g.w), u8_to_f64(g.z), u8_to_f64(g.x),
+                                                 u8_to_f64(g.y));
+                        fbase[(j / kPer) * kPlanePitch + (j % kPer) * (kPipeRole / 64) * kWinStride] =
+                            __double2float_rz(val);
+                    }
+                    if (i < kTotal) {
+                        const int w = i / kPer, sl = i % kDepth;
+                        if (i % kPer == 0) {
+                            const double c = s_kp[4 * w + 2], sn = s_kp[4 * w + 3];
+                            xa = __dadd_rn(s_kp[4 * w + 0], __dmul_rn(c, du));
+                            ya = __dadd_rn(s_kp[4 * w + 1], __dmul_rn(sn, du));
+                        }
+                        const int v = v0 + (i % kPer) * (kPipeRole / 64);
+                        const double sx = __dsub_rn(xa, s_tab[w * 2 * kWindow + v]);
+                        const double sy = __dadd_rn(ya, s_tab[w * 2 * kWindow + kWindow + v]);
+                        int x0, y0;
+                        double x0f, y0f;
+                        floor_exact(sx, x0, x0f);
+                        floor_exact(sy, y0, y0f);
+                        pfx[sl] = __dsub_rn(sx, x0f);
+                        pfy[sl] = __dsub_rn(sy, y0f);
+                        pg[sl] = footprint(p.tex, x0, y0);
+                    }
+                }
+            }
+        } else if (it >= 0 && it < nq) {
+            const unsigned long long kp0 = (blockIdx.x + it * gridDim.x) * kQuad;
+            const float* const my_win = s_f + (cur * kQuad + kb) * kPlanePitch;
+            const int lo_off = (2 - cur) * kQuad * kPlanePitch;          // F[cur][kb] -> LO[kb]
+            const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves a stale window
+            if (rt == 0) s_mask[nxt] = 0;
+            float d1[4], d2[4], diff[4];
+            ssd_estimate_2(my_win, slot[0], slot[1], d1[0], d2[0], d1[1], d2[1]);
+            ssd_estimate_2(my_win, slot[2], slot[3], d1[2], d2[2], d1[3], d2[3]);
+            unsigned need = 0;
+            bool bit[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const bool sure = estimate_decides(d1[j], d2[j], diff[j]);
+                bit[j] = (slot[j].w >> 15) ? diff[j] < 0.0f : diff[j] > 0.0f;
+                need |= (live && !sure) ? 1u << j : 0u;
+            }
+            if (need) atomicOr(s_mask + cur, 1 << kb);
+            role_barrier(2);
+            const int mask = *reinterpret_cast<volatile int*>(s_mask + cur);
+            if (mask) {   // uniform over the consumers: some window needs its LO plane
+                for (int w = 0; w < kQuad; ++w) {
+                    if (!((mask >> w) & 1)) continue;
+                    const double* kpr = p.xycs + 4 * (kp0 + w);
+                    const double c = __ldg(kpr + 2), s = __ldg(kpr + 3);
+                    const double xa = __dadd_rn(__ldg(kpr + 0), __dmul_rn(c, du));
+                    const double ya = __dadd_rn(__ldg(kpr + 1), __dmul_rn(s, du));
+                    int* lopl = reinterpret_cast<int*>(s_f) + (2 * kQuad + w) * kPlanePitch + u;
+#pragma unroll 2
+                    for (int v = v0; v < kWindow; v += kPipeRole / 64) {
+                        const double dv = static_cast<double>(v) - 31.5;
+                        lopl[v * kWinStride] = __double2loint(sample_exact(p.tex, xa, ya, __dmul_rn(s, dv), __dmul_rn(c, dv)));
+                    }
+                    n_windows += rt == 0;
+                }
+                role_barrier(2);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if ((need >> j) & 1) {
+                        bit[j] = triplet_bit_7x7_planes_at(my_win, lo_off, slot[j].x, slot[j].y, slot[j].z, slot[j].w >> 15);
+                        ++n_flagged;
+                    }
+            }
+            uint8_t* const my_bits = s_bits + (cur * kQuad + kb) * kFastT;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) my_bits[slot[j].w & 0x7fff] = bit[j];
+        }
+        __syncthreads();
+    }
+    if (p.stats != nullptr) {   // exact-pass counters (diagnostics; off unless asked for)
+        n_flagged = __reduce_add_sync(0xffffffffu, n_flagged);
+        if (lane == 0 && (n_flagged | n_windows)) {
+            atomicAdd(p.stats + 0, static_cast<unsigned long long>(n_flagged));
+            atomicAdd(p.stats + 1, static_cast<unsigned long long>(n_windows));
+        }
+    }
+}
+
 // Generic pattern: any T (multiple of 8), 1 <= K <= 64, arbitrary non-negative weights.
 // d += (w*e)*e exactly as the reference writes it (src/descriptor.cpp:70-71).
 template <bool kU8>
@@ -685,6 +899,44 @@ int grid_for(const clatch_ctx* ctx, size_t M, int ctas_per_sm) {
     return static_cast<int>(M < cap ? M : cap);
 }
 
+// One gather-enabled u8 CUDA array + texture object per stream that launches the pipelined
+// kernel, re-created when the image size changes.
+int tex_image_for(clatch_ctx* ctx, cudaStream_t stream, int width, int height, clatch_ctx::TexImage** out) {
+    clatch_ctx::TexImage* ti = nullptr;
+    for (auto& t : ctx->tex_images)
+        if (t.stream == stream) ti = &t;
+    if (!ti) {
+        ctx->tex_images.push_back({});
+        ti = &ctx->tex_images.back();
+        ti->stream = stream;
+    }
+    if (ti->width != width || ti->height != height) {
+        if (ti->tex) {
+            CLATCH_CUDA(cudaStreamSynchronize(stream));   // a kernel may still be sampling the old array
+            cudaDestroyTextureObject(ti->tex);
+            cudaFreeArray(ti->array);
+            ti->tex = 0;
+            ti->array = nullptr;
+            ti->width = ti->height = 0;
+        }
+        const cudaChannelFormatDesc fmt = cudaCreateChannelDesc<unsigned char>();
+        CLATCH_CUDA(cudaMallocArray(&ti->array, &fmt, width, height, cudaArrayTextureGather));
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = ti->array;
+        cudaTextureDesc td{};
+        td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModePoint;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        CLATCH_CUDA(cudaCreateTextureObject(&ti->tex, &rd, &td, nullptr));
+        ti->width = width;
+        ti->height = height;
+    }
+    *out = ti;
+    return CLATCH_OK;
+}
+
 // The single-window kernel's placement (16 triplets per half-warp, one million annealing steps)
 // is only needed when extract_variant 0 is selected: plan it on first use.
 int ensure_single_window_plan(clatch_ctx* ctx) {
@@ -720,7 +972,24 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     p.flags = flags;
     p.run_if_flag = run_if_flag;
     p.stats = ctx->extract_stats_on ? ctx->extract_stats.as<unsigned long long>() : nullptr;
-    if (kU8 && pat.fast && ctx->extract_variant == 2) {
+    if (kU8 && pat.fast && ctx->extract_variant == 3) {
+        if (!ctx->pipe_configured) {   // per-device function attribute
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kPipeSmemBytes));
+            ctx->pipe_configured = true;
+        }
+        // The resampler reads footprints through the texture unit: copy the image into this
+        // stream's gather-enabled CUDA array (device to device, stream-ordered).
+        clatch_ctx::TexImage* ti = nullptr;
+        if (int rc = tex_image_for(ctx, stream, width, height, &ti)) return rc;
+        CLATCH_CUDA(cudaMemcpy2DToArrayAsync(ti->array, 0, 0, d_img, pitch, width, height, cudaMemcpyDeviceToDevice,
+                                             stream));
+        p.tex = ti->tex;
+        p.slots = pat.slots_f8.as<ushort4>();
+        const size_t quads = (M + kQuad - 1) / kQuad;
+        const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
+        extract_pipe_kernel<<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
+    } else if (kU8 && pat.fast && ctx->extract_variant == 2) {
         if (!ctx->filt_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_filt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kFiltSmemBytes));
@@ -730,7 +999,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         const size_t quads = (M + kQuad - 1) / kQuad;
         const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
         extract_filt_kernel<<<grid, kQuadThreads, kFiltSmemBytes, stream>>>(p);
-    } else if (pat.fast && ctx->extract_variant >= 1) {
+    } else if (pat.fast && ctx->extract_variant >= 1) {   // (variants 2 and 3 are u8-only: other images land here)
         if (!ctx->quad_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_quad_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kQuadSmemBytes));

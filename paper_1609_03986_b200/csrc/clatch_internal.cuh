@@ -77,10 +77,19 @@ struct clatch_ctx {
     cudaStream_t stream = nullptr;
     clatch::Pattern pattern;
     uint64_t launches = 0;
-    bool tc_configured = false, quad_configured = false, filt_configured = false;   // opt-in smem sizes set on this device
+    bool tc_configured = false, quad_configured = false, filt_configured = false, pipe_configured = false;   // opt-in smem sizes set on this device
     // 0: one window per CTA (4 CTAs/SM); 1: quad kernel (4 fp64 windows per CTA); 2: filtered kernel
-    // (4 split windows per CTA, fp32 estimate + exact recompute; u8 images — others run variant 1)
-    int extract_variant = 2;
+    // (4 split windows per CTA, fp32 estimate + exact recompute); 3: pipelined kernel (producer warps
+    // resample through the texture unit while consumer warps run the estimate). 2 and 3 take u8
+    // images — others run variant 1.
+    int extract_variant = 3;
+    struct TexImage {                // pipelined kernel: the image as a gather-enabled CUDA array
+        cudaStream_t stream = nullptr;
+        cudaArray_t array = nullptr;
+        cudaTextureObject_t tex = 0;
+        int width = 0, height = 0;
+    };
+    std::vector<TexImage> tex_images;
     bool extract_stats_on = false;           // count exact recomputes (clatch_extract_stats)
     clatch::DeviceBuffer extract_stats;      // 2 x u64
     int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)

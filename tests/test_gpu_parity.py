@@ -397,11 +397,11 @@ def test_every_matcher_variant_is_exact(lk, port, variant):
         eng.set_option("match_variant", 3)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_every_extraction_variant_is_exact(lk, port, variant):
     """All specialised extraction kernels (one window per CTA / four fp64 windows per CTA / four
-    split windows with the fp32 filter) must be bit-identical to the oracle, including keypoint
-    counts that do not fill a quad."""
+    split windows with the fp32 filter / the producer-consumer pipeline over the texture unit)
+    must be bit-identical to the oracle, including keypoint counts that do not fill a quad."""
     eng = lk.get_engine()
     eng.set_option("extract_variant", variant)
     try:
@@ -415,7 +415,7 @@ def test_every_extraction_variant_is_exact(lk, port, variant):
         kps = port.random_keypoints(2050, 400, 300, 203)
         assert np.array_equal(lk.describe(fimg, kps)[1], port.describe_all(fimg, kps)[1])
     finally:
-        eng.set_option("extract_variant", 2)
+        eng.set_option("extract_variant", 3)
 
 
 def _near_tie_images(w, h):
@@ -441,13 +441,14 @@ def _near_tie_images(w, h):
     return out
 
 
-def test_filtered_kernel_on_near_ties(lk, port):
-    """The filtered kernel decides a bit from fp32 sums only when a rigorous error bound
+@pytest.mark.parametrize("variant", [2, 3])
+def test_filtered_kernel_on_near_ties(lk, port, variant):
+    """The filtered and pipelined kernels decide a bit from fp32 sums only when a rigorous error bound
     separates them; everything else is recomputed in exact fp64. Flat regions, periodic
     patterns and one-grey-level noise make ties and rounding-level differences the common case:
     descriptors must still be the oracle's, for axis-aligned and arbitrary angles."""
     eng = lk.get_engine()
-    eng.set_option("extract_variant", 2)
+    eng.set_option("extract_variant", variant)
     w, h = 320, 240
     kps = port.random_keypoints(77, w, h, 150)
     kps[::3, 2] = 0.0                            # upright windows: samples land on pixel centres +- 0.5
@@ -458,13 +459,15 @@ def test_filtered_kernel_on_near_ties(lk, port):
         got = lk.describe(img, kps)[1]
         assert np.array_equal(got, want), name
         assert np.array_equal(lk.describe(img.astype(np.float64), kps)[1], want), (name, "f64")
+    eng.set_option("extract_variant", 3)
 
 
-def test_filtered_kernel_exact_pass_rate(lk, port):
+@pytest.mark.parametrize("variant", [2, 3])
+def test_filtered_kernel_exact_pass_rate(lk, port, variant):
     """Diagnostics counters: on noise the exact pass is rare (that is where the speed comes
     from), on a flat image every triplet takes it (that is where the exactness comes from)."""
     eng = lk.get_engine()
-    eng.set_option("extract_variant", 2)
+    eng.set_option("extract_variant", variant)
     w, h, n = 640, 480, 2000
     kps = port.random_keypoints(1610, w, h, n)
     try:
@@ -475,10 +478,11 @@ def test_filtered_kernel_exact_pass_rate(lk, port):
         assert exact < 1e-3 * m * 512, exact
         eng.set_option("extract_stats", 1)       # re-arm: zeroes the counters
         lk.describe(np.full((h, w), 31, np.uint8), kps)
-        exact, warps = eng.extract_stats()
-        assert exact == m * 512 and warps > 0
+        exact, passes = eng.extract_stats()      # passes: warps (variant 2) / windows re-resampled (3)
+        assert exact == m * 512 and passes > 0
     finally:
         eng.set_option("extract_stats", 0)
+        eng.set_option("extract_variant", 3)
 
 
 # ------------------------------------------------------ resident sets, batched pairs ----
