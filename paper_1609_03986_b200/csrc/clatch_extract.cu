@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "clatch_internal.cuh"
 #include "slot_assign.hpp"
@@ -604,32 +605,38 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_filt_kernel(ExtractPa
 
 // ---- pipelined kernel: resampling and SSD run side by side ----------------------------------
 // The filtered kernel alternates two phases that starve each other's pipes: resampling is
-// fp64-bound (LSU half idle), the SSD estimate is LSU-bound (fp64 idle). Here the CTA is split
-// into 16 producer warps and 16 consumer warps (four of each per SM sub-partition):
-//   producers  resample quad q+1 into F planes [next] — footprints come from the texture unit
-//              (tex2Dgather on a u8 CUDA array: the four texels of the bilinear footprint in
-//              one instruction, no tile staging, no LSU traffic), then pack quad q-1's bits;
-//   consumers  run the fp32 estimate of quad q on F planes [cur].
-// One __syncthreads per quad flips the buffers. Eight F planes and four LO planes fit in shared
-// memory (200 KB) because LO planes are no longer written up front: when some lane cannot
-// decide a bit, the consumers re-resample just that window's LO plane (same exact arithmetic,
-// same texels), meet on a consumer-only barrier, and the undecided lanes run the exact chains
-// as in the filtered kernel. On textured images that happens for ~1 % of the windows.
-constexpr int kPipeRole = 512;                                       // threads per role
+// fp64-bound (LSU half idle), the SSD estimate is LSU-bound (fp64 idle). Here the F planes are
+// double-buffered and the two phases of consecutive quads overlap: in iteration `it` every
+// thread resamples its 16 samples of quad it+1 into F[next] AND estimates its 2 triplet slots
+// of quad it from F[cur] — half of the warps (two per SM sub-partition and parity) in that
+// order, the other half in the opposite order, so at any moment about half of the SM is on
+// the fp64 pipe and half on the LSU, with equal work per warp by construction and a single
+// __syncthreads per quad. Footprints come from the texture unit (tex2Dgather on a u8 CUDA
+// array: the four texels of a bilinear footprint in one instruction — no tile staging, no LSU
+// traffic), software-pipelined four samples deep so the gather latency hides behind the warp's
+// own fp64 work. Eight F planes and four LO planes fit in shared memory (200 KB) because LO
+// planes are no longer written up front: when some lane could not decide a bit, the whole CTA
+// re-resamples just that window's LO plane after the barrier (same exact arithmetic, same
+// texels) and the undecided lanes run the exact chains as in the filtered kernel. On textured
+// images that happens for ~1 % of the windows.
 constexpr int kPipePlanes = 12;                                      // F[2][4] + LO[4]
-constexpr int kPipeSmemBytes = kPipePlanes * kPlanePitch * 4 + 2 * kQuad * kFastT + kQuad * 2 * kWindow * 8 + 64 + 128;
-
-__device__ __forceinline__ void role_barrier(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kPipeRole) : "memory");
-}
+constexpr int kPipeRows = kQuadThreads / kWindow;                    // 16: thread -> rows v0 + 16k
+constexpr int kPipePer = kWindow / kPipeRows;                        // 4 samples per thread per window
+constexpr int kPipeBits = kFastT + 16;   // predicate bytes per window; +4 banks so the 4 lanes of a triplet differ
+constexpr int kPipeSmemBytes = kPipePlanes * kPlanePitch * 4         // planes
+                               + 2 * kQuad * kPipeBits               // predicate bytes [2][4][512 + pad]
+                               + 2 * kQuad * kWindow * 16            // {s*dv, c*dv} rows [2][4][64]
+                               + 2 * kQuad * 4 * 8                   // keypoint records [2][4][4]
+                               + 64;                                 // undecided-window masks [3]
 
 // The 2x2 footprint whose top-left texel is (x0, y0): gather at the footprint's centre, half a
-// texel away from every selection boundary (tools/tex_probe.cu checks the component order).
-__device__ __forceinline__ uchar4 footprint(cudaTextureObject_t tex, int x0, int y0) {
+// texel away from every selection boundary (tools/tex_probe.cu checks the component order):
+// w = (x0,y0), z = (x0+1,y0), x = (x0,y0+1), y = (x0+1,y0+1).
+__device__ __forceinline__ uint4 footprint(cudaTextureObject_t tex, int x0, int y0) {
     // (2^23 + x0) - (2^23 - 1) = x0 + 1 exactly, without an integer->float conversion
     const float fx = __uint_as_float(0x4B000000u | static_cast<unsigned>(x0)) - 8388607.0f;
     const float fy = __uint_as_float(0x4B000000u | static_cast<unsigned>(y0)) - 8388607.0f;
-    return tex2Dgather<uchar4>(tex, fx, fy, 0);
+    return tex2Dgather<uint4>(tex, fx, fy, 0);   // u8 texels arrive zero-extended: no masking
 }
 
 // One window sample, exactly as extract_window / sample_bilinear compute it.
@@ -643,7 +650,7 @@ __device__ __forceinline__ double sample_exact(cudaTextureObject_t tex, double x
     floor_exact(sy, y0, y0f);
     const double fx = __dsub_rn(sx, x0f);
     const double fy = __dsub_rn(sy, y0f);
-    const uchar4 g = footprint(tex, x0, y0);   // w = (x0,y0), z = (x0+1,y0), x = (x0,y0+1), y = (x0+1,y0+1)
+    const uint4 g = footprint(tex, x0, y0);
     return blend(fx, fy, u8_to_f64(g.w), u8_to_f64(g.z), u8_to_f64(g.x), u8_to_f64(g.y));
 }
 
@@ -668,141 +675,181 @@ __device__ __noinline__ bool triplet_bit_7x7_planes_at(const float* win, int lo_
     return swapped ? d2 > d1 : d1 > d2;
 }
 
+// One quad iteration of one thread, resampling half: its 16 samples of the next quad (4 windows x 4
+// rows) into F[next]. Four gathers stay in flight: the gather of sample i + 4 is issued before sample
+// i is blended, so the texture latency hides behind the warp's own fp64 work.
+// (Interleaving this stream with the estimate's loads and FMAs in one straight-line block was
+// measured slower than phase-staggered warps: an LSU queue stall then also blocks the fp64 chain.)
+struct PipeStep {
+    cudaTextureObject_t tex;
+    const double2* tab;   // {s*dv, c*dv} rows of the next quad, already offset by this thread's v0
+    const double* kpr;    // keypoint records of the next quad
+    float* fbase;         // F[next] + this thread's (v0, u)
+    double du;
+};
+
+__device__ __forceinline__ void resample_step(const PipeStep& st) {
+    constexpr int kDepth = 4, kTotal = kQuad * kPipePer;
+    double pfx[kDepth], pfy[kDepth], xa = 0.0, ya = 0.0;
+    uint4 pg[kDepth];
+#pragma unroll
+    for (int i = 0; i < kTotal + kDepth; ++i) {
+        if (i >= kDepth) {
+            const int j = i - kDepth, sl = j % kDepth;
+            const uint4 g = pg[sl];
+            const double val = blend(pfx[sl], pfy[sl], u8_to_f64(g.w), u8_to_f64(g.z), u8_to_f64(g.x),
+                                     u8_to_f64(g.y));
+            st.fbase[(j / kPipePer) * kPlanePitch + (j % kPipePer) * kPipeRows * kWinStride] = __double2float_rz(val);
+        }
+        if (i < kTotal) {
+            const int w = i / kPipePer, sl = i % kDepth;
+            if (i % kPipePer == 0) {
+                xa = __dadd_rn(st.kpr[4 * w + 0], __dmul_rn(st.kpr[4 * w + 2], st.du));
+                ya = __dadd_rn(st.kpr[4 * w + 1], __dmul_rn(st.kpr[4 * w + 3], st.du));
+            }
+            const double2 row = st.tab[w * kWindow + (i % kPipePer) * kPipeRows];   // {s*dv, c*dv}
+            const double sx = __dsub_rn(xa, row.x);
+            const double sy = __dadd_rn(ya, row.y);
+            int x0, y0;
+            double x0f, y0f;
+            floor_exact(sx, x0, x0f);
+            floor_exact(sy, y0, y0f);
+            pfx[sl] = __dsub_rn(sx, x0f);
+            pfy[sl] = __dsub_rn(sy, y0f);
+            pg[sl] = footprint(st.tex, x0, y0);
+        }
+    }
+}
+
+// Keypoint records and per-row products {s*dv, c*dv} of extract_window (src/descriptor.cpp:44-45)
+// for the four windows of the quad that starts at keypoint kp0, by threads 0..255. A keypoint past
+// the end repeats the last one (its window is computed and never used).
+__device__ __forceinline__ void stage_quad_rows(const ExtractParams& p, unsigned long long kp0, double2* tab,
+                                                double* kpr, int tid) {
+    if (tid < kQuad * kWindow) {
+        const int w = tid >> 6, row = tid & 63;
+        const unsigned long long kp = min(kp0 + w, p.M - 1);
+        const double c = __ldg(p.xycs + 4 * kp + 2), sn = __ldg(p.xycs + 4 * kp + 3);
+        const double dv = static_cast<double>(row) - 31.5;
+        tab[tid] = make_double2(__dmul_rn(sn, dv), __dmul_rn(c, dv));
+        if (row < 4) kpr[4 * w + row] = __ldg(p.xycs + 4 * kp + row);
+    }
+}
+
 __global__ void __launch_bounds__(kQuadThreads, 1) extract_pipe_kernel(ExtractParams p) {
     if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
 
     extern __shared__ __align__(16) uint8_t s_quad[];
-    float* const s_f = reinterpret_cast<float*>(s_quad);                       // F[2][4], then LO[4]
-    uint8_t* const s_bits = s_quad + kPipePlanes * kPlanePitch * 4;            // [2][4][512]
-    double* const s_tab = reinterpret_cast<double*>(s_bits + 2 * kQuad * kFastT);   // [4][2][64]
-    int* const s_mask = reinterpret_cast<int*>(s_tab + kQuad * 2 * kWindow);   // [2] windows needing LO
-    double* const s_kp = reinterpret_cast<double*>(s_mask + 16);               // [4][x, y, cos, sin] of the next quad
+    float* const s_f = reinterpret_cast<float*>(s_quad);                              // F[2][4], then LO[4]
+    uint8_t* const s_bits = s_quad + kPipePlanes * kPlanePitch * 4;                   // [2][4][512]
+    double2* const s_tab = reinterpret_cast<double2*>(s_bits + 2 * kQuad * kPipeBits);   // [2][4][64]
+    double* const s_kp = reinterpret_cast<double*>(s_tab + 2 * kQuad * kWindow);      // [2][4][x, y, cos, sin]
+    int* const s_mask = reinterpret_cast<int*>(s_kp + 2 * kQuad * 4);                 // [3] windows needing LO
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const bool producer = (warp >> 2) & 1;                   // 4 producer + 4 consumer warps per sub-partition
-    const int rw = ((warp >> 3) << 2) | (warp & 3);          // role-local warp 0..15
-    const int rt = rw * 32 + lane;                           // role-local thread 0..511
-    const int u = rt & 63, v0 = rt >> 6;                     // resampling: column u, rows v0 + 8k
+    const bool ssd_first = (warp >> 2) & 1;                  // per sub-partition: 4 warps each way
+    const int u = tid & 63, v0 = tid >> 6;                   // resampling: column u, rows v0 + 16k
     const double du = static_cast<double>(u) - 31.5;
     const int kb = lane & 3, ti = lane >> 2;                 // SSD: 8 triplets x 4 keypoints per warp
+    const ushort4 slot0 = __ldg(p.slots + 8 * warp + ti);
+    const ushort4 slot1 = __ldg(p.slots + 8 * warp + ti + kFastT / 2);
     const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
     const long long nq = blockIdx.x < quads ? static_cast<long long>((quads - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
-    ushort4 slot[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) slot[j] = __ldg(p.slots + 8 * (rw + 16 * j) + ti);
     unsigned n_flagged = 0, n_windows = 0;
-    if (tid == 0) s_mask[0] = s_mask[1] = 0;
+    if (tid < 3) s_mask[tid] = 0;
+    stage_quad_rows(p, static_cast<unsigned long long>(blockIdx.x) * kQuad, s_tab, s_kp, tid);
+    __syncthreads();
 
     for (long long it = -1; it <= nq; ++it) {
         const int cur = static_cast<int>(it & 1), nxt = cur ^ 1;
-        if (producer) {
-            if (it >= 1) {   // pack the bits of the quad consumed in the previous iteration
-                const unsigned long long kp = (blockIdx.x + (it - 1) * gridDim.x) * kQuad + (rt >> 7);
-                const uint8_t* bits = s_bits + (nxt * kQuad + (rt >> 7)) * kFastT;
-                const int j = rt & 127;
+        const int mslot = static_cast<int>((it + 3) % 3);
+        const unsigned long long kp0 = (blockIdx.x + it * gridDim.x) * kQuad;   // quad `it` (when it >= 0)
+        const bool consume = it >= 0 && it < nq, produce = it + 1 < nq;
+        if (tid == 0) s_mask[(mslot + 1) % 3] = 0;           // quad it-2's mask: every reader is past it
+        if (it + 2 < nq)                                      // rows for quad it+2 -> buffer [cur]
+            stage_quad_rows(p, (blockIdx.x + (it + 2) * gridDim.x) * kQuad, s_tab + cur * kQuad * kWindow,
+                            s_kp + cur * kQuad * 4, tid);
+        if (it >= 1) {   // pack the bits of quad it-1 (buffer [nxt])
+            const unsigned long long kp = (blockIdx.x + (it - 1) * gridDim.x) * kQuad + (tid >> 8);
+            const uint8_t* bits = s_bits + (nxt * kQuad + (tid >> 8)) * kPipeBits;
+            const int j = tid & 255;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const unsigned w32 = __ballot_sync(0xffffffffu, bits[128 * k + j] != 0);
-                    if (lane == 0 && kp < p.M)
-                        reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8))[4 * k + (j >> 5)] = w32;
+            for (int k = 0; k < 2; ++k) {
+                const unsigned w32 = __ballot_sync(0xffffffffu, bits[256 * k + j] != 0);
+                if (lane == 0 && kp < p.M)
+                    reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8))[8 * k + (j >> 5)] = w32;
+            }
+        }
+
+        const float* const my_win = s_f + (cur * kQuad + kb) * kPlanePitch;
+        unsigned need = 0;
+        {
+            PipeStep st;
+            st.tex = p.tex;
+            st.tab = s_tab + nxt * kQuad * kWindow + v0;
+            st.kpr = s_kp + nxt * kQuad * 4;
+            st.fbase = s_f + nxt * kQuad * kPlanePitch + v0 * kWinStride + u;
+            st.du = du;
+            float d1a = 0.f, d2a = 0.f, d1b = 0.f, d2b = 0.f;
+            // Half of the warps (four per SM sub-partition) estimate first and resample second, the
+            // other half the other way round: at any moment about half of the SM is on the LSU and
+            // half on the fp64 pipe, with equal work per warp by construction.
+#pragma unroll 1
+            for (int phase = 0; phase < 2; ++phase) {
+                if ((phase == 0) == ssd_first) {
+                    if (consume) ssd_estimate_2(my_win, slot0, slot1, d1a, d2a, d1b, d2b);
+                } else if (produce) {
+                    resample_step(st);
                 }
             }
-            if (it + 1 < nq) {   // resample the next quad into F[nxt]
-                const unsigned long long kp0 = (blockIdx.x + (it + 1) * gridDim.x) * kQuad;
-                {   // keypoint records and the per-row products of extract_window (src/descriptor.cpp:44-45)
-                    // for all four windows; a keypoint past the end repeats the last one (result unused)
-                    const int w = rt >> 7, e = rt & 127;
-                    const unsigned long long kp = min(kp0 + w, p.M - 1);
-                    const double dv = static_cast<double>(e & 63) - 31.5;
-                    s_tab[w * 2 * kWindow + e] = __dmul_rn(__ldg(p.xycs + 4 * kp + ((e >> 6) ? 2 : 3)), dv);
-                    if (e < 4) s_kp[4 * w + e] = __ldg(p.xycs + 4 * kp + e);
-                }
-                role_barrier(1);
-                // Software pipeline over this thread's 32 samples (4 windows x 8 rows): the gather of
-                // sample i + kDepth is in flight while sample i is blended, so the texture latency
-                // hides behind this warp's own fp64 work instead of stalling it.
-                constexpr int kDepth = 4, kPer = kWindow / (kPipeRole / 64), kTotal = kQuad * kPer;
-                double pfx[kDepth], pfy[kDepth], xa = 0.0, ya = 0.0;
-                uchar4 pg[kDepth];
-                float* const fbase = s_f + nxt * kQuad * kPlanePitch + v0 * kWinStride + u;
-#pragma unroll
-                for (int i = 0; i < kTotal + kDepth; ++i) {
-                    if (i >= kDepth) {
-                        const int j = i - kDepth, sl = j % kDepth;
-                        const uchar4 g = pg[sl];   // w = (x0,y0), z = (x0+1,y0), x = (x0,y0+1), y = (x0+1,y0+1)
-                        const double val = blend(pfx[sl], pfy[sl], u8_to_f64(g.w), u8_to_f64(g.z), u8_to_f64(g.x),
-                                                 u8_to_f64(g.y));
-                        fbase[(j / kPer) * kPlanePitch + (j % kPer) * (kPipeRole / 64) * kWinStride] =
-                            __double2float_rz(val);
-                    }
-                    if (i < kTotal) {
-                        const int w = i / kPer, sl = i % kDepth;
-                        if (i % kPer == 0) {
-                            const double c = s_kp[4 * w + 2], sn = s_kp[4 * w + 3];
-                            xa = __dadd_rn(s_kp[4 * w + 0], __dmul_rn(c, du));
-                            ya = __dadd_rn(s_kp[4 * w + 1], __dmul_rn(sn, du));
-                        }
-                        const int v = v0 + (i % kPer) * (kPipeRole / 64);
-                        const double sx = __dsub_rn(xa, s_tab[w * 2 * kWindow + v]);
-                        const double sy = __dadd_rn(ya, s_tab[w * 2 * kWindow + kWindow + v]);
-                        int x0, y0;
-                        double x0f, y0f;
-                        floor_exact(sx, x0, x0f);
-                        floor_exact(sy, y0, y0f);
-                        pfx[sl] = __dsub_rn(sx, x0f);
-                        pfy[sl] = __dsub_rn(sy, y0f);
-                        pg[sl] = footprint(p.tex, x0, y0);
-                    }
-                }
+            if (consume) {
+                float diff0, diff1;
+                const bool sure0 = estimate_decides(d1a, d2a, diff0);
+                const bool sure1 = estimate_decides(d1b, d2b, diff1);
+                const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves an unused window
+                need = (live && !sure0 ? 1u : 0u) | (live && !sure1 ? 2u : 0u);
+                if (need) atomicOr(s_mask + mslot, 1 << kb);
+                uint8_t* const my_bits = s_bits + (cur * kQuad + kb) * kPipeBits;
+                my_bits[slot0.w & 0x7fff] = (slot0.w >> 15) ? diff0 < 0.0f : diff0 > 0.0f;
+                my_bits[slot1.w & 0x7fff] = (slot1.w >> 15) ? diff1 < 0.0f : diff1 > 0.0f;
             }
-        } else if (it >= 0 && it < nq) {
-            const unsigned long long kp0 = (blockIdx.x + it * gridDim.x) * kQuad;
-            const float* const my_win = s_f + (cur * kQuad + kb) * kPlanePitch;
-            const int lo_off = (2 - cur) * kQuad * kPlanePitch;          // F[cur][kb] -> LO[kb]
-            const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves a stale window
-            if (rt == 0) s_mask[nxt] = 0;
-            float d1[4], d2[4], diff[4];
-            ssd_estimate_2(my_win, slot[0], slot[1], d1[0], d2[0], d1[1], d2[1]);
-            ssd_estimate_2(my_win, slot[2], slot[3], d1[2], d2[2], d1[3], d2[3]);
-            unsigned need = 0;
-            bool bit[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const bool sure = estimate_decides(d1[j], d2[j], diff[j]);
-                bit[j] = (slot[j].w >> 15) ? diff[j] < 0.0f : diff[j] > 0.0f;
-                need |= (live && !sure) ? 1u << j : 0u;
-            }
-            if (need) atomicOr(s_mask + cur, 1 << kb);
-            role_barrier(2);
-            const int mask = *reinterpret_cast<volatile int*>(s_mask + cur);
-            if (mask) {   // uniform over the consumers: some window needs its LO plane
-                for (int w = 0; w < kQuad; ++w) {
-                    if (!((mask >> w) & 1)) continue;
-                    const double* kpr = p.xycs + 4 * (kp0 + w);
-                    const double c = __ldg(kpr + 2), s = __ldg(kpr + 3);
-                    const double xa = __dadd_rn(__ldg(kpr + 0), __dmul_rn(c, du));
-                    const double ya = __dadd_rn(__ldg(kpr + 1), __dmul_rn(s, du));
-                    int* lopl = reinterpret_cast<int*>(s_f) + (2 * kQuad + w) * kPlanePitch + u;
-#pragma unroll 2
-                    for (int v = v0; v < kWindow; v += kPipeRole / 64) {
-                        const double dv = static_cast<double>(v) - 31.5;
-                        lopl[v * kWinStride] = __double2loint(sample_exact(p.tex, xa, ya, __dmul_rn(s, dv), __dmul_rn(c, dv)));
-                    }
-                    n_windows += rt == 0;
-                }
-                role_barrier(2);
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if ((need >> j) & 1) {
-                        bit[j] = triplet_bit_7x7_planes_at(my_win, lo_off, slot[j].x, slot[j].y, slot[j].z, slot[j].w >> 15);
-                        ++n_flagged;
-                    }
-            }
-            uint8_t* const my_bits = s_bits + (cur * kQuad + kb) * kFastT;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) my_bits[slot[j].w & 0x7fff] = bit[j];
         }
         __syncthreads();
+
+        if (consume) {
+            const int mask = *reinterpret_cast<volatile int*>(s_mask + mslot);
+            if (mask) {   // block-uniform: some lane could not decide -> exact pass for those windows
+                for (int w = 0; w < kQuad; ++w) {
+                    if (!((mask >> w) & 1)) continue;
+                    const double* const kpr = p.xycs + 4 * (kp0 + w);   // (the staged copy is already quad it+2's)
+                    const double c = __ldg(kpr + 2), sn = __ldg(kpr + 3);
+                    const double xa = __dadd_rn(__ldg(kpr + 0), __dmul_rn(c, du));
+                    const double ya = __dadd_rn(__ldg(kpr + 1), __dmul_rn(sn, du));
+                    int* lopl = reinterpret_cast<int*>(s_f) + (2 * kQuad + w) * kPlanePitch + u;
+#pragma unroll 2
+                    for (int v = v0; v < kWindow; v += kPipeRows) {
+                        const double dv = static_cast<double>(v) - 31.5;
+                        lopl[v * kWinStride] =
+                            __double2loint(sample_exact(p.tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv)));
+                    }
+                    n_windows += tid == 0;
+                }
+                __syncthreads();
+                const int lo_off = (2 - cur) * kQuad * kPlanePitch;          // F[cur][kb] -> LO[kb]
+                uint8_t* const my_bits = s_bits + (cur * kQuad + kb) * kPipeBits;
+                if (need & 1) {
+                    my_bits[slot0.w & 0x7fff] =
+                        triplet_bit_7x7_planes_at(my_win, lo_off, slot0.x, slot0.y, slot0.z, slot0.w >> 15);
+                    ++n_flagged;
+                }
+                if (need & 2) {
+                    my_bits[slot1.w & 0x7fff] =
+                        triplet_bit_7x7_planes_at(my_win, lo_off, slot1.x, slot1.y, slot1.z, slot1.w >> 15);
+                    ++n_flagged;
+                }
+                __syncthreads();   // the next iteration packs these bits
+            }
+        }
     }
     if (p.stats != nullptr) {   // exact-pass counters (diagnostics; off unless asked for)
         n_flagged = __reduce_add_sync(0xffffffffu, n_flagged);
