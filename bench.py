@@ -39,12 +39,17 @@ METRIC = ("descriptors/sec extracted and Hamming compares/sec matched "
 UNIT = "keypoints/s (1 keypoint = 1 descriptor extracted + M Hamming compares)"
 
 # Algorithmic work per unit.
-FP64_OPS_PER_DESC = 4096 * 15 + 512 * 49 * 2 * 3          # non-fused fp64 ops
-SMEM_BYTES_PER_DESC = 512 * 49 * 3 * 8                     # 8-byte window reads in the SSD phase
+FP64_OPS_PER_DESC = 4096 * 15 + 512 * 49 * 2 * 3          # non-fused fp64 ops (variants 0/1: everything in fp64)
+SMEM_BYTES_PER_DESC = 512 * 49 * 3 * 8                     # 8-byte window reads in the SSD phase (variants 0/1)
+# Variants 2/3 decide each bit from a proven fp32 estimate and recompute in fp64 only when undecided:
+# the SSD phase reads 4-byte planes and runs fp32 FMAs; fp64 is left with the window resampling.
+FILT_FP64_OPS_PER_DESC = 4096 * 15                         # resampling only
+FILT_SMEM_BYTES_PER_DESC = 512 * 49 * 3 * 4                # 4-byte F-plane reads
 POPC_PER_COMPARE = 16
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
 # captures of the same command (profiles/*_ncu.json); cold-cache replay, so an upper bound.
-TRAFFIC_NCU = {"extract_quad_kernel<u8>": 2.419e+06,                 # profiles/r1t_extract_ncu.json
+TRAFFIC_NCU = {"extract_pipe_kernel": 2.419e+06,                     # profiles/r1y_extract_ncu.json
+               "extract_quad_kernel<u8>": 2.419e+06,                 # profiles/r1t_extract_ncu.json
                "match_tc_kernel (tcgen05 kind::i8)": 5.273e+06}     # profiles/r1t_match_tc_ncu.json
 
 
@@ -346,8 +351,10 @@ def run_ours(args):
     kernels, pipe_roofline = {}, {}
     if ext_s > 0:
         alg_bytes = img.nbytes + m * 32 + m * 64            # image once + keypoint records + descriptors out
-        smem_gbs = m * SMEM_BYTES_PER_DESC / ext_s / 1e9
-        fp64_gops = m * FP64_OPS_PER_DESC / ext_s / 1e9
+        filt = ev >= 2
+        smem_bytes = FILT_SMEM_BYTES_PER_DESC if filt else SMEM_BYTES_PER_DESC
+        smem_gbs = m * smem_bytes / ext_s / 1e9
+        fp64_gops = m * (FILT_FP64_OPS_PER_DESC if filt else FP64_OPS_PER_DESC) / ext_s / 1e9
         kernels[ext_name] = {
             "ms": ext_s * 1e3, "descriptors_per_s": m / ext_s,
             "hbm": {"achieved": alg_bytes / ext_s / 1e9, "algorithmic_bytes_per_launch": alg_bytes},
@@ -356,7 +363,8 @@ def run_ours(args):
         smem_peak = pipes.get("lds64_gbs", sms * 128 * sm_mhz * 1e6 / 1e9)
         fp64_peak = pipes.get("fp64_nonfused_gops", sms * 64 * sm_mhz * 1e6 / 1e9)
         pipe_roofline["extract"] = {
-            "bound": "shared-memory wavefronts (602 KB of 8-byte window reads per descriptor)",
+            "bound": (f"shared-memory wavefronts ({smem_bytes // 1000} KB of {4 if filt else 8}-byte window reads per "
+                      "descriptor" + ("; fp32 estimate + exact fp64 recompute of undecided bits)" if filt else ")")),
             "smem": {"achieved_gbs": smem_gbs, "peak_gbs": smem_peak, "frac": smem_gbs / smem_peak},
             "fp64": {"achieved_gops": fp64_gops, "peak_gops": fp64_peak, "frac": fp64_gops / fp64_peak},
             "peak_source": "measured microbench (profiles/pipe_peaks.json)" if pipes else

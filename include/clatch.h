@@ -78,6 +78,10 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * shared loads, 2 = four split (fp32 + low word) windows per CTA: a proven fp32 estimate decides
  * each bit and the rare undecided ones are recomputed exactly (default; u8-valued images — any
  * other image runs variant 1). Every variant returns the same bytes.
+ * key "host_promote": 1 lets clatch_describe_all_f64 convert a float64 image whose pixels are all
+ * integers in [0, 255] to u8 on the host workers before the upload (8x fewer bytes over the bus;
+ * lossless, same descriptors); 0 (default) uploads the doubles and classifies on the device —
+ * faster wherever the host reads its memory more slowly than PCIe 5 carries it.
  * key "extract_stats": non-zero starts counting variant 2's exact recomputes (and zeroes the
  * counters), 0 stops. Unknown keys fail with CLATCH_ERR_INVALID. */
 CLATCH_API int clatch_set_option(clatch_ctx* ctx, const char* key, int value);
@@ -263,6 +267,12 @@ CLATCH_API int clatch_debug_tc_tile(clatch_ctx* ctx, const uint8_t* queries, siz
 /* Kernel launches issued through this context since creation (bench.py's
  * gpu_launches claim is read from here, not estimated). */
 CLATCH_API uint64_t clatch_launch_count(clatch_ctx* ctx);
+
+/* Page-locked host memory for buffers that cross the bus (descriptor arrays a caller passes from
+ * describe to match): with it the transfers above are plain DMAs instead of copies staged through
+ * the driver's bounce buffer. Optional — every entry point accepts ordinary memory. */
+CLATCH_API int clatch_host_alloc(size_t bytes, void** out);
+CLATCH_API int clatch_host_free(void* ptr);
 
 #ifdef __cplusplus
 }

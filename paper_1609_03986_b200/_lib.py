@@ -99,6 +99,8 @@ _SIGNATURES = {
                                          C.c_double, C.c_int, C.c_int, C.c_int, i32p, C.c_size_t, szp]),
     "clatch_debug_tc_tile": (C.c_int, [C.c_void_p, u8p, C.c_size_t, u8p, C.c_size_t, i32p, i32p, i32p, i32p]),
     "clatch_launch_count": (C.c_uint64, [C.c_void_p]),
+    "clatch_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "clatch_host_free": (C.c_int, [C.c_void_p]),
 }
 
 EXPORTS = tuple(_SIGNATURES)

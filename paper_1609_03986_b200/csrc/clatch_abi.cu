@@ -16,6 +16,10 @@
 #include "clatch_internal.cuh"
 #include "slot_assign.hpp"
 
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
+
 namespace clatch {
 namespace {
 #include "default_plan_f8.inc"
@@ -153,6 +157,50 @@ int resolve_workers(int workers) {   // src/parallel.hpp:9-13
     return hw > 0 ? static_cast<int>(hw) : 1;
 }
 
+// Host-side promotion of a float64 image whose pixels are all integers in [0, 255] (every
+// PGM-sourced image, src/image.cpp:75-76) to u8: rows [r0, r1) -> dst, false at the first pixel
+// that is not such a value (NaN and out-of-range values fail the round trip). Same rule as the
+// device's classify_convert_kernel; it exists because 1 byte per pixel crosses the bus 8x faster
+// than 8, and the host can read its own memory faster than PCIe can carry it. SSE2 only (baseline
+// x86-64): 8 pixels per step.
+bool promote_rows_u8(const double* src, size_t src_pitch, uint8_t* dst, size_t dst_pitch, int width, int r0,
+                     int r1) {
+    for (int r = r0; r < r1; ++r) {
+        const double* s = src + static_cast<size_t>(r) * src_pitch;
+        uint8_t* d = dst + static_cast<size_t>(r) * dst_pitch;
+        int x = 0;
+        bool bad = false;
+#if defined(__SSE2__)
+        __m128d ne = _mm_setzero_pd();
+        __m128i high = _mm_setzero_si128();
+        for (; x + 8 <= width; x += 8) {
+            const __m128d a0 = _mm_loadu_pd(s + x), a1 = _mm_loadu_pd(s + x + 2), a2 = _mm_loadu_pd(s + x + 4),
+                          a3 = _mm_loadu_pd(s + x + 6);
+            const __m128i i0 = _mm_cvttpd_epi32(a0), i1 = _mm_cvttpd_epi32(a1), i2 = _mm_cvttpd_epi32(a2),
+                          i3 = _mm_cvttpd_epi32(a3);
+            ne = _mm_or_pd(_mm_or_pd(_mm_cmpneq_pd(_mm_cvtepi32_pd(i0), a0), _mm_cmpneq_pd(_mm_cvtepi32_pd(i1), a1)),
+                           _mm_or_pd(_mm_or_pd(_mm_cmpneq_pd(_mm_cvtepi32_pd(i2), a2),
+                                               _mm_cmpneq_pd(_mm_cvtepi32_pd(i3), a3)),
+                                     ne));
+            const __m128i lo = _mm_unpacklo_epi64(i0, i1), hi = _mm_unpacklo_epi64(i2, i3);
+            high = _mm_or_si128(high, _mm_or_si128(lo, hi));
+            const __m128i p16 = _mm_packs_epi32(lo, hi);
+            _mm_storel_epi64(reinterpret_cast<__m128i*>(d + x), _mm_packus_epi16(p16, p16));
+        }
+        high = _mm_andnot_si128(_mm_set1_epi32(0xFF), high);   // any bit above the low byte (or the sign)
+        bad = _mm_movemask_pd(ne) != 0 || _mm_movemask_epi8(_mm_cmpeq_epi32(high, _mm_setzero_si128())) != 0xFFFF;
+#endif
+        for (; x < width; ++x) {
+            const double v = s[x];
+            const bool ok = v >= 0.0 && v <= 255.0 && v == std::floor(v);
+            bad = bad || !ok;
+            d[x] = ok ? static_cast<uint8_t>(v) : 0;
+        }
+        if (bad) return false;
+    }
+    return true;
+}
+
 // WeightMask::seven_by_seven (src/pattern.cpp:28-35): ones on the top-left 7x7, zero last row/col.
 bool is_seven_by_seven(const std::vector<double>& w, int K) {
     if (K != 8) return false;
@@ -224,6 +272,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
         if (t.array) cudaFreeArray(t.array);
     }
     ctx->pinned.release();
+    ctx->pin_img.release();
     ctx->pin_xycs.release();
     ctx->pin_desc.release();
     if (ctx->copy_stream) {
@@ -265,6 +314,10 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         ctx->extract_variant = value;
         return CLATCH_OK;
     }
+    if (std::strcmp(key, "host_promote") == 0) {   // describe_all: float64 -> u8 on the host workers when lossless
+        ctx->host_promote = value != 0;
+        return CLATCH_OK;
+    }
     if (std::strcmp(key, "extract_stats") == 0) {   // count exact recomputes of the filtered kernel
         CLATCH_CUDA(cudaSetDevice(ctx->device));
         if (int rc = ctx->extract_stats.reserve(2 * sizeof(unsigned long long))) return rc;
@@ -283,6 +336,18 @@ int clatch_synchronize(clatch_ctx* ctx) {
 }
 
 uint64_t clatch_launch_count(clatch_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int clatch_host_alloc(size_t bytes, void** out) {
+    if (!out) return invalid("clatch_host_alloc: out is null");
+    *out = nullptr;
+    CLATCH_CUDA(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable));
+    return CLATCH_OK;
+}
+
+int clatch_host_free(void* ptr) {
+    if (ptr) CLATCH_CUDA(cudaFreeHost(ptr));
+    return CLATCH_OK;
+}
 
 int clatch_extract_stats(clatch_ctx* ctx, uint64_t* exact_triplets, uint64_t* exact_warps) {
     if (!ctx) return invalid("clatch_extract_stats: ctx is null");
@@ -513,6 +578,24 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
     if (!kps || !kept || !out) return invalid("describe_all: null keypoint/output buffer");
     CLATCH_CUDA(cudaSetDevice(ctx->device));
     constexpr bool kU8 = sizeof(Pixel) == 1;
+    if (!kU8 && ctx->host_promote && n >= 256) {
+        // float64 image: try the lossless u8 promotion on the host workers first (page-locked
+        // staging); a non-u8-valued image stops at its first such pixel and takes the f64 route.
+        const size_t upitch = (static_cast<size_t>(width) + 15) / 16 * 16;
+        if (int rc = ctx->pin_img.reserve(upitch * height)) return rc;
+        uint8_t* const staged = static_cast<uint8_t*>(ctx->pin_img.ptr);
+        const int parts = std::max(1, std::min(resolve_workers(workers), height / 8));
+        std::vector<int> ok(parts, 0);
+        const int rows = (height + parts - 1) / parts;
+        WorkerPool::instance().run(parts, [&](int w) {
+            const int r0 = std::min(height, w * rows), r1 = std::min(height, r0 + rows);
+            ok[w] = promote_rows_u8(reinterpret_cast<const double*>(img), pitch, staged, upitch, width, r0, r1);
+        });
+        bool all = true;
+        for (int v : ok) all = all && v;
+        if (all)
+            return describe_all_impl<uint8_t>(ctx, staged, width, height, upitch, kps, n, cols, workers, kept, out, m);
+    }
     const size_t dpitch = kU8 ? (static_cast<size_t>(width) + 15) / 16 * 16 : static_cast<size_t>(width);
     const size_t bytes = static_cast<size_t>(ctx->pattern.T) / 8;
     if (int rc = ctx->img.reserve(sizeof(Pixel) * dpitch * height)) return rc;
@@ -1144,17 +1227,18 @@ int clatch_match_brute_force(clatch_ctx* ctx, const uint8_t* probes, size_t Q,
     int32_t* r = ctx->res.as<int32_t>();
     if (int rc = launch_match_top2(ctx, ctx->q.as<uint8_t>(), Q, d_gallery, N, bytes, r, r + Q, r + 2 * Q, st))
         return rc;
-    std::vector<int32_t> host(3 * Q + (cross_check ? N : 0));
+    const size_t host_count = 3 * Q + (cross_check ? N : 0);
+    if (int rc = ctx->pinned.reserve(sizeof(int32_t) * host_count)) return rc;   // page-locked: a plain DMA
+    int32_t* const host = static_cast<int32_t*>(ctx->pinned.ptr);
     if (cross_check) {   // reverse_best[g] = knn2(gallery[g], probes).best_index, src/match.cpp:62-67
         if (int rc = launch_match_top2(ctx, d_gallery, N, ctx->q.as<uint8_t>(), Q, bytes, r + 3 * Q, nullptr,
                                        nullptr, st))
             return rc;
     }
-    CLATCH_CUDA(cudaMemcpyAsync(host.data(), r, sizeof(int32_t) * host.size(), cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaMemcpyAsync(host, r, sizeof(int32_t) * host_count, cudaMemcpyDeviceToHost, st));
     CLATCH_CUDA(cudaStreamSynchronize(st));
-    return clatch_filter_matches(host.data(), host.data() + Q, host.data() + 2 * Q, Q, has_ratio, ratio,
-                                 has_max, max_distance, cross_check ? host.data() + 3 * Q : nullptr, out,
-                                 count);
+    return clatch_filter_matches(host, host + Q, host + 2 * Q, Q, has_ratio, ratio, has_max, max_distance,
+                                 cross_check ? host + 3 * Q : nullptr, out, count);
 }
 
 } // extern "C"

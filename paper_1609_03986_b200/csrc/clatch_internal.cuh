@@ -98,6 +98,8 @@ struct clatch_ctx {
     std::vector<double> host_xycs;   // describe_all staging
     clatch::PinnedBuffer pinned;     // D2H staging for batched pair results
     clatch::PinnedBuffer pin_xycs, pin_desc;   // describe_all staging (banded upload path)
+    clatch::PinnedBuffer pin_img;              // describe_all: host-promoted u8 copy of a float64 image
+    bool host_promote = false;   // measured slower than the 16.6 MB DMA on the B200 host (profiles/r1y_e2e_breakdown.log)
     cudaStream_t copy_stream = nullptr;        // image bands stream in here while kernels run on `stream`
     cudaEvent_t band_events[8] = {};
     struct PipeSlot {                // describe_batch: one of two pipeline slots

@@ -10,16 +10,56 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import weakref
 
 import numpy as np
 
 from . import _lib
-from ._lib import f64p, i16p, i32p, i64p, u8p
+from ._lib import check, f64p, i16p, i32p, i64p, u8p
 from .pattern import TripletPattern, default_pattern
 
 
 def _ptr(a: np.ndarray, t):
     return a.ctypes.data_as(t)
+
+
+class _PinnedPool:
+    """Page-locked numpy arrays for the results the API hands back (descriptor arrays usually come
+    straight back as match() inputs: page-locked, both transfers are plain DMAs). cudaHostAlloc is
+    slow, so freed blocks are kept by power-of-two size and reused; a block returns to the pool when
+    the last numpy view of it dies."""
+
+    def __init__(self, lib, keep_bytes: int = 256 << 20):
+        self.lib, self.free, self.kept, self.keep_bytes = lib, {}, 0, keep_bytes
+        self.lock = threading.Lock()
+
+    def empty(self, shape, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        cap = 1 << max(12, (max(nbytes, 1) - 1).bit_length())
+        with self.lock:
+            blocks = self.free.get(cap)
+            ptr = blocks.pop() if blocks else None
+            if ptr is not None:
+                self.kept -= cap
+        if ptr is None:
+            p = C.c_void_p()
+            check(self.lib.clatch_host_alloc(cap, C.byref(p)))
+            ptr = p.value
+        owner = (C.c_uint8 * cap).from_address(ptr)
+        weakref.finalize(owner, self._release, ptr, cap)
+        return np.frombuffer(owner, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def _release(self, ptr, cap):
+        with self.lock:
+            if self.kept + cap <= self.keep_bytes:
+                self.free.setdefault(cap, []).append(ptr)
+                self.kept += cap
+                return
+        try:
+            self.lib.clatch_host_free(ptr)
+        except Exception:
+            pass
 
 
 class DescriptorSet:
@@ -56,6 +96,7 @@ class Engine:
         self._pattern_key = None
         self._pattern = None
         self._lock = threading.Lock()
+        self._pinned = _PinnedPool(self.lib)
         sm, khz = C.c_int(), C.c_int()
         name = C.create_string_buffer(256)
         _lib.check(self.lib.clatch_device_info(self.ctx, C.byref(sm), C.byref(khz), name, 256))
@@ -181,7 +222,7 @@ class Engine:
         kps = np.ascontiguousarray(keypoints, np.float64)
         n, cols = kps.shape
         kept = np.empty(n, np.int64)
-        out = np.empty((n, self.descriptor_bytes), np.uint8)
+        out = self._pinned.empty((n, self.descriptor_bytes), np.uint8)
         m = C.c_size_t()
         with self._lock:
             if image.dtype == np.uint8:

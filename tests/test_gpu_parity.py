@@ -485,6 +485,32 @@ def test_filtered_kernel_exact_pass_rate(lk, port, variant):
         eng.set_option("extract_variant", 3)
 
 
+@pytest.mark.parametrize("promote", [1, 0])
+def test_float64_promotion_edges(lk, port, promote):
+    """A float64 image goes to the u8 kernels only if EVERY pixel is an integer in [0, 255] (host
+    workers or device classifier, same rule). One odd pixel anywhere — vector body, scalar tail,
+    first or last row — must send the whole image down the float64 route, and either way the
+    descriptors are the oracle's."""
+    eng = lk.get_engine()
+    eng.set_option("host_promote", promote)
+    try:
+        w, h = 331, 207                                   # width % 8 != 0: exercises the scalar tail
+        base = port.random_image_u8(321, w, h).astype(np.float64)
+        kps = port.random_keypoints(322, w, h, 300)
+        want = port.describe_all(base, kps)[1]
+        assert np.array_equal(lk.describe(base, kps)[1], want)
+        neg_zero = base.copy()
+        neg_zero[base == 0] = -0.0                        # still u8-valued
+        assert np.array_equal(lk.describe(neg_zero, kps)[1], want)
+        for (y, x), v in {(0, 0): 100.5, (h - 1, w - 1): 256.0, (100, 328): -1.0, (57, 160): 1e300,
+                          (101, 7): 254.99999999999997, (h // 2, 3): 2.0 ** -40}.items():
+            img = base.copy()
+            img[y, x] = v
+            assert np.array_equal(lk.describe(img, kps)[1], port.describe_all(img, kps)[1]), (y, x, v)
+    finally:
+        eng.set_option("host_promote", 0)
+
+
 # ------------------------------------------------------ resident sets, batched pairs ----
 
 def test_resident_sets_and_batched_pairs(lk, port):

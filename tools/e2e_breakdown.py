@@ -51,12 +51,23 @@ ms, _ = timeit(lambda: lk.describe(img8, k))
 print(f"lk.describe u8               {ms:.3f} ms")
 ms, _ = timeit(lambda: lk.describe(img64, k))
 print(f"lk.describe f64              {ms:.3f} ms")
+eng.set_option("host_promote", 1)
+ms, _ = timeit(lambda: lk.describe(img64, k))
+print(f"lk.describe f64, host_promote=1 (u8 conversion on the host workers, 2 MB upload) {ms:.3f} ms")
+eng.set_option("host_promote", 0)
+pageable = img.astype(np.float64)
+ms, _ = timeit(lambda: lk.describe(pageable, k))
+print(f"lk.describe f64 pageable image {ms:.3f} ms")
+_, desc = lk.describe(img8, k)                      # page-locked result array, as the API returns it
 ms, _ = timeit(lambda: eng.match_top2(desc, desc))
 print(f"match_top2 host              {ms:.3f} ms")
 ms, _ = timeit(lambda: eng.match_brute_force(desc, desc))
 print(f"match_brute_force host       {ms:.3f} ms")
 ms, _ = timeit(lambda: lk.match(desc, desc))
 print(f"lk.match                     {ms:.3f} ms")
+dpage = desc.copy()
+ms, _ = timeit(lambda: lk.match(dpage, dpage))
+print(f"lk.match pageable arrays     {ms:.3f} ms")
 ms, _ = timeit(lambda: lk.match(desc, desc, ratio=0.8, cross_check=True))
 print(f"lk.match ratio+cross         {ms:.3f} ms")
 d_img = torch.from_numpy(img).cuda()

@@ -1,4 +1,5 @@
 set -u
-OUT=gpurun_out/r1w; mkdir -p $OUT
-timeout 600 python -m pytest tests -m gpu -x -q -k "extraction_variant or filtered or golden or reference_vectors" > $OUT/pytest_sel.log 2>&1; echo "rc=$?"; tail -3 $OUT/pytest_sel.log
-timeout 300 python tools/extract_perf.py 2>&1 | grep "variant [23]" | tee $OUT/extract_perf.log
+OUT=gpurun_out/r1x; mkdir -p $OUT
+timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -4 $OUT/pytest_gpu.log
+timeout 300 python tools/e2e_breakdown.py 2>&1 | tee $OUT/e2e_breakdown.log
+timeout 600 python bench.py --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; cat $OUT/bench.json | python -c "import sys,json; d=json.load(sys.stdin); print({k:d[k] for k in ['value','ms_per_step','descriptors_per_s','compares_per_s','gpu_launches']}); print(d['e2e']['ms_per_step'], d['e2e_u8']['ms_per_step'])"
