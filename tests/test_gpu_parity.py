@@ -418,6 +418,37 @@ def test_every_extraction_variant_is_exact(lk, port, variant):
         eng.set_option("extract_variant", 3)
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_trained_pattern_on_every_fast_kernel(lk, port, variant):
+    """A trained pattern has the built-in shape (T=512, K=8, 7x7-of-8x8 mask) but other triplets:
+    it takes the specialised kernels with a lane placement planned at clatch_set_pattern time
+    (the shipped placement only fits the built-in table). Clustered coordinates make the bank
+    residues as unbalanced as a real table can be."""
+    rng = np.random.default_rng(5120 + variant)
+    trip = rng.integers(0, 57, (512, 6))
+    trip[:128, :] = rng.integers(0, 8, (128, 6)) * 8            # all residues equal: worst case for the planner
+    trip[128:160, 2:4] = trip[128:160, 0:2]                      # companion b on top of the anchor
+    same = (trip[:, 2] == trip[:, 4]) & (trip[:, 3] == trip[:, 5])
+    trip[same, 4] = (trip[same, 4] + 1) % 57                     # companions must differ (DegenerateTriplet)
+    mask = np.ones((8, 8))
+    mask[7, :] = 0.0
+    mask[:, 7] = 0.0
+    text = "LATCHPAT v1 T=512 K=8\n" + "".join(" ".join(map(str, t)) + "\n" for t in trip)
+    text += "WEIGHTS\n" + "".join(" ".join("%.17g" % v for v in row) + "\n" for row in mask)
+    pat = (512, 8, trip.astype(np.int32), mask.reshape(-1))
+    eng = lk.get_engine()
+    eng.set_option("extract_variant", variant)
+    try:
+        for img in (port.random_image_u8(88, 300, 200), port.structured_image(89, 300, 200).astype(np.uint8)):
+            kps = port.random_keypoints(90, 300, 200, 333)
+            want = port.describe_all(img.astype(np.float64), kps, pattern=pat)[1]
+            assert np.array_equal(lk.describe(img, kps, pattern=text)[1], want)
+            assert np.array_equal(lk.describe(img.astype(np.float64), kps, pattern=text)[1], want)
+    finally:
+        eng.set_option("extract_variant", 3)
+        lk.describe(port.random_image_u8(88, 300, 200), port.random_keypoints(90, 300, 200, 4))   # built-in table back
+
+
 def _near_tie_images(w, h):
     """u8 images built to put d1 - d2 at or next to zero: the inputs on which an fp32 estimate
     of the SSD pair must NOT be trusted (exact ties, rounding-level differences, tiny sums)."""
