@@ -346,7 +346,7 @@ def run_ours(args):
     mv = args.match_variant if args.match_variant is not None else 3
     ev = args.extract_variant if args.extract_variant is not None else 3
     ext_name = {0: "extract_fast_kernel<u8>", 1: "extract_quad_kernel<u8>", 2: "extract_filt_kernel",
-                3: "extract_pipe_kernel"}[ev]
+                3: "extract_pipe_kernel", 4: "extract_roles_kernel<16>"}[ev]
     mat_name = "match_tc_kernel (tcgen05 kind::i8)" if mv == 3 else f"match64_kernel<{mv}>"
     kernels, pipe_roofline = {}, {}
     if ext_s > 0:
@@ -449,8 +449,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--phase", choices=["both", "extract", "match"], default="both")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--match-variant", type=int, default=None, help="override the matcher kernel variant (0..3)")
-    ap.add_argument("--extract-variant", type=int, default=None, help="override the extraction kernel variant (0..3)")
+    ap.add_argument("--match-variant", type=int, default=None, help="override the matcher kernel variant (0..4)")
+    ap.add_argument("--extract-variant", type=int, default=None, help="override the extraction kernel variant (0..4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -76,8 +76,10 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * compression + 9 POPC, 2 = 9 CSA + 7 POPC, 3 = tcgen05 int8 GEMM on the tensor cores (default).
  * key "extract_variant": 0 = one window per CTA, 1 = four fp64 windows per CTA with conflict-free
  * shared loads, 2 = four split (fp32 + low word) windows per CTA: a proven fp32 estimate decides
- * each bit and the rare undecided ones are recomputed exactly (default; u8-valued images — any
- * other image runs variant 1). Every variant returns the same bytes.
+ * each bit and the rare undecided ones are recomputed exactly, 3 = the same estimate with
+ * double-buffered planes, texture-unit footprints and resampling overlapped with the estimate
+ * (default), 4 = variant 3 with dedicated producer / consumer warps. 2-4 take u8-valued images; any
+ * other image runs variant 1. Every variant returns the same bytes.
  * key "host_promote": 1 lets clatch_describe_all_f64 convert a float64 image whose pixels are all
  * integers in [0, 255] to u8 on the host workers before the upload (8x fewer bytes over the bus;
  * lossless, same descriptors); 0 (default) uploads the doubles and classifies on the device —

@@ -310,7 +310,7 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         return CLATCH_OK;
     }
     if (std::strcmp(key, "extract_variant") == 0) {
-        if (value < 0 || value > 3) return invalid("extract_variant must be 0..3");
+        if (value < 0 || value > 4) return invalid("extract_variant must be 0..4");
         ctx->extract_variant = value;
         return CLATCH_OK;
     }

@@ -860,6 +860,158 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_pipe_kernel(ExtractPa
     }
 }
 
+// ---- role-split variant of the pipelined kernel (A/B) -----------------------------------------
+// Same planes, same texture path, same estimate and exact code as extract_pipe_kernel, but the
+// warps specialise: kRW producer warps only resample (quad it+1 -> F[next]) and pack bits, the
+// other 32 - kRW consumer warps only estimate (quad it from F[cur]) and own the exact pass. The
+// LSU then sees a steady stream from the consumers instead of bursts from whichever half of the
+// SM is in its estimate phase. Roles are spread evenly over the four SM sub-partitions.
+template <int kRW>
+__global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractParams p) {
+    if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
+    constexpr int kSW = 32 - kRW, kRT = kRW * 32, kST = kSW * 32;
+    constexpr int kStep = 32 / kSW;                          // every kStep-th group of 4 warps consumes
+    constexpr int kRRows = kRT / kWindow;                    // producer thread -> rows v0 + kRRows * k
+    constexpr int kRPer = (kWindow + kRRows - 1) / kRRows;   // samples per producer thread per window (max)
+    constexpr int kSRows = kST / kWindow;                    // exact pass: consumer thread -> rows v0 + kSRows * k
+    constexpr int kSlots = 64 / kSW;                         // groups of 8 triplets per consumer warp
+    static_assert(32 % kSW == 0 && 64 % kSW == 0 && kSlots % 2 == 0 && kRT >= 512, "role split");
+
+    extern __shared__ __align__(16) uint8_t s_quad[];
+    float* const s_f = reinterpret_cast<float*>(s_quad);                              // F[2][4], then LO[4]
+    uint8_t* const s_bits = s_quad + kPipePlanes * kPlanePitch * 4;                   // [2][4][512 + pad]
+    double2* const s_tab = reinterpret_cast<double2*>(s_bits + 2 * kQuad * kPipeBits);   // [4][64] (next quad)
+    double* const s_kp = reinterpret_cast<double*>(s_tab + 2 * kQuad * kWindow);      // [4][x, y, cos, sin]
+    int* const s_mask = reinterpret_cast<int*>(s_kp + 2 * kQuad * 4);                 // [2] windows needing LO
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, grp = warp >> 2;
+    const bool producer = grp % kStep != 0;
+    const int rw = (producer ? grp - grp / kStep - 1 : grp / kStep) * 4 + (warp & 3);   // role-local warp
+    const int rt = rw * 32 + lane;                                                       // role-local thread
+    const int u = rt & 63, v0 = rt >> 6;
+    const double du = static_cast<double>(u) - 31.5;
+    const int kb = lane & 3, ti = lane >> 2;
+    const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
+    const long long nq = blockIdx.x < quads ? static_cast<long long>((quads - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+    ushort4 slot[kSlots];
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) slot[j] = __ldg(p.slots + 8 * (rw % kSW + kSW * j) + ti);
+    unsigned n_flagged = 0, n_windows = 0;
+    if (tid == 0) s_mask[0] = s_mask[1] = 0;
+
+    for (long long it = -1; it <= nq; ++it) {
+        const int cur = static_cast<int>(it & 1), nxt = cur ^ 1;
+        if (producer) {
+            if (it >= 1 && rt < 512) {   // pack the bits of the quad consumed in the previous iteration
+                const unsigned long long kp = (blockIdx.x + (it - 1) * gridDim.x) * kQuad + (rt >> 7);
+                const uint8_t* bits = s_bits + (nxt * kQuad + (rt >> 7)) * kPipeBits;
+                const int j = rt & 127;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const unsigned w32 = __ballot_sync(0xffffffffu, bits[128 * k + j] != 0);
+                    if (lane == 0 && kp < p.M)
+                        reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8))[4 * k + (j >> 5)] = w32;
+                }
+            }
+            if (it + 1 < nq) {   // resample the next quad into F[nxt]
+                stage_quad_rows(p, (blockIdx.x + (it + 1) * gridDim.x) * kQuad, s_tab, s_kp, rt);
+                asm volatile("bar.sync 1, %0;" ::"n"(kRT) : "memory");
+                constexpr int kDepth = 4, kTotal = kQuad * kRPer;
+                double pfx[kDepth], pfy[kDepth], xa = 0.0, ya = 0.0;
+                uint4 pg[kDepth];
+                float* const fbase = s_f + nxt * kQuad * kPlanePitch + v0 * kWinStride + u;
+#pragma unroll
+                for (int i = 0; i < kTotal + kDepth; ++i) {
+                    if (i >= kDepth) {
+                        const int j = i - kDepth, sl = j % kDepth;
+                        if (v0 + (j % kRPer) * kRRows < kWindow) {      // warp-uniform
+                            const uint4 g = pg[sl];
+                            const double val = blend(pfx[sl], pfy[sl], u8_to_f64(g.w), u8_to_f64(g.z), u8_to_f64(g.x),
+                                                     u8_to_f64(g.y));
+                            fbase[(j / kRPer) * kPlanePitch + (j % kRPer) * kRRows * kWinStride] =
+                                __double2float_rz(val);
+                        }
+                    }
+                    if (i < kTotal) {
+                        const int w = i / kRPer, sl = i % kDepth;
+                        if (i % kRPer == 0) {
+                            xa = __dadd_rn(s_kp[4 * w + 0], __dmul_rn(s_kp[4 * w + 2], du));
+                            ya = __dadd_rn(s_kp[4 * w + 1], __dmul_rn(s_kp[4 * w + 3], du));
+                        }
+                        const int v = v0 + (i % kRPer) * kRRows;
+                        if (v < kWindow) {                               // warp-uniform
+                            const double2 row = s_tab[w * kWindow + v];   // {s*dv, c*dv}
+                            const double sx = __dsub_rn(xa, row.x);
+                            const double sy = __dadd_rn(ya, row.y);
+                            int x0, y0;
+                            double x0f, y0f;
+                            floor_exact(sx, x0, x0f);
+                            floor_exact(sy, y0, y0f);
+                            pfx[sl] = __dsub_rn(sx, x0f);
+                            pfy[sl] = __dsub_rn(sy, y0f);
+                            pg[sl] = footprint(p.tex, x0, y0);
+                        }
+                    }
+                }
+            }
+        } else if (it >= 0 && it < nq) {
+            const unsigned long long kp0 = (blockIdx.x + it * gridDim.x) * kQuad;
+            const float* const my_win = s_f + (cur * kQuad + kb) * kPlanePitch;
+            const int lo_off = (2 - cur) * kQuad * kPlanePitch;          // F[cur][kb] -> LO[kb]
+            const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves an unused window
+            if (rt == 0) s_mask[nxt] = 0;
+            uint8_t* const my_bits = s_bits + (cur * kQuad + kb) * kPipeBits;
+            unsigned need = 0;
+#pragma unroll
+            for (int j = 0; j < kSlots; j += 2) {
+                float d1a, d2a, d1b, d2b, diff0, diff1;
+                ssd_estimate_2(my_win, slot[j], slot[j + 1], d1a, d2a, d1b, d2b);
+                const bool sure0 = estimate_decides(d1a, d2a, diff0);
+                const bool sure1 = estimate_decides(d1b, d2b, diff1);
+                need |= (live && !sure0 ? 1u << j : 0u) | (live && !sure1 ? 2u << j : 0u);
+                my_bits[slot[j].w & 0x7fff] = (slot[j].w >> 15) ? diff0 < 0.0f : diff0 > 0.0f;
+                my_bits[slot[j + 1].w & 0x7fff] = (slot[j + 1].w >> 15) ? diff1 < 0.0f : diff1 > 0.0f;
+            }
+            if (need) atomicOr(s_mask + cur, 1 << kb);
+            asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
+            const int mask = *reinterpret_cast<volatile int*>(s_mask + cur);
+            if (mask) {   // uniform over the consumers: some window needs its LO plane
+                for (int w = 0; w < kQuad; ++w) {
+                    if (!((mask >> w) & 1)) continue;
+                    const double* kpr = p.xycs + 4 * (kp0 + w);
+                    const double c = __ldg(kpr + 2), sn = __ldg(kpr + 3);
+                    const double xa = __dadd_rn(__ldg(kpr + 0), __dmul_rn(c, du));
+                    const double ya = __dadd_rn(__ldg(kpr + 1), __dmul_rn(sn, du));
+                    int* lopl = reinterpret_cast<int*>(s_f) + (2 * kQuad + w) * kPlanePitch + u;
+#pragma unroll 2
+                    for (int v = v0; v < kWindow; v += kSRows) {
+                        const double dv = static_cast<double>(v) - 31.5;
+                        lopl[v * kWinStride] =
+                            __double2loint(sample_exact(p.tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv)));
+                    }
+                    n_windows += rt == 0;
+                }
+                asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
+#pragma unroll
+                for (int j = 0; j < kSlots; ++j)
+                    if ((need >> j) & 1) {
+                        my_bits[slot[j].w & 0x7fff] =
+                            triplet_bit_7x7_planes_at(my_win, lo_off, slot[j].x, slot[j].y, slot[j].z, slot[j].w >> 15);
+                        ++n_flagged;
+                    }
+            }
+        }
+        __syncthreads();
+    }
+    if (p.stats != nullptr) {
+        n_flagged = __reduce_add_sync(0xffffffffu, n_flagged);
+        if (lane == 0 && (n_flagged | n_windows)) {
+            atomicAdd(p.stats + 0, static_cast<unsigned long long>(n_flagged));
+            atomicAdd(p.stats + 1, static_cast<unsigned long long>(n_windows));
+        }
+    }
+}
+
 // Generic pattern: any T (multiple of 8), 1 <= K <= 64, arbitrary non-negative weights.
 // d += (w*e)*e exactly as the reference writes it (src/descriptor.cpp:70-71).
 template <bool kU8>
@@ -1019,9 +1171,11 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     p.flags = flags;
     p.run_if_flag = run_if_flag;
     p.stats = ctx->extract_stats_on ? ctx->extract_stats.as<unsigned long long>() : nullptr;
-    if (kU8 && pat.fast && ctx->extract_variant == 3) {
+    if (kU8 && pat.fast && ctx->extract_variant >= 3) {
         if (!ctx->pipe_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kPipeSmemBytes));
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_roles_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kPipeSmemBytes));
             ctx->pipe_configured = true;
         }
@@ -1035,7 +1189,10 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         p.slots = pat.slots_f8.as<ushort4>();
         const size_t quads = (M + kQuad - 1) / kQuad;
         const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
-        extract_pipe_kernel<<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
+        // variant 4: dedicated producer / consumer warps, 16 + 16 (24 + 8 measured 48.8 M desc/s: eight
+        // warps cannot keep the LSU busy; 16 + 16 ties with the symmetric schedule at ~60 M)
+        if (ctx->extract_variant == 4) extract_roles_kernel<16><<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
+        else extract_pipe_kernel<<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
     } else if (kU8 && pat.fast && ctx->extract_variant == 2) {
         if (!ctx->filt_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_filt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

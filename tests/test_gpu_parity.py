@@ -397,7 +397,7 @@ def test_every_matcher_variant_is_exact(lk, port, variant):
         eng.set_option("match_variant", 3)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_every_extraction_variant_is_exact(lk, port, variant):
     """All specialised extraction kernels (one window per CTA / four fp64 windows per CTA / four
     split windows with the fp32 filter / the producer-consumer pipeline over the texture unit)
@@ -472,7 +472,7 @@ def _near_tie_images(w, h):
     return out
 
 
-@pytest.mark.parametrize("variant", [2, 3])
+@pytest.mark.parametrize("variant", [2, 3, 4])
 def test_filtered_kernel_on_near_ties(lk, port, variant):
     """The filtered and pipelined kernels decide a bit from fp32 sums only when a rigorous error bound
     separates them; everything else is recomputed in exact fp64. Flat regions, periodic
@@ -493,7 +493,7 @@ def test_filtered_kernel_on_near_ties(lk, port, variant):
     eng.set_option("extract_variant", 3)
 
 
-@pytest.mark.parametrize("variant", [2, 3])
+@pytest.mark.parametrize("variant", [2, 3, 4])
 def test_filtered_kernel_exact_pass_rate(lk, port, variant):
     """Diagnostics counters: on noise the exact pass is rare (that is where the speed comes
     from), on a flat image every triplet takes it (that is where the exactness comes from)."""

@@ -1,3 +1,4 @@
 set -u
 OUT=gpurun_out/r1z; mkdir -p $OUT
-timeout 1200 python -m pytest tests -m gpu -x -q -k "trained_pattern or custom_patterns" 2>&1 | tail -15
+timeout 600 python -m pytest tests -m gpu -x -q -k "extraction_variant or filtered" 2>&1 | tail -5
+timeout 300 python tools/extract_perf.py 2>&1 | grep "^u8" | tee $OUT/extract_perf.log
