@@ -79,7 +79,7 @@ struct clatch_ctx {
     uint64_t launches = 0;
     bool tc_configured = false, quad_configured = false, filt_configured = false, pipe_configured = false;   // opt-in smem sizes set on this device
     // 0: one window per CTA (4 CTAs/SM); 1: quad kernel (4 fp64 windows per CTA); 2: filtered kernel
-    // (4 split windows per CTA, fp32 estimate + exact recompute); 3: pipelined kernel (producer warps
+    // (4 split windows per CTA, fp32 estimate + exact recompute); 3: pipelined kernel (resampling
     // overlapped with the estimate, footprints from the texture unit); 4: variant 3 with dedicated
     // producer / consumer warps. 2-4 take u8 images — others run variant 1.
     int extract_variant = 3;
