@@ -314,6 +314,10 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         ctx->extract_variant = value;
         return CLATCH_OK;
     }
+    if (std::strcmp(key, "match_streamk") == 0) {   // tensor matcher: stream-K partition for small problems
+        ctx->match_streamk = value != 0;
+        return CLATCH_OK;
+    }
     if (std::strcmp(key, "host_promote") == 0) {   // describe_all: float64 -> u8 on the host workers when lossless
         ctx->host_promote = value != 0;
         return CLATCH_OK;

@@ -92,6 +92,7 @@ struct clatch_ctx {
     std::vector<TexImage> tex_images;
     bool extract_stats_on = false;           // count exact recomputes (clatch_extract_stats)
     clatch::DeviceBuffer extract_stats;      // 2 x u64
+    bool match_streamk = true;     // tensor matcher: equal-share partition for small problems (set_option "match_streamk")
     int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
     // scratch for the host-buffer entry points
     clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t, items, scores, counts, det;

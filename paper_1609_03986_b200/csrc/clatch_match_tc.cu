@@ -175,10 +175,20 @@ struct TcArgs {
     const uint8_t* b_exp;
     unsigned long long Q, N;
     int qtiles, total_tiles, tiles_per_split, num_items;
+    int sk_chunks;           // > 0: "stream-K" partition of the (query tile, train tile) units over this many CTAs
     Partial* partial;
     int* dump;               // optional: raw accumulators of item 0's first tile, 128 x 256
     const TcItem* items;     // optional item table
 };
+
+// Stream-K partition: chunk c owns units [c*U/G, (c+1)*U/G); the chunk that holds unit x.
+__host__ __device__ __forceinline__ unsigned long long tc_sk_chunk_of(unsigned long long x, unsigned long long U,
+                                                                      unsigned long long G) {
+    unsigned long long c = x * G / U;
+    while ((c + 1) * U / G <= x) ++c;
+    while (c * U / G > x) --c;
+    return c;
+}
 
 __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item) {
     TcWork w;
@@ -195,6 +205,36 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item) {
         w.o_idx = it.best_idx;
         w.o_best = it.best_dist;
         w.o_second = it.second_dist;
+    } else if (g.sk_chunks > 0) {
+        // Small problems (train set resident in L2): the qtiles x total_tiles units are cut into
+        // sk_chunks equal runs, one per CTA, in query-tile-major order; a run that crosses a query
+        // tile boundary is several pieces (item = CTA + piece * chunks). Every CTA then carries the
+        // same number of tile-times instead of ceil(items / SMs) whole rounds.
+        const unsigned long long U = static_cast<unsigned long long>(g.qtiles) * g.total_tiles;
+        const unsigned long long G = g.sk_chunks, TT = g.total_tiles;
+        const unsigned long long c = static_cast<unsigned long long>(item) % G;
+        const int piece = static_cast<int>(item / G);
+        unsigned long long u = c * U / G;
+        const unsigned long long ue = (c + 1) * U / G;
+        unsigned long long q = 0, t0 = 0, n = 0;
+        for (int i = 0; i <= piece; ++i, u += n) {
+            if (u >= ue) {
+                n = 0;
+                break;
+            }
+            q = u / TT;
+            t0 = u - q * TT;
+            n = min(ue - u, TT - t0);
+        }
+        w.qtile = static_cast<unsigned>(q);
+        w.tile_begin = static_cast<int>(t0);
+        w.ntiles = static_cast<int>(n);
+        w.split = static_cast<int>(c - tc_sk_chunk_of(q * TT, U, G));   // pieces of a query tile in train order
+        w.a = g.a_exp + q * kTcABytes;
+        w.b = g.b_exp;
+        w.Q = g.Q;
+        w.N = g.N;
+        w.o_idx = w.o_best = w.o_second = nullptr;
     } else {
         // consecutive CTAs take different query tiles of the SAME split: they stream the same
         // train tiles at the same time, so HBM sees them once and L2 serves the rest
@@ -261,6 +301,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
             unsigned phase = 0, a_phase = 0;
             for (int item = blockIdx.x; item < g.num_items; item += gridDim.x) {
                 const TcWork w = tc_decode(g, item);
+                if (w.ntiles == 0) continue;                   // (stream-K: this CTA has fewer pieces)
                 mbar_wait(bar_a_empty, a_phase ^ 1);           // previous item's MMAs are done with A
                 mbar_expect_tx(bar_a_full, kTcABytes);
                 bulk_load(smem_a, w.a, kTcABytes, bar_a_full);
@@ -287,6 +328,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
             unsigned phase = 0, a_phase = 0;
             for (int item = blockIdx.x; item < g.num_items; item += gridDim.x) {
                 const TcWork w = tc_decode(g, item);
+                if (w.ntiles == 0) continue;
                 mbar_wait(bar_a_full, a_phase);
                 a_phase ^= 1;
                 for (int t = 0; t < w.ntiles; ++t, ++tcount) {
@@ -321,6 +363,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
         int tcount = 0;
         for (int item = blockIdx.x; item < g.num_items; item += gridDim.x) {
             const TcWork w = tc_decode(g, item);
+            if (w.ntiles == 0) continue;
             int best = INT_MIN, second = INT_MIN, best_idx = -1;
             for (int t = 0; t < w.ntiles; ++t, ++tcount) {
                 const int buf = tcount & 1;
@@ -414,6 +457,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
 
 } // namespace
 
+namespace {
+
+// Merge of the stream-K pieces: query tile q was cut into the chunks c_first(q) .. c_last(q), whose
+// partials sit in slots 0 .. c_last - c_first in ascending train order (same rule as
+// merge_partials_kernel: strictly better wins, so the earlier piece keeps ties).
+__global__ void merge_partials_sk_kernel(const Partial* __restrict__ partial, unsigned long long Q, int total_tiles,
+                                         int qtiles, int chunks, int32_t* __restrict__ best_idx,
+                                         int32_t* __restrict__ best_dist, int32_t* __restrict__ second_dist) {
+    const unsigned long long qi = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (qi >= Q) return;
+    const unsigned long long U = static_cast<unsigned long long>(qtiles) * total_tiles, TT = total_tiles, q = qi / kTcM;
+    const int pieces = static_cast<int>(tc_sk_chunk_of((q + 1) * TT - 1, U, chunks) - tc_sk_chunk_of(q * TT, U, chunks)) + 1;
+    int best = 513, second = 513, idx = -1;
+    for (int s = 0; s < pieces; ++s) {
+        const Partial r = partial[static_cast<unsigned long long>(s) * Q + qi];
+        if (r.best_dist < best) {
+            second = min(best, r.second_dist);
+            best = r.best_dist;
+            idx = r.best_idx;
+        } else {
+            second = min(second, r.best_dist);
+        }
+    }
+    if (best_idx) best_idx[qi] = idx;
+    if (best_dist) best_dist[qi] = best;
+    if (second_dist) second_dist[qi] = second;
+}
+
+} // namespace
+
 // The opt-in shared-memory size is a per-device function attribute: remember it per context.
 static int configure_tc(clatch_ctx* ctx) {
     if (!ctx->tc_configured) {
@@ -483,7 +556,22 @@ int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
             }
         }
     }
-    if (int rc = ctx->partial.reserve(sizeof(Partial) * splits * Q)) return rc;
+    // Stream-K instead, when the expanded train set stays in L2 (every CTA streams it at its own phase)
+    // and the equal-share makespan beats whole rounds: U / SMs tile-times + one A reload per piece.
+    const size_t sms = static_cast<size_t>(ctx->sm_count);
+    const size_t units = qtiles * ttiles, chunks = std::min(units, sms);
+    bool streamk = false;
+    size_t sk_pieces_per_cta = 1, sk_pieces_per_qtile = 1;
+    if (tc_expanded_bytes(N) <= (32u << 20) && units > 0 && ctx->match_streamk) {
+        const size_t share = (units + chunks - 1) / chunks;                 // tile-times per CTA
+        sk_pieces_per_cta = (share + ttiles - 2) / ttiles + 1;
+        sk_pieces_per_qtile = (ttiles + units / chunks - 1) / (units / chunks) + 1;
+        const size_t rounds = (qtiles * splits + sms - 1) / sms;
+        const double legacy = rounds * (per_split + 1.5), sk = share + 2.0 * sk_pieces_per_cta;   // (measured: tools/sk_perf.py)
+        streamk = sk < legacy;
+    }
+    const size_t slots = streamk ? sk_pieces_per_qtile : splits;
+    if (int rc = ctx->partial.reserve(sizeof(Partial) * slots * Q)) return rc;
     TcArgs g{};
     g.a_exp = a_exp;
     g.b_exp = ctx->exp_t.as<uint8_t>();
@@ -492,14 +580,21 @@ int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
     g.qtiles = static_cast<int>(qtiles);
     g.total_tiles = static_cast<int>(ttiles);
     g.tiles_per_split = static_cast<int>(per_split);
-    g.num_items = static_cast<int>(qtiles * splits);
+    g.num_items = static_cast<int>(streamk ? chunks * sk_pieces_per_cta : qtiles * splits);
+    g.sk_chunks = streamk ? static_cast<int>(chunks) : 0;
     g.partial = ctx->partial.as<Partial>();
     g.dump = d_dump;
-    const unsigned grid = static_cast<unsigned>(std::min<size_t>(qtiles * splits, ctx->sm_count));
+    const unsigned grid = static_cast<unsigned>(streamk ? chunks : std::min<size_t>(qtiles * splits, ctx->sm_count));
     match_tc_kernel<<<grid, kTcThreads, kTcSmemBytes, stream>>>(g);
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
-    launch_merge_partials(ctx->partial.as<Partial>(), Q, static_cast<int>(splits), 513, d_best_idx, d_best_dist, d_second, stream);
+    if (streamk)
+        merge_partials_sk_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(
+            ctx->partial.as<Partial>(), Q, static_cast<int>(ttiles), static_cast<int>(qtiles), static_cast<int>(chunks),
+            d_best_idx, d_best_dist, d_second);
+    else
+        launch_merge_partials(ctx->partial.as<Partial>(), Q, static_cast<int>(splits), 513, d_best_idx, d_best_dist,
+                              d_second, stream);
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
     return CLATCH_OK;

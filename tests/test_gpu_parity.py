@@ -397,6 +397,36 @@ def test_every_matcher_variant_is_exact(lk, port, variant):
         eng.set_option("match_variant", 3)
 
 
+@pytest.mark.parametrize("shape", [(1, 1), (1, 300), (129, 257), (700, 513), (2000, 2000), (5000, 9000),
+                                   (10000, 10000), (300, 70000)])
+def test_tensor_matcher_partitions_agree(lk, port, shape):
+    """Small problems are cut "stream-K" style (every CTA an equal run of (query tile, train tile)
+    units, pieces merged per query tile), larger ones by (query tile, train split) rounds. Both
+    partitions must give the oracle's top-2 — planted duplicates put ties on piece boundaries."""
+    q_n, t_n = shape
+    rng = np.random.default_rng(q_n * 31 + t_n)
+    train = port.random_descriptors(700 + t_n, t_n)
+    query = port.random_descriptors(900 + q_n, q_n)
+    for j in range(0, q_n, 7):                          # exact copies, each present twice or more in train
+        src = int(rng.integers(0, t_n))
+        query[j] = train[src]
+        train[int(rng.integers(0, t_n))] = train[src]
+        for edge in (255, 256, 511, 512, 1023, 1024):   # ... and right at train-tile boundaries
+            if edge < t_n and rng.random() < 0.3:
+                train[edge] = train[src]
+    eng = lk.get_engine()
+    res = {}
+    try:
+        for sk in (1, 0):
+            eng.set_option("match_streamk", sk)
+            res[sk] = np.stack(eng.match_top2(query, train))
+    finally:
+        eng.set_option("match_streamk", 1)
+    assert np.array_equal(res[0], res[1])
+    rows = np.arange(q_n) if q_n * t_n <= 4_000_000 else np.unique(np.r_[np.arange(0, q_n, 7)[:40], rng.integers(0, q_n, 40)])
+    assert np.array_equal(res[1][:, rows].T, port.knn2_all(query[rows], train))
+
+
 @pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_every_extraction_variant_is_exact(lk, port, variant):
     """All specialised extraction kernels (one window per CTA / four fp64 windows per CTA / four
@@ -418,7 +448,7 @@ def test_every_extraction_variant_is_exact(lk, port, variant):
         eng.set_option("extract_variant", 3)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_trained_pattern_on_every_fast_kernel(lk, port, variant):
     """A trained pattern has the built-in shape (T=512, K=8, 7x7-of-8x8 mask) but other triplets:
     it takes the specialised kernels with a lane placement planned at clatch_set_pattern time
