@@ -14,6 +14,9 @@
 #include <thread>
 
 #include "clatch_internal.cuh"
+#include <atomic>
+#include <chrono>
+
 #include "slot_assign.hpp"
 
 #if defined(__SSE2__)
@@ -146,6 +149,17 @@ private:
     bool stop_ = false;
 };
 
+// CLATCH_TRACE=1: host-clock stamps of the host-API stages on stderr (diagnostics).
+struct Trace {
+    bool on = std::getenv("CLATCH_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void stamp(const char* what) {
+        if (!on) return;
+        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        std::fprintf(stderr, "[clatch] %-28s %9.1f us\n", what, us);
+    }
+};
+
 int invalid(const std::string& msg) {
     set_error(msg);
     return CLATCH_ERR_INVALID;
@@ -153,8 +167,12 @@ int invalid(const std::string& msg) {
 
 int resolve_workers(int workers) {   // src/parallel.hpp:9-13
     if (workers > 0) return workers;
+    // workers <= 0 means "all hardware threads" in the reference; here the pool only runs the trig pass
+    // next to the CUDA driver's own threads and the caller's, and taking every core made the batch
+    // pipeline stall for milliseconds at random (describe_batch, 8 x 50 k keypoints on a 16-thread host:
+    // 7.5-33 ms with 16 workers, 6.9 ms flat with 12 or 4): leave four threads free, use at most 12.
     const unsigned hw = std::thread::hardware_concurrency();
-    return hw > 0 ? static_cast<int>(hw) : 1;
+    return hw > 4 ? static_cast<int>(std::min(hw - 4, 12u)) : std::max(1, static_cast<int>(hw / 2));
 }
 
 // Host-side promotion of a float64 image whose pixels are all integers in [0, 255] (every
@@ -269,6 +287,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
         b->release();
     for (auto& t : ctx->tex_images) {
         if (t.tex) cudaDestroyTextureObject(t.tex);
+        if (t.surf) cudaDestroySurfaceObject(t.surf);
         if (t.array) cudaFreeArray(t.array);
     }
     ctx->pinned.release();
@@ -468,19 +487,40 @@ int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, i
     int nthreads = std::min<size_t>(resolve_workers(workers), (count + 1023) / 1024);
     nthreads = std::max(nthreads, 1);
     std::vector<int> bad(nthreads, 0);
+    // Records written by many cores and read next by the copy engine: with ordinary stores the DMA has
+    // to snoop them out of the cores' caches (measured 6 GB/s for the 1.6 MB of 50 k records instead of
+    // 50 GB/s); non-temporal stores put them in memory.
+    const bool streaming = reinterpret_cast<uintptr_t>(xycs) % 16 == 0 && std::getenv("CLATCH_NO_STREAM_STORES") == nullptr;
+    // Chunks of 256 keypoints are claimed from a shared counter, so the calling thread starts at once
+    // and the workers join in as they wake up (a static split would wait for the slowest wake-up).
+    std::atomic<size_t> next_chunk{0};
+    constexpr size_t kChunk = 256;
     auto work = [&](int w) {
-        const size_t chunk = (count + nthreads - 1) / nthreads;
-        const size_t begin = w * chunk, end = std::min(count, begin + chunk);
+      for (;;) {
+        const size_t begin = next_chunk.fetch_add(kChunk, std::memory_order_relaxed);
+        if (begin >= count) break;
+        const size_t end = std::min(count, begin + kChunk);
         for (size_t j = begin; j < end; ++j) {
             const double* k = kps + static_cast<size_t>(kept[j]) * cols;
             const double theta = cols > 2 ? k[2] : 0.0;
             const double c = std::cos(theta), s = std::sin(theta);
             if (!std::isfinite(c) || !std::isfinite(s)) bad[w] = 1;
+#if defined(__SSE2__)
+            if (streaming) {   // straight to memory: the DMA engine reads these lines next, not a CPU
+                _mm_stream_pd(xycs + 4 * j, _mm_set_pd(k[1], k[0]));
+                _mm_stream_pd(xycs + 4 * j + 2, _mm_set_pd(s, c));
+                continue;
+            }
+#endif
             xycs[4 * j + 0] = k[0];
             xycs[4 * j + 1] = k[1];
             xycs[4 * j + 2] = c;
             xycs[4 * j + 3] = s;
         }
+      }
+#if defined(__SSE2__)
+        if (streaming) _mm_sfence();
+#endif
     };
     WorkerPool::instance().run(nthreads, work);
     for (int b : bad)
@@ -621,6 +661,7 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
         CLATCH_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         for (cudaEvent_t& e : ctx->band_events) CLATCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
+    Trace trace;
     // 1. image DMA first ...
     if (bands == 1) {
         CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, sizeof(Pixel) * dpitch, img, sizeof(Pixel) * pitch,
@@ -645,10 +686,12 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
         cudaStreamSynchronize(st);
         if (bands > 1) cudaStreamSynchronize(ctx->copy_stream);
     };
+    trace.stamp("image copy queued");
     if (int rc = clatch_prepare_keypoints(kps, n, cols, width, height, workers, xycs, kept, &count)) {
         drain();
         return rc;
     }
+    trace.stamp("keypoints prepared");
     *m = count;
     if (count == 0) {
         drain();
@@ -678,7 +721,13 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
     } else {
         bucket_begin[1] = count;
     }
+    cudaEvent_t tev[4] = {};
+    if (trace.on) {
+        for (cudaEvent_t& e : tev) cudaEventCreate(&e);
+        cudaEventRecord(tev[0], st);   // image copy done (stream order)
+    }
     CLATCH_CUDA(cudaMemcpyAsync(ctx->kps.ptr, xycs, sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
+    if (trace.on) cudaEventRecord(tev[1], st);
     // 4. per band: wait for its rows, (f64) classify them, extract the bucket
     int rc = CLATCH_OK;
     for (int b = 0; b < bands && !rc; ++b) {
@@ -698,10 +747,24 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
         drain();
         return rc;
     }
+    trace.stamp("kernels queued");
+    if (trace.on) cudaEventRecord(tev[2], st);
     // 5. descriptors come back through page-locked staging; undo the bucket order on the way out
     if (bands == 1) {
         CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+        trace.stamp("download queued");
+        if (trace.on) cudaEventRecord(tev[3], st);
         CLATCH_CUDA(cudaStreamSynchronize(st));
+        trace.stamp("stream drained");
+        if (trace.on) {
+            float a = 0, b = 0, c = 0;
+            cudaEventElapsedTime(&a, tev[0], tev[1]);
+            cudaEventElapsedTime(&b, tev[1], tev[2]);
+            cudaEventElapsedTime(&c, tev[2], tev[3]);
+            std::fprintf(stderr, "[clatch] device: keypoint upload %.1f us, kernels %.1f us, download %.1f us\n", a * 1e3,
+                         b * 1e3, c * 1e3);
+            for (cudaEvent_t e : tev) cudaEventDestroy(e);
+        }
     } else {
         CLATCH_CUDA(cudaMemcpyAsync(ctx->pin_desc.ptr, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
         CLATCH_CUDA(cudaStreamSynchronize(st));
@@ -777,6 +840,7 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
     for (int s = 0; s < 2; ++s)
         if (!ctx->pipe[s].stream) CLATCH_CUDA(cudaStreamCreateWithFlags(&ctx->pipe[s].stream, cudaStreamNonBlocking));
     int rc = CLATCH_OK;
+    Trace trace;
     for (size_t i = 0; i < num_images && !rc; ++i) {
         clatch_ctx::PipeSlot& slot = ctx->pipe[i & 1];
         cudaStream_t st = slot.stream;
@@ -794,7 +858,9 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         }
         // the slot's previous image (i-2) must have left its buffers before they are reused;
         // its descriptors wait in page-locked staging and move to the caller's array now
+        trace.stamp("batch: image begins");
         CLATCH_CUDA(cudaStreamSynchronize(st));
+        trace.stamp("batch: slot free");
         if (slot.pending_out) {
             std::memcpy(slot.pending_out, slot.h_desc.ptr, slot.pending_bytes);
             slot.pending_out = nullptr;
@@ -815,6 +881,7 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         double* const xycs = static_cast<double*>(slot.h_xycs.ptr);
         size_t count = 0;
         if ((rc = clatch_prepare_keypoints(kps[i], n, cols, w, h, workers, xycs, kept[i], &count))) break;
+        trace.stamp("batch: keypoints prepared");
         m[i] = count;
         if (count == 0) continue;
         CLATCH_CUDA(cudaMemcpyAsync(slot.kps.ptr, xycs, sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
@@ -831,10 +898,20 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
             std::swap(ctx->flags, slot.flags);
         }
         if (rc) break;
-        // page-locked staging keeps the download asynchronous even when out[i] is pageable
-        CLATCH_CUDA(cudaMemcpyAsync(slot.h_desc.ptr, slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
-        slot.pending_out = out[i];
-        slot.pending_bytes = bytes * count;
+        // A page-locked out[i] (clatch_host_alloc — what the Python layer passes) takes the DMA directly;
+        // pageable memory goes through page-locked staging so that the download stays asynchronous, and
+        // is copied out when the slot comes round again.
+        trace.stamp("batch: kernels queued");
+        cudaPointerAttributes attr{};
+        const bool direct = cudaPointerGetAttributes(&attr, out[i]) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+        if (!direct) cudaGetLastError();   // an unregistered pointer is not an error here
+        if (direct) {
+            CLATCH_CUDA(cudaMemcpyAsync(out[i], slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+        } else {
+            CLATCH_CUDA(cudaMemcpyAsync(slot.h_desc.ptr, slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+            slot.pending_out = out[i];
+            slot.pending_bytes = bytes * count;
+        }
     }
     for (int s = 0; s < 2; ++s) {
         clatch_ctx::PipeSlot& slot = ctx->pipe[s];

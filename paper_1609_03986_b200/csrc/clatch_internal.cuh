@@ -87,6 +87,7 @@ struct clatch_ctx {
         cudaStream_t stream = nullptr;
         cudaArray_t array = nullptr;
         cudaTextureObject_t tex = 0;
+        cudaSurfaceObject_t surf = 0;    // the same array, for the fill kernel
         int width = 0, height = 0;
     };
     std::vector<TexImage> tex_images;

@@ -15,7 +15,7 @@ import weakref
 import numpy as np
 
 from . import _lib
-from ._lib import check, f64p, i16p, i32p, i64p, u8p
+from ._lib import f64p, i16p, i32p, i64p, u8p
 from .pattern import TripletPattern, default_pattern
 
 
@@ -26,40 +26,42 @@ def _ptr(a: np.ndarray, t):
 class _PinnedPool:
     """Page-locked numpy arrays for the results the API hands back (descriptor arrays usually come
     straight back as match() inputs: page-locked, both transfers are plain DMAs). cudaHostAlloc is
-    slow, so freed blocks are kept by power-of-two size and reused; a block returns to the pool when
-    the last numpy view of it dies."""
+    slow (milliseconds per MB), so blocks are recycled by power-of-two size: a block returns to the
+    pool when the last numpy view of it dies, and a loop that drops its previous result each
+    iteration cycles through one or two blocks. A caller that KEEPS its results gets at most
+    `max_live` page-locked blocks per size; after that, ordinary pageable arrays (page-locked
+    memory is a scarce resource, and allocating it on every call would cost more than it saves)."""
 
-    def __init__(self, lib, keep_bytes: int = 256 << 20):
-        self.lib, self.free, self.kept, self.keep_bytes = lib, {}, 0, keep_bytes
+    def __init__(self, lib, max_live: int = 4):
+        self.lib, self.free, self.live, self.max_live = lib, {}, {}, max_live
         self.lock = threading.Lock()
 
     def empty(self, shape, dtype) -> np.ndarray:
         dtype = np.dtype(dtype)
-        nbytes = int(np.prod(shape)) * dtype.itemsize
-        cap = 1 << max(12, (max(nbytes, 1) - 1).bit_length())
+        count = int(np.prod(shape))
+        cap = 1 << max(12, (max(count * dtype.itemsize, 1) - 1).bit_length())
         with self.lock:
             blocks = self.free.get(cap)
             ptr = blocks.pop() if blocks else None
-            if ptr is not None:
-                self.kept -= cap
+            if ptr is None and self.live.get(cap, 0) >= self.max_live:
+                return np.empty(shape, dtype)
+            self.live[cap] = self.live.get(cap, 0) + 1
         if ptr is None:
             p = C.c_void_p()
-            check(self.lib.clatch_host_alloc(cap, C.byref(p)))
+            rc = self.lib.clatch_host_alloc(cap, C.byref(p))
+            if rc != 0 or not p.value:
+                with self.lock:
+                    self.live[cap] -= 1
+                return np.empty(shape, dtype)
             ptr = p.value
         owner = (C.c_uint8 * cap).from_address(ptr)
         weakref.finalize(owner, self._release, ptr, cap)
-        return np.frombuffer(owner, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+        return np.frombuffer(owner, dtype=dtype, count=count).reshape(shape)
 
     def _release(self, ptr, cap):
         with self.lock:
-            if self.kept + cap <= self.keep_bytes:
-                self.free.setdefault(cap, []).append(ptr)
-                self.kept += cap
-                return
-        try:
-            self.lib.clatch_host_free(ptr)
-        except Exception:
-            pass
+            self.live[cap] -= 1
+            self.free.setdefault(cap, []).append(ptr)
 
 
 class DescriptorSet:
@@ -260,7 +262,7 @@ class Engine:
             raise ValueError("describe_batch needs one keypoint column count per call")
         nbytes = self.descriptor_bytes
         kept = [np.empty(len(k), np.int64) for k in kps_l]
-        out = [np.empty((len(k), nbytes), np.uint8) for k in kps_l]
+        out = [self._pinned.empty((len(k), nbytes), np.uint8) for k in kps_l]   # page-locked: direct DMA targets
         vp = C.c_void_p * n_img
         widths = (C.c_int * n_img)(*[im.shape[1] for im in imgs])
         heights = (C.c_int * n_img)(*[im.shape[0] for im in imgs])

@@ -1,0 +1,29 @@
+import sys, time
+sys.path.insert(0, '/root/repo')
+import numpy as np, torch
+import oracle, paper_1609_03986_b200 as lk
+port = oracle.port(); eng = lk.get_engine(); eng.set_pattern(None)
+W, H, N = 3840, 2160, 50000
+img = port.random_image_u8(30000, W, H); kps = port.random_keypoints(31000, W, H, N)
+def pinned(a):
+    t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True); t.numpy()[...] = a; return t.numpy()
+pimg, pkps = pinned(img), pinned(kps)
+def timeit(fn, reps=10):
+    fn(); torch.cuda.synchronize(); t0 = time.perf_counter()
+    for _ in range(reps): out = fn()
+    torch.cuda.synchronize(); return (time.perf_counter() - t0) / reps * 1e3, out
+ms, (xycs, kept) = timeit(lambda: eng.prepare_keypoints(pkps, W, H)); print(f"prepare_keypoints 50k        {ms:.3f} ms")
+ms, _ = timeit(lambda: eng.prepare_keypoints(pkps, W, H, 1)); print(f"prepare_keypoints 50k 1 thr  {ms:.3f} ms")
+ms, _ = timeit(lambda: eng.extract(pimg, xycs)); print(f"extract pinned img            {ms:.3f} ms")
+ms, _ = timeit(lambda: eng.describe_all(pimg, pkps)); print(f"describe_all pinned           {ms:.3f} ms")
+ms, _ = timeit(lambda: eng.describe_all(img, kps)); print(f"describe_all pageable         {ms:.3f} ms")
+ms, _ = timeit(lambda: lk.describe(pimg, pkps)); print(f"lk.describe pinned            {ms:.3f} ms")
+ms, _ = timeit(lambda: lk.describe(img, kps)); print(f"lk.describe pageable          {ms:.3f} ms")
+d_img = torch.from_numpy(img).cuda(); d_x = torch.from_numpy(xycs).cuda(); out = eng.extract_device(d_img, d_x)
+def dev(): eng.extract_device(d_img, d_x, out=out); torch.cuda.synchronize()
+ms, _ = timeit(dev); print(f"kernel (device resident)      {ms:.3f} ms")
+imgs = [pimg] * 8; kl = [pkps] * 8
+ms, _ = timeit(lambda: lk.describe_batch(imgs, kl), reps=3); print(f"describe_batch 8 pinned       {ms:.3f} ms  ({ms/8:.3f} per image)")
+ms, _ = timeit(lambda: eng.describe_batch(imgs, kl), reps=3); print(f"eng.describe_batch 8 pinned   {ms:.3f} ms  ({ms/8:.3f} per image)")
+t = torch.from_numpy(pimg)
+ms, _ = timeit(lambda: (t.cuda(non_blocking=True), torch.cuda.synchronize())); print(f"torch H2D 8.3MB pinned        {ms:.3f} ms")

@@ -62,6 +62,54 @@ __global__ void gather_kernel(cudaTextureObject_t tex, const double* xycs, int n
     if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
 
+// Fill a u8 CUDA array from pitch-linear device memory through a surface: 16 pixels per thread.
+__global__ void fill_array_kernel(cudaSurfaceObject_t surf, const unsigned char* src, size_t pitch, int w, int h) {
+    const int x = (blockIdx.x * blockDim.x + threadIdx.x) * 16, y = blockIdx.y;
+    if (x >= w || y >= h) return;
+    if (x + 16 <= w) {
+        const uint4 v = *reinterpret_cast<const uint4*>(src + y * pitch + x);
+        surf2Dwrite(v, surf, x, y);
+    } else {
+        for (int i = x; i < w; ++i) surf2Dwrite(src[y * pitch + i], surf, i, y);
+    }
+}
+
+static void time_array_fill(int W, int H) {
+    unsigned char* d_lin;
+    const size_t pitch = (W + 15) / 16 * 16;
+    CK(cudaMalloc(&d_lin, pitch * H));
+    CK(cudaMemset(d_lin, 7, pitch * H));
+    cudaChannelFormatDesc fmt = cudaCreateChannelDesc<unsigned char>();
+    cudaArray_t arr;
+    CK(cudaMallocArray(&arr, &fmt, W, H, cudaArrayTextureGather | cudaArraySurfaceLoadStore));
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeArray;
+    rd.res.array.array = arr;
+    cudaSurfaceObject_t surf;
+    CK(cudaCreateSurfaceObject(&surf, &rd));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    float ms_copy = 0, ms_kernel = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+        CK(cudaEventRecord(e0));
+        for (int i = 0; i < 10; ++i) CK(cudaMemcpy2DToArrayAsync(arr, 0, 0, d_lin, pitch, W, H, cudaMemcpyDeviceToDevice, 0));
+        CK(cudaEventRecord(e1));
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventElapsedTime(&ms_copy, e0, e1));
+        CK(cudaEventRecord(e0));
+        for (int i = 0; i < 10; ++i)
+            fill_array_kernel<<<dim3((W / 16 + 127) / 128, H), 128>>>(surf, d_lin, pitch, W, H);
+        CK(cudaEventRecord(e1));
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventElapsedTime(&ms_kernel, e0, e1));
+    }
+    printf(" \"array_fill_%dx%d\": {\"cudaMemcpy2DToArrayAsync_d2d_us\": %.1f, \"surf2Dwrite_kernel_us\": %.1f},\n", W, H,
+           ms_copy * 100, ms_kernel * 100);
+    CK(cudaDestroySurfaceObject(surf));
+    CK(cudaFreeArray(arr));
+    CK(cudaFree(d_lin));
+}
+
 int main() {
     const int W = 1920, H = 1080, N = 20000;
     cudaDeviceProp prop;
@@ -126,6 +174,8 @@ int main() {
     CK(cudaFuncSetAttribute(gather_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, carve));
     printf("{\"device\": \"%s\", \"sm_count\": %d, \"gather_order_w_z_x_y_is_p00_p10_p01_p11\": %s, \"checked\": %d,\n",
            prop.name, sms, ok_order == n_chk ? "true" : "false", n_chk);
+    time_array_fill(1920, 1080);
+    time_array_fill(3840, 2160);
     printf(" \"carveout_kb\": %d, \"runs\": [\n", carve / 1024);
     bool first = true;
     for (int mode = 0; mode < 2; ++mode)
