@@ -25,15 +25,15 @@ def _ptr(a: np.ndarray, t):
 
 class _PinnedPool:
     """Page-locked numpy arrays for the results the API hands back (descriptor arrays usually come
-    straight back as match() inputs: page-locked, both transfers are plain DMAs). cudaHostAlloc is
-    slow (milliseconds per MB), so blocks are recycled by power-of-two size: a block returns to the
-    pool when the last numpy view of it dies, and a loop that drops its previous result each
-    iteration cycles through one or two blocks. A caller that KEEPS its results gets at most
-    `max_live` page-locked blocks per size; after that, ordinary pageable arrays (page-locked
-    memory is a scarce resource, and allocating it on every call would cost more than it saves)."""
+    straight back as match() inputs: page-locked, both transfers are plain DMAs, and a batch call's
+    downloads never stall its pipeline). cudaHostAlloc is slow (about 3 ms per MB on the B200 hosts),
+    so blocks are recycled by power-of-two size: a block returns to the pool when the last numpy
+    view of it dies, and a loop that drops its previous results cycles through the same blocks.
+    A caller that KEEPS its results is served page-locked memory up to `max_live_bytes`; after
+    that, ordinary pageable arrays (page-locked memory is a scarce resource)."""
 
-    def __init__(self, lib, max_live: int = 4):
-        self.lib, self.free, self.live, self.max_live = lib, {}, {}, max_live
+    def __init__(self, lib, max_live_bytes: int = 256 << 20):
+        self.lib, self.free, self.live_bytes, self.max_live_bytes = lib, {}, 0, max_live_bytes
         self.lock = threading.Lock()
 
     def empty(self, shape, dtype) -> np.ndarray:
@@ -43,15 +43,15 @@ class _PinnedPool:
         with self.lock:
             blocks = self.free.get(cap)
             ptr = blocks.pop() if blocks else None
-            if ptr is None and self.live.get(cap, 0) >= self.max_live:
+            if ptr is None and self.live_bytes + cap > self.max_live_bytes:
                 return np.empty(shape, dtype)
-            self.live[cap] = self.live.get(cap, 0) + 1
+            self.live_bytes += cap
         if ptr is None:
             p = C.c_void_p()
             rc = self.lib.clatch_host_alloc(cap, C.byref(p))
             if rc != 0 or not p.value:
                 with self.lock:
-                    self.live[cap] -= 1
+                    self.live_bytes -= cap
                 return np.empty(shape, dtype)
             ptr = p.value
         owner = (C.c_uint8 * cap).from_address(ptr)
@@ -60,7 +60,7 @@ class _PinnedPool:
 
     def _release(self, ptr, cap):
         with self.lock:
-            self.live[cap] -= 1
+            self.live_bytes -= cap
             self.free.setdefault(cap, []).append(ptr)
 
 

@@ -42,5 +42,10 @@ timeout 300 python tools/extract_perf.py > "$OUT/extract_perf.log" 2>&1
 timeout 900 python tools/run_configs.py > "$OUT/configs.json" 2> "$OUT/configs.err"
 timeout 120 ./tools/tex_probe > "$OUT/tex_probe.json" 2>&1
 timeout 120 ./tools/lat_probe > "$OUT/lat_probe.json" 2>&1
+timeout 300 python tools/sk_perf.py > "$OUT/sk_perf.log" 2>&1
+timeout 600 python tools/cfg3_breakdown.py > "$OUT/cfg3_breakdown.log" 2>&1
+echo "== compute-sanitizer"
+timeout 900 compute-sanitizer --tool memcheck python tools/sanitize.py > "$OUT/sanitize_memcheck.log" 2>&1; tail -2 "$OUT/sanitize_memcheck.log"
+timeout 900 compute-sanitizer --tool racecheck python tools/sanitize.py > "$OUT/sanitize_racecheck.log" 2>&1; tail -2 "$OUT/sanitize_racecheck.log"
 fi
 ls -la "$OUT"
