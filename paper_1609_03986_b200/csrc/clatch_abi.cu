@@ -283,7 +283,8 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
     }
     for (DeviceBuffer* b : {&ctx->img, &ctx->kps, &ctx->desc, &ctx->q, &ctx->t, &ctx->res,
                             &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->items, &ctx->scores, &ctx->counts, &ctx->det, &ctx->pattern.slots, &ctx->pattern.slots_quad,
-                            &ctx->pattern.slots_f8, &ctx->extract_stats, &ctx->pattern.triplets})
+                            &ctx->pattern.slots_f8, &ctx->extract_stats, &ctx->filt_pairs, &ctx->filt_rows, &ctx->filt_out,
+                            &ctx->filt_counts, &ctx->pattern.triplets})
         b->release();
     for (auto& t : ctx->tex_images) {
         if (t.tex) cudaDestroyTextureObject(t.tex);
@@ -331,6 +332,10 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
     if (std::strcmp(key, "extract_variant") == 0) {
         if (value < 0 || value > 4) return invalid("extract_variant must be 0..4");
         ctx->extract_variant = value;
+        return CLATCH_OK;
+    }
+    if (std::strcmp(key, "pairs_filter_on_device") == 0) {   // batched set pairs: filter pass on the device (1) or host (0)
+        ctx->pairs_filter_on_device = value != 0;
         return CLATCH_OK;
     }
     if (std::strcmp(key, "match_streamk") == 0) {   // tensor matcher: stream-K partition for small problems
@@ -1058,10 +1063,50 @@ int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t
     cudaStream_t st = ctx->stream;
     CLATCH_CUDA(cudaMemcpyAsync(ctx->items.ptr, table.data(), sizeof(TcItem) * table.size(), cudaMemcpyHostToDevice, st));
     if (int rc = launch_match_tc_items(ctx, ctx->items.as<TcItem>(), table.size(), st)) return rc;
+    if (host == nullptr) {   // results stay on the device (filtered there)
+        CLATCH_CUDA(cudaStreamSynchronize(st));   // keeps `table` alive until the H2D copy is done
+        return CLATCH_OK;
+    }
     if (int rc = ctx->pinned.reserve(sizeof(int32_t) * std::max<size_t>(total, 1))) return rc;
     *host = static_cast<int32_t*>(ctx->pinned.ptr);
     CLATCH_CUDA(cudaMemcpyAsync(*host, r, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, st));
     CLATCH_CUDA(cudaStreamSynchronize(st));   // also keeps `table` alive until the H2D copy is done
+    return CLATCH_OK;
+}
+
+// The filter pass of a batch on the device: kept rows of all pairs back to back in page-locked memory
+// (*rows), row offsets per pair in offsets[0..count]. Only the surviving rows cross the bus.
+int filter_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t* pairs, size_t first, size_t count,
+                      bool cross_check, const std::vector<size_t>& pair_offset, int has_ratio, double ratio,
+                      int has_max, int max_distance, const int32_t** rows, std::vector<unsigned long long>& offsets) {
+    std::vector<FilterPair> table(count);
+    const int32_t* r = ctx->res.as<int32_t>();
+    unsigned long long probes = 0;
+    for (size_t p = 0; p < count; ++p) {
+        const size_t n = sets[pairs[2 * (first + p)]]->n;
+        const int32_t* base = r + pair_offset[p];
+        table[p] = {base, base + n, base + 2 * n, cross_check ? base + 3 * n : nullptr, static_cast<unsigned>(n), 0, probes};
+        probes += n;
+    }
+    if (int rc = ctx->filt_pairs.reserve(sizeof(FilterPair) * count)) return rc;
+    if (int rc = ctx->filt_rows.reserve(sizeof(int32_t) * 4 * std::max<unsigned long long>(probes, 1))) return rc;
+    if (int rc = ctx->filt_out.reserve(sizeof(int32_t) * 4 * std::max<unsigned long long>(probes, 1))) return rc;
+    if (int rc = ctx->filt_counts.reserve(sizeof(unsigned) * count + sizeof(unsigned long long) * (count + 2))) return rc;
+    unsigned long long* d_offsets = ctx->filt_counts.as<unsigned long long>();
+    unsigned* d_kept = reinterpret_cast<unsigned*>(d_offsets + count + 2);
+    cudaStream_t st = ctx->stream;
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->filt_pairs.ptr, table.data(), sizeof(FilterPair) * count, cudaMemcpyHostToDevice, st));
+    if (int rc = launch_filter_pairs(ctx, ctx->filt_pairs.as<FilterPair>(), count, has_ratio, ratio, has_max, max_distance,
+                                     ctx->filt_rows.as<int32_t>(), d_kept, d_offsets, ctx->filt_out.as<int32_t>(), st))
+        return rc;
+    offsets.resize(count + 1);
+    CLATCH_CUDA(cudaMemcpyAsync(offsets.data(), d_offsets, sizeof(unsigned long long) * (count + 1), cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));   // (also keeps `table` alive until its upload is done)
+    const unsigned long long total = offsets[count];
+    if (int rc = ctx->pinned.reserve(sizeof(int32_t) * 4 * std::max<unsigned long long>(total, 1))) return rc;
+    CLATCH_CUDA(cudaMemcpyAsync(ctx->pinned.ptr, ctx->filt_out.ptr, sizeof(int32_t) * 4 * total, cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    *rows = static_cast<const int32_t*>(ctx->pinned.ptr);
     return CLATCH_OK;
 }
 
@@ -1189,6 +1234,21 @@ int clatch_match_set_pairs(clatch_ctx* ctx, const clatch_set* const* sets, size_
             if (count > 0 && ints + need > kChunkInts) break;
             ints += need;
             ++count;
+        }
+        if (ctx->pairs_filter_on_device) {
+            // top-2 results stay on the device; the filter pass (src/match.cpp:69-79) runs there too
+            if (int rc = run_pair_batch(ctx, sets, pairs, first, count, cross_check != 0, nullptr, pair_offset)) return rc;
+            const int32_t* rows = nullptr;
+            std::vector<unsigned long long> off;
+            if (int rc = filter_pair_batch(ctx, sets, pairs, first, count, cross_check != 0, pair_offset, has_ratio, ratio,
+                                           has_max, max_distance, &rows, off))
+                return rc;
+            if (rows_out + off[count] > cap_rows) return invalid("clatch_match_set_pairs: cap_rows too small");
+            std::memcpy(out + 4 * rows_out, rows, sizeof(int32_t) * 4 * off[count]);
+            for (size_t p = 0; p < count; ++p) offsets[first + p + 1] = rows_out + off[p + 1];
+            rows_out += off[count];
+            first += count;
+            continue;
         }
         if (int rc = run_pair_batch(ctx, sets, pairs, first, count, cross_check != 0, &host, pair_offset)) return rc;
         // filter pass per pair (src/match.cpp:69-79): parallel into per-pair scratch, then compact in order

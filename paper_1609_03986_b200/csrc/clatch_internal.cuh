@@ -93,10 +93,12 @@ struct clatch_ctx {
     std::vector<TexImage> tex_images;
     bool extract_stats_on = false;           // count exact recomputes (clatch_extract_stats)
     clatch::DeviceBuffer extract_stats;      // 2 x u64
+    bool pairs_filter_on_device = true;   // clatch_match_set_pairs: ratio / max / cross-check decisions on the device
     bool match_streamk = true;     // tensor matcher: equal-share partition for small problems (set_option "match_streamk")
     int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
     // scratch for the host-buffer entry points
     clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t, items, scores, counts, det;
+    clatch::DeviceBuffer filt_pairs, filt_rows, filt_out, filt_counts;   // on-device filter pass of batched set pairs
     std::vector<double> host_xycs;   // describe_all staging
     clatch::PinnedBuffer pinned;     // D2H staging for batched pair results
     clatch::PinnedBuffer pin_xycs, pin_desc;   // describe_all staging (banded upload path)
@@ -158,6 +160,18 @@ struct TcItem {    // one CTA of the tensor-core matcher in batched mode: 128 qu
     int32_t* best_dist;
     int32_t* second_dist;
 };
+struct FilterPair {   // one set pair of the on-device filter pass
+    const int32_t* best_idx;       // forward top-2 of the pair's probes
+    const int32_t* best_dist;
+    const int32_t* second_dist;
+    const int32_t* reverse_best;   // reverse pass (cross-check) or null
+    unsigned n;                    // probes
+    unsigned pad;
+    unsigned long long out_base;   // first row of this pair's worst-case slice
+};
+int launch_filter_pairs(clatch_ctx* ctx, const FilterPair* d_pairs, size_t count, int has_ratio, double ratio, int has_max,
+                        int max_distance, int32_t* d_rows, unsigned* d_kept, unsigned long long* d_offsets,
+                        int32_t* d_out, cudaStream_t stream);
 size_t tc_expanded_bytes(size_t rows);
 int tc_query_tiles(size_t rows);
 int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t* d_out, cudaStream_t stream);

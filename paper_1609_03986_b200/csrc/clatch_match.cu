@@ -254,6 +254,112 @@ __global__ void match_generic_kernel(const uint8_t* __restrict__ queries, unsign
 
 } // namespace
 
+// ---- filter pass of match_brute_force on the device (src/match.cpp:69-79), for batched set pairs ----
+// One CTA per pair walks its probes in order: ratio test in double exactly as the reference writes
+// it (best < ratio * second, int -> double), inclusive max distance, cross-check against the
+// reverse pass; kept rows [probe, gallery, distance, second] are written in ascending probe order
+// to the pair's own (worst-case sized) slice, and the count is recorded. A one-block scan and a
+// copy kernel then pack the slices back to back, so only the surviving rows cross the bus.
+__global__ void __launch_bounds__(256) filter_pairs_kernel(const FilterPair* __restrict__ pairs, int has_ratio,
+                                                           double ratio, int has_max, int max_distance,
+                                                           int4* __restrict__ rows, unsigned* __restrict__ kept) {
+    const FilterPair fp = pairs[blockIdx.x];
+    __shared__ unsigned s_warp[8];
+    __shared__ unsigned s_total;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned base = 0;
+    int4* const out = rows + fp.out_base;
+    for (unsigned p0 = 0; p0 < fp.n; p0 += 256) {
+        const unsigned p = p0 + threadIdx.x;
+        bool keep = false;
+        int best = 0, second = 0, idx = 0;
+        if (p < fp.n) {
+            best = fp.best_dist[p];
+            second = fp.second_dist[p];
+            idx = fp.best_idx[p];
+            keep = true;
+            if (has_ratio && !(static_cast<double>(best) < __dmul_rn(ratio, static_cast<double>(second)))) keep = false;
+            if (keep && has_max && best > max_distance) keep = false;
+            if (keep && fp.reverse_best != nullptr && fp.reverse_best[idx] != static_cast<int>(p)) keep = false;
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_warp[warp] = __popc(ballot);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned run = 0;
+            for (int w = 0; w < 8; ++w) {
+                const unsigned c = s_warp[w];
+                s_warp[w] = run;
+                run += c;
+            }
+            s_total = run;
+        }
+        __syncthreads();
+        if (keep) out[base + s_warp[warp] + __popc(ballot & ((1u << lane) - 1u))] = make_int4(static_cast<int>(p), idx, best, second);
+        base += s_total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) kept[blockIdx.x] = base;
+}
+
+// Exclusive scan of the per-pair counts (a few thousand at most): one block, 1024 entries per step.
+__global__ void __launch_bounds__(1024) scan_counts_kernel(const unsigned* __restrict__ kept, unsigned count,
+                                                           unsigned long long* __restrict__ offsets) {
+    __shared__ unsigned s_w[32];
+    __shared__ unsigned long long s_run;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_run = 0;
+    __syncthreads();
+    for (unsigned i0 = 0; i0 < count; i0 += 1024) {
+        const unsigned i = i0 + tid;
+        const unsigned v = i < count ? kept[i] : 0;
+        unsigned x = v;
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned t = s_w[lane];
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, t, d);
+                if (lane >= d) t += y;
+            }
+            s_w[lane] = t;
+        }
+        __syncthreads();
+        const unsigned warp_before = warp ? s_w[warp - 1] : 0;
+        const unsigned long long run = s_run;
+        if (i < count) offsets[i] = run + warp_before + x - v;
+        __syncthreads();   // everyone has read s_run and s_w
+        if (tid == 1023) s_run = run + warp_before + x;
+        __syncthreads();
+    }
+    if (tid == 0) offsets[count] = s_run;
+}
+
+__global__ void compact_rows_kernel(const FilterPair* __restrict__ pairs, const int4* __restrict__ rows,
+                                    const unsigned long long* __restrict__ offsets, int4* __restrict__ out) {
+    const FilterPair fp = pairs[blockIdx.x];
+    const unsigned long long begin = offsets[blockIdx.x], n = offsets[blockIdx.x + 1] - begin;
+    for (unsigned long long i = threadIdx.x; i < n; i += blockDim.x) out[begin + i] = rows[fp.out_base + i];
+}
+
+int launch_filter_pairs(clatch_ctx* ctx, const FilterPair* d_pairs, size_t count, int has_ratio, double ratio, int has_max,
+                        int max_distance, int32_t* d_rows, unsigned* d_kept, unsigned long long* d_offsets,
+                        int32_t* d_out, cudaStream_t stream) {
+    if (count == 0) return CLATCH_OK;
+    filter_pairs_kernel<<<static_cast<unsigned>(count), 256, 0, stream>>>(d_pairs, has_ratio, ratio, has_max, max_distance,
+                                                                           reinterpret_cast<int4*>(d_rows), d_kept);
+    scan_counts_kernel<<<1, 1024, 0, stream>>>(d_kept, static_cast<unsigned>(count), d_offsets);
+    compact_rows_kernel<<<static_cast<unsigned>(count), 256, 0, stream>>>(d_pairs, reinterpret_cast<const int4*>(d_rows),
+                                                                          d_offsets, reinterpret_cast<int4*>(d_out));
+    ctx->launches += 3;
+    CLATCH_CUDA(cudaGetLastError());
+    return CLATCH_OK;
+}
+
 void launch_merge_partials(const Partial* partial, unsigned long long Q, int splits, int sentinel,
                            int32_t* best_idx, int32_t* best_dist, int32_t* second_dist, cudaStream_t stream) {
     merge_partials_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(partial, Q, splits, sentinel,

@@ -574,11 +574,14 @@ def test_float64_promotion_edges(lk, port, promote):
 
 # ------------------------------------------------------ resident sets, batched pairs ----
 
-def test_resident_sets_and_batched_pairs(lk, port):
+@pytest.mark.parametrize("filter_on_device", [1, 0])
+def test_resident_sets_and_batched_pairs(lk, port, filter_on_device):
     """cfg5 shape: every image against every other image through resident descriptor sets.
-    Each pair must equal the reference's match_brute_force with the same filters."""
+    Each pair must equal the reference's match_brute_force with the same filters, whether the
+    filter pass (ratio in double, inclusive max distance, cross-check) runs on the device or the host."""
     torch = pytest.importorskip("torch")
     eng = lk.get_engine()
+    eng.set_option("pairs_filter_on_device", filter_on_device)
     sizes = [300, 1, 257, 128, 1000]
     raw = [port.random_descriptors(900 + i, n, 64) for i, n in enumerate(sizes)]
     raw[2][5] = raw[0][7]                 # cross-image duplicates -> zero distances and ties
@@ -588,7 +591,8 @@ def test_resident_sets_and_batched_pairs(lk, port):
             eng.create_set(torch.from_numpy(raw[3]).cuda()), eng.create_set(raw[4])]
     assert [len(s) for s in sets] == sizes
     pairs = [(i, j) for i in range(5) for j in range(5) if i != j]
-    for kw in ({}, {"ratio": 0.9}, {"cross_check": True}, {"ratio": 0.85, "cross_check": True, "max_distance": 240}):
+    for kw in ({}, {"ratio": 0.9}, {"cross_check": True}, {"ratio": 0.85, "cross_check": True, "max_distance": 240},
+               {"ratio": 1.0, "max_distance": 0}, {"ratio": float("inf")}, {"ratio": float("nan")}, {"max_distance": -1}):
         got = eng.match_set_pairs(sets, pairs, **kw)
         for (i, j), g in zip(pairs, got):
             assert np.array_equal(g, port.match(raw[i], raw[j], **kw)), (i, j, kw)
@@ -607,6 +611,7 @@ def test_resident_sets_and_batched_pairs(lk, port):
     assert sorted(res) == sharded.pairs_for_rank(5, 0, 1)
     for (i, j), m in res.items():
         assert np.array_equal(m, port.match(raw[i], raw[j], ratio=0.9, cross_check=True))
+    eng.set_option("pairs_filter_on_device", 1)
 
 
 def test_describe_batch_matches_per_image_calls(lk, port):

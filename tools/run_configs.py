@@ -149,6 +149,6 @@ same = all(np.array_equal(batched[p], results[p]) for p in pairs)
 out["cfg5"]["batched"] = {"s": t_b, "pairs_per_s": len(pairs) / t_b, "compares_per_s_incl_cross_check": compares / t_b,
                           "identical_to_per_pair_path": bool(same),
                           "note": "resident sets: each image uploaded + expanded once, all pairs in one launch; "
-                                  "time includes set creation, D2H of all top-2 triples and the host filter pass"}
+                                  "time includes set creation, the on-device filter pass and the D2H of the surviving rows"}
 print("cfg5", out["cfg5"], file=sys.stderr, flush=True)
 print(json.dumps(out))
