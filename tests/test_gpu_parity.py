@@ -614,6 +614,31 @@ def test_resident_sets_and_batched_pairs(lk, port, filter_on_device):
     eng.set_option("pairs_filter_on_device", 1)
 
 
+def test_result_arrays_are_never_recycled_while_alive(lk, port):
+    """describe() hands back page-locked arrays from a recycling pool: a block may be reused only
+    after the last view of it is gone. Results that are kept must keep their contents."""
+    import gc
+    w, h = 320, 240
+    imgs = [port.random_image_u8(4000 + i, w, h) for i in range(12)]
+    kps = port.random_keypoints(4100, w, h, 400)
+    want = [port.describe_all(im.astype(np.float64), kps)[1] for im in imgs]
+    kept = []
+    for i, im in enumerate(imgs):                  # keep every other result (through a slice view), drop the rest
+        d = lk.describe(im, kps)[1]
+        assert np.array_equal(d, want[i])
+        if i % 2 == 0:
+            kept.append((i, d[3:]))
+        del d
+        gc.collect()
+    for i, view in kept:
+        assert np.array_equal(view, want[i][3:]), i
+    batch = lk.describe_batch(imgs[:5], [kps] * 5)
+    for i, view in kept:
+        assert np.array_equal(view, want[i][3:]), i
+    for i, (_, d) in enumerate(batch):
+        assert np.array_equal(d, want[i])
+
+
 def test_describe_batch_matches_per_image_calls(lk, port):
     """cfg3 shape: several images per GPU through the pipelined batch call."""
     imgs, kps = [], []
