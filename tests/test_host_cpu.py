@@ -164,3 +164,36 @@ def test_product_never_imports_the_oracle():
         text = path.read_text()
         assert "import oracle" not in text and "from oracle" not in text, path
         assert "latch_oracle" not in text and "liblatch_ref" not in text, path
+
+
+def test_embedded_lane_placement_matches_the_builtin_table():
+    """csrc/default_plan_f8.inc (generated by tools/gen_default_plan.py) is the filtered / pipelined
+    kernels' lane placement of the built-in pattern: every slot must carry the window offsets
+    (y * 65 + x) of one triplet, companions possibly swapped (bit 15), and the slots must be a
+    permutation of the 512 triplets. A stale file would silently compute the wrong bits."""
+    import re
+    from pathlib import Path
+
+    import numpy as np
+
+    root = Path(__file__).resolve().parent.parent
+    text = (root / "paper_1609_03986_b200" / "csrc" / "default_plan_f8.inc").read_text()
+    stride = int(re.search(r"kDefaultPlanStride = (\d+)", text).group(1))
+    rows = re.findall(r"\{(\d+), (\d+), (\d+), 0x([0-9a-f]{4})\}", text)
+    assert len(rows) == 512 and stride == 65
+    trip = np.load(root / "paper_1609_03986_b200" / "data" / "default_pattern.npz")["triplets"].astype(int)
+    off = trip[:, 1::2] * stride + trip[:, 0::2]            # (512, 3): anchor, companion b, companion c
+    seen = set()
+    for a, b, c, w in rows:
+        w = int(w, 16)
+        t, swapped = w & 0x7FFF, w >> 15
+        assert t not in seen
+        seen.add(t)
+        want = (off[t, 0], off[t, 2], off[t, 1]) if swapped else tuple(off[t])
+        assert (int(a), int(b), int(c)) == tuple(int(v) for v in want), t
+    assert seen == set(range(512))
+    # conflict-freeness claim of the header: per group of 8 slots, residues mod 8 of each load
+    slots = np.array([[int(a), int(b), int(c)] for a, b, c, _ in rows]).reshape(64, 8, 3) % 8
+    worst = sum(np.bincount(slots[g, :, k], minlength=8).max() for g in range(64) for k in range(3)) / 192.0
+    stated = float(re.search(r"kDefaultPlanDegree = ([0-9.]+)", text).group(1))
+    assert abs(worst - stated) < 1e-6 and worst < 1.2
