@@ -198,7 +198,7 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------- our arm ----
@@ -232,9 +232,6 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     use_dist = "RANK" in os.environ          # under torchrun (any world size) exercise the NCCL path
     if use_dist:
-        # NCCL_DEBUG=VERSION/INFO writes to stdout; keep stdout to the one JSON line
-        if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", "INFO", "TRACE"):
-            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -435,12 +432,36 @@ def run_ours(args):
         "roofline": roofline, "pipe_roofline": pipe_roofline, "kernels": kernels, "cpu_baseline": cpu,
         "device": eng.name, "sm_count": sms,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if use_dist:
         dist.destroy_process_group()
 
 
+# stdout carries exactly ONE JSON line. Libraries write there too (NCCL prints its version line at
+# every NCCL_DEBUG level from WARN up, straight from C): everything else is pointed at stderr for the
+# whole run and the line goes out through a private duplicate of the original descriptor.
+_JSON_FD = None
+
+
+def capture_stdout():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict):
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def main():
+    capture_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
