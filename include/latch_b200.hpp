@@ -357,6 +357,83 @@ inline Descriptor describe(const Image& image, const Keypoint& keypoint, const T
     return describe_all(image, {keypoint}, pattern, 1).at(0).second;
 }
 
+// ---- LTCH descriptor container (descriptor.hpp:69-79, src/descriptor.cpp:110-211) --------------
+// Host-side, byte for byte the reference's format: "LTCH", u32 version 1, u32 count, u32 descriptor
+// bytes, u32 0, then per record four little-endian float32 (x, y, theta, score) + the descriptor.
+namespace b200 {
+inline void append_u32(std::string& out, std::uint32_t v) {
+    for (int shift = 0; shift < 32; shift += 8) out.push_back(static_cast<char>((v >> shift) & 0xffu));
+}
+inline std::uint32_t read_u32(const std::string& in, std::size_t& pos) {
+    if (in.size() < pos + 4) raise(ErrorCode::Truncated, "descriptor file ends mid-field");
+    std::uint32_t v = 0;
+    for (int i = 0; i < 4; ++i) v |= static_cast<std::uint32_t>(static_cast<unsigned char>(in[pos + i])) << (8 * i);
+    pos += 4;
+    return v;
+}
+} // namespace b200
+
+inline std::string format_descriptor_file(const std::vector<std::pair<Keypoint, Descriptor>>& records) {
+    const std::size_t bytes = records.empty() ? 0 : records.front().second.bytes.size();
+    std::string out = "LTCH";
+    b200::append_u32(out, 1u);
+    b200::append_u32(out, static_cast<std::uint32_t>(records.size()));
+    b200::append_u32(out, static_cast<std::uint32_t>(bytes));
+    b200::append_u32(out, 0u);
+    for (const auto& record : records) {
+        const double fields[4] = {record.first.x, record.first.y, record.first.theta, record.first.score};
+        for (double field : fields) {
+            const float narrow = static_cast<float>(field);
+            std::uint32_t bits;
+            std::memcpy(&bits, &narrow, sizeof bits);
+            b200::append_u32(out, bits);
+        }
+        out.append(reinterpret_cast<const char*>(record.second.bytes.data()), record.second.bytes.size());
+    }
+    return out;
+}
+
+inline std::vector<std::pair<Keypoint, Descriptor>> parse_descriptor_file(const std::string& data) {
+    if (data.size() < 4 || data.compare(0, 4, "LTCH") != 0) raise(ErrorCode::BadHeader, "not a descriptor file (bad magic)");
+    std::size_t pos = 4;
+    const std::uint32_t version = b200::read_u32(data, pos);
+    if (version != 1u) raise(ErrorCode::BadHeader, "unsupported descriptor file version " + std::to_string(version));
+    const std::uint32_t count = b200::read_u32(data, pos), bytes = b200::read_u32(data, pos);
+    b200::read_u32(data, pos);   // reserved
+    std::vector<std::pair<Keypoint, Descriptor>> records;
+    records.reserve(count);
+    for (std::uint32_t i = 0; i < count; ++i) {
+        double fields[4];
+        for (double& field : fields) {
+            const std::uint32_t bits = b200::read_u32(data, pos);
+            float narrow;
+            std::memcpy(&narrow, &bits, sizeof narrow);
+            field = narrow;
+        }
+        if (data.size() < pos + bytes) raise(ErrorCode::Truncated, "descriptor file ends mid-record");
+        Descriptor d;
+        d.bytes.assign(data.begin() + static_cast<std::ptrdiff_t>(pos), data.begin() + static_cast<std::ptrdiff_t>(pos + bytes));
+        pos += bytes;
+        records.emplace_back(Keypoint{fields[0], fields[1], fields[2], fields[3]}, std::move(d));
+    }
+    return records;
+}
+
+inline void save_descriptor_file(const std::vector<std::pair<Keypoint, Descriptor>>& records, const std::string& path) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) raise(ErrorCode::Malformed, "cannot open '" + path + "' for writing");
+    const std::string data = format_descriptor_file(records);
+    f.write(data.data(), static_cast<std::streamsize>(data.size()));
+}
+
+inline std::vector<std::pair<Keypoint, Descriptor>> load_descriptor_file(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) raise(ErrorCode::Malformed, "cannot open '" + path + "'");
+    std::ostringstream buffer;
+    buffer << f.rdbuf();
+    return parse_descriptor_file(buffer.str());
+}
+
 // ---- matching (match.hpp:27-45) ---------------------------------------------------------------
 /// Best and second-best gallery distances for one probe; ties go to the smallest index.
 inline Knn2Result knn2(const Descriptor& probe, const std::vector<Descriptor>& gallery) {

@@ -6,7 +6,8 @@ Drop-in for the two hot paths of the reference package ``latchkit``
 shapes/dtypes and exception types, and produce bit-identical results; the work
 runs in hand-written sm_100a kernels behind the C ABI in include/clatch.h.
 
-``detect`` (FAST-9 + NMS + orientation, the step before the path) is provided as well.
+``detect`` (FAST-9 + NMS + orientation, the step before the path) and the LTCH descriptor
+container (the file between the reference's ``latch describe`` and ``latch match``) are provided as well.
 Not provided (outside the hot path): evaluate, train, warp, load_pgm, save_pgm — keep using the reference's host code for those.
 """
 from __future__ import annotations
@@ -14,6 +15,7 @@ from __future__ import annotations
 import numpy as np
 
 from ._lib import ClatchDeviceError, LatchError
+from .container import format_descriptor_file, load_descriptor_file, parse_descriptor_file, save_descriptor_file
 from .engine import DescriptorSet, Engine, get_engine
 from .pattern import (TripletPattern, default_pattern as _default_pattern, default_pattern_text,
                       format_pattern, parse_pattern, pattern_from_text)
@@ -28,6 +30,7 @@ __all__ = [
     "default_pattern", "describe", "describe_batch", "descriptor_bits", "detect", "descriptor_bytes", "hamming", "match",
     "orientation_radius", "window_margin", "Engine", "DescriptorSet", "get_engine", "LatchError",
     "ClatchDeviceError", "TripletPattern", "parse_pattern", "format_pattern",
+    "format_descriptor_file", "parse_descriptor_file", "save_descriptor_file", "load_descriptor_file",
 ]
 
 

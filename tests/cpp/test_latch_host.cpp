@@ -277,6 +277,25 @@ int main(int argc, char** argv) {
         CHECK(std::string(d.bytes.begin(), d.bytes.end()) == bits);
     }
 
+    // ---- LTCH container: detect + describe the golden image, the file is the fixture byte for byte
+    //      (acceptance.cpp:120-130); parse/format round trip; error categories ----
+    {
+        const std::string pgm = read_file(root + "/tests/golden/golden_image.pgm");
+        const std::string fixture = read_file(root + "/tests/golden/golden_descriptors.bin");
+        Image golden(256, 256);
+        const size_t header = pgm.size() - 65536;
+        for (size_t i = 0; i < 65536; ++i) golden.data[i] = static_cast<unsigned char>(pgm[header + i]);
+        const auto records = latch::describe_all(golden, latch::detect_and_orient(golden, 20.0, true), pattern);
+        CHECK(records.size() == 257);
+        CHECK(latch::format_descriptor_file(records) == fixture);
+        const auto parsed = latch::parse_descriptor_file(fixture);
+        CHECK(parsed.size() == 257 && latch::format_descriptor_file(parsed) == fixture);
+        CHECK(latch::format_descriptor_file({}).size() == 20);
+        CHECK_THROWS_CODE(latch::parse_descriptor_file("LTCX" + fixture.substr(4)), ErrorCode::BadHeader);
+        CHECK_THROWS_CODE(latch::parse_descriptor_file(fixture.substr(0, fixture.size() - 1)), ErrorCode::Truncated);
+        CHECK_THROWS_CODE(latch::load_descriptor_file(root + "/tests/golden/no_such_file.ltch"), ErrorCode::Malformed);
+    }
+
     // ---- detection (test_detect.cpp:34-41, 128-151; acceptance.cpp:120-123) ----
     {
         Image flat(32, 32);

@@ -35,11 +35,16 @@ def test_golden_bits(lk, golden_image_u8):
 def test_golden_descriptor_file(lk, golden_image_u8):
     # acceptance.cpp:120-130
     kps = np.load(GOLDEN / "golden_keypoints_f64.npy")
-    fkps, fdesc = parse_ltch((GOLDEN / "golden_descriptors.bin").read_bytes())
+    blob = (GOLDEN / "golden_descriptors.bin").read_bytes()
+    fkps, fdesc = parse_ltch(blob)
     for img in (golden_image_u8, golden_image_u8.astype(np.float64)):
         kept, desc = lk.describe(img, kps)
         assert np.array_equal(desc, fdesc)
         assert np.array_equal(kept.astype(np.float32), fkps)
+        assert lk.format_descriptor_file(kept, desc) == blob            # the LTCH file, byte for byte
+    # detect -> describe -> file, the reference's `latch describe` pipeline end to end
+    kept, desc = lk.describe(golden_image_u8, lk.detect(golden_image_u8))
+    assert lk.format_descriptor_file(kept, desc) == blob
 
 
 @pytest.mark.parametrize("tag,maker,args", [("struct", "structured_image", (83, 160, 160)),

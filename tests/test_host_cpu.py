@@ -197,3 +197,34 @@ def test_embedded_lane_placement_matches_the_builtin_table():
     worst = sum(np.bincount(slots[g, :, k], minlength=8).max() for g in range(64) for k in range(3)) / 192.0
     stated = float(re.search(r"kDefaultPlanDegree = ([0-9.]+)", text).group(1))
     assert abs(worst - stated) < 1e-6 and worst < 1.2
+
+
+def test_ltch_container_round_trip_and_golden_bytes(tmp_path):
+    """The LTCH container written from describe()'s arrays must be the reference's file byte for
+    byte: tests/golden/golden_descriptors.bin is the regenerated fixture of acceptance.cpp:120-130
+    (257 records, float32-narrowed keypoints). Errors keep the reference's categories."""
+    import numpy as np
+    import pytest
+
+    from conftest import GOLDEN
+    from paper_1609_03986_b200 import container as io
+
+    blob = (GOLDEN / "golden_descriptors.bin").read_bytes()
+    kps, desc = io.parse_descriptor_file(blob)
+    assert kps.shape == (257, 4) and kps.dtype == np.float64 and desc.shape == (257, 64) and desc.dtype == np.uint8
+    assert io.format_descriptor_file(kps, desc) == blob
+    # from the float64 keypoints the detector produced: narrowing happens on write (static_cast<float>)
+    kps64 = np.load(GOLDEN / "golden_keypoints_f64.npy")
+    assert io.format_descriptor_file(kps64, desc) == blob
+    io.save_descriptor_file(kps64, desc, tmp_path / "d.ltch")
+    k2, d2 = io.load_descriptor_file(tmp_path / "d.ltch")
+    assert np.array_equal(k2, kps) and np.array_equal(d2, desc)
+    empty = io.format_descriptor_file(np.zeros((0, 4)), np.zeros((0, 64), np.uint8))
+    assert empty == b"LTCH" + bytes([1, 0, 0, 0]) + bytes(12)          # count 0 -> descriptor bytes 0
+    assert io.parse_descriptor_file(empty)[1].shape == (0, 0)
+    for bad, what in ((b"LTCX" + blob[4:], "BadHeader"), (blob[:4] + bytes([2, 0, 0, 0]) + blob[8:], "BadHeader"),
+                      (blob[:10], "Truncated"), (blob[:-1], "Truncated"), (blob[:20 + 80 * 3 + 7], "Truncated")):
+        with pytest.raises(RuntimeError, match=what):
+            io.parse_descriptor_file(bad)
+    with pytest.raises(RuntimeError, match="Malformed"):
+        io.load_descriptor_file(tmp_path / "missing.ltch")
