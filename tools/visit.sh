@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+mkdir -p gpurun_out/r1z; timeout 600 python tools/exact_rate.py 2>&1 | tee gpurun_out/r1z/exact_rate.log
