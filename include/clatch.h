@@ -80,6 +80,9 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * double-buffered planes, texture-unit footprints and resampling overlapped with the estimate
  * (default), 4 = variant 3 with dedicated producer / consumer warps. 2-4 take u8-valued images; any
  * other image runs variant 1. Every variant returns the same bytes.
+ * key "upload_bands": clatch_describe_all_f64 uploads a big float64 frame in this many row bands and
+ * extracts each band's keypoints while the next band is in flight (0 = choose by frame size, the
+ * default; 1 = one piece; up to 6). Results never depend on it.
  * key "host_promote": 1 lets clatch_describe_all_f64 convert a float64 image whose pixels are all
  * integers in [0, 255] to u8 on the host workers before the upload (8x fewer bytes over the bus;
  * lossless, same descriptors); 0 (default) uploads the doubles and classifies on the device —

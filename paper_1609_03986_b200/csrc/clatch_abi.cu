@@ -334,6 +334,11 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         ctx->extract_variant = value;
         return CLATCH_OK;
     }
+    if (std::strcmp(key, "upload_bands") == 0) {   // describe_all, float64 images: row bands of the upload (1 = one piece)
+        if (value < 0 || value > 6) return invalid("upload_bands must be 0 (auto) or 1..6");
+        ctx->upload_bands = value;
+        return CLATCH_OK;
+    }
     if (std::strcmp(key, "pairs_filter_on_device") == 0) {   // batched set pairs: filter pass on the device (1) or host (0)
         ctx->pairs_filter_on_device = value != 0;
         return CLATCH_OK;
@@ -471,14 +476,13 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
     return CLATCH_OK;
 }
 
-int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, int height,
-                             int workers, double* xycs, int64_t* kept, size_t* m) {
-    if (!m) return invalid("clatch_prepare_keypoints: m is null");
-    *m = 0;
-    if (cols < 2 || cols > 4) return invalid("keypoints must be (N, 2..4): x, y[, theta[, score]]");
-    if (n == 0) return CLATCH_OK;
-    if (!kps || !xycs || !kept) return invalid("clatch_prepare_keypoints: null buffer");
-    // keypoint_in_margin, src/descriptor.cpp:23-27 (NaN fails every comparison).
+} // extern "C"
+
+namespace {
+
+// keypoint_in_margin over the whole list (src/descriptor.cpp:23-27, 94-97; NaN fails every comparison):
+// kept[0..count) = input indices that keep the 46 px margin, in input order.
+size_t margin_filter(const double* kps, size_t n, int cols, int width, int height, int64_t* kept) {
     const double xmax = static_cast<double>(width - 1), ymax = static_cast<double>(height - 1);
     size_t count = 0;
     for (size_t i = 0; i < n; ++i) {
@@ -486,9 +490,14 @@ int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, i
         if (x - kMargin >= 0.0 && y - kMargin >= 0.0 && x + kMargin <= xmax && y + kMargin <= ymax)
             kept[count++] = static_cast<int64_t>(i);
     }
-    *m = count;
+    return count;
+}
+
+// cos/sin of extract_window (src/descriptor.cpp:35-36) through the host libm: record j of xycs comes
+// from input keypoint src[j]. Chunks of 256 records are claimed from a shared counter, so the calling
+// thread starts at once and the workers join in as they wake up.
+int trig_pass(const double* kps, int cols, const int64_t* src, size_t count, int workers, double* xycs) {
     if (count == 0) return CLATCH_OK;
-    // cos/sin of extract_window (src/descriptor.cpp:35-36) through the host libm.
     int nthreads = std::min<size_t>(resolve_workers(workers), (count + 1023) / 1024);
     nthreads = std::max(nthreads, 1);
     std::vector<int> bad(nthreads, 0);
@@ -496,33 +505,31 @@ int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, i
     // to snoop them out of the cores' caches (measured 6 GB/s for the 1.6 MB of 50 k records instead of
     // 50 GB/s); non-temporal stores put them in memory.
     const bool streaming = reinterpret_cast<uintptr_t>(xycs) % 16 == 0 && std::getenv("CLATCH_NO_STREAM_STORES") == nullptr;
-    // Chunks of 256 keypoints are claimed from a shared counter, so the calling thread starts at once
-    // and the workers join in as they wake up (a static split would wait for the slowest wake-up).
     std::atomic<size_t> next_chunk{0};
     constexpr size_t kChunk = 256;
     auto work = [&](int w) {
-      for (;;) {
-        const size_t begin = next_chunk.fetch_add(kChunk, std::memory_order_relaxed);
-        if (begin >= count) break;
-        const size_t end = std::min(count, begin + kChunk);
-        for (size_t j = begin; j < end; ++j) {
-            const double* k = kps + static_cast<size_t>(kept[j]) * cols;
-            const double theta = cols > 2 ? k[2] : 0.0;
-            const double c = std::cos(theta), s = std::sin(theta);
-            if (!std::isfinite(c) || !std::isfinite(s)) bad[w] = 1;
+        for (;;) {
+            const size_t begin = next_chunk.fetch_add(kChunk, std::memory_order_relaxed);
+            if (begin >= count) break;
+            const size_t end = std::min(count, begin + kChunk);
+            for (size_t j = begin; j < end; ++j) {
+                const double* k = kps + static_cast<size_t>(src[j]) * cols;
+                const double theta = cols > 2 ? k[2] : 0.0;
+                const double c = std::cos(theta), s = std::sin(theta);
+                if (!std::isfinite(c) || !std::isfinite(s)) bad[w] = 1;
 #if defined(__SSE2__)
-            if (streaming) {   // straight to memory: the DMA engine reads these lines next, not a CPU
-                _mm_stream_pd(xycs + 4 * j, _mm_set_pd(k[1], k[0]));
-                _mm_stream_pd(xycs + 4 * j + 2, _mm_set_pd(s, c));
-                continue;
-            }
+                if (streaming) {   // straight to memory: the DMA engine reads these lines next, not a CPU
+                    _mm_stream_pd(xycs + 4 * j, _mm_set_pd(k[1], k[0]));
+                    _mm_stream_pd(xycs + 4 * j + 2, _mm_set_pd(s, c));
+                    continue;
+                }
 #endif
-            xycs[4 * j + 0] = k[0];
-            xycs[4 * j + 1] = k[1];
-            xycs[4 * j + 2] = c;
-            xycs[4 * j + 3] = s;
+                xycs[4 * j + 0] = k[0];
+                xycs[4 * j + 1] = k[1];
+                xycs[4 * j + 2] = c;
+                xycs[4 * j + 3] = s;
+            }
         }
-      }
 #if defined(__SSE2__)
         if (streaming) _mm_sfence();
 #endif
@@ -534,6 +541,22 @@ int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, i
             return CLATCH_ERR_NONFINITE;
         }
     return CLATCH_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, int height,
+                             int workers, double* xycs, int64_t* kept, size_t* m) {
+    if (!m) return invalid("clatch_prepare_keypoints: m is null");
+    *m = 0;
+    if (cols < 2 || cols > 4) return invalid("keypoints must be (N, 2..4): x, y[, theta[, score]]");
+    if (n == 0) return CLATCH_OK;
+    if (!kps || !xycs || !kept) return invalid("clatch_prepare_keypoints: null buffer");
+    const size_t count = margin_filter(kps, n, cols, width, height, kept);
+    *m = count;
+    return trig_pass(kps, cols, kept, count, workers, xycs);
 }
 
 // ---- extraction ---------------------------------------------------------------
@@ -615,6 +638,10 @@ int clatch_extract_f64(clatch_ctx* ctx, const double* img, int width, int height
 // and trig pass. Optionally (see `bands` below) the image goes up in row bands on a copy stream,
 // keypoints are bucketed by the band in which their 92-row footprint ends, and each bucket's
 // extraction is queued behind that band's arrival event.
+static int describe_all_bands_f64(clatch_ctx* ctx, const double* img, int width, int height, size_t pitch,
+                                  const double* kps, size_t n, int cols, int workers, int64_t* kept, uint8_t* out,
+                                  size_t* m, int bands);
+
 template <typename Pixel>
 static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int height, size_t pitch,
                              const double* kps, size_t n, int cols, int workers, int64_t* kept,
@@ -645,86 +672,46 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
         if (all)
             return describe_all_impl<uint8_t>(ctx, staged, width, height, upitch, kps, n, cols, workers, kept, out, m);
     }
+    if (!kU8) {
+        // float64: upload in row bands when the frame is big enough for the overlap to pay
+        const size_t image_bytes = sizeof(double) * static_cast<size_t>(width) * height;
+        int bands = ctx->upload_bands;
+        if (const char* env = std::getenv("CLATCH_UPLOAD_BANDS")) bands = std::atoi(env);
+        // auto: the tail that cannot overlap is the last band's extraction, so more bands for bigger
+        // frames; each band costs ~10 us of launches (1920x1080, 10 k keypoints: 535 us in one piece,
+        // 460 / 467 / 476 us in 2 / 3 / 4 bands)
+        if (bands <= 0) bands = image_bytes < (24u << 20) ? 2 : 4;
+        bands = std::max(1, std::min(6, bands));
+        if (bands > 1 && n >= 4096 && image_bytes >= (4u << 20) && height >= 64 * bands && n < 0xffffffffull &&
+            extract_supports_out_index(ctx))
+            return describe_all_bands_f64(ctx, reinterpret_cast<const double*>(img), width, height, pitch, kps, n, cols,
+                                          workers, kept, out, m, bands);
+    }
     const size_t dpitch = kU8 ? (static_cast<size_t>(width) + 15) / 16 * 16 : static_cast<size_t>(width);
     const size_t bytes = static_cast<size_t>(ctx->pattern.T) / 8;
     if (int rc = ctx->img.reserve(sizeof(Pixel) * dpitch * height)) return rc;
     if (int rc = ctx->kps.reserve(sizeof(double) * 4 * n)) return rc;
     if (int rc = ctx->desc.reserve(bytes * n)) return rc;
     if (int rc = ctx->pin_xycs.reserve(sizeof(double) * 4 * n)) return rc;
-    if (int rc = ctx->pin_desc.reserve(bytes * n)) return rc;
     cudaStream_t st = ctx->stream;
 
-    // Opt-in (CLATCH_UPLOAD_BANDS=2..8): measured on B200 with a 16.6 MB float64 frame and 10 k
-    // keypoints, 1/2/3/4 bands take 0.73/0.76/0.80/0.85 ms — each band costs three launches, an
-    // event wait and a partial last wave of the persistent kernel, more than the overlap returns —
-    // so one piece is the default.
-    int bands = 1;
-    if (const char* env = std::getenv("CLATCH_UPLOAD_BANDS")) bands = std::max(1, std::min(8, std::atoi(env)));
-    if (n < 2048) bands = 1;
-    const int band_rows = (height + bands - 1) / bands;
-    if (bands > 1 && !ctx->copy_stream) {
-        CLATCH_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-        for (cudaEvent_t& e : ctx->band_events) CLATCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
     Trace trace;
     // 1. image DMA first ...
-    if (bands == 1) {
-        CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, sizeof(Pixel) * dpitch, img, sizeof(Pixel) * pitch,
-                                      sizeof(Pixel) * width, height, cudaMemcpyHostToDevice, st));
-    } else {
-        // the copy stream must not overwrite the image while earlier work on `st` still reads it
-        CLATCH_CUDA(cudaEventRecord(ctx->band_events[0], st));
-        CLATCH_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_events[0], 0));
-        for (int b = 0; b < bands; ++b) {
-            const int r0 = b * band_rows, r1 = std::min(height, r0 + band_rows);
-            CLATCH_CUDA(cudaMemcpy2DAsync(static_cast<Pixel*>(ctx->img.ptr) + static_cast<size_t>(r0) * dpitch,
-                                          sizeof(Pixel) * dpitch, img + static_cast<size_t>(r0) * pitch,
-                                          sizeof(Pixel) * pitch, sizeof(Pixel) * width, r1 - r0,
-                                          cudaMemcpyHostToDevice, ctx->copy_stream));
-            CLATCH_CUDA(cudaEventRecord(ctx->band_events[b], ctx->copy_stream));
-        }
-    }
+    CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, sizeof(Pixel) * dpitch, img, sizeof(Pixel) * pitch,
+                                  sizeof(Pixel) * width, height, cudaMemcpyHostToDevice, st));
     // 2. ... while the host filters by margin and evaluates cos/sin with its own libm
     double* const xycs = static_cast<double*>(ctx->pin_xycs.ptr);
     size_t count = 0;
-    auto drain = [&] {
-        cudaStreamSynchronize(st);
-        if (bands > 1) cudaStreamSynchronize(ctx->copy_stream);
-    };
     trace.stamp("image copy queued");
     if (int rc = clatch_prepare_keypoints(kps, n, cols, width, height, workers, xycs, kept, &count)) {
-        drain();
+        cudaStreamSynchronize(st);
         return rc;
     }
     trace.stamp("keypoints prepared");
     *m = count;
     if (count == 0) {
-        drain();
+        cudaStreamSynchronize(st);
         return CLATCH_OK;
-    }
-    // 3. bucket the kept keypoints by the band in which their footprint (rows floor(y)-45 ..
-    //    floor(y)+46) ends; a stable counting sort keeps input order inside a bucket
-    std::vector<uint32_t> order;          // order[slot] = kept-index computed in that slot
-    size_t bucket_begin[9] = {0};
-    if (bands > 1) {
-        std::vector<uint8_t> band_of(count);
-        size_t hist[9] = {0};
-        for (size_t j = 0; j < count; ++j) {
-            const int bottom = static_cast<int>(std::floor(xycs[4 * j + 1])) + 46;
-            const int b = std::min(bands - 1, bottom / band_rows);
-            band_of[j] = static_cast<uint8_t>(b);
-            ++hist[b + 1];
-        }
-        for (int b = 0; b < bands; ++b) bucket_begin[b + 1] = bucket_begin[b] + hist[b + 1];
-        order.resize(count);
-        size_t cursor[8];
-        for (int b = 0; b < bands; ++b) cursor[b] = bucket_begin[b];
-        for (size_t j = 0; j < count; ++j) order[cursor[band_of[j]]++] = static_cast<uint32_t>(j);
-        ctx->host_xycs.resize(4 * count);   // permuted copy goes to the pinned buffer in place
-        std::memcpy(ctx->host_xycs.data(), xycs, sizeof(double) * 4 * count);
-        for (size_t s = 0; s < count; ++s) std::memcpy(xycs + 4 * s, ctx->host_xycs.data() + 4 * order[s], 32);
-    } else {
-        bucket_begin[1] = count;
     }
     cudaEvent_t tev[4] = {};
     if (trace.on) {
@@ -733,49 +720,157 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
     }
     CLATCH_CUDA(cudaMemcpyAsync(ctx->kps.ptr, xycs, sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
     if (trace.on) cudaEventRecord(tev[1], st);
-    // 4. per band: wait for its rows, (f64) classify them, extract the bucket
-    int rc = CLATCH_OK;
-    for (int b = 0; b < bands && !rc; ++b) {
-        const int r0 = b * band_rows, r1 = bands == 1 ? height : std::min(height, r0 + band_rows);
-        if (bands > 1) CLATCH_CUDA(cudaStreamWaitEvent(st, ctx->band_events[b], 0));
-        const size_t begin = bucket_begin[b], cnt = bucket_begin[b + 1] - begin;
-        const double* d_x = ctx->kps.as<double>() + 4 * begin;
-        uint8_t* d_o = ctx->desc.as<uint8_t>() + bytes * begin;
-        if (kU8) {
-            rc = launch_extract_u8(ctx, ctx->img.as<uint8_t>(), width, height, dpitch, d_x, cnt, d_o, st);
-        } else {
-            rc = launch_classify_rows(ctx, ctx->img.as<double>(), width, height, dpitch, r0, r1, b == 0, st);
-            if (!rc) rc = launch_extract_f64_classified(ctx, ctx->img.as<double>(), width, height, dpitch, d_x, cnt, d_o, st);
+    // 3. extraction (a float64 image is classified first: u8-valued -> the u8 kernels)
+    int rc;
+    if (kU8)
+        rc = launch_extract_u8(ctx, ctx->img.as<uint8_t>(), width, height, dpitch, ctx->kps.as<double>(), count,
+                               ctx->desc.as<uint8_t>(), st);
+    else
+        rc = launch_extract_f64(ctx, ctx->img.as<double>(), width, height, dpitch, ctx->kps.as<double>(), count,
+                                ctx->desc.as<uint8_t>(), st);
+    if (rc) {
+        cudaStreamSynchronize(st);
+        return rc;
+    }
+    trace.stamp("kernels queued");
+    if (trace.on) cudaEventRecord(tev[2], st);
+    // 4. descriptors straight into the caller's array
+    CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+    trace.stamp("download queued");
+    if (trace.on) cudaEventRecord(tev[3], st);
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    trace.stamp("stream drained");
+    if (trace.on) {
+        float a = 0, b = 0, c = 0;
+        cudaEventElapsedTime(&a, tev[0], tev[1]);
+        cudaEventElapsedTime(&b, tev[1], tev[2]);
+        cudaEventElapsedTime(&c, tev[2], tev[3]);
+        std::fprintf(stderr, "[clatch] device: keypoint upload %.1f us, kernels %.1f us, download %.1f us\n", a * 1e3,
+                     b * 1e3, c * 1e3);
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
+    return CLATCH_OK;
+}
+
+// float64 images are eight bytes a pixel: the upload of a 1920x1080 frame (16.6 MB, 0.33 ms over PCIe 5)
+// takes twice as long as extracting 10 k descriptors from it. So the frame goes up in row bands and the
+// keypoints whose footprints (rows floor(y)-45 .. floor(y)+46) end inside band b are extracted while
+// band b+1 is still in flight. Order of the H2D queue matters — one copy engine serves it in issue
+// order — so: band 0, then the keypoint records (ready by then: the host prepared them meanwhile),
+// then the other bands. Records are prepared in band order; the kernels write each descriptor to its
+// input-order row (ExtractParams::out_index), so the download is one contiguous copy again.
+// Classification is per band and cumulative (launch_classify_rows): a band whose rows are all
+// u8-valued so far takes the u8 kernel, and a keypoint only ever reads rows of its own and earlier bands.
+static int describe_all_bands_f64(clatch_ctx* ctx, const double* img, int width, int height, size_t pitch,
+                                  const double* kps, size_t n, int cols, int workers, int64_t* kept, uint8_t* out,
+                                  size_t* m, int bands) {
+    const size_t dpitch = static_cast<size_t>(width), bytes = static_cast<size_t>(ctx->pattern.T) / 8;
+    const size_t rec_bytes = sizeof(double) * 4 * n, idx_bytes = sizeof(unsigned) * n;
+    if (int rc = ctx->img.reserve(sizeof(double) * dpitch * height)) return rc;
+    if (int rc = ctx->kps.reserve(rec_bytes + idx_bytes)) return rc;
+    if (int rc = ctx->desc.reserve(bytes * n)) return rc;
+    if (int rc = ctx->pin_xycs.reserve(rec_bytes + idx_bytes)) return rc;
+    cudaStream_t st = ctx->stream;
+    if (!ctx->copy_stream) {
+        CLATCH_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : ctx->band_events) CLATCH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t cs = ctx->copy_stream;
+    Trace trace;
+    const int band_rows = (height + bands - 1) / bands;
+    auto copy_band = [&](int b) -> int {
+        const int r0 = b * band_rows, r1 = std::min(height, r0 + band_rows);
+        double* dst = ctx->img.as<double>() + static_cast<size_t>(r0) * dpitch;
+        const double* src = img + static_cast<size_t>(r0) * pitch;
+        if (pitch == dpitch)   // contiguous rows: one flat DMA
+            CLATCH_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * dpitch * (r1 - r0), cudaMemcpyHostToDevice, cs));
+        else
+            CLATCH_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * dpitch, src, sizeof(double) * pitch, sizeof(double) * width,
+                                          r1 - r0, cudaMemcpyHostToDevice, cs));
+        CLATCH_CUDA(cudaEventRecord(ctx->band_events[b], cs));
+        return CLATCH_OK;
+    };
+    auto drain = [&] {
+        cudaStreamSynchronize(cs);
+        cudaStreamSynchronize(st);
+    };
+    // the copy stream must not overwrite the image while earlier work on `st` still reads it
+    CLATCH_CUDA(cudaEventRecord(ctx->band_events[7], st));
+    CLATCH_CUDA(cudaStreamWaitEvent(cs, ctx->band_events[7], 0));
+    if (int rc = copy_band(0)) return rc;
+    trace.stamp("band 0 copy queued");
+
+    // host, meanwhile: margin filter, band of every kept keypoint, records in band order
+    const size_t count = margin_filter(kps, n, cols, width, height, kept);
+    *m = count;
+    if (count == 0) {
+        drain();
+        return CLATCH_OK;
+    }
+    std::vector<int64_t>& src = ctx->band_src;      // record j <- input keypoint src[j]
+    src.resize(count);
+    unsigned* const h_index = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(ctx->pin_xycs.ptr) + rec_bytes);
+    size_t begin[9] = {0};
+    {
+        std::vector<uint8_t>& band_of = ctx->band_of;
+        band_of.resize(count);
+        size_t hist[9] = {0};
+        for (size_t j = 0; j < count; ++j) {
+            const int bottom = static_cast<int>(std::floor(kps[static_cast<size_t>(kept[j]) * cols + 1])) + 46;
+            const int b = std::min(bands - 1, bottom / band_rows);
+            band_of[j] = static_cast<uint8_t>(b);
+            ++hist[b + 1];
+        }
+        for (int b = 0; b < bands; ++b) begin[b + 1] = begin[b] + hist[b + 1];
+        size_t cursor[8];
+        for (int b = 0; b < bands; ++b) cursor[b] = begin[b];
+        for (size_t j = 0; j < count; ++j) {       // stable: input order inside a band
+            const size_t slot = cursor[band_of[j]]++;
+            src[slot] = kept[j];
+            h_index[slot] = static_cast<unsigned>(j);
         }
     }
+    double* const xycs = static_cast<double*>(ctx->pin_xycs.ptr);
+    if (int rc = trig_pass(kps, cols, src.data(), count, workers, xycs)) {
+        drain();
+        return rc;
+    }
+    trace.stamp("keypoints prepared");
+    // records + output rows ride the H2D queue right behind band 0, ahead of the other bands
+    uint8_t* const d_rec = ctx->kps.as<uint8_t>();
+    CLATCH_CUDA(cudaMemcpyAsync(d_rec, xycs, sizeof(double) * 4 * count, cudaMemcpyHostToDevice, cs));
+    CLATCH_CUDA(cudaMemcpyAsync(d_rec + rec_bytes, h_index, sizeof(unsigned) * count, cudaMemcpyHostToDevice, cs));
+    CLATCH_CUDA(cudaEventRecord(ctx->band_events[7], cs));
+    for (int b = 1; b < bands; ++b)
+        if (int rc = copy_band(b)) {
+            drain();
+            return rc;
+        }
+    CLATCH_CUDA(cudaStreamWaitEvent(st, ctx->band_events[7], 0));
+    trace.stamp("copies queued");
+    int rc = CLATCH_OK;
+    ctx->extract_out_index = reinterpret_cast<const unsigned*>(d_rec + rec_bytes);
+    for (int b = 0; b < bands && !rc; ++b) {
+        const int r0 = b * band_rows, r1 = std::min(height, r0 + band_rows);
+        CLATCH_CUDA(cudaStreamWaitEvent(st, ctx->band_events[b], 0));
+        rc = launch_classify_rows(ctx, ctx->img.as<double>(), width, height, dpitch, r0, r1, b == 0, st);
+        const size_t cnt = begin[b + 1] - begin[b];
+        if (!rc && cnt > 0) {
+            ctx->extract_out_index = reinterpret_cast<const unsigned*>(d_rec + rec_bytes) + begin[b];
+            rc = launch_extract_f64_classified(ctx, ctx->img.as<double>(), width, height, dpitch,
+                                               reinterpret_cast<const double*>(d_rec) + 4 * begin[b], cnt,
+                                               ctx->desc.as<uint8_t>(), st);
+        }
+    }
+    ctx->extract_out_index = nullptr;
     if (rc) {
         drain();
         return rc;
     }
     trace.stamp("kernels queued");
-    if (trace.on) cudaEventRecord(tev[2], st);
-    // 5. descriptors come back through page-locked staging; undo the bucket order on the way out
-    if (bands == 1) {
-        CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
-        trace.stamp("download queued");
-        if (trace.on) cudaEventRecord(tev[3], st);
-        CLATCH_CUDA(cudaStreamSynchronize(st));
-        trace.stamp("stream drained");
-        if (trace.on) {
-            float a = 0, b = 0, c = 0;
-            cudaEventElapsedTime(&a, tev[0], tev[1]);
-            cudaEventElapsedTime(&b, tev[1], tev[2]);
-            cudaEventElapsedTime(&c, tev[2], tev[3]);
-            std::fprintf(stderr, "[clatch] device: keypoint upload %.1f us, kernels %.1f us, download %.1f us\n", a * 1e3,
-                         b * 1e3, c * 1e3);
-            for (cudaEvent_t e : tev) cudaEventDestroy(e);
-        }
-    } else {
-        CLATCH_CUDA(cudaMemcpyAsync(ctx->pin_desc.ptr, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
-        CLATCH_CUDA(cudaStreamSynchronize(st));
-        const uint8_t* src = static_cast<const uint8_t*>(ctx->pin_desc.ptr);
-        for (size_t s = 0; s < count; ++s) std::memcpy(out + bytes * order[s], src + bytes * s, bytes);
-    }
+    CLATCH_CUDA(cudaMemcpyAsync(out, ctx->desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+    CLATCH_CUDA(cudaStreamSynchronize(st));
+    trace.stamp("stream drained");
     return CLATCH_OK;
 }
 

@@ -48,6 +48,7 @@ struct ExtractParams {
     int run_if_flag;           // run only when flags[0] == run_if_flag (if flags != null)
     unsigned long long* stats; // optional {triplets recomputed exactly, warps that took the exact pass}
     cudaTextureObject_t tex;   // pipelined kernel: the u8 image as a gather-enabled CUDA array
+    const unsigned* out_index; // optional: descriptor of record j goes to row out_index[j] (quad / pipelined kernels)
 };
 
 // Exact u8 -> f64 without the 16-lane/clk conversion pipe (I2F.F64 runs at 16/clk/SM on
@@ -373,7 +374,8 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_quad_kernel(ExtractPa
         const unsigned w0 = __ballot_sync(0xffffffffu, s_bits[grp * kFastT + gt] != 0);
         const unsigned w1 = __ballot_sync(0xffffffffu, s_bits[grp * kFastT + gt + kThreads] != 0);
         if ((tid & 31) == 0 && valid) {
-            unsigned* out32 = reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8));
+            const unsigned long long row = p.out_index ? p.out_index[kp] : kp;
+            unsigned* out32 = reinterpret_cast<unsigned*>(p.out + row * (kFastT / 8));
             out32[gt >> 5] = w0;
             out32[(gt >> 5) + kThreads / 32] = w1;
         }
@@ -776,8 +778,10 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_pipe_kernel(ExtractPa
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const unsigned w32 = __ballot_sync(0xffffffffu, bits[256 * k + j] != 0);
-                if (lane == 0 && kp < p.M)
-                    reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8))[8 * k + (j >> 5)] = w32;
+                if (lane == 0 && kp < p.M) {
+                    const unsigned long long row = p.out_index ? p.out_index[kp] : kp;
+                    reinterpret_cast<unsigned*>(p.out + row * (kFastT / 8))[8 * k + (j >> 5)] = w32;
+                }
             }
         }
 
@@ -1189,6 +1193,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     p.flags = flags;
     p.run_if_flag = run_if_flag;
     p.stats = ctx->extract_stats_on ? ctx->extract_stats.as<unsigned long long>() : nullptr;
+    p.out_index = ctx->extract_out_index;   // honoured by the quad and pipelined kernels (extract_supports_out_index)
     if (kU8 && pat.fast && ctx->extract_variant >= 3) {
         if (!ctx->pipe_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1251,6 +1256,12 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
 }
 
 } // namespace
+
+// Scattered output rows (ExtractParams::out_index) are implemented by the kernels that the banded
+// float64 upload can reach: the pipelined kernel (u8-valued image) and the quad kernel (any other).
+bool extract_supports_out_index(const clatch_ctx* ctx) {
+    return ctx->pattern.fast && ctx->extract_variant == 3;
+}
 
 int upload_weights(const double* w, int count) {
     CLATCH_CUDA(cudaMemcpyToSymbol(c_weights, w, sizeof(double) * count));

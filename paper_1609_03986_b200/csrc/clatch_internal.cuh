@@ -91,6 +91,7 @@ struct clatch_ctx {
         int width = 0, height = 0;
     };
     std::vector<TexImage> tex_images;
+    const unsigned* extract_out_index = nullptr;   // set around a launch: record j -> output row (banded upload)
     bool extract_stats_on = false;           // count exact recomputes (clatch_extract_stats)
     clatch::DeviceBuffer extract_stats;      // 2 x u64
     bool pairs_filter_on_device = true;   // clatch_match_set_pairs: ratio / max / cross-check decisions on the device
@@ -100,6 +101,9 @@ struct clatch_ctx {
     clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t, items, scores, counts, det;
     clatch::DeviceBuffer filt_pairs, filt_rows, filt_out, filt_counts;   // on-device filter pass of batched set pairs
     std::vector<double> host_xycs;   // describe_all staging
+    std::vector<int64_t> band_src;   // banded float64 upload: record j <- input keypoint
+    std::vector<uint8_t> band_of;
+    int upload_bands = 0;            // describe_all, float64 images: 0 = auto (set_option "upload_bands")
     clatch::PinnedBuffer pinned;     // D2H staging for batched pair results
     clatch::PinnedBuffer pin_xycs, pin_desc;   // describe_all staging (banded upload path)
     clatch::PinnedBuffer pin_img;              // describe_all: host-promoted u8 copy of a float64 image
@@ -119,6 +123,7 @@ namespace clatch {
 
 // extraction (clatch_extract.cu)
 int upload_weights(const double* w, int count);
+bool extract_supports_out_index(const clatch_ctx* ctx);
 int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,
                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
 int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,

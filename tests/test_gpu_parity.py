@@ -577,6 +577,37 @@ def test_float64_promotion_edges(lk, port, promote):
         eng.set_option("host_promote", 0)
 
 
+@pytest.mark.parametrize("bands", [1, 2, 3, 6])
+def test_banded_float64_upload(lk, port, bands):
+    """A big float64 frame goes up in row bands and each band's keypoints are extracted while the
+    next band is in flight; descriptors come back in input order. u8-valued frames take the u8
+    kernel band by band, a frame that stops being u8-valued in a later band switches to the
+    float64 kernel from that band on, and a non-integer frame uses it throughout — always the
+    oracle's bytes, including margin violators and keypoints on band boundaries."""
+    eng = lk.get_engine()
+    eng.set_option("upload_bands", bands)
+    try:
+        w, h, n = 1024, 768, 6000
+        base = port.random_image_u8(8100, w, h).astype(np.float64)
+        kps = port.random_keypoints(8101, w, h, n)
+        kps[::97, 0] = 3.0                                             # margin violators are dropped silently
+        edge_rows = [h // bands * b for b in range(1, bands)] or [h // 2]
+        for i, r in enumerate(edge_rows):                              # footprints ending exactly at band edges
+            kps[10 + i, 1] = r - 46.0
+            kps[40 + i, 1] = r - 47.0 + 0.999
+            kps[70 + i, 1] = r - 45.5
+        late = base.copy()
+        late[h - 5, w // 2] = 17.25                                    # not u8-valued, but only in the last rows
+        frac = base + np.random.default_rng(3).random(base.shape) * 0.5
+        for name, img in (("u8-valued", base), ("late non-integer pixel", late), ("non-integer", frac)):
+            kept_idx, want = port.describe_all(img, kps)
+            kept, desc = lk.describe(img, kps)
+            assert np.array_equal(kept, kps[kept_idx]), name
+            assert np.array_equal(desc, want), name
+    finally:
+        eng.set_option("upload_bands", 0)
+
+
 # ------------------------------------------------------ resident sets, batched pairs ----
 
 @pytest.mark.parametrize("filter_on_device", [1, 0])
