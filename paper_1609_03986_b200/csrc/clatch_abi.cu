@@ -677,10 +677,11 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
         const size_t image_bytes = sizeof(double) * static_cast<size_t>(width) * height;
         int bands = ctx->upload_bands;
         if (const char* env = std::getenv("CLATCH_UPLOAD_BANDS")) bands = std::atoi(env);
-        // auto: the tail that cannot overlap is the last band's extraction, so more bands for bigger
-        // frames; each band costs ~10 us of launches (1920x1080, 10 k keypoints: 535 us in one piece,
-        // 460 / 467 / 476 us in 2 / 3 / 4 bands)
-        if (bands <= 0) bands = image_bytes < (24u << 20) ? 2 : 4;
+        // auto: two bands. More bands shorten the tail that cannot overlap (the last band's extraction) but
+        // each costs ~50 us of host-side launches, which delays everything behind it: 1920x1080 with 10 k
+        // keypoints takes 535 us in one piece, 454 / 523 / 549 us in 2 / 3 / 4 bands; 3840x2160 with 50 k
+        // keypoints 2.23 ms in one piece, 1.81 / 2.10 / 2.28 ms in 2 / 4 / 6.
+        if (bands <= 0) bands = 2;
         bands = std::max(1, std::min(6, bands));
         if (bands > 1 && n >= 4096 && image_bytes >= (4u << 20) && height >= 64 * bands && n < 0xffffffffull &&
             extract_supports_out_index(ctx))
@@ -777,9 +778,29 @@ static int describe_all_bands_f64(clatch_ctx* ctx, const double* img, int width,
     }
     cudaStream_t cs = ctx->copy_stream;
     Trace trace;
-    const int band_rows = (height + bands - 1) / bands;
+    // Band heights: band b+1 should land just as band b's keypoints are done, so that neither the copy
+    // engine nor the SMs wait — heights in geometric progression with ratio (extraction time) / (upload
+    // time), which for a 1920x1080 frame with 10 k keypoints is about 0.5: a tall first band, a short
+    // last one, and only the last band's extraction is left when the upload ends.
+    int row_end[8];
+    {
+        const double upload_s = sizeof(double) * static_cast<double>(width) * height / 50e9;
+        const double extract_s = 20e-6 + 17.5e-9 * static_cast<double>(n);
+        const double ratio = std::min(3.0, std::max(0.3, extract_s / upload_s));
+        double weight[8], total = 0.0, w = 1.0;
+        for (int b = 0; b < bands; ++b, w *= ratio) total += weight[b] = w;
+        double cum = 0.0;
+        int prev = 0;
+        for (int b = 0; b < bands; ++b) {
+            cum += weight[b] / total;
+            int end = b == bands - 1 ? height : static_cast<int>(std::lround(cum * height));
+            end = std::min(height - 48 * (bands - 1 - b), std::max(prev + 48, end));   // every band at least 48 rows
+            row_end[b] = prev = end;
+        }
+        row_end[bands - 1] = height;
+    }
     auto copy_band = [&](int b) -> int {
-        const int r0 = b * band_rows, r1 = std::min(height, r0 + band_rows);
+        const int r0 = b == 0 ? 0 : row_end[b - 1], r1 = row_end[b];
         double* dst = ctx->img.as<double>() + static_cast<size_t>(r0) * dpitch;
         const double* src = img + static_cast<size_t>(r0) * pitch;
         if (pitch == dpitch)   // contiguous rows: one flat DMA
@@ -817,7 +838,8 @@ static int describe_all_bands_f64(clatch_ctx* ctx, const double* img, int width,
         size_t hist[9] = {0};
         for (size_t j = 0; j < count; ++j) {
             const int bottom = static_cast<int>(std::floor(kps[static_cast<size_t>(kept[j]) * cols + 1])) + 46;
-            const int b = std::min(bands - 1, bottom / band_rows);
+            int b = 0;
+            while (b < bands - 1 && bottom >= row_end[b]) ++b;   // first band that holds the footprint's last row
             band_of[j] = static_cast<uint8_t>(b);
             ++hist[b + 1];
         }
@@ -851,7 +873,7 @@ static int describe_all_bands_f64(clatch_ctx* ctx, const double* img, int width,
     int rc = CLATCH_OK;
     ctx->extract_out_index = reinterpret_cast<const unsigned*>(d_rec + rec_bytes);
     for (int b = 0; b < bands && !rc; ++b) {
-        const int r0 = b * band_rows, r1 = std::min(height, r0 + band_rows);
+        const int r0 = b == 0 ? 0 : row_end[b - 1], r1 = row_end[b];
         CLATCH_CUDA(cudaStreamWaitEvent(st, ctx->band_events[b], 0));
         rc = launch_classify_rows(ctx, ctx->img.as<double>(), width, height, dpitch, r0, r1, b == 0, st);
         const size_t cnt = begin[b + 1] - begin[b];
