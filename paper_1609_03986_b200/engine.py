@@ -24,16 +24,23 @@ def _ptr(a: np.ndarray, t):
 
 
 class _PinnedPool:
-    """Page-locked numpy arrays for the results the API hands back (descriptor arrays usually come
-    straight back as match() inputs: page-locked, both transfers are plain DMAs, and a batch call's
-    downloads never stall its pipeline). cudaHostAlloc is slow (about 3 ms per MB on the B200 hosts),
-    so blocks are recycled by power-of-two size: a block returns to the pool when the last numpy
-    view of it dies, and a loop that drops its previous results cycles through the same blocks.
-    A caller that KEEPS its results is served page-locked memory up to `max_live_bytes`; after
-    that, ordinary pageable arrays (page-locked memory is a scarce resource)."""
+    """Result arrays for describe() / describe_batch(). Page-locked memory makes both of their trips
+    over the bus plain DMAs (descriptor arrays usually come straight back as match() inputs, and a
+    batch call's downloads never stall its pipeline) — but cudaHostAlloc costs about 3 ms per MB on
+    the B200 hosts, ten times what first-touching pageable memory costs. So page-locked blocks are
+    handed out only where they will be recycled:
+
+    * blocks are kept by power-of-two size and reused; a block returns to the pool when the last
+      numpy view of it dies;
+    * a NEW block is allocated only after an earlier result of that size has been released (a loop
+      that drops its previous result: the second iteration pays the allocation, the rest reuse it);
+    * a caller that keeps every result gets ordinary pageable arrays, and so does anyone beyond
+      `max_live_bytes` of outstanding page-locked memory.
+    """
 
     def __init__(self, lib, max_live_bytes: int = 256 << 20):
-        self.lib, self.free, self.live_bytes, self.max_live_bytes = lib, {}, 0, max_live_bytes
+        self.lib, self.free, self.released, self.live_bytes = lib, {}, {}, 0
+        self.max_live_bytes = max_live_bytes
         self.lock = threading.Lock()
 
     def empty(self, shape, dtype) -> np.ndarray:
@@ -43,9 +50,17 @@ class _PinnedPool:
         with self.lock:
             blocks = self.free.get(cap)
             ptr = blocks.pop() if blocks else None
-            if ptr is None and self.live_bytes + cap > self.max_live_bytes:
-                return np.empty(shape, dtype)
-            self.live_bytes += cap
+            if ptr is None:
+                if self.released.get(cap, 0) <= 0 or self.live_bytes + cap > self.max_live_bytes:
+                    ptr = False                       # no evidence of recycling (or over budget): pageable
+                else:
+                    self.released[cap] -= 1
+            if ptr is not False:
+                self.live_bytes += cap
+        if ptr is False:
+            arr = np.empty(shape, dtype)
+            weakref.finalize(arr, self._note_release, cap)
+            return arr
         if ptr is None:
             p = C.c_void_p()
             rc = self.lib.clatch_host_alloc(cap, C.byref(p))
@@ -57,6 +72,10 @@ class _PinnedPool:
         owner = (C.c_uint8 * cap).from_address(ptr)
         weakref.finalize(owner, self._release, ptr, cap)
         return np.frombuffer(owner, dtype=dtype, count=count).reshape(shape)
+
+    def _note_release(self, cap):
+        with self.lock:
+            self.released[cap] = self.released.get(cap, 0) + 1
 
     def _release(self, ptr, cap):
         with self.lock:
