@@ -484,6 +484,36 @@ def test_trained_pattern_on_every_fast_kernel(lk, port, variant):
         lk.describe(port.random_image_u8(88, 300, 200), port.random_keypoints(90, 300, 200, 4))   # built-in table back
 
 
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
+def test_smallest_images_and_odd_pitches(lk, port, variant):
+    """93x93 is the smallest image with a describable keypoint (46, 46); widths that are not
+    multiples of 16 take the unaligned staging / array-fill paths when the image arrives as a
+    device tensor with pitch == width."""
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    eng.set_option("extract_variant", variant)
+    try:
+        for w, h in ((93, 93), (94, 93), (107, 131), (160, 97)):
+            img = port.random_image_u8(7000 + w, w, h)
+            kps = np.array([[46.0, 46.0, 0.0, 0.0], [w - 47.0, h - 47.0, 2.5, 0.0], [46.0, h - 47.0, -1.0, 0.0],
+                            [w - 47.0, 46.0, 0.7, 0.0], [45.999, 46.0, 0.0, 0.0], [w / 2, h / 2, 3.1, 0.0]])
+            kept_idx, want = port.describe_all(img.astype(np.float64), kps)
+            assert 4 <= len(kept_idx) <= 5 and 4 not in kept_idx        # (45.999, 46) violates the margin
+            assert np.array_equal(lk.describe(img, kps)[1], want), (w, h, "host u8")
+            assert np.array_equal(lk.describe(img.astype(np.float64), kps)[1], want), (w, h, "host f64")
+            xycs, kept = eng.prepare_keypoints(kps, w, h)
+            d_img = torch.from_numpy(img).cuda()                    # pitch == width: unaligned rows
+            got = eng.extract_device(d_img, torch.from_numpy(xycs).cuda())
+            torch.cuda.synchronize()
+            assert np.array_equal(got.cpu().numpy(), want), (w, h, "device tensor")
+            d_odd = torch.from_numpy(np.pad(img, ((0, 0), (3, 0))))[:, 3:].cuda()   # contiguous copy, odd base offset
+            got = eng.extract_device(d_odd.contiguous(), torch.from_numpy(xycs).cuda())
+            torch.cuda.synchronize()
+            assert np.array_equal(got.cpu().numpy(), want), (w, h, "device tensor 2")
+    finally:
+        eng.set_option("extract_variant", 3)
+
+
 def _near_tie_images(w, h):
     """u8 images built to put d1 - d2 at or next to zero: the inputs on which an fp32 estimate
     of the SSD pair must NOT be trusted (exact ties, rounding-level differences, tiny sums)."""
