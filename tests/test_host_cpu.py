@@ -228,3 +228,71 @@ def test_ltch_container_round_trip_and_golden_bytes(tmp_path):
             io.parse_descriptor_file(bad)
     with pytest.raises(RuntimeError, match="Malformed"):
         io.load_descriptor_file(tmp_path / "missing.ltch")
+
+
+def test_fp32_estimate_bound_never_decides_wrongly():
+    """The filtered / pipelined extraction kernels take sign(d1 - d2) from fp32 sums over the
+    truncated window only when |d1_f - d2_f| exceeds 2.2e-4 (sqrt d1_f + sqrt d2_f) + 3.3e-6 (d1_f + d2_f)
+    + 3e-8. Restated here in numpy — cvt.rz truncation, one rounding per subtraction, one
+    per fused accumulation, the bound in fp32 — against the reference's sequential fp64 chains, on
+    windows built to sit on the decision boundary: whenever the estimate decides, it must agree."""
+    import numpy as np
+
+    rng = np.random.default_rng(160903986)
+
+    def truncate32(v):                       # cvt.rz.f32.f64 for v >= 0
+        f = v.astype(np.float32)
+        over = f.astype(np.float64) > v
+        f[over] = np.nextafter(f[over], np.float32(0))
+        return f
+
+    def exact_chain(a, b):                   # src/descriptor.cpp:61-75, 49 live terms, unfused
+        d = np.zeros(len(a))
+        for k in range(49):
+            e = a[:, k] - b[:, k]
+            d = d + e * e
+        return d
+
+    def fp32_chain(fa, fb):
+        d = np.zeros(len(fa), np.float32)
+        for k in range(49):
+            e = fa[:, k] - fb[:, k]                                       # one rounding (fp32 subtraction)
+            d = (e.astype(np.float64) * e.astype(np.float64) + d.astype(np.float64)).astype(np.float32)   # fused
+        return d
+
+    n = 40000
+    cases = []
+    base = rng.integers(0, 256, (n, 49)).astype(np.float64)
+    frac = rng.random((n, 49))
+    # 1. bilinear-like values of noise: everything far from a tie
+    cases.append((rng.random((n, 49)) * 255, rng.random((n, 49)) * 255, rng.random((n, 49)) * 255))
+    # 2. companions that differ from each other by perturbations from 1e-14 to 1e-1: the boundary region
+    for scale in (1e-14, 1e-10, 1e-7, 3e-6, 1e-5, 1e-4, 1e-3, 1e-2, 1e-1):
+        a = np.clip(base + frac, 0, 255)
+        b = np.clip(a + rng.normal(0, 30, (n, 49)), 0, 255)
+        c = np.clip(b + rng.normal(0, scale, (n, 49)), 0, 255)
+        cases.append((a, b, c))
+    # 3. flat and nearly flat footprints (the reference's bits are decided by rounding noise there)
+    for scale in (0.0, 1e-15, 1e-13, 1e-9):
+        level = rng.integers(0, 256, (n, 1)).astype(np.float64)
+        mk = lambda: np.clip(level * (1 + rng.normal(0, 1, (n, 49)) * scale), 0, 255)   # noqa: E731
+        cases.append((mk(), mk(), mk()))
+    # 4. mirrored companions: d1 == d2 up to rounding, large sums
+    a = rng.random((n, 49)) * 255
+    delta = rng.normal(0, 40, (n, 49))
+    cases.append((a, np.clip(a + delta, 0, 255), np.clip(a - delta, 0, 255)))
+
+    decided_total = total = 0
+    for a, b, c in cases:
+        want = exact_chain(a, b) > exact_chain(a, c)
+        fa, fb, fc = truncate32(a), truncate32(b), truncate32(c)
+        assert np.all((a - fa.astype(np.float64) >= 0) & (a - fa.astype(np.float64) < 2.0 ** -16))
+        d1, d2 = fp32_chain(fa, fb), fp32_chain(fa, fc)
+        diff = d1 - d2
+        bound = (np.float32(2.2e-4) * (np.sqrt(d1) + np.sqrt(d2)) + np.float32(3.3e-6) * (d1 + d2)
+                 + np.float32(3.0e-8)).astype(np.float32)
+        decided = np.abs(diff) > bound
+        assert np.array_equal((diff > 0)[decided], want[decided])
+        decided_total += int(decided.sum())
+        total += len(decided)
+    assert 0.15 < decided_total / total < 0.95       # the cases really straddle the boundary
