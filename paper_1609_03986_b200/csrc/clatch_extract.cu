@@ -10,12 +10,19 @@
 // accumulation order inside one SSD chain is the reference's row-major order, and
 // cos/sin arrive from the host's libm. No tree reductions anywhere.
 //
-// Kernel shape: persistent CTAs (a multiple of the SM count), one keypoint per CTA
-// iteration. Per keypoint: (1) stage the <=92x92 u8 footprint into shared memory with
-// 16-byte loads, (2) 256 threads resample the 4096 window samples into a padded fp64
-// window in shared memory, (3) each thread owns whole triplets (both SSD chains) and
-// reads the window with immediate-offset 64-bit shared loads, (4) predicate bits are
-// packed with __ballot_sync and stored as 32-bit words.
+// Kernels in this file (all persistent, one CTA per SM unless noted), oldest to newest:
+//   extract_fast_kernel     one fp64 window per CTA, 4 CTAs/SM                     (extract_variant 0)
+//   extract_quad_kernel     four fp64 windows per CTA, conflict-free 64-bit loads  (1; also every non-u8-valued image)
+//   extract_filt_kernel     four split (fp32 + low word) windows; every bit decided by an fp32 estimate with a
+//                           proven error bound, exact fp64 chains only for undecided bits     (2)
+//   extract_pipe_kernel     the same estimate with double-buffered planes, texture-unit footprints and resampling
+//                           overlapped with the estimate; the default for u8-valued images   (3)
+//   extract_roles_kernel    variant 3 with dedicated producer / consumer warps              (4, A/B)
+//   extract_generic_kernel  any T % 8 == 0, 1 <= K <= 64, real weights: (w*e)*e literally
+// Common shape: (1) the <=92x92 footprint of a keypoint reaches the SM (u8 tile in shared memory, or
+// tex2Dgather on a u8 CUDA array), (2) the 4096 window samples are resampled in unfused fp64, (3) each
+// thread owns whole triplets and reads the window with immediate-offset shared loads, (4) predicate
+// bits are packed with __ballot_sync and stored as 32-bit words.
 
 #include <algorithm>
 #include <cstdio>
