@@ -416,10 +416,12 @@ def run_ours(args):
                "sample": "the full step twice (describe_all + match_brute_force, workers = all host threads)",
                "descriptors_per_s": mm / td, "compares_per_s": mm * mm / tm}
 
+    dtype = ("f64 resampling, " + ("fp32 estimate + exact f64 recompute" if ev >= 2 else "f64 SSD") + " (extraction) / " +
+             ("int8 tcgen05, int32 accumulate" if mv == 3 else "u32 xor+popc") + " (matching); results bit-exact")
     line = {
         "metric": METRIC, "value": world * m / per_step, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64 (extraction) / u32 xor+popc (matching)", "data": "synthetic",
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic",
         "config": {"workload": f"{args.workload}: {w}x{h} u8 noise image, {n} oriented keypoints per GPU, "
                                f"extract + {m}x{m} Hamming top-2 self-match", "keypoints": n, "descriptors": m,
                    "phase": args.phase,
