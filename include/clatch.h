@@ -123,6 +123,12 @@ CLATCH_API int clatch_descriptor_bytes(clatch_ctx* ctx);
 CLATCH_API int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, int height,
                              int workers, double* xycs, int64_t* kept, size_t* m);
 
+/* The kept keypoints of describe_all as (m, 4) rows [x, y, theta, score] (missing columns read as 0):
+ * out[j] = kps[kept[j]], gathered on the host workers. What the reference returns as the first half
+ * of its (Keypoint, Descriptor) pairs (src/descriptor.cpp:99-104). */
+CLATCH_API int clatch_take_keypoints(const double* kps, int cols, const int64_t* kept, size_t m, int workers,
+                                     double* out);
+
 /* ---- detection (the step before the path: fast_detect / detect_and_orient,
  * src/detect.cpp:76-157) -------------------------------------------------------------------
  * FAST-9 segment test with `threshold`, optional 3x3 non-maximum suppression (ties keep the

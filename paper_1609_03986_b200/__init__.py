@@ -94,11 +94,7 @@ def describe(image, keypoints, pattern=None, workers=0):
     eng = get_engine()
     eng.set_pattern(pat)
     kept, desc = eng.describe_all(img, kps, workers)
-    if kps.shape[1] == 4:
-        return kps.take(kept, axis=0), desc
-    full = np.zeros((len(kept), 4), np.float64)
-    full[:, :kps.shape[1]] = kps.take(kept, axis=0)
-    return full, desc
+    return eng.take_keypoints(kps, kept, workers), desc
 
 
 def describe_batch(images, keypoints, pattern=None, workers=0):
@@ -118,15 +114,7 @@ def describe_batch(images, keypoints, pattern=None, workers=0):
     eng = get_engine()
     eng.set_pattern(pat)
     res = eng.describe_batch(imgs, kps, workers)
-    out = []
-    for k, (kept, desc) in zip(kps, res):
-        if k.shape[1] == 4:
-            out.append((k.take(kept, axis=0), desc))
-            continue
-        full = np.zeros((len(kept), 4), np.float64)
-        full[:, :k.shape[1]] = k.take(kept, axis=0)
-        out.append((full, desc))
-    return out
+    return [(eng.take_keypoints(k, kept, workers), desc) for k, (kept, desc) in zip(kps, res)]
 
 
 def match(probes, gallery, ratio=None, cross_check=False, max_distance=None, workers=0):

@@ -58,6 +58,7 @@ _SIGNATURES = {
     "clatch_descriptor_bytes": (C.c_int, [C.c_void_p]),
     "clatch_prepare_keypoints": (C.c_int, [f64p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, f64p,
                                            i64p, szp]),
+    "clatch_take_keypoints": (C.c_int, [f64p, C.c_int, i64p, C.c_size_t, C.c_int, f64p]),
     "clatch_detect_u8": (C.c_int, [C.c_void_p, u8p, C.c_int, C.c_int, C.c_size_t, C.c_double, C.c_int, C.c_int,
                                    C.c_int, f64p, C.c_size_t, szp]),
     "clatch_detect_f64": (C.c_int, [C.c_void_p, f64p, C.c_int, C.c_int, C.c_size_t, C.c_double, C.c_int, C.c_int,

@@ -547,6 +547,30 @@ int trig_pass(const double* kps, int cols, const int64_t* src, size_t count, int
 
 extern "C" {
 
+int clatch_take_keypoints(const double* kps, int cols, const int64_t* kept, size_t m, int workers, double* out) {
+    if (cols < 2 || cols > 4) return invalid("keypoints must be (N, 2..4): x, y[, theta[, score]]");
+    if (m == 0) return CLATCH_OK;
+    if (!kps || !kept || !out) return invalid("clatch_take_keypoints: null buffer");
+    const int parts = static_cast<int>(std::max<size_t>(1, std::min<size_t>(resolve_workers(workers), m / 4096)));
+    std::atomic<size_t> next{0};
+    WorkerPool::instance().run(parts, [&](int) {
+        for (;;) {
+            const size_t begin = next.fetch_add(2048, std::memory_order_relaxed);
+            if (begin >= m) break;
+            const size_t end = std::min(m, begin + 2048);
+            for (size_t j = begin; j < end; ++j) {
+                const double* k = kps + static_cast<size_t>(kept[j]) * cols;
+                double* o = out + 4 * j;
+                o[0] = k[0];
+                o[1] = k[1];
+                o[2] = cols > 2 ? k[2] : 0.0;   // missing theta / score read as 0 (bindings/module.cpp:49-62)
+                o[3] = cols > 3 ? k[3] : 0.0;
+            }
+        }
+    });
+    return CLATCH_OK;
+}
+
 int clatch_prepare_keypoints(const double* kps, size_t n, int cols, int width, int height,
                              int workers, double* xycs, int64_t* kept, size_t* m) {
     if (!m) return invalid("clatch_prepare_keypoints: m is null");

@@ -183,6 +183,15 @@ class Engine:
                                                      _ptr(xycs, f64p), _ptr(kept, i64p), C.byref(m)))
         return xycs[:m.value], kept[:m.value]
 
+    def take_keypoints(self, keypoints: np.ndarray, kept: np.ndarray, workers: int = 0) -> np.ndarray:
+        """(M, 4) float64 rows keypoints[kept] with missing theta / score columns read as 0."""
+        kps = np.ascontiguousarray(keypoints, np.float64)
+        idx = np.ascontiguousarray(kept, np.int64)
+        out = np.empty((len(idx), 4), np.float64)
+        _lib.check(self.lib.clatch_take_keypoints(_ptr(kps, f64p), kps.shape[1], _ptr(idx, i64p), len(idx), workers,
+                                                  _ptr(out, f64p)))
+        return out
+
     # ---- detection ----------------------------------------------------------------------
     def detect(self, image: np.ndarray, threshold: float = 20.0, nms: bool = True, orient: bool = True,
                radius: int = 15) -> np.ndarray:

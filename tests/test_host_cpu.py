@@ -296,3 +296,26 @@ def test_fp32_estimate_bound_never_decides_wrongly():
         decided_total += int(decided.sum())
         total += len(decided)
     assert 0.15 < decided_total / total < 0.95       # the cases really straddle the boundary
+
+
+def test_take_keypoints_matches_numpy(lib):
+    """clatch_take_keypoints: out[j] = kps[kept[j]] as (m, 4) rows, missing theta / score = 0
+    (bindings/module.cpp:49-62), for every accepted column count and worker count."""
+    import ctypes as C
+
+    import numpy as np
+
+    rng = np.random.default_rng(4)
+    for cols in (2, 3, 4):
+        for n in (1, 7, 5000, 40000):
+            kps = rng.random((n, cols))
+            kept = np.sort(rng.choice(n, size=max(1, n - n // 10), replace=False)).astype(np.int64)
+            want = np.zeros((len(kept), 4))
+            want[:, :cols] = kps[kept]
+            for workers in (0, 1, 3):
+                out = np.full((len(kept), 4), -1.0)
+                rc = lib.clatch_take_keypoints(kps.ctypes.data_as(C.POINTER(C.c_double)), cols,
+                                               kept.ctypes.data_as(C.POINTER(C.c_int64)), len(kept), workers,
+                                               out.ctypes.data_as(C.POINTER(C.c_double)))
+                assert rc == 0 and np.array_equal(out, want)
+    assert lib.clatch_take_keypoints(None, 5, None, 0, 0, None) != 0          # bad column count
