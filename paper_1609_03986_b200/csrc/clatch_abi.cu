@@ -987,6 +987,12 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         if (!ctx->pipe[s].stream) CLATCH_CUDA(cudaStreamCreateWithFlags(&ctx->pipe[s].stream, cudaStreamNonBlocking));
     int rc = CLATCH_OK;
     Trace trace;
+    std::vector<cudaEvent_t> bev;   // trace mode: per image {upload done, kernels done, download done}, + origin
+    if (trace.on) {
+        bev.resize(3 * num_images + 1);
+        for (cudaEvent_t& e : bev) cudaEventCreate(&e);
+        cudaEventRecord(bev[3 * num_images], ctx->pipe[0].stream);
+    }
     for (size_t i = 0; i < num_images && !rc; ++i) {
         clatch_ctx::PipeSlot& slot = ctx->pipe[i & 1];
         cudaStream_t st = slot.stream;
@@ -1031,6 +1037,7 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         m[i] = count;
         if (count == 0) continue;
         CLATCH_CUDA(cudaMemcpyAsync(slot.kps.ptr, xycs, sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
+        if (trace.on) cudaEventRecord(bev[3 * i], st);
         if (kU8) {
             rc = launch_extract_u8(ctx, slot.img.template as<uint8_t>(), w, h, dpitch, slot.kps.template as<double>(),
                                    count, slot.desc.template as<uint8_t>(), st);
@@ -1048,6 +1055,7 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         // pageable memory goes through page-locked staging so that the download stays asynchronous, and
         // is copied out when the slot comes round again.
         trace.stamp("batch: kernels queued");
+        if (trace.on) cudaEventRecord(bev[3 * i + 1], st);
         cudaPointerAttributes attr{};
         const bool direct = cudaPointerGetAttributes(&attr, out[i]) == cudaSuccess && attr.type == cudaMemoryTypeHost;
         if (!direct) cudaGetLastError();   // an unregistered pointer is not an error here
@@ -1058,7 +1066,21 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
             slot.pending_out = out[i];
             slot.pending_bytes = bytes * count;
         }
+        if (trace.on) cudaEventRecord(bev[3 * i + 2], st);
     }
+    if (trace.on && !rc) {
+        for (int s = 0; s < 2; ++s) cudaStreamSynchronize(ctx->pipe[s].stream);
+        for (size_t i = 0; i < num_images; ++i) {
+            float a = 0, b = 0, c = 0;
+            if (cudaEventElapsedTime(&a, bev[3 * num_images], bev[3 * i]) == cudaSuccess &&
+                cudaEventElapsedTime(&b, bev[3 * num_images], bev[3 * i + 1]) == cudaSuccess &&
+                cudaEventElapsedTime(&c, bev[3 * num_images], bev[3 * i + 2]) == cudaSuccess)
+                std::fprintf(stderr, "[clatch] device: image %zu uploaded at %.0f us, extracted at %.0f us, downloaded at %.0f us\n",
+                             i, a * 1e3, b * 1e3, c * 1e3);
+        }
+        cudaGetLastError();
+    }
+    for (cudaEvent_t e : bev) cudaEventDestroy(e);
     for (int s = 0; s < 2; ++s) {
         clatch_ctx::PipeSlot& slot = ctx->pipe[s];
         cudaError_t e = cudaStreamSynchronize(slot.stream);

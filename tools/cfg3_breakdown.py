@@ -9,7 +9,9 @@ def pinned(a):
     t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True); t.numpy()[...] = a; return t.numpy()
 pimg, pkps = pinned(img), pinned(kps)
 def timeit(fn, reps=10):
-    fn(); fn(); fn(); torch.cuda.synchronize(); t0 = time.perf_counter()   # (the page-locked pool settles by the third call)
+    for _ in range(5):   # (the page-locked result pool settles within four calls)
+        fn()
+    torch.cuda.synchronize(); t0 = time.perf_counter()
     for _ in range(reps): out = fn()
     torch.cuda.synchronize(); return (time.perf_counter() - t0) / reps * 1e3, out
 ms, (xycs, kept) = timeit(lambda: eng.prepare_keypoints(pkps, W, H)); print(f"prepare_keypoints 50k        {ms:.3f} ms")

@@ -42,7 +42,7 @@ def pinned(a):
     t.numpy()[...] = a
     return t.numpy()
 pimgs, pkps = [pinned(a) for a in imgs], [pinned(a) for a in kps]
-for _ in range(2):                         # steady state: the page-locked result blocks exist and are recycled
+for _ in range(4):                         # steady state: the page-locked result blocks exist and are recycled
     warm = lk.describe_batch(pimgs, pkps)  # (the pool allocates them once it has seen results of this size released)
     del warm
 sync()
