@@ -161,7 +161,10 @@ CLATCH_API int clatch_extract_f64(clatch_ctx* ctx, const double* img, int width,
 /* describe_all in one call (src/descriptor.cpp:90-105): margin filter + host trig +
  * upload + extraction + download. The image upload is queued first so the DMA overlaps
  * the host-side trig pass. kps: n rows of `cols` (2..4) doubles; kept: room for n input
- * indices; out: room for n descriptors; *m receives the number kept (input order). */
+ * indices; out: room for n descriptors; *m receives the number kept (input order).
+ * A big float64 frame goes up in row bands and each band's keypoints are extracted while the
+ * next band is in flight ("upload_bands"). Page-locked img / out buffers (cudaHostAlloc,
+ * clatch_host_alloc) make the transfers plain DMAs; ordinary memory works, only slower. */
 CLATCH_API int clatch_describe_all_u8(clatch_ctx* ctx, const uint8_t* img, int width, int height, size_t pitch,
                            const double* kps, size_t n, int cols, int workers, int64_t* kept,
                            uint8_t* out, size_t* m);
