@@ -48,9 +48,10 @@ FILT_SMEM_BYTES_PER_DESC = 512 * 49 * 3 * 4                # 4-byte F-plane read
 POPC_PER_COMPARE = 16
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
 # captures of the same command (profiles/*_ncu.json); cold-cache replay, so an upper bound.
-TRAFFIC_NCU = {"extract_pipe_kernel": 2.419e+06,                     # profiles/r2a_extract_ncu.json
+TRAFFIC_NCU = {"extract_roles_kernel<16>": 2.419e+06,                # profiles/r2c_extract_ncu.json
+               "extract_pipe_kernel": 2.419e+06,                     # profiles/r2c_extract_ncu.json
                "extract_quad_kernel<u8>": 2.419e+06,                 # profiles/r1t_extract_ncu.json
-               "match_tc_kernel (tcgen05 kind::i8)": 5.288e+06}     # profiles/r2a_match_tc_ncu.json
+               "match_tc_kernel (tcgen05 kind::i8)": 5.288e+06}     # profiles/r2c_match_tc_ncu.json
 
 
 def synth_inputs(workload: str, rank: int = 0):
@@ -341,7 +342,7 @@ def run_ours(args):
     sms = eng.sm_count
     pipes = peaks.get("pipes", {})
     mv = args.match_variant if args.match_variant is not None else 3
-    ev = args.extract_variant if args.extract_variant is not None else 3
+    ev = args.extract_variant if args.extract_variant is not None else 4
     ext_name = {0: "extract_fast_kernel<u8>", 1: "extract_quad_kernel<u8>", 2: "extract_filt_kernel",
                 3: "extract_pipe_kernel", 4: "extract_roles_kernel<16>"}[ev]
     mat_name = "match_tc_kernel (tcgen05 kind::i8)" if mv == 3 else f"match64_kernel<{mv}>"

@@ -920,8 +920,10 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const unsigned w32 = __ballot_sync(0xffffffffu, bits[128 * k + j] != 0);
-                    if (lane == 0 && kp < p.M)
-                        reinterpret_cast<unsigned*>(p.out + kp * (kFastT / 8))[4 * k + (j >> 5)] = w32;
+                    if (lane == 0 && kp < p.M) {
+                        const unsigned long long row = p.out_index ? p.out_index[kp] : kp;
+                        reinterpret_cast<unsigned*>(p.out + row * (kFastT / 8))[4 * k + (j >> 5)] = w32;
+                    }
                 }
             }
             if (it + 1 < nq) {   // resample the next quad into F[nxt]
@@ -1224,8 +1226,9 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         p.slots = pat.slots_f8.as<ushort4>();
         const size_t quads = (M + kQuad - 1) / kQuad;
         const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
-        // variant 4: dedicated producer / consumer warps, 16 + 16 (24 + 8 measured 48.8 M desc/s: eight
-        // warps cannot keep the LSU busy; 16 + 16 ties with the symmetric schedule at ~60 M)
+        // variant 4 (default): dedicated producer / consumer warps, 16 + 16 — 60.1 vs 58.1 M desc/s at 10 k
+        // keypoints and 72.3 vs 68.3 M at 50 k against the symmetric schedule of variant 3 (24 + 8 warps
+        // measured 48.8 M: eight warps cannot keep the LSU busy)
         if (ctx->extract_variant == 4) extract_roles_kernel<16><<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
         else extract_pipe_kernel<<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
     } else if (kU8 && pat.fast && ctx->extract_variant == 2) {
@@ -1267,7 +1270,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
 // Scattered output rows (ExtractParams::out_index) are implemented by the kernels that the banded
 // float64 upload can reach: the pipelined kernel (u8-valued image) and the quad kernel (any other).
 bool extract_supports_out_index(const clatch_ctx* ctx) {
-    return ctx->pattern.fast && ctx->extract_variant == 3;
+    return ctx->pattern.fast && (ctx->extract_variant == 3 || ctx->extract_variant == 4);
 }
 
 int upload_weights(const double* w, int count) {

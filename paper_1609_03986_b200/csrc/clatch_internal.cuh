@@ -82,7 +82,7 @@ struct clatch_ctx {
     // (4 split windows per CTA, fp32 estimate + exact recompute); 3: pipelined kernel (resampling
     // overlapped with the estimate, footprints from the texture unit); 4: variant 3 with dedicated
     // producer / consumer warps. 2-4 take u8 images — others run variant 1.
-    int extract_variant = 3;
+    int extract_variant = 4;
     struct TexImage {                // pipelined kernel: the image as a gather-enabled CUDA array
         cudaStream_t stream = nullptr;
         cudaArray_t array = nullptr;

@@ -450,7 +450,7 @@ def test_every_extraction_variant_is_exact(lk, port, variant):
         kps = port.random_keypoints(2050, 400, 300, 203)
         assert np.array_equal(lk.describe(fimg, kps)[1], port.describe_all(fimg, kps)[1])
     finally:
-        eng.set_option("extract_variant", 3)
+        eng.set_option("extract_variant", 4)
 
 
 @pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
@@ -480,7 +480,7 @@ def test_trained_pattern_on_every_fast_kernel(lk, port, variant):
             assert np.array_equal(lk.describe(img, kps, pattern=text)[1], want)
             assert np.array_equal(lk.describe(img.astype(np.float64), kps, pattern=text)[1], want)
     finally:
-        eng.set_option("extract_variant", 3)
+        eng.set_option("extract_variant", 4)
         lk.describe(port.random_image_u8(88, 300, 200), port.random_keypoints(90, 300, 200, 4))   # built-in table back
 
 
@@ -511,7 +511,7 @@ def test_smallest_images_and_odd_pitches(lk, port, variant):
             torch.cuda.synchronize()
             assert np.array_equal(got.cpu().numpy(), want), (w, h, "device tensor 2")
     finally:
-        eng.set_option("extract_variant", 3)
+        eng.set_option("extract_variant", 4)
 
 
 def _near_tie_images(w, h):
@@ -555,7 +555,7 @@ def test_filtered_kernel_on_near_ties(lk, port, variant):
         got = lk.describe(img, kps)[1]
         assert np.array_equal(got, want), name
         assert np.array_equal(lk.describe(img.astype(np.float64), kps)[1], want), (name, "f64")
-    eng.set_option("extract_variant", 3)
+    eng.set_option("extract_variant", 4)
 
 
 @pytest.mark.parametrize("variant", [2, 3, 4])
@@ -578,7 +578,7 @@ def test_filtered_kernel_exact_pass_rate(lk, port, variant):
         assert exact == m * 512 and passes > 0
     finally:
         eng.set_option("extract_stats", 0)
-        eng.set_option("extract_variant", 3)
+        eng.set_option("extract_variant", 4)
 
 
 @pytest.mark.parametrize("promote", [1, 0])

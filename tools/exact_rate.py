@@ -27,13 +27,13 @@ images = {
     "half saturated": np.where(xx < w // 2, 255, img).astype(np.uint8),
     "flat": np.full((h, w), 99, np.uint8),
 }
-for variant in (3, 2, 1):
+for variant in (4, 3, 2, 1):
     eng.set_option("extract_variant", variant)
     for name, im in images.items():
         eng.set_option("extract_stats", 1)
         m = len(lk.describe(im, kps)[1])
         exact, passes = eng.extract_stats() if variant >= 2 else (0, 0)
-        unit = "windows re-resampled" if variant == 3 else "warp passes"
+        unit = "windows re-resampled" if variant >= 3 else "warp passes"
         eng.set_option("extract_stats", 0)
         xycs, _ = eng.prepare_keypoints(kps, w, h)
         d_img, d_x = torch.from_numpy(im).cuda(), torch.from_numpy(xycs).cuda()
@@ -49,4 +49,4 @@ for variant in (3, 2, 1):
         print(f"variant {variant}  {name:36s} exact triplets {exact:9d} of {m * 512} = {exact / (m * 512):.2e}; "
               f"{unit}: {passes} ({passes / m:.3f} per descriptor); {rate:.1f} M desc/s", flush=True)
 eng.set_option("extract_stats", 0)
-eng.set_option("extract_variant", 3)
+eng.set_option("extract_variant", 4)

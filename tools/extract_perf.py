@@ -32,4 +32,4 @@ for tag, im in (("u8", img), ("f64 integer-valued", img.astype(np.float64)), ("f
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
         print(f"{tag:22s} variant {variant}: {ms:.3f} ms  {len(xycs) / ms * 1e3 / 1e6:.1f} M desc/s", flush=True)
-eng.set_option("extract_variant", 3)
+eng.set_option("extract_variant", 4)

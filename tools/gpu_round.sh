@@ -14,7 +14,7 @@ tail -5 "$OUT/pytest_gpu.log"
 echo "== pipe peaks"; timeout 120 ./tools/pipe_peaks > "$OUT/pipe_peaks.json" 2> "$OUT/pipe_peaks.err"; cat "$OUT/pipe_peaks.json"
 echo "== bench ours"; timeout 900 python bench.py --steps 20 --warmup 5 > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?"; cat "$OUT/bench.json"; tail -3 "$OUT/bench.err"
 if [ "${VARIANTS:-0}" = "1" ]; then
-for v in 0 1 2 3; do
+for v in 0 1 2 3 4; do
   echo "== extraction variant $v"
   timeout 300 python bench.py --steps 20 --warmup 5 --phase extract --no-cpu-baseline --extract-variant $v > "$OUT/bench_extract_v$v.json" 2>> "$OUT/bench.err"
   python -c "import json;d=json.load(open('$OUT/bench_extract_v$v.json'));print('extract variant $v desc/s', d['descriptors_per_s'])"
@@ -31,7 +31,7 @@ echo "== ncu launch list"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$OUT/launches.csv" \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$OUT/ncu_launches.log" 2>&1
 echo "== ncu full: extraction"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:extract_pipe -s 3 -c 1 -f -o "$OUT/prof_extract" \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:extract_roles -s 3 -c 1 -f -o "$OUT/prof_extract" \
     python bench.py --steps 2 --warmup 3 --phase extract --no-cpu-baseline > "$OUT/ncu_extract.log" 2>&1
 echo "== ncu full: tensor-core matching"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_tc -s 3 -c 1 -f -o "$OUT/prof_match_tc" \

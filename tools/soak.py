@@ -67,7 +67,7 @@ while time.time() < t_end:
             assert np.array_equal(d2, port.describe_all(im.astype(np.float64), k)[1]), ("batch", it, variant)
         cases["batch"] += 1
     if it % 9 == 0:                                   # banded float64 upload: needs a big frame and >= 4096 keypoints
-        eng.set_option("extract_variant", 3)
+        eng.set_option("extract_variant", 4)
         W, H, N = 1100 + int(rng.integers(0, 200)), 800 + int(rng.integers(0, 100)), 4200
         big = image("noise", W, H).astype(np.float64)
         if rng.random() < 0.5:
@@ -98,6 +98,6 @@ while time.time() < t_end:
         for s in sets:
             s.close()
         cases["pairs"] += 1
-eng.set_option("extract_variant", 3)
+eng.set_option("extract_variant", 4)
 eng.set_option("match_streamk", 1)
 print(f"soak ok: {it} iterations in {budget:.0f} s; cases {cases}")
