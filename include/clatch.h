@@ -77,8 +77,8 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * key "extract_variant": 0 = one window per CTA, 1 = four fp64 windows per CTA with conflict-free
  * shared loads, 2 = four split (fp32 + low word) windows per CTA: a proven fp32 estimate decides
  * each bit and the rare undecided ones are recomputed exactly, 3 = the same estimate with
- * double-buffered planes, texture-unit footprints and resampling overlapped with the estimate
- * (default), 4 = variant 3 with dedicated producer / consumer warps. 2-4 take u8-valued images; any
+ * double-buffered planes, texture-unit footprints and resampling overlapped with the estimate,
+ * 4 = variant 3 with dedicated producer / consumer warps (default). 2-4 take u8-valued images; any
  * other image runs variant 1. Every variant returns the same bytes.
  * key "upload_bands": clatch_describe_all_f64 uploads a big float64 frame in this many row bands and
  * extracts each band's keypoints while the next band is in flight (0 = choose by frame size, the

@@ -16,8 +16,8 @@
 //   extract_filt_kernel     four split (fp32 + low word) windows; every bit decided by an fp32 estimate with a
 //                           proven error bound, exact fp64 chains only for undecided bits     (2)
 //   extract_pipe_kernel     the same estimate with double-buffered planes, texture-unit footprints and resampling
-//                           overlapped with the estimate; the default for u8-valued images   (3)
-//   extract_roles_kernel    variant 3 with dedicated producer / consumer warps              (4, A/B)
+//                           overlapped with the estimate (every warp does both halves)       (3)
+//   extract_roles_kernel    variant 3 with dedicated producer / consumer warps; the default for u8-valued images (4)
 //   extract_generic_kernel  any T % 8 == 0, 1 <= K <= 64, real weights: (w*e)*e literally
 // Common shape: (1) the <=92x92 footprint of a keypoint reaches the SM (u8 tile in shared memory, or
 // tex2Dgather on a u8 CUDA array), (2) the 4096 window samples are resampled in unfused fp64, (3) each
