@@ -891,8 +891,8 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
     extern __shared__ __align__(16) uint8_t s_quad[];
     float* const s_f = reinterpret_cast<float*>(s_quad);                              // F[2][4], then LO[4]
     uint8_t* const s_bits = s_quad + kPipePlanes * kPlanePitch * 4;                   // [2][4][512 + pad]
-    double2* const s_tab = reinterpret_cast<double2*>(s_bits + 2 * kQuad * kPipeBits);   // [4][64] (next quad)
-    double* const s_kp = reinterpret_cast<double*>(s_tab + 2 * kQuad * kWindow);      // [4][x, y, cos, sin]
+    double2* const s_tab = reinterpret_cast<double2*>(s_bits + 2 * kQuad * kPipeBits);   // [2][4][64]
+    double* const s_kp = reinterpret_cast<double*>(s_tab + 2 * kQuad * kWindow);      // [2][4][x, y, cos, sin]
     int* const s_mask = reinterpret_cast<int*>(s_kp + 2 * kQuad * 4);                 // [2] windows needing LO
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, grp = warp >> 2;
@@ -909,11 +909,18 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
     for (int j = 0; j < kSlots; ++j) slot[j] = __ldg(p.slots + 8 * (rw % kSW + kSW * j) + ti);
     unsigned n_flagged = 0, n_windows = 0;
     if (tid == 0) s_mask[0] = s_mask[1] = 0;
+    // Producers only resample. The consumers, which have slack, also stage the keypoint records and
+    // row products two quads ahead (buffer [quad & 1]) and pack the previous quad's bits.
+    stage_quad_rows(p, static_cast<unsigned long long>(blockIdx.x) * kQuad, s_tab, s_kp, tid);
+    __syncthreads();
 
     for (long long it = -1; it <= nq; ++it) {
         const int cur = static_cast<int>(it & 1), nxt = cur ^ 1;
-        if (producer) {
-            if (it >= 1 && rt < 512) {   // pack the bits of the quad consumed in the previous iteration
+        if (!producer) {
+            if (it + 2 < nq)   // rows for quad it+2 -> buffer [cur] (its last readers resampled quad `it`, an iteration ago)
+                stage_quad_rows(p, (blockIdx.x + (it + 2) * gridDim.x) * kQuad, s_tab + cur * kQuad * kWindow,
+                                s_kp + cur * kQuad * 4, rt);
+            if (it >= 1) {   // pack the bits of the quad consumed in the previous iteration
                 const unsigned long long kp = (blockIdx.x + (it - 1) * gridDim.x) * kQuad + (rt >> 7);
                 const uint8_t* bits = s_bits + (nxt * kQuad + (rt >> 7)) * kPipeBits;
                 const int j = rt & 127;
@@ -926,9 +933,11 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
                     }
                 }
             }
+        }
+        if (producer) {
             if (it + 1 < nq) {   // resample the next quad into F[nxt]
-                stage_quad_rows(p, (blockIdx.x + (it + 1) * gridDim.x) * kQuad, s_tab, s_kp, rt);
-                asm volatile("bar.sync 1, %0;" ::"n"(kRT) : "memory");
+                const double2* const tab = s_tab + nxt * kQuad * kWindow;
+                const double* const kpr = s_kp + nxt * kQuad * 4;
                 constexpr int kDepth = 4, kTotal = kQuad * kRPer;
                 double pfx[kDepth], pfy[kDepth], xa = 0.0, ya = 0.0;
                 uint4 pg[kDepth];
@@ -948,12 +957,12 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
                     if (i < kTotal) {
                         const int w = i / kRPer, sl = i % kDepth;
                         if (i % kRPer == 0) {
-                            xa = __dadd_rn(s_kp[4 * w + 0], __dmul_rn(s_kp[4 * w + 2], du));
-                            ya = __dadd_rn(s_kp[4 * w + 1], __dmul_rn(s_kp[4 * w + 3], du));
+                            xa = __dadd_rn(kpr[4 * w + 0], __dmul_rn(kpr[4 * w + 2], du));
+                            ya = __dadd_rn(kpr[4 * w + 1], __dmul_rn(kpr[4 * w + 3], du));
                         }
                         const int v = v0 + (i % kRPer) * kRRows;
                         if (v < kWindow) {                               // warp-uniform
-                            const double2 row = s_tab[w * kWindow + v];   // {s*dv, c*dv}
+                            const double2 row = tab[w * kWindow + v];   // {s*dv, c*dv}
                             const double sx = __dsub_rn(xa, row.x);
                             const double sy = __dadd_rn(ya, row.y);
                             int x0, y0;
