@@ -551,7 +551,8 @@ int clatch_take_keypoints(const double* kps, int cols, const int64_t* kept, size
     if (cols < 2 || cols > 4) return invalid("keypoints must be (N, 2..4): x, y[, theta[, score]]");
     if (m == 0) return CLATCH_OK;
     if (!kps || !kept || !out) return invalid("clatch_take_keypoints: null buffer");
-    const int parts = static_cast<int>(std::max<size_t>(1, std::min<size_t>(resolve_workers(workers), m / 4096)));
+    // (below ~16 k rows the gather costs less than waking a worker)
+    const int parts = static_cast<int>(std::max<size_t>(1, std::min<size_t>(resolve_workers(workers), m / 16384)));
     std::atomic<size_t> next{0};
     WorkerPool::instance().run(parts, [&](int) {
         for (;;) {
