@@ -69,29 +69,45 @@ def extract_images_sharded(images: Sequence, keypoints: Sequence, describe: Call
 
 def all_gather_descriptor_sets(local: dict, num_images: int, device=None):
     """The one exchange step before all-pairs matching (cfg5): every rank ends up with
-    every image's descriptors. `local` maps image index -> uint8 (M_i, B) array for the
-    images this rank extracted. Returns a list of num_images uint8 torch tensors on
-    `device` (the rank's GPU under NCCL, CPU under gloo)."""
+    every image's descriptors. `local` maps image index -> uint8 (M_i, B) array (numpy or
+    torch) for the images this rank extracted (image i lives on rank i mod world, as
+    extract_images_sharded deals them). One all_reduce of the row counts and ONE padded
+    all_gather_into_tensor of the rank's rows (131 MB in total at cfg5) — not a broadcast per
+    image. Returns a list of num_images uint8 torch tensors on `device` (the rank's GPU under
+    NCCL, CPU under gloo); entry i is a view into the gathered block."""
     import torch
     dist = _dist()
     rank, world = _world()
     device = device or torch.device("cpu")
-    nbytes = next((v.shape[1] for v in local.values()), 64)
+    nbytes = next((int(v.shape[1]) for v in local.values()), 64)
     counts = torch.zeros(num_images, dtype=torch.int64, device=device)
     for i, d in local.items():
         counts[i] = len(d)
     if world > 1:
         dist.all_reduce(counts)                       # each image is owned by exactly one rank
-    sets = []
-    for i in range(num_images):
-        owner = i % world
-        if i in local:
-            t = torch.as_tensor(np.ascontiguousarray(local[i]), device=device)
-        else:
-            t = torch.empty((int(counts[i]), nbytes), dtype=torch.uint8, device=device)
-        if world > 1:
-            dist.broadcast(t, src=owner)
-        sets.append(t)
+    counts = counts.cpu().tolist()
+    owned = [list(range(r, num_images, world)) for r in range(world)]
+    rows_of = [sum(counts[i] for i in owned[r]) for r in range(world)]
+    cap = max(max(rows_of), 1)
+    mine = torch.zeros((cap, nbytes), dtype=torch.uint8, device=device)
+    at = 0
+    for i in owned[rank]:
+        if counts[i]:
+            mine[at:at + counts[i]] = torch.as_tensor(np.ascontiguousarray(local[i]) if isinstance(local[i], np.ndarray)
+                                                      else local[i], device=device)
+        at += counts[i]
+    if world > 1:
+        flat = torch.empty((world * cap, nbytes), dtype=torch.uint8, device=device)
+        dist.all_gather_into_tensor(flat, mine)       # rank r's rows land at [r * cap, (r + 1) * cap)
+        block = flat.view(world, cap, nbytes)
+    else:
+        block = mine.unsqueeze(0)
+    sets = [None] * num_images
+    for r in range(world):
+        at = 0
+        for i in owned[r]:
+            sets[i] = block[r, at:at + counts[i]]
+            at += counts[i]
     return sets
 
 
@@ -113,22 +129,15 @@ def match_top2_sharded(queries, train, top2: Callable = default_top2, train_src:
     import torch
     dist = _dist()
     rank, world = _world()
-    if world > 1:
-        dist.broadcast(train, src=train_src)          # the single large message (N x 64 B)
     q_total = queries.shape[0]
     begin, end = shard_bounds(q_total, world)[rank]
+    if gather:
+        return match_top2_sharded_device(queries[begin:end], train, q_total, train_src, top2)
+    if world > 1:
+        dist.broadcast(train, src=train_src)          # the single large message (N x 64 B)
     local = top2(queries[begin:end], train) if end > begin else \
         torch.empty((3, 0), dtype=torch.int32, device=queries.device)
-    if not gather:
-        return local, (begin, end)
-    if world == 1:
-        return local
-    chunk = (q_total + world - 1) // world
-    padded = torch.zeros((3, chunk), dtype=torch.int32, device=queries.device)
-    padded[:, :end - begin] = local
-    parts = [torch.empty_like(padded) for _ in range(world)]
-    dist.all_gather(parts, padded)                    # 12 B per query
-    return torch.cat(parts, dim=1)[:, :q_total].contiguous()
+    return local, (begin, end)
 
 
 def match_all_pairs_sharded(desc_sets: Sequence, match_pair: Callable, num_images: int | None = None):
@@ -141,25 +150,84 @@ def match_all_pairs_sharded(desc_sets: Sequence, match_pair: Callable, num_image
 
 
 def match_all_pairs_resident(desc_sets: Sequence, ratio=None, cross_check=False, max_distance=None,
-                             num_images: int | None = None):
+                             num_images: int | None = None, resident: dict | None = None):
     """cfg5 on the CUDA path: this rank's share of the (i < j) pairs, batched through resident
     descriptor sets (each image is uploaded and expanded once, all pairs run in a few launches).
-    `desc_sets[i]` is a (M_i, 64) uint8 numpy array or CUDA tensor. Returns {(i, j): (M,4) int32}."""
+    `desc_sets[i]` is a (M_i, 64) uint8 numpy array or CUDA tensor; `resident` (from
+    create_resident_sets) skips the upload when the sets already live on the device.
+    Returns {(i, j): (M,4) int32}."""
     from .engine import get_engine
     rank, world = _world()
     n = num_images if num_images is not None else len(desc_sets)
     mine = pairs_for_rank(n, rank, world)
+    if not mine:
+        return {}
     eng = get_engine()
     needed = sorted({i for p in mine for i in p})
-    sets = {i: eng.create_set(desc_sets[i]) for i in needed}
+    sets = resident if resident is not None else {i: eng.create_set(desc_sets[i]) for i in needed}
     order = {i: k for k, i in enumerate(needed)}
     try:
         res = eng.match_set_pairs([sets[i] for i in needed], [(order[i], order[j]) for i, j in mine],
                                   ratio=ratio, cross_check=cross_check, max_distance=max_distance)
     finally:
-        for s in sets.values():
-            s.close()
+        if resident is None:
+            for s in sets.values():
+                s.close()
     return dict(zip(mine, res))          # views into one result block
+
+
+def create_resident_sets(desc_sets: Sequence, num_images: int | None = None) -> dict:
+    """Device-resident sets {image index: DescriptorSet} for the images this rank's pairs touch."""
+    from .engine import get_engine
+    rank, world = _world()
+    n = num_images if num_images is not None else len(desc_sets)
+    needed = sorted({i for p in pairs_for_rank(n, rank, world) for i in p})
+    eng = get_engine()
+    return {i: eng.create_set(desc_sets[i]) for i in needed}
+
+
+def match_sharded_host(queries: np.ndarray, train: np.ndarray, ratio=None, max_distance=None, train_src: int = 0):
+    """cfg4 end to end from HOST arrays: rank `train_src` uploads the train set and broadcasts it
+    over NCCL, every rank uploads only its own query block, matches it, and the (3, Q) top-2
+    triples are all-gathered; the reference's filter pass (src/match.cpp:69-79, ratio / max
+    distance) then runs on the gathered triples. Returns (M, 4) int32 rows like match()."""
+    import torch
+    from .engine import get_engine
+    rank, world = _world()
+    eng = get_engine()
+    dev = torch.device("cuda", eng.device)
+    q_total = len(queries)
+    begin, end = shard_bounds(q_total, world)[rank]
+    if world == 1:
+        bi, bd, sd = eng.match_top2(queries, train)
+    else:
+        d_train = torch.empty(train.shape, dtype=torch.uint8, device=dev)
+        if rank == train_src:
+            d_train.copy_(torch.from_numpy(train))
+        d_q = torch.from_numpy(np.ascontiguousarray(queries[begin:end])).to(dev)
+        full = match_top2_sharded_device(d_q, d_train, q_total, train_src).cpu().numpy()
+        bi, bd, sd = full[0], full[1], full[2]
+    return eng.filter_matches(bi, bd, sd, ratio=ratio, max_distance=max_distance)
+
+
+def match_top2_sharded_device(q_shard, train, q_total: int, train_src: int = 0, top2: Callable = default_top2):
+    """The collective part of cfg4 on device tensors: `q_shard` holds this rank's contiguous query
+    block (shard_bounds(q_total, world)[rank]), `train` is valid on `train_src` and is broadcast in
+    place; returns the full (3, q_total) int32 result on every rank."""
+    import torch
+    dist = _dist()
+    rank, world = _world()
+    if world > 1:
+        dist.broadcast(train, src=train_src)
+    local = top2(q_shard, train) if q_shard.shape[0] else torch.empty((3, 0), dtype=torch.int32, device=train.device)
+    if world == 1:
+        return local
+    chunk = (q_total + world - 1) // world
+    padded = torch.zeros((3, chunk), dtype=torch.int32, device=train.device)
+    padded[:, :local.shape[1]] = local
+    flat = torch.empty((world * 3, chunk), dtype=torch.int32, device=train.device)
+    dist.all_gather_into_tensor(flat, padded)             # 12 B per query
+    return flat.view(world, 3, chunk).permute(1, 0, 2).reshape(3, world * chunk)[:, :q_total].contiguous()
 
 
 def default_match_pair(ratio=None, cross_check=False, max_distance=None):
