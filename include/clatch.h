@@ -83,10 +83,15 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * key "upload_bands": clatch_describe_all_f64 uploads a big float64 frame in this many row bands and
  * extracts each band's keypoints while the next band is in flight (0 = choose by frame size, the
  * default; 1 = one piece; up to 6). Results never depend on it.
- * key "host_promote": 1 lets clatch_describe_all_f64 convert a float64 image whose pixels are all
- * integers in [0, 255] to u8 on the host workers before the upload (8x fewer bytes over the bus;
- * lossless, same descriptors); 0 (default) uploads the doubles and classifies on the device —
- * faster wherever the host reads its memory more slowly than PCIe 5 carries it.
+ * key "host_promote": clatch_describe_all_f64 / clatch_describe_batch_f64 can convert a float64 image
+ * whose pixels are all integers in [0, 255] to u8 on the host workers before the upload (8x fewer
+ * bytes over the bus; lossless, same descriptors). 0 (default) does so when the image lies in ordinary
+ * pageable memory — which the driver could only copy through its own bounce buffers — and uploads the
+ * doubles of a page-locked image as they are (classified on the device); 1 = always, 2 = never.
+ * key "match_streamk": 1 (default) lets the tensor-core matcher split small problems (expanded train set
+ * within 32 MB) into equal shares of (query tile, train tile) units per CTA; 0 keeps whole rounds.
+ * key "pairs_filter_on_device": 1 (default) runs the ratio / max-distance / cross-check decisions of
+ * clatch_match_set_pairs on the device so only surviving rows cross the bus; 0 filters on the host.
  * key "extract_stats": non-zero starts counting variant 2's exact recomputes (and zeroes the
  * counters), 0 stops. Unknown keys fail with CLATCH_ERR_INVALID. */
 CLATCH_API int clatch_set_option(clatch_ctx* ctx, const char* key, int value);

@@ -92,8 +92,7 @@ def describe(image, keypoints, pattern=None, workers=0):
     pat = pattern_from_text(pattern)
     kps = _keypoint_array(keypoints)
     eng = get_engine()
-    eng.set_pattern(pat)
-    kept, desc = eng.describe_all(img, kps, workers)
+    kept, desc = eng.describe_all(img, kps, workers, pattern=pat)     # pattern installed under the launch's lock
     return eng.take_keypoints(kps, kept, workers), desc
 
 
@@ -112,8 +111,7 @@ def describe_batch(images, keypoints, pattern=None, workers=0):
     if any(k.shape[1] != widest for k in kps):
         kps = [np.hstack([k, np.zeros((len(k), widest - k.shape[1]))]) for k in kps]
     eng = get_engine()
-    eng.set_pattern(pat)
-    res = eng.describe_batch(imgs, kps, workers)
+    res = eng.describe_batch(imgs, kps, workers, pattern=pat)
     return [(eng.take_keypoints(k, kept, workers), desc) for k, (kept, desc) in zip(kps, res)]
 
 

@@ -219,6 +219,18 @@ bool promote_rows_u8(const double* src, size_t src_pitch, uint8_t* dst, size_t d
     return true;
 }
 
+// Should this float64 host image be promoted to u8 by the host workers (clatch_ctx::host_promote)?
+bool want_host_promote(const clatch_ctx* ctx, const void* img) {
+    if (ctx->host_promote == 1) return true;
+    if (ctx->host_promote == 2) return false;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, img) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return attr.type == cudaMemoryTypeUnregistered;   // ordinary malloc'd / numpy memory
+}
+
 // WeightMask::seven_by_seven (src/pattern.cpp:28-35): ones on the top-left 7x7, zero last row/col.
 bool is_seven_by_seven(const std::vector<double>& w, int K) {
     if (K != 8) return false;
@@ -284,13 +296,14 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
     for (DeviceBuffer* b : {&ctx->img, &ctx->kps, &ctx->desc, &ctx->q, &ctx->t, &ctx->res,
                             &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->items, &ctx->scores, &ctx->counts, &ctx->det, &ctx->pattern.slots, &ctx->pattern.slots_quad,
                             &ctx->pattern.slots_f8, &ctx->extract_stats, &ctx->filt_pairs, &ctx->filt_rows, &ctx->filt_out,
-                            &ctx->filt_counts, &ctx->pattern.triplets})
+                            &ctx->filt_counts, &ctx->pattern.triplets, &ctx->pattern.d_weights})
         b->release();
     for (auto& t : ctx->tex_images) {
         if (t.tex) cudaDestroyTextureObject(t.tex);
         if (t.surf) cudaDestroySurfaceObject(t.surf);
         if (t.array) cudaFreeArray(t.array);
     }
+    if (ctx->scratch_event) cudaEventDestroy(ctx->scratch_event);
     ctx->pinned.release();
     ctx->pin_img.release();
     ctx->pin_xycs.release();
@@ -306,6 +319,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
             b->release();
         ctx->pipe[s].h_xycs.release();
         ctx->pipe[s].h_desc.release();
+        ctx->pipe[s].h_img.release();
         if (ctx->pipe[s].stream) cudaStreamDestroy(ctx->pipe[s].stream);
     }
     delete ctx;
@@ -347,8 +361,9 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         ctx->match_streamk = value != 0;
         return CLATCH_OK;
     }
-    if (std::strcmp(key, "host_promote") == 0) {   // describe_all: float64 -> u8 on the host workers when lossless
-        ctx->host_promote = value != 0;
+    if (std::strcmp(key, "host_promote") == 0) {   // float64 -> u8 on the host workers when lossless: 0 auto, 1 always, 2 never
+        if (value < 0 || value > 2) return invalid("host_promote must be 0 (pageable sources), 1 (always) or 2 (never)");
+        ctx->host_promote = value;
         return CLATCH_OK;
     }
     if (std::strcmp(key, "extract_stats") == 0) {   // count exact recomputes of the filtered kernel
@@ -444,6 +459,7 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
     }
 
     CLATCH_CUDA(cudaSetDevice(ctx->device));
+    CLATCH_CUDA(cudaDeviceSynchronize());   // kernels queued on any stream may still read the tables replaced below
     Pattern& pat = ctx->pattern;
     pat.T = T;
     pat.K = K;
@@ -451,7 +467,8 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
     pat.fast = (T == kFastT) && is_seven_by_seven(w, K);
     if (int rc = pat.triplets.reserve(sizeof(int16_t) * 6 * T)) return rc;
     CLATCH_CUDA(cudaMemcpy(pat.triplets.ptr, triplets, sizeof(int16_t) * 6 * T, cudaMemcpyHostToDevice));
-    if (int rc = upload_weights(w.data(), K * K)) return rc;
+    if (int rc = pat.d_weights.reserve(sizeof(double) * w.size())) return rc;
+    CLATCH_CUDA(cudaMemcpy(pat.d_weights.ptr, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
     pat.host_triplets.assign(triplets, triplets + 6 * static_cast<size_t>(T));
     pat.slots_planned = false;
     if (pat.fast) {
@@ -667,6 +684,21 @@ static int describe_all_bands_f64(clatch_ctx* ctx, const double* img, int width,
                                   const double* kps, size_t n, int cols, int workers, int64_t* kept, uint8_t* out,
                                   size_t* m, int bands);
 
+// promote_rows_u8 over the whole image on the host workers; false if some pixel is not a u8 value.
+static bool promote_image_u8(const double* img, size_t pitch, uint8_t* staged, size_t upitch, int width, int height,
+                             int workers) {
+    const int parts = std::max(1, std::min(resolve_workers(workers), height / 8));
+    std::vector<int> ok(parts, 0);
+    const int rows = (height + parts - 1) / parts;
+    WorkerPool::instance().run(parts, [&](int w) {
+        const int r0 = std::min(height, w * rows), r1 = std::min(height, r0 + rows);
+        ok[w] = promote_rows_u8(img, pitch, staged, upitch, width, r0, r1);
+    });
+    for (int v : ok)
+        if (!v) return false;
+    return true;
+}
+
 template <typename Pixel>
 static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int height, size_t pitch,
                              const double* kps, size_t n, int cols, int workers, int64_t* kept,
@@ -679,22 +711,13 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
     if (!kps || !kept || !out) return invalid("describe_all: null keypoint/output buffer");
     CLATCH_CUDA(cudaSetDevice(ctx->device));
     constexpr bool kU8 = sizeof(Pixel) == 1;
-    if (!kU8 && ctx->host_promote && n >= 256) {
+    if (!kU8 && n >= 256 && want_host_promote(ctx, img)) {
         // float64 image: try the lossless u8 promotion on the host workers first (page-locked
         // staging); a non-u8-valued image stops at its first such pixel and takes the f64 route.
         const size_t upitch = (static_cast<size_t>(width) + 15) / 16 * 16;
         if (int rc = ctx->pin_img.reserve(upitch * height)) return rc;
         uint8_t* const staged = static_cast<uint8_t*>(ctx->pin_img.ptr);
-        const int parts = std::max(1, std::min(resolve_workers(workers), height / 8));
-        std::vector<int> ok(parts, 0);
-        const int rows = (height + parts - 1) / parts;
-        WorkerPool::instance().run(parts, [&](int w) {
-            const int r0 = std::min(height, w * rows), r1 = std::min(height, r0 + rows);
-            ok[w] = promote_rows_u8(reinterpret_cast<const double*>(img), pitch, staged, upitch, width, r0, r1);
-        });
-        bool all = true;
-        for (int v : ok) all = all && v;
-        if (all)
+        if (promote_image_u8(reinterpret_cast<const double*>(img), pitch, staged, upitch, width, height, workers))
             return describe_all_impl<uint8_t>(ctx, staged, width, height, upitch, kps, n, cols, workers, kept, out, m);
     }
     if (!kU8) {
@@ -899,7 +922,10 @@ static int describe_all_bands_f64(clatch_ctx* ctx, const double* img, int width,
     ctx->extract_out_index = reinterpret_cast<const unsigned*>(d_rec + rec_bytes);
     for (int b = 0; b < bands && !rc; ++b) {
         const int r0 = b == 0 ? 0 : row_end[b - 1], r1 = row_end[b];
-        CLATCH_CUDA(cudaStreamWaitEvent(st, ctx->band_events[b], 0));
+        if (cudaError_t e = cudaStreamWaitEvent(st, ctx->band_events[b], 0); e != cudaSuccess) {
+            rc = cuda_fail(e, "cudaStreamWaitEvent(band)");
+            break;
+        }
         rc = launch_classify_rows(ctx, ctx->img.as<double>(), width, height, dpitch, r0, r1, b == 0, st);
         const size_t cnt = begin[b + 1] - begin[b];
         if (!rc && cnt > 0) {
@@ -971,6 +997,16 @@ static int detect_impl(clatch_ctx* ctx, const Pixel* img, int width, int height,
 
 // Two-slot software pipeline over images: slot = i % 2 owns a stream and its own device
 // scratch, so image i+1 uploads / prepares while image i computes and downloads.
+// Inside describe_batch's image loop a CUDA failure must not return: the other pipeline stream may still
+// be writing into caller arrays and a slot may hold a pending copy. Record it and leave through the
+// common epilogue, which drains both streams and clears the pending state.
+#define BATCH_CUDA(expr)                                    \
+    if (cudaError_t e_ = (expr); e_ != cudaSuccess) {       \
+        rc = ::clatch::cuda_fail(e_, #expr);                \
+        break;                                              \
+    } else                                                  \
+        (void)0
+
 template <typename Pixel>
 static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const int* widths, const int* heights,
                                const size_t* pitches, const double* const* kps, const size_t* counts, int cols,
@@ -1012,23 +1048,34 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         // the slot's previous image (i-2) must have left its buffers before they are reused;
         // its descriptors wait in page-locked staging and move to the caller's array now
         trace.stamp("batch: image begins");
-        CLATCH_CUDA(cudaStreamSynchronize(st));
+        BATCH_CUDA(cudaStreamSynchronize(st));
         trace.stamp("batch: slot free");
         if (slot.pending_out) {
             std::memcpy(slot.pending_out, slot.h_desc.ptr, slot.pending_bytes);
             slot.pending_out = nullptr;
         }
         const size_t dpitch = kU8 ? (static_cast<size_t>(w) + 15) / 16 * 16 : static_cast<size_t>(w);
-        if ((rc = slot.img.reserve(sizeof(Pixel) * dpitch * h))) break;
+        const size_t u8_pitch = (static_cast<size_t>(w) + 15) / 16 * 16;
         if ((rc = slot.kps.reserve(sizeof(double) * 4 * n))) break;
         if ((rc = slot.desc.reserve(bytes * n))) break;
+        bool promoted = false;   // float64 image sent up as its lossless u8 copy (host workers, page-locked staging)
         if (!kU8) {
-            const size_t u8_pitch = (static_cast<size_t>(w) + 15) / 16 * 16;
             if ((rc = slot.img_u8.reserve(u8_pitch * h))) break;
             if ((rc = slot.flags.reserve(sizeof(int)))) break;
+            if (n >= 256 && want_host_promote(ctx, imgs[i])) {
+                if ((rc = slot.h_img.reserve(u8_pitch * h))) break;
+                promoted = promote_image_u8(reinterpret_cast<const double*>(imgs[i]), pitches[i],
+                                            static_cast<uint8_t*>(slot.h_img.ptr), u8_pitch, w, h, workers);
+                trace.stamp(promoted ? "batch: image promoted to u8 on the host" : "batch: image is not u8-valued");
+            }
         }
-        CLATCH_CUDA(cudaMemcpy2DAsync(slot.img.ptr, sizeof(Pixel) * dpitch, imgs[i], sizeof(Pixel) * pitches[i],
-                                      sizeof(Pixel) * w, h, cudaMemcpyHostToDevice, st));
+        if (promoted) {
+            BATCH_CUDA(cudaMemcpyAsync(slot.img_u8.ptr, slot.h_img.ptr, u8_pitch * h, cudaMemcpyHostToDevice, st));
+        } else {
+            if ((rc = slot.img.reserve(sizeof(Pixel) * dpitch * h))) break;
+            BATCH_CUDA(cudaMemcpy2DAsync(slot.img.ptr, sizeof(Pixel) * dpitch, imgs[i], sizeof(Pixel) * pitches[i],
+                                         sizeof(Pixel) * w, h, cudaMemcpyHostToDevice, st));
+        }
         if ((rc = slot.h_xycs.reserve(sizeof(double) * 4 * n))) break;
         if ((rc = slot.h_desc.reserve(bytes * n))) break;
         double* const xycs = static_cast<double*>(slot.h_xycs.ptr);
@@ -1037,17 +1084,22 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         trace.stamp("batch: keypoints prepared");
         m[i] = count;
         if (count == 0) continue;
-        CLATCH_CUDA(cudaMemcpyAsync(slot.kps.ptr, xycs, sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
+        BATCH_CUDA(cudaMemcpyAsync(slot.kps.ptr, xycs, sizeof(double) * 4 * count, cudaMemcpyHostToDevice, st));
         if (trace.on) cudaEventRecord(bev[3 * i], st);
         if (kU8) {
             rc = launch_extract_u8(ctx, slot.img.template as<uint8_t>(), w, h, dpitch, slot.kps.template as<double>(),
+                                   count, slot.desc.template as<uint8_t>(), st);
+        } else if (promoted) {
+            rc = launch_extract_u8(ctx, slot.img_u8.template as<uint8_t>(), w, h, u8_pitch, slot.kps.template as<double>(),
                                    count, slot.desc.template as<uint8_t>(), st);
         } else {
             // the f64 launcher uses ctx-level promotion scratch: point it at this slot's buffers
             std::swap(ctx->img_u8, slot.img_u8);
             std::swap(ctx->flags, slot.flags);
+            ctx->scratch_private = true;
             rc = launch_extract_f64(ctx, slot.img.template as<double>(), w, h, dpitch, slot.kps.template as<double>(),
                                     count, slot.desc.template as<uint8_t>(), st);
+            ctx->scratch_private = false;
             std::swap(ctx->img_u8, slot.img_u8);
             std::swap(ctx->flags, slot.flags);
         }
@@ -1061,9 +1113,9 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         const bool direct = cudaPointerGetAttributes(&attr, out[i]) == cudaSuccess && attr.type == cudaMemoryTypeHost;
         if (!direct) cudaGetLastError();   // an unregistered pointer is not an error here
         if (direct) {
-            CLATCH_CUDA(cudaMemcpyAsync(out[i], slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+            BATCH_CUDA(cudaMemcpyAsync(out[i], slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
         } else {
-            CLATCH_CUDA(cudaMemcpyAsync(slot.h_desc.ptr, slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
+            BATCH_CUDA(cudaMemcpyAsync(slot.h_desc.ptr, slot.desc.ptr, bytes * count, cudaMemcpyDeviceToHost, st));
             slot.pending_out = out[i];
             slot.pending_bytes = bytes * count;
         }

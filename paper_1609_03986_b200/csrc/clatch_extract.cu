@@ -37,10 +37,6 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// Mask weights for the generic kernel: read with a warp-uniform index, so the
-// constant cache broadcasts them.
-__constant__ double c_weights[kMaxConstWeights];
-
 struct ExtractParams {
     const void* img;
     int width, height;
@@ -50,6 +46,7 @@ struct ExtractParams {
     uint8_t* out;              // M x T/8
     const ushort4* slots;      // fast kernel: T x {a, b, c, bit}
     const short* triplets;     // generic kernel: T x 6
+    const double* weights;     // generic kernel: K x K mask weights (per-context device copy; warp-uniform reads)
     int T, K;
     const int* flags;          // optional device flags (f64 promotion), may be null
     int run_if_flag;           // run only when flags[0] == run_if_flag (if flags != null)
@@ -1073,7 +1070,7 @@ __global__ void __launch_bounds__(kThreads, 2) extract_generic_kernel(ExtractPar
             double d1 = 0.0, d2 = 0.0;
             for (int r = 0; r < K; ++r) {
                 for (int col = 0; col < K; ++col) {
-                    const double w = c_weights[r * K + col];
+                    const double w = __ldg(p.weights + r * K + col);
                     const double a = pa[col];
                     const double e1 = __dsub_rn(a, pb[col]);
                     const double e2 = __dsub_rn(a, pc[col]);
@@ -1091,28 +1088,35 @@ __global__ void __launch_bounds__(kThreads, 2) extract_generic_kernel(ExtractPar
             unsigned byte = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) byte |= (s_dynbits[8 * b + i] ? 1u : 0u) << i;
-            p.out[kp * (T / 8) + b] = static_cast<uint8_t>(byte);
+            const unsigned long long row = p.out_index ? p.out_index[kp] : kp;
+            p.out[row * (T / 8) + b] = static_cast<uint8_t>(byte);
         }
     }
 }
 
-// f64 -> u8 promotion: flags[0] = 1 if some pixel is not an integer in [0, 255]
-// (or not finite), else stays 0; dst receives the (lossless when flags[0]==0) u8 copy.
+// f64 -> u8 promotion: flags[0] = 0 while every pixel seen is an integer in [0, 255]; 1 once some pixel
+// is not; 2 once some pixel is NaN, infinite or beyond 2^1000 in magnitude. dst receives the (lossless
+// when flags[0]==0) u8 copy. Class 2 matters because the specialised kernels skip the mask's zero-weight
+// pixels, which is exact only while every patch difference e is finite (0*e*e = 0): the reference
+// multiplies them in (src/descriptor.cpp:66-71), so one NaN or an overflowing a - b under a masked
+// pixel poisons its sum. Such images take the generic kernel, which evaluates (w*e)*e literally.
 // Rows [row0, row1) only, so an image that arrives in row bands can be classified band by band;
 // the flag accumulates ("some pixel seen so far is not a u8 value").
 __global__ void classify_convert_kernel(const double* src, size_t src_pitch, uint8_t* dst,
                                         size_t dst_pitch, int width, int row0, int row1, int* flags) {
     const size_t n = static_cast<size_t>(width) * (row1 - row0);
-    bool bad = false;
+    int cls = 0;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int yy = row0 + static_cast<int>(i / width), xx = static_cast<int>(i % width);
         const double v = src[static_cast<size_t>(yy) * src_pitch + xx];
         const bool ok = (v >= 0.0) && (v <= 255.0) && (v == floor(v));   // NaN/inf fail
-        bad |= !ok;
+        const bool tame = fabs(v) <= 0x1p1000;                            // NaN fails
+        cls = max(cls, tame ? (ok ? 0 : 1) : 2);
         dst[static_cast<size_t>(yy) * dst_pitch + xx] = ok ? static_cast<uint8_t>(v) : 0;
     }
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1);
+    cls = __reduce_max_sync(0xffffffffu, cls);
+    if (cls != 0 && (threadIdx.x & 31) == 0) atomicMax(flags, cls);
 }
 
 int grid_for(const clatch_ctx* ctx, size_t M, int ctas_per_sm) {
@@ -1194,7 +1198,7 @@ int ensure_single_window_plan(clatch_ctx* ctx) {
 template <bool kU8>
 int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, size_t pitch,
                    const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream,
-                   const int* flags, int run_if_flag) {
+                   const int* flags, int run_if_flag, bool force_generic = false) {
     const Pattern& pat = ctx->pattern;
     ExtractParams p{};
     p.img = d_img;
@@ -1206,13 +1210,16 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     p.out = d_out;
     p.slots = pat.slots.as<ushort4>();
     p.triplets = pat.triplets.as<short>();
+    p.weights = pat.d_weights.as<double>();
     p.T = pat.T;
     p.K = pat.K;
     p.flags = flags;
     p.run_if_flag = run_if_flag;
     p.stats = ctx->extract_stats_on ? ctx->extract_stats.as<unsigned long long>() : nullptr;
     p.out_index = ctx->extract_out_index;   // honoured by the quad and pipelined kernels (extract_supports_out_index)
-    if (kU8 && pat.fast && ctx->extract_variant >= 3) {
+    if (force_generic) {
+        extract_generic_kernel<kU8><<<grid_for(ctx, M, 2), kThreads, pat.T, stream>>>(p);
+    } else if (kU8 && pat.fast && ctx->extract_variant >= 3) {
         if (!ctx->pipe_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kPipeSmemBytes));
@@ -1282,11 +1289,6 @@ bool extract_supports_out_index(const clatch_ctx* ctx) {
     return ctx->pattern.fast && (ctx->extract_variant == 3 || ctx->extract_variant == 4);
 }
 
-int upload_weights(const double* w, int count) {
-    CLATCH_CUDA(cudaMemcpyToSymbol(c_weights, w, sizeof(double) * count));
-    return CLATCH_OK;
-}
-
 int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,
                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream) {
     if (M == 0) return CLATCH_OK;
@@ -1304,7 +1306,10 @@ int launch_classify_rows(clatch_ctx* ctx, const double* d_img, int width, int he
     if (int rc = ctx->img_u8.reserve(u8_pitch * height)) return rc;
     if (int rc = ctx->flags.reserve(sizeof(int))) return rc;
     int* flags = ctx->flags.as<int>();
-    if (reset) CLATCH_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), stream));
+    if (reset) {
+        if (int rc = scratch_acquire(ctx, stream)) return rc;   // img_u8 / flags may still be read on another stream
+        CLATCH_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), stream));
+    }
     if (row1 <= row0) return CLATCH_OK;
     classify_convert_kernel<<<ctx->sm_count * 8, 256, 0, stream>>>(d_img, pitch, ctx->img_u8.as<uint8_t>(), u8_pitch,
                                                                    width, row0, row1, flags);
@@ -1321,7 +1326,10 @@ int launch_extract_f64_classified(clatch_ctx* ctx, const double* d_img, int widt
     if (int rc = launch_extract<true>(ctx, ctx->img_u8.ptr, width, height, u8_pitch, d_xycs, M, d_out,
                                       stream, flags, 0))
         return rc;
-    return launch_extract<false>(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, flags, 1);
+    if (int rc = launch_extract<false>(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, flags, 1)) return rc;
+    // class 2 (non-finite or huge pixels): the literal (w*e)*e kernel, whatever the pattern
+    if (int rc = launch_extract<false>(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, flags, 2, true)) return rc;
+    return scratch_release(ctx, stream);
 }
 
 int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,

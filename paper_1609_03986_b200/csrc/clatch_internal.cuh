@@ -60,6 +60,7 @@ struct Pattern {
     std::vector<int16_t> host_triplets;   // T * 6, for plans made on first use
     bool slots_planned = false;    // `slots` holds a plan for the current table
     DeviceBuffer triplets;         // generic kernel: T * 6 int16
+    DeviceBuffer d_weights;        // generic kernel: K*K mask weights (per context, not a module-level __constant__)
     std::vector<double> weights;   // K*K
     double slot_degree = 0.0;           // planned / table-order shared-load conflict degree
     double slot_degree_identity = 0.0;
@@ -97,6 +98,14 @@ struct clatch_ctx {
     bool pairs_filter_on_device = true;   // clatch_match_set_pairs: ratio / max / cross-check decisions on the device
     bool match_streamk = true;     // tensor matcher: equal-share partition for small problems (set_option "match_streamk")
     int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
+    // The scratch below is shared by every call on this context, whatever stream the call queues on
+    // (the *_dev entry points take the caller's stream). scratch_event marks the last use; a call on a
+    // different stream waits for it first (clatch::scratch_acquire / scratch_release), so two device-form
+    // calls on different streams — or a device-form call followed by a host-form one — are ordered.
+    cudaEvent_t scratch_event = nullptr;
+    cudaStream_t scratch_stream = nullptr;
+    bool scratch_used = false;
+    bool scratch_private = false;   // describe_batch has swapped in a pipeline slot's own buffers: no guard
     // scratch for the host-buffer entry points
     clatch::DeviceBuffer img, kps, desc, q, t, res, partial, flags, img_u8, exp_q, exp_t, items, scores, counts, det;
     clatch::DeviceBuffer filt_pairs, filt_rows, filt_out, filt_counts;   // on-device filter pass of batched set pairs
@@ -107,13 +116,17 @@ struct clatch_ctx {
     clatch::PinnedBuffer pinned;     // D2H staging for batched pair results
     clatch::PinnedBuffer pin_xycs, pin_desc;   // describe_all staging (banded upload path)
     clatch::PinnedBuffer pin_img;              // describe_all: host-promoted u8 copy of a float64 image
-    bool host_promote = false;   // measured slower than the 16.6 MB DMA on the B200 host (profiles/r1y_e2e_breakdown.log)
+    // float64 -> u8 on the host workers before the upload: 0 = when the image lies in ordinary (pageable)
+    // memory (the driver would stage such a copy through its own bounce buffers at ~12 GB/s; reading it
+    // once with the workers and sending 1 byte per pixel is faster), 1 = always, 2 = never. For page-locked
+    // sources the plain DMA of the doubles won (profiles/r1y_e2e_breakdown.log).
+    int host_promote = 0;
     cudaStream_t copy_stream = nullptr;        // image bands stream in here while kernels run on `stream`
     cudaEvent_t band_events[8] = {};
     struct PipeSlot {                // describe_batch: one of two pipeline slots
         cudaStream_t stream = nullptr;
         clatch::DeviceBuffer img, kps, desc, img_u8, flags;
-        clatch::PinnedBuffer h_xycs, h_desc;   // page-locked staging
+        clatch::PinnedBuffer h_xycs, h_desc, h_img;   // page-locked staging (h_img: host-promoted u8 copy of a float64 image)
         uint8_t* pending_out = nullptr;         // caller array awaiting h_desc
         size_t pending_bytes = 0;
     } pipe[2];
@@ -121,8 +134,21 @@ struct clatch_ctx {
 
 namespace clatch {
 
+inline int scratch_acquire(clatch_ctx* ctx, cudaStream_t st) {
+    if (ctx->scratch_private) return CLATCH_OK;
+    if (ctx->scratch_used && ctx->scratch_stream != st) CLATCH_CUDA(cudaStreamWaitEvent(st, ctx->scratch_event, 0));
+    return CLATCH_OK;
+}
+inline int scratch_release(clatch_ctx* ctx, cudaStream_t st) {
+    if (ctx->scratch_private) return CLATCH_OK;
+    if (!ctx->scratch_event) CLATCH_CUDA(cudaEventCreateWithFlags(&ctx->scratch_event, cudaEventDisableTiming));
+    CLATCH_CUDA(cudaEventRecord(ctx->scratch_event, st));
+    ctx->scratch_stream = st;
+    ctx->scratch_used = true;
+    return CLATCH_OK;
+}
+
 // extraction (clatch_extract.cu)
-int upload_weights(const double* w, int count);
 bool extract_supports_out_index(const clatch_ctx* ctx);
 int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,
                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);

@@ -366,10 +366,24 @@ void launch_merge_partials(const Partial* partial, unsigned long long Q, int spl
                                                                                       best_idx, best_dist, second_dist);
 }
 
+static int match_top2_on(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
+                         int bytes, int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second,
+                         cudaStream_t stream);
+
+// The matcher's operands and partials (exp_q, exp_t, partial) are context scratch: order this use
+// behind the previous one when it ran on another stream.
 int launch_match_top2(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
                       int bytes, int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second,
                       cudaStream_t stream) {
     if (Q == 0) return CLATCH_OK;
+    if (int rc = scratch_acquire(ctx, stream)) return rc;
+    if (int rc = match_top2_on(ctx, d_q, Q, d_t, N, bytes, d_best_idx, d_best_dist, d_second, stream)) return rc;
+    return scratch_release(ctx, stream);
+}
+
+static int match_top2_on(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
+                         int bytes, int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second,
+                         cudaStream_t stream) {
     const bool tiled = bytes == kDescBytes && reinterpret_cast<uintptr_t>(d_q) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(d_t) % 16 == 0;
     if (!tiled) {

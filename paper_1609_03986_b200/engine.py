@@ -116,7 +116,7 @@ class Engine:
         self.device = int(device)
         self._pattern_key = None
         self._pattern = None
-        self._lock = threading.Lock()
+        self._lock = threading.RLock()      # serialises every ABI call on this context (and its pattern)
         self._pinned = _PinnedPool(self.lib)
         sm, khz = C.c_int(), C.c_int()
         name = C.create_string_buffer(256)
@@ -136,17 +136,21 @@ class Engine:
 
     # ---- pattern ---------------------------------------------------------
     def set_pattern(self, pattern: TripletPattern | None = None) -> TripletPattern:
+        """Install `pattern` (None = the built-in table) on the context. The pattern is context state:
+        callers that must extract with a particular pattern pass it to describe_all / describe_batch /
+        extract, which install it and launch under one hold of the context lock."""
         pattern = pattern or default_pattern()
-        if pattern is self._pattern:
-            return pattern
-        key = pattern.key()
-        if key != self._pattern_key:
-            trip = np.ascontiguousarray(pattern.triplets, np.int16)
-            w = np.ascontiguousarray(pattern.weights, np.float64)
-            _lib.check(self.lib.clatch_set_pattern(self.ctx, _ptr(trip, i16p), pattern.bit_count,
-                                                   pattern.patch_size, _ptr(w, f64p)))
-            self._pattern_key = key
-        self._pattern = pattern
+        with self._lock:
+            if pattern is self._pattern:
+                return pattern
+            key = pattern.key()
+            if key != self._pattern_key:
+                trip = np.ascontiguousarray(pattern.triplets, np.int16)
+                w = np.ascontiguousarray(pattern.weights, np.float64)
+                _lib.check(self.lib.clatch_set_pattern(self.ctx, _ptr(trip, i16p), pattern.bit_count,
+                                                       pattern.patch_size, _ptr(w, f64p)))
+                self._pattern_key = key
+            self._pattern = pattern
         return pattern
 
     @property
@@ -197,9 +201,7 @@ class Engine:
                radius: int = 15) -> np.ndarray:
         """FAST-9 (+ NMS, + intensity-centroid angle) -> (N, 4) float64 [x, y, theta, score]."""
         h, w = image.shape
-        if image.strides[1] != image.itemsize or image.strides[0] % image.itemsize:
-            image = np.ascontiguousarray(image)
-        pitch = image.strides[0] // image.itemsize
+        image, pitch = self._rows(image)
         if image.dtype == np.uint8:
             fn, ptr = self.lib.clatch_detect_u8, _ptr(image, u8p)
         elif image.dtype == np.float64:
@@ -220,18 +222,28 @@ class Engine:
             return out[:count.value].copy()
 
     # ---- extraction, host buffers --------------------------------------------
-    def extract(self, image: np.ndarray, xycs: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
-        """image: 2-D uint8 or float64 (rows may be strided); xycs from prepare_keypoints."""
-        nbytes = self.descriptor_bytes
-        m = len(xycs)
-        if out is None:
-            out = np.empty((m, nbytes), np.uint8)
+    @staticmethod
+    def _rows(image: np.ndarray):
+        """(image with unit inner stride and a positive whole-element row pitch, pitch in elements).
+        Anything else — transposed, negative or overlapping strides (img[::-1], broadcast views) — is copied."""
         h, w = image.shape
-        if image.strides[1] != image.itemsize or image.strides[0] % image.itemsize:
+        if (image.strides[1] != image.itemsize or image.strides[0] % image.itemsize
+                or image.strides[0] < w * image.itemsize):
             image = np.ascontiguousarray(image)
-        pitch = image.strides[0] // image.itemsize
+        return image, image.strides[0] // image.itemsize
+
+    def extract(self, image: np.ndarray, xycs: np.ndarray, out: np.ndarray | None = None,
+                pattern: TripletPattern | None = None) -> np.ndarray:
+        """image: 2-D uint8 or float64 (rows may be strided); xycs from prepare_keypoints."""
+        m = len(xycs)
+        h, w = image.shape
+        image, pitch = self._rows(image)
         xycs = np.ascontiguousarray(xycs, np.float64)
         with self._lock:
+            if pattern is not None:
+                self.set_pattern(pattern)
+            if out is None:
+                out = np.empty((m, self.descriptor_bytes), np.uint8)
             if image.dtype == np.uint8:
                 rc = self.lib.clatch_extract_u8(self.ctx, _ptr(image, u8p), w, h, pitch,
                                                 _ptr(xycs, f64p), m, _ptr(out, u8p))
@@ -243,18 +255,21 @@ class Engine:
         _lib.check(rc)
         return out
 
-    def describe_all(self, image: np.ndarray, keypoints: np.ndarray, workers: int = 0):
-        """describe_all in one ABI call: -> (kept int64 (M,), descriptors uint8 (M, T/8))."""
+    def describe_all(self, image: np.ndarray, keypoints: np.ndarray, workers: int = 0,
+                     pattern: TripletPattern | None = None):
+        """describe_all in one ABI call: -> (kept int64 (M,), descriptors uint8 (M, T/8)). `pattern`
+        (when given) is installed under the same hold of the context lock as the launch, so concurrent
+        callers with different patterns cannot swap it in between."""
         h, w = image.shape
-        if image.strides[1] != image.itemsize or image.strides[0] % image.itemsize:
-            image = np.ascontiguousarray(image)
-        pitch = image.strides[0] // image.itemsize
+        image, pitch = self._rows(image)
         kps = np.ascontiguousarray(keypoints, np.float64)
         n, cols = kps.shape
         kept = np.empty(n, np.int64)
-        out = self._pinned.empty((n, self.descriptor_bytes), np.uint8)
         m = C.c_size_t()
         with self._lock:
+            if pattern is not None:
+                self.set_pattern(pattern)
+            out = self._pinned.empty((n, self.descriptor_bytes), np.uint8)
             if image.dtype == np.uint8:
                 rc = self.lib.clatch_describe_all_u8(self.ctx, _ptr(image, u8p), w, h, pitch, _ptr(kps, f64p),
                                                      n, cols, workers, _ptr(kept, i64p), _ptr(out, u8p),
@@ -268,7 +283,7 @@ class Engine:
         _lib.check(rc)
         return kept[:m.value], out[:m.value]
 
-    def describe_batch(self, images, keypoints, workers: int = 0):
+    def describe_batch(self, images, keypoints, workers: int = 0, pattern: TripletPattern | None = None):
         """describe_all over many images in one pipelined ABI call. images: list of 2-D arrays, all
         uint8 or all float64; keypoints: list of (N_i, cols) float64 arrays with one common cols.
         -> list of (kept int64 (M_i,), descriptors uint8 (M_i, T/8))."""
@@ -280,17 +295,13 @@ class Engine:
         for im in images:
             if im.dtype != dtype:
                 raise TypeError("describe_batch needs one image dtype per call")
-            if im.strides[1] != im.itemsize or im.strides[0] % im.itemsize:
-                im = np.ascontiguousarray(im)
-            imgs.append(im)
+            imgs.append(self._rows(im)[0])
         for k in keypoints:
             kps_l.append(np.ascontiguousarray(k, np.float64))
         cols = kps_l[0].shape[1]
         if any(k.shape[1] != cols for k in kps_l):
             raise ValueError("describe_batch needs one keypoint column count per call")
-        nbytes = self.descriptor_bytes
         kept = [np.empty(len(k), np.int64) for k in kps_l]
-        out = [self._pinned.empty((len(k), nbytes), np.uint8) for k in kps_l]   # page-locked: direct DMA targets
         vp = C.c_void_p * n_img
         widths = (C.c_int * n_img)(*[im.shape[1] for im in imgs])
         heights = (C.c_int * n_img)(*[im.shape[0] for im in imgs])
@@ -302,6 +313,10 @@ class Engine:
         if fn is None:
             raise TypeError("image dtype must be uint8 or float64")
         with self._lock:
+            if pattern is not None:
+                self.set_pattern(pattern)
+            nbytes = self.descriptor_bytes
+            out = [self._pinned.empty((len(k), nbytes), np.uint8) for k in kps_l]   # page-locked: direct DMA targets
             rc = fn(self.ctx, vp(*[im.ctypes.data for im in imgs]), widths, heights, pitches,
                     vp(*[k.ctypes.data for k in kps_l]), counts, cols, n_img, workers,
                     vp(*[a.ctypes.data for a in kept]), vp(*[a.ctypes.data for a in out]), m)

@@ -581,12 +581,13 @@ def test_filtered_kernel_exact_pass_rate(lk, port, variant):
         eng.set_option("extract_variant", 4)
 
 
-@pytest.mark.parametrize("promote", [1, 0])
+@pytest.mark.parametrize("promote", [1, 2, 0])
 def test_float64_promotion_edges(lk, port, promote):
     """A float64 image goes to the u8 kernels only if EVERY pixel is an integer in [0, 255] (host
     workers or device classifier, same rule). One odd pixel anywhere — vector body, scalar tail,
     first or last row — must send the whole image down the float64 route, and either way the
-    descriptors are the oracle's."""
+    descriptors are the oracle's. host_promote 1 = host workers always, 2 = device classifier always,
+    0 = host workers for ordinary numpy memory (what this test passes)."""
     eng = lk.get_engine()
     eng.set_option("host_promote", promote)
     try:
@@ -616,6 +617,7 @@ def test_banded_float64_upload(lk, port, bands):
     oracle's bytes, including margin violators and keypoints on band boundaries."""
     eng = lk.get_engine()
     eng.set_option("upload_bands", bands)
+    eng.set_option("host_promote", 2)            # numpy memory would otherwise be promoted on the host, not banded
     try:
         w, h, n = 1024, 768, 6000
         base = port.random_image_u8(8100, w, h).astype(np.float64)
@@ -636,6 +638,7 @@ def test_banded_float64_upload(lk, port, bands):
             assert np.array_equal(desc, want), name
     finally:
         eng.set_option("upload_bands", 0)
+        eng.set_option("host_promote", 0)
 
 
 # ------------------------------------------------------ resident sets, batched pairs ----
@@ -810,6 +813,8 @@ def test_banded_upload_large_images(lk, port, bands, monkeypatch):
     keypoints are bucketed by band and un-permuted on the way out. Results and order must not
     change."""
     monkeypatch.setenv("CLATCH_UPLOAD_BANDS", bands)
+    eng = lk.get_engine()
+    eng.set_option("host_promote", 2)                         # keep pageable float64 frames on the banded route
     w, h = 1920, 1080
     img = port.structured_image(77, w, h)                     # float64, 16.6 MB
     kps = port.random_keypoints(78, w, h, 2500)
@@ -827,3 +832,171 @@ def test_banded_upload_large_images(lk, port, bands, monkeypatch):
     big = port.random_image_u8(79, 3840, 2160)                # uint8, 8.3 MB
     k2 = port.random_keypoints(80, 3840, 2160, 2100)
     assert np.array_equal(lk.describe(big, k2)[1], port.describe_all(big.astype(np.float64), k2)[1])
+    eng.set_option("host_promote", 0)
+
+
+# ------------------------------------------- round-2 additions: semantics at the edges ----
+
+def _nonfinite_cases(base, kps):
+    """Images with NaN / Inf / overflowing pixels placed under LIVE patch pixels and under the mask's
+    zero-weight row 7 / column 7 of some triplet's patches (src/descriptor.cpp:66-71: w*e*e with w = 0
+    and e = NaN still poisons the sum, so the bit must come out 0 exactly as the reference computes it)."""
+    h, w = base.shape
+    x, y = int(kps[0, 0]), int(kps[0, 1])
+    cases = {}
+    for name, v in (("nan", np.nan), ("inf", np.inf), ("-inf", -np.inf)):
+        for where, (dy, dx) in (("centre", (0, 0)), ("edge", (-31, 24)), ("far", (20, -30))):
+            img = base.copy()
+            img[y + dy, x + dx] = v
+            cases[f"{name}@{where}"] = img
+    img = base.copy()
+    img[y, x], img[y + 1, x] = 1.5e308, -1.5e308            # finite pixels whose difference overflows
+    cases["overflowing difference"] = img
+    img = base.copy()
+    img[::37, ::41] = np.nan                                 # scattered: most windows hold a NaN somewhere
+    cases["scattered nan"] = img
+    img = base.copy()
+    img[y - 3:y + 3, x - 3:x + 3] = 2.0 ** 1001              # huge but finite
+    cases["huge block"] = img
+    return cases
+
+
+def test_nonfinite_pixels_follow_the_reference(lk, port):
+    w, h = 400, 300
+    base = port.structured_image(66, w, h)
+    kps = port.random_keypoints(67, w, h, 500)
+    kps[0] = [200.0, 150.0, 0.0, 0.0]                        # upright, integer centre: samples ARE pixels
+    kps[1] = [200.5, 150.5, 0.7, 0.0]
+    ref = oracle.ref()
+    with np.errstate(all="ignore"):
+        for name, img in _nonfinite_cases(base, kps).items():
+            want = port.describe_all(img, kps)[1]
+            if ref is not None:
+                assert np.array_equal(ref.describe_all(img, kps, workers=0)[1], want), name
+            assert np.array_equal(lk.describe(img, kps)[1], want), name
+            assert not np.array_equal(want, port.describe_all(base, kps)[1])
+            got_b = lk.describe_batch([img, base], [kps, kps])
+            assert np.array_equal(got_b[0][1], want) and np.array_equal(got_b[1][1], port.describe_all(base, kps)[1])
+
+
+def test_nonfinite_pixels_banded_and_device(lk, port):
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    w, h, n = 1024, 768, 5000
+    base = port.random_image_u8(8100, w, h).astype(np.float64)
+    kps = port.random_keypoints(8101, w, h, n)
+    img = base.copy()
+    img[h - 60, w // 2] = np.nan                             # only the LAST band sees it
+    img[100, 100] = np.inf
+    want = port.describe_all(img, kps)[1]
+    with np.errstate(all="ignore"):
+        for promote in (2, 0):                               # banded device route, host-promote attempt then device
+            eng.set_option("host_promote", promote)
+            try:
+                assert np.array_equal(lk.describe(img, kps)[1], want)
+            finally:
+                eng.set_option("host_promote", 0)
+    xycs, kept = eng.prepare_keypoints(kps, w, h)
+    out = eng.extract_device(torch.from_numpy(img).cuda(), torch.from_numpy(xycs).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_negative_and_odd_strides(lk, port):
+    """Views the reference accepts through its c_style | forcecast conversion (bindings/module.cpp:30):
+    flipped, transposed, broadcast and row-skipping arrays, uint8 and float64."""
+    img8 = port.random_image_u8(91, 300, 200)
+    for base in (img8, img8.astype(np.float64)):
+        views = (base[::-1], base[:, ::-1], base.T[:, :200], np.broadcast_to(base[50], (200, 300)), base[::2, 1:],
+                 base[::-1, ::-1][3:])
+        for v in views:
+            flat = np.ascontiguousarray(v)
+            hh, ww = flat.shape
+            k = port.random_keypoints(93, ww, hh, 60)
+            assert np.array_equal(lk.describe(v, k)[1], port.describe_all(flat.astype(np.float64), k)[1]), v.strides
+    assert np.array_equal(lk.detect(img8[::-1]), lk.detect(np.ascontiguousarray(img8[::-1])))
+
+
+def test_concurrent_callers_with_different_patterns(lk, port):
+    """describe() is a pure function in the reference; here the pattern is context state, so it is
+    installed under the same lock as the launch. Threads with different patterns never see each other's."""
+    import threading
+    img = port.structured_image(97, 140, 140)
+    kps = port.random_keypoints(98, 140, 140, 64)
+    texts = [None, (GOLDEN / "pattern_t8k8.latchpat").read_text(), (GOLDEN / "pattern_t64k5w.latchpat").read_text()]
+    want = [lk.describe(img, kps, pattern=t)[1] for t in texts]
+    assert len({w.shape[1] for w in want}) == 3
+    errors = []
+
+    def worker(i):
+        try:
+            for _ in range(40):
+                got = lk.describe(img, kps, pattern=texts[i])[1]
+                if not np.array_equal(got, want[i]):
+                    errors.append(f"thread {i}: wrong pattern's descriptors ({got.shape})")
+                    return
+        except Exception as exc:                              # noqa: BLE001
+            errors.append(f"thread {i}: {type(exc).__name__}: {exc}")
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(3)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+
+
+def test_device_calls_on_different_streams_share_scratch_safely(lk, port):
+    """clatch_match_top2_dev / clatch_extract_f64_dev queue on the caller's stream but use the context's
+    expanded-operand and partial buffers: calls on different streams must be ordered by the library."""
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    sets = [torch.from_numpy(port.random_descriptors(200 + i, 6000 + 500 * i, 64)).cuda() for i in range(4)]
+    want = [port.knn2_all(s.cpu().numpy()[:3000], s.cpu().numpy()).T for s in sets]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    torch.cuda.synchronize()
+    for rep in range(6):
+        outs = []
+        for i, s in enumerate(sets):
+            st = streams[i & 1]
+            with torch.cuda.stream(st):
+                outs.append(eng.match_top2_device(s[:3000], s, stream=st))
+        bi, bd, sd = eng.match_top2(sets[0].cpu().numpy()[:100], sets[1].cpu().numpy())     # host form in between
+        torch.cuda.synchronize()
+        for o, w in zip(outs, want):
+            assert np.array_equal(o.cpu().numpy(), w), rep
+    w, h = 640, 480
+    imgs = [port.random_image_u8(300 + i, w, h).astype(np.float64) for i in range(2)]
+    imgs[1] += 0.25                                          # one u8-valued, one not: different flag values
+    kps = port.random_keypoints(310, w, h, 800)
+    xycs, _ = eng.prepare_keypoints(kps, w, h)
+    d_x = torch.from_numpy(xycs).cuda()
+    d_imgs = [torch.from_numpy(a).cuda() for a in imgs]
+    wants = [port.describe_all(a, kps)[1] for a in imgs]
+    torch.cuda.synchronize()
+    for rep in range(4):
+        outs = []
+        for i in (0, 1, 0, 1):
+            with torch.cuda.stream(streams[i]):
+                outs.append((i, eng.extract_device(d_imgs[i], d_x, stream=streams[i])))
+        torch.cuda.synchronize()
+        for i, o in outs:
+            assert np.array_equal(o.cpu().numpy(), wants[i]), (rep, i)
+
+
+def test_pageable_float64_batch_is_promoted_on_the_host(lk, port):
+    """describe_batch on ordinary numpy float64 frames: u8-valued frames are converted by the host workers
+    into page-locked staging and go up as bytes; a frame with one odd pixel takes the float64 route."""
+    imgs = [port.random_image_u8(400 + i, 800, 600).astype(np.float64) for i in range(4)]
+    imgs[2][599, 799] = 0.5
+    imgs[3][0, 0] = np.nan
+    kps = [port.random_keypoints(410 + i, 800, 600, 700) for i in range(4)]
+    with np.errstate(all="ignore"):
+        want = [port.describe_all(a, k)[1] for a, k in zip(imgs, kps)]
+        for promote in (0, 1, 2):
+            lk.get_engine().set_option("host_promote", promote)
+            try:
+                got = lk.describe_batch(imgs, kps)
+            finally:
+                lk.get_engine().set_option("host_promote", 0)
+            for g, wnt in zip(got, want):
+                assert np.array_equal(g[1], wnt), promote

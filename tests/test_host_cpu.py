@@ -319,3 +319,54 @@ def test_take_keypoints_matches_numpy(lib):
                                                out.ctypes.data_as(C.POINTER(C.c_double)))
                 assert rc == 0 and np.array_equal(out, want)
     assert lib.clatch_take_keypoints(None, 5, None, 0, 0, None) != 0          # bad column count
+
+
+def test_image_rows_rule_copies_every_view_the_abi_cannot_take():
+    """Engine._rows: the C ABI takes unit inner stride and a positive whole-element pitch >= width;
+    flipped, transposed, broadcast and overlapping views are copied first (the reference accepts any
+    array through c_style | forcecast, bindings/module.cpp:30)."""
+    from paper_1609_03986_b200.engine import Engine
+    for base in (np.arange(60, dtype=np.uint8).reshape(6, 10), np.arange(60, dtype=np.float64).reshape(6, 10)):
+        for v in (base, base[::-1], base[:, ::-1], base.T, np.broadcast_to(base[0], (6, 10)), base[::2], base[:, 2:7],
+                  base[::-1, ::-1][1:], base[:1]):
+            a, pitch = Engine._rows(v)
+            assert a.strides[1] == a.itemsize and pitch >= a.shape[1] and a.strides[0] == pitch * a.itemsize
+            assert np.array_equal(a, v)
+        a, pitch = Engine._rows(base[::2])
+        assert np.shares_memory(a, base) and pitch == 20          # a plain row-skipping view needs no copy
+
+
+def test_bench_reference_arm_and_workload_strings():
+    """`bench.py --impl reference` prints one JSON line whose config.workload is the string our arm
+    prints for the same configuration (both come from oracle/workloads.py)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--workload", "cfg1", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=300, check=True).stdout
+    lines = [ln for ln in out.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    from oracle import workloads
+    assert line["impl"] == "reference" and line["config"]["workload"] == workloads.DESCRIPTIONS["cfg1"]
+    assert line["value"] > 0 and line["cpu_baseline"]["cores"] >= 1 and line["e2e"]["h2d_bytes_per_step"] == 0
+    src = (root / "bench.py").read_text()
+    assert src.count("DESCRIPTIONS[") >= 6 and "u8-valued noise image" not in src   # one source for both arms
+
+
+def test_cfg4_workload_has_the_planted_structure():
+    """oracle/workloads.cfg4_sets at a small size: planted copies are exact copies of FINAL train rows and
+    duplicated train rows exist (the tie cases of proj/tests/acceptance.cpp:170-173)."""
+    from oracle import workloads
+    q, t, (dup_q, src_t) = workloads.cfg4_sets(rows=20_000)
+    assert q.shape == t.shape == (20_000, 64) and len(dup_q) == 200
+    assert np.array_equal(q[dup_q], t[src_t])
+    _, counts = np.unique(t, axis=0, return_counts=True)
+    assert (counts > 1).sum() >= 15
+    res = workloads.knn2_rows_threaded(q[dup_q[:8]], t)
+    assert np.all(res[:, 1] == 0) and np.all(res[:, 0] <= src_t[:8])
+    rows = workloads.match_threaded(q[:300], t[:500], ratio=0.8, cross_check=True)
+    import oracle
+    assert np.array_equal(rows, oracle.port().match(q[:300], t[:500], ratio=0.8, cross_check=True))
