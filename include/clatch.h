@@ -88,6 +88,8 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * bytes over the bus; lossless, same descriptors). 0 (default) does so when the image lies in ordinary
  * pageable memory — which the driver could only copy through its own bounce buffers — and uploads the
  * doubles of a page-locked image as they are (classified on the device); 1 = always, 2 = never.
+ * key "match_pairs": 1 (default) runs the tensor-core matcher as clusters of two CTAs that share one stream of
+ * train tiles through TMA multicast (half the L2 traffic per compare); 0 = every CTA streams for itself.
  * key "match_streamk": 1 (default) lets the tensor-core matcher split small problems (expanded train set
  * within 32 MB) into equal shares of (query tile, train tile) units per CTA; 0 keeps whole rounds.
  * key "pairs_filter_on_device": 1 (default) runs the ratio / max-distance / cross-check decisions of

@@ -357,6 +357,10 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         ctx->pairs_filter_on_device = value != 0;
         return CLATCH_OK;
     }
+    if (std::strcmp(key, "match_pairs") == 0) {   // tensor matcher: CTA pairs sharing the train stream by TMA multicast
+        ctx->match_pairs = value != 0;
+        return CLATCH_OK;
+    }
     if (std::strcmp(key, "match_streamk") == 0) {   // tensor matcher: stream-K partition for small problems
         ctx->match_streamk = value != 0;
         return CLATCH_OK;
@@ -1254,7 +1258,7 @@ int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t
         const clatch_set* a = sets[pairs[2 * (first + p)]];
         const clatch_set* b = sets[pairs[2 * (first + p) + 1]];
         pair_offset[p + 1] = pair_offset[p] + 3 * a->n + (cross_check ? b->n : 0);
-        items += tc_query_tiles(a->n) + (cross_check ? tc_query_tiles(b->n) : 0);
+        items += tc_query_tiles(a->n) + 1 + (cross_check ? tc_query_tiles(b->n) + 1 : 0);   // (+1: a filler per odd pass)
     }
     const size_t total = pair_offset[count];
     if (int rc = ctx->res.reserve(sizeof(int32_t) * std::max<size_t>(total, 1))) return rc;
@@ -1266,15 +1270,25 @@ int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t
         const clatch_set* a = sets[pairs[2 * (first + p)]];
         const clatch_set* b = sets[pairs[2 * (first + p) + 1]];
         int32_t* base = r + pair_offset[p];
+        const bool paired = tc_items_paired(ctx);   // CTA pairs: entries (2k, 2k + 1) must scan the same train set
         for (int q = 0; q < tc_query_tiles(a->n); ++q)
             table.push_back({a->exp, b->exp, static_cast<unsigned>(a->n),
                              static_cast<unsigned>(b->n), static_cast<unsigned>(q), 0, base, base + a->n,
                              base + 2 * a->n});
-        if (cross_check)   // reverse_best[g] = knn2(gallery[g], probes).best_index, src/match.cpp:62-67
+        if (paired && (table.size() & 1)) {         // odd tile count: a filler keeps the last tile's partner in step
+            table.push_back(table.back());
+            table.back().pad = 1;
+        }
+        if (cross_check) {   // reverse_best[g] = knn2(gallery[g], probes).best_index, src/match.cpp:62-67
             for (int q = 0; q < tc_query_tiles(b->n); ++q)
                 table.push_back({b->exp, a->exp, static_cast<unsigned>(b->n),
                                  static_cast<unsigned>(a->n), static_cast<unsigned>(q), 0, base + 3 * a->n, nullptr,
                                  nullptr});
+            if (paired && (table.size() & 1)) {
+                table.push_back(table.back());
+                table.back().pad = 1;
+            }
+        }
     }
     cudaStream_t st = ctx->stream;
     CLATCH_CUDA(cudaMemcpyAsync(ctx->items.ptr, table.data(), sizeof(TcItem) * table.size(), cudaMemcpyHostToDevice, st));

@@ -96,6 +96,9 @@ struct clatch_ctx {
     bool extract_stats_on = false;           // count exact recomputes (clatch_extract_stats)
     clatch::DeviceBuffer extract_stats;      // 2 x u64
     bool pairs_filter_on_device = true;   // clatch_match_set_pairs: ratio / max / cross-check decisions on the device
+    // tensor matcher: clusters of two CTAs share the train-set stream through TMA multicast (one L2 read feeds two
+    // SMs) wherever two query tiles scan the same train tiles; set_option "match_pairs" 0 = every CTA on its own.
+    bool match_pairs = true;
     bool match_streamk = true;     // tensor matcher: equal-share partition for small problems (set_option "match_streamk")
     int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
     // The scratch below is shared by every call on this context, whatever stream the call queues on
@@ -205,6 +208,7 @@ int launch_filter_pairs(clatch_ctx* ctx, const FilterPair* d_pairs, size_t count
                         int32_t* d_out, cudaStream_t stream);
 size_t tc_expanded_bytes(size_t rows);
 int tc_query_tiles(size_t rows);
+bool tc_items_paired(const clatch_ctx* ctx);   // item tables must hold entries (2k, 2k + 1) over one train set; TcItem::pad = 1 marks a filler
 int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t* d_out, cudaStream_t stream);
 int launch_match_tc_items(clatch_ctx* ctx, const TcItem* d_items, size_t count, cudaStream_t stream);
 void launch_merge_partials(const Partial* partial, unsigned long long Q, int splits, int sentinel,

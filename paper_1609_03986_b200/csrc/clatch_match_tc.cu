@@ -112,10 +112,32 @@ __device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigne
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
+// The same copy delivered to the same CTA-relative offsets (data and mbarrier) of every CTA in `mask`.
+__device__ __forceinline__ void bulk_load_multicast(unsigned dst, const void* src, unsigned bytes, unsigned bar,
+                                                    unsigned short mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(unsigned bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// ... arriving on the barrier at the same offset in every CTA of `mask`.
+__device__ __forceinline__ void tc_commit_multicast(unsigned bar, unsigned short mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+                 "h"(mask)
+                 : "memory");
 }
 // D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32, M=128, N=256, K=32.
 __device__ __forceinline__ void tc_mma_i8(unsigned tmem_d, uint64_t desc_a, uint64_t desc_b, unsigned idesc,
@@ -168,6 +190,7 @@ struct TcWork {
     unsigned qtile;
     int tile_begin, ntiles, split;
     int32_t *o_idx, *o_best, *o_second;   // final outputs (item-table mode) or null
+    bool ghost;           // pair mode: this CTA only keeps its partner's operand stream company (no output)
 };
 
 struct TcArgs {
@@ -190,10 +213,15 @@ __host__ __device__ __forceinline__ unsigned long long tc_sk_chunk_of(unsigned l
     return c;
 }
 
-__device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item) {
+// kPair: `item` counts PAIR items; the two CTAs of a cluster (rank 0 / 1) take two query tiles that scan the same
+// train tiles — table entries 2 * item + rank, or query tiles 2j + rank of one split.
+template <bool kPair>
+__device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned rank) {
     TcWork w;
+    w.ghost = false;
     if (g.items != nullptr) {
-        const TcItem it = g.items[item];
+        const TcItem it = g.items[kPair ? 2 * item + static_cast<int>(rank) : item];
+        w.ghost = it.pad != 0;
         w.a = it.a_exp + static_cast<unsigned long long>(it.qtile) * kTcABytes;
         w.b = it.b_exp;
         w.Q = it.Q;
@@ -235,6 +263,22 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item) {
         w.Q = g.Q;
         w.N = g.N;
         w.o_idx = w.o_best = w.o_second = nullptr;
+    } else if (kPair) {
+        const int pps = (g.qtiles + 1) / 2;                  // pair items per split
+        w.split = item / pps;
+        int qt = 2 * (item - w.split * pps) + static_cast<int>(rank);
+        if (qt >= g.qtiles) {                                // odd tile count: the last pair's second CTA
+            qt = g.qtiles - 1;
+            w.ghost = true;
+        }
+        w.qtile = static_cast<unsigned>(qt);
+        w.a = g.a_exp + static_cast<unsigned long long>(w.qtile) * kTcABytes;
+        w.b = g.b_exp;
+        w.Q = g.Q;
+        w.N = g.N;
+        w.tile_begin = w.split * g.tiles_per_split;
+        w.ntiles = min(g.total_tiles, w.tile_begin + g.tiles_per_split) - w.tile_begin;
+        w.o_idx = w.o_best = w.o_second = nullptr;
     } else {
         // consecutive CTAs take different query tiles of the SAME split: they stream the same
         // train tiles at the same time, so HBM sees them once and L2 serves the rest
@@ -251,7 +295,17 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item) {
     return w;
 }
 
+// kPair = true: launched as clusters of two CTAs. Every CTA used to pull the whole train stream out of L2 by
+// itself — 64 B/clk/SM at the tensor pipe's pace, 9.5 KB/clk over 148 SMs, which is more than L2 delivers
+// (tools/tc_peak.cu: ~4.3-6 KB/clk) and held the kernel at 72-77 % of the MMA rate. Paired CTAs work on two
+// query tiles against the SAME train tiles: each loads half of every B stage and multicasts it into both
+// CTAs' shared memory (one L2 read feeds two SMs), and a stage is handed back to the producers only when both
+// CTAs' MMAs have read it (multicast tcgen05.commit onto both `empty` barriers).
+template <bool kPair>
 __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g) {
+    const unsigned rank = kPair ? cluster_rank() : 0u;
+    const int first_item = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int item_step = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
     extern __shared__ uint8_t smem_raw[];
     const unsigned raw = smem_u32(smem_raw);
     const unsigned base = (raw + 1023u) & ~1023u;              // SWIZZLE_128B atoms need 1024-B alignment
@@ -276,7 +330,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
         mbar_init(bar_a_empty, 1);
         for (int s = 0; s < kTcStages; ++s) {
             mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_empty + 8 * s, 1);
+            mbar_init(bar_empty + 8 * s, kPair ? 2 : 1);       // pair mode: both CTAs' MMAs must have read the stage
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
@@ -291,6 +345,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
     }
     tc_fence_before();
     __syncthreads();
+    if (kPair) cluster_sync_all();                             // the partner's barriers exist before anything lands on them
     tc_fence_after();
     const unsigned tmem_base = *tmem_slot;
 
@@ -299,8 +354,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
         if (lane == 0) {
             int stage = 0;
             unsigned phase = 0, a_phase = 0;
-            for (int item = blockIdx.x; item < g.num_items; item += gridDim.x) {
-                const TcWork w = tc_decode(g, item);
+            for (int item = first_item; item < g.num_items; item += item_step) {
+                const TcWork w = tc_decode<kPair>(g, item, rank);
                 if (w.ntiles == 0) continue;                   // (stream-K: this CTA has fewer pieces)
                 mbar_wait(bar_a_empty, a_phase ^ 1);           // previous item's MMAs are done with A
                 mbar_expect_tx(bar_a_full, kTcABytes);
@@ -313,9 +368,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
                         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
                         mbar_expect_tx(bar_full + 8 * stage, kTcStageBytes);
                         const unsigned dst = smem_b + stage * kTcStageBytes;
-                        bulk_load(dst, src + kb * (kTcStageBytes / 2), kTcStageBytes / 2, bar_full + 8 * stage);
-                        bulk_load(dst + kTcStageBytes / 2, src + kTcABytes + kb * (kTcStageBytes / 2), kTcStageBytes / 2,
-                                  bar_full + 8 * stage);
+                        if (kPair) {   // this CTA's half of the stage, to both CTAs
+                            bulk_load_multicast(dst + rank * (kTcStageBytes / 2),
+                                                src + rank * kTcABytes + kb * (kTcStageBytes / 2), kTcStageBytes / 2,
+                                                bar_full + 8 * stage, 3);
+                        } else {
+                            bulk_load(dst, src + kb * (kTcStageBytes / 2), kTcStageBytes / 2, bar_full + 8 * stage);
+                            bulk_load(dst + kTcStageBytes / 2, src + kTcABytes + kb * (kTcStageBytes / 2), kTcStageBytes / 2,
+                                      bar_full + 8 * stage);
+                        }
                         if (++stage == kTcStages) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -326,8 +387,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
         if (lane == 0) {
             int stage = 0, tcount = 0;
             unsigned phase = 0, a_phase = 0;
-            for (int item = blockIdx.x; item < g.num_items; item += gridDim.x) {
-                const TcWork w = tc_decode(g, item);
+            for (int item = first_item; item < g.num_items; item += item_step) {
+                const TcWork w = tc_decode<kPair>(g, item, rank);
                 if (w.ntiles == 0) continue;
                 mbar_wait(bar_a_full, a_phase);
                 a_phase ^= 1;
@@ -345,7 +406,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
                         for (int k = 0; k < kTcKBlock / 32; ++k)
                             tc_mma_i8(tmem_d, umma_desc(a_addr + 32 * k), umma_desc(b_addr + 32 * k), kIdesc,
                                       (kb | k) != 0);
-                        tc_commit(bar_empty + 8 * stage);      // stage reusable once these MMAs have read it
+                        if (kPair) tc_commit_multicast(bar_empty + 8 * stage, 3);
+                        else tc_commit(bar_empty + 8 * stage);  // stage reusable once these MMAs have read it
                         if (++stage == kTcStages) { stage = 0; phase ^= 1; }
                     }
                     tc_commit(bar_tfull + 8 * buf);            // accumulator complete
@@ -361,8 +423,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
         const unsigned lane_addr = static_cast<unsigned>(quarter * 32) << 16;
         const int row = quarter * 32 + lane;
         int tcount = 0;
-        for (int item = blockIdx.x; item < g.num_items; item += gridDim.x) {
-            const TcWork w = tc_decode(g, item);
+        for (int item = first_item; item < g.num_items; item += item_step) {
+            const TcWork w = tc_decode<kPair>(g, item, rank);
             if (w.ntiles == 0) continue;
             int best = INT_MIN, second = INT_MIN, best_idx = -1;
             for (int t = 0; t < w.ntiles; ++t, ++tcount) {
@@ -375,7 +437,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
                 for (int chunk = 0; chunk < 4; ++chunk) {
                     int v[32];
                     tmem_ld32(tmem_base + lane_addr + buf * kTcN + half * 128 + chunk * 32, v);
-                    if (g.dump != nullptr && item == 0 && t == 0) {
+                    if (g.dump != nullptr && item == 0 && t == 0 && rank == 0) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) g.dump[row * kTcN + half * 128 + chunk * 32 + i] = v[i];
                     }
@@ -425,7 +487,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
                     second = max(second, ob);
                 }
                 const unsigned long long qi = static_cast<unsigned long long>(w.qtile) * kTcM + row;
-                if (qi < w.Q) {
+                if (qi < w.Q && !w.ghost) {
                     const int idx = best_idx < 0 ? -1 : w.tile_begin * kTcN + best_idx;
                     const int bd = best == INT_MIN ? 513 : (512 - best) >> 1;
                     const int sd = second == INT_MIN ? 513 : (512 - second) >> 1;
@@ -449,6 +511,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
 
     tc_fence_before();
     __syncthreads();
+    if (kPair) cluster_sync_all();                             // nothing of the partner's is still bound for this CTA
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
@@ -490,7 +553,8 @@ __global__ void merge_partials_sk_kernel(const Partial* __restrict__ partial, un
 // The opt-in shared-memory size is a per-device function attribute: remember it per context.
 static int configure_tc(clatch_ctx* ctx) {
     if (!ctx->tc_configured) {
-        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemBytes));
+        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemBytes));
+        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemBytes));
         ctx->tc_configured = true;
     }
     return CLATCH_OK;
@@ -509,18 +573,43 @@ int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t
 
 int tc_query_tiles(size_t rows) { return static_cast<int>((rows + kTcM - 1) / kTcM); }
 
+// Clusters of two CTAs (cudaLaunchKernelEx): the paired form of the kernel.
+static int launch_tc_pairs(clatch_ctx* ctx, const TcArgs& g, unsigned ctas, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctas & ~1u);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = kTcSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    CLATCH_CUDA(cudaLaunchKernelEx(&cfg, match_tc_kernel<true>, g));
+    ++ctx->launches;
+    return CLATCH_OK;
+}
+
 int launch_match_tc_items(clatch_ctx* ctx, const TcItem* d_items, size_t count, cudaStream_t stream) {
     if (count == 0) return CLATCH_OK;
     if (int rc = configure_tc(ctx)) return rc;
     TcArgs g{};
-    g.num_items = static_cast<int>(count);
     g.items = d_items;
+    if (ctx->match_pairs) {   // the table holds entries (2k, 2k + 1) that scan the same train set (tc_items_paired)
+        g.num_items = static_cast<int>(count / 2);
+        return launch_tc_pairs(ctx, g, static_cast<unsigned>(std::min<size_t>(count, ctx->sm_count)), stream);
+    }
+    g.num_items = static_cast<int>(count);
     const unsigned grid = static_cast<unsigned>(std::min<size_t>(count, ctx->sm_count));
-    match_tc_kernel<<<grid, kTcThreads, kTcSmemBytes, stream>>>(g);
+    match_tc_kernel<false><<<grid, kTcThreads, kTcSmemBytes, stream>>>(g);
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
     return CLATCH_OK;
 }
+
+bool tc_items_paired(const clatch_ctx* ctx) { return ctx->match_pairs; }
 
 int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
                          int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
@@ -570,6 +659,23 @@ int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
         const double legacy = rounds * (per_split + 1.5), sk = share + 2.0 * sk_pieces_per_cta;   // (measured: tools/sk_perf.py)
         streamk = sk < legacy;
     }
+    // Otherwise pairs of CTAs share the train stream (match_tc_kernel<true>): the schedulable unit is a pair of
+    // query tiles on a pair of SMs, so the split count is chosen again in those units.
+    const bool paired = !streamk && ctx->match_pairs && qtiles >= 2 && sms >= 2;
+    if (paired) {
+        const size_t pq = (qtiles + 1) / 2, slots2 = sms / 2;
+        double best_cost = 1e300;
+        for (size_t s = 1; s <= std::min<size_t>(ttiles, 64); ++s) {
+            const size_t per = (ttiles + s - 1) / s, actual = (ttiles + per - 1) / per;
+            const size_t rounds = (pq * actual + slots2 - 1) / slots2;
+            const double cost = rounds * (per + 1.5);
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                splits = actual;
+                per_split = per;
+            }
+        }
+    }
     const size_t slots = streamk ? sk_pieces_per_qtile : splits;
     if (int rc = ctx->partial.reserve(sizeof(Partial) * slots * Q)) return rc;
     TcArgs g{};
@@ -584,9 +690,15 @@ int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
     g.sk_chunks = streamk ? static_cast<int>(chunks) : 0;
     g.partial = ctx->partial.as<Partial>();
     g.dump = d_dump;
-    const unsigned grid = static_cast<unsigned>(streamk ? chunks : std::min<size_t>(qtiles * splits, ctx->sm_count));
-    match_tc_kernel<<<grid, kTcThreads, kTcSmemBytes, stream>>>(g);
-    ++ctx->launches;
+    if (paired) {
+        const size_t pair_items = (qtiles + 1) / 2 * splits;
+        g.num_items = static_cast<int>(pair_items);
+        if (int rc = launch_tc_pairs(ctx, g, static_cast<unsigned>(std::min<size_t>(2 * pair_items, sms)), stream)) return rc;
+    } else {
+        const unsigned grid = static_cast<unsigned>(streamk ? chunks : std::min<size_t>(qtiles * splits, ctx->sm_count));
+        match_tc_kernel<false><<<grid, kTcThreads, kTcSmemBytes, stream>>>(g);
+        ++ctx->launches;
+    }
     CLATCH_CUDA(cudaGetLastError());
     if (streamk)
         merge_partials_sk_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(

@@ -38,7 +38,7 @@ class _PinnedPool:
       `max_live_bytes` of outstanding page-locked memory.
     """
 
-    def __init__(self, lib, max_live_bytes: int = 256 << 20):
+    def __init__(self, lib, max_live_bytes: int = 1 << 30):
         self.lib, self.free, self.released, self.live_bytes = lib, {}, {}, 0
         self.max_live_bytes = max_live_bytes
         self.lock = threading.Lock()

@@ -403,7 +403,7 @@ def test_every_matcher_variant_is_exact(lk, port, variant):
 
 
 @pytest.mark.parametrize("shape", [(1, 1), (1, 300), (129, 257), (700, 513), (2000, 2000), (5000, 9000),
-                                   (10000, 10000), (300, 70000)])
+                                   (10000, 10000), (300, 70000), (256, 1), (385, 66000), (40000, 3000)])
 def test_tensor_matcher_partitions_agree(lk, port, shape):
     """Small problems are cut "stream-K" style (every CTA an equal run of (query tile, train tile)
     units, pieces merged per query tile), larger ones by (query tile, train split) rounds. Both
@@ -425,9 +425,12 @@ def test_tensor_matcher_partitions_agree(lk, port, shape):
         for sk in (1, 0):
             eng.set_option("match_streamk", sk)
             res[sk] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_pairs", 0)                # every CTA streams the train set for itself
+        res[2] = np.stack(eng.match_top2(query, train))
     finally:
         eng.set_option("match_streamk", 1)
-    assert np.array_equal(res[0], res[1])
+        eng.set_option("match_pairs", 1)                # default: CTA pairs share the stream by TMA multicast
+    assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
     rows = np.arange(q_n) if q_n * t_n <= 4_000_000 else np.unique(np.r_[np.arange(0, q_n, 7)[:40], rng.integers(0, q_n, 40)])
     assert np.array_equal(res[1][:, rows].T, port.knn2_all(query[rows], train))
 
@@ -643,14 +646,15 @@ def test_banded_float64_upload(lk, port, bands):
 
 # ------------------------------------------------------ resident sets, batched pairs ----
 
-@pytest.mark.parametrize("filter_on_device", [1, 0])
-def test_resident_sets_and_batched_pairs(lk, port, filter_on_device):
+@pytest.mark.parametrize("filter_on_device,cta_pairs", [(1, 1), (0, 1), (1, 0)])
+def test_resident_sets_and_batched_pairs(lk, port, filter_on_device, cta_pairs):
     """cfg5 shape: every image against every other image through resident descriptor sets.
     Each pair must equal the reference's match_brute_force with the same filters, whether the
     filter pass (ratio in double, inclusive max distance, cross-check) runs on the device or the host."""
     torch = pytest.importorskip("torch")
     eng = lk.get_engine()
     eng.set_option("pairs_filter_on_device", filter_on_device)
+    eng.set_option("match_pairs", cta_pairs)      # item tables in CTA-pair form (fillers for odd tile counts) or plain
     sizes = [300, 1, 257, 128, 1000]
     raw = [port.random_descriptors(900 + i, n, 64) for i, n in enumerate(sizes)]
     raw[2][5] = raw[0][7]                 # cross-image duplicates -> zero distances and ties
@@ -681,6 +685,7 @@ def test_resident_sets_and_batched_pairs(lk, port, filter_on_device):
     for (i, j), m in res.items():
         assert np.array_equal(m, port.match(raw[i], raw[j], ratio=0.9, cross_check=True))
     eng.set_option("pairs_filter_on_device", 1)
+    eng.set_option("match_pairs", 1)
 
 
 def test_result_arrays_are_never_recycled_while_alive(lk, port):
@@ -950,6 +955,7 @@ def test_device_calls_on_different_streams_share_scratch_safely(lk, port):
     expanded-operand and partial buffers: calls on different streams must be ordered by the library."""
     torch = pytest.importorskip("torch")
     eng = lk.get_engine()
+    eng.set_pattern(None)                                # extract_device uses the context's installed pattern
     sets = [torch.from_numpy(port.random_descriptors(200 + i, 6000 + 500 * i, 64)).cuda() for i in range(4)]
     want = [port.knn2_all(s.cpu().numpy()[:3000], s.cpu().numpy()).T for s in sets]
     streams = [torch.cuda.Stream() for _ in range(2)]
@@ -1000,3 +1006,35 @@ def test_pageable_float64_batch_is_promoted_on_the_host(lk, port):
                 lk.get_engine().set_option("host_promote", 0)
             for g, wnt in zip(got, want):
                 assert np.array_equal(g[1], wnt), promote
+
+
+def test_tensor_matcher_extreme_distances(lk, port):
+    """The tensor-core matcher over the whole distance range: identical rows (D = +512), complements
+    (D = -512), all-zero / all-one descriptors, ties on tile boundaries, graded small distances."""
+    eng = lk.get_engine()
+    rng = np.random.default_rng(16)
+    train = port.random_descriptors(77, 3000)
+    train[0] = 0
+    train[1] = 255
+    train[2] = ~train[5]
+    train[2999] = train[5]
+    query = port.random_descriptors(78, 700)
+    query[0] = 0
+    query[1] = 255
+    query[2] = train[5]                                  # exact copy, twice in train (5 and 2999)
+    query[3] = ~train[7]                                 # complement: distance 512 to row 7
+    for k in range(4, 40):                               # graded distances 0..35 from train[100 + k]
+        query[k] = train[100 + k]
+        for b in rng.choice(512, k - 4, replace=False):
+            query[k, b >> 3] ^= np.uint8(1 << (b & 7))
+    only = np.stack([train[7], train[7]])                # every distance 512 for query 3
+    got = np.stack(eng.match_top2(query, train), 1)
+    assert np.array_equal(got, port.knn2_all(query, train))
+    assert got[2].tolist() == [5, 0, 0] and got[0].tolist()[:2] == [0, 0] and got[1].tolist()[:2] == [1, 0]
+    far = np.stack(eng.match_top2(query[3:4], only), 1)
+    assert far.tolist() == [[0, 512, 512]]
+    sets = [eng.create_set(query), eng.create_set(train)]
+    rows = eng.match_sets(sets[0], sets[1], ratio=0.9, cross_check=True)
+    assert np.array_equal(rows, port.match(query, train, ratio=0.9, cross_check=True))
+    rows = eng.match_sets(sets[0], sets[1], max_distance=40)
+    assert np.array_equal(rows, port.match(query, train, max_distance=40))

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -24,6 +25,7 @@ constexpr int kUnroll = 8;
 
 template <int OP>
 __global__ void alu_kernel(unsigned long long* cycles, double* sink, unsigned seed) {
+    unsigned long long n0, n1;
     unsigned a[kUnroll];
     double d[kUnroll];
     for (int i = 0; i < kUnroll; ++i) {
@@ -31,6 +33,7 @@ __global__ void alu_kernel(unsigned long long* cycles, double* sink, unsigned se
         d[i] = 1.0 + 1e-9 * (threadIdx.x + i);
     }
     const double m = 1.0 + 1e-12 * seed, c = 1e-13 * seed;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(n0));
     const long long t0 = clock64();
     for (int it = 0; it < kIters; ++it) {
 #pragma unroll
@@ -45,10 +48,11 @@ __global__ void alu_kernel(unsigned long long* cycles, double* sink, unsigned se
         }
     }
     const long long t1 = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(n1));
     double s = 0;
     for (int i = 0; i < kUnroll; ++i) s += d[i] + a[i];
     if (s == 12345.678) sink[0] = s;
-    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0, cycles[gridDim.x + blockIdx.x] = n1 - n0;
 }
 
 // mode 0: lane-linear (conflict free); 1: random slots; 2: random with distinct bank pairs per half-warp
@@ -59,6 +63,8 @@ __global__ void lds_kernel(unsigned long long* cycles, double* sink, const unsig
     unsigned off[kUnroll];
     for (int i = 0; i < kUnroll; ++i) off[i] = offsets[threadIdx.x * kUnroll + i];
     double acc[kUnroll] = {0};
+    unsigned long long n0, n1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(n0));
     const long long t0 = clock64();
     for (int it = 0; it < kIters; ++it) {
 #pragma unroll
@@ -68,13 +74,14 @@ __global__ void lds_kernel(unsigned long long* cycles, double* sink, const unsig
         }
     }
     const long long t1 = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(n1));
     double s = 0;
     for (int i = 0; i < kUnroll; ++i) s += acc[i];
     if (s == 12345.678) sink[0] = s;
-    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0, cycles[gridDim.x + blockIdx.x] = n1 - n0;
 }
 
-struct Result { double gops; double per_clk_sm; };
+struct Result { double gops; double per_clk_sm; double sm_mhz; };   // sm_mhz: clock64 ticks / globaltimer ns while the kernel ran, median over CTAs
 
 template <typename Launch>
 Result run(Launch launch, int blocks, int sms, unsigned long long* d_cycles, double ops_per_thread,
@@ -89,14 +96,20 @@ Result run(Launch launch, int blocks, int sms, unsigned long long* d_cycles, dou
     CK(cudaEventSynchronize(e1));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
-    std::vector<unsigned long long> cyc(blocks);
-    CK(cudaMemcpy(cyc.data(), d_cycles, sizeof(unsigned long long) * blocks, cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> cyc(2 * blocks);
+    CK(cudaMemcpy(cyc.data(), d_cycles, sizeof(unsigned long long) * 2 * blocks, cudaMemcpyDeviceToHost));
     unsigned long long mx = 0;
-    for (auto c : cyc) mx = c > mx ? c : mx;
+    std::vector<double> mhz(blocks);
+    for (int b = 0; b < blocks; ++b) {
+        mx = cyc[b] > mx ? cyc[b] : mx;
+        mhz[b] = cyc[b] * 1e3 / static_cast<double>(cyc[blocks + b]);
+    }
+    std::sort(mhz.begin(), mhz.end());
     const double total = ops_per_thread * kThreads * blocks;
     Result r;
     r.gops = total / (ms * 1e-3) / 1e9;
     r.per_clk_sm = ops_per_thread * kThreads * (blocks / sms) / static_cast<double>(mx);
+    r.sm_mhz = mhz[blocks / 2];
     return r;
 }
 
@@ -107,7 +120,7 @@ int main() {
     const int blocks = sms * 2;   // 2 x 512 threads per SM, all resident
     unsigned long long* d_cycles;
     double* d_sink;
-    CK(cudaMalloc(&d_cycles, sizeof(unsigned long long) * blocks));
+    CK(cudaMalloc(&d_cycles, sizeof(unsigned long long) * 2 * blocks));
     CK(cudaMalloc(&d_sink, sizeof(double)));
     const double ops = static_cast<double>(kIters) * kUnroll;
 
@@ -145,12 +158,12 @@ int main() {
     cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);
     printf("{\"device\": \"%s\", \"sm_count\": %d, \"max_sm_mhz\": %.0f,\n", prop.name, sms, khz / 1e3);
     for (int i = 0; i < 7; ++i)
-        printf(" \"%s_gops\": %.1f, \"%s_per_clk_sm\": %.2f,\n", names[i], res[i].gops, names[i],
-               res[i].per_clk_sm);
+        printf(" \"%s_gops\": %.1f, \"%s_per_clk_sm\": %.2f, \"%s_sm_mhz\": %.0f,\n", names[i], res[i].gops, names[i],
+               res[i].per_clk_sm, names[i], res[i].sm_mhz);
     const char* lnames[] = {"lds64", "lds64_rand", "lds64_hw16"};
     for (int i = 0; i < 3; ++i)
-        printf(" \"%s_gbs\": %.1f, \"%s_bytes_per_clk_sm\": %.2f,\n", lnames[i], lds[i].gops * 8,
-               lnames[i], lds[i].per_clk_sm * 8);
+        printf(" \"%s_gbs\": %.1f, \"%s_bytes_per_clk_sm\": %.2f, \"%s_sm_mhz\": %.0f,\n", lnames[i], lds[i].gops * 8,
+               lnames[i], lds[i].per_clk_sm * 8, lnames[i], lds[i].sm_mhz);
     printf(" \"popc_gops_roofline\": %.1f, \"fp64_nonfused_gops\": %.1f, \"how\": \"tools/pipe_peaks.cu: %d CTAs x %d threads, %d x %d independent ops per thread; G-ops/s from CUDA events, per-clk from clock64\"}\n",
            res[0].gops, (res[2].gops + res[3].gops) / 2, blocks, kThreads, kIters, kUnroll);
     return 0;
