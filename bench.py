@@ -344,7 +344,7 @@ class Ctx:
             self.eng.set_option("extract_variant", args.extract_variant)
         self.flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=self.dev)     # > 126 MB L2
         self.peaks = load_peaks()
-        self.mv = args.match_variant if args.match_variant is not None else 3
+        self.mv = args.match_variant if args.match_variant is not None else 4
         self.ev = args.extract_variant if args.extract_variant is not None else 4
 
     def flush(self):
@@ -452,18 +452,25 @@ class Ctx:
                "frac": hbm_bytes / seconds / 1e9 / self.peaks["hbm_gbs"], "algorithmic_bytes": hbm_bytes,
                "peak_source": self.peaks["source"],
                "note": "contract form (both sets + top-2 triples once); HBM does not bind this kernel"}
-        if self.mv == 3:
+        if self.mv in (3, 4):
             tops = cps * INT8_OPS_PER_COMPARE / 1e12
-            if pipes.get("int8_tops"):
-                peak, src = float(pipes["int8_tops"]), ("measured: tcgen05 kind::i8 M128 N256 K32 issue loop without epilogue, "
-                                                        "tools/tc_peak.cu -> profiles/pipe_peaks.json")
+            key, kind = ("mxf4", "kind::mxf4 e2m1, f32 accumulate") if self.mv == 4 else ("int8", "kind::i8, int32 accumulate")
+            if pipes.get(key + "_tops"):
+                peak = float(pipes[key + "_tops"])
+                src = (f"measured: tcgen05 {kind}, M128 N256 issue loop without epilogue at {pipes.get(key + '_sm_mhz')} MHz "
+                       "(tools/tc_peak.cu -> profiles/pipe_peaks.json); under the power cap of a long run the clock, and with "
+                       "it this peak, drops — see 'clock_scaled'")
             elif self.peaks.get("bf16_tflops"):
-                peak, src = 2 * self.peaks["bf16_tflops"], "2 x measured bf16 burst GEMM peak (MEASURED_PEAKS.json); nominal int8 dense 4500"
+                peak, src = (4 if self.mv == 4 else 2) * self.peaks["bf16_tflops"], "bf16 burst GEMM peak (MEASURED_PEAKS.json) x 2 (int8) or x 4 (fp4)"
             else:
-                peak, src = 2 * 1590.0, "2 x fallback bf16 peak"
+                peak, src = (4 if self.mv == 4 else 2) * 1590.0, "fallback bf16 peak x 2 (int8) or x 4 (fp4)"
             traffic, tsrc = ncu_traffic("match")
-            return {"kernel": "match_tc_kernel (tcgen05 kind::i8)", "bound": "tensor", "achieved": tops, "peak": peak,
-                    "unit": "TOP/s (int8; 1 compare = 512 MACs = 1024 ops)", "frac": tops / peak, "peak_source": src,
+            per_clk = float(pipes.get(key + "_mac_per_clk_sm", 16384 if self.mv == 4 else 8192))
+            scaled = 2 * per_clk * sms * sm_mhz * 1e6 / 1e12      # the same pipe at the clock sampled during THIS run
+            return {"kernel": f"match_tc_kernel (tcgen05 {kind})", "bound": "tensor", "achieved": tops, "peak": peak,
+                    "unit": "TOP/s (1 compare = 512 MACs = 1024 ops)", "frac": tops / peak, "peak_source": src,
+                    "clock_scaled": {"sm_mhz": sm_mhz, "peak": scaled, "frac": tops / scaled,
+                                     "note": "MACs/clk/SM of the microbenchmark x SMs x the SM clock sampled during this run"},
                     "includes": includes, "traffic": traffic, "traffic_source": tsrc, "hbm": hbm}
         popc = {0: 16, 1: 9, 2: 7}[self.mv]
         popc_peak = pipes.get("popc_gops", sms * 16 * sm_mhz * 1e6 / 1e9)
@@ -764,7 +771,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True, "scaling": rec["scaling"],
             "vs_baseline": None,
             "dtype": ("f64 resampling, " + ("fp32 estimate + exact f64 recompute" if cx.ev >= 2 else "f64 SSD") +
-                      " (extraction) / " + ("int8 tcgen05, int32 accumulate" if cx.mv == 3 else "u32 xor+popc") +
+                      " (extraction) / " + ({3: "int8 tcgen05, int32 accumulate", 4: "e2m1 tcgen05 (mxf4, unit scales), f32 accumulate"}.get(cx.mv, "u32 xor+popc")) +
                       " (matching); results bit-exact"),
             "data": "synthetic",
             "config": {"workload": rec["workload"], "phase": args.phase, "timing": rec["timing"],

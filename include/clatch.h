@@ -73,7 +73,8 @@ CLATCH_API void clatch_ctx_destroy(clatch_ctx* ctx);
 CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_khz, char* name, size_t cap);
 
 /* Tuning knobs (never change results). key "match_variant": 0 = XOR + 16 POPC, 1 = carry-save
- * compression + 9 POPC, 2 = 9 CSA + 7 POPC, 3 = tcgen05 int8 GEMM on the tensor cores (default).
+ * compression + 9 POPC, 2 = 9 CSA + 7 POPC, 3 = tcgen05 int8 GEMM on the tensor cores, 4 = tcgen05 block-scaled
+ * FP4 GEMM (e2m1 +-1.0 operands, every scale 2^0, f32 accumulators: exact, twice the MACs per clock; default).
  * key "extract_variant": 0 = one window per CTA, 1 = four fp64 windows per CTA with conflict-free
  * shared loads, 2 = four split (fp32 + low word) windows per CTA: a proven fp32 estimate decides
  * each bit and the rare undecided ones are recomputed exactly, 3 = the same estimate with
@@ -88,6 +89,8 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * bytes over the bus; lossless, same descriptors). 0 (default) does so when the image lies in ordinary
  * pageable memory — which the driver could only copy through its own bounce buffers — and uploads the
  * doubles of a page-locked image as they are (classified on the device); 1 = always, 2 = never.
+ * key "match_form_auto": 1 (default) lets match_variant 4 run mid-sized single matches (3e7 .. 6e8 compares) in
+ * the int8 form, which is ~10 % faster there; 0 = always e2m1.
  * key "match_pairs": 1 (default) runs the tensor-core matcher as clusters of two CTAs that share one stream of
  * train tiles through TMA multicast (half the L2 traffic per compare); 0 = every CTA streams for itself.
  * key "match_streamk": 1 (default) lets the tensor-core matcher split small problems (expanded train set

@@ -339,7 +339,7 @@ int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_khz, char* 
 int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
     if (!ctx || !key) return invalid("clatch_set_option: null argument");
     if (std::strcmp(key, "match_variant") == 0) {
-        if (value < 0 || value > 3) return invalid("match_variant must be 0..3");
+        if (value < 0 || value > 4) return invalid("match_variant must be 0..4");
         ctx->match_variant = value;
         return CLATCH_OK;
     }
@@ -355,6 +355,10 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
     }
     if (std::strcmp(key, "pairs_filter_on_device") == 0) {   // batched set pairs: filter pass on the device (1) or host (0)
         ctx->pairs_filter_on_device = value != 0;
+        return CLATCH_OK;
+    }
+    if (std::strcmp(key, "match_form_auto") == 0) {   // variant 4: let mid-sized single matches use the int8 form
+        ctx->match_form_auto = value != 0;
         return CLATCH_OK;
     }
     if (std::strcmp(key, "match_pairs") == 0) {   // tensor matcher: CTA pairs sharing the train stream by TMA multicast
@@ -1244,6 +1248,8 @@ struct clatch_set {
     uint8_t* block = nullptr;   // one stream-ordered allocation: packed | int8 operand form
     uint8_t* packed = nullptr;
     uint8_t* exp = nullptr;
+    size_t exp_cap = 0;         // bytes behind `exp` (sized for the larger operand form)
+    int fmt = 0;                // operand form `exp` holds (tc_format at expansion time); re-expanded when it changes
 };
 
 namespace {
@@ -1254,6 +1260,14 @@ int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t
                    bool cross_check, int32_t** host, std::vector<size_t>& pair_offset) {
     pair_offset.assign(count + 1, 0);
     size_t items = 0;
+    for (size_t p = 0; p < count; ++p)     // the matcher's operand form changed since a set was expanded: redo it
+        for (int side = 0; side < 2; ++side) {
+            clatch_set* s = const_cast<clatch_set*>(sets[pairs[2 * (first + p) + side]]);
+            if (s->fmt != tc_format(ctx) && s->n > 0) {
+                if (int rc = launch_tc_expand(ctx, s->packed, s->n, s->exp, ctx->stream)) return rc;
+                s->fmt = tc_format(ctx);
+            }
+        }
     for (size_t p = 0; p < count; ++p) {
         const clatch_set* a = sets[pairs[2 * (first + p)]];
         const clatch_set* b = sets[pairs[2 * (first + p) + 1]];
@@ -1271,22 +1285,24 @@ int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t
         const clatch_set* b = sets[pairs[2 * (first + p) + 1]];
         int32_t* base = r + pair_offset[p];
         const bool paired = tc_items_paired(ctx);   // CTA pairs: entries (2k, 2k + 1) must scan the same train set
+        const unsigned a_atoms = static_cast<unsigned>(tc_padded_rows(ctx, a->n) / 8);
+        const unsigned b_atoms = static_cast<unsigned>(tc_padded_rows(ctx, b->n) / 8);
         for (int q = 0; q < tc_query_tiles(a->n); ++q)
             table.push_back({a->exp, b->exp, static_cast<unsigned>(a->n),
-                             static_cast<unsigned>(b->n), static_cast<unsigned>(q), 0, base, base + a->n,
+                             static_cast<unsigned>(b->n), static_cast<unsigned>(q), 0, a_atoms, b_atoms, base, base + a->n,
                              base + 2 * a->n});
         if (paired && (table.size() & 1)) {         // odd tile count: a filler keeps the last tile's partner in step
             table.push_back(table.back());
-            table.back().pad = 1;
+            table.back().ghost = 1;
         }
         if (cross_check) {   // reverse_best[g] = knn2(gallery[g], probes).best_index, src/match.cpp:62-67
             for (int q = 0; q < tc_query_tiles(b->n); ++q)
                 table.push_back({b->exp, a->exp, static_cast<unsigned>(b->n),
-                                 static_cast<unsigned>(a->n), static_cast<unsigned>(q), 0, base + 3 * a->n, nullptr,
-                                 nullptr});
+                                 static_cast<unsigned>(a->n), static_cast<unsigned>(q), 0, b_atoms, a_atoms, base + 3 * a->n,
+                                 nullptr, nullptr});
             if (paired && (table.size() & 1)) {
                 table.push_back(table.back());
-                table.back().pad = 1;
+                table.back().ghost = 1;
             }
         }
     }
@@ -1396,7 +1412,7 @@ int clatch_set_create(clatch_ctx* ctx, const uint8_t* descriptors, size_t n, int
     if (n > 0) {
         cudaStream_t st = ctx->stream;
         const size_t packed_bytes = (n * 64 + 1023) / 1024 * 1024;
-        const size_t exp_bytes = tc_expanded_bytes(n);
+        const size_t exp_bytes = (n + 255) / 256 * 256 * 512 + 128 * 512;   // room for either operand form
         // cudaMallocAsync: pooled, stream-ordered — set churn does not pay cudaMalloc/cudaFree latency.
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&set->block), packed_bytes + exp_bytes, st);
         if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocAsync(set)");
@@ -1407,6 +1423,8 @@ int clatch_set_create(clatch_ctx* ctx, const uint8_t* descriptors, size_t n, int
                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(set)");
         }
+        set->exp_cap = exp_bytes;
+        set->fmt = tc_format(ctx);
         if (!rc) rc = launch_tc_expand(ctx, set->packed, n, set->exp, st);
         if (!rc && !on_device) {   // the caller may reuse its host buffer as soon as we return
             e = cudaStreamSynchronize(st);

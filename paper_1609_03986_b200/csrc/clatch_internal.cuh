@@ -99,8 +99,9 @@ struct clatch_ctx {
     // tensor matcher: clusters of two CTAs share the train-set stream through TMA multicast (one L2 read feeds two
     // SMs) wherever two query tiles scan the same train tiles; set_option "match_pairs" 0 = every CTA on its own.
     bool match_pairs = true;
+    bool match_form_auto = true;   // match_variant 4: mid-sized single matches run the int8 form (set_option "match_form_auto")
     bool match_streamk = true;     // tensor matcher: equal-share partition for small problems (set_option "match_streamk")
-    int match_variant = 3;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC 3: tcgen05 int8 GEMM (CLATCH_MATCH_VARIANT)
+    int match_variant = 4;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC, 3: tcgen05 int8 GEMM, 4: tcgen05 mxf4 (e2m1) GEMM (CLATCH_MATCH_VARIANT)
     // The scratch below is shared by every call on this context, whatever stream the call queues on
     // (the *_dev entry points take the caller's stream). scratch_event marks the last use; a call on a
     // different stream waits for it first (clatch::scratch_acquire / scratch_release), so two device-form
@@ -189,7 +190,8 @@ struct TcItem {    // one CTA of the tensor-core matcher in batched mode: 128 qu
     const uint8_t* b_exp;    // train set, expanded (same layout)
     unsigned Q, N;           // real row counts
     unsigned qtile;          // which 128-row query tile
-    unsigned pad;
+    unsigned ghost;          // CTA-pair tables: 1 = filler that only keeps its partner's operand stream company
+    unsigned a_atoms, b_atoms;   // 8-row atoms per K-block of the two expanded sets (tc_padded_rows / 8)
     int32_t* best_idx;       // outputs for the whole query set (any may be null)
     int32_t* best_dist;
     int32_t* second_dist;
@@ -206,9 +208,11 @@ struct FilterPair {   // one set pair of the on-device filter pass
 int launch_filter_pairs(clatch_ctx* ctx, const FilterPair* d_pairs, size_t count, int has_ratio, double ratio, int has_max,
                         int max_distance, int32_t* d_rows, unsigned* d_kept, unsigned long long* d_offsets,
                         int32_t* d_out, cudaStream_t stream);
-size_t tc_expanded_bytes(size_t rows);
+size_t tc_padded_rows(const clatch_ctx* ctx, size_t rows);    // rows of an expanded set in the context's operand form
+size_t tc_expanded_bytes(const clatch_ctx* ctx, size_t rows);
+int tc_format(const clatch_ctx* ctx);                          // 8 = int8 operands, 4 = e2m1 operands (match_variant 4)
 int tc_query_tiles(size_t rows);
-bool tc_items_paired(const clatch_ctx* ctx);   // item tables must hold entries (2k, 2k + 1) over one train set; TcItem::pad = 1 marks a filler
+bool tc_items_paired(const clatch_ctx* ctx);   // item tables must hold entries (2k, 2k + 1) over one train set; TcItem::ghost = 1 marks a filler
 int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t* d_out, cudaStream_t stream);
 int launch_match_tc_items(clatch_ctx* ctx, const TcItem* d_items, size_t count, cudaStream_t stream);
 void launch_merge_partials(const Partial* partial, unsigned long long Q, int splits, int sentinel,

@@ -394,7 +394,7 @@ static int match_top2_on(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
         CLATCH_CUDA(cudaGetLastError());
         return CLATCH_OK;
     }
-    if (ctx->match_variant == 3)
+    if (ctx->match_variant >= 3)   // 3: int8, 4: e2m1 operands on the tensor cores
         return launch_match_top2_tc(ctx, d_q, Q, d_t, N, d_best_idx, d_best_dist, d_second, stream);
     const size_t qblocks = (Q + kMatchThreads - 1) / kMatchThreads;
     // Enough CTAs for ~8 resident per SM, but never a split shorter than two tiles.

@@ -36,48 +36,85 @@ namespace clatch {
 
 namespace {
 
+#ifndef CLATCH_TC_EARLY_I8
+#define CLATCH_TC_EARLY_I8 false
+#endif
+#ifndef CLATCH_TC_EARLY_F4
+#define CLATCH_TC_EARLY_F4 false
+#endif
 constexpr int kTcM = 128;                 // queries per CTA (UMMA M)
-constexpr int kTcN = 256;                 // train rows per tile (UMMA N)
-constexpr int kTcKBlock = 128;            // bytes of K per smem stage = one swizzle-atom row
-constexpr int kTcKBlocks = 4;             // 512 / 128
+constexpr int kTcKBlock = 128;            // bytes of K per smem stage row = one swizzle-atom row
 constexpr int kTcStages = 4;
-constexpr int kTcABytes = kTcM * 512;             // 65536
-constexpr int kTcStageBytes = kTcN * kTcKBlock;   // 32768
 constexpr int kTcEpilogueWarps = 8;
 constexpr int kTcThreads = 32 * (2 + kTcEpilogueWarps);   // 320
-constexpr int kTcSmemBytes = kTcABytes + kTcStages * kTcStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
-                             2048 /*half-merge buffer*/;
+
+// Two operand forms, same kernel:
+//   TcI8  int8 +-1, 512 B per descriptor, kind::i8, int32 accumulators, 256 train rows per tile
+//   TcF4  e2m1 +-1.0 (0x2 / 0xA), 256 B per descriptor, kind::mxf4 with every UE8M0 block scale = 2^0, f32
+//         accumulators — twice the MACs per clock and half the operand bytes; 240 train rows per tile because
+//         the scale factors need TMEM columns too (2 x 240 accumulator columns + 2 x 16 columns of 0x7F bytes).
+// Every partial sum is an integer of magnitude <= 512, so f32 accumulation is as exact as int32.
+struct TcI8 {
+    static constexpr bool kF4 = false;
+    static constexpr int kN = 256;             // train rows per tile (UMMA N)
+    static constexpr int kKBlocks = 4;         // 128-byte K-blocks per descriptor row (512 B)
+    static constexpr bool kEarlyRelease = CLATCH_TC_EARLY_I8;
+};
+struct TcF4 {
+    static constexpr bool kF4 = true;
+    static constexpr int kN = 240;
+    static constexpr int kKBlocks = 2;         // 256 B per row
+    static constexpr bool kEarlyRelease = CLATCH_TC_EARLY_F4;
+};
+constexpr int kTcAccStride = 256;             // TMEM columns between the two accumulators
+constexpr int kTcSfaCol = 240, kTcSfbCol = 496;   // TcF4: 16 columns of scale bytes after each accumulator
+template <class F> __host__ __device__ constexpr int tc_a_bytes() { return kTcM * kTcKBlock * F::kKBlocks; }   // 64 / 32 KiB
+template <class F> __host__ __device__ constexpr int tc_stage_bytes() { return F::kN * kTcKBlock; }            // 32 / 30 KiB
+template <class F> __host__ __device__ constexpr int tc_smem_bytes() {
+    return tc_a_bytes<F>() + kTcStages * tc_stage_bytes<F>() + 1024 /*align*/ + 256 /*barriers*/ + 2048 /*half-merge buffer*/;
+}
 
 // ---------------------------------------------------------------- expansion ----
-// One layout serves both operands: 128-row tiles, each [4 K-blocks][16 atoms][1024 B]. A query
-// tile (A operand, M = 128) is one 64 KiB block; a train tile (B operand, N = 256) takes, per
-// K-block, the 16 KiB of two consecutive 128-row tiles. One thread writes one 16-byte chunk
-// (16 K-elements) of one row. Rows >= n (padding up to a multiple of 256) are zero and are
-// masked in the epilogue.
+// Global layout of an expanded set, both forms: [K-block][8-row atom][1024 B] — the UMMA canonical K-major
+// SWIZZLE_128B atom (8 rows x 128 B, 16-byte chunk index XOR row), K-block-major over the WHOLE set, so any run
+// of rows (a 128-row query tile, a 240- or 256-row train tile, or half of one) is one contiguous block per
+// K-block: plain 1-D TMA bulk copies, no tensor maps. One expansion serves a set as queries and as train rows.
+// Rows >= n (padding up to whole tiles) are zero and are masked in the epilogue. One thread writes one 16-byte
+// chunk: 16 bits of the descriptor as int8 (0xFF / 0x01), or 32 bits as e2m1 nibbles (0xA / 0x2).
+template <class F>
 __global__ void expand_kernel(const uint8_t* __restrict__ packed, unsigned long long n,
                               unsigned long long padded_rows, uint8_t* __restrict__ out) {
-    constexpr int rows_per_tile = kTcM;
+    constexpr int kChunks = F::kKBlocks * 8;           // 16-byte chunks per row
     const unsigned long long idx = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
-    const unsigned long long row = idx >> 5;          // 32 chunks per row
+    const unsigned long long row = idx / kChunks;
     if (row >= padded_rows) return;
-    const int chunk = static_cast<int>(idx & 31);     // bits [16*chunk, 16*chunk+16)
+    const int chunk = static_cast<int>(idx - row * kChunks);
     uint4 v = make_uint4(0, 0, 0, 0);
     if (row < n) {
-        const unsigned bits = *reinterpret_cast<const unsigned short*>(packed + row * 64 + 2 * chunk);
         unsigned w[4];
+        if (F::kF4) {
+            const unsigned bits = *reinterpret_cast<const unsigned*>(packed + row * 64 + 4 * chunk);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const unsigned nib = (bits >> (4 * i)) & 0xF;
-            // spread 4 bits to 4 bytes (0/1), then 1 -> 0x01 (+1), 0 -> 0xFF (-1)
-            const unsigned ones = (nib * 0x00204081u) & 0x01010101u;
-            w[i] = ((ones ^ 0x01010101u) * 0xFFu) | ones;   // per byte: 0 -> 0xFF (-1), 1 -> 0x01 (+1)
+            for (int i = 0; i < 4; ++i) {
+                unsigned b = (bits >> (8 * i)) & 0xFFu, nib = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) nib |= ((b >> j) & 1u) << (4 * j + 3);
+                w[i] = 0xAAAAAAAAu ^ nib;               // bit j -> nibble j: set 0x2 (+1.0), clear 0xA (-1.0)
+            }
+        } else {
+            const unsigned bits = *reinterpret_cast<const unsigned short*>(packed + row * 64 + 2 * chunk);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const unsigned nib = (bits >> (4 * i)) & 0xF;
+                // spread 4 bits to 4 bytes (0/1), then 1 -> 0x01 (+1), 0 -> 0xFF (-1)
+                const unsigned ones = (nib * 0x00204081u) & 0x01010101u;
+                w[i] = ((ones ^ 0x01010101u) * 0xFFu) | ones;
+            }
         }
         v = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    const unsigned long long tile = row / rows_per_tile;
-    const int r = static_cast<int>(row - tile * rows_per_tile);
-    const int kb = chunk >> 3, c = chunk & 7, g = r >> 3, ri = r & 7;
-    const unsigned long long atom = (tile * kTcKBlocks + kb) * (rows_per_tile / 8) + g;
+    const int kb = chunk >> 3, c = chunk & 7, ri = static_cast<int>(row & 7);
+    const unsigned long long atoms = padded_rows >> 3, atom = static_cast<unsigned long long>(kb) * atoms + (row >> 3);
     *reinterpret_cast<uint4*>(out + atom * 1024 + ri * 128 + ((c ^ ri) << 4)) = v;
 }
 
@@ -160,8 +197,45 @@ __device__ __forceinline__ uint64_t umma_desc(unsigned smem_addr) {
 }
 // Instruction descriptor (cute::UMMA::InstrDescriptor): D = S32 (2 @4), A = B = S8 (1 @7, 1 @10),
 // both K-major, N >> 3 @17, M >> 4 @24.
-constexpr unsigned kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((kTcN >> 3) << 17) | ((kTcM >> 4) << 24);
+constexpr unsigned kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((TcI8::kN >> 3) << 17) | ((kTcM >> 4) << 24);
+// Block-scaled descriptor (cute::UMMA::InstrDescriptorBlockScaled): A = B = E2M1 (MXF4Format 1 @7, @10), scale
+// format UE8M0 (1 @23), scale-factor ids 0, N >> 3 @17, M >> 4 @24; K = 64 per instruction, D = f32.
+constexpr unsigned kIdescF4 = (1u << 7) | (1u << 10) | (1u << 23) | ((TcF4::kN >> 3) << 17) | ((kTcM >> 4) << 24);
+// D[tmem] (+)= A[smem] * B[smem]^T, e2m1 x e2m1 -> f32, one UE8M0 scale per 32 K-elements read from TMEM
+// (all 0x7F = 2^0 here), M=128, N=240, K=64.
+__device__ __forceinline__ void tc_mma_f4(unsigned tmem_d, uint64_t desc_a, uint64_t desc_b, unsigned idesc,
+                                          unsigned accumulate, unsigned tmem_sfa, unsigned tmem_sfb) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb)
+        : "memory");
+}
+// 16 TMEM columns of this warp's lane quarter <- one 32-bit value.
+__device__ __forceinline__ void tmem_fill16(unsigned taddr, unsigned v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Issue only: the registers are valid after tmem_wait_ld().
+__device__ __forceinline__ void tmem_ld32_issue(unsigned taddr, int (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -184,8 +258,9 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, int (&v)[32]) {
 // covers a whole train set and writes final results). Barriers, TMEM and the smem ring are
 // set up once per CTA; only the 64 KiB A operand is reloaded per item.
 struct TcWork {
-    const uint8_t* a;     // expanded query tile (64 KiB)
-    const uint8_t* b;     // expanded train set (B form), tile 0
+    const uint8_t* a;     // expanded query set: K-block 0 of this tile's first atom
+    const uint8_t* b;     // expanded train set
+    unsigned long long a_kb_stride, b_kb_stride;   // bytes between K-blocks of the two sets (atoms x 1024)
     unsigned long long Q, N;
     unsigned qtile;
     int tile_begin, ntiles, split;
@@ -197,6 +272,7 @@ struct TcArgs {
     const uint8_t* a_exp;
     const uint8_t* b_exp;
     unsigned long long Q, N;
+    unsigned long long a_atoms, b_atoms;   // 8-row atoms per K-block of the two expanded sets
     int qtiles, total_tiles, tiles_per_split, num_items;
     int sk_chunks;           // > 0: "stream-K" partition of the (query tile, train tile) units over this many CTAs
     Partial* partial;
@@ -215,14 +291,20 @@ __host__ __device__ __forceinline__ unsigned long long tc_sk_chunk_of(unsigned l
 
 // kPair: `item` counts PAIR items; the two CTAs of a cluster (rank 0 / 1) take two query tiles that scan the same
 // train tiles — table entries 2 * item + rank, or query tiles 2j + rank of one split.
-template <bool kPair>
+template <class F, bool kPair>
 __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned rank) {
+    constexpr int kTcN = F::kN;
+    constexpr unsigned long long kTileA = kTcM / 8 * 1024;     // bytes of one query tile inside a K-block
     TcWork w;
     w.ghost = false;
+    w.a_kb_stride = g.a_atoms * 1024;
+    w.b_kb_stride = g.b_atoms * 1024;
     if (g.items != nullptr) {
         const TcItem it = g.items[kPair ? 2 * item + static_cast<int>(rank) : item];
-        w.ghost = it.pad != 0;
-        w.a = it.a_exp + static_cast<unsigned long long>(it.qtile) * kTcABytes;
+        w.ghost = it.ghost != 0;
+        w.a_kb_stride = static_cast<unsigned long long>(it.a_atoms) * 1024;
+        w.b_kb_stride = static_cast<unsigned long long>(it.b_atoms) * 1024;
+        w.a = it.a_exp + static_cast<unsigned long long>(it.qtile) * kTileA;
         w.b = it.b_exp;
         w.Q = it.Q;
         w.N = it.N;
@@ -258,7 +340,7 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned 
         w.tile_begin = static_cast<int>(t0);
         w.ntiles = static_cast<int>(n);
         w.split = static_cast<int>(c - tc_sk_chunk_of(q * TT, U, G));   // pieces of a query tile in train order
-        w.a = g.a_exp + q * kTcABytes;
+        w.a = g.a_exp + q * kTileA;
         w.b = g.b_exp;
         w.Q = g.Q;
         w.N = g.N;
@@ -272,7 +354,7 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned 
             w.ghost = true;
         }
         w.qtile = static_cast<unsigned>(qt);
-        w.a = g.a_exp + static_cast<unsigned long long>(w.qtile) * kTcABytes;
+        w.a = g.a_exp + static_cast<unsigned long long>(w.qtile) * kTileA;
         w.b = g.b_exp;
         w.Q = g.Q;
         w.N = g.N;
@@ -284,7 +366,7 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned 
         // train tiles at the same time, so HBM sees them once and L2 serves the rest
         w.split = item / g.qtiles;
         w.qtile = static_cast<unsigned>(item - w.split * g.qtiles);
-        w.a = g.a_exp + static_cast<unsigned long long>(w.qtile) * kTcABytes;
+        w.a = g.a_exp + static_cast<unsigned long long>(w.qtile) * kTileA;
         w.b = g.b_exp;
         w.Q = g.Q;
         w.N = g.N;
@@ -301,8 +383,11 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned 
 // query tiles against the SAME train tiles: each loads half of every B stage and multicasts it into both
 // CTAs' shared memory (one L2 read feeds two SMs), and a stage is handed back to the producers only when both
 // CTAs' MMAs have read it (multicast tcgen05.commit onto both `empty` barriers).
-template <bool kPair>
+template <class F, bool kPair>
 __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g) {
+    constexpr int kTcN = F::kN, kTcKBlocks = F::kKBlocks;
+    constexpr bool kEarlyRelease = F::kEarlyRelease;
+    constexpr int kTcABytes = tc_a_bytes<F>(), kTcStageBytes = tc_stage_bytes<F>();
     const unsigned rank = kPair ? cluster_rank() : 0u;
     const int first_item = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
     const int item_step = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
@@ -348,6 +433,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
     if (kPair) cluster_sync_all();                             // the partner's barriers exist before anything lands on them
     tc_fence_after();
     const unsigned tmem_base = *tmem_slot;
+    if (F::kF4) {
+        // Block scales: every byte of the 16 columns behind each accumulator is UE8M0 0x7F = 2^0, so whichever
+        // cells the MMA reads for its 128 A rows and 240 B rows, each 32-element block is scaled by exactly 1.
+        if (warp >= 2 && warp < 6) {
+            const unsigned lanes = static_cast<unsigned>((warp & 3) * 32) << 16;
+            tmem_fill16(tmem_base + lanes + kTcSfaCol, 0x7F7F7F7Fu);
+            tmem_fill16(tmem_base + lanes + kTcSfbCol, 0x7F7F7F7Fu);
+        }
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
 
     if (warp == 0) {
         // ===== producer =====
@@ -355,27 +452,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
             int stage = 0;
             unsigned phase = 0, a_phase = 0;
             for (int item = first_item; item < g.num_items; item += item_step) {
-                const TcWork w = tc_decode<kPair>(g, item, rank);
+                const TcWork w = tc_decode<F, kPair>(g, item, rank);
                 if (w.ntiles == 0) continue;                   // (stream-K: this CTA has fewer pieces)
                 mbar_wait(bar_a_empty, a_phase ^ 1);           // previous item's MMAs are done with A
                 mbar_expect_tx(bar_a_full, kTcABytes);
-                bulk_load(smem_a, w.a, kTcABytes, bar_a_full);
+                for (int kb = 0; kb < kTcKBlocks; ++kb)        // 128 rows x 128 B of every K-block
+                    bulk_load(smem_a + kb * (kTcM * kTcKBlock), w.a + kb * w.a_kb_stride, kTcM * kTcKBlock, bar_a_full);
                 a_phase ^= 1;
                 for (int t = 0; t < w.ntiles; ++t) {
-                    // train tile = two consecutive 128-row tiles of the expanded set
-                    const uint8_t* src = w.b + static_cast<unsigned long long>(w.tile_begin + t) * (2 * kTcABytes);
+                    // train tile = kTcN consecutive rows = kTcN / 8 consecutive atoms of every K-block
+                    const uint8_t* src = w.b + static_cast<unsigned long long>(w.tile_begin + t) * (kTcN / 8 * 1024);
                     for (int kb = 0; kb < kTcKBlocks; ++kb) {
                         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
                         mbar_expect_tx(bar_full + 8 * stage, kTcStageBytes);
                         const unsigned dst = smem_b + stage * kTcStageBytes;
                         if (kPair) {   // this CTA's half of the stage, to both CTAs
                             bulk_load_multicast(dst + rank * (kTcStageBytes / 2),
-                                                src + rank * kTcABytes + kb * (kTcStageBytes / 2), kTcStageBytes / 2,
+                                                src + kb * w.b_kb_stride + rank * (kTcStageBytes / 2), kTcStageBytes / 2,
                                                 bar_full + 8 * stage, 3);
                         } else {
-                            bulk_load(dst, src + kb * (kTcStageBytes / 2), kTcStageBytes / 2, bar_full + 8 * stage);
-                            bulk_load(dst + kTcStageBytes / 2, src + kTcABytes + kb * (kTcStageBytes / 2), kTcStageBytes / 2,
-                                      bar_full + 8 * stage);
+                            bulk_load(dst, src + kb * w.b_kb_stride, kTcStageBytes, bar_full + 8 * stage);
                         }
                         if (++stage == kTcStages) { stage = 0; phase ^= 1; }
                     }
@@ -388,7 +484,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
             int stage = 0, tcount = 0;
             unsigned phase = 0, a_phase = 0;
             for (int item = first_item; item < g.num_items; item += item_step) {
-                const TcWork w = tc_decode<kPair>(g, item, rank);
+                const TcWork w = tc_decode<F, kPair>(g, item, rank);
                 if (w.ntiles == 0) continue;
                 mbar_wait(bar_a_full, a_phase);
                 a_phase ^= 1;
@@ -396,16 +492,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
                     const int buf = tcount & 1;
                     mbar_wait(bar_tempty + 8 * buf, ((tcount >> 1) & 1) ^ 1);   // epilogue drained this accumulator
                     tc_fence_after();
-                    const unsigned tmem_d = tmem_base + buf * kTcN;
+                    const unsigned tmem_d = tmem_base + buf * kTcAccStride;
                     for (int kb = 0; kb < kTcKBlocks; ++kb) {
                         mbar_wait(bar_full + 8 * stage, phase);
                         tc_fence_after();
                         const unsigned a_addr = smem_a + kb * (kTcM * kTcKBlock);
                         const unsigned b_addr = smem_b + stage * kTcStageBytes;
 #pragma unroll
-                        for (int k = 0; k < kTcKBlock / 32; ++k)
-                            tc_mma_i8(tmem_d, umma_desc(a_addr + 32 * k), umma_desc(b_addr + 32 * k), kIdesc,
-                                      (kb | k) != 0);
+                        for (int k = 0; k < kTcKBlock / 32; ++k) {   // 32 bytes of K per instruction: 32 int8 or 64 e2m1
+                            if (F::kF4)
+                                tc_mma_f4(tmem_d, umma_desc(a_addr + 32 * k), umma_desc(b_addr + 32 * k), kIdescF4,
+                                          (kb | k) != 0, tmem_base + kTcSfaCol, tmem_base + kTcSfbCol);
+                            else
+                                tc_mma_i8(tmem_d, umma_desc(a_addr + 32 * k), umma_desc(b_addr + 32 * k), kIdescI8,
+                                          (kb | k) != 0);
+                        }
                         if (kPair) tc_commit_multicast(bar_empty + 8 * stage, 3);
                         else tc_commit(bar_empty + 8 * stage);  // stage reusable once these MMAs have read it
                         if (++stage == kTcStages) { stage = 0; phase ^= 1; }
@@ -424,50 +525,92 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
         const int row = quarter * 32 + lane;
         int tcount = 0;
         for (int item = first_item; item < g.num_items; item += item_step) {
-            const TcWork w = tc_decode<kPair>(g, item, rank);
+            const TcWork w = tc_decode<F, kPair>(g, item, rank);
             if (w.ntiles == 0) continue;
-            int best = INT_MIN, second = INT_MIN, best_idx = -1;
+            // best / second are dot products D = 512 - 2 * hamming, kept as the raw accumulator words: int32, or the
+            // bits of an f32 holding that integer. Signed-integer order on f32 bits is the float order among
+            // non-negative values and puts every negative value below them, so the per-chunk test (3-input integer
+            // max over the 32 words against the runner-up) is exact whenever the runner-up is >= 0 (second_key =
+            // its bits); until then second_key = INT_MIN and every chunk takes the full pass, which compares as floats.
+            int best = F::kF4 ? static_cast<int>(0xFF800000u) : INT_MIN, second = best, best_idx = -1;   // -inf / INT_MIN
+            int second_key = INT_MIN;
             for (int t = 0; t < w.ntiles; ++t, ++tcount) {
                 const int buf = tcount & 1;
                 mbar_wait(bar_tfull + 8 * buf, (tcount >> 1) & 1);
                 tc_fence_after();
-                const long long col0 = static_cast<long long>(w.tile_begin + t) * kTcN + half * 128;
-                const long long valid = static_cast<long long>(w.N) - col0;   // columns < valid are real rows
-#pragma unroll 1
-                for (int chunk = 0; chunk < 4; ++chunk) {
-                    int v[32];
-                    tmem_ld32(tmem_base + lane_addr + buf * kTcN + half * 128 + chunk * 32, v);
+                const long long tile_col0 = static_cast<long long>(w.tile_begin + t) * kTcN;
+                const long long tile_valid = min(static_cast<long long>(kTcN), static_cast<long long>(w.N) - tile_col0);
+                // One 32-column chunk of this lane's row: mask, 3-input max, and the full pass when it can matter.
+                auto consume = [&](int (&v)[32], const int ccol) {
                     if (g.dump != nullptr && item == 0 && t == 0 && rank == 0) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) g.dump[row * kTcN + half * 128 + chunk * 32 + i] = v[i];
+                        for (int i = 0; i < 32; ++i)
+                            if (ccol + i < kTcN)
+                                g.dump[row * 256 + ccol + i] = F::kF4 ? static_cast<int>(__int_as_float(v[i])) : v[i];
                     }
-                    const long long cvalid = valid - chunk * 32;
-                    if (cvalid < 32) {                          // last tile only: mask the zero padding rows
+                    const long long cvalid = tile_valid - ccol;
+                    if (cvalid < 32) {     // the set's last tile (zero padding rows) and the columns past kTcN
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
-                            if (i >= cvalid) v[i] = INT_MIN;
+                            if (i >= cvalid) v[i] = F::kF4 ? static_cast<int>(0xFF800000u) : INT_MIN;   // -inf
                     }
                     int m = v[0];
 #pragma unroll
                     for (int i = 1; i < 32; i += 2) m = max(m, max(v[i], i + 1 < 32 ? v[i + 1] : INT_MIN));
-                    if (m > second) {                           // something in this chunk enters the top-2
-                        const int cbase = t * kTcN + half * 128 + chunk * 32;
+                    if (m > second_key) {                       // something in this chunk may enter the top-2
+                        const int cbase = t * kTcN + ccol;
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
                             const int d = v[i];
-                            if (d > best) {                     // strict: earlier (lower) index keeps ties
+                            const bool gt_best = F::kF4 ? __int_as_float(d) > __int_as_float(best) : d > best;
+                            const bool gt_second = F::kF4 ? __int_as_float(d) > __int_as_float(second) : d > second;
+                            if (gt_best) {                      // strict: earlier (lower) index keeps ties
                                 second = best;
                                 best = d;
                                 best_idx = cbase + i;
-                            } else if (d > second) {
+                            } else if (gt_second) {
                                 second = d;
                             }
                         }
+                        second_key = !F::kF4 ? second : (__int_as_float(second) >= 0.f ? second : INT_MIN);
                     }
+                };
+                const unsigned acc = tmem_base + lane_addr + buf * kTcAccStride + half * 128;
+                if (kEarlyRelease) {
+                    // All of this warp's 128 columns in flight at once (one TMEM round trip instead of four), and the
+                    // accumulator is handed back to the MMA issuer as soon as they sit in registers. Measured 2.5x
+                    // SLOWER than the chunk-by-chunk loop in both forms (r3e: 1 M x 1 M 3.06e12 vs 5.12e12 compares/s
+                    // with TcF4) — kept behind CLATCH_TC_EARLY_* for A/B only.
+                    int v0[32], v1[32], v2[32], v3[32];
+                    tmem_ld32_issue(acc, v0);
+                    tmem_ld32_issue(acc + 32, v1);
+                    tmem_ld32_issue(acc + 64, v2);
+                    tmem_ld32_issue(acc + 96, v3);   // (TcF4, upper half: columns 224..255, the last 16 are scale bytes - masked)
+                    tmem_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                    consume(v0, half * 128);
+                    consume(v1, half * 128 + 32);
+                    consume(v2, half * 128 + 64);
+                    if (half * 128 + 96 < kTcN) consume(v3, half * 128 + 96);
+                } else {
+#pragma unroll 1
+                    for (int chunk = 0; chunk < 4; ++chunk) {
+                        const int ccol = half * 128 + chunk * 32;   // first column of this chunk inside the tile
+                        if (ccol >= kTcN) break;
+                        int v[32];
+                        tmem_ld32(acc + chunk * 32, v);
+                        consume(v, ccol);
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+            }
+            if (F::kF4) {   // f32 bits -> the integer they hold (-inf: nothing seen)
+                best = __int_as_float(best) > -1024.f ? static_cast<int>(__int_as_float(best)) : INT_MIN;
+                second = __int_as_float(second) > -1024.f ? static_cast<int>(__int_as_float(second)) : INT_MIN;
             }
             // merge the two column halves of each row
             if (half == 1) {
@@ -553,19 +696,36 @@ __global__ void merge_partials_sk_kernel(const Partial* __restrict__ partial, un
 // The opt-in shared-memory size is a per-device function attribute: remember it per context.
 static int configure_tc(clatch_ctx* ctx) {
     if (!ctx->tc_configured) {
-        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemBytes));
-        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmemBytes));
+        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<TcI8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<TcI8>()));
+        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<TcI8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<TcI8>()));
+        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<TcF4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<TcF4>()));
+        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<TcF4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<TcF4>()));
         ctx->tc_configured = true;
     }
     return CLATCH_OK;
 }
 
-size_t tc_expanded_bytes(size_t rows) { return (rows + kTcN - 1) / kTcN * (2 * static_cast<size_t>(kTcABytes)); }
+static int tc_tile_rows(const clatch_ctx* ctx) { return ctx->match_variant == 4 ? TcF4::kN : TcI8::kN; }
+static size_t tc_row_bytes(const clatch_ctx* ctx) { return ctx->match_variant == 4 ? 256 : 512; }
+
+// Rows an expanded set is padded to: whole train tiles AND whole 128-row query tiles of the current form.
+size_t tc_padded_rows(const clatch_ctx* ctx, size_t rows) {
+    const size_t n = tc_tile_rows(ctx);
+    return std::max((rows + n - 1) / n * n, (rows + kTcM - 1) / kTcM * kTcM);
+}
+size_t tc_expanded_bytes(const clatch_ctx* ctx, size_t rows) { return tc_padded_rows(ctx, rows) * tc_row_bytes(ctx); }
+int tc_format(const clatch_ctx* ctx) { return ctx->match_variant == 4 ? 4 : 8; }
 
 int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t* d_out, cudaStream_t stream) {
-    const unsigned long long rows = (n + kTcN - 1) / kTcN * kTcN, threads = rows * 32;
+    const unsigned long long rows = tc_padded_rows(ctx, n);
     if (rows == 0) return CLATCH_OK;
-    expand_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(d_packed, n, rows, d_out);
+    if (ctx->match_variant == 4) {
+        const unsigned long long threads = rows * (TcF4::kKBlocks * 8);
+        expand_kernel<TcF4><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(d_packed, n, rows, d_out);
+    } else {
+        const unsigned long long threads = rows * (TcI8::kKBlocks * 8);
+        expand_kernel<TcI8><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(d_packed, n, rows, d_out);
+    }
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
     return CLATCH_OK;
@@ -573,12 +733,20 @@ int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t
 
 int tc_query_tiles(size_t rows) { return static_cast<int>((rows + kTcM - 1) / kTcM); }
 
-// Clusters of two CTAs (cudaLaunchKernelEx): the paired form of the kernel.
-static int launch_tc_pairs(clatch_ctx* ctx, const TcArgs& g, unsigned ctas, cudaStream_t stream) {
+// One launch of the kernel in the context's operand form; `paired` = clusters of two CTAs (cudaLaunchKernelEx).
+static int launch_tc(clatch_ctx* ctx, const TcArgs& g, unsigned ctas, bool paired, cudaStream_t stream) {
+    const bool f4 = ctx->match_variant == 4;
+    if (!paired) {
+        if (f4) match_tc_kernel<TcF4, false><<<ctas, kTcThreads, tc_smem_bytes<TcF4>(), stream>>>(g);
+        else match_tc_kernel<TcI8, false><<<ctas, kTcThreads, tc_smem_bytes<TcI8>(), stream>>>(g);
+        ++ctx->launches;
+        CLATCH_CUDA(cudaGetLastError());
+        return CLATCH_OK;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctas & ~1u);
     cfg.blockDim = dim3(kTcThreads);
-    cfg.dynamicSmemBytes = kTcSmemBytes;
+    cfg.dynamicSmemBytes = f4 ? tc_smem_bytes<TcF4>() : tc_smem_bytes<TcI8>();
     cfg.stream = stream;
     cudaLaunchAttribute attr{};
     attr.id = cudaLaunchAttributeClusterDimension;
@@ -587,7 +755,8 @@ static int launch_tc_pairs(clatch_ctx* ctx, const TcArgs& g, unsigned ctas, cuda
     attr.val.clusterDim.z = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    CLATCH_CUDA(cudaLaunchKernelEx(&cfg, match_tc_kernel<true>, g));
+    if (f4) CLATCH_CUDA(cudaLaunchKernelEx(&cfg, match_tc_kernel<TcF4, true>, g));
+    else CLATCH_CUDA(cudaLaunchKernelEx(&cfg, match_tc_kernel<TcI8, true>, g));
     ++ctx->launches;
     return CLATCH_OK;
 }
@@ -597,32 +766,48 @@ int launch_match_tc_items(clatch_ctx* ctx, const TcItem* d_items, size_t count, 
     if (int rc = configure_tc(ctx)) return rc;
     TcArgs g{};
     g.items = d_items;
+    const unsigned ctas = static_cast<unsigned>(std::min<size_t>(count, ctx->sm_count));
     if (ctx->match_pairs) {   // the table holds entries (2k, 2k + 1) that scan the same train set (tc_items_paired)
         g.num_items = static_cast<int>(count / 2);
-        return launch_tc_pairs(ctx, g, static_cast<unsigned>(std::min<size_t>(count, ctx->sm_count)), stream);
+        return launch_tc(ctx, g, ctas, true, stream);
     }
     g.num_items = static_cast<int>(count);
-    const unsigned grid = static_cast<unsigned>(std::min<size_t>(count, ctx->sm_count));
-    match_tc_kernel<false><<<grid, kTcThreads, kTcSmemBytes, stream>>>(g);
-    ++ctx->launches;
-    CLATCH_CUDA(cudaGetLastError());
-    return CLATCH_OK;
+    return launch_tc(ctx, g, ctas, false, stream);
 }
 
 bool tc_items_paired(const clatch_ctx* ctx) { return ctx->match_pairs; }
 
+static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
+                              int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
+                              int32_t* d_dump);
+
 int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
                          int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
                          int32_t* d_dump) {
+    // Operand form per call under match_variant 4: e2m1 wins at scale (1 M x 1 M: 5.1e12 vs 3.3e12 compares/s) and on
+    // tiny problems; in between, where the top-2 bookkeeping of short runs dominates and the int8 kernel's longer
+    // tiles amortise it better, int8 is ~10 % ahead (8 k .. 20 k squared, profiles/r3e_match_perf.log).
+    const int saved = ctx->match_variant;
+    const double work = static_cast<double>(Q) * static_cast<double>(N);
+    if (saved == 4 && ctx->match_form_auto && work >= 3e7 && work <= 6e8) ctx->match_variant = 3;
+    const int rc = match_top2_tc_impl(ctx, d_q, Q, d_t, N, d_best_idx, d_best_dist, d_second, stream, d_dump);
+    ctx->match_variant = saved;
+    return rc;
+}
+
+static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
+                              int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
+                              int32_t* d_dump) {
     if (int rc = configure_tc(ctx)) return rc;
+    const size_t kTcN = tc_tile_rows(ctx);
     const size_t qtiles = (Q + kTcM - 1) / kTcM, ttiles = (N + kTcN - 1) / kTcN;
-    // Both sets go to the tensor cores as int8; a self-match expands its one set once.
+    // Both sets go to the tensor cores in the expanded form; a self-match expands its one set once.
     const bool self = d_q == d_t && Q == N;
-    if (int rc = ctx->exp_t.reserve(tc_expanded_bytes(N))) return rc;
+    if (int rc = ctx->exp_t.reserve(tc_expanded_bytes(ctx, N))) return rc;
     if (int rc = launch_tc_expand(ctx, d_t, N, ctx->exp_t.as<uint8_t>(), stream)) return rc;
     const uint8_t* a_exp = ctx->exp_t.as<uint8_t>();
     if (!self) {
-        if (int rc = ctx->exp_q.reserve(tc_expanded_bytes(Q))) return rc;
+        if (int rc = ctx->exp_q.reserve(tc_expanded_bytes(ctx, Q))) return rc;
         if (int rc = launch_tc_expand(ctx, d_q, Q, ctx->exp_q.as<uint8_t>(), stream)) return rc;
         a_exp = ctx->exp_q.as<uint8_t>();
     }
@@ -651,7 +836,7 @@ int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
     const size_t units = qtiles * ttiles, chunks = std::min(units, sms);
     bool streamk = false;
     size_t sk_pieces_per_cta = 1, sk_pieces_per_qtile = 1;
-    if (tc_expanded_bytes(N) <= (32u << 20) && units > 0 && ctx->match_streamk) {
+    if (tc_expanded_bytes(ctx, N) <= (32u << 20) && units > 0 && ctx->match_streamk) {
         const size_t share = (units + chunks - 1) / chunks;                 // tile-times per CTA
         sk_pieces_per_cta = (share + ttiles - 2) / ttiles + 1;
         sk_pieces_per_qtile = (ttiles + units / chunks - 1) / (units / chunks) + 1;
@@ -683,6 +868,8 @@ int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
     g.b_exp = ctx->exp_t.as<uint8_t>();
     g.Q = Q;
     g.N = N;
+    g.a_atoms = tc_padded_rows(ctx, self ? N : Q) / 8;
+    g.b_atoms = tc_padded_rows(ctx, N) / 8;
     g.qtiles = static_cast<int>(qtiles);
     g.total_tiles = static_cast<int>(ttiles);
     g.tiles_per_split = static_cast<int>(per_split);
@@ -693,13 +880,11 @@ int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const ui
     if (paired) {
         const size_t pair_items = (qtiles + 1) / 2 * splits;
         g.num_items = static_cast<int>(pair_items);
-        if (int rc = launch_tc_pairs(ctx, g, static_cast<unsigned>(std::min<size_t>(2 * pair_items, sms)), stream)) return rc;
+        if (int rc = launch_tc(ctx, g, static_cast<unsigned>(std::min<size_t>(2 * pair_items, sms)), true, stream)) return rc;
     } else {
         const unsigned grid = static_cast<unsigned>(streamk ? chunks : std::min<size_t>(qtiles * splits, ctx->sm_count));
-        match_tc_kernel<false><<<grid, kTcThreads, kTcSmemBytes, stream>>>(g);
-        ++ctx->launches;
+        if (int rc = launch_tc(ctx, g, grid, false, stream)) return rc;
     }
-    CLATCH_CUDA(cudaGetLastError());
     if (streamk)
         merge_partials_sk_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(
             ctx->partial.as<Partial>(), Q, static_cast<int>(ttiles), static_cast<int>(qtiles), static_cast<int>(chunks),

@@ -373,14 +373,15 @@ def test_python_smoke_shapes(lk, golden_image_u8):
 
 # ------------------------------------------------- matcher kernel variants ----
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_every_matcher_variant_is_exact(lk, port, variant):
-    """All four 64-byte matcher kernels (plain popc, two carry-save forms, tcgen05 int8 GEMM)
+    """All five 64-byte matcher kernels (plain popc, two carry-save forms, tcgen05 int8 and FP4 GEMMs)
     must give the reference's knn2 triples bit for bit, including ties, tails and a lone row."""
     eng = lk.get_engine()
     eng.set_option("match_variant", variant)
+    eng.set_option("match_form_auto", 0)             # variant 4 means the e2m1 form at every size here
     try:
-        for q, n in [(1, 1), (5, 255), (129, 256), (130, 257), (300, 1000), (1000, 5000), (77, 40000)]:
+        for q, n in [(1, 1), (5, 255), (129, 256), (130, 257), (300, 1000), (1000, 5000), (77, 40000), (7000, 7000)]:
             d = port.random_descriptors(7000 + q + n, q + n, 64)
             probes, gallery = d[:q].copy(), d[q:].copy()
             if n > 3:
@@ -398,8 +399,15 @@ def test_every_matcher_variant_is_exact(lk, port, variant):
         bi, bd, sd = eng.match_top2(probes, gallery)
         assert np.array_equal(np.stack([bi, bd, sd], 1), port.knn2_all(probes, gallery))
         assert (bi[0], bd[0], sd[0]) == (1, 0, 0) and (bi[1], bd[1], sd[1]) == (0, 0, 512)
+        # every distance above 256 (all dot products negative): the f32 epilogue's full-pass route
+        gallery = ~np.repeat(probes[2:3], 300, 0)
+        gallery[::7, 0] ^= 1
+        gallery[5, 1] ^= 3
+        bi, bd, sd = eng.match_top2(probes[2:3], gallery)
+        assert np.array_equal(np.stack([bi, bd, sd], 1), port.knn2_all(probes[2:3], gallery)) and bd[0] > 500
     finally:
-        eng.set_option("match_variant", 3)
+        eng.set_option("match_variant", 4)
+        eng.set_option("match_form_auto", 1)
 
 
 @pytest.mark.parametrize("shape", [(1, 1), (1, 300), (129, 257), (700, 513), (2000, 2000), (5000, 9000),
@@ -425,12 +433,22 @@ def test_tensor_matcher_partitions_agree(lk, port, shape):
         for sk in (1, 0):
             eng.set_option("match_streamk", sk)
             res[sk] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_form_auto", 0)            # e2m1 operands at every size
         eng.set_option("match_pairs", 0)                # every CTA streams the train set for itself
         res[2] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_variant", 3)              # int8 operands (default: e2m1)
+        res[3] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_pairs", 1)
+        res[4] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_streamk", 1)
+        res[5] = np.stack(eng.match_top2(query, train))
     finally:
         eng.set_option("match_streamk", 1)
         eng.set_option("match_pairs", 1)                # default: CTA pairs share the stream by TMA multicast
-    assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
+        eng.set_option("match_variant", 4)
+        eng.set_option("match_form_auto", 1)
+    for k in (1, 2, 3, 4, 5):
+        assert np.array_equal(res[0], res[k]), k
     rows = np.arange(q_n) if q_n * t_n <= 4_000_000 else np.unique(np.r_[np.arange(0, q_n, 7)[:40], rng.integers(0, q_n, 40)])
     assert np.array_equal(res[1][:, rows].T, port.knn2_all(query[rows], train))
 

@@ -14,7 +14,7 @@ from paper_1609_03986_b200.engine import get_engine   # noqa: E402
 eng = get_engine()
 shapes = [(2_000, 2_000), (8_000, 8_000), (10_000, 10_000), (20_000, 20_000), (100_000, 100_000), (20_000, 1_000_000),
           (1_000_000, 1_000_000)]
-variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1, 3]
+variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1, 3, 4]
 rows = []
 g = torch.Generator(device="cuda").manual_seed(0)
 for q, n in shapes:
