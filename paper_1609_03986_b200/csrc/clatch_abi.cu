@@ -1320,6 +1320,10 @@ int run_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t
     return CLATCH_OK;
 }
 
+int filter_table_on_device(clatch_ctx* ctx, const std::vector<FilterPair>& table, unsigned long long probes, int has_ratio,
+                           double ratio, int has_max, int max_distance, const int32_t** rows,
+                           std::vector<unsigned long long>& offsets);
+
 // The filter pass of a batch on the device: kept rows of all pairs back to back in page-locked memory
 // (*rows), row offsets per pair in offsets[0..count]. Only the surviving rows cross the bus.
 int filter_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int32_t* pairs, size_t first, size_t count,
@@ -1334,6 +1338,14 @@ int filter_pair_batch(clatch_ctx* ctx, const clatch_set* const* sets, const int3
         table[p] = {base, base + n, base + 2 * n, cross_check ? base + 3 * n : nullptr, static_cast<unsigned>(n), 0, probes};
         probes += n;
     }
+    return filter_table_on_device(ctx, table, probes, has_ratio, ratio, has_max, max_distance, rows, offsets);
+}
+
+// The filter pass (src/match.cpp:69-79) of `table.size()` result blocks that already sit on the device.
+int filter_table_on_device(clatch_ctx* ctx, const std::vector<FilterPair>& table, unsigned long long probes, int has_ratio,
+                           double ratio, int has_max, int max_distance, const int32_t** rows,
+                           std::vector<unsigned long long>& offsets) {
+    const size_t count = table.size();
     if (int rc = ctx->filt_pairs.reserve(sizeof(FilterPair) * count)) return rc;
     if (int rc = ctx->filt_rows.reserve(sizeof(int32_t) * 4 * std::max<unsigned long long>(probes, 1))) return rc;
     if (int rc = ctx->filt_out.reserve(sizeof(int32_t) * 4 * std::max<unsigned long long>(probes, 1))) return rc;
@@ -1602,6 +1614,29 @@ int clatch_match_brute_force(clatch_ctx* ctx, const uint8_t* probes, size_t Q,
     if (Q == 0) return CLATCH_OK;   // src/match.cpp:56
     if (!out) return invalid("clatch_match_brute_force: out is null");
     CLATCH_CUDA(cudaSetDevice(ctx->device));
+    const bool on_device = ctx->pairs_filter_on_device && bytes == 64 && ctx->match_variant >= 3;
+    {
+        // Cross-check between two sets of similar size (an image pair): both passes go out as ONE launch over two
+        // temporary resident sets — forward and reverse query tiles in one item table — and the filter pass runs on
+        // the device, so only the surviving rows come back (src/match.cpp:58-79).
+        const size_t tq = (Q + 127) / 128, tn = (N + 127) / 128;
+        if (on_device && cross_check && Q >= 1024 && N >= 1024 && std::max(tq, tn) <= 2 * std::min(tq, tn)) {
+            clatch_set *a = nullptr, *b = nullptr;
+            const bool self = gallery == probes && N == Q;
+            int rc = clatch_set_create(ctx, probes, Q, 0, &a);
+            if (!rc && !self) rc = clatch_set_create(ctx, gallery, N, 0, &b);
+            if (!rc) {
+                const clatch_set* sets[2] = {a, self ? a : b};
+                const int32_t pair[2] = {0, 1};
+                size_t offsets[2] = {0, 0};
+                rc = clatch_match_set_pairs(ctx, sets, 2, pair, 1, has_ratio, ratio, 1, has_max, max_distance, out, Q, offsets);
+                *count = rc ? 0 : offsets[1];
+            }
+            clatch_set_destroy(a);
+            clatch_set_destroy(b);
+            return rc;
+        }
+    }
     // Both sets go up once; forward and (optionally) reverse passes reuse them on the device.
     if (int rc = ctx->q.reserve(Q * bytes)) return rc;
     if (int rc = ctx->res.reserve(sizeof(int32_t) * (3 * Q + N))) return rc;
@@ -1623,6 +1658,17 @@ int clatch_match_brute_force(clatch_ctx* ctx, const uint8_t* probes, size_t Q,
         if (int rc = launch_match_top2(ctx, d_gallery, N, ctx->q.as<uint8_t>(), Q, bytes, r + 3 * Q, nullptr,
                                        nullptr, st))
             return rc;
+    }
+    if (on_device && (has_ratio || has_max || cross_check) && Q >= 4096) {
+        // some rows will be dropped: decide on the device and bring back the survivors only
+        std::vector<FilterPair> table(1);
+        table[0] = {r, r + Q, r + 2 * Q, cross_check ? r + 3 * Q : nullptr, static_cast<unsigned>(Q), 0, 0ull};
+        const int32_t* rows = nullptr;
+        std::vector<unsigned long long> off;
+        if (int rc = filter_table_on_device(ctx, table, Q, has_ratio, ratio, has_max, max_distance, &rows, off)) return rc;
+        std::memcpy(out, rows, sizeof(int32_t) * 4 * off[1]);
+        *count = off[1];
+        return CLATCH_OK;
     }
     CLATCH_CUDA(cudaMemcpyAsync(host, r, sizeof(int32_t) * host_count, cudaMemcpyDeviceToHost, st));
     CLATCH_CUDA(cudaStreamSynchronize(st));

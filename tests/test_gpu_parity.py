@@ -1056,3 +1056,34 @@ def test_tensor_matcher_extreme_distances(lk, port):
     assert np.array_equal(rows, port.match(query, train, ratio=0.9, cross_check=True))
     rows = eng.match_sets(sets[0], sets[1], max_distance=40)
     assert np.array_equal(rows, port.match(query, train, max_distance=40))
+
+
+@pytest.mark.parametrize("q,n", [(5000, 6000), (5000, 300), (4096, 40000), (1500, 1200)])
+def test_single_pair_match_filters_on_the_device(lk, port, q, n):
+    """match() between two sets big enough for the device-side filter pass: cross-check between sets of
+    similar size runs both passes as one launch over temporary resident sets, anything else keeps the two
+    launches and filters the result block on the device. Rows must be the reference's in every combination,
+    including planted duplicates (ties on both passes) and with the host filter."""
+    d = port.random_descriptors(4200 + q, q + n, 64)
+    probes, gallery = d[:q].copy(), d[q:].copy()
+    rng = np.random.default_rng(q + n)
+    rows = rng.choice(q, min(q, n) // 4, replace=False)
+    gallery[rng.choice(n, len(rows), replace=False)] = probes[rows]       # true matches ...
+    for r in rows[:len(rows) // 2]:                                        # ... half of them a few bits off
+        for b in rng.integers(0, 512, 5):
+            probes[r, b >> 3] ^= np.uint8(1 << (b & 7))
+    gallery[n - 1] = gallery[0]
+    probes[q - 1] = probes[1]
+    eng = lk.get_engine()
+    combos = ({"ratio": 0.8}, {"cross_check": True}, {"max_distance": 200}, {"ratio": 0.8, "cross_check": True},
+              {"ratio": 0.9, "cross_check": True, "max_distance": 240})
+    want = [port.match(probes, gallery, **kw) for kw in combos]
+    assert all(len(w) > 0 for w in want)
+    try:
+        for on_device in (1, 0):
+            eng.set_option("pairs_filter_on_device", on_device)
+            for kw, w in zip(combos, want):
+                assert np.array_equal(lk.match(probes, gallery, **kw), w), (on_device, kw)
+    finally:
+        eng.set_option("pairs_filter_on_device", 1)
+    assert np.array_equal(lk.match(probes, probes, cross_check=True), port.match(probes, probes, cross_check=True))
