@@ -22,17 +22,21 @@
 #pragma once
 
 #include <algorithm>
+#include <cctype>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <fstream>
+#include <memory>
 #include <mutex>
 #include <optional>
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -170,6 +174,19 @@ inline Context& context() {
     }
     return c;
 }
+
+// One context per entry of a device list (the same device may appear more than once: each entry gets its
+// own context, stream and scratch). Used by the sharded helpers at the end of this header, which run one
+// host thread per entry — the C++ counterpart of paper_1609_03986_b200/sharded.py's one process per GPU.
+struct ContextPool {
+    std::vector<std::unique_ptr<Context>> slots;
+    explicit ContextPool(const std::vector<int>& devices) {
+        for (int d : devices) {
+            slots.emplace_back(new Context);
+            check(clatch_ctx_create(d, &slots.back()->ctx));
+        }
+    }
+};
 
 // Installs `pattern` unless the very same table is already on the device.
 inline void use_pattern(Context& c, const TripletPattern& pattern) {
@@ -478,6 +495,239 @@ inline std::vector<MatchPair> match_brute_force(const std::vector<Descriptor>& p
     std::vector<MatchPair> out(count);
     for (std::size_t i = 0; i < count; ++i)
         out[i] = {rows[4 * i], rows[4 * i + 1], rows[4 * i + 2], rows[4 * i + 3]};
+    return out;
+}
+
+// ---- text / image files around the path (src/image.cpp:52-78, src/detect.cpp:158-185, src/match.cpp:83-92) ----
+// Host-side restatements of the reference's file formats so that a `latch detect | describe | match` pipeline can
+// run on this library with the same files (tools: paper_1609_03986_b200/csrc/latch_cli.cpp).
+namespace b200 {
+inline std::string read_file(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) raise(ErrorCode::Malformed, "cannot open '" + path + "'");
+    std::ostringstream buf;
+    buf << f.rdbuf();
+    return buf.str();
+}
+inline void write_file(const std::string& path, const std::string& bytes) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) raise(ErrorCode::Malformed, "cannot open '" + path + "' for writing");
+    f.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
+    if (!f) raise(ErrorCode::Malformed, "write failed for '" + path + "'");
+}
+// One header token of a binary PGM: whitespace and '#' comments (to end of line) are skipped first.
+inline std::string pgm_token(const std::string& b, std::size_t& pos) {
+    for (;;) {
+        while (pos < b.size() && std::isspace(static_cast<unsigned char>(b[pos]))) ++pos;
+        if (pos < b.size() && b[pos] == '#') {
+            while (pos < b.size() && b[pos] != '\n') ++pos;
+            continue;
+        }
+        break;
+    }
+    const std::size_t start = pos;
+    while (pos < b.size() && !std::isspace(static_cast<unsigned char>(b[pos])) && b[pos] != '#') ++pos;
+    return b.substr(start, pos - start);
+}
+inline int pgm_number(const std::string& tok, const char* what) {
+    if (tok.empty()) raise(ErrorCode::Malformed, std::string("missing ") + what);
+    for (char ch : tok)
+        if (!std::isdigit(static_cast<unsigned char>(ch)))
+            raise(ErrorCode::Malformed, std::string("non-numeric ") + what + " '" + tok + "'");
+    if (tok.size() > 9) raise(ErrorCode::Malformed, std::string("unparsable ") + what + " '" + tok + "'");
+    return std::atoi(tok.c_str());
+}
+} // namespace b200
+
+/// Binary PGM (P5, maxval <= 255) -> Image with integer-valued pixels (src/image.cpp:52-78).
+inline Image load_pgm(const std::string& bytes) {
+    std::size_t pos = 0;
+    const std::string magic = b200::pgm_token(bytes, pos);
+    if (magic != "P5") raise(ErrorCode::NotPGM, "expected magic 'P5', got '" + magic + "'");
+    const int w = b200::pgm_number(b200::pgm_token(bytes, pos), "width");
+    const int h = b200::pgm_number(b200::pgm_token(bytes, pos), "height");
+    const int maxval = b200::pgm_number(b200::pgm_token(bytes, pos), "maxval");
+    if (w < 1 || h < 1) raise(ErrorCode::Malformed, "non-positive dimensions");
+    if (maxval < 1) raise(ErrorCode::Malformed, "maxval must be >= 1");
+    if (maxval > 255) raise(ErrorCode::UnsupportedDepth, "maxval > 255 not supported");
+    if (pos >= bytes.size() || !std::isspace(static_cast<unsigned char>(bytes[pos])))
+        raise(ErrorCode::Malformed, "missing separator before payload");
+    ++pos;   // exactly one whitespace byte before the pixels
+    const std::size_t count = static_cast<std::size_t>(w) * h;
+    if (bytes.size() - pos < count)
+        raise(ErrorCode::Truncated, "payload has " + std::to_string(bytes.size() - pos) + " bytes, need " +
+                                        std::to_string(count));
+    Image image(w, h);
+    for (std::size_t i = 0; i < count; ++i) image.data[i] = static_cast<unsigned char>(bytes[pos + i]);
+    return image;
+}
+inline Image load_pgm_file(const std::string& path) { return load_pgm(b200::read_file(path)); }
+
+/// Keypoint TSV: header line "x\ty\ttheta\tscore", then one "%.9g" row per keypoint (src/detect.cpp:158-185).
+inline std::string format_keypoints(const std::vector<Keypoint>& keypoints) {
+    std::string out = "x\ty\ttheta\tscore\n";
+    char line[128];
+    for (const Keypoint& k : keypoints) {
+        std::snprintf(line, sizeof(line), "%.9g\t%.9g\t%.9g\t%.9g\n", k.x, k.y, k.theta, k.score);
+        out += line;
+    }
+    return out;
+}
+inline std::vector<Keypoint> parse_keypoints(const std::string& text) {
+    std::vector<Keypoint> out;
+    std::istringstream in(text);
+    std::string line;
+    for (bool header = true; std::getline(in, line); header = false) {
+        if (header || line.empty()) continue;
+        Keypoint k;
+        if (std::sscanf(line.c_str(), "%lf\t%lf\t%lf\t%lf", &k.x, &k.y, &k.theta, &k.score) != 4)
+            raise(ErrorCode::Malformed, "bad keypoint line '" + line + "'");
+        out.push_back(k);
+    }
+    return out;
+}
+inline void save_keypoints_file(const std::vector<Keypoint>& k, const std::string& path) { b200::write_file(path, format_keypoints(k)); }
+inline std::vector<Keypoint> load_keypoints_file(const std::string& path) { return parse_keypoints(b200::read_file(path)); }
+
+/// Match TSV: "probe\tgallery\tdistance\tsecond_distance" rows, no header (src/match.cpp:83-92).
+inline std::string format_matches(const std::vector<MatchPair>& matches) {
+    std::string out;
+    char line[96];
+    for (const MatchPair& m : matches) {
+        std::snprintf(line, sizeof(line), "%d\t%d\t%d\t%d\n", m.probe_index, m.gallery_index, m.distance, m.second_distance);
+        out += line;
+    }
+    return out;
+}
+inline void save_matches_file(const std::vector<MatchPair>& m, const std::string& path) { b200::write_file(path, format_matches(m)); }
+
+// ---- sharding over several GPUs from C++ (the reference fans out over std::thread, src/parallel.hpp:17-38) ----
+// One host thread and one context per entry of `devices`; units are dealt round-robin exactly as
+// paper_1609_03986_b200/sharded.py deals them across processes (image i -> entry i mod D; pair k of the row-major
+// (i < j) list -> entry k mod D), no data-path collective. Results do not depend on the device list.
+namespace b200 {
+template <class Fn>
+inline void run_sharded(const std::vector<int>& devices, Fn&& per_slot) {
+    if (devices.empty()) throw std::invalid_argument("device list is empty");
+    ContextPool pool(devices);
+    std::vector<std::thread> threads;
+    std::vector<std::exception_ptr> errors(devices.size());
+    for (std::size_t d = 0; d < devices.size(); ++d)
+        threads.emplace_back([&, d] {
+            try {
+                per_slot(*pool.slots[d], d, devices.size());
+            } catch (...) {
+                errors[d] = std::current_exception();
+            }
+        });
+    for (std::thread& t : threads) t.join();
+    for (const std::exception_ptr& e : errors)
+        if (e) std::rethrow_exception(e);
+}
+} // namespace b200
+
+/// describe_all over many images, images dealt across `devices` (cfg3's partition). out[i] == describe_all(images[i], ...).
+inline std::vector<std::vector<std::pair<Keypoint, Descriptor>>> describe_all_images(
+    const std::vector<Image>& images, const std::vector<std::vector<Keypoint>>& keypoints, const TripletPattern& pattern,
+    const std::vector<int>& devices = {0}, int workers = 0) {
+    if (images.size() != keypoints.size()) throw std::invalid_argument("one keypoint list per image");
+    std::vector<std::vector<std::pair<Keypoint, Descriptor>>> out(images.size());
+    const std::size_t bytes = static_cast<std::size_t>(pattern.bit_count) / 8;
+    b200::run_sharded(devices, [&](b200::Context& c, std::size_t slot, std::size_t slots) {
+        b200::use_pattern(c, pattern);
+        std::vector<const double*> img, kps;
+        std::vector<int> w, h;
+        std::vector<std::size_t> pitch, count, m;
+        std::vector<std::vector<std::int64_t>> kept;
+        std::vector<std::vector<std::uint8_t>> flat;
+        std::vector<std::int64_t*> kept_p;
+        std::vector<std::uint8_t*> flat_p;
+        std::vector<std::size_t> mine;
+        for (std::size_t i = slot; i < images.size(); i += slots) mine.push_back(i);
+        if (mine.empty()) return;
+        for (std::size_t i : mine) {
+            img.push_back(images[i].data.data());
+            w.push_back(images[i].width);
+            h.push_back(images[i].height);
+            pitch.push_back(static_cast<std::size_t>(images[i].width));
+            kps.push_back(reinterpret_cast<const double*>(keypoints[i].data()));
+            count.push_back(keypoints[i].size());
+            kept.emplace_back(keypoints[i].size());
+            flat.emplace_back(keypoints[i].size() * bytes);
+        }
+        for (std::size_t k = 0; k < mine.size(); ++k) {
+            kept_p.push_back(kept[k].data());
+            flat_p.push_back(flat[k].data());
+        }
+        m.assign(mine.size(), 0);
+        b200::check(clatch_describe_batch_f64(c.ctx, img.data(), w.data(), h.data(), pitch.data(), kps.data(), count.data(), 4,
+                                              mine.size(), workers, kept_p.data(), flat_p.data(), m.data()));
+        for (std::size_t k = 0; k < mine.size(); ++k) {
+            auto& rec = out[mine[k]];
+            rec.resize(m[k]);
+            for (std::size_t j = 0; j < m[k]; ++j) {
+                rec[j].first = keypoints[mine[k]][static_cast<std::size_t>(kept[k][j])];
+                rec[j].second.bytes.assign(flat[k].begin() + static_cast<std::ptrdiff_t>(j * bytes),
+                                           flat[k].begin() + static_cast<std::ptrdiff_t>((j + 1) * bytes));
+            }
+        }
+    });
+    return out;
+}
+
+/// match_brute_force over every (i < j) pair of descriptor sets (cfg5's partition), pairs dealt across `devices`;
+/// each entry uploads the sets its pairs touch once and runs them as resident sets. Returned in row-major pair order:
+/// result[k] is the pair (i, j) at position k of {(0,1), (0,2), ..., (n-2,n-1)} and equals
+/// match_brute_force(sets[i], sets[j], options). 64-byte descriptors.
+inline std::vector<std::vector<MatchPair>> match_all_pairs(const std::vector<std::vector<Descriptor>>& sets,
+                                                           const MatchOptions& options = {},
+                                                           const std::vector<int>& devices = {0}) {
+    std::vector<std::pair<int, int>> pairs;
+    for (std::size_t i = 0; i < sets.size(); ++i)
+        for (std::size_t j = i + 1; j < sets.size(); ++j) pairs.emplace_back(static_cast<int>(i), static_cast<int>(j));
+    for (const auto& set : sets)
+        if (set.empty()) raise(ErrorCode::EmptyGallery, "matching needs nonempty descriptor sets");
+    std::vector<std::vector<MatchPair>> out(pairs.size());
+    b200::run_sharded(devices, [&](b200::Context& c, std::size_t slot, std::size_t slots) {
+        std::vector<std::size_t> mine;
+        for (std::size_t k = slot; k < pairs.size(); k += slots) mine.push_back(k);
+        if (mine.empty()) return;
+        std::vector<int> local(sets.size(), -1);
+        std::vector<clatch_set*> handles;
+        struct Guard {
+            std::vector<clatch_set*>& h;
+            ~Guard() { for (clatch_set* s : h) clatch_set_destroy(s); }
+        } guard{handles};
+        std::vector<std::int32_t> idx;
+        std::size_t cap = 0;
+        for (std::size_t k : mine) {
+            for (int side : {pairs[k].first, pairs[k].second})
+                if (local[static_cast<std::size_t>(side)] < 0) {
+                    const std::vector<std::uint8_t> flat = b200::flatten(sets[static_cast<std::size_t>(side)], 64);
+                    clatch_set* s = nullptr;
+                    b200::check(clatch_set_create(c.ctx, flat.data(), sets[static_cast<std::size_t>(side)].size(), 0, &s));
+                    local[static_cast<std::size_t>(side)] = static_cast<int>(handles.size());
+                    handles.push_back(s);
+                }
+            idx.push_back(local[static_cast<std::size_t>(pairs[k].first)]);
+            idx.push_back(local[static_cast<std::size_t>(pairs[k].second)]);
+            cap += sets[static_cast<std::size_t>(pairs[k].first)].size();
+        }
+        std::vector<std::int32_t> rows(std::max<std::size_t>(cap, 1) * 4);
+        std::vector<std::size_t> offsets(mine.size() + 1, 0);
+        b200::check(clatch_match_set_pairs(c.ctx, handles.data(), handles.size(), idx.data(), mine.size(),
+                                           options.ratio.has_value(), options.ratio.value_or(0.0), options.cross_check,
+                                           options.max_distance.has_value(), options.max_distance.value_or(0), rows.data(),
+                                           cap, offsets.data()));
+        for (std::size_t q = 0; q < mine.size(); ++q) {
+            auto& dst = out[mine[q]];
+            dst.resize(offsets[q + 1] - offsets[q]);
+            for (std::size_t r = 0; r < dst.size(); ++r) {
+                const std::int32_t* row = rows.data() + 4 * (offsets[q] + r);
+                dst[r] = {row[0], row[1], row[2], row[3]};
+            }
+        }
+    });
     return out;
 }
 

@@ -323,6 +323,80 @@ int main(int argc, char** argv) {
         }
     }
 
+    // ---- sharding from C++ (latch_b200.hpp: one host thread + context per device-list entry) ----
+    //      describe_all_images / match_all_pairs must equal the per-call API whatever the device list;
+    //      {0, 0} runs two contexts on this box's one GPU concurrently.
+    {
+        std::vector<Image> images;
+        std::vector<std::vector<Keypoint>> kps;
+        for (int i = 0; i < 5; ++i) {
+            images.push_back(make_image(i % 2 == 0, 300 + i, 200 + 16 * i, 180));
+            std::vector<double> k(4 * 120);
+            oracle_random_keypoints(400 + i, images.back().width, 180, 120, k.data());
+            std::vector<Keypoint> list;
+            for (int j = 0; j < 120; ++j) list.push_back({k[4 * j], k[4 * j + 1], k[4 * j + 2], 0.0});
+            list[7].x = 3.0;   // a margin violator
+            kps.push_back(list);
+        }
+        std::vector<std::vector<std::pair<Keypoint, Descriptor>>> want;
+        for (int i = 0; i < 5; ++i) want.push_back(latch::describe_all(images[i], kps[i], pattern));
+        for (const std::vector<int>& devices : {std::vector<int>{0}, std::vector<int>{0, 0}, std::vector<int>{0, 0, 0}}) {
+            const auto got = latch::describe_all_images(images, kps, pattern, devices);
+            CHECK(got.size() == 5);
+            for (int i = 0; i < 5 && got.size() == 5; ++i) {
+                CHECK(got[i].size() == want[i].size() && got[i].size() == 119);
+                bool same_desc = got[i].size() == want[i].size();
+                for (size_t j = 0; same_desc && j < got[i].size(); ++j)
+                    same_desc = got[i][j].second == want[i][j].second && got[i][j].first.x == want[i][j].first.x;
+                CHECK(same_desc);
+            }
+            std::vector<std::vector<Descriptor>> sets;
+            for (const auto& rec : got) {
+                sets.emplace_back();
+                for (const auto& r : rec) sets.back().push_back(r.second);
+            }
+            sets[3][5] = sets[0][9];        // cross-image duplicates -> real matches and ties
+            sets[3][6] = sets[0][9];
+            sets[1][2] = sets[0][9];
+            latch::MatchOptions opt;
+            opt.ratio = 0.95;
+            opt.cross_check = true;
+            const auto all = latch::match_all_pairs(sets, opt, devices);
+            CHECK(all.size() == 10);
+            size_t k = 0, rows = 0;
+            for (size_t i = 0; i < sets.size(); ++i)
+                for (size_t j = i + 1; j < sets.size(); ++j, ++k) {
+                    const auto one = latch::match_brute_force(sets[i], sets[j], opt);
+                    bool eq = k < all.size() && all[k].size() == one.size();
+                    for (size_t r = 0; eq && r < one.size(); ++r)
+                        eq = all[k][r].probe_index == one[r].probe_index && all[k][r].gallery_index == one[r].gallery_index &&
+                             all[k][r].distance == one[r].distance && all[k][r].second_distance == one[r].second_distance;
+                    CHECK(eq);
+                    rows += one.size();
+                }
+            CHECK(rows > 0);
+        }
+        CHECK(latch::describe_all_images({}, {}, pattern).empty());
+        CHECK(latch::match_all_pairs({}, {}).empty());
+    }
+
+    // ---- the file formats around the path: PGM in, keypoint TSV both ways, match TSV out ----
+    {
+        const latch::Image golden = latch::load_pgm_file(root + "/tests/golden/golden_image.pgm");
+        CHECK(golden.width == 256 && golden.height == 256);
+        CHECK(latch::load_pgm("P5\n# a comment\n2 1\n255\n\x07\xff").data == (std::vector<double>{7.0, 255.0}));
+        CHECK_THROWS_CODE(latch::load_pgm("P2\n2 1\n255\n12"), ErrorCode::NotPGM);
+        CHECK_THROWS_CODE(latch::load_pgm("P5\n2 2\n255\nabc"), ErrorCode::Truncated);
+        CHECK_THROWS_CODE(latch::load_pgm("P5\n2 2\n65535\nabcdefgh"), ErrorCode::UnsupportedDepth);
+        const std::vector<Keypoint> kp = {{10.5, 20.25, -0.5, 33.0}, {1e-3, 123456.789, 3.14159265358979, 0.0}};
+        const std::string text = latch::format_keypoints(kp);
+        CHECK(text.rfind("x\ty\ttheta\tscore\n", 0) == 0);
+        const auto back = latch::parse_keypoints(text);
+        CHECK(back.size() == 2 && back[0].x == 10.5 && back[0].theta == -0.5 && latch::format_keypoints(back) == text);
+        CHECK_THROWS_CODE(latch::parse_keypoints("x\ty\ttheta\tscore\n1\t2\tthree\t4\n"), ErrorCode::Malformed);
+        CHECK(latch::format_matches({{0, 5, 12, 40}, {3, 1, 0, 513}}) == "0\t5\t12\t40\n3\t1\t0\t513\n");
+    }
+
     std::printf("%s: %d checks, %d failures\n", g_failures ? "FAILED" : "PASSED", g_checks, g_failures);
     return g_failures ? 1 : 0;
 }
