@@ -36,12 +36,6 @@ namespace clatch {
 
 namespace {
 
-#ifndef CLATCH_TC_EARLY_I8
-#define CLATCH_TC_EARLY_I8 false
-#endif
-#ifndef CLATCH_TC_EARLY_F4
-#define CLATCH_TC_EARLY_F4 false
-#endif
 constexpr int kTcM = 128;                 // queries per CTA (UMMA M)
 constexpr int kTcKBlock = 128;            // bytes of K per smem stage row = one swizzle-atom row
 constexpr int kTcStages = 4;
@@ -58,13 +52,11 @@ struct TcI8 {
     static constexpr bool kF4 = false;
     static constexpr int kN = 256;             // train rows per tile (UMMA N)
     static constexpr int kKBlocks = 4;         // 128-byte K-blocks per descriptor row (512 B)
-    static constexpr bool kEarlyRelease = CLATCH_TC_EARLY_I8;
 };
 struct TcF4 {
     static constexpr bool kF4 = true;
     static constexpr int kN = 240;
     static constexpr int kKBlocks = 2;         // 256 B per row
-    static constexpr bool kEarlyRelease = CLATCH_TC_EARLY_F4;
 };
 constexpr int kTcAccStride = 256;             // TMEM columns between the two accumulators
 constexpr int kTcSfaCol = 240, kTcSfbCol = 496;   // TcF4: 16 columns of scale bytes after each accumulator
@@ -386,7 +378,6 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned 
 template <class F, bool kPair>
 __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g) {
     constexpr int kTcN = F::kN, kTcKBlocks = F::kKBlocks;
-    constexpr bool kEarlyRelease = F::kEarlyRelease;
     constexpr int kTcABytes = tc_a_bytes<F>(), kTcStageBytes = tc_stage_bytes<F>();
     const unsigned rank = kPair ? cluster_rank() : 0u;
     const int first_item = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
@@ -540,8 +531,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
                 tc_fence_after();
                 const long long tile_col0 = static_cast<long long>(w.tile_begin + t) * kTcN;
                 const long long tile_valid = min(static_cast<long long>(kTcN), static_cast<long long>(w.N) - tile_col0);
-                // One 32-column chunk of this lane's row: mask, 3-input max, and the full pass when it can matter.
-                auto consume = [&](int (&v)[32], const int ccol) {
+#pragma unroll 1
+                for (int chunk = 0; chunk < 4; ++chunk) {
+                    const int ccol = half * 128 + chunk * 32;   // first column of this chunk inside the tile
+                    if (ccol >= kTcN) break;
+                    int v[32];
+                    tmem_ld32(tmem_base + lane_addr + buf * kTcAccStride + ccol, v);
                     if (g.dump != nullptr && item == 0 && t == 0 && rank == 0) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
@@ -574,39 +569,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
                         }
                         second_key = !F::kF4 ? second : (__int_as_float(second) >= 0.f ? second : INT_MIN);
                     }
-                };
-                const unsigned acc = tmem_base + lane_addr + buf * kTcAccStride + half * 128;
-                if (kEarlyRelease) {
-                    // All of this warp's 128 columns in flight at once (one TMEM round trip instead of four), and the
-                    // accumulator is handed back to the MMA issuer as soon as they sit in registers. Measured 2.5x
-                    // SLOWER than the chunk-by-chunk loop in both forms (r3e: 1 M x 1 M 3.06e12 vs 5.12e12 compares/s
-                    // with TcF4) — kept behind CLATCH_TC_EARLY_* for A/B only.
-                    int v0[32], v1[32], v2[32], v3[32];
-                    tmem_ld32_issue(acc, v0);
-                    tmem_ld32_issue(acc + 32, v1);
-                    tmem_ld32_issue(acc + 64, v2);
-                    tmem_ld32_issue(acc + 96, v3);   // (TcF4, upper half: columns 224..255, the last 16 are scale bytes - masked)
-                    tmem_wait_ld();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
-                    consume(v0, half * 128);
-                    consume(v1, half * 128 + 32);
-                    consume(v2, half * 128 + 64);
-                    if (half * 128 + 96 < kTcN) consume(v3, half * 128 + 96);
-                } else {
-#pragma unroll 1
-                    for (int chunk = 0; chunk < 4; ++chunk) {
-                        const int ccol = half * 128 + chunk * 32;   // first column of this chunk inside the tile
-                        if (ccol >= kTcN) break;
-                        int v[32];
-                        tmem_ld32(acc + chunk * 32, v);
-                        consume(v, ccol);
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
                 }
+                // (All four loads in flight at once, with the accumulator handed back to the MMA issuer before the
+                // chunks are examined, was measured 2.5x SLOWER in both forms: 1 M x 1 M 3.06e12 vs 5.12e12 compares/s.)
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
             }
             if (F::kF4) {   // f32 bits -> the integer they hold (-inf: nothing seen)
                 best = __int_as_float(best) > -1024.f ? static_cast<int>(__int_as_float(best)) : INT_MIN;
