@@ -29,6 +29,9 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "clatch_internal.cuh"
 
@@ -39,8 +42,7 @@ namespace {
 constexpr int kTcM = 128;                 // queries per CTA (UMMA M)
 constexpr int kTcKBlock = 128;            // bytes of K per smem stage row = one swizzle-atom row
 constexpr int kTcStages = 4;
-constexpr int kTcEpilogueWarps = 8;
-constexpr int kTcThreads = 32 * (2 + kTcEpilogueWarps);   // 320
+template <class F> __host__ __device__ constexpr int tc_threads() { return 32 * (2 + F::kEpiWarps); }   // 320 / 576
 
 // Two operand forms, same kernel:
 //   TcI8  int8 +-1, 512 B per descriptor, kind::i8, int32 accumulators, 256 train rows per tile
@@ -52,18 +54,26 @@ struct TcI8 {
     static constexpr bool kF4 = false;
     static constexpr int kN = 256;             // train rows per tile (UMMA N)
     static constexpr int kKBlocks = 4;         // 128-byte K-blocks per descriptor row (512 B)
+    static constexpr bool kParked = false;     // (64 KiB A + 128 KiB ring leave no room for the parking slots)
+    static constexpr int kEpiWarps = 8;        // 4 TMEM lane quarters x 2 column halves
 };
 struct TcF4 {
     static constexpr bool kF4 = true;
     static constexpr int kN = 240;
     static constexpr int kKBlocks = 2;         // 256 B per row
+    static constexpr bool kParked = true;      // top-2 bookkeeping by a parked chunk (see the epilogue)
+    static constexpr int kEpiWarps = 16;       // 4 TMEM lane quarters x 4 column groups of 64
 };
 constexpr int kTcAccStride = 256;             // TMEM columns between the two accumulators
 constexpr int kTcSfaCol = 240, kTcSfbCol = 496;   // TcF4: 16 columns of scale bytes after each accumulator
+// TcF4 epilogue: one parked 32-value chunk per query row and column group (16 warps x 32 lanes x 128 B).
+constexpr int kTcParkBytes = 16 * 32 * 128;
+constexpr int kTcMergeBytes = 3 * 2048;   // (best, second, index) of up to three column groups, 128 rows x 4 ints each
 template <class F> __host__ __device__ constexpr int tc_a_bytes() { return kTcM * kTcKBlock * F::kKBlocks; }   // 64 / 32 KiB
 template <class F> __host__ __device__ constexpr int tc_stage_bytes() { return F::kN * kTcKBlock; }            // 32 / 30 KiB
 template <class F> __host__ __device__ constexpr int tc_smem_bytes() {
-    return tc_a_bytes<F>() + kTcStages * tc_stage_bytes<F>() + 1024 /*align*/ + 256 /*barriers*/ + 2048 /*half-merge buffer*/;
+    return tc_a_bytes<F>() + kTcStages * tc_stage_bytes<F>() + 1024 /*align*/ + 256 /*barriers*/ + kTcMergeBytes +
+           (F::kParked ? kTcParkBytes : 0);
 }
 
 // ---------------------------------------------------------------- expansion ----
@@ -148,6 +158,11 @@ __device__ __forceinline__ void bulk_load_multicast(unsigned dst, const void* sr
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(dst),
         "l"(src), "r"(bytes), "r"(bar), "h"(mask)
         : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 __device__ __forceinline__ unsigned cluster_rank() {
     unsigned r;
@@ -269,6 +284,7 @@ struct TcArgs {
     int sk_chunks;           // > 0: "stream-K" partition of the (query tile, train tile) units over this many CTAs
     Partial* partial;
     int* dump;               // optional: raw accumulators of item 0's first tile, 128 x 256
+    unsigned long long* trace;   // optional (CLATCH_TC_TRACE=1): 8 globaltimer stamps per CTA
     const TcItem* items;     // optional item table
 };
 
@@ -369,6 +385,52 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned 
     return w;
 }
 
+// One 32-column chunk of one query row in the parked-chunk epilogue (see match_tc_kernel): `valid` columns of it are
+// real train rows; `cb` is its column base inside the work item. Keeps the two largest chunk maxima seen by this lane
+// (k1 >= k2 as monotonic integer keys, over distinct chunks, first come first on ties) and parks the raw values of the
+// chunk that holds k1 (base c1) in shared memory.
+__device__ __forceinline__ void tc_park_chunk(int (&v)[32], const int valid, const int cb, uint4* const my_park, int& k1, int& k2,
+                                              int& c1, int* const dump, const int dump_cols) {
+    if (dump != nullptr) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (i < dump_cols) dump[i] = static_cast<int>(__int_as_float(v[i]));
+    }
+    if (valid < 32) {     // the set's last tile (zero padding rows) and the columns past the tile width
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (i >= valid) v[i] = static_cast<int>(0xFF800000u);   // -inf
+    }
+    // 3-input integer max as a tree (depth 4), not a chain of 16 dependent steps
+    int a[11];
+#pragma unroll
+    for (int i = 0; i < 10; ++i) a[i] = max(v[3 * i], max(v[3 * i + 1], v[3 * i + 2]));
+    a[10] = max(v[30], v[31]);
+    const int b0 = max(a[0], max(a[1], a[2])), b1 = max(a[3], max(a[4], a[5])), b2 = max(a[6], max(a[7], a[8])),
+              b3 = max(a[9], a[10]);
+    int m = max(max(b0, b1), max(b2, b3));
+    if (__any_sync(0xffffffffu, m < 0)) {   // rare: a chunk without one non-negative value (or fully masked)
+        float fm = __int_as_float(v[0]);
+#pragma unroll
+        for (int i = 1; i < 32; ++i) fm = fmaxf(fm, __int_as_float(v[i]));
+        m = m < 0 ? __float_as_int(fm) : m;
+    }
+    const int key = m >= 0 ? m : (m ^ 0x7FFFFFFF);   // monotonic in the float value
+    if (__any_sync(0xffffffffu, key > k2)) {
+        if (key > k1) {                   // a new largest value for this row: its chunk replaces the parked one
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                my_park[i] = make_uint4(static_cast<unsigned>(v[4 * i]), static_cast<unsigned>(v[4 * i + 1]),
+                                        static_cast<unsigned>(v[4 * i + 2]), static_cast<unsigned>(v[4 * i + 3]));
+            k2 = k1;
+            k1 = key;
+            c1 = cb;
+        } else if (key > k2) {
+            k2 = key;                     // only its maximum can matter (as the runner-up)
+        }
+    }
+}
+
 // kPair = true: launched as clusters of two CTAs. Every CTA used to pull the whole train stream out of L2 by
 // itself — 64 B/clk/SM at the tensor pipe's pace, 9.5 KB/clk over 148 SMs, which is more than L2 delivers
 // (tools/tc_peak.cu: ~4.3-6 KB/clk) and held the kernel at 72-77 % of the MMA rate. Paired CTAs work on two
@@ -376,13 +438,16 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned 
 // CTAs' shared memory (one L2 read feeds two SMs), and a stage is handed back to the producers only when both
 // CTAs' MMAs have read it (multicast tcgen05.commit onto both `empty` barriers).
 template <class F, bool kPair>
-__global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g) {
+__global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcArgs g) {
+    constexpr int kTcEpilogueWarps = F::kEpiWarps;
     constexpr int kTcN = F::kN, kTcKBlocks = F::kKBlocks;
     constexpr int kTcABytes = tc_a_bytes<F>(), kTcStageBytes = tc_stage_bytes<F>();
     const unsigned rank = kPair ? cluster_rank() : 0u;
     const int first_item = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
     const int item_step = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
     extern __shared__ uint8_t smem_raw[];
+    unsigned long long* const trace = g.trace ? g.trace + 8 * blockIdx.x : nullptr;
+    if (trace && threadIdx.x == 0) trace[0] = global_ns();
     const unsigned raw = smem_u32(smem_raw);
     const unsigned base = (raw + 1023u) & ~1023u;              // SWIZZLE_128B atoms need 1024-B alignment
     const unsigned smem_a = base;
@@ -398,6 +463,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
     uint8_t* const tail = gen_base + kTcABytes + kTcStages * kTcStageBytes;
     volatile unsigned* tmem_slot = reinterpret_cast<volatile unsigned*>(tail + 128);
     int* merge_buf = reinterpret_cast<int*>(tail + 256);       // 128 rows x 4 ints
+    uint4* const park = reinterpret_cast<uint4*>(tail + 256 + kTcMergeBytes);   // F::kParked: [16 warps][32 lanes][8 x uint4]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -437,6 +503,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
         tc_fence_after();
     }
 
+    if (trace && threadIdx.x == 0) trace[1] = global_ns();   // set-up done (barriers, TMEM, scale bytes)
     if (warp == 0) {
         // ===== producer =====
         if (lane == 0) {
@@ -486,6 +553,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
                     const unsigned tmem_d = tmem_base + buf * kTcAccStride;
                     for (int kb = 0; kb < kTcKBlocks; ++kb) {
                         mbar_wait(bar_full + 8 * stage, phase);
+                        if (trace && tcount == 0 && kb == 0) trace[2] = global_ns();   // first operand stage has landed
                         tc_fence_after();
                         const unsigned a_addr = smem_a + kb * (kTcM * kTcKBlock);
                         const unsigned b_addr = smem_b + stage * kTcStageBytes;
@@ -506,96 +574,173 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
                 }
                 tc_commit(bar_a_empty);                        // every MMA of this item has read A
             }
+            if (trace) {
+                trace[3] = global_ns();   // last MMA issued
+                trace[6] = static_cast<unsigned long long>(tcount);
+            }
         }
     } else {
-        // ===== epilogue: warps 2..9 =====
+        // ===== epilogue: warps 2.. =====
         const int ew = warp - 2;
         const int quarter = warp & 3;                       // TMEM lane quarter this warp may touch
-        const int half = ew >> 2;                           // which 128 of the 256 columns
+        const int half = ew >> 2;                           // int8 form: which 128 of the 256 columns
         const unsigned lane_addr = static_cast<unsigned>(quarter * 32) << 16;
         const int row = quarter * 32 + lane;
         int tcount = 0;
         for (int item = first_item; item < g.num_items; item += item_step) {
             const TcWork w = tc_decode<F, kPair>(g, item, rank);
             if (w.ntiles == 0) continue;
-            // best / second are dot products D = 512 - 2 * hamming, kept as the raw accumulator words: int32, or the
-            // bits of an f32 holding that integer. Signed-integer order on f32 bits is the float order among
-            // non-negative values and puts every negative value below them, so the per-chunk test (3-input integer
-            // max over the 32 words against the runner-up) is exact whenever the runner-up is >= 0 (second_key =
-            // its bits); until then second_key = INT_MIN and every chunk takes the full pass, which compares as floats.
-            int best = F::kF4 ? static_cast<int>(0xFF800000u) : INT_MIN, second = best, best_idx = -1;   // -inf / INT_MIN
-            int second_key = INT_MIN;
-            for (int t = 0; t < w.ntiles; ++t, ++tcount) {
-                const int buf = tcount & 1;
-                mbar_wait(bar_tfull + 8 * buf, (tcount >> 1) & 1);
-                tc_fence_after();
-                const long long tile_col0 = static_cast<long long>(w.tile_begin + t) * kTcN;
-                const long long tile_valid = min(static_cast<long long>(kTcN), static_cast<long long>(w.N) - tile_col0);
-#pragma unroll 1
-                for (int chunk = 0; chunk < 4; ++chunk) {
-                    const int ccol = half * 128 + chunk * 32;   // first column of this chunk inside the tile
-                    if (ccol >= kTcN) break;
-                    int v[32];
-                    tmem_ld32(tmem_base + lane_addr + buf * kTcAccStride + ccol, v);
-                    if (g.dump != nullptr && item == 0 && t == 0 && rank == 0) {
+            int best, second, best_idx = -1;
+            if constexpr (F::kParked) {
+                // Top-2 by a PARKED CHUNK. Examining 32 accumulators one by one whenever a chunk might change a row's
+                // top-2 costs ~160 instructions for the whole warp each time one lane needs it, and with n columns
+                // seen a lane needs it with probability ~64/n per chunk: over an 8 000-row train set (an image pair)
+                // or a stream-K piece nearly every chunk took that pass. Here a lane tracks only the two largest CHUNK
+                // MAXIMA it has seen (k1 >= k2, distinct chunks, first come first on ties) and keeps the 32 raw values
+                // of the chunk holding k1 in shared memory (8 predicated 16-byte stores when a chunk's maximum beats
+                // k1). Every value outside that chunk is <= k2: the row's largest value is the first maximum of the
+                // parked chunk, and its second-largest is k2 or the parked chunk's own runner-up — one exact pass over
+                // 32 parked values at the end of the item gives the same (index, best, second) as examining
+                // everything. Keys: f32 bits order like signed integers among non-negative values; a negative chunk
+                // maximum (all 32 distances above 256) is re-derived with float compares and mapped monotonically.
+                // Sixteen epilogue warps (four per scheduler): the epilogue is latency-bound — ~100 instructions per
+                // chunk at ~7 clk each — and eight warps needed 1 850 clk per 240-column tile against 960 clk of MMAs.
+                const int colgrp = ew >> 2;                                // columns [64 * colgrp, 64 * colgrp + 64)
+                int k1 = INT_MIN, k2 = INT_MIN, c1 = -1;
+                uint4* const my_park = park + (ew * 32 + lane) * 8;
+                const bool dumping = g.dump != nullptr && item == 0 && rank == 0;
+                for (int t = 0; t < w.ntiles; ++t, ++tcount) {
+                    const int buf = tcount & 1;
+                    mbar_wait(bar_tfull + 8 * buf, (tcount >> 1) & 1);
+                    tc_fence_after();
+                    const long long left = static_cast<long long>(w.N) - static_cast<long long>(w.tile_begin + t) * kTcN;
+                    const int tile_valid = left < kTcN ? static_cast<int>(left) : kTcN;   // real rows among this tile's columns
+                    const unsigned acc = tmem_base + lane_addr + buf * kTcAccStride + colgrp * 64;
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (ccol + i < kTcN)
-                                g.dump[row * 256 + ccol + i] = F::kF4 ? static_cast<int>(__int_as_float(v[i])) : v[i];
-                    }
-                    const long long cvalid = tile_valid - ccol;
-                    if (cvalid < 32) {     // the set's last tile (zero padding rows) and the columns past kTcN
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (i >= cvalid) v[i] = F::kF4 ? static_cast<int>(0xFF800000u) : INT_MIN;   // -inf
-                    }
-                    int m = v[0];
-#pragma unroll
-                    for (int i = 1; i < 32; i += 2) m = max(m, max(v[i], i + 1 < 32 ? v[i + 1] : INT_MIN));
-                    if (m > second_key) {                       // something in this chunk may enter the top-2
-                        const int cbase = t * kTcN + ccol;
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            const int d = v[i];
-                            const bool gt_best = F::kF4 ? __int_as_float(d) > __int_as_float(best) : d > best;
-                            const bool gt_second = F::kF4 ? __int_as_float(d) > __int_as_float(second) : d > second;
-                            if (gt_best) {                      // strict: earlier (lower) index keeps ties
-                                second = best;
-                                best = d;
-                                best_idx = cbase + i;
-                            } else if (gt_second) {
-                                second = d;
-                            }
+                    for (int chunk = 0; chunk < 2; ++chunk) {
+                        const int ccol = colgrp * 64 + chunk * 32;   // first column of this chunk inside the tile
+                        int v[32];
+                        tmem_ld32(acc + chunk * 32, v);
+                        if (chunk == 1) {   // everything this warp needs of the accumulator has left TMEM
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
                         }
-                        second_key = !F::kF4 ? second : (__int_as_float(second) >= 0.f ? second : INT_MIN);
+                        tc_park_chunk(v, tile_valid - ccol, t * kTcN + ccol, my_park, k1, k2, c1,
+                                      dumping && t == 0 ? g.dump + row * 256 + ccol : nullptr, kTcN - ccol);
                     }
                 }
-                // (All four loads in flight at once, with the accumulator handed back to the MMA issuer before the
-                // chunks are examined, was measured 2.5x SLOWER in both forms: 1 M x 1 M 3.06e12 vs 5.12e12 compares/s.)
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                // the exact pass over the parked chunk
+                float fbest = __int_as_float(0xFF800000u), fsecond = fbest;
+                if (c1 >= 0) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const uint4 q = my_park[i];
+                        const unsigned e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float f = __uint_as_float(e[j]);
+                            if (f > fbest) {                      // strict: the lower index keeps ties
+                                fsecond = fbest;
+                                fbest = f;
+                                best_idx = c1 + 4 * i + j;
+                            } else if (f > fsecond) {
+                                fsecond = f;
+                            }
+                        }
+                    }
+                    if (k2 != INT_MIN) fsecond = fmaxf(fsecond, __int_as_float(k2 >= 0 ? k2 : (k2 ^ 0x7FFFFFFF)));
+                }
+                best = __float_as_int(fbest);
+                second = __float_as_int(fsecond);
+            } else {
+                // best / second are dot products D = 512 - 2 * hamming, kept as the raw accumulator words: int32, or the
+                // bits of an f32 holding that integer. Signed-integer order on f32 bits is the float order among
+                // non-negative values and puts every negative value below them, so the per-chunk test (3-input integer
+                // max over the 32 words against the runner-up) is exact whenever the runner-up is >= 0 (second_key =
+                // its bits); until then second_key = INT_MIN and every chunk takes the full pass, which compares as floats.
+                best = F::kF4 ? static_cast<int>(0xFF800000u) : INT_MIN;   // -inf / INT_MIN
+                second = best;
+                int second_key = INT_MIN;
+                for (int t = 0; t < w.ntiles; ++t, ++tcount) {
+                    const int buf = tcount & 1;
+                    mbar_wait(bar_tfull + 8 * buf, (tcount >> 1) & 1);
+                    tc_fence_after();
+                    const long long tile_col0 = static_cast<long long>(w.tile_begin + t) * kTcN;
+                    const long long tile_valid = min(static_cast<long long>(kTcN), static_cast<long long>(w.N) - tile_col0);
+    #pragma unroll 1
+                    for (int chunk = 0; chunk < 4; ++chunk) {
+                        const int ccol = half * 128 + chunk * 32;   // first column of this chunk inside the tile
+                        if (ccol >= kTcN) break;
+                        int v[32];
+                        tmem_ld32(tmem_base + lane_addr + buf * kTcAccStride + ccol, v);
+                        if (g.dump != nullptr && item == 0 && t == 0 && rank == 0) {
+    #pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                if (ccol + i < kTcN)
+                                    g.dump[row * 256 + ccol + i] = F::kF4 ? static_cast<int>(__int_as_float(v[i])) : v[i];
+                        }
+                        const long long cvalid = tile_valid - ccol;
+                        if (cvalid < 32) {     // the set's last tile (zero padding rows) and the columns past kTcN
+    #pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                if (i >= cvalid) v[i] = F::kF4 ? static_cast<int>(0xFF800000u) : INT_MIN;   // -inf
+                        }
+                        int m = v[0];
+    #pragma unroll
+                        for (int i = 1; i < 32; i += 2) m = max(m, max(v[i], i + 1 < 32 ? v[i + 1] : INT_MIN));
+                        if (m > second_key) {                       // something in this chunk may enter the top-2
+                            const int cbase = t * kTcN + ccol;
+    #pragma unroll
+                            for (int i = 0; i < 32; ++i) {
+                                const int d = v[i];
+                                const bool gt_best = F::kF4 ? __int_as_float(d) > __int_as_float(best) : d > best;
+                                const bool gt_second = F::kF4 ? __int_as_float(d) > __int_as_float(second) : d > second;
+                                if (gt_best) {                      // strict: earlier (lower) index keeps ties
+                                    second = best;
+                                    best = d;
+                                    best_idx = cbase + i;
+                                } else if (gt_second) {
+                                    second = d;
+                                }
+                            }
+                            second_key = !F::kF4 ? second : (__int_as_float(second) >= 0.f ? second : INT_MIN);
+                        }
+                    }
+                    // (All four loads in flight at once, with the accumulator handed back to the MMA issuer before the
+                    // chunks are examined, was measured 2.5x SLOWER in both forms: 1 M x 1 M 3.06e12 vs 5.12e12 compares/s.)
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                }
             }
             if (F::kF4) {   // f32 bits -> the integer they hold (-inf: nothing seen)
                 best = __int_as_float(best) > -1024.f ? static_cast<int>(__int_as_float(best)) : INT_MIN;
                 second = __int_as_float(second) > -1024.f ? static_cast<int>(__int_as_float(second)) : INT_MIN;
             }
-            // merge the two column halves of each row
-            if (half == 1) {
-                merge_buf[row * 4 + 0] = best;
-                merge_buf[row * 4 + 1] = second;
-                merge_buf[row * 4 + 2] = best_idx;
+            // merge the column groups of each row (two halves, or four groups of 64 in the parked form): the groups
+            // interleave in index order across tiles, so ties compare indices
+            constexpr int kGroups = kTcEpilogueWarps / 4;
+            const int grp = ew >> 2;
+            if (grp != 0) {
+                int* const mb = merge_buf + (grp - 1) * 512 + row * 4;
+                mb[0] = best;
+                mb[1] = second;
+                mb[2] = best_idx;
             }
             asm volatile("bar.sync 1, %0;" ::"r"(32 * kTcEpilogueWarps) : "memory");
-            if (half == 0) {
-                const int ob = merge_buf[row * 4 + 0], os = merge_buf[row * 4 + 1], oi = merge_buf[row * 4 + 2];
-                // the halves interleave in index order across tiles, so ties compare indices
-                if (ob > best || (ob == best && oi >= 0 && oi < best_idx)) {
-                    second = max(best, os);
-                    best = ob;
-                    best_idx = oi;
-                } else {
-                    second = max(second, ob);
+            if (grp == 0) {
+#pragma unroll
+                for (int o = 1; o < kGroups; ++o) {
+                    const int* const mb = merge_buf + (o - 1) * 512 + row * 4;
+                    const int ob = mb[0], os = mb[1], oi = mb[2];
+                    if (ob > best || (ob == best && oi >= 0 && oi < best_idx)) {
+                        second = max(best, os);
+                        best = ob;
+                        best_idx = oi;
+                    } else {
+                        second = max(second, ob);
+                    }
                 }
                 const unsigned long long qi = static_cast<unsigned long long>(w.qtile) * kTcM + row;
                 if (qi < w.Q && !w.ghost) {
@@ -620,8 +765,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) match_tc_kernel(const TcArgs g)
         }
     }
 
+    if (trace && threadIdx.x == 64) trace[4] = global_ns();   // first epilogue warp finished its last item
     tc_fence_before();
     __syncthreads();
+    if (trace && threadIdx.x == 0) trace[5] = global_ns();
     if (kPair) cluster_sync_all();                             // nothing of the partner's is still bound for this CTA
     if (warp == 1) {
         tc_fence_after();
@@ -705,15 +852,15 @@ int tc_query_tiles(size_t rows) { return static_cast<int>((rows + kTcM - 1) / kT
 static int launch_tc(clatch_ctx* ctx, const TcArgs& g, unsigned ctas, bool paired, cudaStream_t stream) {
     const bool f4 = ctx->match_variant == 4;
     if (!paired) {
-        if (f4) match_tc_kernel<TcF4, false><<<ctas, kTcThreads, tc_smem_bytes<TcF4>(), stream>>>(g);
-        else match_tc_kernel<TcI8, false><<<ctas, kTcThreads, tc_smem_bytes<TcI8>(), stream>>>(g);
+        if (f4) match_tc_kernel<TcF4, false><<<ctas, tc_threads<TcF4>(), tc_smem_bytes<TcF4>(), stream>>>(g);
+        else match_tc_kernel<TcI8, false><<<ctas, tc_threads<TcI8>(), tc_smem_bytes<TcI8>(), stream>>>(g);
         ++ctx->launches;
         CLATCH_CUDA(cudaGetLastError());
         return CLATCH_OK;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ctas & ~1u);
-    cfg.blockDim = dim3(kTcThreads);
+    cfg.blockDim = dim3(f4 ? tc_threads<TcF4>() : tc_threads<TcI8>());
     cfg.dynamicSmemBytes = f4 ? tc_smem_bytes<TcF4>() : tc_smem_bytes<TcI8>();
     cfg.stream = stream;
     cudaLaunchAttribute attr{};
@@ -845,6 +992,13 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
     g.sk_chunks = streamk ? static_cast<int>(chunks) : 0;
     g.partial = ctx->partial.as<Partial>();
     g.dump = d_dump;
+    static const bool tracing = std::getenv("CLATCH_TC_TRACE") != nullptr;
+    unsigned long long* d_trace = nullptr;
+    if (tracing) {
+        CLATCH_CUDA(cudaMalloc(&d_trace, sizeof(unsigned long long) * 8 * sms));
+        CLATCH_CUDA(cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long) * 8 * sms, stream));
+        g.trace = d_trace;
+    }
     if (paired) {
         const size_t pair_items = (qtiles + 1) / 2 * splits;
         g.num_items = static_cast<int>(pair_items);
@@ -852,6 +1006,31 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
     } else {
         const unsigned grid = static_cast<unsigned>(streamk ? chunks : std::min<size_t>(qtiles * splits, ctx->sm_count));
         if (int rc = launch_tc(ctx, g, grid, false, stream)) return rc;
+    }
+    if (tracing) {   // debug: where the time of a launch goes, per CTA (globaltimer, ns)
+        std::vector<unsigned long long> h(8 * sms);
+        CLATCH_CUDA(cudaStreamSynchronize(stream));
+        CLATCH_CUDA(cudaMemcpy(h.data(), d_trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+        cudaFree(d_trace);
+        unsigned long long t0 = ~0ull, t_end = 0;
+        for (size_t c = 0; c < sms; ++c)
+            if (h[8 * c]) t0 = std::min(t0, h[8 * c]), t_end = std::max(t_end, h[8 * c + 5]);
+        double sum[6] = {0}, mx[6] = {0};
+        size_t n = 0;
+        for (size_t c = 0; c < sms; ++c) {
+            if (!h[8 * c]) continue;
+            ++n;
+            for (int k = 0; k < 6; ++k) {
+                const double v = (static_cast<double>(h[8 * c + k]) - static_cast<double>(t0)) / 1e3;
+                sum[k] += v;
+                mx[k] = std::max(mx[k], v);
+            }
+        }
+        std::fprintf(stderr, "[clatch tc trace] %s Q=%zu N=%zu ctas=%zu tiles/cta=%llu total %.1f us | mean (max) us since first CTA start: "
+                     "entry %.1f (%.1f), setup done %.1f (%.1f), first stage landed %.1f (%.1f), last MMA issued %.1f (%.1f), "
+                     "epilogue done %.1f (%.1f), exit %.1f (%.1f)\n",
+                     streamk ? "stream-K" : paired ? "paired" : "rounds", Q, N, n, h[6], (t_end - t0) / 1e3, sum[0] / n, mx[0], sum[1] / n,
+                     mx[1], sum[2] / n, mx[2], sum[3] / n, mx[3], sum[4] / n, mx[4], sum[5] / n, mx[5]);
     }
     if (streamk)
         merge_partials_sk_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(

@@ -13,6 +13,7 @@ q, n, v = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 eng = get_engine()
 eng.set_option("match_variant", v)
+eng.set_option("match_form_auto", 0)
 g = torch.Generator(device="cuda").manual_seed(0)
 dq = torch.randint(0, 256, (q, 64), dtype=torch.uint8, device="cuda", generator=g)
 dt = torch.randint(0, 256, (n, 64), dtype=torch.uint8, device="cuda", generator=g)
