@@ -89,8 +89,8 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * bytes over the bus; lossless, same descriptors). 0 (default) does so when the image lies in ordinary
  * pageable memory — which the driver could only copy through its own bounce buffers — and uploads the
  * doubles of a page-locked image as they are (classified on the device); 1 = always, 2 = never.
- * key "match_form_auto": 1 (default) lets match_variant 4 run mid-sized single matches (3e7 .. 6e8 compares) in
- * the int8 form, which is ~10 % faster there; 0 = always e2m1.
+ * key "match_form_auto": 1 lets match_variant 4 run mid-sized single matches (3e7 .. 6e8 compares) in the int8
+ * form (an A/B switch from before the e2m1 form's parked-chunk epilogue); 0 (default) = always e2m1.
  * key "match_pairs": 1 (default) runs the tensor-core matcher as clusters of two CTAs that share one stream of
  * train tiles through TMA multicast (half the L2 traffic per compare); 0 = every CTA streams for itself.
  * key "match_streamk": 1 (default) lets the tensor-core matcher split small problems (expanded train set

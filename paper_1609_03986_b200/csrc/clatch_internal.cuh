@@ -99,7 +99,7 @@ struct clatch_ctx {
     // tensor matcher: clusters of two CTAs share the train-set stream through TMA multicast (one L2 read feeds two
     // SMs) wherever two query tiles scan the same train tiles; set_option "match_pairs" 0 = every CTA on its own.
     bool match_pairs = true;
-    bool match_form_auto = true;   // match_variant 4: mid-sized single matches run the int8 form (set_option "match_form_auto")
+    bool match_form_auto = false;  // match_variant 4: 1 = mid-sized single matches run the int8 form (it was ahead there before the parked-chunk epilogue; kept for A/B)
     bool match_streamk = true;     // tensor matcher: equal-share partition for small problems (set_option "match_streamk")
     int match_variant = 4;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC, 3: tcgen05 int8 GEMM, 4: tcgen05 mxf4 (e2m1) GEMM (CLATCH_MATCH_VARIANT)
     // The scratch below is shared by every call on this context, whatever stream the call queues on

@@ -164,6 +164,18 @@ __device__ __forceinline__ unsigned long long global_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// One lane of a converged warp (the same one every time on current hardware).
+__device__ __forceinline__ bool elect_one() {
+    unsigned pred;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "selp.b32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ unsigned cluster_rank() {
     unsigned r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -285,6 +297,7 @@ struct TcArgs {
     Partial* partial;
     int* dump;               // optional: raw accumulators of item 0's first tile, 128 x 256
     unsigned long long* trace;   // optional (CLATCH_TC_TRACE=1): 8 globaltimer stamps per CTA
+    int debug;                   // CLATCH_TC_DEBUG bits (wrong results!): 1 = epilogue releases accumulators unread
     const TcItem* items;     // optional item table
 };
 
@@ -538,46 +551,52 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
         }
     } else if (warp == 1) {
         // ===== MMA issuer =====
-        if (lane == 0) {
-            int stage = 0, tcount = 0;
-            unsigned phase = 0, a_phase = 0;
-            for (int item = first_item; item < g.num_items; item += item_step) {
-                const TcWork w = tc_decode<F, kPair>(g, item, rank);
-                if (w.ntiles == 0) continue;
-                mbar_wait(bar_a_full, a_phase);
-                a_phase ^= 1;
-                for (int t = 0; t < w.ntiles; ++t, ++tcount) {
-                    const int buf = tcount & 1;
-                    mbar_wait(bar_tempty + 8 * buf, ((tcount >> 1) & 1) ^ 1);   // epilogue drained this accumulator
+        // The WHOLE warp walks the loop, converged, and one elected lane issues the tensor-core instructions: with
+        // warp-uniform control flow the descriptor arithmetic stays on the uniform datapath. Issued from a lone
+        // `lane == 0` thread every MMA cost ~20 instructions of register -> uniform-register shuffling, ~250 per tile,
+        // and at the ~7 clk per instruction a single warp gets next to four busy epilogue warps on its scheduler that
+        // chain (not the tensor pipe, not shared memory) set the tile time: 1 700 clk against 960 clk of MMAs.
+        int stage = 0, tcount = 0;
+        unsigned phase = 0, a_phase = 0;
+        const unsigned sfa = tmem_base + kTcSfaCol, sfb = tmem_base + kTcSfbCol;
+        for (int item = first_item; item < g.num_items; item += item_step) {
+            const TcWork w = tc_decode<F, kPair>(g, item, rank);
+            if (w.ntiles == 0) continue;
+            mbar_wait(bar_a_full, a_phase);
+            a_phase ^= 1;
+            for (int t = 0; t < w.ntiles; ++t, ++tcount) {
+                const int buf = tcount & 1;
+                mbar_wait(bar_tempty + 8 * buf, ((tcount >> 1) & 1) ^ 1);   // epilogue drained this accumulator
+                tc_fence_after();
+                const unsigned tmem_d = tmem_base + buf * kTcAccStride;
+#pragma unroll
+                for (int kb = 0; kb < kTcKBlocks; ++kb) {
+                    mbar_wait(bar_full + 8 * stage, phase);
+                    if (trace && tcount == 0 && kb == 0 && lane == 0) trace[2] = global_ns();   // first operand stage has landed
                     tc_fence_after();
-                    const unsigned tmem_d = tmem_base + buf * kTcAccStride;
-                    for (int kb = 0; kb < kTcKBlocks; ++kb) {
-                        mbar_wait(bar_full + 8 * stage, phase);
-                        if (trace && tcount == 0 && kb == 0) trace[2] = global_ns();   // first operand stage has landed
-                        tc_fence_after();
-                        const unsigned a_addr = smem_a + kb * (kTcM * kTcKBlock);
-                        const unsigned b_addr = smem_b + stage * kTcStageBytes;
+                    const uint64_t a_desc = umma_desc(smem_a + kb * (kTcM * kTcKBlock));
+                    const uint64_t b_desc = umma_desc(smem_b + stage * kTcStageBytes);
+                    if (elect_one()) {
 #pragma unroll
                         for (int k = 0; k < kTcKBlock / 32; ++k) {   // 32 bytes of K per instruction: 32 int8 or 64 e2m1
-                            if (F::kF4)
-                                tc_mma_f4(tmem_d, umma_desc(a_addr + 32 * k), umma_desc(b_addr + 32 * k), kIdescF4,
-                                          (kb | k) != 0, tmem_base + kTcSfaCol, tmem_base + kTcSfbCol);
-                            else
-                                tc_mma_i8(tmem_d, umma_desc(a_addr + 32 * k), umma_desc(b_addr + 32 * k), kIdescI8,
-                                          (kb | k) != 0);
+                            // (start address field counts 16-byte units: + 2 per 32 bytes of K)
+                            if (F::kF4) tc_mma_f4(tmem_d, a_desc + 2 * k, b_desc + 2 * k, kIdescF4, (kb | k) != 0, sfa, sfb);
+                            else tc_mma_i8(tmem_d, a_desc + 2 * k, b_desc + 2 * k, kIdescI8, (kb | k) != 0);
                         }
                         if (kPair) tc_commit_multicast(bar_empty + 8 * stage, 3);
                         else tc_commit(bar_empty + 8 * stage);  // stage reusable once these MMAs have read it
-                        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+                        if (kb == kTcKBlocks - 1) tc_commit(bar_tfull + 8 * buf);   // accumulator complete
                     }
-                    tc_commit(bar_tfull + 8 * buf);            // accumulator complete
+                    __syncwarp();
+                    if (++stage == kTcStages) { stage = 0; phase ^= 1; }
                 }
-                tc_commit(bar_a_empty);                        // every MMA of this item has read A
             }
-            if (trace) {
-                trace[3] = global_ns();   // last MMA issued
-                trace[6] = static_cast<unsigned long long>(tcount);
-            }
+            if (elect_one()) tc_commit(bar_a_empty);           // every MMA of this item has read A
+            __syncwarp();
+        }
+        if (trace && lane == 0) {
+            trace[3] = global_ns();   // last MMA issued
+            trace[6] = static_cast<unsigned long long>(tcount);
         }
     } else {
         // ===== epilogue: warps 2.. =====
@@ -616,6 +635,12 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
                     const long long left = static_cast<long long>(w.N) - static_cast<long long>(w.tile_begin + t) * kTcN;
                     const int tile_valid = left < kTcN ? static_cast<int>(left) : kTcN;   // real rows among this tile's columns
                     const unsigned acc = tmem_base + lane_addr + buf * kTcAccStride + colgrp * 64;
+                    if (g.debug & 1) {   // measurement only: how fast is everything BUT the epilogue?
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                        continue;
+                    }
 #pragma unroll
                     for (int chunk = 0; chunk < 2; ++chunk) {
                         const int ccol = colgrp * 64 + chunk * 32;   // first column of this chunk inside the tile
@@ -899,9 +924,8 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
 int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
                          int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
                          int32_t* d_dump) {
-    // Operand form per call under match_variant 4: e2m1 wins at scale (1 M x 1 M: 5.1e12 vs 3.3e12 compares/s) and on
-    // tiny problems; in between, where the top-2 bookkeeping of short runs dominates and the int8 kernel's longer
-    // tiles amortise it better, int8 is ~10 % ahead (8 k .. 20 k squared, profiles/r3e_match_perf.log).
+    // Operand form per call under match_variant 4 (A/B switch, off by default): before the parked-chunk epilogue the
+    // int8 kernel was ~10 % ahead between 8 k and 20 k squared, where top-2 bookkeeping of short runs dominated.
     const int saved = ctx->match_variant;
     const double work = static_cast<double>(Q) * static_cast<double>(N);
     if (saved == 4 && ctx->match_form_auto && work >= 3e7 && work <= 6e8) ctx->match_variant = 3;
@@ -993,6 +1017,8 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
     g.partial = ctx->partial.as<Partial>();
     g.dump = d_dump;
     static const bool tracing = std::getenv("CLATCH_TC_TRACE") != nullptr;
+    static const int debug_bits = std::getenv("CLATCH_TC_DEBUG") ? std::atoi(std::getenv("CLATCH_TC_DEBUG")) : 0;
+    g.debug = debug_bits;
     unsigned long long* d_trace = nullptr;
     if (tracing) {
         CLATCH_CUDA(cudaMalloc(&d_trace, sizeof(unsigned long long) * 8 * sms));
