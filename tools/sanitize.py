@@ -15,7 +15,7 @@ eng = lk.get_engine()
 img = port.structured_image(3, 320, 240)
 kps = lk.detect(img)
 kps = np.vstack([kps, port.random_keypoints(4, 320, 240, 37)])
-for variant in (0, 1, 2, 3):
+for variant in (0, 1, 2, 3, 4):
     eng.set_option("extract_variant", variant)
     for im in (img.astype(np.uint8), img, img + 0.25):
         kept, desc = lk.describe(im, kps)
@@ -23,10 +23,23 @@ for variant in (0, 1, 2, 3):
 text = (ROOT / "tests/golden/pattern_t64k5w.latchpat").read_text()
 lk.describe(img, kps[:50], pattern=text)
 kept, desc = lk.describe(img.astype(np.uint8), kps)
-for variant in (0, 1, 2, 3):
+for variant in (0, 1, 2, 3, 4):
     eng.set_option("match_variant", variant)
     got = lk.match(desc, desc[::2], ratio=0.9, cross_check=True)
     assert np.array_equal(got, port.match(desc, desc[::2], ratio=0.9, cross_check=True))
+big = port.random_descriptors(5, 3000, 64)
+for variant, pairs in ((3, 1), (4, 1), (4, 0)):                      # paired (multicast) and plain tensor-core launches
+    eng.set_option("match_variant", variant)
+    eng.set_option("match_pairs", pairs)
+    eng.set_option("match_streamk", 0)
+    bi, bd, sd = eng.match_top2(big[:700], big)
+    assert np.array_equal(np.stack([bi, bd, sd], 1), port.knn2_all(big[:700], big))
+eng.set_option("match_streamk", 1)
+eng.set_option("match_pairs", 1)
+nan_img = img.copy()
+nan_img[100, 100] = np.nan
+with np.errstate(all="ignore"):
+    assert np.array_equal(lk.describe(nan_img, kps)[1], port.describe_all(nan_img, kps)[1])
 d13 = port.random_descriptors(1, 90, 13)
 lk.match(d13[:40], d13[40:])
 third = max(1, len(desc) // 3)

@@ -49,7 +49,13 @@ while time.time() < t_end:
     eng.set_option("extract_variant", variant)
     as_f64 = rng.random() < 0.4
     src = img.astype(np.float64) + (rng.random(img.shape) * 0.3 if rng.random() < 0.3 and as_f64 else 0.0) if as_f64 else img
-    kept_idx, want = port.describe_all(np.asarray(src, np.float64), kps)
+    if as_f64:
+        eng.set_option("host_promote", int(rng.integers(0, 3)))          # pageable rule / always / never
+        if rng.random() < 0.15:                                          # non-finite pixels: the literal (w*e)*e kernel
+            src = src.copy()
+            src[int(rng.integers(0, h)), int(rng.integers(0, w))] = [np.nan, np.inf, -np.inf, 1e308][int(rng.integers(0, 4))]
+    with np.errstate(all="ignore"):
+        kept_idx, want = port.describe_all(np.asarray(src, np.float64), kps)
     kept, desc = lk.describe(src, kps)
     assert np.array_equal(kept, kps[kept_idx]) and np.array_equal(desc, want), ("describe", it, w, h, n, kind, variant, as_f64)
     cases["describe"] += 1
@@ -78,11 +84,13 @@ while time.time() < t_end:
         eng.set_option("upload_bands", 0)
         cases["banded"] += 1
     # matching
-    q_n, t_n = int(rng.choice([1, 2, 127, 129, 600, 3000])), int(rng.choice([1, 2, 255, 257, 1000, 5000]))
+    q_n, t_n = int(rng.choice([1, 2, 127, 129, 600, 3000, 9000])), int(rng.choice([1, 2, 239, 241, 255, 257, 1000, 5000, 12000]))
     q, t = port.random_descriptors(it, q_n), port.random_descriptors(it + 100000, t_n)
     for j in range(0, q_n, 5):
         q[j] = t[int(rng.integers(0, t_n))]
     eng.set_option("match_streamk", int(rng.integers(0, 2)))
+    eng.set_option("match_variant", int(rng.choice([3, 4, 4])))          # int8 / e2m1 operands on the tensor cores
+    eng.set_option("match_pairs", int(rng.integers(0, 2)))               # CTA pairs sharing the train stream or not
     kw = [{}, {"ratio": 0.8}, {"cross_check": True}, {"ratio": 0.9, "cross_check": True, "max_distance": 230}][int(rng.integers(0, 4))]
     assert np.array_equal(lk.match(q, t, **kw), port.match(q, t, **kw)), ("match", it, q_n, t_n, kw)
     cases["match"] += 1
@@ -100,4 +108,7 @@ while time.time() < t_end:
         cases["pairs"] += 1
 eng.set_option("extract_variant", 4)
 eng.set_option("match_streamk", 1)
+eng.set_option("match_variant", 4)
+eng.set_option("match_pairs", 1)
+eng.set_option("host_promote", 0)
 print(f"soak ok: {it} iterations in {budget:.0f} s; cases {cases}")
