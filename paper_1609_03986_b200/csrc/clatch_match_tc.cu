@@ -433,8 +433,8 @@ __device__ __forceinline__ void tc_park_chunk(int (&v)[32], const int valid, con
         if (key > k1) {                   // a new largest value for this row: its chunk replaces the parked one
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-                my_park[i] = make_uint4(static_cast<unsigned>(v[4 * i]), static_cast<unsigned>(v[4 * i + 1]),
-                                        static_cast<unsigned>(v[4 * i + 2]), static_cast<unsigned>(v[4 * i + 3]));
+                my_park[32 * i] = make_uint4(static_cast<unsigned>(v[4 * i]), static_cast<unsigned>(v[4 * i + 1]),
+                                             static_cast<unsigned>(v[4 * i + 2]), static_cast<unsigned>(v[4 * i + 3]));
             k2 = k1;
             k1 = key;
             c1 = cb;
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
     uint8_t* const tail = gen_base + kTcABytes + kTcStages * kTcStageBytes;
     volatile unsigned* tmem_slot = reinterpret_cast<volatile unsigned*>(tail + 128);
     int* merge_buf = reinterpret_cast<int*>(tail + 256);       // 128 rows x 4 ints
-    uint4* const park = reinterpret_cast<uint4*>(tail + 256 + kTcMergeBytes);   // F::kParked: [16 warps][32 lanes][8 x uint4]
+    uint4* const park = reinterpret_cast<uint4*>(tail + 256 + kTcMergeBytes);   // F::kParked: [16 warps][8 pieces][32 lanes] x uint4
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
                 // chunk at ~7 clk each — and eight warps needed 1 850 clk per 240-column tile against 960 clk of MMAs.
                 const int colgrp = ew >> 2;                                // columns [64 * colgrp, 64 * colgrp + 64)
                 int k1 = INT_MIN, k2 = INT_MIN, c1 = -1;
-                uint4* const my_park = park + (ew * 32 + lane) * 8;
+                uint4* const my_park = park + ew * (32 * 8) + lane;   // [warp][16-byte piece i][lane]: a warp's stores of one piece are contiguous
                 const bool dumping = g.dump != nullptr && item == 0 && rank == 0;
                 for (int t = 0; t < w.ntiles; ++t, ++tcount) {
                     const int buf = tcount & 1;
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
                 if (c1 >= 0) {
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const uint4 q = my_park[i];
+                        const uint4 q = my_park[32 * i];
                         const unsigned e[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
