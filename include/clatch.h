@@ -81,6 +81,9 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * double-buffered planes, texture-unit footprints and resampling overlapped with the estimate,
  * 4 = variant 3 with dedicated producer / consumer warps (default). 2-4 take u8-valued images; any
  * other image runs variant 1. Every variant returns the same bytes.
+ * key "extract_route": 1 (default) lets a context whose last u8 launch needed the exact pass for more than 35 % of its
+ * windows (flat / saturated images: exact ties) run the next launches on the all-fp64 quad kernel, probing the default
+ * kernel again every 16th launch; 0 = always the selected variant.
  * key "upload_bands": clatch_describe_all_f64 uploads a big float64 frame in this many row bands and
  * extracts each band's keypoints while the next band is in flight (0 = choose by frame size, the
  * default; 1 = one piece; up to 6). Results never depend on it.

@@ -290,6 +290,17 @@ int clatch_ctx_create(int device, clatch_ctx** out) {
         return cuda_fail(se, "cudaStreamCreateWithFlags");
     }
     if (const char* v = std::getenv("CLATCH_MATCH_VARIANT")) ctx->match_variant = std::atoi(v);
+    // per-CTA slots of the extraction router, written by the device into page-locked host memory (no copy, no sync)
+    if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->route_host), sizeof(uint2) * ctx->sm_count, cudaHostAllocMapped) == cudaSuccess) {
+        std::memset(ctx->route_host, 0, sizeof(uint2) * ctx->sm_count);
+        if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->route_dev), ctx->route_host, 0) != cudaSuccess) {
+            cudaFreeHost(ctx->route_host);
+            ctx->route_host = nullptr;
+        }
+    } else {
+        ctx->route_host = nullptr;
+    }
+    cudaGetLastError();
     *out = ctx;
     return CLATCH_OK;
 }
@@ -312,6 +323,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
         if (t.array) cudaFreeArray(t.array);
     }
     if (ctx->scratch_event) cudaEventDestroy(ctx->scratch_event);
+    if (ctx->route_host) cudaFreeHost(ctx->route_host);
     ctx->pinned.release();
     ctx->pin_img.release();
     ctx->pin_xycs.release();
@@ -354,6 +366,14 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
     if (std::strcmp(key, "extract_variant") == 0) {
         if (value < 0 || value > 4) return invalid("extract_variant must be 0..4");
         ctx->extract_variant = value;
+        ctx->route_quad = ctx->route_pending = false;
+        ctx->route_age = 0;
+        return CLATCH_OK;
+    }
+    if (std::strcmp(key, "extract_route") == 0) {   // route degenerate image streams to the all-fp64 quad kernel (1, default) or never (0)
+        ctx->extract_route = value != 0;
+        ctx->route_quad = ctx->route_pending = false;
+        ctx->route_age = 0;
         return CLATCH_OK;
     }
     if (std::strcmp(key, "upload_bands") == 0) {   // describe_all, float64 images: row bands of the upload (1 = one piece)

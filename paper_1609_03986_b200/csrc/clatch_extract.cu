@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "clatch_internal.cuh"
 #include "slot_assign.hpp"
@@ -51,6 +52,7 @@ struct ExtractParams {
     const int* flags;          // optional device flags (f64 promotion), may be null
     int run_if_flag;           // run only when flags[0] == run_if_flag (if flags != null)
     unsigned long long* stats; // optional {triplets recomputed exactly, warps that took the exact pass}
+    uint2* route;              // optional, host-mapped: per CTA {windows that took the exact pass, windows} of this launch
     cudaTextureObject_t tex;   // pipelined kernel: the u8 image as a gather-enabled CUDA array
     const unsigned* out_index; // optional: descriptor of record j goes to row out_index[j] (quad / pipelined kernels)
 };
@@ -1029,6 +1031,10 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
             atomicAdd(p.stats + 1, static_cast<unsigned long long>(n_windows));
         }
     }
+    // How many of this CTA's windows needed the exact pass: one plain 8-byte store into page-locked host memory per
+    // CTA, read by the host before the NEXT launch of this context (extraction routing, launch_extract).
+    if (p.route != nullptr && !producer && rt == 0)
+        p.route[blockIdx.x] = make_uint2(n_windows, static_cast<unsigned>(nq > 0 ? nq * kQuad : 0));
 }
 
 // Generic pattern: any T (multiple of 8), 1 <= K <= 64, arbitrary non-negative weights.
@@ -1217,8 +1223,43 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     p.run_if_flag = run_if_flag;
     p.stats = ctx->extract_stats_on ? ctx->extract_stats.as<unsigned long long>() : nullptr;
     p.out_index = ctx->extract_out_index;   // honoured by the quad and pipelined kernels (extract_supports_out_index)
+    // Degenerate input (flat or saturated regions: exact ties, which the fp32 estimate can never decide) makes the
+    // estimate-based kernels pay the estimate, a re-resampling and the exact chains — 23 M desc/s on a flat image
+    // against 36 M for the all-fp64 quad kernel. The default kernel reports, per launch, how many windows took the
+    // exact pass (ExtractParams::route, a host-mapped slot per CTA); when the previous launch of this context saw
+    // more than 35 % the next ones run the quad kernel, and every 16th launch probes with the default kernel again.
+    bool quad_routed = false;
+    const bool routing = kU8 && pat.fast && ctx->extract_variant == 4 && ctx->extract_route && !ctx->extract_stats_on &&
+                         flags == nullptr && ctx->route_host != nullptr && !force_generic;
+    if (routing) {
+        if (ctx->route_pending) {   // fold the last probe's slots (its kernel may still be running: then they read 0 / stale, harmless)
+            unsigned long long hot = 0, all = 0;
+            for (int c = 0; c < ctx->sm_count; ++c) {
+                hot += ctx->route_host[c].x;
+                all += ctx->route_host[c].y;
+            }
+            if (all > 0) {
+                ctx->route_quad = hot * 100 > all * 35;
+                ctx->route_pending = false;
+            }
+        }
+        ++ctx->route_age;
+        if (ctx->route_quad && (ctx->route_age & 15) != 0) quad_routed = true;
+    }
     if (force_generic) {
         extract_generic_kernel<kU8><<<grid_for(ctx, M, 2), kThreads, pat.T, stream>>>(p);
+    } else if (quad_routed) {
+        if (!ctx->quad_configured) {   // per-device function attribute
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_quad_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kQuadSmemBytes));
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_quad_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kQuadSmemBytes));
+            ctx->quad_configured = true;
+        }
+        p.slots = pat.slots_quad.as<ushort4>();
+        const size_t quads = (M + kQuad - 1) / kQuad;
+        const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
+        extract_quad_kernel<kU8><<<grid, kQuadThreads, kQuadSmemBytes, stream>>>(p);
     } else if (kU8 && pat.fast && ctx->extract_variant >= 3) {
         if (!ctx->pipe_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1245,6 +1286,13 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         // variant 4 (default): dedicated producer / consumer warps, 16 + 16 — 60.1 vs 58.1 M desc/s at 10 k
         // keypoints and 72.3 vs 68.3 M at 50 k against the symmetric schedule of variant 3 (24 + 8 warps
         // measured 48.8 M: eight warps cannot keep the LSU busy)
+        // a probe: every launch while the stream is degenerate (they are the 16th ones), every 8th one otherwise — the
+        // store into host memory at the end of the kernel costs ~2 us per launch
+        if (routing && M >= 64 && (ctx->route_quad || (ctx->route_age & 7) == 1)) {
+            std::memset(ctx->route_host, 0, sizeof(uint2) * ctx->sm_count);
+            p.route = ctx->route_dev;
+            ctx->route_pending = true;
+        }
         if (ctx->extract_variant == 4) extract_roles_kernel<16><<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
         else extract_pipe_kernel<<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
     } else if (kU8 && pat.fast && ctx->extract_variant == 2) {

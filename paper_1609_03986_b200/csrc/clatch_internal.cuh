@@ -92,6 +92,12 @@ struct clatch_ctx {
         int width = 0, height = 0;
     };
     std::vector<TexImage> tex_images;
+    // extraction routing for degenerate images (launch_extract): host-mapped per-CTA slots written by the default kernel
+    bool extract_route = true;       // set_option "extract_route"
+    uint2* route_host = nullptr;     // page-locked, mapped
+    uint2* route_dev = nullptr;      // the device's view of route_host
+    bool route_pending = false, route_quad = false;
+    unsigned route_age = 0;
     const unsigned* extract_out_index = nullptr;   // set around a launch: record j -> output row (banded upload)
     bool extract_stats_on = false;           // count exact recomputes (clatch_extract_stats)
     clatch::DeviceBuffer extract_stats;      // 2 x u64

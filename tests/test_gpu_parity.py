@@ -1087,3 +1087,38 @@ def test_single_pair_match_filters_on_the_device(lk, port, q, n):
     finally:
         eng.set_option("pairs_filter_on_device", 1)
     assert np.array_equal(lk.match(probes, probes, cross_check=True), port.match(probes, probes, cross_check=True))
+
+
+def test_degenerate_streams_are_routed_to_the_quad_kernel_and_stay_exact(lk, port):
+    """A context whose last launch needed the exact pass for more than 35 % of its windows (flat or saturated
+    images) runs its next launches on the all-fp64 quad kernel and probes the default kernel again every 16th
+    launch. Whatever the router decides, and however flat and textured images alternate, the descriptors are
+    the oracle's."""
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    eng.set_pattern(None)
+    w, h = 640, 480
+    kps = port.random_keypoints(5151, w, h, 900)
+    noise = port.random_image_u8(5150, w, h)
+    flat = np.full((h, w), 77, np.uint8)
+    half = noise.copy()
+    half[:, : w // 2] = 255
+    want = {name: port.describe_all(im.astype(np.float64), kps)[1] for name, im in (("noise", noise), ("flat", flat), ("half", half))}
+    imgs = {"noise": noise, "flat": flat, "half": half}
+    xycs, _ = eng.prepare_keypoints(kps, w, h)
+    d_x = torch.from_numpy(xycs).cuda()
+    d_imgs = {k: torch.from_numpy(v).cuda() for k, v in imgs.items()}
+    order = ["flat"] * 20 + ["noise"] * 20 + ["flat", "noise", "half"] * 8
+    try:
+        for route in (1, 0):
+            eng.set_option("extract_route", route)
+            for i, name in enumerate(order):
+                if i % 3 == 0:
+                    got = lk.describe(imgs[name], kps)[1]
+                else:
+                    got = eng.extract_device(d_imgs[name], d_x)
+                    torch.cuda.synchronize()
+                    got = got.cpu().numpy()
+                assert np.array_equal(got, want[name]), (route, i, name)
+    finally:
+        eng.set_option("extract_route", 1)
