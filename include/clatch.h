@@ -81,6 +81,9 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * double-buffered planes, texture-unit footprints and resampling overlapped with the estimate,
  * 4 = variant 3 with dedicated producer / consumer warps (default). 2-4 take u8-valued images; any
  * other image runs variant 1. Every variant returns the same bytes.
+ * key "pdl": 1 (default) launches the dependent kernels of the library's own chains (array fill -> extraction; operand
+ * expansion -> tensor-core matcher -> merge) with programmatic stream serialization: their CTAs are scheduled and run
+ * their set-up while the predecessor finishes, and wait (griddepcontrol.wait) before touching its output; 0 = plain launches.
  * key "extract_route": 1 (default) lets a context whose last u8 launch needed the exact pass for more than 35 % of its
  * windows (flat / saturated images: exact ties) run the next launches on the all-fp64 quad kernel, probing the default
  * kernel again every 16th launch; 0 = always the selected variant.

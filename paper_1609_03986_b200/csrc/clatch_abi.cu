@@ -370,6 +370,10 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         ctx->route_age = 0;
         return CLATCH_OK;
     }
+    if (std::strcmp(key, "pdl") == 0) {   // programmatic dependent launch inside the library's kernel chains
+        ctx->pdl = value != 0;
+        return CLATCH_OK;
+    }
     if (std::strcmp(key, "extract_route") == 0) {   // route degenerate image streams to the all-fp64 quad kernel (1, default) or never (0)
         ctx->extract_route = value != 0;
         ctx->route_quad = ctx->route_pending = false;

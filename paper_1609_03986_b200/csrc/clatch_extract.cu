@@ -912,6 +912,7 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
     // row products two quads ahead (buffer [quad & 1]) and pack the previous quad's bits.
     stage_quad_rows(p, static_cast<unsigned long long>(blockIdx.x) * kQuad, s_tab, s_kp, tid);
     __syncthreads();
+    pdl_wait();   // launched early behind fill_array_kernel: the texture array is complete from here on
 
     for (long long it = -1; it <= nq; ++it) {
         const int cur = static_cast<int>(it & 1), nxt = cur ^ 1;
@@ -1134,6 +1135,7 @@ int grid_for(const clatch_ctx* ctx, size_t M, int ctas_per_sm) {
 // 6.6 us for 3840x2160; cudaMemcpy2DToArrayAsync takes 8.4 / 21 us — tools/tex_probe.cu).
 __global__ void fill_array_kernel(cudaSurfaceObject_t surf, const uint8_t* __restrict__ src, size_t pitch, int w, int h,
                                   bool aligned, const int* flags, int run_if_flag) {
+    pdl_launch_dependents();   // the extraction kernel's CTAs may load their tables while the array is being filled
     if (flags != nullptr && flags[0] != run_if_flag) return;
     const int x = (blockIdx.x * blockDim.x + threadIdx.x) * 16, y = blockIdx.y;
     if (x >= w || y >= h) return;
@@ -1293,7 +1295,8 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
             p.route = ctx->route_dev;
             ctx->route_pending = true;
         }
-        if (ctx->extract_variant == 4) extract_roles_kernel<16><<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
+        if (ctx->extract_variant == 4)   // may start (tables, first keypoint rows) while fill_array_kernel is still writing
+            CLATCH_CUDA(launch_kernel(extract_roles_kernel<16>, dim3(grid), dim3(kQuadThreads), kPipeSmemBytes, stream, ctx->pdl, 1, p));
         else extract_pipe_kernel<<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
     } else if (kU8 && pat.fast && ctx->extract_variant == 2) {
         if (!ctx->filt_configured) {   // per-device function attribute

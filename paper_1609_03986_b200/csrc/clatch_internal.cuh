@@ -104,6 +104,7 @@ struct clatch_ctx {
     bool pairs_filter_on_device = true;   // clatch_match_set_pairs: ratio / max / cross-check decisions on the device
     // tensor matcher: clusters of two CTAs share the train-set stream through TMA multicast (one L2 read feeds two
     // SMs) wherever two query tiles scan the same train tiles; set_option "match_pairs" 0 = every CTA on its own.
+    bool pdl = true;               // programmatic dependent launch inside the library's own kernel chains (set_option "pdl")
     bool match_pairs = true;
     bool match_form_auto = false;  // match_variant 4: 1 = mid-sized single matches run the int8 form (it was ahead there before the parked-chunk epilogue; kept for A/B)
     bool match_streamk = true;     // tensor matcher: equal-share partition for small problems (set_option "match_streamk")
@@ -143,6 +144,45 @@ struct clatch_ctx {
 };
 
 namespace clatch {
+
+// Programmatic dependent launch (PDL): a kernel launched with launch_kernel(..., pdl = true) may start while its
+// predecessor in the stream is still running — its CTAs get scheduled and run their set-up — and must execute
+// pdl_wait() before it touches anything the predecessor writes (or writes anything the predecessor reads); the
+// predecessor calls pdl_launch_dependents() as early as it likes (here: at its start). Without the attribute both
+// instructions are no-ops. Only kernels whose predecessor was launched the ordinary way (fully ordered behind
+// ITS predecessors) or is itself a PDL kernel that waits at its start are launched like this, so that
+// pdl_wait() transitively covers everything earlier in the stream.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, bool pdl,
+                                 unsigned cluster_x, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attrs[2]{};
+    unsigned n = 0;
+    if (cluster_x > 1) {
+        attrs[n].id = cudaLaunchAttributeClusterDimension;
+        attrs[n].val.clusterDim.x = cluster_x;
+        attrs[n].val.clusterDim.y = 1;
+        attrs[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    if (pdl) {
+        attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+#endif
 
 inline int scratch_acquire(clatch_ctx* ctx, cudaStream_t st) {
     if (ctx->scratch_private) return CLATCH_OK;
@@ -222,7 +262,7 @@ bool tc_items_paired(const clatch_ctx* ctx);   // item tables must hold entries 
 int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t* d_out, cudaStream_t stream);
 int launch_match_tc_items(clatch_ctx* ctx, const TcItem* d_items, size_t count, cudaStream_t stream);
 void launch_merge_partials(const Partial* partial, unsigned long long Q, int splits, int sentinel,
-                           int32_t* best_idx, int32_t* best_dist, int32_t* second_dist, cudaStream_t stream);
+                           int32_t* best_idx, int32_t* best_dist, int32_t* second_dist, cudaStream_t stream, bool pdl = false);
 int launch_match_top2_tc(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,
                          int32_t* d_best_idx, int32_t* d_best_dist, int32_t* d_second, cudaStream_t stream,
                          int32_t* d_dump = nullptr);

@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kMatchThreads) match64_kernel(const uint8_t* _
 __global__ void merge_partials_kernel(const Partial* __restrict__ partial, unsigned long long Q,
                                       int splits, int sentinel, int32_t* __restrict__ best_idx,
                                       int32_t* __restrict__ best_dist, int32_t* __restrict__ second_dist) {
+    pdl_wait();   // (launched early behind the tensor-core matcher: its partials are complete from here on)
     const unsigned long long qi = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (qi >= Q) return;
     int best = sentinel, second = sentinel, idx = -1;
@@ -361,9 +362,9 @@ int launch_filter_pairs(clatch_ctx* ctx, const FilterPair* d_pairs, size_t count
 }
 
 void launch_merge_partials(const Partial* partial, unsigned long long Q, int splits, int sentinel,
-                           int32_t* best_idx, int32_t* best_dist, int32_t* second_dist, cudaStream_t stream) {
-    merge_partials_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(partial, Q, splits, sentinel,
-                                                                                      best_idx, best_dist, second_dist);
+                           int32_t* best_idx, int32_t* best_dist, int32_t* second_dist, cudaStream_t stream, bool pdl) {
+    launch_kernel(merge_partials_kernel, dim3(static_cast<unsigned>((Q + 255) / 256)), dim3(256), 0, stream, pdl, 1, partial, Q,
+                  splits, sentinel, best_idx, best_dist, second_dist);
 }
 
 static int match_top2_on(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, const uint8_t* d_t, size_t N,

@@ -87,6 +87,7 @@ template <class F>
 __global__ void expand_kernel(const uint8_t* __restrict__ packed, unsigned long long n,
                               unsigned long long padded_rows, uint8_t* __restrict__ out) {
     constexpr int kChunks = F::kKBlocks * 8;           // 16-byte chunks per row
+    pdl_launch_dependents();                           // the matcher's CTAs may start their set-up now
     const unsigned long long idx = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     const unsigned long long row = idx / kChunks;
     if (row >= padded_rows) return;
@@ -516,6 +517,8 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
         tc_fence_after();
     }
 
+    pdl_launch_dependents();                                   // (the merge kernel's blocks may take their seats)
+    pdl_wait();                                                // the expanded operands are complete and visible
     if (trace && threadIdx.x == 0) trace[1] = global_ns();   // set-up done (barriers, TMEM, scale bytes)
     if (warp == 0) {
         // ===== producer =====
@@ -811,6 +814,7 @@ namespace {
 __global__ void merge_partials_sk_kernel(const Partial* __restrict__ partial, unsigned long long Q, int total_tiles,
                                          int qtiles, int chunks, int32_t* __restrict__ best_idx,
                                          int32_t* __restrict__ best_dist, int32_t* __restrict__ second_dist) {
+    pdl_wait();                                                // every partial of the GEMM launch is in place
     const unsigned long long qi = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (qi >= Q) return;
     const unsigned long long U = static_cast<unsigned long long>(qtiles) * total_tiles, TT = total_tiles, q = qi / kTcM;
@@ -873,30 +877,20 @@ int launch_tc_expand(clatch_ctx* ctx, const uint8_t* d_packed, size_t n, uint8_t
 
 int tc_query_tiles(size_t rows) { return static_cast<int>((rows + kTcM - 1) / kTcM); }
 
-// One launch of the kernel in the context's operand form; `paired` = clusters of two CTAs (cudaLaunchKernelEx).
-static int launch_tc(clatch_ctx* ctx, const TcArgs& g, unsigned ctas, bool paired, cudaStream_t stream) {
+// One launch of the kernel in the context's operand form; `paired` = clusters of two CTAs; `pdl` = may start while the
+// expansion kernel queued just before it is still running (it waits for it after its own set-up).
+static int launch_tc(clatch_ctx* ctx, const TcArgs& g, unsigned ctas, bool paired, cudaStream_t stream, bool pdl = false) {
     const bool f4 = ctx->match_variant == 4;
-    if (!paired) {
-        if (f4) match_tc_kernel<TcF4, false><<<ctas, tc_threads<TcF4>(), tc_smem_bytes<TcF4>(), stream>>>(g);
-        else match_tc_kernel<TcI8, false><<<ctas, tc_threads<TcI8>(), tc_smem_bytes<TcI8>(), stream>>>(g);
-        ++ctx->launches;
-        CLATCH_CUDA(cudaGetLastError());
-        return CLATCH_OK;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(ctas & ~1u);
-    cfg.blockDim = dim3(f4 ? tc_threads<TcF4>() : tc_threads<TcI8>());
-    cfg.dynamicSmemBytes = f4 ? tc_smem_bytes<TcF4>() : tc_smem_bytes<TcI8>();
-    cfg.stream = stream;
-    cudaLaunchAttribute attr{};
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = 2;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    if (f4) CLATCH_CUDA(cudaLaunchKernelEx(&cfg, match_tc_kernel<TcF4, true>, g));
-    else CLATCH_CUDA(cudaLaunchKernelEx(&cfg, match_tc_kernel<TcI8, true>, g));
+    const dim3 grid(paired ? (ctas & ~1u) : ctas), block(f4 ? tc_threads<TcF4>() : tc_threads<TcI8>());
+    const size_t smem = f4 ? tc_smem_bytes<TcF4>() : tc_smem_bytes<TcI8>();
+    const unsigned cluster = paired ? 2 : 1;
+    pdl = pdl && ctx->pdl;
+    cudaError_t e;
+    if (f4) e = paired ? launch_kernel(match_tc_kernel<TcF4, true>, grid, block, smem, stream, pdl, cluster, g)
+                       : launch_kernel(match_tc_kernel<TcF4, false>, grid, block, smem, stream, pdl, cluster, g);
+    else e = paired ? launch_kernel(match_tc_kernel<TcI8, true>, grid, block, smem, stream, pdl, cluster, g)
+                    : launch_kernel(match_tc_kernel<TcI8, false>, grid, block, smem, stream, pdl, cluster, g);
+    CLATCH_CUDA(e);
     ++ctx->launches;
     return CLATCH_OK;
 }
@@ -1028,10 +1022,10 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
     if (paired) {
         const size_t pair_items = (qtiles + 1) / 2 * splits;
         g.num_items = static_cast<int>(pair_items);
-        if (int rc = launch_tc(ctx, g, static_cast<unsigned>(std::min<size_t>(2 * pair_items, sms)), true, stream)) return rc;
+        if (int rc = launch_tc(ctx, g, static_cast<unsigned>(std::min<size_t>(2 * pair_items, sms)), true, stream, !tracing)) return rc;
     } else {
         const unsigned grid = static_cast<unsigned>(streamk ? chunks : std::min<size_t>(qtiles * splits, ctx->sm_count));
-        if (int rc = launch_tc(ctx, g, grid, false, stream)) return rc;
+        if (int rc = launch_tc(ctx, g, grid, false, stream, !tracing)) return rc;
     }
     if (tracing) {   // debug: where the time of a launch goes, per CTA (globaltimer, ns)
         std::vector<unsigned long long> h(8 * sms);
@@ -1059,12 +1053,13 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
                      mx[1], sum[2] / n, mx[2], sum[3] / n, mx[3], sum[4] / n, mx[4], sum[5] / n, mx[5]);
     }
     if (streamk)
-        merge_partials_sk_kernel<<<static_cast<unsigned>((Q + 255) / 256), 256, 0, stream>>>(
-            ctx->partial.as<Partial>(), Q, static_cast<int>(ttiles), static_cast<int>(qtiles), static_cast<int>(chunks),
-            d_best_idx, d_best_dist, d_second);
+        CLATCH_CUDA(launch_kernel(merge_partials_sk_kernel, dim3(static_cast<unsigned>((Q + 255) / 256)), dim3(256), 0, stream,
+                                  ctx->pdl && !tracing, 1, static_cast<const Partial*>(ctx->partial.as<Partial>()),
+                                  static_cast<unsigned long long>(Q), static_cast<int>(ttiles), static_cast<int>(qtiles),
+                                  static_cast<int>(chunks), d_best_idx, d_best_dist, d_second));
     else
         launch_merge_partials(ctx->partial.as<Partial>(), Q, static_cast<int>(splits), 513, d_best_idx, d_best_dist,
-                              d_second, stream);
+                              d_second, stream, ctx->pdl && !tracing);
     ++ctx->launches;
     CLATCH_CUDA(cudaGetLastError());
     return CLATCH_OK;
