@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "clatch_internal.cuh"
 #include "slot_assign.hpp"
@@ -55,7 +56,16 @@ struct ExtractParams {
     uint2* route;              // optional, host-mapped: per CTA {windows that took the exact pass, windows} of this launch
     cudaTextureObject_t tex;   // pipelined kernel: the u8 image as a gather-enabled CUDA array
     const unsigned* out_index; // optional: descriptor of record j goes to row out_index[j] (quad / pipelined kernels)
+    unsigned long long* trace; // optional (CLATCH_EX_TRACE=1): kExTrace globaltimer stamps per CTA of the default kernel
 };
+
+constexpr int kExTrace = 128;   // [0] entry, [1] texture array complete, [2 + i] end of pipeline iteration i - 1 (bit 63: exact pass)
+
+__device__ __forceinline__ unsigned long long ex_global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Exact u8 -> f64 without the 16-lane/clk conversion pipe (I2F.F64 runs at 16/clk/SM on
 // B200, profiles/r1a_pipe_peaks.json): splice the byte into the mantissa of 2^52 and
@@ -635,7 +645,16 @@ constexpr int kPipeSmemBytes = kPipePlanes * kPlanePitch * 4         // planes
                                + 2 * kQuad * kPipeBits               // predicate bytes [2][4][512 + pad]
                                + 2 * kQuad * kWindow * 16            // {s*dv, c*dv} rows [2][4][64]
                                + 2 * kQuad * 4 * 8                   // keypoint records [2][4][4]
-                               + 64;                                 // undecided-window masks [3]
+                               + 64;                                 // undecided-window masks [3], deferred-queue tail
+// Deferred exact bits (roles kernel): undecided (keypoint, triplet) items parked in shared memory and recomputed by
+// whole warps after the pipeline has drained, instead of stalling it (see extract_roles_kernel).
+constexpr int kQueueCap = 1024;          // items per CTA
+constexpr int kDeferMax = 48;            // a quad with more undecided triplets than this takes the window-wide pass
+struct DeferredBit {
+    ushort4 slot;                        // {a, b, c, bit | swapped << 15} as in the slot table
+    unsigned kp;                         // keypoint record index
+};
+constexpr int kRolesSmemBytes = kPipeSmemBytes + kQueueCap * static_cast<int>(sizeof(DeferredBit));
 
 // The 2x2 footprint whose top-left texel is (x0, y0): gather at the footprint's centre, half a
 // texel away from every selection boundary (tools/tex_probe.cu checks the component order):
@@ -870,6 +889,48 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_pipe_kernel(ExtractPa
     }
 }
 
+// One deferred bit, by one warp: the 3 x 49 live samples of the triplet's patches are resampled exactly as
+// extract_window / sample_bilinear compute them (the same code as the window-wide pass: sample_exact) into
+// `scratch` (147 doubles), lanes 0 and 1 run the two 49-term chains in the reference's row-major order, and the
+// descriptor word is patched in global memory (the estimate's guess was stored there by this CTA earlier).
+__device__ __noinline__ void recompute_deferred_bit(cudaTextureObject_t tex, const double* xycs, uint8_t* out,
+                                                    const unsigned* out_index, const DeferredBit item, double* scratch,
+                                                    int lane) {
+    const double* const kpr = xycs + 4 * static_cast<unsigned long long>(item.kp);
+    const double kx = __ldg(kpr + 0), ky = __ldg(kpr + 1), c = __ldg(kpr + 2), sn = __ldg(kpr + 3);
+    const unsigned offs[3] = {item.slot.x, item.slot.y, item.slot.z};
+#pragma unroll 1
+    for (int i = lane; i < 3 * 49; i += 32) {
+        const int patch = i / 49, pix = i - 49 * patch, r = pix / 7, cc = pix - 7 * r;
+        const unsigned off = patch == 0 ? offs[0] : (patch == 1 ? offs[1] : offs[2]);
+        const int v = static_cast<int>(off / kWinStride) + r, u = static_cast<int>(off % kWinStride) + cc;
+        const double du = static_cast<double>(u) - 31.5, dv = static_cast<double>(v) - 31.5;
+        const double xa = __dadd_rn(kx, __dmul_rn(c, du));
+        const double ya = __dadd_rn(ky, __dmul_rn(sn, du));
+        scratch[i] = sample_exact(tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv));
+    }
+    __syncwarp();
+    double d = 0.0;
+    if (lane < 2) {
+        const double* const other = scratch + 49 * (1 + lane);
+#pragma unroll 7
+        for (int k = 0; k < 49; ++k) {
+            const double e = __dsub_rn(scratch[k], other[k]);
+            d = __dadd_rn(d, __dmul_rn(e, e));
+        }
+    }
+    const double d2 = __shfl_sync(0xffffffffu, d, 1);
+    if (lane == 0) {
+        const bool bit = (item.slot.w >> 15) ? d2 > d : d > d2;
+        const unsigned t = item.slot.w & 0x7fffu;
+        const unsigned long long row = out_index ? out_index[item.kp] : item.kp;
+        unsigned* const word = reinterpret_cast<unsigned*>(out + row * (kFastT / 8)) + (t >> 5);
+        if (bit) atomicOr(word, 1u << (t & 31));
+        else atomicAnd(word, ~(1u << (t & 31)));
+    }
+    __syncwarp();
+}
+
 // ---- role-split variant of the pipelined kernel (A/B) -----------------------------------------
 // Same planes, same texture path, same estimate and exact code as extract_pipe_kernel, but the
 // warps specialise: kRW producer warps only resample (quad it+1 -> F[next]) and pack bits, the
@@ -893,6 +954,8 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
     double2* const s_tab = reinterpret_cast<double2*>(s_bits + 2 * kQuad * kPipeBits);   // [2][4][64]
     double* const s_kp = reinterpret_cast<double*>(s_tab + 2 * kQuad * kWindow);      // [2][4][x, y, cos, sin]
     int* const s_mask = reinterpret_cast<int*>(s_kp + 2 * kQuad * 4);                 // [2] windows needing LO
+    unsigned* const s_qtail = reinterpret_cast<unsigned*>(s_mask + 2);                // deferred bits queued so far
+    DeferredBit* const s_queue = reinterpret_cast<DeferredBit*>(s_quad + kPipeSmemBytes);   // [kQueueCap]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, grp = warp >> 2;
     const bool producer = grp % kStep != 0;
@@ -907,15 +970,28 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
 #pragma unroll
     for (int j = 0; j < kSlots; ++j) slot[j] = __ldg(p.slots + 8 * (rw % kSW + kSW * j) + ti);
     unsigned n_flagged = 0, n_windows = 0;
-    if (tid == 0) s_mask[0] = s_mask[1] = 0;
+    unsigned long long* const trace = p.trace != nullptr && tid == 0 ? p.trace + static_cast<size_t>(kExTrace) * blockIdx.x : nullptr;
+    if (trace) trace[0] = ex_global_ns();
+    if (tid == 0) s_mask[0] = s_mask[1] = 0, *s_qtail = 0;
+    // Undecided bits are rare on textured images (2e-5 of the triplets on noise), but the window-wide exact pass
+    // below stalls the whole CTA for ~4 us each time (one quad in 25 at that rate; the slowest CTA of a 10 k
+    // launch took four). So a quad with few of them only PARKS them — {slot, keypoint} in a shared-memory queue —
+    // and carries on with the estimate's guess in the descriptor; after the pipeline has drained every warp of
+    // the CTA takes parked items and recomputes each bit exactly (recompute_deferred_bit). Dense quads (flat or
+    // saturated regions: more than kDeferMax undecided triplets, or a full queue) take the window-wide pass as
+    // before. Either way the bit that ends up in the descriptor comes from the exact fp64 chains.
+    const bool defer_ok = p.M <= 0xffffffffull;
+    unsigned q_prev = 0;                 // queue tail after the previous quad (uniform over the consumers)
     // Producers only resample. The consumers, which have slack, also stage the keypoint records and
     // row products two quads ahead (buffer [quad & 1]) and pack the previous quad's bits.
     stage_quad_rows(p, static_cast<unsigned long long>(blockIdx.x) * kQuad, s_tab, s_kp, tid);
     __syncthreads();
     pdl_wait();   // launched early behind fill_array_kernel: the texture array is complete from here on
+    if (trace) trace[1] = ex_global_ns();
 
     for (long long it = -1; it <= nq; ++it) {
         const int cur = static_cast<int>(it & 1), nxt = cur ^ 1;
+        unsigned windows_before = n_windows;
         if (!producer) {
             if (it + 2 < nq)   // rows for quad it+2 -> buffer [cur] (its last readers resampled quad `it`, an iteration ago)
                 stage_quad_rows(p, (blockIdx.x + (it + 2) * gridDim.x) * kQuad, s_tab + cur * kQuad * kWindow,
@@ -994,10 +1070,28 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
                 my_bits[slot[j].w & 0x7fff] = (slot[j].w >> 15) ? diff0 < 0.0f : diff0 > 0.0f;
                 my_bits[slot[j + 1].w & 0x7fff] = (slot[j + 1].w >> 15) ? diff1 < 0.0f : diff1 > 0.0f;
             }
-            if (need) atomicOr(s_mask + cur, 1 << kb);
+            if (need) {
+                atomicOr(s_mask + cur, 1 << kb);
+                if (defer_ok) {
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j)
+                        if ((need >> j) & 1) {
+                            const unsigned at = atomicAdd(s_qtail, 1u);
+                            if (at < kQueueCap) s_queue[at] = DeferredBit{slot[j], static_cast<unsigned>(kp0 + kb)};
+                        }
+                }
+            }
             asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
             const int mask = *reinterpret_cast<volatile int*>(s_mask + cur);
-            if (mask) {   // uniform over the consumers: some window needs its LO plane
+            bool window_pass = mask != 0;
+            if (mask && defer_ok) {
+                const unsigned tail = *reinterpret_cast<volatile unsigned*>(s_qtail);
+                if (tail <= kQueueCap && tail - q_prev <= kDeferMax) {   // few: they stay parked
+                    q_prev = tail;
+                    window_pass = false;
+                }
+            }
+            if (window_pass) {   // uniform over the consumers: some window needs its LO plane
                 for (int w = 0; w < kQuad; ++w) {
                     if (!((mask >> w) & 1)) continue;
                     const double* kpr = p.xycs + 4 * (kp0 + w);
@@ -1014,6 +1108,7 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
                     n_windows += rt == 0;
                 }
                 asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
+                if (rt == 0) *s_qtail = q_prev;   // this quad's parked items are withdrawn (every consumer has read the tail)
 #pragma unroll
                 for (int j = 0; j < kSlots; ++j)
                     if ((need >> j) & 1) {
@@ -1024,6 +1119,19 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
             }
         }
         __syncthreads();
+        if (trace && it + 3 < kExTrace)
+            trace[it + 3] = ex_global_ns() | (n_windows != windows_before ? 1ull << 63 : 0ull);
+    }
+    // The pipeline has drained (the loop ends on a CTA-wide barrier, every descriptor word of this CTA is in global
+    // memory): all 32 warps take the parked bits, the plane memory serves as their scratch.
+    {
+        const unsigned parked = *reinterpret_cast<volatile unsigned*>(s_qtail);
+        double* const scratch = reinterpret_cast<double*>(s_f) + warp * 160;   // 147 doubles per warp
+        for (unsigned i = warp; i < parked; i += kQuadThreads / 32) {
+            recompute_deferred_bit(p.tex, p.xycs, p.out, p.out_index, s_queue[i], scratch, lane);
+            n_flagged += lane == 0;
+        }
+        if (trace && parked) trace[kExTrace - 1] = ex_global_ns() | static_cast<unsigned long long>(parked) << 48;
     }
     if (p.stats != nullptr) {
         n_flagged = __reduce_add_sync(0xffffffffu, n_flagged);
@@ -1203,6 +1311,66 @@ int ensure_single_window_plan(clatch_ctx* ctx) {
     return CLATCH_OK;
 }
 
+// CLATCH_EX_TRACE=1: where one launch of the default kernel spends its time (stamps of extract_roles_kernel).
+void print_extract_trace(const std::vector<unsigned long long>& h, int grid, size_t quads) {
+    const unsigned long long kFlag = 1ull << 63;
+    unsigned long long t0 = ~0ull, t_end = 0;
+    for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[static_cast<size_t>(kExTrace) * c]);
+    double entry_max = 0, ready_mean = 0, ready_max = 0, fill_mean = 0, drain_mean = 0, end_mean = 0, end_min = 1e30;
+    double steady_sum = 0, exact_sum = 0;
+    size_t steady_n = 0, exact_n = 0, parked = 0, parked_ctas = 0;
+    double parked_us = 0;
+    std::vector<double> ends(grid);
+    std::vector<int> exacts(grid, 0);
+    for (int c = 0; c < grid; ++c) {
+        const unsigned long long* t = h.data() + static_cast<size_t>(kExTrace) * c;
+        const long long nq = static_cast<long long>((quads - c + grid - 1) / grid);
+        const long long last = std::min<long long>(nq + 3, kExTrace - 1);   // stamp index of iteration nq
+        entry_max = std::max(entry_max, (t[0] - t0) * 1e-3);
+        ready_mean += (t[1] - t0) * 1e-3;
+        ready_max = std::max(ready_max, (t[1] - t0) * 1e-3);
+        fill_mean += ((t[2] & ~kFlag) - t[1]) * 1e-3;
+        for (long long i = 3; i < last; ++i) {   // iterations 0 .. nq-1
+            const double d = ((t[i] & ~kFlag) - (t[i - 1] & ~kFlag)) * 1e-3;
+            if (t[i] & kFlag) {
+                exact_sum += d;
+                ++exact_n;
+                ++exacts[c];
+            } else if (i + 1 < last) {
+                steady_sum += d;
+                ++steady_n;
+            } else {
+                drain_mean += d;
+            }
+        }
+        double e = ((t[last] & ~kFlag) - t0) * 1e-3;
+        if (t[kExTrace - 1]) {   // parked bits recomputed after the pipeline drained
+            parked += t[kExTrace - 1] >> 48;
+            const double after = ((t[kExTrace - 1] & 0xffffffffffffull) - (t0 & 0xffffffffffffull)) * 1e-3;
+            parked_us += after - e;
+            ++parked_ctas;
+            e = after;
+            t_end = std::max(t_end, (t0 & ~0xffffffffffffull) | (t[kExTrace - 1] & 0xffffffffffffull));
+        }
+        ends[c] = e;
+        end_mean += e;
+        end_min = std::min(end_min, e);
+        t_end = std::max(t_end, t[last] & ~kFlag);
+    }
+    int worst = 0;
+    for (int c = 0; c < grid; ++c)
+        if (ends[c] > ends[worst]) worst = c;
+    std::fprintf(stderr,
+                 "[clatch ex trace] ctas=%d quads=%zu span %.1f us | entry max %.1f, texture ready mean %.1f max %.1f, first resample %.1f, "
+                 "steady iteration %.2f (n=%zu), iteration with an exact pass %.2f (n=%zu), last estimate %.2f | CTA end mean %.1f min %.1f "
+                 "max %.1f (cta %d: %d exact passes, %lld quads) | parked bits %zu in %zu CTAs, %.2f us per such CTA\n",
+                 grid, quads, (t_end - t0) * 1e-3, entry_max, ready_mean / grid, ready_max, fill_mean / grid,
+                 steady_n ? steady_sum / steady_n : 0.0, steady_n, exact_n ? exact_sum / exact_n : 0.0, exact_n, drain_mean / grid,
+                 end_mean / grid, end_min, ends[worst], worst, exacts[worst],
+                 static_cast<long long>((quads - worst + grid - 1) / grid), parked, parked_ctas,
+                 parked_ctas ? parked_us / parked_ctas : 0.0);
+}
+
 template <bool kU8>
 int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, size_t pitch,
                    const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream,
@@ -1267,7 +1435,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
             CLATCH_CUDA(cudaFuncSetAttribute(extract_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kPipeSmemBytes));
             CLATCH_CUDA(cudaFuncSetAttribute(extract_roles_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kPipeSmemBytes));
+                                             kRolesSmemBytes));
             ctx->pipe_configured = true;
         }
         // The resampler reads footprints through the texture unit: copy the image into this
@@ -1295,9 +1463,23 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
             p.route = ctx->route_dev;
             ctx->route_pending = true;
         }
+        static const bool tracing = std::getenv("CLATCH_EX_TRACE") != nullptr;
+        unsigned long long* d_trace = nullptr;
+        if (tracing && ctx->extract_variant == 4) {   // diagnostics: per-CTA timeline of the launch (synchronises)
+            CLATCH_CUDA(cudaMalloc(&d_trace, sizeof(unsigned long long) * kExTrace * grid));
+            CLATCH_CUDA(cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long) * kExTrace * grid, stream));
+            p.trace = d_trace;
+        }
         if (ctx->extract_variant == 4)   // may start (tables, first keypoint rows) while fill_array_kernel is still writing
-            CLATCH_CUDA(launch_kernel(extract_roles_kernel<16>, dim3(grid), dim3(kQuadThreads), kPipeSmemBytes, stream, ctx->pdl, 1, p));
+            CLATCH_CUDA(launch_kernel(extract_roles_kernel<16>, dim3(grid), dim3(kQuadThreads), kRolesSmemBytes, stream, ctx->pdl, 1, p));
         else extract_pipe_kernel<<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
+        if (d_trace) {
+            std::vector<unsigned long long> h(static_cast<size_t>(kExTrace) * grid);
+            CLATCH_CUDA(cudaStreamSynchronize(stream));
+            CLATCH_CUDA(cudaMemcpy(h.data(), d_trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+            cudaFree(d_trace);
+            print_extract_trace(h, grid, quads);
+        }
     } else if (kU8 && pat.fast && ctx->extract_variant == 2) {
         if (!ctx->filt_configured) {   // per-device function attribute
             CLATCH_CUDA(cudaFuncSetAttribute(extract_filt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -602,6 +602,44 @@ def test_filtered_kernel_exact_pass_rate(lk, port, variant):
         eng.set_option("extract_variant", 4)
 
 
+def test_sparse_undecided_bits_are_parked_and_recomputed_exactly(lk, port):
+    """Default kernel: a quad with only a few undecided triplets parks them and the whole CTA recomputes
+    each one exactly after its pipeline has drained (no window-wide pass, no stall). Images where that is
+    the common case — noise with a few saturated blobs, isolated flat patches — must give the oracle's
+    descriptors, the counters must show parked bits, and scattered output rows (banded float64 upload)
+    must be patched in the right place."""
+    eng = lk.get_engine()
+    w, h, n = 1024, 768, 6000
+    rng = np.random.default_rng(20261017)
+    yy, xx = np.mgrid[0:h, 0:w]
+    noise = port.random_image_u8(4242, w, h)
+    blobs = noise.copy()
+    for _ in range(160):                                   # small saturated discs: ties inside, texture around
+        cy, cx, r = rng.integers(0, h), rng.integers(0, w), rng.integers(5, 12)
+        blobs[(yy - cy) ** 2 + (xx - cx) ** 2 <= r * r] = 255
+    kps = port.random_keypoints(4243, w, h, n)
+    try:
+        for name, img in (("noise", noise), ("blobs", blobs)):
+            want = port.describe_all(img.astype(np.float64), kps)[1]
+            eng.set_option("extract_stats", 1)
+            got = lk.describe(img, kps)[1]
+            exact, window_passes = eng.extract_stats()
+            assert np.array_equal(got, want), name
+            assert exact > 0, (name, "no undecided bit at all: the test image is too tame")
+            if name == "noise":
+                assert window_passes == 0, (name, exact, window_passes)   # every undecided bit was parked
+            eng.set_option("extract_stats", 0)
+            f64 = np.ascontiguousarray(img, dtype=np.float64)           # banded upload: out_index rows
+            eng.set_option("host_promote", 2)                           # (the doubles go up, the device classifies)
+            for bands in (1, 3):
+                eng.set_option("upload_bands", bands)
+                assert np.array_equal(lk.describe(f64, kps)[1], want), (name, bands)
+    finally:
+        eng.set_option("extract_stats", 0)
+        eng.set_option("upload_bands", 0)
+        eng.set_option("host_promote", 0)
+
+
 @pytest.mark.parametrize("promote", [1, 2, 0])
 def test_float64_promotion_edges(lk, port, promote):
     """A float64 image goes to the u8 kernels only if EVERY pixel is an integer in [0, 255] (host
