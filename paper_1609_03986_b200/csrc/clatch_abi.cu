@@ -26,6 +26,7 @@
 namespace clatch {
 namespace {
 #include "default_plan_f8.inc"
+#include "default_plan_h16.inc"
 }
 }
 
@@ -314,11 +315,12 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
     }
     for (DeviceBuffer* b : {&ctx->img, &ctx->kps, &ctx->desc, &ctx->q, &ctx->t, &ctx->res,
                             &ctx->partial, &ctx->flags, &ctx->img_u8, &ctx->exp_q, &ctx->exp_t, &ctx->items, &ctx->scores, &ctx->counts, &ctx->det, &ctx->pattern.slots, &ctx->pattern.slots_quad,
-                            &ctx->pattern.slots_f8, &ctx->extract_stats, &ctx->filt_pairs, &ctx->filt_rows, &ctx->filt_out,
+                            &ctx->pattern.slots_f8, &ctx->pattern.slots_h16, &ctx->extract_stats, &ctx->filt_pairs, &ctx->filt_rows, &ctx->filt_out,
                             &ctx->filt_counts, &ctx->pattern.triplets, &ctx->pattern.d_weights})
         b->release();
     for (auto& t : ctx->tex_images) {
         if (t.tex) cudaDestroyTextureObject(t.tex);
+        if (t.texn) cudaDestroyTextureObject(t.texn);
         if (t.surf) cudaDestroySurfaceObject(t.surf);
         if (t.array) cudaFreeArray(t.array);
     }
@@ -364,7 +366,7 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         return CLATCH_OK;
     }
     if (std::strcmp(key, "extract_variant") == 0) {
-        if (value < 0 || value > 4) return invalid("extract_variant must be 0..4");
+        if (value < 0 || value > 5) return invalid("extract_variant must be 0..5");
         ctx->extract_variant = value;
         ctx->route_quad = ctx->route_pending = false;
         ctx->route_age = 0;
@@ -528,6 +530,16 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
             const SlotPlan f8 = plan_slots_grouped(triplets, T, kWinStride, 8, 8, 1500000);
             pat.slot_degree_f8 = f8.avg_degree;
             CLATCH_CUDA(cudaMemcpy(pat.slots_f8.ptr, f8.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
+        }
+        if (int rc = pat.slots_h16.reserve(sizeof(SlotEntry) * T)) return rc;
+        if (triplet_hash(triplets, T) == kDefaultPlanHash && kDefaultPlanH16RowWords == kH16RowWords) {
+            static_assert(sizeof(kDefaultPlanH16) == sizeof(SlotEntry) * kFastT, "embedded plan size");
+            pat.slot_degree_h16 = kDefaultPlanH16Degree;
+            CLATCH_CUDA(cudaMemcpy(pat.slots_h16.ptr, kDefaultPlanH16, sizeof(kDefaultPlanH16), cudaMemcpyHostToDevice));
+        } else {
+            const SlotPlan h16 = plan_slots_h16(triplets, T, 1500000);
+            pat.slot_degree_h16 = h16.avg_degree;
+            CLATCH_CUDA(cudaMemcpy(pat.slots_h16.ptr, h16.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
         }
     }
     return CLATCH_OK;

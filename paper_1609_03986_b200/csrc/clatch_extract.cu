@@ -55,6 +55,8 @@ struct ExtractParams {
     unsigned long long* stats; // optional {triplets recomputed exactly, warps that took the exact pass}
     uint2* route;              // optional, host-mapped: per CTA {windows that took the exact pass, windows} of this launch
     cudaTextureObject_t tex;   // pipelined kernel: the u8 image as a gather-enabled CUDA array
+    cudaTextureObject_t texn;  // packed-plane kernel: the same array read as texel / 255 (cudaReadModeNormalizedFloat)
+    unsigned two23;            // packed-plane kernel: 0x4B000000, see ssd_estimate_h16_2
     const unsigned* out_index; // optional: descriptor of record j goes to row out_index[j] (quad / pipelined kernels)
     unsigned long long* trace; // optional (CLATCH_EX_TRACE=1): kExTrace globaltimer stamps per CTA of the default kernel
 };
@@ -893,6 +895,15 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_pipe_kernel(ExtractPa
 // extract_window / sample_bilinear compute them (the same code as the window-wide pass: sample_exact) into
 // `scratch` (147 doubles), lanes 0 and 1 run the two 49-term chains in the reference's row-major order, and the
 // descriptor word is patched in global memory (the estimate's guess was stored there by this CTA earlier).
+// Patch anchor (column, row) of a packed-plane slot offset (slot_assign.hpp: h16_offset).
+__device__ __forceinline__ void h16_anchor_dev(unsigned off, int& x, int& y) {
+    const int odd = off >= static_cast<unsigned>(kH16CopyWords);
+    const int r = static_cast<int>(off) - odd * kH16CopyWords;
+    y = r / kH16RowWords;
+    x = 2 * (r - y * kH16RowWords) - odd;
+}
+
+template <bool kH16>   // slot offsets: row * kWinStride + column (fp32 planes) or packed-plane word offsets
 __device__ __noinline__ void recompute_deferred_bit(cudaTextureObject_t tex, const double* xycs, uint8_t* out,
                                                     const unsigned* out_index, const DeferredBit item, double* scratch,
                                                     int lane) {
@@ -903,7 +914,15 @@ __device__ __noinline__ void recompute_deferred_bit(cudaTextureObject_t tex, con
     for (int i = lane; i < 3 * 49; i += 32) {
         const int patch = i / 49, pix = i - 49 * patch, r = pix / 7, cc = pix - 7 * r;
         const unsigned off = patch == 0 ? offs[0] : (patch == 1 ? offs[1] : offs[2]);
-        const int v = static_cast<int>(off / kWinStride) + r, u = static_cast<int>(off % kWinStride) + cc;
+        int v, u;
+        if (kH16) {
+            h16_anchor_dev(off, u, v);
+            v += r;
+            u += cc;
+        } else {
+            v = static_cast<int>(off / kWinStride) + r;
+            u = static_cast<int>(off % kWinStride) + cc;
+        }
         const double du = static_cast<double>(u) - 31.5, dv = static_cast<double>(v) - 31.5;
         const double xa = __dadd_rn(kx, __dmul_rn(c, du));
         const double ya = __dadd_rn(ky, __dmul_rn(sn, du));
@@ -1128,7 +1147,7 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
         const unsigned parked = *reinterpret_cast<volatile unsigned*>(s_qtail);
         double* const scratch = reinterpret_cast<double*>(s_f) + warp * 160;   // 147 doubles per warp
         for (unsigned i = warp; i < parked; i += kQuadThreads / 32) {
-            recompute_deferred_bit(p.tex, p.xycs, p.out, p.out_index, s_queue[i], scratch, lane);
+            recompute_deferred_bit<false>(p.tex, p.xycs, p.out, p.out_index, s_queue[i], scratch, lane);
             n_flagged += lane == 0;
         }
         if (trace && parked) trace[kExTrace - 1] = ex_global_ns() | static_cast<unsigned long long>(parked) << 48;
@@ -1142,6 +1161,337 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
     }
     // How many of this CTA's windows needed the exact pass: one plain 8-byte store into page-locked host memory per
     // CTA, read by the host before the NEXT launch of this context (extraction routing, launch_extract).
+    if (p.route != nullptr && !producer && rt == 0)
+        p.route[blockIdx.x] = make_uint2(n_windows, static_cast<unsigned>(nq > 0 ? nq * kQuad : 0));
+}
+
+// ---- packed 16-bit planes: extract_h16_kernel (variant 5) ------------------------------------------------------
+// The role-split pipeline above is bound by two things at once (profiles/r4a_extract_ncu.json): the shared-memory
+// pipe (3 431 wavefronts per descriptor, 80 % busy) and the issue slots (10 769 warp instructions per descriptor,
+// 67 %), half of which are the producers' unfused fp64 resampling. But the planes only feed the ESTIMATE — every bit
+// the estimate cannot prove is recomputed from the image by the exact code (recompute_deferred_bit, or the
+// window-wide pass below) — so nothing in them has to be the reference's value, only provably close to it:
+//   * a window is stored as 16-bit fixed point, A = round(65280 * b) with b the bilinear sample of the image scaled
+//     to [0, 1] (8.8 fixed point of the grey level), TWICE: copy E with sample (v, u) in halfword 66 v + u, copy O in
+//     halfword 66 v + u + 1. The 7 live pixels of a patch row starting at any column are then four aligned 32-bit
+//     words of one copy: 28 loads per patch instead of 49, half the bytes, no misaligned pairs.
+//   * the consumers unpack a halfword with one PRMT into the mantissa of 2^23 (0x4B00hhhh = 2^23 + A as a float):
+//     differences of two such floats are exact, and the packed FFMA2 sums of squares run as before.
+//   * the producers resample in fp32: sample coordinates in 7.25 fixed point (start value from the keypoint's
+//     fp64 record, one integer add per row step), footprints through a second texture object on the same array
+//     that returns texel / 255 as floats (no conversions), three fused lerps, one FFMA that rounds 65280 * b into
+//     the mantissa of 2^23. No fp64 pipe, no row tables, 24 instructions per sample instead of ~40.
+// Error budget, in units of the stored integers (1 = 2^-8 grey levels). Per stored sample, against the true
+// bilinear value: rounding to an integer 0.5; coordinates (start value rounded once, step rounded once and added
+// <= 7 times, fraction cut to 23 bits: <= 8 * 2^-25 px per axis, slope <= 1 per axis in [0,1] units), texel / 255 in
+// fp32 (<= 2 ulp) and six fp32 roundings in the lerps: <= 1e-6 * 65280 = 0.07. So |A - true| <= 0.6 and a
+// difference of two samples is off by at most eta = 1.2. Per chain, with d_f the fp32 sum:
+//   |65536 d_ref - d_f| <= 2 eta sum|e| + 49 eta^2      (sum|e| <= 7 sqrt(d) over the 49 terms)
+//                          + 52 * 2^-24 d_f              (49 fused accumulations; the differences are exact)
+//                          + 6e-15 d_f                   (the reference's own fp64 roundings)
+// The kernel tests |d1_f - d2_f| > 17.5 (sqrt d1_f + sqrt d2_f) + 3.3e-6 (d1_f + d2_f) + 150 (constants rounded up
+// >= 3 %): on noise images 5e-4 of the bits stay undecided (the fp32 planes: 2e-5) — a quarter of a bit per
+// descriptor, parked and recomputed exactly by whole warps after the pipeline has drained.
+constexpr int kHRow = kH16RowWords;                                  // 33 words per plane row
+constexpr int kHCopy = kH16CopyWords;                                // 2112 words: copy E, then copy O
+constexpr int kHPitch = 2 * kHCopy + 8;                              // words per window; % 32 == 8
+constexpr int kHRecDoubles = 8;                                      // per-window record, see stage_quad_h16
+constexpr int kH16PlaneBytes = 2 * kQuad * kHPitch * 4;              // [2][4] windows
+constexpr int kH16ExactBytes = kWindow * kWinStride * 8;             // one fp64 window for the window-wide exact pass
+constexpr int kH16SmemBytes = kH16PlaneBytes + kH16ExactBytes
+                              + 2 * kQuad * kPipeBits                // predicate bytes [2][4][512 + pad]
+                              + 2 * kQuad * kHRecDoubles * 8         // window records [2][4]
+                              + 64                                   // undecided-window masks, deferred-queue tail
+                              + kQueueCap * static_cast<int>(sizeof(DeferredBit));
+static_assert(kHPitch % 32 == 8 && kH16SmemBytes <= 227 * 1024, "packed-plane layout");
+
+// The exact chains as a call (rare path: keeps the pipelined loop's code small).
+__device__ __noinline__ bool triplet_bit_7x7_cold(const double* win, int oa, int ob, int oc, bool swapped) {
+    return triplet_bit_7x7(win, oa, ob, oc, swapped);
+}
+
+// fp32 estimate of both chains of two slots from the packed planes (component 0 = slot 0, 1 = slot 1).
+// kBig = 0x4B000000 (2^23: PRMT drops a halfword into its mantissa) arrives as a kernel PARAMETER: PRMT takes one
+// immediate, and when ptxas knows both the selector and this word it keeps the selector in a register that it
+// re-materialises with a MOV in front of every PRMT (measured: 380 extra instructions per pass).
+__device__ __forceinline__ void ssd_estimate_h16_2(const unsigned* win, const ushort4 s0, const ushort4 s1, const unsigned kBig,
+                                                   float& d1a, float& d2a, float& d1b, float& d2b) {
+    const unsigned* pa0 = win + s0.x;
+    const unsigned* pb0 = win + s0.y;
+    const unsigned* pc0 = win + s0.z;
+    const unsigned* pa1 = win + s1.x;
+    const unsigned* pb1 = win + s1.y;
+    const unsigned* pc1 = win + s1.z;
+    const float2 neg1 = make_float2(-1.0f, -1.0f);
+    float2 d1 = make_float2(0.0f, 0.0f), d2 = d1;
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int o = r * kHRow + k;
+            const unsigned wa0 = pa0[o], wa1 = pa1[o], wb0 = pb0[o], wb1 = pb1[o], wc0 = pc0[o], wc1 = pc1[o];
+#pragma unroll
+            for (int h = 0; h < (k < 3 ? 2 : 1); ++h) {
+                const unsigned sel = h ? 0x7632u : 0x7610u;
+                const float2 a = make_float2(__uint_as_float(__byte_perm(wa0, kBig, sel)), __uint_as_float(__byte_perm(wa1, kBig, sel)));
+                const float2 b = make_float2(__uint_as_float(__byte_perm(wb0, kBig, sel)), __uint_as_float(__byte_perm(wb1, kBig, sel)));
+                const float2 c = make_float2(__uint_as_float(__byte_perm(wc0, kBig, sel)), __uint_as_float(__byte_perm(wc1, kBig, sel)));
+                const float2 e1 = __ffma2_rn(b, neg1, a);   // exact: both are 2^23 + a 16-bit integer
+                const float2 e2 = __ffma2_rn(c, neg1, a);
+                d1 = __ffma2_rn(e1, e1, d1);
+                d2 = __ffma2_rn(e2, e2, d2);
+            }
+        }
+    }
+    d1a = d1.x;
+    d1b = d1.y;
+    d2a = d2.x;
+    d2b = d2.y;
+}
+
+// True when sign(d1 - d2) of the packed-plane estimate is provably the reference's (budget above).
+__device__ __forceinline__ bool estimate_decides_h16(float d1, float d2, float& diff) {
+    float r1, r2;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d1));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r2) : "f"(d2));
+    diff = d1 - d2;
+    const float bound = __fmaf_rn(17.5f, r1 + r2, __fmaf_rn(3.3e-6f, d1 + d2, 150.0f));
+    return fabsf(diff) > bound;
+}
+
+// Window records of the quad that starts at keypoint kp0, by threads 0..3 of the staging role: the keypoint
+// {x, y, cos, sin}, floor(x), floor(y) as doubles, then four ints — the texel coordinates of the footprint centre of
+// relative cell (0, 0) as floats-to-be {0x4B000000 + floor(x) + 1, 0x4B000000 + floor(y) + 1} and the per-row-step
+// increments of the 7.25 fixed-point sample coordinates {round(-sin * rows * 2^25), round(cos * rows * 2^25)}.
+// A keypoint past the end repeats the last one (its window is computed and never used).
+__device__ __forceinline__ void stage_quad_h16(const ExtractParams& p, unsigned long long kp0, double* rec, int rt, int rows) {
+    if (rt < kQuad) {
+        const unsigned long long kp = min(kp0 + rt, p.M - 1);
+        const double x = __ldg(p.xycs + 4 * kp + 0), y = __ldg(p.xycs + 4 * kp + 1);
+        const double c = __ldg(p.xycs + 4 * kp + 2), sn = __ldg(p.xycs + 4 * kp + 3);
+        int xi, yi;
+        double xid, yid;
+        floor_exact(x, xi, xid);
+        floor_exact(y, yi, yid);
+        double* const r = rec + kHRecDoubles * rt;
+        r[0] = x;
+        r[1] = y;
+        r[2] = c;
+        r[3] = sn;
+        r[4] = xid;
+        r[5] = yid;
+        const double step = static_cast<double>(rows) * 33554432.0;          // rows * 2^25
+        const double kRound = 6755399441055744.0;                             // 1.5 * 2^52: low word = round-to-nearest integer
+        const int dx = __double2loint(__dadd_rn(__dmul_rn(-sn, step), kRound));
+        const int dy = __double2loint(__dadd_rn(__dmul_rn(c, step), kRound));
+        reinterpret_cast<int4*>(r + 6)[0] = make_int4(0x4B000000 + xi + 1, 0x4B000000 + yi + 1, dx, dy);
+    }
+}
+
+template <int kRW>
+__global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractParams p) {
+    if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
+    constexpr int kSW = 32 - kRW, kRT = kRW * 32, kST = kSW * 32;
+    constexpr int kStep = 32 / kSW;                          // every kStep-th group of 4 warps consumes
+    constexpr int kRRows = kRT / kWindow;                    // producer thread -> rows v0 + kRRows * k
+    constexpr int kRPer = kWindow / kRRows;                  // samples per producer thread per window
+    constexpr int kSRows = kST / kWindow;                    // exact pass: consumer thread -> rows v0 + kSRows * k
+    constexpr int kSlots = 64 / kSW;                         // groups of 8 triplets per consumer warp
+    static_assert(32 % kSW == 0 && 64 % kSW == 0 && kSlots % 2 == 0 && kRT >= 512 && kWindow % kRRows == 0, "role split");
+
+    extern __shared__ __align__(16) uint8_t s_quad[];
+    unsigned* const s_h = reinterpret_cast<unsigned*>(s_quad);                                   // packed planes [2][4]
+    double* const s_exact = reinterpret_cast<double*>(s_quad + kH16PlaneBytes);                  // one fp64 window
+    uint8_t* const s_bits = s_quad + kH16PlaneBytes + kH16ExactBytes;                            // [2][4][512 + pad]
+    double* const s_rec = reinterpret_cast<double*>(s_bits + 2 * kQuad * kPipeBits);             // [2][4][8]
+    int* const s_mask = reinterpret_cast<int*>(s_rec + 2 * kQuad * kHRecDoubles);                // [2] windows needing the exact pass
+    unsigned* const s_qtail = reinterpret_cast<unsigned*>(s_mask + 2);                           // deferred bits queued so far
+    DeferredBit* const s_queue = reinterpret_cast<DeferredBit*>(s_mask + 16);                    // [kQueueCap]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, grp = warp >> 2;
+    const bool producer = grp % kStep != 0;
+    const int rw = (producer ? grp - grp / kStep - 1 : grp / kStep) * 4 + (warp & 3);   // role-local warp
+    const int rt = rw * 32 + lane;                                                       // role-local thread
+    const int u = rt & 63, v0 = rt >> 6;
+    const double du = static_cast<double>(u) - 31.5, dv0 = static_cast<double>(v0) - 31.5;
+    const int kb = lane & 3, ti = lane >> 2;
+    const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
+    const long long nq = blockIdx.x < quads ? static_cast<long long>((quads - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+    ushort4 slot[kSlots];
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) slot[j] = __ldg(p.slots + 8 * (rw % kSW + kSW * j) + ti);
+    unsigned n_flagged = 0, n_windows = 0;
+    unsigned long long* const trace = p.trace != nullptr && tid == 0 ? p.trace + static_cast<size_t>(kExTrace) * blockIdx.x : nullptr;
+    if (trace) trace[0] = ex_global_ns();
+    if (tid == 0) s_mask[0] = s_mask[1] = 0, *s_qtail = 0;
+    const bool defer_ok = p.M <= 0xffffffffull;
+    unsigned q_prev = 0;                 // queue tail after the previous quad (uniform over the consumers)
+    stage_quad_h16(p, static_cast<unsigned long long>(blockIdx.x) * kQuad, s_rec, tid, kRRows);
+    __syncthreads();
+    pdl_wait();   // launched early behind fill_array_kernel: the texture array is complete from here on
+    if (trace) trace[1] = ex_global_ns();
+
+    for (long long it = -1; it <= nq; ++it) {
+        const int cur = static_cast<int>(it & 1), nxt = cur ^ 1;
+        unsigned windows_before = n_windows;
+        if (!producer) {
+            if (it + 2 < nq)   // records for quad it+2 -> buffer [cur] (its last readers resampled quad `it`, an iteration ago)
+                stage_quad_h16(p, (blockIdx.x + (it + 2) * gridDim.x) * kQuad, s_rec + cur * kQuad * kHRecDoubles, rt, kRRows);
+            if (it >= 1) {   // pack the bits of the quad consumed in the previous iteration
+                const unsigned long long kp = (blockIdx.x + (it - 1) * gridDim.x) * kQuad + (rt >> 7);
+                const uint8_t* bits = s_bits + (nxt * kQuad + (rt >> 7)) * kPipeBits;
+                const int j = rt & 127;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const unsigned w32 = __ballot_sync(0xffffffffu, bits[128 * k + j] != 0);
+                    if (lane == 0 && kp < p.M) {
+                        const unsigned long long row = p.out_index ? p.out_index[kp] : kp;
+                        reinterpret_cast<unsigned*>(p.out + row * (kFastT / 8))[4 * k + (j >> 5)] = w32;
+                    }
+                }
+            }
+        }
+        if (producer) {
+            if (it + 1 < nq) {   // resample the next quad into the planes [nxt]
+                const double* const rec = s_rec + nxt * kQuad * kHRecDoubles;
+                constexpr int kDepth = 4, kTotal = kQuad * kRPer;
+                float pfx[kDepth], pfy[kDepth];
+                float4 pg[kDepth];
+                int X = 0, Y = 0, dX = 0, dY = 0, bx = 0, by = 0;
+                unsigned short* const hbase = reinterpret_cast<unsigned short*>(s_h + nxt * kQuad * kHPitch) + v0 * (2 * kHRow) + u;
+#pragma unroll
+                for (int i = 0; i < kTotal + kDepth; ++i) {
+                    if (i >= kDepth) {
+                        const int j = i - kDepth, sl = j % kDepth;
+                        const float4 g = pg[sl];   // w = (x0,y0), z = (x0+1,y0), x = (x0,y0+1), y = (x0+1,y0+1), each texel / 255
+                        const float top = __fmaf_rn(pfx[sl], g.z - g.w, g.w);
+                        const float bot = __fmaf_rn(pfx[sl], g.y - g.x, g.x);
+                        const float val = __fmaf_rn(pfy[sl], bot - top, top);
+                        const unsigned short q = static_cast<unsigned short>(__float_as_uint(__fmaf_rn(val, 65280.0f, 8388608.0f)));
+                        unsigned short* const dst = hbase + (j / kRPer) * (2 * kHPitch) + (j % kRPer) * kRRows * (2 * kHRow);
+                        dst[0] = q;                      // copy E: halfword 66 v + u
+                        dst[2 * kHCopy + 1] = q;         // copy O: halfword 66 v + u + 1
+                    }
+                    if (i < kTotal) {
+                        const int w = i / kRPer, sl = i % kDepth;
+                        if (i % kRPer == 0) {
+                            const double* const r = rec + kHRecDoubles * w;
+                            const double c = r[2], sn = r[3];
+                            const double sx0 = __dsub_rn(__dadd_rn(r[0], __dmul_rn(c, du)), __dmul_rn(sn, dv0));
+                            const double sy0 = __dadd_rn(__dadd_rn(r[1], __dmul_rn(sn, du)), __dmul_rn(c, dv0));
+                            // (s - floor) * 2^25 rounded to an integer: the ulp at 1.5 * 2^27 is 2^-25
+                            X = __double2loint(__dadd_rn(__dsub_rn(sx0, r[4]), 201326592.0));
+                            Y = __double2loint(__dadd_rn(__dsub_rn(sy0, r[5]), 201326592.0));
+                            const int4 k4 = reinterpret_cast<const int4*>(r + 6)[0];
+                            bx = k4.x;
+                            by = k4.y;
+                            dX = k4.z;
+                            dY = k4.w;
+                        } else {
+                            X += dX;
+                            Y += dY;
+                        }
+                        const float tx = __int_as_float(bx + (X >> 25)) - 8388608.0f;   // floor + 1: the footprint's centre
+                        const float ty = __int_as_float(by + (Y >> 25)) - 8388608.0f;
+                        pfx[sl] = __int_as_float(((X >> 2) & 0x7fffff) | 0x3f800000) - 1.0f;
+                        pfy[sl] = __int_as_float(((Y >> 2) & 0x7fffff) | 0x3f800000) - 1.0f;
+                        pg[sl] = tex2Dgather<float4>(p.texn, tx, ty, 0);
+                    }
+                }
+            }
+        } else if (it >= 0 && it < nq) {
+            const unsigned long long kp0 = (blockIdx.x + it * gridDim.x) * kQuad;
+            const unsigned* const my_win = s_h + (cur * kQuad + kb) * kHPitch;
+            const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves an unused window
+            if (rt == 0) s_mask[nxt] = 0;
+            uint8_t* const my_bits = s_bits + (cur * kQuad + kb) * kPipeBits;
+            unsigned need = 0;
+#pragma unroll
+            for (int j = 0; j < kSlots; j += 2) {
+                float d1a, d2a, d1b, d2b, diff0, diff1;
+                ssd_estimate_h16_2(my_win, slot[j], slot[j + 1], p.two23, d1a, d2a, d1b, d2b);
+                const bool sure0 = estimate_decides_h16(d1a, d2a, diff0);
+                const bool sure1 = estimate_decides_h16(d1b, d2b, diff1);
+                need |= (live && !sure0 ? 1u << j : 0u) | (live && !sure1 ? 2u << j : 0u);
+                my_bits[slot[j].w & 0x7fff] = (slot[j].w >> 15) ? diff0 < 0.0f : diff0 > 0.0f;
+                my_bits[slot[j + 1].w & 0x7fff] = (slot[j + 1].w >> 15) ? diff1 < 0.0f : diff1 > 0.0f;
+            }
+            if (need) {
+                atomicOr(s_mask + cur, 1 << kb);
+                if (defer_ok) {
+#pragma unroll
+                    for (int j = 0; j < kSlots; ++j)
+                        if ((need >> j) & 1) {
+                            const unsigned at = atomicAdd(s_qtail, 1u);
+                            if (at < kQueueCap) s_queue[at] = DeferredBit{slot[j], static_cast<unsigned>(kp0 + kb)};
+                        }
+                }
+            }
+            asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
+            const int mask = *reinterpret_cast<volatile int*>(s_mask + cur);
+            bool window_pass = mask != 0;
+            if (mask && defer_ok) {
+                const unsigned tail = *reinterpret_cast<volatile unsigned*>(s_qtail);
+                if (tail <= kQueueCap && tail - q_prev <= kDeferMax) {   // few: they stay parked
+                    q_prev = tail;
+                    window_pass = false;
+                }
+            }
+            if (window_pass) {   // uniform over the consumers: dense undecided bits (flat / saturated footprints)
+                for (int w = 0; w < kQuad; ++w) {
+                    if (!((mask >> w) & 1)) continue;
+                    // the consumers resample window w exactly (fp64, the reference's operation order) ...
+                    const double* kpr = p.xycs + 4 * (kp0 + w);
+                    const double c = __ldg(kpr + 2), sn = __ldg(kpr + 3);
+                    const double xa = __dadd_rn(__ldg(kpr + 0), __dmul_rn(c, du));
+                    const double ya = __dadd_rn(__ldg(kpr + 1), __dmul_rn(sn, du));
+#pragma unroll 2
+                    for (int v = v0; v < kWindow; v += kSRows) {
+                        const double dv = static_cast<double>(v) - 31.5;
+                        s_exact[v * kWinStride + u] = sample_exact(p.tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv));
+                    }
+                    n_windows += rt == 0;
+                    asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
+                    // ... and the lanes of that window run the exact chains of their undecided triplets
+                    if (kb == w) {
+#pragma unroll
+                        for (int j = 0; j < kSlots; ++j)
+                            if ((need >> j) & 1) {
+                                int ax, ay, bxx, byy, cx, cy;
+                                h16_anchor_dev(slot[j].x, ax, ay);
+                                h16_anchor_dev(slot[j].y, bxx, byy);
+                                h16_anchor_dev(slot[j].z, cx, cy);
+                                my_bits[slot[j].w & 0x7fff] = triplet_bit_7x7_cold(s_exact, ay * kWinStride + ax, byy * kWinStride + bxx,
+                                                                                   cy * kWinStride + cx, slot[j].w >> 15);
+                                ++n_flagged;
+                            }
+                    }
+                    asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");   // the next window overwrites the scratch
+                }
+                if (rt == 0) *s_qtail = q_prev;   // this quad's parked items are withdrawn (every consumer has read the tail)
+            }
+        }
+        __syncthreads();
+        if (trace && it + 3 < kExTrace)
+            trace[it + 3] = ex_global_ns() | (n_windows != windows_before ? 1ull << 63 : 0ull);
+    }
+    // The pipeline has drained: all 32 warps take the parked bits, the plane memory serves as their scratch.
+    {
+        const unsigned parked = *reinterpret_cast<volatile unsigned*>(s_qtail);
+        double* const scratch = reinterpret_cast<double*>(s_h) + warp * 160;   // 147 doubles per warp
+        for (unsigned i = warp; i < parked; i += kQuadThreads / 32) {
+            recompute_deferred_bit<true>(p.tex, p.xycs, p.out, p.out_index, s_queue[i], scratch, lane);
+            n_flagged += lane == 0;
+        }
+        if (trace && parked) trace[kExTrace - 1] = ex_global_ns() | static_cast<unsigned long long>(parked) << 48;
+    }
+    if (p.stats != nullptr) {
+        n_flagged = __reduce_add_sync(0xffffffffu, n_flagged);
+        if (lane == 0 && (n_flagged | n_windows)) {
+            atomicAdd(p.stats + 0, static_cast<unsigned long long>(n_flagged));
+            atomicAdd(p.stats + 1, static_cast<unsigned long long>(n_windows));
+        }
+    }
     if (p.route != nullptr && !producer && rt == 0)
         p.route[blockIdx.x] = make_uint2(n_windows, static_cast<unsigned>(nq > 0 ? nq * kQuad : 0));
 }
@@ -1270,9 +1620,11 @@ int tex_image_for(clatch_ctx* ctx, cudaStream_t stream, int width, int height, c
         if (ti->tex) {
             CLATCH_CUDA(cudaStreamSynchronize(stream));   // a kernel may still be sampling the old array
             cudaDestroyTextureObject(ti->tex);
+            cudaDestroyTextureObject(ti->texn);
             cudaDestroySurfaceObject(ti->surf);
             cudaFreeArray(ti->array);
             ti->tex = 0;
+            ti->texn = 0;
             ti->surf = 0;
             ti->array = nullptr;
             ti->width = ti->height = 0;
@@ -1288,6 +1640,8 @@ int tex_image_for(clatch_ctx* ctx, cudaStream_t stream, int width, int height, c
         td.readMode = cudaReadModeElementType;
         td.normalizedCoords = 0;
         CLATCH_CUDA(cudaCreateTextureObject(&ti->tex, &rd, &td, nullptr));
+        td.readMode = cudaReadModeNormalizedFloat;   // the packed-plane kernel's resampler: texel / 255 as a float
+        CLATCH_CUDA(cudaCreateTextureObject(&ti->texn, &rd, &td, nullptr));
         CLATCH_CUDA(cudaCreateSurfaceObject(&ti->surf, &rd));
         ti->width = width;
         ti->height = height;
@@ -1399,7 +1753,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     // exact pass (ExtractParams::route, a host-mapped slot per CTA); when the previous launch of this context saw
     // more than 35 % the next ones run the quad kernel, and every 16th launch probes with the default kernel again.
     bool quad_routed = false;
-    const bool routing = kU8 && pat.fast && ctx->extract_variant == 4 && ctx->extract_route && !ctx->extract_stats_on &&
+    const bool routing = kU8 && pat.fast && ctx->extract_variant >= 4 && ctx->extract_route && !ctx->extract_stats_on &&
                          flags == nullptr && ctx->route_host != nullptr && !force_generic;
     if (routing) {
         if (ctx->route_pending) {   // fold the last probe's slots (its kernel may still be running: then they read 0 / stale, harmless)
@@ -1436,6 +1790,8 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
                                              kPipeSmemBytes));
             CLATCH_CUDA(cudaFuncSetAttribute(extract_roles_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kRolesSmemBytes));
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_h16_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kH16SmemBytes));
             ctx->pipe_configured = true;
         }
         // The resampler reads footprints through the texture unit: copy the image into this
@@ -1450,7 +1806,9 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
             ++ctx->launches;
         }
         p.tex = ti->tex;
-        p.slots = pat.slots_f8.as<ushort4>();
+        p.texn = ti->texn;
+        p.two23 = 0x4B000000u;
+        p.slots = ctx->extract_variant == 5 ? pat.slots_h16.as<ushort4>() : pat.slots_f8.as<ushort4>();
         const size_t quads = (M + kQuad - 1) / kQuad;
         const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
         // variant 4 (default): dedicated producer / consumer warps, 16 + 16 — 60.1 vs 58.1 M desc/s at 10 k
@@ -1465,12 +1823,14 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         }
         static const bool tracing = std::getenv("CLATCH_EX_TRACE") != nullptr;
         unsigned long long* d_trace = nullptr;
-        if (tracing && ctx->extract_variant == 4) {   // diagnostics: per-CTA timeline of the launch (synchronises)
+        if (tracing && ctx->extract_variant >= 4) {   // diagnostics: per-CTA timeline of the launch (synchronises)
             CLATCH_CUDA(cudaMalloc(&d_trace, sizeof(unsigned long long) * kExTrace * grid));
             CLATCH_CUDA(cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long) * kExTrace * grid, stream));
             p.trace = d_trace;
         }
-        if (ctx->extract_variant == 4)   // may start (tables, first keypoint rows) while fill_array_kernel is still writing
+        if (ctx->extract_variant == 5)   // packed 16-bit planes, fp32 resampling
+            CLATCH_CUDA(launch_kernel(extract_h16_kernel<16>, dim3(grid), dim3(kQuadThreads), kH16SmemBytes, stream, ctx->pdl, 1, p));
+        else if (ctx->extract_variant == 4)   // may start (tables, first keypoint rows) while fill_array_kernel is still writing
             CLATCH_CUDA(launch_kernel(extract_roles_kernel<16>, dim3(grid), dim3(kQuadThreads), kRolesSmemBytes, stream, ctx->pdl, 1, p));
         else extract_pipe_kernel<<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
         if (d_trace) {
@@ -1519,7 +1879,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
 // Scattered output rows (ExtractParams::out_index) are implemented by the kernels that the banded
 // float64 upload can reach: the pipelined kernel (u8-valued image) and the quad kernel (any other).
 bool extract_supports_out_index(const clatch_ctx* ctx) {
-    return ctx->pattern.fast && (ctx->extract_variant == 3 || ctx->extract_variant == 4);
+    return ctx->pattern.fast && ctx->extract_variant >= 3;
 }
 
 int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,

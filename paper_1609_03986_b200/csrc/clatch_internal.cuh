@@ -57,6 +57,7 @@ struct Pattern {
     DeviceBuffer slots;            // T * ushort4 (single-window kernel: half-warps of 16 triplets)
     DeviceBuffer slots_quad;       // T * ushort4 (quad kernel: half-warps of 4 triplets x 4 keypoints)
     DeviceBuffer slots_f8;         // T * ushort4 (filtered kernel: warps of 8 triplets x 4 keypoints)
+    DeviceBuffer slots_h16;        // T * ushort4 (packed-plane kernel: the same lanes, word offsets into the 16-bit copies)
     std::vector<int16_t> host_triplets;   // T * 6, for plans made on first use
     bool slots_planned = false;    // `slots` holds a plan for the current table
     DeviceBuffer triplets;         // generic kernel: T * 6 int16
@@ -66,6 +67,7 @@ struct Pattern {
     double slot_degree_identity = 0.0;
     double slot_degree_quad = 0.0;
     double slot_degree_f8 = 0.0;
+    double slot_degree_h16 = 0.0;
 };
 
 } // namespace clatch
@@ -88,6 +90,7 @@ struct clatch_ctx {
         cudaStream_t stream = nullptr;
         cudaArray_t array = nullptr;
         cudaTextureObject_t tex = 0;
+        cudaTextureObject_t texn = 0;    // the same array, texels read as value / 255 (packed-plane kernel)
         cudaSurfaceObject_t surf = 0;    // the same array, for the fill kernel
         int width = 0, height = 0;
     };

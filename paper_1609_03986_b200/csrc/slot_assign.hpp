@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 namespace clatch {
@@ -163,13 +164,43 @@ inline SlotPlan plan_slots(const int16_t* triplets, int T, int stride, int itera
 // the three loads — far weaker than distinct residues across the whole domain. What remains
 // is the histogram imbalance of the table (a residue class holding more than T/mod anchors
 // forces a collision somewhere): degree 1.07 for (4,4), 1.14 for (8,8) on the built-in table.
+// Packed 16-bit planes (extract_h16_kernel): a window is stored twice as 16-bit samples, row stride 33 words —
+// copy E holds sample (v, u) in halfword 66 v + u, copy O (kH16CopyWords further on) in halfword 66 v + u + 1 — so
+// the 7 live pixels of a patch row that starts at ANY column are four aligned 32-bit words of one of the copies.
+// A patch anchored at column x, row y is addressed by the word offset of its first pair.
+constexpr int kH16RowWords = 33, kH16CopyWords = 64 * kH16RowWords;
+inline uint16_t h16_offset(int x, int y) {
+    return static_cast<uint16_t>((x & 1) * kH16CopyWords + y * kH16RowWords + ((x + 1) >> 1));
+}
+// ... and back: word offset -> (column, row) of the patch anchor.
+inline void h16_anchor(unsigned off, int& x, int& y) {
+    const int odd = off >= static_cast<unsigned>(kH16CopyWords);
+    const int r = static_cast<int>(off) - odd * kH16CopyWords;
+    y = r / kH16RowWords;
+    x = 2 * (r % kH16RowWords) - odd;
+}
+
+inline SlotPlan plan_slots_grouped_off(std::vector<uint16_t> off, int T, int group, int mod, int iterations);
+
 inline SlotPlan plan_slots_grouped(const int16_t* triplets, int T, int stride, int group, int mod,
                                    int iterations) {
-    const int G = T / group;
     std::vector<uint16_t> off(3 * T);
     for (int t = 0; t < T; ++t)
         for (int k = 0; k < 3; ++k)
             off[3 * t + k] = static_cast<uint16_t>(triplets[6 * t + 2 * k + 1] * stride + triplets[6 * t + 2 * k]);
+    return plan_slots_grouped_off(std::move(off), T, group, mod, iterations);
+}
+
+// The packed-plane layout: 8 triplets x 4 windows per warp, window w displaced by 8 w banks (as the filtered kernel).
+inline SlotPlan plan_slots_h16(const int16_t* triplets, int T, int iterations) {
+    std::vector<uint16_t> off(3 * T);
+    for (int t = 0; t < T; ++t)
+        for (int k = 0; k < 3; ++k) off[3 * t + k] = h16_offset(triplets[6 * t + 2 * k], triplets[6 * t + 2 * k + 1]);
+    return plan_slots_grouped_off(std::move(off), T, 8, 8, iterations);
+}
+
+inline SlotPlan plan_slots_grouped_off(std::vector<uint16_t> off, int T, int group, int mod, int iterations) {
+    const int G = T / group;
     std::vector<int> order(T);
     std::vector<uint8_t> flip(T, 0);
     for (int t = 0; t < T; ++t) order[t] = t;

@@ -453,7 +453,7 @@ def test_tensor_matcher_partitions_agree(lk, port, shape):
     assert np.array_equal(res[1][:, rows].T, port.knn2_all(query[rows], train))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
 def test_every_extraction_variant_is_exact(lk, port, variant):
     """All specialised extraction kernels (one window per CTA / four fp64 windows per CTA / four
     split windows with the fp32 filter / the producer-consumer pipeline over the texture unit)
@@ -474,7 +474,7 @@ def test_every_extraction_variant_is_exact(lk, port, variant):
         eng.set_option("extract_variant", 4)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
 def test_trained_pattern_on_every_fast_kernel(lk, port, variant):
     """A trained pattern has the built-in shape (T=512, K=8, 7x7-of-8x8 mask) but other triplets:
     it takes the specialised kernels with a lane placement planned at clatch_set_pattern time
@@ -505,7 +505,7 @@ def test_trained_pattern_on_every_fast_kernel(lk, port, variant):
         lk.describe(port.random_image_u8(88, 300, 200), port.random_keypoints(90, 300, 200, 4))   # built-in table back
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
 def test_smallest_images_and_odd_pitches(lk, port, variant):
     """93x93 is the smallest image with a describable keypoint (46, 46); widths that are not
     multiples of 16 take the unaligned staging / array-fill paths when the image arrives as a
@@ -558,7 +558,7 @@ def _near_tie_images(w, h):
     return out
 
 
-@pytest.mark.parametrize("variant", [2, 3, 4])
+@pytest.mark.parametrize("variant", [2, 3, 4, 5])
 def test_filtered_kernel_on_near_ties(lk, port, variant):
     """The filtered and pipelined kernels decide a bit from fp32 sums only when a rigorous error bound
     separates them; everything else is recomputed in exact fp64. Flat regions, periodic
@@ -579,7 +579,7 @@ def test_filtered_kernel_on_near_ties(lk, port, variant):
     eng.set_option("extract_variant", 4)
 
 
-@pytest.mark.parametrize("variant", [2, 3, 4])
+@pytest.mark.parametrize("variant", [2, 3, 4, 5])
 def test_filtered_kernel_exact_pass_rate(lk, port, variant):
     """Diagnostics counters: on noise the exact pass is rare (that is where the speed comes
     from), on a flat image every triplet takes it (that is where the exactness comes from)."""
@@ -592,7 +592,7 @@ def test_filtered_kernel_exact_pass_rate(lk, port, variant):
         noise = port.random_image_u8(1609, w, h)
         m = len(lk.describe(noise, kps)[1])
         exact, _ = eng.extract_stats()
-        assert exact < 1e-3 * m * 512, exact
+        assert exact < (3e-3 if variant == 5 else 1e-3) * m * 512, exact   # 16-bit planes: a looser bound, ~6e-4
         eng.set_option("extract_stats", 1)       # re-arm: zeroes the counters
         lk.describe(np.full((h, w), 31, np.uint8), kps)
         exact, passes = eng.extract_stats()      # passes: warps (variant 2) / windows re-resampled (3)

@@ -27,14 +27,14 @@ images = {
     "half saturated": np.where(xx < w // 2, 255, img).astype(np.uint8),
     "flat": np.full((h, w), 99, np.uint8),
 }
-for variant in (4, 40, 3, 2, 1):          # 40 = variant 4 with the degenerate-image router switched off
+for variant in (5, 4, 40, 3, 2, 1):          # 40 = variant 4 with the degenerate-image router switched off
     eng.set_option("extract_variant", 4 if variant == 40 else variant)
     eng.set_option("extract_route", 0 if variant == 40 else 1)
     for name, im in images.items():
         eng.set_option("extract_stats", 1)
         m = len(lk.describe(im, kps)[1])
         exact, passes = eng.extract_stats() if variant >= 2 else (0, 0)
-        if variant == 4:
+        if variant in (4, 5):
             eng.set_option("extract_route", 1)      # (resets the router's state between image kinds)
         unit = "windows re-resampled" if variant >= 3 else "warp passes"
         eng.set_option("extract_stats", 0)
