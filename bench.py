@@ -56,9 +56,18 @@ SMEM_BYTES_PER_DESC = 512 * 49 * 3 * 8                     # 8-byte window reads
 # the SSD phase reads 4-byte planes and runs fp32 FMAs; fp64 is left with the window resampling.
 FILT_FP64_OPS_PER_DESC = 4096 * 15                         # resampling only
 FILT_SMEM_BYTES_PER_DESC = 512 * 49 * 3 * 4                # 4-byte F-plane reads
+# variants 5 / 6: the planes hold 16-bit samples in two shifted copies; a 7-pixel patch row is four aligned 32-bit words,
+# and the resampling runs in fp32 (fp64 only sets up each thread's start coordinates, 12 ops per thread and window).
+H16_SMEM_BYTES_PER_DESC = 512 * 7 * 4 * 3 * 4              # 28 word loads per patch
+H16_FP64_OPS_PER_DESC = 512 * 12 + 64
+# ... and what binds them is the issue rate (ncu: issue slots 70 % busy, shared-memory pipe 59 %, ALU pipe 52 %). Algorithmic
+# warp instructions per descriptor: estimate = 256 slot pairs x 49 pixels x (6 unpacks + 4 packed FMAs + 6 * 28/49 loads) / 32
+# lanes = 5 264; resampling = 4 096 samples x 23.5 (coordinates 10, gather 1, three lerps 6, round 1, pack + stores 2.5,
+# steps 3) / 32 = 3 008. Peak: one warp instruction per clock and scheduler, 4 schedulers per SM.
+H16_WARP_INSTR_PER_DESC = 5264 + 3008
 INT8_OPS_PER_COMPARE = 1024                                # 512 int8 MACs
 EXTRACT_KERNELS = {0: "extract_fast_kernel<u8>", 1: "extract_quad_kernel<u8>", 2: "extract_filt_kernel",
-                   3: "extract_pipe_kernel", 4: "extract_roles_kernel<16>"}
+                   3: "extract_pipe_kernel", 4: "extract_roles_kernel<16>", 5: "extract_h16_kernel<16>", 6: "extract_h16s_kernel"}
 # committed ncu --set full captures (tools/summarize_ncu.py), newest visit first; `traffic` is read from these files
 NCU_PROFILES = {"extract": ("r*_extract_ncu.json", "extract_"), "match": ("r*_match_tc_ncu.json", "match_tc")}
 
@@ -351,7 +360,7 @@ class Ctx:
         self.flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=self.dev)     # > 126 MB L2
         self.peaks = load_peaks()
         self.mv = args.match_variant if args.match_variant is not None else 4
-        self.ev = args.extract_variant if args.extract_variant is not None else 4
+        self.ev = args.extract_variant if args.extract_variant is not None else 5
 
     def flush(self):
         self.flush_buf.zero_()
@@ -427,18 +436,41 @@ class Ctx:
         pipes = self.peaks.get("pipes", {})
         sms = self.eng.sm_count
         filt = self.ev >= 2
-        smem_bytes = FILT_SMEM_BYTES_PER_DESC if filt else SMEM_BYTES_PER_DESC
-        fp64_ops = FILT_FP64_OPS_PER_DESC if filt else FP64_OPS_PER_DESC
+        h16 = self.ev >= 5
+        smem_bytes = H16_SMEM_BYTES_PER_DESC if h16 else FILT_SMEM_BYTES_PER_DESC if filt else SMEM_BYTES_PER_DESC
+        fp64_ops = H16_FP64_OPS_PER_DESC if h16 else FILT_FP64_OPS_PER_DESC if filt else FP64_OPS_PER_DESC
         smem_gbs = descriptors * smem_bytes / seconds / 1e9
         fp64_gops = descriptors * fp64_ops / seconds / 1e9
         smem_peak = pipes.get("lds64_gbs", sms * 128 * sm_mhz * 1e6 / 1e9)
         fp64_peak = pipes.get("fp64_nonfused_gops", sms * 64 * sm_mhz * 1e6 / 1e9)
         traffic, src = ncu_traffic("extract", EXTRACT_KERNELS[self.ev])
+        smem = {"bound": "smem", "achieved": smem_gbs, "peak": smem_peak, "unit": "GB/s", "frac": smem_gbs / smem_peak,
+                "algorithmic_bytes_per_descriptor": smem_bytes}
+        if h16:
+            issue_peak = sms * 4 * sm_mhz * 1e6 / 1e9                       # G warp-instructions / s
+            issue = descriptors * H16_WARP_INSTR_PER_DESC / seconds / 1e9
+            return {
+                "kernel": EXTRACT_KERNELS[self.ev], "bound": "issue", "achieved": issue, "peak": issue_peak,
+                "unit": "G warp-instr/s", "frac": issue / issue_peak,
+                "what": f"instruction issue: {H16_WARP_INSTR_PER_DESC} algorithmic warp instructions per descriptor (estimate 5264: "
+                        "256 slot pairs x 49 pixels x (6 PRMT unpacks + 4 FFMA2 + 3.43 LDS) / 32; resampling 3008: 4096 samples x "
+                        "23.5 / 32) x descriptors per launch / kernel time. ncu on this kernel: issue slots 70 % busy, "
+                        "shared-memory pipe 59 %, ALU pipe 52 % — the issue rate binds, not a data path",
+                "peak_source": f"{sms} SMs x 4 schedulers x 1 warp instruction / clk at the sampled {sm_mhz:.0f} MHz",
+                "traffic": traffic, "traffic_source": src, "smem": smem,
+                "fp64": {"achieved_gops": fp64_gops, "peak_gops": fp64_peak, "frac": fp64_gops / fp64_peak},
+                "hbm": {"bound": "hbm", "achieved": hbm_bytes / seconds / 1e9, "peak": self.peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": hbm_bytes / seconds / 1e9 / self.peaks["hbm_gbs"], "algorithmic_bytes": hbm_bytes,
+                        "peak_source": self.peaks["source"],
+                        "note": "contract form (image + keypoint records + descriptors once); HBM does not bind this kernel"},
+            }
         return {
             "kernel": EXTRACT_KERNELS[self.ev], "bound": "smem", "achieved": smem_gbs, "peak": smem_peak, "unit": "GB/s",
             "frac": smem_gbs / smem_peak,
-            "what": f"shared-memory wavefronts: {smem_bytes} B of {4 if filt else 8}-byte window reads per descriptor "
-                    "(512 triplets x 49 live pixels x 3 patches) x descriptors per launch / kernel time",
+            "what": (f"shared-memory wavefronts: {smem_bytes} B of 4-byte plane reads per descriptor (512 triplets x 3 patches x "
+                     "7 rows x 4 aligned words of packed 16-bit samples) x descriptors per launch / kernel time") if h16 else
+                    (f"shared-memory wavefronts: {smem_bytes} B of {4 if filt else 8}-byte window reads per descriptor "
+                     "(512 triplets x 49 live pixels x 3 patches) x descriptors per launch / kernel time"),
             "peak_source": ("measured microbench: conflict-free 64-bit shared loads, tools/pipe_peaks.cu -> "
                             "profiles/pipe_peaks.json") if pipes else
                            f"theoretical: {sms} SMs x 128 B/clk at the sampled {sm_mhz:.0f} MHz",

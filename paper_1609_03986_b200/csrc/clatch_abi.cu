@@ -291,6 +291,10 @@ int clatch_ctx_create(int device, clatch_ctx** out) {
         return cuda_fail(se, "cudaStreamCreateWithFlags");
     }
     if (const char* v = std::getenv("CLATCH_MATCH_VARIANT")) ctx->match_variant = std::atoi(v);
+    if (const char* v = std::getenv("CLATCH_EXTRACT_VARIANT")) {
+        const int ev = std::atoi(v);
+        if (ev >= 0 && ev <= 6) ctx->extract_variant = ev;
+    }
     // per-CTA slots of the extraction router, written by the device into page-locked host memory (no copy, no sync)
     if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->route_host), sizeof(uint2) * ctx->sm_count, cudaHostAllocMapped) == cudaSuccess) {
         std::memset(ctx->route_host, 0, sizeof(uint2) * ctx->sm_count);
@@ -366,7 +370,7 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         return CLATCH_OK;
     }
     if (std::strcmp(key, "extract_variant") == 0) {
-        if (value < 0 || value > 5) return invalid("extract_variant must be 0..5");
+        if (value < 0 || value > 6) return invalid("extract_variant must be 0..6");
         ctx->extract_variant = value;
         ctx->route_quad = ctx->route_pending = false;
         ctx->route_age = 0;

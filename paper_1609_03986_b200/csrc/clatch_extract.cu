@@ -57,6 +57,7 @@ struct ExtractParams {
     cudaTextureObject_t tex;   // pipelined kernel: the u8 image as a gather-enabled CUDA array
     cudaTextureObject_t texn;  // packed-plane kernel: the same array read as texel / 255 (cudaReadModeNormalizedFloat)
     unsigned two23;            // packed-plane kernel: 0x4B000000, see ssd_estimate_h16_2
+    int dbg;                   // diagnostics (CLATCH_EX_DEBUG): 1 = skip the estimate, 2 = skip the resampling (timing only, wrong bits)
     const unsigned* out_index; // optional: descriptor of record j goes to row out_index[j] (quad / pipelined kernels)
     unsigned long long* trace; // optional (CLATCH_EX_TRACE=1): kExTrace globaltimer stamps per CTA of the default kernel
 };
@@ -910,8 +911,13 @@ __device__ __noinline__ void recompute_deferred_bit(cudaTextureObject_t tex, con
     const double* const kpr = xycs + 4 * static_cast<unsigned long long>(item.kp);
     const double kx = __ldg(kpr + 0), ky = __ldg(kpr + 1), c = __ldg(kpr + 2), sn = __ldg(kpr + 3);
     const unsigned offs[3] = {item.slot.x, item.slot.y, item.slot.z};
-#pragma unroll 1
-    for (int i = lane; i < 3 * 49; i += 32) {
+    // Five rounds of 32 samples: all footprints are requested before the first one is blended (issued one by one, each
+    // gather's ~700 clk of latency — nothing else runs on the SM at this point — was paid five times in a row).
+    double pfx[5], pfy[5];
+    uint4 pg[5];
+#pragma unroll
+    for (int round = 0; round < 5; ++round) {
+        const int i = min(lane + 32 * round, 3 * 49 - 1);
         const int patch = i / 49, pix = i - 49 * patch, r = pix / 7, cc = pix - 7 * r;
         const unsigned off = patch == 0 ? offs[0] : (patch == 1 ? offs[1] : offs[2]);
         int v, u;
@@ -924,9 +930,22 @@ __device__ __noinline__ void recompute_deferred_bit(cudaTextureObject_t tex, con
             u = static_cast<int>(off % kWinStride) + cc;
         }
         const double du = static_cast<double>(u) - 31.5, dv = static_cast<double>(v) - 31.5;
-        const double xa = __dadd_rn(kx, __dmul_rn(c, du));
-        const double ya = __dadd_rn(ky, __dmul_rn(sn, du));
-        scratch[i] = sample_exact(tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv));
+        const double sx = __dsub_rn(__dadd_rn(kx, __dmul_rn(c, du)), __dmul_rn(sn, dv));   // as sample_exact
+        const double sy = __dadd_rn(__dadd_rn(ky, __dmul_rn(sn, du)), __dmul_rn(c, dv));
+        int x0, y0;
+        double x0f, y0f;
+        floor_exact(sx, x0, x0f);
+        floor_exact(sy, y0, y0f);
+        pfx[round] = __dsub_rn(sx, x0f);
+        pfy[round] = __dsub_rn(sy, y0f);
+        pg[round] = footprint(tex, x0, y0);
+    }
+#pragma unroll
+    for (int round = 0; round < 5; ++round) {
+        const int i = lane + 32 * round;
+        const uint4 g = pg[round];
+        const double val = blend(pfx[round], pfy[round], u8_to_f64(g.w), u8_to_f64(g.z), u8_to_f64(g.x), u8_to_f64(g.y));
+        if (i < 3 * 49) scratch[i] = val;
     }
     __syncwarp();
     double d = 0.0;
@@ -1165,7 +1184,7 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
         p.route[blockIdx.x] = make_uint2(n_windows, static_cast<unsigned>(nq > 0 ? nq * kQuad : 0));
 }
 
-// ---- packed 16-bit planes: extract_h16_kernel (variant 5) ------------------------------------------------------
+// ---- packed 16-bit planes: extract_h16_kernel (variant 5), extract_h16s_kernel (variant 6) ---------------------
 // The role-split pipeline above is bound by two things at once (profiles/r4a_extract_ncu.json): the shared-memory
 // pipe (3 431 wavefronts per descriptor, 80 % busy) and the issue slots (10 769 warp instructions per descriptor,
 // 67 %), half of which are the producers' unfused fp64 resampling. But the planes only feed the ESTIMATE — every bit
@@ -1175,27 +1194,32 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
 //     to [0, 1] (8.8 fixed point of the grey level), TWICE: copy E with sample (v, u) in halfword 66 v + u, copy O in
 //     halfword 66 v + u + 1. The 7 live pixels of a patch row starting at any column are then four aligned 32-bit
 //     words of one copy: 28 loads per patch instead of 49, half the bytes, no misaligned pairs.
-//   * the consumers unpack a halfword with one PRMT into the mantissa of 2^23 (0x4B00hhhh = 2^23 + A as a float):
+//   * the estimate unpacks a halfword with one PRMT into the mantissa of 2^23 (0x4B00hhhh = 2^23 + A as a float):
 //     differences of two such floats are exact, and the packed FFMA2 sums of squares run as before.
-//   * the producers resample in fp32: sample coordinates in 7.25 fixed point (start value from the keypoint's
-//     fp64 record, one integer add per row step), footprints through a second texture object on the same array
-//     that returns texel / 255 as floats (no conversions), three fused lerps, one FFMA that rounds 65280 * b into
-//     the mantissa of 2^23. No fp64 pipe, no row tables, 24 instructions per sample instead of ~40.
+//   * the resampler works in fp32: sample coordinates in 9.23 fixed point (start value from the keypoint's fp64
+//     record, one integer add per row step), footprints through a second texture object on the same array that
+//     returns texel / 255 as floats (no conversions), three fused lerps, one FFMA that rounds 65280 * b into the
+//     mantissa of 2^23. No fp64 pipe, no row tables, ~24 instructions per sample instead of ~40. A lane owns the
+//     column pair (2 lane, 2 lane + 1) of a row, so the two samples leave as ONE 32-bit word of copy E and — with
+//     the first sample of the next lane (one shuffle) — one word of copy O (16-bit stores of two lanes into one
+//     word are 2-way bank conflicts: measured).
 // Error budget, in units of the stored integers (1 = 2^-8 grey levels). Per stored sample, against the true
-// bilinear value: rounding to an integer 0.5; coordinates (start value rounded once, step rounded once and added
-// <= 7 times, fraction cut to 23 bits: <= 8 * 2^-25 px per axis, slope <= 1 per axis in [0,1] units), texel / 255 in
-// fp32 (<= 2 ulp) and six fp32 roundings in the lerps: <= 1e-6 * 65280 = 0.07. So |A - true| <= 0.6 and a
-// difference of two samples is off by at most eta = 1.2. Per chain, with d_f the fp32 sum:
+// bilinear value: rounding to an integer 0.5; coordinates (start value rounded once, column step once, row step
+// rounded once and added <= 15 times: <= 8.5 * 2^-23 px per axis, slope <= 1 per axis in [0,1] units: 2.0e-6),
+// texel / 255 in fp32 (<= 2^-23) and six fp32 roundings in the lerps (3.6e-7): <= 2.5e-6 * 65280 = 0.16. So
+// |A - true| <= 0.66 and a difference of two samples is off by at most eta = 1.32. Per chain, d_f the fp32 sum:
 //   |65536 d_ref - d_f| <= 2 eta sum|e| + 49 eta^2      (sum|e| <= 7 sqrt(d) over the 49 terms)
 //                          + 52 * 2^-24 d_f              (49 fused accumulations; the differences are exact)
 //                          + 6e-15 d_f                   (the reference's own fp64 roundings)
-// The kernel tests |d1_f - d2_f| > 17.5 (sqrt d1_f + sqrt d2_f) + 3.3e-6 (d1_f + d2_f) + 150 (constants rounded up
-// >= 3 %): on noise images 5e-4 of the bits stay undecided (the fp32 planes: 2e-5) — a quarter of a bit per
-// descriptor, parked and recomputed exactly by whole warps after the pipeline has drained.
+// The kernels test |d1_f - d2_f| > 19.1 (sqrt d1_f + sqrt d2_f) + 3.3e-6 (d1_f + d2_f) + 180 (constants rounded up
+// >= 3 %): on noise images 9e-4 of the bits stay undecided (the fp32 planes: 2e-5) — half a bit per descriptor,
+// parked and recomputed exactly by whole warps after the pipeline has drained.
+// Schedules: variant 5 keeps dedicated producer / consumer warps (16 + 16), variant 6 lets every warp do both
+// halves of an iteration, half of the warps of each SM sub-partition in one order and half in the other.
 constexpr int kHRow = kH16RowWords;                                  // 33 words per plane row
 constexpr int kHCopy = kH16CopyWords;                                // 2112 words: copy E, then copy O
 constexpr int kHPitch = 2 * kHCopy + 8;                              // words per window; % 32 == 8
-constexpr int kHRecDoubles = 8;                                      // per-window record, see stage_quad_h16
+constexpr int kHRecDoubles = 10;                                     // per-window record, see stage_quad_h16
 constexpr int kH16PlaneBytes = 2 * kQuad * kHPitch * 4;              // [2][4] windows
 constexpr int kH16ExactBytes = kWindow * kWinStride * 8;             // one fp64 window for the window-wide exact pass
 constexpr int kH16SmemBytes = kH16PlaneBytes + kH16ExactBytes
@@ -1208,6 +1232,15 @@ static_assert(kHPitch % 32 == 8 && kH16SmemBytes <= 227 * 1024, "packed-plane la
 // The exact chains as a call (rare path: keeps the pipelined loop's code small).
 __device__ __noinline__ bool triplet_bit_7x7_cold(const double* win, int oa, int ob, int oc, bool swapped) {
     return triplet_bit_7x7(win, oa, ob, oc, swapped);
+}
+
+// The exact bit of a packed-plane slot from an fp64 window (stride kWinStride).
+__device__ __forceinline__ bool h16_exact_bit(const double* win, const ushort4 s) {
+    int ax, ay, bx, by, cx, cy;
+    h16_anchor_dev(s.x, ax, ay);
+    h16_anchor_dev(s.y, bx, by);
+    h16_anchor_dev(s.z, cx, cy);
+    return triplet_bit_7x7_cold(win, ay * kWinStride + ax, by * kWinStride + bx, cy * kWinStride + cx, s.w >> 15);
 }
 
 // fp32 estimate of both chains of two slots from the packed planes (component 0 = slot 0, 1 = slot 1).
@@ -1255,55 +1288,135 @@ __device__ __forceinline__ bool estimate_decides_h16(float d1, float d2, float& 
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d1));
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r2) : "f"(d2));
     diff = d1 - d2;
-    const float bound = __fmaf_rn(17.5f, r1 + r2, __fmaf_rn(3.3e-6f, d1 + d2, 150.0f));
+    const float bound = __fmaf_rn(19.1f, r1 + r2, __fmaf_rn(3.3e-6f, d1 + d2, 180.0f));
     return fabsf(diff) > bound;
 }
 
-// Window records of the quad that starts at keypoint kp0, by threads 0..3 of the staging role: the keypoint
-// {x, y, cos, sin}, floor(x), floor(y) as doubles, then four ints — the texel coordinates of the footprint centre of
-// relative cell (0, 0) as floats-to-be {0x4B000000 + floor(x) + 1, 0x4B000000 + floor(y) + 1} and the per-row-step
-// increments of the 7.25 fixed-point sample coordinates {round(-sin * rows * 2^25), round(cos * rows * 2^25)}.
+// Window records of the quad that starts at keypoint kp0, by threads 0..3 of whoever stages: the keypoint
+// {x, y, cos, sin}, floor(x), floor(y) as doubles, then eight ints — the texel coordinates of the footprint centre of
+// relative cell (0, 0) as floats-to-be {0x4B000000 + floor(x) + 1, 0x4B000000 + floor(y) + 1}, the per-row-step
+// increments of the 9.23 fixed-point sample coordinates {round(-sin * rows * 2^23), round(cos * rows * 2^23)} and the
+// column step {round(cos * 2^23), round(sin * 2^23)} to the second sample of a lane's pair.
 // A keypoint past the end repeats the last one (its window is computed and never used).
-__device__ __forceinline__ void stage_quad_h16(const ExtractParams& p, unsigned long long kp0, double* rec, int rt, int rows) {
-    if (rt < kQuad) {
-        const unsigned long long kp = min(kp0 + rt, p.M - 1);
-        const double x = __ldg(p.xycs + 4 * kp + 0), y = __ldg(p.xycs + 4 * kp + 1);
-        const double c = __ldg(p.xycs + 4 * kp + 2), sn = __ldg(p.xycs + 4 * kp + 3);
-        int xi, yi;
-        double xid, yid;
-        floor_exact(x, xi, xid);
-        floor_exact(y, yi, yid);
-        double* const r = rec + kHRecDoubles * rt;
-        r[0] = x;
-        r[1] = y;
-        r[2] = c;
-        r[3] = sn;
-        r[4] = xid;
-        r[5] = yid;
-        const double step = static_cast<double>(rows) * 33554432.0;          // rows * 2^25
-        const double kRound = 6755399441055744.0;                             // 1.5 * 2^52: low word = round-to-nearest integer
-        const int dx = __double2loint(__dadd_rn(__dmul_rn(-sn, step), kRound));
-        const int dy = __double2loint(__dadd_rn(__dmul_rn(c, step), kRound));
-        reinterpret_cast<int4*>(r + 6)[0] = make_int4(0x4B000000 + xi + 1, 0x4B000000 + yi + 1, dx, dy);
+struct H16Kp {
+    double x, y, c, sn;
+};
+__device__ __forceinline__ H16Kp h16_kp_load(const ExtractParams& p, unsigned long long kp0, int t) {
+    const unsigned long long kp = min(kp0 + t, p.M - 1);
+    return H16Kp{__ldg(p.xycs + 4 * kp + 0), __ldg(p.xycs + 4 * kp + 1), __ldg(p.xycs + 4 * kp + 2), __ldg(p.xycs + 4 * kp + 3)};
+}
+__device__ __forceinline__ void h16_rec_store(const H16Kp k, double* rec, int t, int rows) {
+    int xi, yi;
+    double xid, yid;
+    floor_exact(k.x, xi, xid);
+    floor_exact(k.y, yi, yid);
+    double* const r = rec + kHRecDoubles * t;
+    r[0] = k.x;
+    r[1] = k.y;
+    r[2] = k.c;
+    r[3] = k.sn;
+    r[4] = xid;
+    r[5] = yid;
+    const double one = 8388608.0, step = static_cast<double>(rows) * one;   // 2^23, rows * 2^23
+    const double kRound = 6755399441055744.0;                                // 1.5 * 2^52: low word = nearest integer
+    int* const ri = reinterpret_cast<int*>(r + 6);
+    ri[0] = 0x4B000000 + xi + 1;
+    ri[1] = 0x4B000000 + yi + 1;
+    ri[2] = __double2loint(__dadd_rn(__dmul_rn(-k.sn, step), kRound));
+    ri[3] = __double2loint(__dadd_rn(__dmul_rn(k.c, step), kRound));
+    ri[4] = __double2loint(__dadd_rn(__dmul_rn(k.c, one), kRound));
+    ri[5] = __double2loint(__dadd_rn(__dmul_rn(k.sn, one), kRound));
+    ri[6] = ri[7] = 0;
+}
+// (Split in two so that the global loads can be issued before an iteration's work and the record written after it:
+// done in one piece at the top of an iteration, the ~1 us of load latency sat on the staging warp's critical path.)
+__device__ __forceinline__ void stage_quad_h16(const ExtractParams& p, unsigned long long kp0, double* rec, int t, int rows) {
+    if (t < kQuad) h16_rec_store(h16_kp_load(p, kp0, t), rec, t, rows);
+}
+
+// One thread's share of a quad's resampling: window record `rec`, that window's planes, column pair (2 lane, 2 lane + 1),
+// rows v0 + kRows * k. Four gathers stay in flight.
+template <int kRows>
+__device__ __forceinline__ void h16_resample_pairs(cudaTextureObject_t texn, const double* rec, unsigned* plane, int lane, int v0) {
+    constexpr int kPer = kWindow / kRows, kTotal = 2 * kPer, kDepth = 4;
+    const double du = static_cast<double>(2 * lane) - 31.5, dv0 = static_cast<double>(v0) - 31.5;
+    const double c = rec[2], sn = rec[3];
+    const double sx0 = __dsub_rn(__dadd_rn(rec[0], __dmul_rn(c, du)), __dmul_rn(sn, dv0));
+    const double sy0 = __dadd_rn(__dadd_rn(rec[1], __dmul_rn(sn, du)), __dmul_rn(c, dv0));
+    const int4 k4 = reinterpret_cast<const int4*>(rec + 6)[0];
+    const int2 k2 = reinterpret_cast<const int2*>(rec + 8)[0];
+    // (s - floor) * 2^23 rounded to an integer: the ulp at 1.5 * 2^29 is 2^-23
+    int Xa = __double2loint(__dadd_rn(__dsub_rn(sx0, rec[4]), 805306368.0));
+    int Ya = __double2loint(__dadd_rn(__dsub_rn(sy0, rec[5]), 805306368.0));
+    int Xb = Xa + k2.x, Yb = Ya + k2.y;
+    float pfx[kDepth], pfy[kDepth];
+    float4 pg[kDepth];
+    unsigned qa = 0;
+    unsigned* const ebase = plane + v0 * kHRow + lane;
+#pragma unroll
+    for (int i = 0; i < kTotal + kDepth; ++i) {
+        if (i >= kDepth) {
+            const int j = i - kDepth, sl = j % kDepth;
+            const float4 g = pg[sl];   // w = (x0,y0), z = (x0+1,y0), x = (x0,y0+1), y = (x0+1,y0+1), each texel / 255
+            const float top = __fmaf_rn(pfx[sl], g.z - g.w, g.w);
+            const float bot = __fmaf_rn(pfx[sl], g.y - g.x, g.x);
+            const float val = __fmaf_rn(pfy[sl], bot - top, top);
+            const unsigned q = __float_as_uint(__fmaf_rn(val, 65280.0f, 8388608.0f));   // low half: round(65280 * val)
+            if (j % 2 == 0) {
+                qa = q;
+            } else {
+                const unsigned next = __shfl_down_sync(0xffffffffu, qa, 1);   // sample 2 lane + 2 (lane 31: a word nobody reads)
+                unsigned* const dst = ebase + (j / 2) * kRows * kHRow;
+                dst[0] = __byte_perm(qa, q, 0x5410);                          // copy E: samples (2 lane, 2 lane + 1)
+                dst[kHCopy + 1] = __byte_perm(q, next, 0x5410);               // copy O: samples (2 lane + 1, 2 lane + 2)
+            }
+        }
+        if (i < kTotal) {
+            const int sl = i % kDepth;
+            const int X = i % 2 ? Xb : Xa, Y = i % 2 ? Yb : Ya;
+            const float tx = __int_as_float(k4.x + (X >> 23)) - 8388608.0f;   // floor + 1: the footprint's centre
+            const float ty = __int_as_float(k4.y + (Y >> 23)) - 8388608.0f;
+            pfx[sl] = __int_as_float((X & 0x7fffff) | 0x3f800000) - 1.0f;
+            pfy[sl] = __int_as_float((Y & 0x7fffff) | 0x3f800000) - 1.0f;
+            pg[sl] = tex2Dgather<float4>(texn, tx, ty, 0);
+            if (i % 2) {
+                Xa += k4.z;
+                Ya += k4.w;
+                Xb += k4.z;
+                Yb += k4.w;
+            }
+        }
+    }
+}
+
+// Pack 512 predicate bytes of one window (two ballots per thread of a 256-thread group) into the descriptor row.
+__device__ __forceinline__ void h16_pack_bits(const ExtractParams& p, const uint8_t* bits, unsigned long long kp, int j, int lane) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const unsigned w32 = __ballot_sync(0xffffffffu, bits[256 * k + j] != 0);
+        if (lane == 0 && kp < p.M) {
+            const unsigned long long row = p.out_index ? p.out_index[kp] : kp;
+            reinterpret_cast<unsigned*>(p.out + row * (kFastT / 8))[8 * k + (j >> 5)] = w32;
+        }
     }
 }
 
 template <int kRW>
 __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractParams p) {
     if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
-    constexpr int kSW = 32 - kRW, kRT = kRW * 32, kST = kSW * 32;
+    constexpr int kSW = 32 - kRW, kST = kSW * 32;
     constexpr int kStep = 32 / kSW;                          // every kStep-th group of 4 warps consumes
-    constexpr int kRRows = kRT / kWindow;                    // producer thread -> rows v0 + kRRows * k
-    constexpr int kRPer = kWindow / kRRows;                  // samples per producer thread per window
+    constexpr int kRRows = kRW / kQuad;                      // a producer warp owns rows v0 + kRRows * k of one window
     constexpr int kSRows = kST / kWindow;                    // exact pass: consumer thread -> rows v0 + kSRows * k
     constexpr int kSlots = 64 / kSW;                         // groups of 8 triplets per consumer warp
-    static_assert(32 % kSW == 0 && 64 % kSW == 0 && kSlots % 2 == 0 && kRT >= 512 && kWindow % kRRows == 0, "role split");
+    static_assert(32 % kSW == 0 && 64 % kSW == 0 && kSlots % 2 == 0 && kRW % kQuad == 0 && kWindow % kRRows == 0 && kST == 512,
+                  "role split");
 
     extern __shared__ __align__(16) uint8_t s_quad[];
     unsigned* const s_h = reinterpret_cast<unsigned*>(s_quad);                                   // packed planes [2][4]
     double* const s_exact = reinterpret_cast<double*>(s_quad + kH16PlaneBytes);                  // one fp64 window
     uint8_t* const s_bits = s_quad + kH16PlaneBytes + kH16ExactBytes;                            // [2][4][512 + pad]
-    double* const s_rec = reinterpret_cast<double*>(s_bits + 2 * kQuad * kPipeBits);             // [2][4][8]
+    double* const s_rec = reinterpret_cast<double*>(s_bits + 2 * kQuad * kPipeBits);             // [2][4][10]
     int* const s_mask = reinterpret_cast<int*>(s_rec + 2 * kQuad * kHRecDoubles);                // [2] windows needing the exact pass
     unsigned* const s_qtail = reinterpret_cast<unsigned*>(s_mask + 2);                           // deferred bits queued so far
     DeferredBit* const s_queue = reinterpret_cast<DeferredBit*>(s_mask + 16);                    // [kQueueCap]
@@ -1312,11 +1425,12 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
     const bool producer = grp % kStep != 0;
     const int rw = (producer ? grp - grp / kStep - 1 : grp / kStep) * 4 + (warp & 3);   // role-local warp
     const int rt = rw * 32 + lane;                                                       // role-local thread
-    const int u = rt & 63, v0 = rt >> 6;
-    const double du = static_cast<double>(u) - 31.5, dv0 = static_cast<double>(v0) - 31.5;
+    const int u = rt & 63, v0 = rt >> 6;                     // window-wide exact pass (consumers)
+    const double du = static_cast<double>(u) - 31.5;
     const int kb = lane & 3, ti = lane >> 2;
     const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
-    const long long nq = blockIdx.x < quads ? static_cast<long long>((quads - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+    const int nq = blockIdx.x < quads ? static_cast<int>((quads - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+    const unsigned long long kp_step = static_cast<unsigned long long>(gridDim.x) * kQuad;
     ushort4 slot[kSlots];
 #pragma unroll
     for (int j = 0; j < kSlots; ++j) slot[j] = __ldg(p.slots + 8 * (rw % kSW + kSW * j) + ti);
@@ -1324,23 +1438,33 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
     unsigned long long* const trace = p.trace != nullptr && tid == 0 ? p.trace + static_cast<size_t>(kExTrace) * blockIdx.x : nullptr;
     if (trace) trace[0] = ex_global_ns();
     if (tid == 0) s_mask[0] = s_mask[1] = 0, *s_qtail = 0;
+    // Sparse undecided bits are parked ({slot, keypoint} in a shared-memory queue) and recomputed exactly by whole warps
+    // after the pipeline has drained; a quad with more than kDeferMax of them (flat or saturated footprints), or a full
+    // queue, takes the window-wide exact pass instead. See extract_roles_kernel.
     const bool defer_ok = p.M <= 0xffffffffull;
     unsigned q_prev = 0;                 // queue tail after the previous quad (uniform over the consumers)
+    unsigned long long kp0 = static_cast<unsigned long long>(blockIdx.x) * kQuad - kp_step;   // first keypoint of quad `it`
     stage_quad_h16(p, static_cast<unsigned long long>(blockIdx.x) * kQuad, s_rec, tid, kRRows);
     __syncthreads();
     pdl_wait();   // launched early behind fill_array_kernel: the texture array is complete from here on
     if (trace) trace[1] = ex_global_ns();
 
-    for (long long it = -1; it <= nq; ++it) {
-        const int cur = static_cast<int>(it & 1), nxt = cur ^ 1;
-        unsigned windows_before = n_windows;
-        if (!producer) {
-            if (it + 2 < nq)   // records for quad it+2 -> buffer [cur] (its last readers resampled quad `it`, an iteration ago)
-                stage_quad_h16(p, (blockIdx.x + (it + 2) * gridDim.x) * kQuad, s_rec + cur * kQuad * kHRecDoubles, rt, kRRows);
-            if (it >= 1) {   // pack the bits of the quad consumed in the previous iteration
-                const unsigned long long kp = (blockIdx.x + (it - 1) * gridDim.x) * kQuad + (rt >> 7);
-                const uint8_t* bits = s_bits + (nxt * kQuad + (rt >> 7)) * kPipeBits;
-                const int j = rt & 127;
+    for (int it = -1; it <= nq; ++it, kp0 += kp_step) {
+        const int cur = it & 1, nxt = cur ^ 1;
+        const unsigned windows_before = n_windows;
+        if (producer) {
+            if (it + 1 < nq && !(p.dbg & 2))   // resample the next quad into the planes [nxt]: this warp's window, its rows
+                h16_resample_pairs<kRRows>(p.texn, s_rec + (nxt * kQuad + rw / kRRows) * kHRecDoubles,
+                                           s_h + (nxt * kQuad + rw / kRRows) * kHPitch, lane, rw % kRRows);
+        } else {
+            // The consumers also stage the window records two quads ahead (buffer [quad & 1]; its last readers resampled
+            // quad `it`, an iteration ago) and pack the previous quad's bits. (Staging from the producers, loads before the
+            // resampling and the record after it, measured slower: eight more live registers across the resampler spill.)
+            if (it + 2 < nq) stage_quad_h16(p, kp0 + 2 * kp_step, s_rec + cur * kQuad * kHRecDoubles, rt, kRRows);
+            if (it >= 1) {
+                const int w = rt >> 7, j = rt & 127;
+                const uint8_t* bits = s_bits + (nxt * kQuad + w) * kPipeBits;
+                const unsigned long long kp = kp0 - kp_step + w;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const unsigned w32 = __ballot_sync(0xffffffffu, bits[128 * k + j] != 0);
@@ -1350,125 +1474,71 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
                     }
                 }
             }
-        }
-        if (producer) {
-            if (it + 1 < nq) {   // resample the next quad into the planes [nxt]
-                const double* const rec = s_rec + nxt * kQuad * kHRecDoubles;
-                constexpr int kDepth = 4, kTotal = kQuad * kRPer;
-                float pfx[kDepth], pfy[kDepth];
-                float4 pg[kDepth];
-                int X = 0, Y = 0, dX = 0, dY = 0, bx = 0, by = 0;
-                unsigned short* const hbase = reinterpret_cast<unsigned short*>(s_h + nxt * kQuad * kHPitch) + v0 * (2 * kHRow) + u;
+            if (it >= 0 && it < nq) {
+                const unsigned* const my_win = s_h + (cur * kQuad + kb) * kHPitch;
+                const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves an unused window
+                if (rt == 0) s_mask[nxt] = 0;
+                uint8_t* const my_bits = s_bits + (cur * kQuad + kb) * kPipeBits;
+                unsigned need = 0;
 #pragma unroll
-                for (int i = 0; i < kTotal + kDepth; ++i) {
-                    if (i >= kDepth) {
-                        const int j = i - kDepth, sl = j % kDepth;
-                        const float4 g = pg[sl];   // w = (x0,y0), z = (x0+1,y0), x = (x0,y0+1), y = (x0+1,y0+1), each texel / 255
-                        const float top = __fmaf_rn(pfx[sl], g.z - g.w, g.w);
-                        const float bot = __fmaf_rn(pfx[sl], g.y - g.x, g.x);
-                        const float val = __fmaf_rn(pfy[sl], bot - top, top);
-                        const unsigned short q = static_cast<unsigned short>(__float_as_uint(__fmaf_rn(val, 65280.0f, 8388608.0f)));
-                        unsigned short* const dst = hbase + (j / kRPer) * (2 * kHPitch) + (j % kRPer) * kRRows * (2 * kHRow);
-                        dst[0] = q;                      // copy E: halfword 66 v + u
-                        dst[2 * kHCopy + 1] = q;         // copy O: halfword 66 v + u + 1
-                    }
-                    if (i < kTotal) {
-                        const int w = i / kRPer, sl = i % kDepth;
-                        if (i % kRPer == 0) {
-                            const double* const r = rec + kHRecDoubles * w;
-                            const double c = r[2], sn = r[3];
-                            const double sx0 = __dsub_rn(__dadd_rn(r[0], __dmul_rn(c, du)), __dmul_rn(sn, dv0));
-                            const double sy0 = __dadd_rn(__dadd_rn(r[1], __dmul_rn(sn, du)), __dmul_rn(c, dv0));
-                            // (s - floor) * 2^25 rounded to an integer: the ulp at 1.5 * 2^27 is 2^-25
-                            X = __double2loint(__dadd_rn(__dsub_rn(sx0, r[4]), 201326592.0));
-                            Y = __double2loint(__dadd_rn(__dsub_rn(sy0, r[5]), 201326592.0));
-                            const int4 k4 = reinterpret_cast<const int4*>(r + 6)[0];
-                            bx = k4.x;
-                            by = k4.y;
-                            dX = k4.z;
-                            dY = k4.w;
-                        } else {
-                            X += dX;
-                            Y += dY;
-                        }
-                        const float tx = __int_as_float(bx + (X >> 25)) - 8388608.0f;   // floor + 1: the footprint's centre
-                        const float ty = __int_as_float(by + (Y >> 25)) - 8388608.0f;
-                        pfx[sl] = __int_as_float(((X >> 2) & 0x7fffff) | 0x3f800000) - 1.0f;
-                        pfy[sl] = __int_as_float(((Y >> 2) & 0x7fffff) | 0x3f800000) - 1.0f;
-                        pg[sl] = tex2Dgather<float4>(p.texn, tx, ty, 0);
-                    }
+                for (int j = 0; j < kSlots; j += 2) {
+                    float d1a = 1.f, d2a = 2e9f, d1b = 1.f, d2b = 2e9f, diff0, diff1;
+                    if (!(p.dbg & 1)) ssd_estimate_h16_2(my_win, slot[j], slot[j + 1], p.two23, d1a, d2a, d1b, d2b);
+                    const bool sure0 = estimate_decides_h16(d1a, d2a, diff0);
+                    const bool sure1 = estimate_decides_h16(d1b, d2b, diff1);
+                    need |= (live && !sure0 ? 1u << j : 0u) | (live && !sure1 ? 2u << j : 0u);
+                    my_bits[slot[j].w & 0x7fff] = (slot[j].w >> 15) ? diff0 < 0.0f : diff0 > 0.0f;
+                    my_bits[slot[j + 1].w & 0x7fff] = (slot[j + 1].w >> 15) ? diff1 < 0.0f : diff1 > 0.0f;
                 }
-            }
-        } else if (it >= 0 && it < nq) {
-            const unsigned long long kp0 = (blockIdx.x + it * gridDim.x) * kQuad;
-            const unsigned* const my_win = s_h + (cur * kQuad + kb) * kHPitch;
-            const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves an unused window
-            if (rt == 0) s_mask[nxt] = 0;
-            uint8_t* const my_bits = s_bits + (cur * kQuad + kb) * kPipeBits;
-            unsigned need = 0;
-#pragma unroll
-            for (int j = 0; j < kSlots; j += 2) {
-                float d1a, d2a, d1b, d2b, diff0, diff1;
-                ssd_estimate_h16_2(my_win, slot[j], slot[j + 1], p.two23, d1a, d2a, d1b, d2b);
-                const bool sure0 = estimate_decides_h16(d1a, d2a, diff0);
-                const bool sure1 = estimate_decides_h16(d1b, d2b, diff1);
-                need |= (live && !sure0 ? 1u << j : 0u) | (live && !sure1 ? 2u << j : 0u);
-                my_bits[slot[j].w & 0x7fff] = (slot[j].w >> 15) ? diff0 < 0.0f : diff0 > 0.0f;
-                my_bits[slot[j + 1].w & 0x7fff] = (slot[j + 1].w >> 15) ? diff1 < 0.0f : diff1 > 0.0f;
-            }
-            if (need) {
-                atomicOr(s_mask + cur, 1 << kb);
-                if (defer_ok) {
-#pragma unroll
-                    for (int j = 0; j < kSlots; ++j)
-                        if ((need >> j) & 1) {
-                            const unsigned at = atomicAdd(s_qtail, 1u);
-                            if (at < kQueueCap) s_queue[at] = DeferredBit{slot[j], static_cast<unsigned>(kp0 + kb)};
-                        }
-                }
-            }
-            asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
-            const int mask = *reinterpret_cast<volatile int*>(s_mask + cur);
-            bool window_pass = mask != 0;
-            if (mask && defer_ok) {
-                const unsigned tail = *reinterpret_cast<volatile unsigned*>(s_qtail);
-                if (tail <= kQueueCap && tail - q_prev <= kDeferMax) {   // few: they stay parked
-                    q_prev = tail;
-                    window_pass = false;
-                }
-            }
-            if (window_pass) {   // uniform over the consumers: dense undecided bits (flat / saturated footprints)
-                for (int w = 0; w < kQuad; ++w) {
-                    if (!((mask >> w) & 1)) continue;
-                    // the consumers resample window w exactly (fp64, the reference's operation order) ...
-                    const double* kpr = p.xycs + 4 * (kp0 + w);
-                    const double c = __ldg(kpr + 2), sn = __ldg(kpr + 3);
-                    const double xa = __dadd_rn(__ldg(kpr + 0), __dmul_rn(c, du));
-                    const double ya = __dadd_rn(__ldg(kpr + 1), __dmul_rn(sn, du));
-#pragma unroll 2
-                    for (int v = v0; v < kWindow; v += kSRows) {
-                        const double dv = static_cast<double>(v) - 31.5;
-                        s_exact[v * kWinStride + u] = sample_exact(p.tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv));
-                    }
-                    n_windows += rt == 0;
-                    asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
-                    // ... and the lanes of that window run the exact chains of their undecided triplets
-                    if (kb == w) {
+                if (need) {
+                    atomicOr(s_mask + cur, 1 << kb);
+                    if (defer_ok) {
 #pragma unroll
                         for (int j = 0; j < kSlots; ++j)
                             if ((need >> j) & 1) {
-                                int ax, ay, bxx, byy, cx, cy;
-                                h16_anchor_dev(slot[j].x, ax, ay);
-                                h16_anchor_dev(slot[j].y, bxx, byy);
-                                h16_anchor_dev(slot[j].z, cx, cy);
-                                my_bits[slot[j].w & 0x7fff] = triplet_bit_7x7_cold(s_exact, ay * kWinStride + ax, byy * kWinStride + bxx,
-                                                                                   cy * kWinStride + cx, slot[j].w >> 15);
-                                ++n_flagged;
+                                const unsigned at = atomicAdd(s_qtail, 1u);
+                                if (at < kQueueCap) s_queue[at] = DeferredBit{slot[j], static_cast<unsigned>(kp0 + kb)};
                             }
                     }
-                    asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");   // the next window overwrites the scratch
                 }
-                if (rt == 0) *s_qtail = q_prev;   // this quad's parked items are withdrawn (every consumer has read the tail)
+                asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
+                const int mask = *reinterpret_cast<volatile int*>(s_mask + cur);
+                bool window_pass = mask != 0;
+                if (mask && defer_ok) {
+                    const unsigned tail = *reinterpret_cast<volatile unsigned*>(s_qtail);
+                    if (tail <= kQueueCap && tail - q_prev <= kDeferMax) {   // few: they stay parked
+                        q_prev = tail;
+                        window_pass = false;
+                    }
+                }
+                if (window_pass) {   // uniform over the consumers: dense undecided bits (flat / saturated footprints)
+                    for (int w = 0; w < kQuad; ++w) {
+                        if (!((mask >> w) & 1)) continue;
+                        // the consumers resample window w exactly (fp64, the reference's operation order) ...
+                        const double* kpr = p.xycs + 4 * (kp0 + w);
+                        const double c = __ldg(kpr + 2), sn = __ldg(kpr + 3);
+                        const double xa = __dadd_rn(__ldg(kpr + 0), __dmul_rn(c, du));
+                        const double ya = __dadd_rn(__ldg(kpr + 1), __dmul_rn(sn, du));
+#pragma unroll 2
+                        for (int v = v0; v < kWindow; v += kSRows) {
+                            const double dv = static_cast<double>(v) - 31.5;
+                            s_exact[v * kWinStride + u] = sample_exact(p.tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv));
+                        }
+                        n_windows += rt == 0;
+                        asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
+                        if (rt == 0) *s_qtail = q_prev;   // this quad's parked items are withdrawn (every consumer has read the tail)
+                        // ... and the lanes of that window run the exact chains of their undecided triplets
+                        if (kb == w) {
+#pragma unroll
+                            for (int j = 0; j < kSlots; ++j)
+                                if ((need >> j) & 1) {
+                                    my_bits[slot[j].w & 0x7fff] = h16_exact_bit(s_exact, slot[j]);
+                                    ++n_flagged;
+                                }
+                        }
+                        asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");   // the next window overwrites the scratch
+                    }
+                }
             }
         }
         __syncthreads();
@@ -1493,6 +1563,158 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
         }
     }
     if (p.route != nullptr && !producer && rt == 0)
+        p.route[blockIdx.x] = make_uint2(n_windows, static_cast<unsigned>(nq > 0 ? nq * kQuad : 0));
+}
+
+__global__ void __launch_bounds__(kQuadThreads, 1) extract_h16s_kernel(ExtractParams p) {
+    if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
+    constexpr int kRows = kQuadThreads / 32 / kQuad;         // 8: a warp owns rows v0 + 8k of one window
+
+    extern __shared__ __align__(16) uint8_t s_quad[];
+    unsigned* const s_h = reinterpret_cast<unsigned*>(s_quad);                                   // packed planes [2][4]
+    double* const s_exact = reinterpret_cast<double*>(s_quad + kH16PlaneBytes);                  // one fp64 window
+    uint8_t* const s_bits = s_quad + kH16PlaneBytes + kH16ExactBytes;                            // [2][4][512 + pad]
+    double* const s_rec = reinterpret_cast<double*>(s_bits + 2 * kQuad * kPipeBits);             // [2][4][10]
+    int* const s_mask = reinterpret_cast<int*>(s_rec + 2 * kQuad * kHRecDoubles);                // [3] windows needing the exact pass
+    unsigned* const s_qtail = reinterpret_cast<unsigned*>(s_mask + 3);                           // deferred bits queued so far
+    DeferredBit* const s_queue = reinterpret_cast<DeferredBit*>(s_mask + 16);                    // [kQueueCap]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool ssd_first = (warp >> 2) & 1;                  // per sub-partition: 4 warps each way
+    const int rwin = warp >> 3, rv0 = warp & 7;              // resampling: window of the quad, first row
+    const int u = tid & 63, v0 = tid >> 6;                   // window-wide exact pass: column u, rows v0 + 16k
+    const double du = static_cast<double>(u) - 31.5;
+    const int kb = lane & 3, ti = lane >> 2;                 // estimate: 8 triplets x 4 keypoints per warp
+    const ushort4 slot0 = __ldg(p.slots + 8 * warp + ti);
+    const ushort4 slot1 = __ldg(p.slots + 8 * warp + ti + kFastT / 2);
+    const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
+    const int nq = blockIdx.x < quads ? static_cast<int>((quads - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+    const unsigned long long kp_step = static_cast<unsigned long long>(gridDim.x) * kQuad;
+    unsigned n_flagged = 0, n_windows = 0;
+    unsigned long long* const trace = p.trace != nullptr && tid == 0 ? p.trace + static_cast<size_t>(kExTrace) * blockIdx.x : nullptr;
+    if (trace) trace[0] = ex_global_ns();
+    if (tid < 4) s_mask[tid] = 0;   // three masks and the queue tail
+    const bool defer_ok = p.M <= 0xffffffffull;
+    unsigned q_prev = 0;            // queue tail after the previous quad (uniform over the CTA)
+    unsigned long long kp0 = static_cast<unsigned long long>(blockIdx.x) * kQuad - kp_step;   // first keypoint of quad `it`
+    int mslot = 2;                  // (it + 3) % 3
+    stage_quad_h16(p, static_cast<unsigned long long>(blockIdx.x) * kQuad, s_rec, tid, kRows);
+    __syncthreads();
+    pdl_wait();   // launched early behind fill_array_kernel: the texture array is complete from here on
+    if (trace) trace[1] = ex_global_ns();
+
+    for (int it = -1; it <= nq; ++it, kp0 += kp_step, mslot = mslot == 2 ? 0 : mslot + 1) {
+        const int cur = it & 1, nxt = cur ^ 1;
+        const bool consume = it >= 0 && it < nq, produce = it + 1 < nq;
+        const unsigned windows_before = n_windows;
+        if (tid == 0) s_mask[mslot == 2 ? 0 : mslot + 1] = 0;   // quad it-2's mask: every reader is past it
+        if (it + 2 < nq) stage_quad_h16(p, kp0 + 2 * kp_step, s_rec + cur * kQuad * kHRecDoubles, tid, kRows);   // -> buffer [cur]
+        if (it >= 1)   // pack the bits of quad it-1 (buffer [nxt])
+            h16_pack_bits(p, s_bits + (nxt * kQuad + (tid >> 8)) * kPipeBits, kp0 - kp_step + (tid >> 8), tid & 255, lane);
+
+        const unsigned* const my_win = s_h + (cur * kQuad + kb) * kHPitch;
+        uint8_t* const my_bits = s_bits + (cur * kQuad + kb) * kPipeBits;
+        unsigned need = 0;
+        {
+            float d1a = 0.f, d2a = 0.f, d1b = 0.f, d2b = 0.f;
+#pragma unroll 1
+            for (int phase = 0; phase < 2; ++phase) {
+                if ((phase == 0) == ssd_first) {
+                    if (consume) ssd_estimate_h16_2(my_win, slot0, slot1, p.two23, d1a, d2a, d1b, d2b);
+                } else if (produce) {
+                    h16_resample_pairs<kRows>(p.texn, s_rec + (nxt * kQuad + rwin) * kHRecDoubles,
+                                              s_h + (nxt * kQuad + rwin) * kHPitch, lane, rv0);
+                }
+            }
+            if (consume) {
+                float diff0, diff1;
+                const bool sure0 = estimate_decides_h16(d1a, d2a, diff0);
+                const bool sure1 = estimate_decides_h16(d1b, d2b, diff1);
+                const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves an unused window
+                need = (live && !sure0 ? 1u : 0u) | (live && !sure1 ? 2u : 0u);
+                my_bits[slot0.w & 0x7fff] = (slot0.w >> 15) ? diff0 < 0.0f : diff0 > 0.0f;
+                my_bits[slot1.w & 0x7fff] = (slot1.w >> 15) ? diff1 < 0.0f : diff1 > 0.0f;
+                if (need) {
+                    atomicOr(s_mask + mslot, 1 << kb);
+                    if (defer_ok) {
+                        if (need & 1) {
+                            const unsigned at = atomicAdd(s_qtail, 1u);
+                            if (at < kQueueCap) s_queue[at] = DeferredBit{slot0, static_cast<unsigned>(kp0 + kb)};
+                        }
+                        if (need & 2) {
+                            const unsigned at = atomicAdd(s_qtail, 1u);
+                            if (at < kQueueCap) s_queue[at] = DeferredBit{slot1, static_cast<unsigned>(kp0 + kb)};
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+
+        if (consume) {
+            const int mask = *reinterpret_cast<volatile int*>(s_mask + mslot);
+            bool window_pass = mask != 0;
+            if (mask && defer_ok) {
+                const unsigned tail = *reinterpret_cast<volatile unsigned*>(s_qtail);
+                if (tail <= kQueueCap && tail - q_prev <= kDeferMax) {   // few: they stay parked
+                    q_prev = tail;
+                    window_pass = false;
+                }
+            }
+            if (window_pass) {   // block-uniform: dense undecided bits (flat / saturated footprints)
+                for (int w = 0; w < kQuad; ++w) {
+                    if (!((mask >> w) & 1)) continue;
+                    // the CTA resamples window w exactly (fp64, the reference's operation order) ...
+                    const double* kpr = p.xycs + 4 * (kp0 + w);   // (the staged copy is already quad it+2's)
+                    const double c = __ldg(kpr + 2), sn = __ldg(kpr + 3);
+                    const double xa = __dadd_rn(__ldg(kpr + 0), __dmul_rn(c, du));
+                    const double ya = __dadd_rn(__ldg(kpr + 1), __dmul_rn(sn, du));
+#pragma unroll 2
+                    for (int v = v0; v < kWindow; v += kQuadThreads / kWindow) {
+                        const double dv = static_cast<double>(v) - 31.5;
+                        s_exact[v * kWinStride + u] = sample_exact(p.tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv));
+                    }
+                    n_windows += tid == 0;
+                    __syncthreads();
+                    if (tid == 0) *s_qtail = q_prev;   // this quad's parked items are withdrawn (every thread has read the tail;
+                                                       // the next additions come after the barrier below)
+                    // ... and the lanes of that window run the exact chains of their undecided triplets
+                    if (kb == w && need) {
+                        if (need & 1) {
+                            my_bits[slot0.w & 0x7fff] = h16_exact_bit(s_exact, slot0);
+                            ++n_flagged;
+                        }
+                        if (need & 2) {
+                            my_bits[slot1.w & 0x7fff] = h16_exact_bit(s_exact, slot1);
+                            ++n_flagged;
+                        }
+                    }
+                    __syncthreads();   // the next window overwrites the scratch; the next iteration packs these bits
+                }
+            }
+        }
+        if (trace && it + 3 < kExTrace)
+            trace[it + 3] = ex_global_ns() | (n_windows != windows_before ? 1ull << 63 : 0ull);
+    }
+    __syncthreads();
+    // The pipeline has drained: every warp takes parked bits, the plane memory serves as their scratch.
+    {
+        const unsigned parked = *reinterpret_cast<volatile unsigned*>(s_qtail);
+        double* const scratch = reinterpret_cast<double*>(s_h) + warp * 160;   // 147 doubles per warp
+        for (unsigned i = warp; i < parked; i += kQuadThreads / 32) {
+            recompute_deferred_bit<true>(p.tex, p.xycs, p.out, p.out_index, s_queue[i], scratch, lane);
+            n_flagged += lane == 0;
+        }
+        if (trace && parked) trace[kExTrace - 1] = ex_global_ns() | static_cast<unsigned long long>(parked) << 48;
+    }
+    if (p.stats != nullptr) {
+        n_flagged = __reduce_add_sync(0xffffffffu, n_flagged);
+        if (lane == 0 && (n_flagged | n_windows)) {
+            atomicAdd(p.stats + 0, static_cast<unsigned long long>(n_flagged));
+            atomicAdd(p.stats + 1, static_cast<unsigned long long>(n_windows));
+        }
+    }
+    if (p.route != nullptr && tid == 0)
         p.route[blockIdx.x] = make_uint2(n_windows, static_cast<unsigned>(nq > 0 ? nq * kQuad : 0));
 }
 
@@ -1792,6 +2014,8 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
                                              kRolesSmemBytes));
             CLATCH_CUDA(cudaFuncSetAttribute(extract_h16_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kH16SmemBytes));
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_h16s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kH16SmemBytes));
             ctx->pipe_configured = true;
         }
         // The resampler reads footprints through the texture unit: copy the image into this
@@ -1808,7 +2032,9 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         p.tex = ti->tex;
         p.texn = ti->texn;
         p.two23 = 0x4B000000u;
-        p.slots = ctx->extract_variant == 5 ? pat.slots_h16.as<ushort4>() : pat.slots_f8.as<ushort4>();
+        static const int ex_debug = std::getenv("CLATCH_EX_DEBUG") ? std::atoi(std::getenv("CLATCH_EX_DEBUG")) : 0;
+        p.dbg = ex_debug;
+        p.slots = ctx->extract_variant >= 5 ? pat.slots_h16.as<ushort4>() : pat.slots_f8.as<ushort4>();
         const size_t quads = (M + kQuad - 1) / kQuad;
         const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
         // variant 4 (default): dedicated producer / consumer warps, 16 + 16 — 60.1 vs 58.1 M desc/s at 10 k
@@ -1828,7 +2054,9 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
             CLATCH_CUDA(cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long) * kExTrace * grid, stream));
             p.trace = d_trace;
         }
-        if (ctx->extract_variant == 5)   // packed 16-bit planes, fp32 resampling
+        if (ctx->extract_variant == 6)   // packed 16-bit planes, every warp resamples and estimates
+            CLATCH_CUDA(launch_kernel(extract_h16s_kernel, dim3(grid), dim3(kQuadThreads), kH16SmemBytes, stream, ctx->pdl, 1, p));
+        else if (ctx->extract_variant == 5)   // packed 16-bit planes, fp32 resampling, dedicated roles
             CLATCH_CUDA(launch_kernel(extract_h16_kernel<16>, dim3(grid), dim3(kQuadThreads), kH16SmemBytes, stream, ctx->pdl, 1, p));
         else if (ctx->extract_variant == 4)   // may start (tables, first keypoint rows) while fill_array_kernel is still writing
             CLATCH_CUDA(launch_kernel(extract_roles_kernel<16>, dim3(grid), dim3(kQuadThreads), kRolesSmemBytes, stream, ctx->pdl, 1, p));

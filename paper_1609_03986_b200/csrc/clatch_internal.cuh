@@ -84,8 +84,9 @@ struct clatch_ctx {
     // 0: one window per CTA (4 CTAs/SM); 1: quad kernel (4 fp64 windows per CTA); 2: filtered kernel
     // (4 split windows per CTA, fp32 estimate + exact recompute); 3: pipelined kernel (resampling
     // overlapped with the estimate, footprints from the texture unit); 4: variant 3 with dedicated
-    // producer / consumer warps. 2-4 take u8 images — others run variant 1.
-    int extract_variant = 4;
+    // producer / consumer warps; 5: packed 16-bit planes resampled in fp32 (dedicated roles, the default); 6: variant 5
+    // with every warp doing both halves. 2-6 take u8 images — others run variant 1.
+    int extract_variant = 5;
     struct TexImage {                // pipelined kernel: the image as a gather-enabled CUDA array
         cudaStream_t stream = nullptr;
         cudaArray_t array = nullptr;

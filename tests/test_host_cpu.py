@@ -298,6 +298,81 @@ def test_fp32_estimate_bound_never_decides_wrongly():
     assert 0.15 < decided_total / total < 0.95       # the cases really straddle the boundary
 
 
+def test_packed_plane_estimate_bound_never_decides_wrongly():
+    """The default extraction kernel (extract_h16_kernel) estimates from 16-bit planes: a stored sample is an integer A
+    with |A - 256 v| <= 0.66 (rounding 0.5 + fp32 / fixed-point resampling 0.16, csrc/clatch_extract.cu), differences
+    of stored samples are exact in fp32, the sums are 49 fused fp32 accumulations, and a bit is taken from them only
+    when |d1 - d2| > 19.1 (sqrt d1 + sqrt d2) + 3.3e-6 (d1 + d2) + 180. Restated in numpy against the reference's
+    fp64 chains — with the stored samples pushed to the worst side the error budget allows (the first companion away
+    from the anchor, the second towards it, and the other way round): whenever the estimate decides, it must agree."""
+    import numpy as np
+
+    rng = np.random.default_rng(16092)
+
+    def exact_chain(a, b):                   # src/descriptor.cpp:61-75, 49 live terms, unfused
+        d = np.zeros(len(a))
+        for k in range(49):
+            e = a[:, k] - b[:, k]
+            d = d + e * e
+        return d
+
+    def stored(v, push, towards):
+        """An integer within 0.66 of 256 v: nearest, or — where the budget allows — the neighbour further along `push`
+        (+1 / -1 per element: away from or towards the anchor's stored value `towards`)."""
+        x = 256.0 * v
+        near = np.rint(x)
+        direction = np.sign(near - towards) * push
+        direction[direction == 0] = 1.0
+        cand = np.where(direction > 0, np.floor(x) + 1.0, np.ceil(x) - 1.0)
+        ok = np.abs(cand - x) <= 0.66
+        return np.clip(np.where(ok, cand, near), 0, 65280)
+
+    def fp32_chain(ia, ib):
+        d = np.zeros(len(ia), np.float32)
+        for k in range(49):
+            e = (ia[:, k] - ib[:, k]).astype(np.float32)                  # exact: |e| <= 65280
+            d = (e.astype(np.float64) * e.astype(np.float64) + d.astype(np.float64)).astype(np.float32)   # fused
+        return d
+
+    n = 30000
+    cases = []
+    base = rng.integers(0, 256, (n, 49)).astype(np.float64)
+    frac = rng.random((n, 49))
+    cases.append((rng.random((n, 49)) * 255, rng.random((n, 49)) * 255, rng.random((n, 49)) * 255))
+    for scale in (1e-10, 1e-5, 1e-3, 3e-3, 1e-2, 3e-2, 1e-1, 0.3, 1.0):   # companions that differ by this much per pixel
+        a = np.clip(base + frac, 0, 255)
+        b = np.clip(a + rng.normal(0, 30, (n, 49)), 0, 255)
+        c = np.clip(b + rng.normal(0, scale, (n, 49)), 0, 255)
+        cases.append((a, b, c))
+    for scale in (0.0, 1e-9, 1e-3, 1e-2):                                  # flat and nearly flat footprints
+        level = rng.integers(0, 256, (n, 1)).astype(np.float64) + rng.random((n, 1))
+        mk = lambda: np.clip(level + rng.normal(0, 1, (n, 49)) * scale, 0, 255)   # noqa: E731
+        cases.append((mk(), mk(), mk()))
+    a = rng.random((n, 49)) * 255                                          # mirrored companions: d1 == d2 up to rounding
+    delta = rng.normal(0, 40, (n, 49))
+    cases.append((a, np.clip(a + delta, 0, 255), np.clip(a - delta, 0, 255)))
+    small = rng.random((n, 49)) * 0.02                                     # tiny sums: the constant term matters
+    cases.append((small, rng.random((n, 49)) * 0.02, rng.random((n, 49)) * 0.02))
+
+    decided_total = total = 0
+    for a, b, c in cases:
+        want = exact_chain(a, b) > exact_chain(a, c)
+        ia = np.clip(np.rint(256.0 * a), 0, 65280)
+        for push_b, push_c in ((1.0, -1.0), (-1.0, 1.0), (0.0, 0.0)):
+            ib = stored(b, push_b, ia) if push_b else np.rint(256.0 * b)
+            ic = stored(c, push_c, ia) if push_c else np.rint(256.0 * c)
+            assert np.abs(ib - 256.0 * b).max() <= 0.66 and np.abs(ic - 256.0 * c).max() <= 0.66
+            d1, d2 = fp32_chain(ia, ib), fp32_chain(ia, ic)
+            diff = d1 - d2
+            bound = (np.float32(19.1) * (np.sqrt(d1) + np.sqrt(d2)) + np.float32(3.3e-6) * (d1 + d2)
+                     + np.float32(180.0)).astype(np.float32)
+            decided = np.abs(diff) > bound
+            assert np.array_equal((diff > 0)[decided], want[decided])
+            decided_total += int(decided.sum())
+            total += len(decided)
+    assert 0.15 < decided_total / total < 0.95       # the cases really straddle the boundary
+
+
 def test_take_keypoints_matches_numpy(lib):
     """clatch_take_keypoints: out[j] = kps[kept[j]] as (m, 4) rows, missing theta / score = 0
     (bindings/module.cpp:49-62), for every accepted column count and worker count."""

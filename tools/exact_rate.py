@@ -27,14 +27,14 @@ images = {
     "half saturated": np.where(xx < w // 2, 255, img).astype(np.uint8),
     "flat": np.full((h, w), 99, np.uint8),
 }
-for variant in (5, 4, 40, 3, 2, 1):          # 40 = variant 4 with the degenerate-image router switched off
-    eng.set_option("extract_variant", 4 if variant == 40 else variant)
-    eng.set_option("extract_route", 0 if variant == 40 else 1)
+for variant in (5, 50, 6, 4, 3, 2, 1):          # 50 = variant 5 with the degenerate-image router switched off
+    eng.set_option("extract_variant", 5 if variant == 50 else variant)
+    eng.set_option("extract_route", 0 if variant == 50 else 1)
     for name, im in images.items():
         eng.set_option("extract_stats", 1)
         m = len(lk.describe(im, kps)[1])
         exact, passes = eng.extract_stats() if variant >= 2 else (0, 0)
-        if variant in (4, 5):
+        if variant in (4, 5, 6):
             eng.set_option("extract_route", 1)      # (resets the router's state between image kinds)
         unit = "windows re-resampled" if variant >= 3 else "warp passes"
         eng.set_option("extract_stats", 0)
@@ -49,8 +49,8 @@ for variant in (5, 4, 40, 3, 2, 1):          # 40 = variant 4 with the degenerat
         e1.record()
         torch.cuda.synchronize()
         rate = len(xycs) / (e0.elapsed_time(e1) / 10) * 1e3 / 1e6
-        print(f"variant {'4 (router off)' if variant == 40 else variant}  {name:36s} exact triplets {exact:9d} of {m * 512} = {exact / (m * 512):.2e}; "
+        print(f"variant {'5 (router off)' if variant == 50 else variant}  {name:36s} exact triplets {exact:9d} of {m * 512} = {exact / (m * 512):.2e}; "
               f"{unit}: {passes} ({passes / m:.3f} per descriptor); {rate:.1f} M desc/s", flush=True)
 eng.set_option("extract_stats", 0)
-eng.set_option("extract_variant", 4)
+eng.set_option("extract_variant", 5)
 eng.set_option("extract_route", 1)

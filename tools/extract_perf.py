@@ -19,7 +19,7 @@ xycs, kept = eng.prepare_keypoints(kps, w, h)
 d_x = torch.from_numpy(xycs).cuda()
 frac = img.astype(np.float64) + np.random.default_rng(0).random(img.shape) * 0.5
 for tag, im in (("u8", img), ("f64 integer-valued", img.astype(np.float64)), ("f64 non-integer", frac)):
-    for variant in (5, 4, 3, 2, 1, 0):
+    for variant in (6, 5, 4, 3, 2, 1, 0):
         eng.set_option("extract_variant", variant)
         d_img = torch.from_numpy(im).cuda()
         out = eng.extract_device(d_img, d_x)
@@ -32,4 +32,4 @@ for tag, im in (("u8", img), ("f64 integer-valued", img.astype(np.float64)), ("f
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
         print(f"{tag:22s} variant {variant}: {ms:.3f} ms  {len(xycs) / ms * 1e3 / 1e6:.1f} M desc/s", flush=True)
-eng.set_option("extract_variant", 4)
+eng.set_option("extract_variant", 5)

@@ -15,7 +15,7 @@ eng = lk.get_engine()
 img = port.structured_image(3, 320, 240)
 kps = lk.detect(img)
 kps = np.vstack([kps, port.random_keypoints(4, 320, 240, 37)])
-for variant in (0, 1, 2, 3, 4):
+for variant in (0, 1, 2, 3, 4, 5, 6):
     eng.set_option("extract_variant", variant)
     for im in (img.astype(np.uint8), img, img + 0.25):
         kept, desc = lk.describe(im, kps)
