@@ -1453,14 +1453,9 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
         const int cur = it & 1, nxt = cur ^ 1;
         const unsigned windows_before = n_windows;
         if (producer) {
-            if (it + 1 < nq && !(p.dbg & 2))   // resample the next quad into the planes [nxt]: this warp's window, its rows
-                h16_resample_pairs<kRRows>(p.texn, s_rec + (nxt * kQuad + rw / kRRows) * kHRecDoubles,
-                                           s_h + (nxt * kQuad + rw / kRRows) * kHPitch, lane, rw % kRRows);
-        } else {
-            // The consumers also stage the window records two quads ahead (buffer [quad & 1]; its last readers resampled
-            // quad `it`, an iteration ago) and pack the previous quad's bits. (Staging from the producers, loads before the
-            // resampling and the record after it, measured slower: eight more live registers across the resampler spill.)
-            if (it + 2 < nq) stage_quad_h16(p, kp0 + 2 * kp_step, s_rec + cur * kQuad * kHRecDoubles, rt, kRRows);
+            // The producers, which have slack (they resample a quad in half the time the consumers need to estimate one),
+            // also pack the previous quad's bits and stage the window records two quads ahead (buffer [quad & 1]; its last
+            // readers resampled quad `it`, an iteration ago): the consumers' critical path is the estimate alone.
             if (it >= 1) {
                 const int w = rt >> 7, j = rt & 127;
                 const uint8_t* bits = s_bits + (nxt * kQuad + w) * kPipeBits;
@@ -1474,6 +1469,11 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
                     }
                 }
             }
+            if (it + 1 < nq && !(p.dbg & 2))   // resample the next quad into the planes [nxt]: this warp's window, its rows
+                h16_resample_pairs<kRRows>(p.texn, s_rec + (nxt * kQuad + rw / kRRows) * kHRecDoubles,
+                                           s_h + (nxt * kQuad + rw / kRRows) * kHPitch, lane, rw % kRRows);
+            if (it + 2 < nq) stage_quad_h16(p, kp0 + 2 * kp_step, s_rec + cur * kQuad * kHRecDoubles, rt, kRRows);
+        } else {
             if (it >= 0 && it < nq) {
                 const unsigned* const my_win = s_h + (cur * kQuad + kb) * kHPitch;
                 const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves an unused window

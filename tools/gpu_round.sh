@@ -27,7 +27,7 @@ echo "== ncu launch list"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$OUT/launches.csv" \
     python bench.py --workload cfg2 --steps 2 --warmup 3 --no-cpu-baseline > "$OUT/ncu_launches.log" 2>&1
 echo "== ncu full: extraction"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:extract_roles -s 3 -c 1 -f -o "$OUT/prof_extract" \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:extract_h16_kernel -s 3 -c 1 -f -o "$OUT/prof_extract" \
     python bench.py --workload cfg2 --steps 2 --warmup 3 --phase extract --no-cpu-baseline > "$OUT/ncu_extract.log" 2>&1
 echo "== ncu full: tensor-core matching (cfg2 size, 100k x 100k, batched pairs)"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:match_tc -s 3 -c 1 -f -o "$OUT/prof_match_tc" \
