@@ -79,8 +79,12 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * shared loads, 2 = four split (fp32 + low word) windows per CTA: a proven fp32 estimate decides
  * each bit and the rare undecided ones are recomputed exactly, 3 = the same estimate with
  * double-buffered planes, texture-unit footprints and resampling overlapped with the estimate,
- * 4 = variant 3 with dedicated producer / consumer warps (default). 2-4 take u8-valued images; any
- * other image runs variant 1. Every variant returns the same bytes.
+ * 4 = variant 3 with dedicated producer / consumer warps, 5 = the estimate from packed 16-bit planes (two shifted
+ * copies: a 7-pixel patch row is four aligned 32-bit words) resampled in fp32 with fixed-point coordinates, dedicated
+ * producer / consumer warps (default), 6 = variant 5 with every warp doing both halves. 2-6 take u8-valued images;
+ * any other image runs variant 1. Every variant returns the same bytes (an estimate only ever decides a bit under a
+ * proven error bound; undecided bits are recomputed with the reference's exact arithmetic). The environment variable
+ * CLATCH_EXTRACT_VARIANT sets the initial value of a new context.
  * key "pdl": 1 (default) launches the dependent kernels of the library's own chains (array fill -> extraction; operand
  * expansion -> tensor-core matcher -> merge) with programmatic stream serialization: their CTAs are scheduled and run
  * their set-up while the predecessor finishes, and wait (griddepcontrol.wait) before touching its output; 0 = plain launches.
@@ -101,6 +105,8 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * train tiles through TMA multicast (half the L2 traffic per compare); 0 = every CTA streams for itself.
  * key "match_streamk": 1 (default) lets the tensor-core matcher split small problems (expanded train set
  * within 32 MB) into equal shares of (query tile, train tile) units per CTA; 0 keeps whole rounds.
+ * key "match_streamk_pairs": 1 cuts those shares over (query tile pair, train tile) units and runs them on CTA pairs
+ * that share the train stream by multicast (needs match_pairs); 0 (default) = one CTA per share (measured equal).
  * key "pairs_filter_on_device": 1 (default) runs the ratio / max-distance / cross-check decisions of
  * clatch_match_set_pairs on the device so only surviving rows cross the bus; 0 filters on the host.
  * key "extract_stats": non-zero starts counting variant 2's exact recomputes (and zeroes the

@@ -291,6 +291,7 @@ int clatch_ctx_create(int device, clatch_ctx** out) {
         return cuda_fail(se, "cudaStreamCreateWithFlags");
     }
     if (const char* v = std::getenv("CLATCH_MATCH_VARIANT")) ctx->match_variant = std::atoi(v);
+    if (const char* v = std::getenv("CLATCH_MATCH_STREAMK_PAIRS")) ctx->match_streamk_pairs = std::atoi(v) != 0;
     if (const char* v = std::getenv("CLATCH_EXTRACT_VARIANT")) {
         const int ev = std::atoi(v);
         if (ev >= 0 && ev <= 6) ctx->extract_variant = ev;
@@ -405,6 +406,10 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
     }
     if (std::strcmp(key, "match_streamk") == 0) {   // tensor matcher: stream-K partition for small problems
         ctx->match_streamk = value != 0;
+        return CLATCH_OK;
+    }
+    if (std::strcmp(key, "match_streamk_pairs") == 0) {   // ... cut over query tile pairs, runs on CTA pairs (multicast)
+        ctx->match_streamk_pairs = value != 0;
         return CLATCH_OK;
     }
     if (std::strcmp(key, "host_promote") == 0) {   // float64 -> u8 on the host workers when lossless: 0 auto, 1 always, 2 never

@@ -112,6 +112,8 @@ struct clatch_ctx {
     bool match_pairs = true;
     bool match_form_auto = false;  // match_variant 4: 1 = mid-sized single matches run the int8 form (it was ahead there before the parked-chunk epilogue; kept for A/B)
     bool match_streamk = true;     // tensor matcher: equal-share partition for small problems (set_option "match_streamk")
+    bool match_streamk_pairs = false;  // ... over (query tile pair, train tile) units on CTA pairs (set_option "match_streamk_pairs";
+                                       // measured equal at 10 k x 10 k — 31.2 vs 31.1 us under ncu, 44.0 vs 42.9 us in bench — so off)
     int match_variant = 4;         // 0: 16 POPC, 1: 7 CSA + 9 POPC, 2: 9 CSA + 7 POPC, 3: tcgen05 int8 GEMM, 4: tcgen05 mxf4 (e2m1) GEMM (CLATCH_MATCH_VARIANT)
     // The scratch below is shared by every call on this context, whatever stream the call queues on
     // (the *_dev entry points take the caller's stream). scratch_event marks the last use; a call on a

@@ -342,7 +342,10 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned 
         // sk_chunks equal runs, one per CTA, in query-tile-major order; a run that crosses a query
         // tile boundary is several pieces (item = CTA + piece * chunks). Every CTA then carries the
         // same number of tile-times instead of ceil(items / SMs) whole rounds.
-        const unsigned long long U = static_cast<unsigned long long>(g.qtiles) * g.total_tiles;
+        // kPair: the same cut over (query tile PAIR, train tile) units, one run per cluster — both CTAs of a cluster walk
+        // the same train tiles for the two query tiles of the pair and share the stream by multicast.
+        const unsigned long long QT = kPair ? (g.qtiles + 1) / 2 : g.qtiles;
+        const unsigned long long U = QT * g.total_tiles;
         const unsigned long long G = g.sk_chunks, TT = g.total_tiles;
         const unsigned long long c = static_cast<unsigned long long>(item) % G;
         const int piece = static_cast<int>(item / G);
@@ -358,10 +361,17 @@ __device__ __forceinline__ TcWork tc_decode(const TcArgs& g, int item, unsigned 
             t0 = u - q * TT;
             n = min(ue - u, TT - t0);
         }
-        w.qtile = static_cast<unsigned>(q);
         w.tile_begin = static_cast<int>(t0);
         w.ntiles = static_cast<int>(n);
-        w.split = static_cast<int>(c - tc_sk_chunk_of(q * TT, U, G));   // pieces of a query tile in train order
+        w.split = static_cast<int>(c - tc_sk_chunk_of(q * TT, U, G));   // pieces of a query tile (pair) in train order
+        if (kPair) {
+            q = 2 * q + rank;
+            if (q >= static_cast<unsigned long long>(g.qtiles)) {       // odd tile count: the last pair's second CTA
+                q = g.qtiles - 1;
+                w.ghost = true;
+            }
+        }
+        w.qtile = static_cast<unsigned>(q);
         w.a = g.a_exp + q * kTileA;
         w.b = g.b_exp;
         w.Q = g.Q;
@@ -812,12 +822,13 @@ namespace {
 // partials sit in slots 0 .. c_last - c_first in ascending train order (same rule as
 // merge_partials_kernel: strictly better wins, so the earlier piece keeps ties).
 __global__ void merge_partials_sk_kernel(const Partial* __restrict__ partial, unsigned long long Q, int total_tiles,
-                                         int qtiles, int chunks, int32_t* __restrict__ best_idx,
+                                         int qtiles, int chunks, int pair_shift, int32_t* __restrict__ best_idx,
                                          int32_t* __restrict__ best_dist, int32_t* __restrict__ second_dist) {
     pdl_wait();                                                // every partial of the GEMM launch is in place
     const unsigned long long qi = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (qi >= Q) return;
-    const unsigned long long U = static_cast<unsigned long long>(qtiles) * total_tiles, TT = total_tiles, q = qi / kTcM;
+    // (pair_shift = 1: the cut ran over query tile PAIRS, `qtiles` counts pairs)
+    const unsigned long long U = static_cast<unsigned long long>(qtiles) * total_tiles, TT = total_tiles, q = (qi / kTcM) >> pair_shift;
     const int pieces = static_cast<int>(tc_sk_chunk_of((q + 1) * TT - 1, U, chunks) - tc_sk_chunk_of(q * TT, U, chunks)) + 1;
     int best = 513, second = 513, idx = -1;
     for (int s = 0; s < pieces; ++s) {
@@ -965,8 +976,13 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
     }
     // Stream-K instead, when the expanded train set stays in L2 (every CTA streams it at its own phase)
     // and the equal-share makespan beats whole rounds: U / SMs tile-times + one A reload per piece.
+    // With CTA pairs (match_pairs) the units are (query tile pair, train tile) and a run belongs to a cluster of two CTAs
+    // that share the train stream by multicast: on its own a CTA pulls 60 KB per tile out of L2 and is bound by that
+    // (1.17 us per tile at 10 k x 10 k against 0.72 us for paired CTAs at scale).
     const size_t sms = static_cast<size_t>(ctx->sm_count);
-    const size_t units = qtiles * ttiles, chunks = std::min(units, sms);
+    const bool sk_pairs = ctx->match_pairs && ctx->match_streamk_pairs && qtiles >= 2 && sms >= 2;
+    const size_t sk_q = sk_pairs ? (qtiles + 1) / 2 : qtiles, sk_slots = sk_pairs ? sms / 2 : sms;
+    const size_t units = sk_q * ttiles, chunks = std::min(units, sk_slots);
     bool streamk = false;
     size_t sk_pieces_per_cta = 1, sk_pieces_per_qtile = 1;
     if (tc_expanded_bytes(ctx, N) <= (32u << 20) && units > 0 && ctx->match_streamk) {
@@ -974,12 +990,14 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
         sk_pieces_per_cta = (share + ttiles - 2) / ttiles + 1;
         sk_pieces_per_qtile = (ttiles + units / chunks - 1) / (units / chunks) + 1;
         const size_t rounds = (qtiles * splits + sms - 1) / sms;
-        const double legacy = rounds * (per_split + 1.5), sk = share + 2.0 * sk_pieces_per_cta;   // (measured: tools/sk_perf.py)
+        // (in tile-times of an unpaired CTA; a paired tile takes ~0.65 of one)
+        const double legacy = rounds * (per_split + 1.5), sk = (share + 2.0 * sk_pieces_per_cta) * (sk_pairs ? 0.65 : 1.0);   // (measured: tools/sk_perf.py)
         streamk = sk < legacy;
     }
     // Otherwise pairs of CTAs share the train stream (match_tc_kernel<true>): the schedulable unit is a pair of
     // query tiles on a pair of SMs, so the split count is chosen again in those units.
     const bool paired = !streamk && ctx->match_pairs && qtiles >= 2 && sms >= 2;
+    const bool sk_paired = streamk && sk_pairs;
     if (paired) {
         const size_t pq = (qtiles + 1) / 2, slots2 = sms / 2;
         double best_cost = 1e300;
@@ -1019,7 +1037,9 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
         CLATCH_CUDA(cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long) * 8 * sms, stream));
         g.trace = d_trace;
     }
-    if (paired) {
+    if (sk_paired) {   // g.num_items = clusters x pieces: item = cluster + piece * clusters
+        if (int rc = launch_tc(ctx, g, static_cast<unsigned>(2 * chunks), true, stream, !tracing)) return rc;
+    } else if (paired) {
         const size_t pair_items = (qtiles + 1) / 2 * splits;
         g.num_items = static_cast<int>(pair_items);
         if (int rc = launch_tc(ctx, g, static_cast<unsigned>(std::min<size_t>(2 * pair_items, sms)), true, stream, !tracing)) return rc;
@@ -1049,14 +1069,14 @@ static int match_top2_tc_impl(clatch_ctx* ctx, const uint8_t* d_q, size_t Q, con
         std::fprintf(stderr, "[clatch tc trace] %s Q=%zu N=%zu ctas=%zu tiles/cta=%llu total %.1f us | mean (max) us since first CTA start: "
                      "entry %.1f (%.1f), setup done %.1f (%.1f), first stage landed %.1f (%.1f), last MMA issued %.1f (%.1f), "
                      "epilogue done %.1f (%.1f), exit %.1f (%.1f)\n",
-                     streamk ? "stream-K" : paired ? "paired" : "rounds", Q, N, n, h[6], (t_end - t0) / 1e3, sum[0] / n, mx[0], sum[1] / n,
+                     sk_paired ? "stream-K pairs" : streamk ? "stream-K" : paired ? "paired" : "rounds", Q, N, n, h[6], (t_end - t0) / 1e3, sum[0] / n, mx[0], sum[1] / n,
                      mx[1], sum[2] / n, mx[2], sum[3] / n, mx[3], sum[4] / n, mx[4], sum[5] / n, mx[5]);
     }
     if (streamk)
         CLATCH_CUDA(launch_kernel(merge_partials_sk_kernel, dim3(static_cast<unsigned>((Q + 255) / 256)), dim3(256), 0, stream,
                                   ctx->pdl && !tracing, 1, static_cast<const Partial*>(ctx->partial.as<Partial>()),
-                                  static_cast<unsigned long long>(Q), static_cast<int>(ttiles), static_cast<int>(qtiles),
-                                  static_cast<int>(chunks), d_best_idx, d_best_dist, d_second));
+                                  static_cast<unsigned long long>(Q), static_cast<int>(ttiles), static_cast<int>(sk_q),
+                                  static_cast<int>(chunks), sk_paired ? 1 : 0, d_best_idx, d_best_dist, d_second));
     else
         launch_merge_partials(ctx->partial.as<Partial>(), Q, static_cast<int>(splits), 513, d_best_idx, d_best_dist,
                               d_second, stream, ctx->pdl && !tracing);

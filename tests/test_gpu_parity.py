@@ -433,6 +433,11 @@ def test_tensor_matcher_partitions_agree(lk, port, shape):
         for sk in (1, 0):
             eng.set_option("match_streamk", sk)
             res[sk] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_streamk", 1)
+        eng.set_option("match_streamk_pairs", 1)        # stream-K runs on CTA pairs (default: single CTAs)
+        res[6] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_streamk_pairs", 0)
+        eng.set_option("match_streamk", 0)
         eng.set_option("match_form_auto", 0)            # e2m1 operands at every size
         eng.set_option("match_pairs", 0)                # every CTA streams the train set for itself
         res[2] = np.stack(eng.match_top2(query, train))
@@ -444,10 +449,11 @@ def test_tensor_matcher_partitions_agree(lk, port, shape):
         res[5] = np.stack(eng.match_top2(query, train))
     finally:
         eng.set_option("match_streamk", 1)
+        eng.set_option("match_streamk_pairs", 0)
         eng.set_option("match_pairs", 1)                # default: CTA pairs share the stream by TMA multicast
         eng.set_option("match_variant", 4)
         eng.set_option("match_form_auto", 1)
-    for k in (1, 2, 3, 4, 5):
+    for k in (1, 2, 3, 4, 5, 6):
         assert np.array_equal(res[0], res[k]), k
     rows = np.arange(q_n) if q_n * t_n <= 4_000_000 else np.unique(np.r_[np.arange(0, q_n, 7)[:40], rng.integers(0, q_n, 40)])
     assert np.array_equal(res[1][:, rows].T, port.knn2_all(query[rows], train))
