@@ -91,6 +91,10 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * key "extract_route": 1 (default) lets a context whose last u8 launch needed the exact pass for more than 35 % of its
  * windows (flat / saturated images: exact ties) run the next launches on the all-fp64 quad kernel, probing the default
  * kernel again every 16th launch; 0 = always the selected variant.
+ * key "extract_f64_h16": 1 (default) sends a float64 image that is not u8-valued but tame (finite, a value range between
+ * 2^-400 and 2^400, no pixel further than 2^20 ranges from zero) through the packed-plane kernel, its estimate planes resampled from a
+ * float texture of the image scaled to [0, 1] and every undecided bit recomputed from the doubles; 0 = the all-fp64
+ * kernel (variant 1), which also takes whatever is not tame and frames that arrive in row bands.
  * key "upload_bands": clatch_describe_all_f64 uploads a big float64 frame in this many row bands and
  * extracts each band's keypoints while the next band is in flight (0 = choose by frame size, the
  * default; 1 = one piece; up to 6). Results never depend on it.

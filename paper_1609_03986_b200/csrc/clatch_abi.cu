@@ -326,6 +326,9 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
     for (auto& t : ctx->tex_images) {
         if (t.tex) cudaDestroyTextureObject(t.tex);
         if (t.texn) cudaDestroyTextureObject(t.texn);
+        if (t.texf) cudaDestroyTextureObject(t.texf);
+        if (t.surff) cudaDestroySurfaceObject(t.surff);
+        if (t.arrayf) cudaFreeArray(t.arrayf);
         if (t.surf) cudaDestroySurfaceObject(t.surf);
         if (t.array) cudaFreeArray(t.array);
     }
@@ -406,6 +409,10 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
     }
     if (std::strcmp(key, "match_streamk") == 0) {   // tensor matcher: stream-K partition for small problems
         ctx->match_streamk = value != 0;
+        return CLATCH_OK;
+    }
+    if (std::strcmp(key, "extract_f64_h16") == 0) {   // tame non-u8 float64 images: packed-plane kernel (1) or the all-fp64 quad kernel (0)
+        ctx->extract_f64_h16 = value != 0;
         return CLATCH_OK;
     }
     if (std::strcmp(key, "match_streamk_pairs") == 0) {   // ... cut over query tile pairs, runs on CTA pairs (multicast)
@@ -1144,7 +1151,7 @@ static int describe_batch_impl(clatch_ctx* ctx, const Pixel* const* imgs, const 
         bool promoted = false;   // float64 image sent up as its lossless u8 copy (host workers, page-locked staging)
         if (!kU8) {
             if ((rc = slot.img_u8.reserve(u8_pitch * h))) break;
-            if ((rc = slot.flags.reserve(sizeof(int)))) break;
+            if ((rc = slot.flags.reserve(64))) break;   // the flag block (clatch_extract.cu: kFlagBlockBytes)
             if (n >= 256 && want_host_promote(ctx, imgs[i])) {
                 if ((rc = slot.h_img.reserve(u8_pitch * h))) break;
                 promoted = promote_image_u8(reinterpret_cast<const double*>(imgs[i]), pitches[i],

@@ -62,6 +62,7 @@ struct ExtractParams {
     unsigned long long* trace; // optional (CLATCH_EX_TRACE=1): kExTrace globaltimer stamps per CTA of the default kernel
 };
 
+constexpr int kFlagBlockBytes = 64;   // classification flag + pixel range of a float64 image, see classify_convert_kernel
 constexpr int kExTrace = 128;   // [0] entry, [1] texture array complete, [2 + i] end of pipeline iteration i - 1 (bit 63: exact pass)
 
 __device__ __forceinline__ unsigned long long ex_global_ns() {
@@ -684,6 +685,20 @@ __device__ __forceinline__ double sample_exact(cudaTextureObject_t tex, double x
     return blend(fx, fy, u8_to_f64(g.w), u8_to_f64(g.z), u8_to_f64(g.x), u8_to_f64(g.y));
 }
 
+// The same sample from a float64 image in global memory (what extract_quad_kernel<false> computes).
+__device__ __forceinline__ double sample_exact_f64(const double* img, size_t pitch, double xa, double ya, double sdv, double cdv) {
+    const double sx = __dsub_rn(xa, sdv);
+    const double sy = __dadd_rn(ya, cdv);
+    int x0, y0;
+    double x0f, y0f;
+    floor_exact(sx, x0, x0f);
+    floor_exact(sy, y0, y0f);
+    const double fx = __dsub_rn(sx, x0f);
+    const double fy = __dsub_rn(sy, y0f);
+    const double* q = img + static_cast<size_t>(y0) * pitch + x0;
+    return blend(fx, fy, __ldg(q), __ldg(q + 1), __ldg(q + pitch), __ldg(q + pitch + 1));
+}
+
 __device__ __noinline__ bool triplet_bit_7x7_planes_at(const float* win, int lo_off, int oa, int ob, int oc,
                                                        bool swapped) {
     const float* pa = win + oa;
@@ -904,19 +919,33 @@ __device__ __forceinline__ void h16_anchor_dev(unsigned off, int& x, int& y) {
     x = 2 * (r - y * kH16RowWords) - odd;
 }
 
-template <bool kH16>   // slot offsets: row * kWinStride + column (fp32 planes) or packed-plane word offsets
+// kH16: slot offsets are packed-plane word offsets (else row * kWinStride + column, the fp32 planes).
+// kF64: the image is float64 in global memory (img64 / pitch64) instead of the u8 texture.
+template <bool kH16, bool kF64 = false>
 __device__ __noinline__ void recompute_deferred_bit(cudaTextureObject_t tex, const double* xycs, uint8_t* out,
                                                     const unsigned* out_index, const DeferredBit item, double* scratch,
-                                                    int lane) {
+                                                    int lane, const double* img64 = nullptr, size_t pitch64 = 0) {
     const double* const kpr = xycs + 4 * static_cast<unsigned long long>(item.kp);
     const double kx = __ldg(kpr + 0), ky = __ldg(kpr + 1), c = __ldg(kpr + 2), sn = __ldg(kpr + 3);
     const unsigned offs[3] = {item.slot.x, item.slot.y, item.slot.z};
+    if (kF64) {
+#pragma unroll 1
+        for (int i = lane; i < 3 * 49; i += 32) {
+            const int patch = i / 49, pix = i - 49 * patch, r = pix / 7, cc = pix - 7 * r;
+            const unsigned off = patch == 0 ? offs[0] : (patch == 1 ? offs[1] : offs[2]);
+            int v, u;
+            h16_anchor_dev(off, u, v);
+            const double du = static_cast<double>(u + cc) - 31.5, dv = static_cast<double>(v + r) - 31.5;
+            scratch[i] = sample_exact_f64(img64, pitch64, __dadd_rn(kx, __dmul_rn(c, du)), __dadd_rn(ky, __dmul_rn(sn, du)),
+                                          __dmul_rn(sn, dv), __dmul_rn(c, dv));
+        }
+    }
     // Five rounds of 32 samples: all footprints are requested before the first one is blended (issued one by one, each
     // gather's ~700 clk of latency — nothing else runs on the SM at this point — was paid five times in a row).
     double pfx[5], pfy[5];
     uint4 pg[5];
 #pragma unroll
-    for (int round = 0; round < 5; ++round) {
+    for (int round = 0; round < (kF64 ? 0 : 5); ++round) {
         const int i = min(lane + 32 * round, 3 * 49 - 1);
         const int patch = i / 49, pix = i - 49 * patch, r = pix / 7, cc = pix - 7 * r;
         const unsigned off = patch == 0 ? offs[0] : (patch == 1 ? offs[1] : offs[2]);
@@ -941,7 +970,7 @@ __device__ __noinline__ void recompute_deferred_bit(cudaTextureObject_t tex, con
         pg[round] = footprint(tex, x0, y0);
     }
 #pragma unroll
-    for (int round = 0; round < 5; ++round) {
+    for (int round = 0; round < (kF64 ? 0 : 5); ++round) {
         const int i = lane + 32 * round;
         const uint4 g = pg[round];
         const double val = blend(pfx[round], pfy[round], u8_to_f64(g.w), u8_to_f64(g.z), u8_to_f64(g.x), u8_to_f64(g.y));
@@ -1401,7 +1430,10 @@ __device__ __forceinline__ void h16_pack_bits(const ExtractParams& p, const uint
     }
 }
 
-template <int kRW>
+// kF64: a float64 image whose pixels are not all u8 values. The planes then come from a float texture of the image
+// scaled to [0, 1] over its own range (fill_array_f32_kernel; the estimate and its bound only see that texture, and
+// bilinear sampling commutes with the affine map), the exact paths sample the doubles in global memory.
+template <int kRW, bool kF64>
 __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractParams p) {
     if (p.flags != nullptr && p.flags[0] != p.run_if_flag) return;
     constexpr int kSW = 32 - kRW, kST = kSW * 32;
@@ -1522,7 +1554,9 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
 #pragma unroll 2
                         for (int v = v0; v < kWindow; v += kSRows) {
                             const double dv = static_cast<double>(v) - 31.5;
-                            s_exact[v * kWinStride + u] = sample_exact(p.tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv));
+                            s_exact[v * kWinStride + u] =
+                                kF64 ? sample_exact_f64(static_cast<const double*>(p.img), p.pitch, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv))
+                                     : sample_exact(p.tex, xa, ya, __dmul_rn(sn, dv), __dmul_rn(c, dv));
                         }
                         n_windows += rt == 0;
                         asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
@@ -1550,7 +1584,8 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
         const unsigned parked = *reinterpret_cast<volatile unsigned*>(s_qtail);
         double* const scratch = reinterpret_cast<double*>(s_h) + warp * 160;   // 147 doubles per warp
         for (unsigned i = warp; i < parked; i += kQuadThreads / 32) {
-            recompute_deferred_bit<true>(p.tex, p.xycs, p.out, p.out_index, s_queue[i], scratch, lane);
+            recompute_deferred_bit<true, kF64>(p.tex, p.xycs, p.out, p.out_index, s_queue[i], scratch, lane,
+                                               static_cast<const double*>(p.img), p.pitch);
             n_flagged += lane == 0;
         }
         if (trace && parked) trace[kExTrace - 1] = ex_global_ns() | static_cast<unsigned long long>(parked) << 48;
@@ -1789,10 +1824,23 @@ __global__ void __launch_bounds__(kThreads, 2) extract_generic_kernel(ExtractPar
 // pixel poisons its sum. Such images take the generic kernel, which evaluates (w*e)*e literally.
 // Rows [row0, row1) only, so an image that arrives in row bands can be classified band by band;
 // the flag accumulates ("some pixel seen so far is not a u8 value").
+// The flag block (64 bytes): int flags[0] as above; at byte 8 two u64 keys, the smallest and the largest pixel seen as
+// order-preserving integers; at byte 24 two doubles {lo, 1 / (hi - lo)} written by range_finalize_kernel.
+__host__ __device__ __forceinline__ unsigned long long* flag_keys(int* flags) { return reinterpret_cast<unsigned long long*>(flags + 2); }
+__host__ __device__ __forceinline__ double* flag_range(int* flags) { return reinterpret_cast<double*>(flags + 6); }
+__device__ __forceinline__ unsigned long long ordered_key(double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ordered_value(unsigned long long k) {
+    return __longlong_as_double(static_cast<long long>((k >> 63) ? (k ^ 0x8000000000000000ull) : ~k));
+}
+
 __global__ void classify_convert_kernel(const double* src, size_t src_pitch, uint8_t* dst,
                                         size_t dst_pitch, int width, int row0, int row1, int* flags) {
     const size_t n = static_cast<size_t>(width) * (row1 - row0);
     int cls = 0;
+    double lo = 1.0e308, hi = -1.0e308;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int yy = row0 + static_cast<int>(i / width), xx = static_cast<int>(i % width);
@@ -1801,9 +1849,52 @@ __global__ void classify_convert_kernel(const double* src, size_t src_pitch, uin
         const bool tame = fabs(v) <= 0x1p1000;                            // NaN fails
         cls = max(cls, tame ? (ok ? 0 : 1) : 2);
         dst[static_cast<size_t>(yy) * dst_pitch + xx] = ok ? static_cast<uint8_t>(v) : 0;
+        lo = fmin(lo, v);   // (NaN is ignored by fmin / fmax; such an image is class 2 anyway)
+        hi = fmax(hi, v);
     }
     cls = __reduce_max_sync(0xffffffffu, cls);
     if (cls != 0 && (threadIdx.x & 31) == 0) atomicMax(flags, cls);
+    // the range of ALL pixels (it only matters to the non-u8 route, but which route that is is not known yet)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0 && lo <= hi) {
+        atomicMin(flag_keys(flags) + 0, ordered_key(lo));
+        atomicMax(flag_keys(flags) + 1, ordered_key(hi));
+    }
+}
+
+// After the WHOLE image has been classified as "tame, not u8-valued" (flags[0] == 1): if its range is usable —
+// 2^-400 <= hi - lo <= 2^400, and no pixel further than 2^20 ranges from zero, so that the reference's own fp64
+// roundings (relative to the pixel values) stay below 1e-4 stored units — publish {lo, 1 / (hi - lo)} and move the image to class 3, the
+// packed-plane kernel's float64 route. Anything else stays with extract_quad_kernel<false>.
+__global__ void range_finalize_kernel(int* flags) {
+    if (flags[0] != 1) return;
+    const double lo = ordered_value(flag_keys(flags)[0]), hi = ordered_value(flag_keys(flags)[1]);
+    // 2^-400 <= r <= 2^400: a squared difference neither overflows nor reaches the denormals in the reference's sums (an
+    // image of values around 1e-290 has every bit 0 there: all its squares underflow, which a scale-free estimate cannot see)
+    const double r = hi - lo, inv = 1.0 / r;
+    if (r >= 0x1p-400 && r <= 0x1p400 && fmax(fabs(lo), fabs(hi)) <= r * 1048576.0) {
+        flag_range(flags)[0] = lo;
+        flag_range(flags)[1] = inv;
+        __threadfence();
+        flags[0] = 3;
+    }
+}
+
+// float64 image -> float CUDA array of (v - lo) / (hi - lo), 4 pixels per thread (class 3 images only).
+__global__ void fill_array_f32_kernel(cudaSurfaceObject_t surf, const double* __restrict__ src, size_t pitch, int w, int h,
+                                      const int* flags, int run_if_flag) {
+    pdl_launch_dependents();
+    if (flags[0] != run_if_flag) return;
+    const double lo = flag_range(const_cast<int*>(flags))[0], inv = flag_range(const_cast<int*>(flags))[1];
+    const int x = (blockIdx.x * blockDim.x + threadIdx.x) * 4, y = blockIdx.y;
+    if (x >= w || y >= h) return;
+    const double* row = src + static_cast<size_t>(y) * pitch;
+    for (int i = x; i < min(w, x + 4); ++i)
+        surf2Dwrite(static_cast<float>((row[i] - lo) * inv), surf, i * 4, y);
 }
 
 int grid_for(const clatch_ctx* ctx, size_t M, int ctas_per_sm) {
@@ -1869,6 +1960,37 @@ int tex_image_for(clatch_ctx* ctx, cudaStream_t stream, int width, int height, c
         ti->height = height;
     }
     *out = ti;
+    return CLATCH_OK;
+}
+
+// The float companion of a stream's texture image (class 3 float64 images): a gather-enabled float array.
+int tex_image_f32_for(clatch_ctx* ctx, clatch_ctx::TexImage* ti, cudaStream_t stream, int width, int height) {
+    if (ti->widthf != width || ti->heightf != height) {
+        if (ti->texf) {
+            CLATCH_CUDA(cudaStreamSynchronize(stream));   // a kernel may still be sampling the old array
+            cudaDestroyTextureObject(ti->texf);
+            cudaDestroySurfaceObject(ti->surff);
+            cudaFreeArray(ti->arrayf);
+            ti->texf = 0;
+            ti->surff = 0;
+            ti->arrayf = nullptr;
+            ti->widthf = ti->heightf = 0;
+        }
+        const cudaChannelFormatDesc fmt = cudaCreateChannelDesc<float>();
+        CLATCH_CUDA(cudaMallocArray(&ti->arrayf, &fmt, width, height, cudaArrayTextureGather | cudaArraySurfaceLoadStore));
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = ti->arrayf;
+        cudaTextureDesc td{};
+        td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModePoint;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        CLATCH_CUDA(cudaCreateTextureObject(&ti->texf, &rd, &td, nullptr));
+        CLATCH_CUDA(cudaCreateSurfaceObject(&ti->surff, &rd));
+        ti->widthf = width;
+        ti->heightf = height;
+    }
     return CLATCH_OK;
 }
 
@@ -2012,7 +2134,9 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
                                              kPipeSmemBytes));
             CLATCH_CUDA(cudaFuncSetAttribute(extract_roles_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kRolesSmemBytes));
-            CLATCH_CUDA(cudaFuncSetAttribute(extract_h16_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_h16_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kH16SmemBytes));
+            CLATCH_CUDA(cudaFuncSetAttribute(extract_h16_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kH16SmemBytes));
             CLATCH_CUDA(cudaFuncSetAttribute(extract_h16s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kH16SmemBytes));
@@ -2057,7 +2181,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         if (ctx->extract_variant == 6)   // packed 16-bit planes, every warp resamples and estimates
             CLATCH_CUDA(launch_kernel(extract_h16s_kernel, dim3(grid), dim3(kQuadThreads), kH16SmemBytes, stream, ctx->pdl, 1, p));
         else if (ctx->extract_variant == 5)   // packed 16-bit planes, fp32 resampling, dedicated roles
-            CLATCH_CUDA(launch_kernel(extract_h16_kernel<16>, dim3(grid), dim3(kQuadThreads), kH16SmemBytes, stream, ctx->pdl, 1, p));
+            CLATCH_CUDA(launch_kernel(extract_h16_kernel<16, false>, dim3(grid), dim3(kQuadThreads), kH16SmemBytes, stream, ctx->pdl, 1, p));
         else if (ctx->extract_variant == 4)   // may start (tables, first keypoint rows) while fill_array_kernel is still writing
             CLATCH_CUDA(launch_kernel(extract_roles_kernel<16>, dim3(grid), dim3(kQuadThreads), kRolesSmemBytes, stream, ctx->pdl, 1, p));
         else extract_pipe_kernel<<<grid, kQuadThreads, kPipeSmemBytes, stream>>>(p);
@@ -2125,11 +2249,12 @@ int launch_classify_rows(clatch_ctx* ctx, const double* d_img, int width, int he
                          int row1, bool reset, cudaStream_t stream) {
     const size_t u8_pitch = (static_cast<size_t>(width) + 15) / 16 * 16;
     if (int rc = ctx->img_u8.reserve(u8_pitch * height)) return rc;
-    if (int rc = ctx->flags.reserve(sizeof(int))) return rc;
+    if (int rc = ctx->flags.reserve(kFlagBlockBytes)) return rc;
     int* flags = ctx->flags.as<int>();
     if (reset) {
         if (int rc = scratch_acquire(ctx, stream)) return rc;   // img_u8 / flags may still be read on another stream
-        CLATCH_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), stream));
+        CLATCH_CUDA(cudaMemsetAsync(flags, 0, kFlagBlockBytes, stream));
+        CLATCH_CUDA(cudaMemsetAsync(flag_keys(flags), 0xFF, sizeof(unsigned long long), stream));   // the running minimum
     }
     if (row1 <= row0) return CLATCH_OK;
     classify_convert_kernel<<<ctx->sm_count * 8, 256, 0, stream>>>(d_img, pitch, ctx->img_u8.as<uint8_t>(), u8_pitch,
@@ -2139,14 +2264,63 @@ int launch_classify_rows(clatch_ctx* ctx, const double* d_img, int width, int he
     return CLATCH_OK;
 }
 
+// Class 3 (launch_extract_f64_classified, whole images): the packed-plane kernel over a float texture of the image.
+static int launch_extract_h16_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
+                                  const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream, int* flags) {
+    const Pattern& pat = ctx->pattern;
+    if (!ctx->pipe_configured) {   // per-device function attributes
+        CLATCH_CUDA(cudaFuncSetAttribute(extract_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmemBytes));
+        CLATCH_CUDA(cudaFuncSetAttribute(extract_roles_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRolesSmemBytes));
+        CLATCH_CUDA(cudaFuncSetAttribute(extract_h16_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kH16SmemBytes));
+        CLATCH_CUDA(cudaFuncSetAttribute(extract_h16_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kH16SmemBytes));
+        CLATCH_CUDA(cudaFuncSetAttribute(extract_h16s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kH16SmemBytes));
+        ctx->pipe_configured = true;
+    }
+    clatch_ctx::TexImage* ti = nullptr;
+    if (int rc = tex_image_for(ctx, stream, width, height, &ti)) return rc;
+    if (int rc = tex_image_f32_for(ctx, ti, stream, width, height)) return rc;
+    range_finalize_kernel<<<1, 1, 0, stream>>>(flags);
+    const dim3 fgrid((width / 4 + 1 + 127) / 128, height);
+    fill_array_f32_kernel<<<fgrid, 128, 0, stream>>>(ti->surff, d_img, pitch, width, height, flags, 3);
+    ctx->launches += 2;
+    ExtractParams p{};
+    p.img = d_img;
+    p.width = width;
+    p.height = height;
+    p.pitch = pitch;
+    p.xycs = d_xycs;
+    p.M = M;
+    p.out = d_out;
+    p.slots = pat.slots_h16.as<ushort4>();
+    p.T = pat.T;
+    p.K = pat.K;
+    p.flags = flags;
+    p.run_if_flag = 3;
+    p.stats = ctx->extract_stats_on ? ctx->extract_stats.as<unsigned long long>() : nullptr;
+    p.out_index = ctx->extract_out_index;
+    p.tex = 0;
+    p.texn = ti->texf;
+    p.two23 = 0x4B000000u;
+    const size_t quads = (M + kQuad - 1) / kQuad;
+    const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
+    CLATCH_CUDA(launch_kernel(extract_h16_kernel<16, true>, dim3(grid), dim3(kQuadThreads), kH16SmemBytes, stream, ctx->pdl, 1, p));
+    ++ctx->launches;
+    CLATCH_CUDA(cudaGetLastError());
+    return CLATCH_OK;
+}
+
 int launch_extract_f64_classified(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
-                                  const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream) {
+                                  const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream, bool whole_image) {
     if (M == 0) return CLATCH_OK;
     const size_t u8_pitch = (static_cast<size_t>(width) + 15) / 16 * 16;
     int* flags = ctx->flags.as<int>();
     if (int rc = launch_extract<true>(ctx, ctx->img_u8.ptr, width, height, u8_pitch, d_xycs, M, d_out,
                                       stream, flags, 0))
         return rc;
+    // tame but not u8-valued, every row classified, a usable range: class 1 becomes class 3 and takes the packed-plane
+    // kernel (extract_f64_h16, on by default with extract_variant 5); otherwise the all-fp64 quad kernel below runs
+    if (whole_image && ctx->pattern.fast && ctx->extract_variant == 5 && ctx->extract_f64_h16)
+        if (int rc = launch_extract_h16_f64(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, flags)) return rc;
     if (int rc = launch_extract<false>(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, flags, 1)) return rc;
     // class 2 (non-finite or huge pixels): the literal (w*e)*e kernel, whatever the pattern
     if (int rc = launch_extract<false>(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, flags, 2, true)) return rc;
@@ -2157,7 +2331,7 @@ int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int heig
                        const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream) {
     if (M == 0) return CLATCH_OK;
     if (int rc = launch_classify_rows(ctx, d_img, width, height, pitch, 0, height, true, stream)) return rc;
-    return launch_extract_f64_classified(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream);
+    return launch_extract_f64_classified(ctx, d_img, width, height, pitch, d_xycs, M, d_out, stream, true);
 }
 
 } // namespace clatch

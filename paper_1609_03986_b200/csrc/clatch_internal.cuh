@@ -92,12 +92,17 @@ struct clatch_ctx {
         cudaArray_t array = nullptr;
         cudaTextureObject_t tex = 0;
         cudaTextureObject_t texn = 0;    // the same array, texels read as value / 255 (packed-plane kernel)
+        cudaArray_t arrayf = nullptr;    // float64 images that are not u8-valued: the image scaled to [0, 1] as floats
+        cudaTextureObject_t texf = 0;
+        cudaSurfaceObject_t surff = 0;
+        int widthf = 0, heightf = 0;
         cudaSurfaceObject_t surf = 0;    // the same array, for the fill kernel
         int width = 0, height = 0;
     };
     std::vector<TexImage> tex_images;
     // extraction routing for degenerate images (launch_extract): host-mapped per-CTA slots written by the default kernel
     bool extract_route = true;       // set_option "extract_route"
+    bool extract_f64_h16 = true;     // set_option "extract_f64_h16": tame float64 images that are not u8-valued take the packed-plane kernel
     uint2* route_host = nullptr;     // page-locked, mapped
     uint2* route_dev = nullptr;      // the device's view of route_host
     bool route_pending = false, route_quad = false;
@@ -213,7 +218,7 @@ int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int heig
 int launch_classify_rows(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch, int row0,
                          int row1, bool reset, cudaStream_t stream);
 int launch_extract_f64_classified(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
-                                  const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
+                                  const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream, bool whole_image = false);
 
 // detection (clatch_detect.cu)
 struct Detection {   // one FAST detection as the device leaves it (row-major order)

@@ -646,6 +646,64 @@ def test_sparse_undecided_bits_are_parked_and_recomputed_exactly(lk, port):
         eng.set_option("host_promote", 0)
 
 
+def test_float64_images_through_the_packed_plane_kernel(lk, port):
+    """A float64 image that is not u8-valued but tame (finite, a value range between 2^-400 and 2^400, no pixel further than
+    2^20 ranges from zero) takes the default kernel as well: its estimate planes come from a float texture of the image scaled to [0, 1]
+    over its own range, every undecided bit is recomputed from the doubles in global memory. Anything else (flat,
+    a ripple on a huge offset) stays with the all-fp64 kernel. Either way the descriptors are the oracle's — through
+    describe(), a device tensor and describe_batch(), with the route switched on and off."""
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    w, h, n = 640, 400, 1500
+    rng = np.random.default_rng(31)
+    yy, xx = np.mgrid[0:h, 0:w]
+    noise = rng.random((h, w))
+    blocks = np.where(((xx // 24) + (yy // 24)) % 2 == 0, 0.5, 200.25)          # two levels: ties everywhere inside a block
+    images = {
+        "noise x 255": (noise * 255.0, True),
+        "negative": (noise * 300.0 - 128.5, True),
+        "ramp with repeats": ((xx * 0.37 + yy * 0.11) % 50.0, True),
+        "two levels": (blocks, True),
+        "two levels + speckle": (np.where(rng.random((h, w)) < 0.02, noise * 255.0, blocks), True),
+        "offset 1e5": (1.0e5 + noise, True),
+        "small values": (noise * 3.0e-100 + 1.0e-101, True),
+        "tiny values": (noise * 3.0e-290 + 1.0e-291, False),                     # the reference's squares underflow: every bit 0
+        "big values": (noise * 3.0e200, False),                                  # ... or overflow
+        "offset 1e9": (1.0e9 + noise, False),                                    # further than 2^20 ranges from zero
+        "flat": (np.full((h, w), 100.5), False),
+        "nearly flat": (100.5 + 1.0e-12 * noise, False),
+    }
+    kps = port.random_keypoints(32, w, h, n)
+    kps[::4, 2] = 0.0
+    kps[::9, :2] = np.floor(kps[::9, :2]) + 0.5
+    try:
+        for name, (img, routed) in images.items():
+            want = port.describe_all(img, kps)[1]
+            eng.set_option("extract_stats", 1)
+            got = lk.describe(img, kps)[1]
+            exact, _ = eng.extract_stats()
+            eng.set_option("extract_stats", 0)
+            assert np.array_equal(got, want), name
+            if name.startswith("two levels"):
+                assert exact > 0, name                 # the estimate-based kernel ran (the all-fp64 kernel counts nothing)
+            if not routed:
+                assert exact == 0, name
+            xycs, _ = eng.prepare_keypoints(kps, w, h)
+            dev = eng.extract_device(torch.from_numpy(img).cuda(), torch.from_numpy(xycs).cuda())
+            torch.cuda.synchronize()
+            assert np.array_equal(dev.cpu().numpy(), want), (name, "device tensor")
+            eng.set_option("extract_f64_h16", 0)
+            assert np.array_equal(lk.describe(img, kps)[1], want), (name, "route off")
+            eng.set_option("extract_f64_h16", 1)
+        names = ["noise x 255", "two levels", "flat", "negative"]
+        res = lk.describe_batch([images[k][0] for k in names], [kps] * len(names))
+        for k, (_, desc) in zip(names, res):
+            assert np.array_equal(desc, port.describe_all(images[k][0], kps)[1]), (k, "batch")
+    finally:
+        eng.set_option("extract_stats", 0)
+        eng.set_option("extract_f64_h16", 1)
+
+
 @pytest.mark.parametrize("promote", [1, 2, 0])
 def test_float64_promotion_edges(lk, port, promote):
     """A float64 image goes to the u8 kernels only if EVERY pixel is an integer in [0, 255] (host

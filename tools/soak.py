@@ -49,6 +49,9 @@ while time.time() < t_end:
     eng.set_option("extract_variant", variant)
     as_f64 = rng.random() < 0.4
     src = img.astype(np.float64) + (rng.random(img.shape) * 0.3 if rng.random() < 0.3 and as_f64 else 0.0) if as_f64 else img
+    if as_f64 and rng.random() < 0.3:                                    # other value ranges: the float64 route of the default kernel
+        scale = 10.0 ** float(rng.uniform(-60, 60))
+        src = (src + rng.random(img.shape) * 0.7) * scale + float(rng.choice([0.0, 37.25, -1e3, 3e5])) * scale
     if as_f64:
         eng.set_option("host_promote", int(rng.integers(0, 3)))          # pageable rule / always / never
         if rng.random() < 0.15:                                          # non-finite pixels: the literal (w*e)*e kernel
