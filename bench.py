@@ -809,7 +809,9 @@ def run_ours(args):
             "metric": METRICS[head], "value": rec["value"], "unit": rec["unit"], "n_gpus": cx.world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True, "scaling": rec["scaling"],
             "vs_baseline": None,
-            "dtype": ("f64 resampling, " + ("fp32 estimate + exact f64 recompute" if cx.ev >= 2 else "f64 SSD") +
+            "dtype": (("fp32 resampling into 16-bit planes + fp32 estimate under a proven bound, exact f64 recompute of every "
+                       "undecided bit" if cx.ev >= 5 else
+                       "f64 resampling, " + ("fp32 estimate + exact f64 recompute" if cx.ev >= 2 else "f64 SSD")) +
                       " (extraction) / " + ({3: "int8 tcgen05, int32 accumulate", 4: "e2m1 tcgen05 (mxf4, unit scales), f32 accumulate"}.get(cx.mv, "u32 xor+popc")) +
                       " (matching); results bit-exact"),
             "data": "synthetic",
