@@ -107,6 +107,8 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * form (an A/B switch from before the e2m1 form's parked-chunk epilogue); 0 (default) = always e2m1.
  * key "match_pairs": 1 (default) runs the tensor-core matcher as clusters of two CTAs that share one stream of
  * train tiles through TMA multicast (half the L2 traffic per compare); 0 = every CTA streams for itself.
+ * key "match_2cta": 1 runs paired launches of the e2m1 form as ONE M = 256 MMA stream per CTA pair (tcgen05 cta_group::2,
+ * each CTA holding half of every train tile); 0 (default) = two M = 128 streams over multicast train tiles (measured faster).
  * key "match_streamk": 1 (default) lets the tensor-core matcher split small problems (expanded train set
  * within 32 MB) into equal shares of (query tile, train tile) units per CTA; 0 keeps whole rounds.
  * key "match_streamk_pairs": 1 cuts those shares over (query tile pair, train tile) units and runs them on CTA pairs

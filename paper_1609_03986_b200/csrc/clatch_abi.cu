@@ -291,6 +291,7 @@ int clatch_ctx_create(int device, clatch_ctx** out) {
         return cuda_fail(se, "cudaStreamCreateWithFlags");
     }
     if (const char* v = std::getenv("CLATCH_MATCH_VARIANT")) ctx->match_variant = std::atoi(v);
+    if (const char* v = std::getenv("CLATCH_MATCH_2CTA")) ctx->match_2cta = std::atoi(v) != 0;
     if (const char* v = std::getenv("CLATCH_MATCH_STREAMK_PAIRS")) ctx->match_streamk_pairs = std::atoi(v) != 0;
     if (const char* v = std::getenv("CLATCH_EXTRACT_VARIANT")) {
         const int ev = std::atoi(v);
@@ -405,6 +406,10 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
     }
     if (std::strcmp(key, "match_pairs") == 0) {   // tensor matcher: CTA pairs sharing the train stream by TMA multicast
         ctx->match_pairs = value != 0;
+        return CLATCH_OK;
+    }
+    if (std::strcmp(key, "match_2cta") == 0) {   // tensor matcher, paired e2m1 launches: one M = 256 MMA stream per CTA pair
+        ctx->match_2cta = value != 0;
         return CLATCH_OK;
     }
     if (std::strcmp(key, "match_streamk") == 0) {   // tensor matcher: stream-K partition for small problems

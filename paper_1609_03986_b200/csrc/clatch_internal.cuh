@@ -115,6 +115,9 @@ struct clatch_ctx {
     // SMs) wherever two query tiles scan the same train tiles; set_option "match_pairs" 0 = every CTA on its own.
     bool pdl = true;               // programmatic dependent launch inside the library's own kernel chains (set_option "pdl")
     bool match_pairs = true;
+    bool match_2cta = false;       // paired launches of the e2m1 form run one M = 256 MMA stream per pair (tcgen05 cta_group::2; set_option
+                                   // "match_2cta"). Correct, and the bare instruction runs at full rate (tools/tc_pair_probe.cu), but next to
+                                   // the TMA stream a tile takes 2 240 clk instead of 1 400: off
     bool match_form_auto = false;  // match_variant 4: 1 = mid-sized single matches run the int8 form (it was ahead there before the parked-chunk epilogue; kept for A/B)
     bool match_streamk = true;     // tensor matcher: equal-share partition for small problems (set_option "match_streamk")
     bool match_streamk_pairs = false;  // ... over (query tile pair, train tile) units on CTA pairs (set_option "match_streamk_pairs";

@@ -72,7 +72,7 @@ constexpr int kTcMergeBytes = 3 * 2048;   // (best, second, index) of up to thre
 template <class F> __host__ __device__ constexpr int tc_a_bytes() { return kTcM * kTcKBlock * F::kKBlocks; }   // 64 / 32 KiB
 template <class F> __host__ __device__ constexpr int tc_stage_bytes() { return F::kN * kTcKBlock; }            // 32 / 30 KiB
 template <class F> __host__ __device__ constexpr int tc_smem_bytes() {
-    return tc_a_bytes<F>() + kTcStages * tc_stage_bytes<F>() + 1024 /*align*/ + 256 /*barriers*/ + kTcMergeBytes +
+    return tc_a_bytes<F>() + kTcStages * tc_stage_bytes<F>() + 1024 /*align*/ + 512 /*barriers*/ + kTcMergeBytes +
            (F::kParked ? kTcParkBytes : 0);
 }
 
@@ -185,6 +185,29 @@ __device__ __forceinline__ unsigned cluster_rank() {
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Cluster-wide handshakes of the 2-CTA MMA form: the address of `addr` (an mbarrier of this CTA's layout) in the
+// shared memory of CTA `rank`, an arrive on it, and a wait that also acquires what a remote arriver released.
+__device__ __forceinline__ unsigned mapa_rank(unsigned addr, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(unsigned cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TC_WAITC:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra TC_DONEC;\n"
+        "bra TC_WAITC;\n"
+        "TC_DONEC:\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(unsigned bar) {
@@ -234,6 +257,27 @@ __device__ __forceinline__ void tc_mma_f4(unsigned tmem_d, uint64_t desc_a, uint
         "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb)
         : "memory");
 }
+// The same instruction over a CTA pair (cta_group::2): M = 256, each CTA contributes its 128 rows of A (same shared-
+// memory offset in both) and HALF of the B tile (rows [120 rank, 120 rank + 120) at the same offset), each CTA's TMEM
+// receives its own 128 accumulator rows; issued by the pair's rank-0 CTA only (tools/tc_pair_probe.cu checks the
+// mapping and the rate: 16 382 MAC/clk/SM).
+__device__ __forceinline__ void tc_mma_f4_pair(unsigned tmem_d, uint64_t desc_a, uint64_t desc_b, unsigned idesc,
+                                               unsigned accumulate, unsigned tmem_sfa, unsigned tmem_sfb) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(unsigned bar) {   // ... arrives on `bar` of BOTH CTAs once the pair's MMAs are done
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+                 "h"(static_cast<unsigned short>(3))
+                 : "memory");
+}
+constexpr unsigned kIdescF4Pair = (1u << 7) | (1u << 10) | (1u << 23) | ((TcF4::kN >> 3) << 17) | ((256u >> 4) << 24);
 // 16 TMEM columns of this warp's lane quarter <- one 32-bit value.
 __device__ __forceinline__ void tmem_fill16(unsigned taddr, unsigned v) {
     asm volatile(
@@ -461,8 +505,21 @@ __device__ __forceinline__ void tc_park_chunk(int (&v)[32], const int valid, con
 // query tiles against the SAME train tiles: each loads half of every B stage and multicasts it into both
 // CTAs' shared memory (one L2 read feeds two SMs), and a stage is handed back to the producers only when both
 // CTAs' MMAs have read it (multicast tcgen05.commit onto both `empty` barriers).
-template <class F, bool kPair>
+// k2Cta (needs kPair and the e2m1 form; set_option "match_2cta", OFF by default): the pair runs ONE MMA stream of M = 256
+// (tcgen05 cta_group::2) issued by its rank-0 CTA. Each CTA then loads only HALF of every B stage: per tile 32 KB of A
+// reads + 30 KB of B reads + 30 KB of TMA writes = 92 KB through a CTA's shared-memory port instead of 152 KB. Measured
+// (20 k x 1 M, profiles/r4g_match_2cta.log): results identical, and with no B traffic at all (CLATCH_TC_DEBUG=3) a tile
+// takes 1 100 clk — the M = 256 MMAs and the handshakes are fine — but WITH the TMA stream 2 240 clk (2 500 with the
+// epilogue off) against 1 400 for the multicast pairs, whether the ring has four or eight stages and whether the loads
+// hit one L2-resident tile or stream the set. What the pair form changes is only WHEN the partner's half of B crosses
+// between the SMs — at MMA time instead of as a prefetched multicast write; each SM still takes in 60 KB per tile, and
+// the synchronous fetch next to the TMA fills is the slower of the two. Kept for A/B.
+// Handshakes across the pair: the rank-1 CTA's MMA warp relays its "A landed" / "stage landed" barriers to rank 0
+// (remote arrive), its epilogue warps hand accumulators back on rank 0's barrier, and every commit of the issuer
+// arrives on both CTAs' barriers.
+template <class F, bool kPair, bool k2Cta = false>
 __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcArgs g) {
+    static_assert(!k2Cta || (kPair && F::kF4), "the 2-CTA MMA form is built for paired CTAs and e2m1 operands");
     constexpr int kTcEpilogueWarps = F::kEpiWarps;
     constexpr int kTcN = F::kN, kTcKBlocks = F::kKBlocks;
     constexpr int kTcABytes = tc_a_bytes<F>(), kTcStageBytes = tc_stage_bytes<F>();
@@ -476,38 +533,54 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
     const unsigned base = (raw + 1023u) & ~1023u;              // SWIZZLE_128B atoms need 1024-B alignment
     const unsigned smem_a = base;
     const unsigned smem_b = base + kTcABytes;
-    const unsigned bars = smem_b + kTcStages * kTcStageBytes;  // 8-byte mbarriers
+    // The 2-CTA form keeps half a K-block of B per stage and CTA, so the same ring memory holds twice as many stages:
+    // the operand loop (TMA latency + relay + MMAs + the commit's way back) is ~2 500 clk long, and with four stages in
+    // flight it, not the tensor pipe, set the tile time (measured: 2 240 clk per tile).
+    constexpr int kStages = k2Cta ? 2 * kTcStages : kTcStages;
+    constexpr int kStageStride = k2Cta ? kTcStageBytes / 2 : kTcStageBytes;
+    const unsigned bars = smem_b + kTcStages * kTcStageBytes;  // 8-byte mbarriers (512 bytes; the TMEM slot sits at +128)
     const unsigned bar_a_full = bars;
     const unsigned bar_a_empty = bars + 8;
-    const unsigned bar_full = bars + 16;                       // [kTcStages]
-    const unsigned bar_empty = bar_full + 8 * kTcStages;       // [kTcStages]
-    const unsigned bar_tfull = bar_empty + 8 * kTcStages;      // [2]
-    const unsigned bar_tempty = bar_tfull + 16;                // [2]
+    const unsigned bar_tfull = bars + 16;                      // [2]
+    const unsigned bar_tempty = bars + 32;                     // [2]
+    const unsigned bar_peer_a_full = bars + 48;                // 2-CTA form, rank 0: the partner's A tile has landed
+    const unsigned bar_full = bars + 136;                      // [kStages]
+    const unsigned bar_empty = bar_full + 8 * kStages;         // [kStages]
+    const unsigned bar_peer_full = bar_empty + 8 * kStages;    // [kStages] 2-CTA form, rank 0: the partner's half of a stage has landed
+    static_assert(136 + 3 * 8 * kStages <= 512, "barrier block");
     uint8_t* const gen_base = smem_raw + (base - raw);
     uint8_t* const tail = gen_base + kTcABytes + kTcStages * kTcStageBytes;
     volatile unsigned* tmem_slot = reinterpret_cast<volatile unsigned*>(tail + 128);
-    int* merge_buf = reinterpret_cast<int*>(tail + 256);       // 128 rows x 4 ints
-    uint4* const park = reinterpret_cast<uint4*>(tail + 256 + kTcMergeBytes);   // F::kParked: [16 warps][8 pieces][32 lanes] x uint4
+    int* merge_buf = reinterpret_cast<int*>(tail + 512);       // 128 rows x 4 ints
+    uint4* const park = reinterpret_cast<uint4*>(tail + 512 + kTcMergeBytes);   // F::kParked: [16 warps][8 pieces][32 lanes] x uint4
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
         mbar_init(bar_a_full, 1);
         mbar_init(bar_a_empty, 1);
-        for (int s = 0; s < kTcStages; ++s) {
+        for (int s = 0; s < kStages; ++s) {
             mbar_init(bar_full + 8 * s, 1);
-            mbar_init(bar_empty + 8 * s, kPair ? 2 : 1);       // pair mode: both CTAs' MMAs must have read the stage
+            mbar_init(bar_empty + 8 * s, kPair && !k2Cta ? 2 : 1);   // pair mode: both CTAs' MMAs must have read the stage
+            mbar_init(bar_peer_full + 8 * s, 1);
         }
+        mbar_init(bar_peer_a_full, 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(bar_tfull + 8 * b, 1);
-            mbar_init(bar_tempty + 8 * b, kTcEpilogueWarps);
+            mbar_init(bar_tempty + 8 * b, k2Cta ? 2 * kTcEpilogueWarps : kTcEpilogueWarps);   // 2-CTA form: both CTAs' epilogues
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {   // TMEM: all 512 columns (two 256-column accumulators)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-            smem_u32(const_cast<unsigned*>(tmem_slot))));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (k2Cta) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                smem_u32(const_cast<unsigned*>(tmem_slot))));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                smem_u32(const_cast<unsigned*>(tmem_slot))));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -545,19 +618,27 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
                 a_phase ^= 1;
                 for (int t = 0; t < w.ntiles; ++t) {
                     // train tile = kTcN consecutive rows = kTcN / 8 consecutive atoms of every K-block
-                    const uint8_t* src = w.b + static_cast<unsigned long long>(w.tile_begin + t) * (kTcN / 8 * 1024);
+                    const uint8_t* src = w.b + static_cast<unsigned long long>((g.debug & 4) ? 0 : w.tile_begin + t) * (kTcN / 8 * 1024);   // (debug 4: one tile over and over — timing only)
                     for (int kb = 0; kb < kTcKBlocks; ++kb) {
                         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-                        mbar_expect_tx(bar_full + 8 * stage, kTcStageBytes);
-                        const unsigned dst = smem_b + stage * kTcStageBytes;
-                        if (kPair) {   // this CTA's half of the stage, to both CTAs
+                        if (k2Cta && (g.debug & 2)) {   // measurement only (wrong results): no B traffic at all
+                            mbar_arrive(bar_full + 8 * stage);
+                            if (++stage == kStages) { stage = 0; phase ^= 1; }
+                            continue;
+                        }
+                        mbar_expect_tx(bar_full + 8 * stage, k2Cta ? kTcStageBytes / 2 : kTcStageBytes);
+                        const unsigned dst = smem_b + stage * kStageStride;
+                        if (k2Cta) {   // this CTA's half of the tile's rows, for this CTA alone (the pair's MMA reads both)
+                            bulk_load(dst, src + kb * w.b_kb_stride + rank * (kTcStageBytes / 2), kTcStageBytes / 2,
+                                      bar_full + 8 * stage);
+                        } else if (kPair) {   // this CTA's half of the stage, to both CTAs
                             bulk_load_multicast(dst + rank * (kTcStageBytes / 2),
                                                 src + kb * w.b_kb_stride + rank * (kTcStageBytes / 2), kTcStageBytes / 2,
                                                 bar_full + 8 * stage, 3);
                         } else {
                             bulk_load(dst, src + kb * w.b_kb_stride, kTcStageBytes, bar_full + 8 * stage);
                         }
-                        if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+                        if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
                 }
             }
@@ -572,39 +653,70 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
         int stage = 0, tcount = 0;
         unsigned phase = 0, a_phase = 0;
         const unsigned sfa = tmem_base + kTcSfaCol, sfb = tmem_base + kTcSfbCol;
+        if (k2Cta && rank != 0) {
+            // The partner of the issuing CTA: relay "my A tile / my half of a stage has landed" to rank 0.
+            const unsigned r_a = mapa_rank(bar_peer_a_full, 0), r_full = mapa_rank(bar_peer_full, 0);
+            for (int item = first_item; item < g.num_items; item += item_step) {
+                const TcWork w = tc_decode<F, kPair>(g, item, rank);
+                if (w.ntiles == 0) continue;
+                mbar_wait(bar_a_full, a_phase);
+                a_phase ^= 1;
+                if (lane == 0) mbar_arrive_cluster(r_a);
+                for (int t = 0; t < w.ntiles; ++t, ++tcount) {
+#pragma unroll
+                    for (int kb = 0; kb < kTcKBlocks; ++kb) {
+                        mbar_wait(bar_full + 8 * stage, phase);
+                        if (lane == 0) mbar_arrive_cluster(r_full + 8 * stage);
+                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    }
+                }
+                __syncwarp();
+            }
+        } else
         for (int item = first_item; item < g.num_items; item += item_step) {
             const TcWork w = tc_decode<F, kPair>(g, item, rank);
             if (w.ntiles == 0) continue;
             mbar_wait(bar_a_full, a_phase);
+            if (k2Cta) mbar_wait_cluster(bar_peer_a_full, a_phase);
             a_phase ^= 1;
             for (int t = 0; t < w.ntiles; ++t, ++tcount) {
                 const int buf = tcount & 1;
-                mbar_wait(bar_tempty + 8 * buf, ((tcount >> 1) & 1) ^ 1);   // epilogue drained this accumulator
+                if (k2Cta) mbar_wait_cluster(bar_tempty + 8 * buf, ((tcount >> 1) & 1) ^ 1);   // both CTAs' epilogues drained it
+                else mbar_wait(bar_tempty + 8 * buf, ((tcount >> 1) & 1) ^ 1);   // epilogue drained this accumulator
                 tc_fence_after();
                 const unsigned tmem_d = tmem_base + buf * kTcAccStride;
 #pragma unroll
                 for (int kb = 0; kb < kTcKBlocks; ++kb) {
                     mbar_wait(bar_full + 8 * stage, phase);
+                    if (k2Cta) mbar_wait_cluster(bar_peer_full + 8 * stage, phase);
                     if (trace && tcount == 0 && kb == 0 && lane == 0) trace[2] = global_ns();   // first operand stage has landed
                     tc_fence_after();
                     const uint64_t a_desc = umma_desc(smem_a + kb * (kTcM * kTcKBlock));
-                    const uint64_t b_desc = umma_desc(smem_b + stage * kTcStageBytes);
+                    const uint64_t b_desc = umma_desc(smem_b + stage * kStageStride);
                     if (elect_one()) {
 #pragma unroll
                         for (int k = 0; k < kTcKBlock / 32; ++k) {   // 32 bytes of K per instruction: 32 int8 or 64 e2m1
                             // (start address field counts 16-byte units: + 2 per 32 bytes of K)
-                            if (F::kF4) tc_mma_f4(tmem_d, a_desc + 2 * k, b_desc + 2 * k, kIdescF4, (kb | k) != 0, sfa, sfb);
+                            if (k2Cta) tc_mma_f4_pair(tmem_d, a_desc + 2 * k, b_desc + 2 * k, kIdescF4Pair, (kb | k) != 0, sfa, sfb);
+                            else if (F::kF4) tc_mma_f4(tmem_d, a_desc + 2 * k, b_desc + 2 * k, kIdescF4, (kb | k) != 0, sfa, sfb);
                             else tc_mma_i8(tmem_d, a_desc + 2 * k, b_desc + 2 * k, kIdescI8, (kb | k) != 0);
                         }
-                        if (kPair) tc_commit_multicast(bar_empty + 8 * stage, 3);
+                        if (k2Cta) tc_commit_pair(bar_empty + 8 * stage);
+                        else if (kPair) tc_commit_multicast(bar_empty + 8 * stage, 3);
                         else tc_commit(bar_empty + 8 * stage);  // stage reusable once these MMAs have read it
-                        if (kb == kTcKBlocks - 1) tc_commit(bar_tfull + 8 * buf);   // accumulator complete
+                        if (kb == kTcKBlocks - 1) {             // accumulator complete (in both CTAs' TMEM)
+                            if (k2Cta) tc_commit_pair(bar_tfull + 8 * buf);
+                            else tc_commit(bar_tfull + 8 * buf);
+                        }
                     }
                     __syncwarp();
-                    if (++stage == kTcStages) { stage = 0; phase ^= 1; }
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
-            if (elect_one()) tc_commit(bar_a_empty);           // every MMA of this item has read A
+            if (elect_one()) {                                 // every MMA of this item has read A
+                if (k2Cta) tc_commit_pair(bar_a_empty);
+                else tc_commit(bar_a_empty);
+            }
             __syncwarp();
         }
         if (trace && lane == 0) {
@@ -614,6 +726,12 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
     } else {
         // ===== epilogue: warps 2.. =====
         const int ew = warp - 2;
+        // hand an accumulator back to the MMA issuer — which, in the 2-CTA form, is the pair's rank-0 CTA
+        const unsigned r_tempty = k2Cta ? mapa_rank(bar_tempty, 0) : 0u;
+        auto tempty_arrive = [&](int buf) {
+            if (k2Cta) mbar_arrive_cluster(r_tempty + 8 * buf);
+            else mbar_arrive(bar_tempty + 8 * buf);
+        };
         const int quarter = warp & 3;                       // TMEM lane quarter this warp may touch
         const int half = ew >> 2;                           // int8 form: which 128 of the 256 columns
         const unsigned lane_addr = static_cast<unsigned>(quarter * 32) << 16;
@@ -651,7 +769,7 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
                     if (g.debug & 1) {   // measurement only: how fast is everything BUT the epilogue?
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                        if (lane == 0) tempty_arrive(buf);
                         continue;
                     }
 #pragma unroll
@@ -662,7 +780,7 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
                         if (chunk == 1) {   // everything this warp needs of the accumulator has left TMEM
                             tc_fence_before();
                             __syncwarp();
-                            if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                            if (lane == 0) tempty_arrive(buf);
                         }
                         tc_park_chunk(v, tile_valid - ccol, t * kTcN + ccol, my_park, k1, k2, c1,
                                       dumping && t == 0 ? g.dump + row * 256 + ccol : nullptr, kTcN - ccol);
@@ -749,7 +867,7 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
                     // chunks are examined, was measured 2.5x SLOWER in both forms: 1 M x 1 M 3.06e12 vs 5.12e12 compares/s.)
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+                    if (lane == 0) tempty_arrive(buf);
                 }
             }
             if (F::kF4) {   // f32 bits -> the integer they hold (-inf: nothing seen)
@@ -810,7 +928,8 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
     if (kPair) cluster_sync_all();                             // nothing of the partner's is still bound for this CTA
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+        if (k2Cta) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
 }
 
@@ -855,6 +974,7 @@ static int configure_tc(clatch_ctx* ctx) {
         CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<TcI8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<TcI8>()));
         CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<TcF4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<TcF4>()));
         CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<TcF4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<TcF4>()));
+        CLATCH_CUDA(cudaFuncSetAttribute(match_tc_kernel<TcF4, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<TcF4>()));
         ctx->tc_configured = true;
     }
     return CLATCH_OK;
@@ -897,7 +1017,8 @@ static int launch_tc(clatch_ctx* ctx, const TcArgs& g, unsigned ctas, bool paire
     const unsigned cluster = paired ? 2 : 1;
     pdl = pdl && ctx->pdl;
     cudaError_t e;
-    if (f4) e = paired ? launch_kernel(match_tc_kernel<TcF4, true>, grid, block, smem, stream, pdl, cluster, g)
+    if (f4) e = paired ? (ctx->match_2cta ? launch_kernel(match_tc_kernel<TcF4, true, true>, grid, block, smem, stream, pdl, cluster, g)
+                                          : launch_kernel(match_tc_kernel<TcF4, true>, grid, block, smem, stream, pdl, cluster, g))
                        : launch_kernel(match_tc_kernel<TcF4, false>, grid, block, smem, stream, pdl, cluster, g);
     else e = paired ? launch_kernel(match_tc_kernel<TcI8, true>, grid, block, smem, stream, pdl, cluster, g)
                     : launch_kernel(match_tc_kernel<TcI8, false>, grid, block, smem, stream, pdl, cluster, g);

@@ -436,6 +436,12 @@ def test_tensor_matcher_partitions_agree(lk, port, shape):
         eng.set_option("match_streamk", 1)
         eng.set_option("match_streamk_pairs", 1)        # stream-K runs on CTA pairs (default: single CTAs)
         res[6] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_2cta", 1)                 # ... as one M = 256 MMA stream per pair (tcgen05 cta_group::2)
+        res[7] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_streamk", 0)              # ... and the (query tile pair, split) rounds in that form
+        res[8] = np.stack(eng.match_top2(query, train))
+        eng.set_option("match_streamk", 1)
+        eng.set_option("match_2cta", 0)
         eng.set_option("match_streamk_pairs", 0)
         eng.set_option("match_streamk", 0)
         eng.set_option("match_form_auto", 0)            # e2m1 operands at every size
@@ -450,10 +456,11 @@ def test_tensor_matcher_partitions_agree(lk, port, shape):
     finally:
         eng.set_option("match_streamk", 1)
         eng.set_option("match_streamk_pairs", 0)
+        eng.set_option("match_2cta", 0)
         eng.set_option("match_pairs", 1)                # default: CTA pairs share the stream by TMA multicast
         eng.set_option("match_variant", 4)
         eng.set_option("match_form_auto", 1)
-    for k in (1, 2, 3, 4, 5, 6):
+    for k in (1, 2, 3, 4, 5, 6, 7, 8):
         assert np.array_equal(res[0], res[k]), k
     rows = np.arange(q_n) if q_n * t_n <= 4_000_000 else np.unique(np.r_[np.arange(0, q_n, 7)[:40], rng.integers(0, q_n, 40)])
     assert np.array_equal(res[1][:, rows].T, port.knn2_all(query[rows], train))
