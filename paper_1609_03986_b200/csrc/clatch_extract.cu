@@ -1235,7 +1235,8 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
 // Error budget, in units of the stored integers (1 = 2^-8 grey levels). Per stored sample, against the true
 // bilinear value: rounding to an integer 0.5; coordinates (start value rounded once, column step once, row step
 // rounded once and added <= 15 times: <= 8.5 * 2^-23 px per axis, slope <= 1 per axis in [0,1] units: 2.0e-6),
-// texel / 255 in fp32 (<= 2^-23) and six fp32 roundings in the lerps (3.6e-7): <= 2.5e-6 * 65280 = 0.16. So
+// texel / 255 in fp32 (<= 2^-23; the unit returns the correctly rounded quotient for all 256 levels, tools/tex_probe.cu
+// -> profiles/r4g_tex_probe.json) and six fp32 roundings in the lerps (3.6e-7): <= 2.5e-6 * 65280 = 0.16. So
 // |A - true| <= 0.66 and a difference of two samples is off by at most eta = 1.32. Per chain, d_f the fp32 sum:
 //   |65536 d_ref - d_f| <= 2 eta sum|e| + 49 eta^2      (sum|e| <= 7 sqrt(d) over the 49 terms)
 //                          + 52 * 2^-24 d_f              (49 fused accumulations; the differences are exact)

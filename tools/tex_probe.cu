@@ -7,6 +7,7 @@
 // Prints one JSON object.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,12 @@
 __global__ void order_kernel(cudaTextureObject_t tex, const int* xy, int n, uchar4* out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = tex2Dgather<uchar4>(tex, xy[2 * i] + 1.0f, xy[2 * i + 1] + 1.0f, 0);
+}
+
+// The packed-plane resampler reads the same array through a normalised-float texture object: texel / 255 as a float.
+__global__ void norm_kernel(cudaTextureObject_t texn, const int* xy, int n, float4* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = tex2Dgather<float4>(texn, xy[2 * i] + 1.0f, xy[2 * i + 1] + 1.0f, 0);
 }
 
 __device__ __forceinline__ double u8_to_f64(unsigned v) {
@@ -172,8 +179,35 @@ int main() {
     const int carve = 200 * 1024;
     CK(cudaFuncSetAttribute(gather_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, carve));
     CK(cudaFuncSetAttribute(gather_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, carve));
+    // 1b. the normalised-float view of the same array: is every component float(texel) / 255.0f, correctly rounded?
+    td.readMode = cudaReadModeNormalizedFloat;
+    cudaTextureObject_t texn;
+    CK(cudaCreateTextureObject(&texn, &rd, &td, nullptr));
+    float4* d_outf;
+    CK(cudaMalloc(&d_outf, sizeof(float4) * n_chk));
+    norm_kernel<<<(n_chk + 255) / 256, 256>>>(texn, d_xy, n_chk, d_outf);
+    std::vector<float4> outf(n_chk);
+    CK(cudaMemcpy(outf.data(), d_outf, sizeof(float4) * n_chk, cudaMemcpyDeviceToHost));
+    int norm_exact = 0, levels_seen[256] = {0}, n_levels = 0;
+    double norm_max_rel = 0.0;
+    for (int i = 0; i < n_chk; ++i) {
+        const int x0 = xy[2 * i], y0 = xy[2 * i + 1];
+        const unsigned char p[4] = {img[(y0 + 1) * W + x0], img[(y0 + 1) * W + x0 + 1], img[y0 * W + x0 + 1], img[y0 * W + x0]};   // x, y, z, w
+        const float got[4] = {outf[i].x, outf[i].y, outf[i].z, outf[i].w};
+        bool all = true;
+        for (int k = 0; k < 4; ++k) {
+            const float want = static_cast<float>(p[k]) / 255.0f;
+            all = all && got[k] == want;
+            if (p[k]) norm_max_rel = std::max(norm_max_rel, std::fabs(static_cast<double>(got[k]) - p[k] / 255.0) / (p[k] / 255.0));
+            if (!levels_seen[p[k]]++) ++n_levels;
+        }
+        norm_exact += all;
+    }
     printf("{\"device\": \"%s\", \"sm_count\": %d, \"gather_order_w_z_x_y_is_p00_p10_p01_p11\": %s, \"checked\": %d,\n",
            prop.name, sms, ok_order == n_chk ? "true" : "false", n_chk);
+    printf(" \"normalized_float_gather\": {\"footprints_equal_to_float_texel_over_255\": %d, \"of\": %d, \"grey_levels_seen\": %d, "
+           "\"max_relative_error_vs_exact_quotient\": %.3g, \"two_pow_minus_24\": %.3g},\n",
+           norm_exact, n_chk, n_levels, norm_max_rel, 5.96e-8);
     time_array_fill(1920, 1080);
     time_array_fill(3840, 2160);
     printf(" \"carveout_kb\": %d, \"runs\": [\n", carve / 1024);
