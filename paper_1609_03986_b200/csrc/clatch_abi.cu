@@ -547,10 +547,9 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
             static_assert(sizeof(kDefaultPlanF8) == sizeof(SlotEntry) * kFastT, "embedded plan size");
             pat.slot_degree_f8 = kDefaultPlanDegree;
             CLATCH_CUDA(cudaMemcpy(pat.slots_f8.ptr, kDefaultPlanF8, sizeof(kDefaultPlanF8), cudaMemcpyHostToDevice));
+            pat.slots_f8_planned = true;
         } else {
-            const SlotPlan f8 = plan_slots_grouped(triplets, T, kWinStride, 8, 8, 1500000);
-            pat.slot_degree_f8 = f8.avg_degree;
-            CLATCH_CUDA(cudaMemcpy(pat.slots_f8.ptr, f8.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
+            pat.slots_f8_planned = false;   // planned on first use (variants 2-4 are A/B selections now): 0.3 s of annealing
         }
         if (int rc = pat.slots_h16.reserve(sizeof(SlotEntry) * T)) return rc;
         if (triplet_hash(triplets, T) == kDefaultPlanHash && kDefaultPlanH16RowWords == kH16RowWords) {

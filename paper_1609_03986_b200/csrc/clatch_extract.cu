@@ -2010,6 +2010,18 @@ int ensure_single_window_plan(clatch_ctx* ctx) {
     return CLATCH_OK;
 }
 
+// The fp32-plane kernels' placement (variants 2-4) for a table other than the built-in one: planned on first use.
+int ensure_f8_plan(clatch_ctx* ctx) {
+    Pattern& pat = ctx->pattern;
+    if (pat.slots_f8_planned) return CLATCH_OK;
+    const SlotPlan f8 = plan_slots_grouped(pat.host_triplets.data(), pat.T, kWinStride, 8, 8, 1500000);
+    pat.slot_degree_f8 = f8.avg_degree;
+    if (int rc = pat.slots_f8.reserve(sizeof(SlotEntry) * pat.T)) return rc;
+    CLATCH_CUDA(cudaMemcpy(pat.slots_f8.ptr, f8.slots.data(), sizeof(SlotEntry) * pat.T, cudaMemcpyHostToDevice));
+    pat.slots_f8_planned = true;
+    return CLATCH_OK;
+}
+
 // CLATCH_EX_TRACE=1: where one launch of the default kernel spends its time (stamps of extract_roles_kernel).
 void print_extract_trace(const std::vector<unsigned long long>& h, int grid, size_t quads) {
     const unsigned long long kFlag = 1ull << 63;
@@ -2159,6 +2171,8 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         p.two23 = 0x4B000000u;
         static const int ex_debug = std::getenv("CLATCH_EX_DEBUG") ? std::atoi(std::getenv("CLATCH_EX_DEBUG")) : 0;
         p.dbg = ex_debug;
+        if (ctx->extract_variant < 5)
+            if (int rc = ensure_f8_plan(ctx)) return rc;
         p.slots = ctx->extract_variant >= 5 ? pat.slots_h16.as<ushort4>() : pat.slots_f8.as<ushort4>();
         const size_t quads = (M + kQuad - 1) / kQuad;
         const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
@@ -2199,6 +2213,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
                                              kFiltSmemBytes));
             ctx->filt_configured = true;
         }
+        if (int rc = ensure_f8_plan(ctx)) return rc;
         p.slots = pat.slots_f8.as<ushort4>();
         const size_t quads = (M + kQuad - 1) / kQuad;
         const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));

@@ -60,6 +60,7 @@ struct Pattern {
     DeviceBuffer slots_h16;        // T * ushort4 (packed-plane kernel: the same lanes, word offsets into the 16-bit copies)
     std::vector<int16_t> host_triplets;   // T * 6, for plans made on first use
     bool slots_planned = false;    // `slots` holds a plan for the current table
+    bool slots_f8_planned = false; // `slots_f8` does (the built-in table's ships precomputed; others are planned on first use)
     DeviceBuffer triplets;         // generic kernel: T * 6 int16
     DeviceBuffer d_weights;        // generic kernel: K*K mask weights (per context, not a module-level __constant__)
     std::vector<double> weights;   // K*K
