@@ -621,7 +621,8 @@ __global__ void __launch_bounds__(tc_threads<F>(), 1) match_tc_kernel(const TcAr
                     const uint8_t* src = w.b + static_cast<unsigned long long>((g.debug & 4) ? 0 : w.tile_begin + t) * (kTcN / 8 * 1024);   // (debug 4: one tile over and over — timing only)
                     for (int kb = 0; kb < kTcKBlocks; ++kb) {
                         mbar_wait(bar_empty + 8 * stage, phase ^ 1);
-                        if (k2Cta && (g.debug & 2)) {   // measurement only (wrong results): no B traffic at all
+                        if ((g.debug & 2) || ((g.debug & 8) && (t & 1))) {   // measurement only (wrong results): no B
+                                                                                          // traffic at all / for odd tiles (8)
                             mbar_arrive(bar_full + 8 * stage);
                             if (++stage == kStages) { stage = 0; phase ^= 1; }
                             continue;
