@@ -67,7 +67,7 @@ H16_FP64_OPS_PER_DESC = 512 * 12 + 64
 H16_WARP_INSTR_PER_DESC = 5264 + 3008
 INT8_OPS_PER_COMPARE = 1024                                # 512 int8 MACs
 EXTRACT_KERNELS = {0: "extract_fast_kernel<u8>", 1: "extract_quad_kernel<u8>", 2: "extract_filt_kernel",
-                   3: "extract_pipe_kernel", 4: "extract_roles_kernel<16>", 5: "extract_h16_kernel<16>", 6: "extract_h16s_kernel"}
+                   3: "extract_pipe_kernel", 4: "extract_roles_kernel<16>", 5: "extract_h16_kernel<16, false>", 6: "extract_h16s_kernel"}
 # committed ncu --set full captures (tools/summarize_ncu.py), newest visit first; `traffic` is read from these files
 NCU_PROFILES = {"extract": ("r*_extract_ncu.json", "extract_"), "match": ("r*_match_tc_ncu.json", "match_tc")}
 
