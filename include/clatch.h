@@ -226,6 +226,15 @@ CLATCH_API int clatch_extract_f64_dev(clatch_ctx* ctx, const double* d_img, int 
                            size_t pitch, const double* d_xycs, size_t M, uint8_t* d_out,
                            void* stream);
 
+/* Diagnostics, device-resident form: the samples the default extraction kernel's ESTIMATE works from — for each
+ * prepared keypoint record its 64 x 64 window as round(256 * v) uint16, resampled in fp32 with fixed-point
+ * coordinates (M x 4096 values, row-major). Nothing in the reference corresponds to it: the reference's window
+ * (src/descriptor.cpp:29-49) is what these values must stay within 0.66 units of for the estimate's error bound to
+ * hold, and a test checks exactly that; descriptors never depend on it beyond that bound. */
+CLATCH_API int clatch_estimate_planes_u8_dev(clatch_ctx* ctx, const uint8_t* d_img, int width, int height,
+                                  size_t pitch, const double* d_xycs, size_t M, uint16_t* d_out,
+                                  void* stream);
+
 /* ---- matching (replaces knn2 / the two parallel_for passes of match_brute_force,
  * src/match.cpp:33-67; hamming :14-31 is the per-pair arithmetic) -----------------
  * For every query q: best_idx = lowest train index at the minimum Hamming

@@ -81,6 +81,8 @@ _SIGNATURES = {
                                         C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
     "clatch_extract_f64_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_size_t,
                                          C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
+    "clatch_estimate_planes_u8_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_size_t,
+                                                C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
     "clatch_match_top2": (C.c_int, [C.c_void_p, u8p, C.c_size_t, u8p, C.c_size_t, C.c_int, i32p, i32p,
                                     i32p]),
     "clatch_match_top2_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,

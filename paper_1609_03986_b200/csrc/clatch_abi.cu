@@ -694,6 +694,13 @@ int clatch_extract_u8_dev(clatch_ctx* ctx, const uint8_t* d_img, int width, int 
                              static_cast<cudaStream_t>(stream));
 }
 
+int clatch_estimate_planes_u8_dev(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,
+                                  const double* d_xycs, size_t M, uint16_t* d_out, void* stream) {
+    if (int rc = check_extract(ctx, d_img, width, height, pitch, d_xycs, M, d_out)) return rc;
+    CLATCH_CUDA(cudaSetDevice(ctx->device));
+    return launch_estimate_planes_u8(ctx, d_img, width, height, pitch, d_xycs, M, d_out, static_cast<cudaStream_t>(stream));
+}
+
 int clatch_extract_f64_dev(clatch_ctx* ctx, const double* d_img, int width, int height,
                            size_t pitch, const double* d_xycs, size_t M, uint8_t* d_out,
                            void* stream) {

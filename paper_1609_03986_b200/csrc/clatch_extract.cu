@@ -1431,6 +1431,30 @@ __device__ __forceinline__ void h16_pack_bits(const ExtractParams& p, const uint
     }
 }
 
+// Diagnostics (clatch_estimate_planes_u8_dev): the stored samples of the default kernel's estimate planes — the same
+// resampler, one CTA of 16 warps per quad — as M x 64 x 64 uint16 (row-major, copy E), so that a test can hold
+// every sample against the reference's fp64 window and the error budget above (|A - 256 v| <= 0.66).
+__global__ void __launch_bounds__(512, 1) h16_planes_kernel(ExtractParams p, unsigned short* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t s_quad[];
+    unsigned* const s_h = reinterpret_cast<unsigned*>(s_quad);                        // [4] windows
+    double* const s_rec = reinterpret_cast<double*>(s_quad + kQuad * kHPitch * 4);    // [4][10]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
+    for (unsigned long long q = blockIdx.x; q < quads; q += gridDim.x) {
+        stage_quad_h16(p, q * kQuad, s_rec, tid, 4);
+        __syncthreads();
+        h16_resample_pairs<4>(p.texn, s_rec + (warp >> 2) * kHRecDoubles, s_h + (warp >> 2) * kHPitch, lane, warp & 3);
+        __syncthreads();
+        for (int i = tid; i < kQuad * kWindow * kWindow; i += blockDim.x) {
+            const int w = i >> 12, v = (i >> 6) & 63, u = i & 63;
+            if (q * kQuad + w < p.M)
+                out[(q * kQuad + w) * (kWindow * kWindow) + v * kWindow + u] =
+                    reinterpret_cast<const unsigned short*>(s_h + w * kHPitch)[v * (2 * kHRow) + u];
+        }
+        __syncthreads();
+    }
+}
+
 // kF64: a float64 image whose pixels are not all u8 values. The planes then come from a float texture of the image
 // scaled to [0, 1] over its own range (fill_array_f32_kernel; the estimate and its bound only see that texture, and
 // bilinear sampling commutes with the affine map), the exact paths sample the doubles in global memory.
@@ -2248,6 +2272,32 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
 // float64 upload can reach: the pipelined kernel (u8-valued image) and the quad kernel (any other).
 bool extract_supports_out_index(const clatch_ctx* ctx) {
     return ctx->pattern.fast && ctx->extract_variant >= 3;
+}
+
+int launch_estimate_planes_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,
+                              const double* d_xycs, size_t M, uint16_t* d_out, cudaStream_t stream) {
+    if (M == 0) return CLATCH_OK;
+    constexpr int kSmem = kQuad * kHPitch * 4 + kQuad * kHRecDoubles * 8;
+    CLATCH_CUDA(cudaFuncSetAttribute(h16_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    clatch_ctx::TexImage* ti = nullptr;
+    if (int rc = tex_image_for(ctx, stream, width, height, &ti)) return rc;
+    const bool al = reinterpret_cast<uintptr_t>(d_img) % 16 == 0 && pitch % 16 == 0;
+    const dim3 fgrid((width / 16 + 1 + 127) / 128, height);
+    fill_array_kernel<<<fgrid, 128, 0, stream>>>(ti->surf, d_img, pitch, width, height, al, nullptr, 0);
+    ExtractParams p{};
+    p.img = d_img;
+    p.width = width;
+    p.height = height;
+    p.pitch = pitch;
+    p.xycs = d_xycs;
+    p.M = M;
+    p.texn = ti->texn;
+    const size_t quads = (M + kQuad - 1) / kQuad;
+    h16_planes_kernel<<<static_cast<unsigned>(std::min<size_t>(quads, ctx->sm_count)), 512, kSmem, stream>>>(
+        p, reinterpret_cast<unsigned short*>(d_out));
+    ctx->launches += 2;
+    CLATCH_CUDA(cudaGetLastError());
+    return CLATCH_OK;
 }
 
 int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,

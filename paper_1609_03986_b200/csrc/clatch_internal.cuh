@@ -217,6 +217,8 @@ inline int scratch_release(clatch_ctx* ctx, cudaStream_t st) {
 bool extract_supports_out_index(const clatch_ctx* ctx);
 int launch_extract_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,
                       const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
+int launch_estimate_planes_u8(clatch_ctx* ctx, const uint8_t* d_img, int width, int height, size_t pitch,
+                              const double* d_xycs, size_t M, uint16_t* d_out, cudaStream_t stream);
 int launch_extract_f64(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch,
                        const double* d_xycs, size_t M, uint8_t* d_out, cudaStream_t stream);
 int launch_classify_rows(clatch_ctx* ctx, const double* d_img, int width, int height, size_t pitch, int row0,

@@ -340,6 +340,20 @@ class Engine:
                       out.data_ptr(), st))
         return out
 
+    def estimate_planes_device(self, image, xycs, stream=None):
+        """Diagnostics: the 64 x 64 samples (uint16, round(256 * v)) the default extraction kernel's estimate works
+        from, for a uint8 CUDA image and prepared keypoint records — (M, 64, 64) on the device."""
+        import torch
+        assert image.is_cuda and xycs.is_cuda and image.dtype == torch.uint8 and image.stride(1) == 1
+        m = xycs.shape[0]
+        out = torch.empty((m, 64, 64), dtype=torch.int16, device=image.device)
+        st = (stream or torch.cuda.current_stream(image.device)).cuda_stream
+        h, w = image.shape
+        with self._lock:
+            _lib.check(self.lib.clatch_estimate_planes_u8_dev(self.ctx, image.data_ptr(), w, h, image.stride(0),
+                                                              xycs.data_ptr(), m, out.data_ptr(), st))
+        return out
+
     # ---- matching, host buffers ------------------------------------------------
     def match_top2(self, queries: np.ndarray, train: np.ndarray):
         """-> (best_idx, best_dist, second_dist) int32 (Q,) each."""

@@ -653,6 +653,47 @@ def test_sparse_undecided_bits_are_parked_and_recomputed_exactly(lk, port):
         eng.set_option("host_promote", 0)
 
 
+def test_estimate_planes_stay_within_the_error_budget(lk, port):
+    """The default kernel decides a bit from 16-bit samples that its fp32 / fixed-point resampler produces, and its error
+    bound (csrc/clatch_extract.cu) rests on one measurable claim: every stored sample A is within 0.66 units of 256 x
+    the reference's window value (rounding 0.5 + resampling 0.16). clatch_estimate_planes_u8_dev returns those samples
+    from the production resampler; here every sample of every window — noise, hard edges, ramps, saturated blocks,
+    upright / half-integer / arbitrary keypoints — is held against the oracle's extract_window."""
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    eng.set_pattern(None)                  # (the entry point only needs some pattern to be installed)
+    w, h, n = 640, 480, 220
+    rng = np.random.default_rng(66)
+    yy, xx = np.mgrid[0:h, 0:w]
+    images = {
+        "noise": port.random_image_u8(660, w, h),
+        "checker3": (((xx // 3 + yy // 3) % 2) * 255).astype(np.uint8),            # the steepest slopes there are
+        "ramp": ((xx * 3 + yy) % 256).astype(np.uint8),
+        "blocks": (rng.integers(0, 2, (h // 16 + 1, w // 16 + 1)) * 255).astype(np.uint8).repeat(16, 0).repeat(16, 1)[:h, :w],
+        "structured": port.structured_image(661, w, h).astype(np.uint8),
+    }
+    kps = port.random_keypoints(662, w, h, n)
+    kps[::4, 2] = 0.0
+    kps[1::8, 2] = np.pi / 2
+    kps[::5, :2] = np.floor(kps[::5, :2]) + 0.5
+    kps[3::7, :2] = np.floor(kps[3::7, :2])
+    xycs, kept = eng.prepare_keypoints(kps, w, h)
+    d_x = torch.from_numpy(xycs).cuda()
+    worst = 0.0
+    for name, img in images.items():
+        planes = eng.estimate_planes_device(torch.from_numpy(img).cuda(), d_x)
+        torch.cuda.synchronize()
+        got = planes.cpu().numpy().view(np.uint16).astype(np.float64)
+        f64 = img.astype(np.float64)
+        for j, i in enumerate(kept):
+            want = 256.0 * np.asarray(port.extract_window(f64, kps[i])).reshape(64, 64)
+            err = np.abs(got[j] - want).max()
+            worst = max(worst, err)
+            assert err <= 0.66, (name, j, err)
+    assert worst > 0.4            # (rounding alone reaches 0.5: the check is not vacuous)
+    print(f"largest |A - 256 v| over {len(images) * len(kept)} windows: {worst:.4f} of the 0.66 budgeted")
+
+
 def test_float64_images_through_the_packed_plane_kernel(lk, port):
     """A float64 image that is not u8-valued but tame (finite, a value range between 2^-400 and 2^400, no pixel further than
     2^20 ranges from zero) takes the default kernel as well: its estimate planes come from a float texture of the image scaled to [0, 1]
