@@ -822,7 +822,24 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
         // each costs ~50 us of host-side launches, which delays everything behind it: 1920x1080 with 10 k
         // keypoints takes 535 us in one piece, 454 / 523 / 549 us in 2 / 3 / 4 bands; 3840x2160 with 50 k
         // keypoints 2.23 ms in one piece, 1.81 / 2.10 / 2.28 ms in 2 / 4 / 6.
-        if (bands <= 0) bands = 2;
+        if (bands <= 0) {
+            bands = 2;
+            // A frame that is visibly not u8-valued goes up in one piece: its keypoints then take the packed-plane kernel
+            // over a float texture of the whole frame (51 M desc/s), which needs the frame's value range before the first
+            // keypoint is extracted; in bands they would run the all-fp64 kernel (19 M desc/s). 256 probes on the host.
+            const double* const px = reinterpret_cast<const double*>(img);
+            uint64_t lcg = 0x9E3779B97F4A7C15ull;
+            for (int i = 0; i < 256; ++i) {
+                lcg = lcg * 6364136223846793005ull + 1442695040888963407ull;
+                const size_t y = static_cast<size_t>((lcg >> 33) % static_cast<uint64_t>(height));
+                const size_t x = static_cast<size_t>((lcg >> 13) % static_cast<uint64_t>(width));
+                const double v = px[y * pitch + x];
+                if (!(v >= 0.0 && v <= 255.0 && v == std::floor(v))) {
+                    bands = 1;
+                    break;
+                }
+            }
+        }
         bands = std::max(1, std::min(6, bands));
         if (bands > 1 && n >= 4096 && image_bytes >= (4u << 20) && height >= 64 * bands && n < 0xffffffffull &&
             extract_supports_out_index(ctx))
@@ -846,6 +863,29 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
         stage_rows_u8(reinterpret_cast<const uint8_t*>(img), pitch, static_cast<uint8_t*>(ctx->pin_img.ptr), dpitch, width,
                       height, workers);
         CLATCH_CUDA(cudaMemcpyAsync(ctx->img.ptr, ctx->pin_img.ptr, dpitch * height, cudaMemcpyHostToDevice, st));
+    } else if (!kU8 && sizeof(Pixel) * static_cast<size_t>(width) * height >= (4u << 20) && height >= 64 &&
+               static_cast<const void*>(img) != ctx->pin_img.ptr && is_pageable(img)) {
+        // ... a big float64 frame in ordinary memory (one that is not u8-valued, or host_promote = never): the driver
+        // would bounce it through its own staging at ~13 GB/s; instead the workers copy it into page-locked staging in
+        // eight row chunks and each chunk's DMA runs while the next one is being copied.
+        const size_t row_bytes = sizeof(Pixel) * static_cast<size_t>(width);
+        if (int rc = ctx->pin_img.reserve(row_bytes * height)) return rc;
+        uint8_t* const staging = static_cast<uint8_t*>(ctx->pin_img.ptr);
+        const uint8_t* const src = reinterpret_cast<const uint8_t*>(img);
+        const size_t src_pitch = sizeof(Pixel) * pitch;
+        const int chunks = 8, rows_per = (height + chunks - 1) / chunks;
+        for (int c = 0; c < chunks; ++c) {
+            const int c0 = std::min(height, c * rows_per), c1 = std::min(height, c0 + rows_per);
+            if (c1 <= c0) break;
+            const int parts = std::max(1, std::min(resolve_workers(workers), (c1 - c0) / 8));
+            const int rows = (c1 - c0 + parts - 1) / parts;
+            WorkerPool::instance().run(parts, [&](int w) {
+                const int r0 = std::min(c1, c0 + w * rows), r1 = std::min(c1, r0 + rows);
+                for (int r = r0; r < r1; ++r) std::memcpy(staging + static_cast<size_t>(r) * row_bytes, src + static_cast<size_t>(r) * src_pitch, row_bytes);
+            });
+            CLATCH_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(ctx->img.ptr) + static_cast<size_t>(c0) * row_bytes,
+                                        staging + static_cast<size_t>(c0) * row_bytes, row_bytes * (c1 - c0), cudaMemcpyHostToDevice, st));
+        }
     } else
     CLATCH_CUDA(cudaMemcpy2DAsync(ctx->img.ptr, sizeof(Pixel) * dpitch, img, sizeof(Pixel) * pitch,
                                   sizeof(Pixel) * width, height, cudaMemcpyHostToDevice, st));

@@ -743,6 +743,17 @@ def test_float64_images_through_the_packed_plane_kernel(lk, port):
             eng.set_option("extract_f64_h16", 0)
             assert np.array_equal(lk.describe(img, kps)[1], want), (name, "route off")
             eng.set_option("extract_f64_h16", 1)
+        # a frame big enough (>= 4 MB) for the host paths that only big frames take: the probe that sends a visibly
+        # non-u8 frame up in one piece, and the chunked page-locked staging of frames in ordinary numpy memory
+        big = rng.random((800, 1100)) * 200.0 + 3.5
+        big_kps = port.random_keypoints(33, 1100, 800, 5000)
+        want_big = port.describe_all(big, big_kps)[1]
+        assert np.array_equal(lk.describe(big, big_kps)[1], want_big), "big pageable frame"
+        pin = torch.empty(big.shape, dtype=torch.float64, pin_memory=True)
+        pin.numpy()[...] = big
+        assert np.array_equal(lk.describe(pin.numpy(), big_kps)[1], want_big), "big page-locked frame"
+        big_int = np.floor(big)                                                   # u8-valued: the banded upload, u8 kernels
+        assert np.array_equal(lk.describe(big_int, big_kps)[1], port.describe_all(big_int, big_kps)[1]), "big u8-valued frame"
         names = ["noise x 255", "two levels", "flat", "negative"]
         res = lk.describe_batch([images[k][0] for k in names], [kps] * len(names))
         for k, (_, desc) in zip(names, res):
