@@ -42,7 +42,7 @@ timeout 300 python tools/extract_perf.py > "$OUT/extract_perf.log" 2>&1
 timeout 300 python tools/exact_rate.py > "$OUT/exact_rate.log" 2>&1
 echo "== soak"; timeout 700 python tools/soak.py 420 > "$OUT/soak.log" 2>&1; tail -2 "$OUT/soak.log"
 echo "== compute-sanitizer"
-timeout 900 compute-sanitizer --tool memcheck python tools/sanitize.py > "$OUT/sanitize_memcheck.log" 2>&1; tail -2 "$OUT/sanitize_memcheck.log"
+timeout 900 compute-sanitizer --tool memcheck python tools/sanitize.py all > "$OUT/sanitize_memcheck.log" 2>&1; tail -2 "$OUT/sanitize_memcheck.log"
 timeout 900 compute-sanitizer --tool racecheck python tools/sanitize.py > "$OUT/sanitize_racecheck.log" 2>&1; tail -2 "$OUT/sanitize_racecheck.log"
 fi
 ls -la "$OUT"

@@ -36,6 +36,26 @@ for variant, pairs in ((3, 1), (4, 1), (4, 0)):                      # paired (m
     assert np.array_equal(np.stack([bi, bd, sd], 1), port.knn2_all(big[:700], big))
 eng.set_option("match_streamk", 1)
 eng.set_option("match_pairs", 1)
+eng.set_option("match_variant", 4)
+# The 2-CTA MMA form (off by default) runs under memcheck only ("all"): racecheck reports its cross-CTA mbarrier traffic —
+# remote arrives and multicast commits onto the partner's barriers — as potential RAW hazards on the barrier objects,
+# an ordering the tool does not model (profiles/r4g_racecheck_2cta.log); every other path is raced-checked clean.
+forms = [{"match_streamk_pairs": 1}]
+if len(sys.argv) > 1 and sys.argv[1] == "all":
+    forms += [{"match_2cta": 1}, {"match_2cta": 1, "match_streamk_pairs": 1, "match_streamk": 0}]
+for opts in forms:
+    for k, v in opts.items():                                        # stream-K on CTA pairs (and the 2-CTA MMA form)
+        eng.set_option(k, v)
+    bi, bd, sd = eng.match_top2(big[:700], big)
+    assert np.array_equal(np.stack([bi, bd, sd], 1), port.knn2_all(big[:700], big))
+    for k in opts:
+        eng.set_option(k, 1 if k == "match_streamk" else 0)
+import torch                                                         # noqa: E402
+xycs, _ = eng.prepare_keypoints(kps, 320, 240)                       # diagnostics entry point: the estimate planes
+eng.estimate_planes_device(torch.from_numpy(img.astype(np.uint8)).cuda(), torch.from_numpy(xycs).cuda())
+torch.cuda.synchronize()
+two_level = np.where((np.indices(img.shape).sum(0) // 24) % 2 == 0, 0.5, 200.25)   # float64 route: parked bits + window pass
+assert np.array_equal(lk.describe(two_level, kps)[1], port.describe_all(two_level, kps)[1])
 nan_img = img.copy()
 nan_img[100, 100] = np.nan
 with np.errstate(all="ignore"):
