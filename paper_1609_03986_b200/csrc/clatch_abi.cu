@@ -864,7 +864,9 @@ static int describe_all_impl(clatch_ctx* ctx, const Pixel* img, int width, int h
                       height, workers);
         CLATCH_CUDA(cudaMemcpyAsync(ctx->img.ptr, ctx->pin_img.ptr, dpitch * height, cudaMemcpyHostToDevice, st));
     } else if (!kU8 && sizeof(Pixel) * static_cast<size_t>(width) * height >= (4u << 20) && height >= 64 &&
-               static_cast<const void*>(img) != ctx->pin_img.ptr && is_pageable(img)) {
+               static_cast<const void*>(img) != ctx->pin_img.ptr && is_pageable(img) &&
+               (ctx->pin_img.cap >= sizeof(Pixel) * static_cast<size_t>(width) * height || ++ctx->pageable_f64_frames >= 2)) {
+        // (from the second such frame on, or when the staging is already there: page-locking 16.6 MB takes ~50 ms once)
         // ... a big float64 frame in ordinary memory (one that is not u8-valued, or host_promote = never): the driver
         // would bounce it through its own staging at ~13 GB/s; instead the workers copy it into page-locked staging in
         // eight row chunks and each chunk's DMA runs while the next one is being copied.

@@ -147,6 +147,7 @@ struct clatch_ctx {
     // once with the workers and sending 1 byte per pixel is faster), 1 = always, 2 = never. For page-locked
     // sources the plain DMA of the doubles won (profiles/r1y_e2e_breakdown.log).
     int host_promote = 0;
+    int pageable_f64_frames = 0;   // big float64 frames in ordinary memory seen without page-locked staging (describe_all)
     cudaStream_t copy_stream = nullptr;        // image bands stream in here while kernels run on `stream`
     cudaEvent_t band_events[8] = {};
     struct PipeSlot {                // describe_batch: one of two pipeline slots
