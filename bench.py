@@ -636,7 +636,7 @@ def run_cfg3(cx: Ctx, steps: int, warmup: int, cpu: bool, clocks_out: dict):
         for i, a, k in zip(mine, host_imgs, kps):
             li[i], lk_[i] = a, k
         # (warm-up >= 5: the page-locked result pool grows by one round of blocks per call that releases its results)
-        s, out = cx.time_wall(lambda: sharded.extract_images_sharded(li, lk_), steps, max(warmup, 5))
+        s, out = cx.time_wall(lambda: sharded.extract_images_sharded(li, lk_), steps, max(warmup, 8))
         assert sum(len(v[1]) for v in out.values()) == m_local
         return {"value": m_total / s, "unit": UNITS["cfg3"], "ms_per_step": s * 1e3,
                 "h2d_bytes_per_step": int(sum(a.nbytes for a in host_imgs) + m_local * 32),
@@ -750,7 +750,7 @@ def run_cfg5(cx: Ctx, steps: int, warmup: int, cpu: bool, clocks_out: dict):
     del resident, sets, out
 
     def e2e_leg(host_imgs, tag, memory):
-        s, o = cx.time_wall(lambda: whole_job(host_imgs)[1], steps, max(warmup, 5))
+        s, o = cx.time_wall(lambda: whole_job(host_imgs)[1], steps, max(warmup, 8))
         return {"value": pairs_total / s, "unit": UNITS["cfg5"], "ms_per_step": s * 1e3,
                 "compares_per_s": compares_total / s,
                 "h2d_bytes_per_step": int(sum(a.nbytes for a in host_imgs) + sum(rows_per_set[i] for i in mine) * 32),
