@@ -1230,8 +1230,7 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_roles_kernel(ExtractP
 //     returns texel / 255 as floats (no conversions), three fused lerps, one FFMA that rounds 65280 * b into the
 //     mantissa of 2^23. No fp64 pipe, no row tables, ~24 instructions per sample instead of ~40. A lane owns the
 //     column pair (2 lane, 2 lane + 1) of a row, so the two samples leave as ONE 32-bit word of copy E and — with
-//     the first sample of the next lane (one shuffle) — one word of copy O (16-bit stores of two lanes into one
-//     word are 2-way bank conflicts: measured).
+//     the first sample of the next lane (one shuffle) — one word of copy O: one store instruction per sample.
 // Error budget, in units of the stored integers (1 = 2^-8 grey levels). Per stored sample, against the true
 // bilinear value: rounding to an integer 0.5; coordinates (start value rounded once, column step once, row step
 // rounded once and added <= 15 times: <= 8.5 * 2^-23 px per axis, slope <= 1 per axis in [0,1] units: 2.0e-6),
