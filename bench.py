@@ -565,6 +565,11 @@ def run_image_step(cx: Ctx, cfg: str, steps: int, warmup: int, cpu: bool, clocks
     e2e = e2e_leg(cx.pinned(img64), cx.pinned(kps), "f64", "page-locked")
     e2e_pageable = e2e_leg(img64, kps.copy(), "f64", "ordinary (pageable) numpy")
     e2e_u8 = e2e_leg(cx.pinned(img), cx.pinned(kps), "u8", "page-locked")
+    # ... and a float64 frame that is NOT u8-valued (a warped / noisy frame): the float-texture route of the default kernel
+    frac = img64 * 0.93 + np.random.default_rng(3988).random(img64.shape) * 3.0
+    m_saved, m = m, len(lk.describe(frac, kps)[1])
+    e2e_frac = e2e_leg(cx.pinned(frac), cx.pinned(kps), "non-integer f64", "page-locked")
+    m = m_saved
 
     per_step = (t_ext + t_mat) / steps
     ext_s, mat_s = t_ext / steps, t_mat / steps
@@ -585,7 +590,7 @@ def run_image_step(cx: Ctx, cfg: str, steps: int, warmup: int, cpu: bool, clocks
         "descriptors_per_s": cx.world * m / ext_s if ext_s > 0 else None,
         "compares_per_s": cx.world * m * m / mat_s if mat_s > 0 else None,
         "wall_ms_per_step_incl_flush": wall / steps * 1e3,
-        "e2e": e2e, "e2e_pageable": e2e_pageable, "e2e_u8": e2e_u8, "gpu_launches": int(launches),
+        "e2e": e2e, "e2e_pageable": e2e_pageable, "e2e_u8": e2e_u8, "e2e_noninteger_f64": e2e_frac, "gpu_launches": int(launches),
         "roofline": roofline, "kernels": kernels, "keypoints": n, "descriptors": m,
         "timing": "sum of per-step CUDA-event durations on the launching stream, max over ranks; "
                   "256 MiB device memset between steps, outside the event pairs",
