@@ -15,6 +15,8 @@ timeout 120 ./tools/pipe_peaks > "$OUT/pipe_peaks.json" 2> "$OUT/pipe_peaks.err"
 timeout 120 ./tools/tc_peak > "$OUT/tc_peak.json" 2>&1
 timeout 120 ./tools/tmem_ld_probe > "$OUT/tmem_ld_probe.json" 2>&1
 timeout 120 ./tools/tmem_contention > "$OUT/tmem_contention.json" 2>&1
+timeout 120 ./tools/tc_pair_probe > "$OUT/tc_pair_probe.json" 2>&1
+timeout 120 ./tools/tex_probe > "$OUT/tex_probe.json" 2>&1
 echo "== bench ours"; timeout 900 python bench.py --steps 20 --warmup 5 > "$OUT/bench.json" 2> "$OUT/bench.err"; echo "bench rc=$?"; tail -6 "$OUT/bench.err"
 echo "== bench reference"; timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"; echo "rc=$?"
 echo "== torchrun world size 1 (NCCL path)"
