@@ -5,6 +5,7 @@ is present, the unmodified reference itself.
 
   cfg3  two FULL 3840x2160 images x 50 000 keypoints: every descriptor compared
         (reference paths: proj/src/descriptor.cpp:90-105)
+        + one frame of non-integer float64 pixels at that size (the float-texture route of the default kernel)
   cfg4  the FULL 1 M x 1 M match: 4 096 sampled rows against the oracle's knn2, every planted copy,
         every duplicated train row (lowest index wins), the ratio pass on all 1 M triples
         (proj/src/match.cpp:33-81)
@@ -46,6 +47,25 @@ def test_cfg3_two_full_images(lk):
         for i in (0, 1):
             _, rdesc = ref.describe_all(imgs[i].astype(np.float64), kps[i][:4000], workers=0)
             assert np.array_equal(got[i][1][:len(rdesc)], rdesc)
+
+
+def test_cfg3_size_frame_of_non_integer_doubles(lk):
+    """The float-texture route of the default kernel at cfg3 size: one 3840x2160 frame of float64 pixels that are not
+    u8 values (a warped, noisy frame; ordinary numpy memory and page-locked) x 50 000 keypoints, every descriptor
+    against the oracle on all host threads (reference path: proj/src/descriptor.cpp:29-105)."""
+    torch = pytest.importorskip("torch")
+    imgs, kps = W.images_and_keypoints("cfg3", [7])
+    rng = np.random.default_rng(1609_7)
+    frame = imgs[0].astype(np.float64) * 0.87 + rng.random(imgs[0].shape) * 7.5 - 3.0
+    kept_idx, want = W.describe_all_threaded(frame, kps[0])
+    assert len(want) >= 49_900
+    kept, desc = lk.describe(frame, kps[0])
+    assert np.array_equal(kept, kps[0][kept_idx])
+    assert np.array_equal(desc, want), f"{(desc != want).any(1).sum()} descriptors differ"
+    pin = torch.empty(frame.shape, dtype=torch.float64, pin_memory=True)
+    pin.numpy()[...] = frame
+    assert np.array_equal(lk.describe(pin.numpy(), kps[0])[1], want)
+    assert np.array_equal(lk.describe(frame, kps[0])[1], want)          # (second call from numpy memory: chunked staging)
 
 
 def test_cfg4_full_match(lk):
