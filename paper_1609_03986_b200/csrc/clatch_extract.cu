@@ -2131,7 +2131,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     // estimate-based kernels pay the estimate, a re-resampling and the exact chains — 23 M desc/s on a flat image
     // against 36 M for the all-fp64 quad kernel. The default kernel reports, per launch, how many windows took the
     // exact pass (ExtractParams::route, a host-mapped slot per CTA); when the previous launch of this context saw
-    // more than 35 % the next ones run the quad kernel, and every 16th launch probes with the default kernel again.
+    // more than 18 % (35 % for the fp32-plane kernel) the next ones run the quad kernel, and every 16th launch probes with the default kernel again.
     bool quad_routed = false;
     const bool routing = kU8 && pat.fast && ctx->extract_variant >= 4 && ctx->extract_route && !ctx->extract_stats_on &&
                          flags == nullptr && ctx->route_host != nullptr && !force_generic;
@@ -2143,7 +2143,9 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
                 all += ctx->route_host[c].y;
             }
             if (all > 0) {
-                ctx->route_quad = hot * 100 > all * 35;
+                // break-even against the quad kernel (16.4 us per quad): the packed-plane kernel pays ~13 us per window
+                // that takes the window-wide pass on top of its 6.8 us (18 % of the windows), the fp32-plane kernel ~4 us (35 %)
+                ctx->route_quad = hot * 100 > all * (ctx->extract_variant >= 5 ? 18u : 35u);
                 ctx->route_pending = false;
             }
         }
