@@ -27,6 +27,7 @@ namespace clatch {
 namespace {
 #include "default_plan_f8.inc"
 #include "default_plan_h16.inc"
+#include "default_plan_sw.inc"
 }
 }
 
@@ -330,6 +331,7 @@ void clatch_ctx_destroy(clatch_ctx* ctx) {
         if (t.texf) cudaDestroyTextureObject(t.texf);
         if (t.surff) cudaDestroySurfaceObject(t.surff);
         if (t.arrayf) cudaFreeArray(t.arrayf);
+        if (t.tickets) cudaFree(t.tickets);
         if (t.surf) cudaDestroySurfaceObject(t.surf);
         if (t.array) cudaFreeArray(t.array);
     }
@@ -550,6 +552,15 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
             pat.slots_f8_planned = true;
         } else {
             pat.slots_f8_planned = false;   // planned on first use (variants 2-4 are A/B selections now): 0.3 s of annealing
+        }
+        if (triplet_hash(triplets, T) == kDefaultPlanHash && kDefaultPlanSWStride == kWinStride) {
+            // ... and the one-window placement (variant 0; the packed-plane kernel's window-wide exact pass)
+            static_assert(sizeof(kDefaultPlanSW) == sizeof(SlotEntry) * kFastT, "embedded plan size");
+            if (int rc = pat.slots.reserve(sizeof(SlotEntry) * T)) return rc;
+            pat.slot_degree = kDefaultPlanSWDegree;
+            pat.slot_degree_identity = kDefaultPlanSWDegreeIdentity;
+            CLATCH_CUDA(cudaMemcpy(pat.slots.ptr, kDefaultPlanSW, sizeof(kDefaultPlanSW), cudaMemcpyHostToDevice));
+            pat.slots_planned = true;
         }
         if (int rc = pat.slots_h16.reserve(sizeof(SlotEntry) * T)) return rc;
         if (triplet_hash(triplets, T) == kDefaultPlanHash && kDefaultPlanH16RowWords == kH16RowWords) {

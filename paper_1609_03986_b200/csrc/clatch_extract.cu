@@ -47,6 +47,7 @@ struct ExtractParams {
     unsigned long long M;
     uint8_t* out;              // M x T/8
     const ushort4* slots;      // fast kernel: T x {a, b, c, bit}
+    const ushort4* slots_sw;   // packed-plane kernel: the one-window placement (fp64 window, stride kWinStride) of its window-wide pass
     const short* triplets;     // generic kernel: T x 6
     const double* weights;     // generic kernel: K x K mask weights (per-context device copy; warp-uniform reads)
     int T, K;
@@ -59,6 +60,7 @@ struct ExtractParams {
     unsigned two23;            // packed-plane kernel: 0x4B000000, see ssd_estimate_h16_2
     int dbg;                   // diagnostics (CLATCH_EX_DEBUG): 1 = skip the estimate, 2 = skip the resampling (timing only, wrong bits)
     const unsigned* out_index; // optional: descriptor of record j goes to row out_index[j] (quad / pipelined kernels)
+    unsigned* tickets;         // packed-plane kernel: {next quad ticket, CTAs finished}, both 0 between launches (nullptr: static round-robin)
     unsigned long long* trace; // optional (CLATCH_EX_TRACE=1): kExTrace globaltimer stamps per CTA of the default kernel
 };
 
@@ -1475,6 +1477,7 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
     double* const s_rec = reinterpret_cast<double*>(s_bits + 2 * kQuad * kPipeBits);             // [2][4][10]
     int* const s_mask = reinterpret_cast<int*>(s_rec + 2 * kQuad * kHRecDoubles);                // [2] windows needing the exact pass
     unsigned* const s_qtail = reinterpret_cast<unsigned*>(s_mask + 2);                           // deferred bits queued so far
+    unsigned* const s_qid = reinterpret_cast<unsigned*>(s_mask + 4);                             // [8] quad of pipeline iteration it at [it & 7]
     DeferredBit* const s_queue = reinterpret_cast<DeferredBit*>(s_mask + 16);                    // [kQueueCap]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, grp = warp >> 2;
@@ -1484,38 +1487,54 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
     const int u = rt & 63, v0 = rt >> 6;                     // window-wide exact pass (consumers)
     const double du = static_cast<double>(u) - 31.5;
     const int kb = lane & 3, ti = lane >> 2;
-    const unsigned long long quads = (p.M + kQuad - 1) / kQuad;
-    const int nq = blockIdx.x < quads ? static_cast<int>((quads - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
-    const unsigned long long kp_step = static_cast<unsigned long long>(gridDim.x) * kQuad;
+    // Quads are handed out dynamically (ExtractParams::tickets: a device counter the last CTA to finish resets): a CTA's
+    // first three quads are the round-robin ones (every CTA draws at the same moment at the start: 148 atomics on one word
+    // take 4 us, which only a full pipeline iteration hides), every further one a ticket drawn three iterations ahead. On images whose
+    // flat or saturated regions send some windows through the window-wide exact pass (6 us each against 1.9 us for the
+    // estimate alone) a static round-robin left the launch waiting for the unluckiest CTA (span 226 us, mean 160).
+    const unsigned nquads = static_cast<unsigned>(min((p.M + kQuad - 1) / kQuad, 0xffffffffull));   // also "no quad"
     ushort4 slot[kSlots];
 #pragma unroll
     for (int j = 0; j < kSlots; ++j) slot[j] = __ldg(p.slots + 8 * (rw % kSW + kSW * j) + ti);
     unsigned n_flagged = 0, n_windows = 0;
     unsigned long long* const trace = p.trace != nullptr && tid == 0 ? p.trace + static_cast<size_t>(kExTrace) * blockIdx.x : nullptr;
     if (trace) trace[0] = ex_global_ns();
-    if (tid == 0) s_mask[0] = s_mask[1] = 0, *s_qtail = 0;
+    if (tid == 0) {
+        s_mask[0] = s_mask[1] = 0, *s_qtail = 0;
+        for (unsigned i = 0; i < 3; ++i) s_qid[i] = min(blockIdx.x + i * gridDim.x, nquads);
+    }
     // Sparse undecided bits are parked ({slot, keypoint} in a shared-memory queue) and recomputed exactly by whole warps
     // after the pipeline has drained; a quad with more than kDeferMax of them (flat or saturated footprints), or a full
     // queue, takes the window-wide exact pass instead. See extract_roles_kernel.
     const bool defer_ok = p.M <= 0xffffffffull;
     unsigned q_prev = 0;                 // queue tail after the previous quad (uniform over the consumers)
-    unsigned long long kp0 = static_cast<unsigned long long>(blockIdx.x) * kQuad - kp_step;   // first keypoint of quad `it`
+    unsigned quads_done = 0;
+    bool prev_live = false;              // consumers: the previous iteration's quad existed
+    bool checked_out = false;            // producer thread 0: this CTA has drawn its last ticket
     stage_quad_h16(p, static_cast<unsigned long long>(blockIdx.x) * kQuad, s_rec, tid, kRRows);
     __syncthreads();
     pdl_wait();   // launched early behind fill_array_kernel: the texture array is complete from here on
     if (trace) trace[1] = ex_global_ns();
 
-    for (int it = -1; it <= nq; ++it, kp0 += kp_step) {
+    for (int it = -1;; ++it) {
         const int cur = it & 1, nxt = cur ^ 1;
         const unsigned windows_before = n_windows;
+        // Each role reads only the ring entries it needs, where it needs them (the consumers one per iteration). Both leave
+        // the loop in the iteration after the one whose quad did not exist: tickets only grow, so nothing is in flight then.
         if (producer) {
+            const unsigned q_done = it >= 1 ? s_qid[(it - 1) & 7] : nquads;   // its bits are complete: packed and stored now
+            if (it >= 1 && q_done >= nquads) break;
+            const unsigned q_stage = s_qid[(it + 2) & 7];
+            unsigned ticket = nquads;   // drawn now, stored at the end of the iteration: the round trip hides behind the resampling
+            if (rt == 0 && it >= 0 && q_stage < nquads)   // (after pdl_wait: the previous launch's rewind of the counter is visible)
+                ticket = p.tickets != nullptr ? 3 * gridDim.x + atomicAdd(p.tickets, 1u) : q_stage + gridDim.x;
             // The producers, which have slack (they resample a quad in half the time the consumers need to estimate one),
             // also pack the previous quad's bits and stage the window records two quads ahead (buffer [quad & 1]; its last
             // readers resampled quad `it`, an iteration ago): the consumers' critical path is the estimate alone.
-            if (it >= 1) {
+            if (q_done < nquads) {
                 const int w = rt >> 7, j = rt & 127;
                 const uint8_t* bits = s_bits + (nxt * kQuad + w) * kPipeBits;
-                const unsigned long long kp = kp0 - kp_step + w;
+                const unsigned long long kp = static_cast<unsigned long long>(q_done) * kQuad + w;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const unsigned w32 = __ballot_sync(0xffffffffu, bits[128 * k + j] != 0);
@@ -1525,12 +1544,27 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
                     }
                 }
             }
-            if (it + 1 < nq && !(p.dbg & 2))   // resample the next quad into the planes [nxt]: this warp's window, its rows
+            if (s_qid[(it + 1) & 7] < nquads && !(p.dbg & 2))   // resample the next quad into the planes [nxt]: this warp's window, its rows
                 h16_resample_pairs<kRRows>(p.texn, s_rec + (nxt * kQuad + rw / kRRows) * kHRecDoubles,
                                            s_h + (nxt * kQuad + rw / kRRows) * kHPitch, lane, rw % kRRows);
-            if (it + 2 < nq) stage_quad_h16(p, kp0 + 2 * kp_step, s_rec + cur * kQuad * kHRecDoubles, rt, kRRows);
+            if (q_stage < nquads)
+                stage_quad_h16(p, static_cast<unsigned long long>(q_stage) * kQuad, s_rec + cur * kQuad * kHRecDoubles, rt, kRRows);
+            if (rt == 0 && it >= 0) {
+                s_qid[(it + 3) & 7] = ticket < nquads ? ticket : nquads;
+                // This CTA's first ticket past the end is its last draw: it checks out here, inside the producers' slack, and
+                // the last CTA to do so rewinds the counter for the next launch on this stream (nothing draws any more).
+                if (ticket >= nquads && !checked_out) {
+                    checked_out = true;
+                    if (p.tickets != nullptr && atomicInc(p.tickets + 1, gridDim.x - 1) == gridDim.x - 1) p.tickets[0] = 0;
+                }
+            }
         } else {
-            if (it >= 0 && it < nq) {
+            if (it >= 1 && !prev_live) break;
+            const unsigned q_now = it >= 0 ? s_qid[it & 7] : nquads;          // estimated now
+            const unsigned long long kp0 = static_cast<unsigned long long>(q_now) * kQuad;   // first keypoint of quad `it`
+            prev_live = q_now < nquads;
+            if (prev_live) {
+                ++quads_done;
                 const unsigned* const my_win = s_h + (cur * kQuad + kb) * kHPitch;
                 const bool live = kp0 + kb < p.M;   // a keypoint past the end leaves an unused window
                 if (rt == 0) s_mask[nxt] = 0;
@@ -1585,14 +1619,14 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
                         n_windows += rt == 0;
                         asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");
                         if (rt == 0) *s_qtail = q_prev;   // this quad's parked items are withdrawn (every consumer has read the tail)
-                        // ... and the lanes of that window run the exact chains of their undecided triplets
-                        if (kb == w) {
-#pragma unroll
-                            for (int j = 0; j < kSlots; ++j)
-                                if ((need >> j) & 1) {
-                                    my_bits[slot[j].w & 0x7fff] = h16_exact_bit(s_exact, slot[j]);
-                                    ++n_flagged;
-                                }
+                        // ... and the 512 consumer threads run the exact chains of ALL 512 triplets of that window, one
+                        // each, in the one-window lane placement (bank pairs planned for a single fp64 window): with only
+                        // the undecided lanes of the packed-plane placement at work — a quarter of the lanes, their
+                        // patches colliding 4-8-way in the fp64 window — a flat window took 13 us, this way ~6.
+                        {
+                            const ushort4 sw = __ldg(p.slots_sw + rt);
+                            s_bits[(cur * kQuad + w) * kPipeBits + (sw.w & 0x7fff)] = triplet_bit_7x7_cold(s_exact, sw.x, sw.y, sw.z, sw.w >> 15);
+                            ++n_flagged;
                         }
                         asm volatile("bar.sync 2, %0;" ::"n"(kST) : "memory");   // the next window overwrites the scratch
                     }
@@ -1600,7 +1634,7 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
             }
         }
         __syncthreads();
-        if (trace && it + 3 < kExTrace)
+        if (trace && it + 3 < kExTrace - 2)
             trace[it + 3] = ex_global_ns() | (n_windows != windows_before ? 1ull << 63 : 0ull);
     }
     // The pipeline has drained: all 32 warps take the parked bits, the plane memory serves as their scratch.
@@ -1612,7 +1646,8 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
                                                static_cast<const double*>(p.img), p.pitch);
             n_flagged += lane == 0;
         }
-        if (trace && parked) trace[kExTrace - 1] = ex_global_ns() | static_cast<unsigned long long>(parked) << 48;
+        if (trace && parked) trace[kExTrace - 1] = (ex_global_ns() & 0xffffffffffffull) | static_cast<unsigned long long>(parked) << 48;
+        if (trace) trace[kExTrace - 2] = quads_done;
     }
     if (p.stats != nullptr) {
         n_flagged = __reduce_add_sync(0xffffffffu, n_flagged);
@@ -1622,7 +1657,7 @@ __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16_kernel(ExtractPar
         }
     }
     if (p.route != nullptr && !producer && rt == 0)
-        p.route[blockIdx.x] = make_uint2(n_windows, static_cast<unsigned>(nq > 0 ? nq * kQuad : 0));
+        p.route[blockIdx.x] = make_uint2(n_windows, quads_done * kQuad);
 }
 
 __global__ void __launch_bounds__(kQuadThreads, 1) extract_h16s_kernel(ExtractParams p) {
@@ -1953,6 +1988,10 @@ int tex_image_for(clatch_ctx* ctx, cudaStream_t stream, int width, int height, c
         ti = &ctx->tex_images.back();
         ti->stream = stream;
     }
+    if (!ti->tickets) {
+        CLATCH_CUDA(cudaMalloc(&ti->tickets, 2 * sizeof(unsigned)));
+        CLATCH_CUDA(cudaMemsetAsync(ti->tickets, 0, 2 * sizeof(unsigned), stream));
+    }
     if (ti->width != width || ti->height != height) {
         if (ti->tex) {
             CLATCH_CUDA(cudaStreamSynchronize(stream));   // a kernel may still be sampling the old array
@@ -2056,9 +2095,11 @@ void print_extract_trace(const std::vector<unsigned long long>& h, int grid, siz
     double parked_us = 0;
     std::vector<double> ends(grid);
     std::vector<int> exacts(grid, 0);
+    std::vector<long long> taken(grid, 0);
     for (int c = 0; c < grid; ++c) {
         const unsigned long long* t = h.data() + static_cast<size_t>(kExTrace) * c;
-        const long long nq = static_cast<long long>((quads - c + grid - 1) / grid);
+        const long long nq = t[kExTrace - 2] ? static_cast<long long>(t[kExTrace - 2])   // (quads drawn from the ticket counter)
+                                             : static_cast<long long>((quads - c + grid - 1) / grid);
         const long long last = std::min<long long>(nq + 3, kExTrace - 1);   // stamp index of iteration nq
         entry_max = std::max(entry_max, (t[0] - t0) * 1e-3);
         ready_mean += (t[1] - t0) * 1e-3;
@@ -2087,6 +2128,7 @@ void print_extract_trace(const std::vector<unsigned long long>& h, int grid, siz
             t_end = std::max(t_end, (t0 & ~0xffffffffffffull) | (t[kExTrace - 1] & 0xffffffffffffull));
         }
         ends[c] = e;
+        taken[c] = nq;
         end_mean += e;
         end_min = std::min(end_min, e);
         t_end = std::max(t_end, t[last] & ~kFlag);
@@ -2101,7 +2143,7 @@ void print_extract_trace(const std::vector<unsigned long long>& h, int grid, siz
                  grid, quads, (t_end - t0) * 1e-3, entry_max, ready_mean / grid, ready_max, fill_mean / grid,
                  steady_n ? steady_sum / steady_n : 0.0, steady_n, exact_n ? exact_sum / exact_n : 0.0, exact_n, drain_mean / grid,
                  end_mean / grid, end_min, ends[worst], worst, exacts[worst],
-                 static_cast<long long>((quads - worst + grid - 1) / grid), parked, parked_ctas,
+                 taken[worst], parked, parked_ctas,
                  parked_ctas ? parked_us / parked_ctas : 0.0);
 }
 
@@ -2131,7 +2173,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     // estimate-based kernels pay the estimate, a re-resampling and the exact chains — 23 M desc/s on a flat image
     // against 36 M for the all-fp64 quad kernel. The default kernel reports, per launch, how many windows took the
     // exact pass (ExtractParams::route, a host-mapped slot per CTA); when the previous launch of this context saw
-    // more than 18 % (35 % for the fp32-plane kernel) the next ones run the quad kernel, and every 16th launch probes with the default kernel again.
+    // more than 25 % (35 % for the fp32-plane kernel) the next ones run the quad kernel, and every 16th launch probes with the default kernel again.
     bool quad_routed = false;
     const bool routing = kU8 && pat.fast && ctx->extract_variant >= 4 && ctx->extract_route && !ctx->extract_stats_on &&
                          flags == nullptr && ctx->route_host != nullptr && !force_generic;
@@ -2143,9 +2185,10 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
                 all += ctx->route_host[c].y;
             }
             if (all > 0) {
-                // break-even against the quad kernel (16.4 us per quad): the packed-plane kernel pays ~13 us per window
-                // that takes the window-wide pass on top of its 6.8 us (18 % of the windows), the fp32-plane kernel ~4 us (35 %)
-                ctx->route_quad = hot * 100 > all * (ctx->extract_variant >= 5 ? 18u : 35u);
+                // measured break-even against the quad kernel (tools/route_perf.py: 36 M desc/s whatever the image): the
+                // packed-plane kernel with ticketed quads falls below it at 25 % of the windows in the window-wide pass
+                // (18 % for its symmetric, statically scheduled form), the fp32-plane kernel at 35 %
+                ctx->route_quad = hot * 100 > all * (ctx->extract_variant == 5 ? 25u : ctx->extract_variant == 6 ? 18u : 35u);
                 ctx->route_pending = false;
             }
         }
@@ -2194,6 +2237,12 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         p.tex = ti->tex;
         p.texn = ti->texn;
         p.two23 = 0x4B000000u;
+        if (ctx->extract_variant == 5) {
+            if (int rc = ensure_single_window_plan(ctx)) return rc;
+            p.slots_sw = pat.slots.as<ushort4>();
+            static const bool static_quads = std::getenv("CLATCH_EX_STATIC") != nullptr;   // diagnostics: round-robin quads
+            p.tickets = static_quads ? nullptr : ti->tickets;
+        }
         static const int ex_debug = std::getenv("CLATCH_EX_DEBUG") ? std::atoi(std::getenv("CLATCH_EX_DEBUG")) : 0;
         p.dbg = ex_debug;
         if (ctx->extract_variant < 5)
@@ -2368,6 +2417,9 @@ static int launch_extract_h16_f64(clatch_ctx* ctx, const double* d_img, int widt
     p.tex = 0;
     p.texn = ti->texf;
     p.two23 = 0x4B000000u;
+    if (int rc = ensure_single_window_plan(ctx)) return rc;
+    p.slots_sw = pat.slots.as<ushort4>();
+    p.tickets = ti->tickets;
     const size_t quads = (M + kQuad - 1) / kQuad;
     const int grid = static_cast<int>(std::min<size_t>(quads, ctx->sm_count));
     CLATCH_CUDA(launch_kernel(extract_h16_kernel<16, true>, dim3(grid), dim3(kQuadThreads), kH16SmemBytes, stream, ctx->pdl, 1, p));

@@ -99,6 +99,7 @@ struct clatch_ctx {
         int widthf = 0, heightf = 0;
         cudaSurfaceObject_t surf = 0;    // the same array, for the fill kernel
         int width = 0, height = 0;
+        unsigned* tickets = nullptr;     // {next quad ticket, CTAs finished}: the packed-plane kernel hands out its quads dynamically
     };
     std::vector<TexImage> tex_images;
     // extraction routing for degenerate images (launch_extract): host-mapped per-CTA slots written by the default kernel

@@ -1251,7 +1251,7 @@ def test_single_pair_match_filters_on_the_device(lk, port, q, n):
 
 
 def test_degenerate_streams_are_routed_to_the_quad_kernel_and_stay_exact(lk, port):
-    """A context whose last launch needed the exact pass for more than 35 % of its windows (flat or saturated
+    """A context whose last launch needed the exact pass for more than a quarter of its windows (flat or saturated
     images) runs its next launches on the all-fp64 quad kernel and probes the default kernel again every 16th
     launch. Whatever the router decides, and however flat and textured images alternate, the descriptors are
     the oracle's."""
@@ -1281,5 +1281,41 @@ def test_degenerate_streams_are_routed_to_the_quad_kernel_and_stay_exact(lk, por
                     torch.cuda.synchronize()
                     got = got.cpu().numpy()
                 assert np.array_equal(got, want[name]), (route, i, name)
+    finally:
+        eng.set_option("extract_route", 1)
+
+
+def test_dynamically_scheduled_quads_cover_every_keypoint_once(lk, port):
+    """The default kernel hands its quads (four keypoints) out through a device counter that the last CTA to draw
+    rewinds for the next launch: back-to-back launches of very different sizes — fewer quads than CTAs, exactly the
+    statically assigned first three rounds, one more, many more, ragged last quads — on a clean and on a partly
+    saturated image (where the window-wide pass makes the CTAs' speeds differ) must all give the oracle's bits,
+    with no launch inheriting a counter that was not rewound."""
+    torch = pytest.importorskip("torch")
+    eng = lk.get_engine()
+    eng.set_pattern(None)
+    w, h = 800, 600
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    noise = port.random_image_u8(6060, w, h)
+    part = noise.copy()
+    part[:, : w // 6] = 255
+    part[h // 2 :, w // 2 :] = 0
+    sizes = [1, 3, 4, 5, 4 * sms - 1, 4 * sms, 4 * sms + 1, 12 * sms - 2, 12 * sms, 12 * sms + 1, 16 * sms + 3, 5000, 7, 4 * sms + 2, 9001]
+    kps = port.random_keypoints(6061, w, h, 12000)
+    xycs, _ = eng.prepare_keypoints(kps, w, h)
+    assert len(xycs) >= max(sizes)
+    want = {name: port.describe_all(im.astype(np.float64), kps)[1] for name, im in (("noise", noise), ("part", part))}
+    d_imgs = {"noise": torch.from_numpy(noise).cuda(), "part": torch.from_numpy(part).cuda()}
+    d_x = torch.from_numpy(xycs).cuda()
+    try:
+        eng.set_option("extract_route", 0)          # keep the default kernel on the partly saturated image too
+        outs = []
+        for rep in range(3):
+            for i, m in enumerate(sizes):
+                name = "part" if (i + rep) % 2 else "noise"
+                outs.append((name, m, eng.extract_device(d_imgs[name], d_x[:m].contiguous())))   # no sync in between
+        torch.cuda.synchronize()
+        for name, m, got in outs:
+            assert np.array_equal(got.cpu().numpy(), want[name][:m]), (name, m)
     finally:
         eng.set_option("extract_route", 1)
