@@ -90,7 +90,7 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * their set-up while the predecessor finishes, and wait (griddepcontrol.wait) before touching its output; 0 = plain launches.
  * key "extract_route": 1 (default) lets a context whose last u8 launch needed the window-wide exact pass for more than 25 %
  * of its windows (18 % with extract_variant 6, 35 % with extract_variant 4; flat / saturated images: exact ties) run the next launches on the all-fp64 quad kernel, probing the default
- * kernel again every 16th launch; 0 = always the selected variant.
+ * kernel again after 16 launches (then 32, 64, 128 while the probes keep finding the stream degenerate); 0 = always the selected variant.
  * key "extract_f64_h16": 1 (default) sends a float64 image that is not u8-valued but tame (finite, a value range between
  * 2^-400 and 2^400, no pixel further than 2^20 ranges from zero) through the packed-plane kernel, its estimate planes resampled from a
  * float texture of the image scaled to [0, 1] and every undecided bit recomputed from the doubles; 0 = the all-fp64

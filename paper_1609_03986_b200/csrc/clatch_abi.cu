@@ -381,6 +381,7 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         ctx->extract_variant = value;
         ctx->route_quad = ctx->route_pending = false;
         ctx->route_age = 0;
+        ctx->route_period = 16;
         return CLATCH_OK;
     }
     if (std::strcmp(key, "pdl") == 0) {   // programmatic dependent launch inside the library's kernel chains
@@ -391,6 +392,7 @@ int clatch_set_option(clatch_ctx* ctx, const char* key, int value) {
         ctx->extract_route = value != 0;
         ctx->route_quad = ctx->route_pending = false;
         ctx->route_age = 0;
+        ctx->route_period = 16;
         return CLATCH_OK;
     }
     if (std::strcmp(key, "upload_bands") == 0) {   // describe_all, float64 images: row bands of the upload (1 = one piece)

@@ -2173,7 +2173,8 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
     // estimate-based kernels pay the estimate, a re-resampling and the exact chains — 23 M desc/s on a flat image
     // against 36 M for the all-fp64 quad kernel. The default kernel reports, per launch, how many windows took the
     // exact pass (ExtractParams::route, a host-mapped slot per CTA); when the previous launch of this context saw
-    // more than 25 % (35 % for the fp32-plane kernel) the next ones run the quad kernel, and every 16th launch probes with the default kernel again.
+    // more than 25 % (35 % for the fp32-plane kernel) the next ones run the quad kernel; the default kernel probes again after
+    // 16 launches, then 32, 64, 128 while the probes keep finding the stream degenerate.
     bool quad_routed = false;
     const bool routing = kU8 && pat.fast && ctx->extract_variant >= 4 && ctx->extract_route && !ctx->extract_stats_on &&
                          flags == nullptr && ctx->route_host != nullptr && !force_generic;
@@ -2188,12 +2189,21 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
                 // measured break-even against the quad kernel (tools/route_perf.py: 36 M desc/s whatever the image): the
                 // packed-plane kernel with ticketed quads falls below it at 25 % of the windows in the window-wide pass
                 // (18 % for its symmetric, statically scheduled form), the fp32-plane kernel at 35 %
+                const bool was = ctx->route_quad;
                 ctx->route_quad = hot * 100 > all * (ctx->extract_variant == 5 ? 25u : ctx->extract_variant == 6 ? 18u : 35u);
                 ctx->route_pending = false;
+                // every probe of a degenerate stream costs a launch at half the quad kernel's rate: the first one comes
+                // after 16 launches, each confirming one doubles the distance (up to 128: a flat stream then runs at
+                // 36 M desc/s, 34 M with a probe every 16th launch), the first clean one ends the routing
+                ctx->route_period = ctx->route_quad && was ? std::min(ctx->route_period * 2, 128u) : 16u;
+                if (ctx->route_quad) ctx->route_probe_at = ctx->route_age + ctx->route_period;
             }
         }
         ++ctx->route_age;
-        if (ctx->route_quad && (ctx->route_age & 15) != 0) quad_routed = true;
+        if (ctx->route_quad) {
+            if (ctx->route_age != ctx->route_probe_at) quad_routed = true;
+            else ctx->route_probe_at += ctx->route_period;   // (this launch probes; its answer is folded a launch or more later)
+        }
     }
     if (force_generic) {
         extract_generic_kernel<kU8><<<grid_for(ctx, M, 2), kThreads, pat.T, stream>>>(p);

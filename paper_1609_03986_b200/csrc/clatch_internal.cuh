@@ -109,6 +109,7 @@ struct clatch_ctx {
     uint2* route_dev = nullptr;      // the device's view of route_host
     bool route_pending = false, route_quad = false;
     unsigned route_age = 0;
+    unsigned route_period = 16, route_probe_at = 0;   // while routed: the default kernel probes again at launch route_probe_at
     const unsigned* extract_out_index = nullptr;   // set around a launch: record j -> output row (banded upload)
     bool extract_stats_on = false;           // count exact recomputes (clatch_extract_stats)
     clatch::DeviceBuffer extract_stats;      // 2 x u64
