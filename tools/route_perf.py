@@ -43,3 +43,22 @@ for frac in (0.0, 0.05, 0.1, 0.15, 0.2, 0.3, 0.4, 0.5, 0.7, 1.0):
           f"quad kernel {quad:.1f}, with the router {routed:.1f} M desc/s", flush=True)
 eng.set_option("extract_variant", 5)
 eng.set_option("extract_route", 1)
+
+# A caller that waits for every frame (describe() does): the router's probes of a degenerate stream thin out to one in 128.
+flat = torch.full((h, w), 99, dtype=torch.uint8, device="cuda")
+for label, variant, route in (("default kernel, router on", 5, 1), ("quad kernel", 1, 0)):
+    eng.set_option("extract_variant", variant)
+    eng.set_option("extract_route", route)
+    out = eng.extract_device(flat, d_x)
+    for _ in range(300):
+        eng.extract_device(flat, d_x, out=out)
+        torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(512):
+        eng.extract_device(flat, d_x, out=out)
+        torch.cuda.synchronize()
+    e1.record(); torch.cuda.synchronize()
+    print(f"flat frames, one at a time ({label}): {len(xycs) / (e0.elapsed_time(e1) / 512) * 1e3 / 1e6:.1f} M desc/s", flush=True)
+eng.set_option("extract_variant", 5)
+eng.set_option("extract_route", 1)
