@@ -563,6 +563,14 @@ int clatch_set_pattern(clatch_ctx* ctx, const int16_t* triplets, int T, int K, c
             pat.slot_degree_identity = kDefaultPlanSWDegreeIdentity;
             CLATCH_CUDA(cudaMemcpy(pat.slots.ptr, kDefaultPlanSW, sizeof(kDefaultPlanSW), cudaMemcpyHostToDevice));
             pat.slots_planned = true;
+        } else if (ctx->extract_variant == 5) {
+            // another table: plan it here (0.2 s of annealing) rather than inside the first describe() that meets a flat window
+            const SlotPlan sw = plan_slots(triplets, T, kWinStride, 1000000);
+            pat.slot_degree = sw.avg_degree;
+            pat.slot_degree_identity = sw.avg_degree_identity;
+            if (int rc = pat.slots.reserve(sizeof(SlotEntry) * T)) return rc;
+            CLATCH_CUDA(cudaMemcpy(pat.slots.ptr, sw.slots.data(), sizeof(SlotEntry) * T, cudaMemcpyHostToDevice));
+            pat.slots_planned = true;
         }
         if (int rc = pat.slots_h16.reserve(sizeof(SlotEntry) * T)) return rc;
         if (triplet_hash(triplets, T) == kDefaultPlanHash && kDefaultPlanH16RowWords == kH16RowWords) {
