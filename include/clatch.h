@@ -81,7 +81,9 @@ CLATCH_API int clatch_device_info(clatch_ctx* ctx, int* sm_count, int* sm_clock_
  * double-buffered planes, texture-unit footprints and resampling overlapped with the estimate,
  * 4 = variant 3 with dedicated producer / consumer warps, 5 = the estimate from packed 16-bit planes (two shifted
  * copies: a 7-pixel patch row is four aligned 32-bit words) resampled in fp32 with fixed-point coordinates, dedicated
- * producer / consumer warps (default), 6 = variant 5 with every warp doing both halves. 2-6 take u8-valued images;
+ * producer / consumer warps, its groups of four keypoints drawn from a per-stream device counter that rewinds itself
+ * (default; the launches of one stream must not overlap, which stream order guarantees), 6 = variant 5 with every warp
+ * doing both halves and a static round-robin. 2-6 take u8-valued images;
  * any other image runs variant 1. Every variant returns the same bytes (an estimate only ever decides a bit under a
  * proven error bound; undecided bits are recomputed with the reference's exact arithmetic). The environment variable
  * CLATCH_EXTRACT_VARIANT sets the initial value of a new context.
