@@ -2263,7 +2263,7 @@ int launch_extract(clatch_ctx* ctx, const void* d_img, int width, int height, si
         // variant 4 (default): dedicated producer / consumer warps, 16 + 16 — 60.1 vs 58.1 M desc/s at 10 k
         // keypoints and 72.3 vs 68.3 M at 50 k against the symmetric schedule of variant 3 (24 + 8 warps
         // measured 48.8 M: eight warps cannot keep the LSU busy)
-        // a probe: every launch while the stream is degenerate (they are the 16th ones), every 8th one otherwise — the
+        // a probe: every default-kernel launch while the stream is degenerate (the 16th, then 32nd, 64th, 128th ones), every 8th one otherwise — the
         // store into host memory at the end of the kernel costs ~2 us per launch
         if (routing && M >= 64 && (ctx->route_quad || (ctx->route_age & 7) == 1)) {
             std::memset(ctx->route_host, 0, sizeof(uint2) * ctx->sm_count);

@@ -1252,8 +1252,8 @@ def test_single_pair_match_filters_on_the_device(lk, port, q, n):
 
 def test_degenerate_streams_are_routed_to_the_quad_kernel_and_stay_exact(lk, port):
     """A context whose last launch needed the exact pass for more than a quarter of its windows (flat or saturated
-    images) runs its next launches on the all-fp64 quad kernel and probes the default kernel again every 16th
-    launch. Whatever the router decides, and however flat and textured images alternate, the descriptors are
+    images) runs its next launches on the all-fp64 quad kernel and probes the default kernel again after 16 launches
+    (then 32, 64, 128 while the probes agree). Whatever the router decides, and however flat and textured images alternate, the descriptors are
     the oracle's."""
     torch = pytest.importorskip("torch")
     eng = lk.get_engine()
